@@ -1,0 +1,374 @@
+"""CPU oracle for the VecInfer decode-attention hot path (arXiv 2510.06175).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+--impl reference legs may import or execute anything under oracle/.  The product path
+(paper_2510_06175_b200/) never imports it and shares no code, headers, constants or helpers
+with it.
+
+Plain, slow, obviously-correct NumPy, following the paper equation by equation:
+  * fp64 for the attention path (Eq. 1, 3, 5-7, 10; Alg. 1 outputs),
+  * pinned fp32 where an fp32 decision selects an integer (the VQ code, Eq. 2) -- both the
+    oracle and the GPU take that decision in the same precision (readings R9, R10).
+Every function cites the passage it follows (P:n = /root/reference/PAPER.md line n).
+
+Parity status: every function below is pinned by tests/test_oracle_pins.py against closed
+forms, worked examples, invariants or brute force, except `kmeans` (codebook quality needs the
+paper's datasets) -- "parity unpinned" for kmeans' optimality; its determinism and the SPEC
+worked examples are checked, and it only produces frozen *inputs*, never expected values.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+# --------------------------------------------------------------------------------------------
+# Eq. 5: Walsh-Hadamard matrix, Sylvester recursion, natural order.
+# --------------------------------------------------------------------------------------------
+
+
+def hadamard_pm(D: int) -> np.ndarray:
+    """Unnormalised +-1 Hadamard matrix H_pm with H_D = H_pm / sqrt(D) (Eq. 5).
+
+    Built by the recursion [[H, H], [H, -H]] starting from H_1 = [1]; the per-level 1/sqrt(2)
+    of Eq. 5 is collected into the single 1/sqrt(D) factor of `hadamard`.
+    """
+    if D < 1 or (D & (D - 1)) != 0:
+        raise ValueError("D must be a power of two (Eq. 5 is defined for D = 2^k)")
+    H = np.ones((1, 1), dtype=np.int64)
+    while H.shape[0] < D:
+        H = np.block([[H, H], [H, -H]])
+    return H
+
+
+def hadamard(D: int) -> np.ndarray:
+    """Orthonormal H_D of Eq. 5 (H_D H_D^T = I), fp64."""
+    return hadamard_pm(D).astype(np.float64) / math.sqrt(D)
+
+
+# --------------------------------------------------------------------------------------------
+# Eq. 4: smoothing factors from calibration keys.
+# --------------------------------------------------------------------------------------------
+
+EPS_FLOOR = np.float32(1e-6)   # SPEC S:91 degenerate-channel floor (reading R6)
+
+
+def calibrate_smooth(k_cal: np.ndarray, eps: float = 1e-6):
+    """lambda_i = sqrt(max |K_i|) per (KV head, channel), Eq. 4.
+
+    k_cal: [n_tokens, n_kv_heads, D], bf16-valued.  Returns (lambda, inv_lambda) fp32
+    [n_kv_heads, D] with lambda = max(RN32(sqrt(amax)), RN32(eps)) and inv_lambda = RN32(1/lambda)
+    (reading R6: both sides multiply; keys by inv_lambda, queries by lambda).
+    """
+    k_cal = np.asarray(k_cal, dtype=np.float32)
+    if k_cal.shape[0] == 0:
+        raise ValueError("empty calibration set")
+    amax = np.abs(k_cal).max(axis=0)                         # exact on bf16 values
+    lam = np.sqrt(amax.astype(np.float32))                   # IEEE correctly-rounded fp32 sqrt
+    lam = np.maximum(lam, np.float32(eps))
+    inv = (np.float32(1.0) / lam).astype(np.float32)         # IEEE correctly-rounded fp32 divide
+    return lam.astype(np.float32), inv
+
+
+# --------------------------------------------------------------------------------------------
+# Eq. 3 + Eq. 6 + Eq. 7: dual equivalent transformation.
+# --------------------------------------------------------------------------------------------
+
+
+def transform_query(q: np.ndarray, lam: np.ndarray) -> np.ndarray:
+    """q~ = q diag(lambda) H_D (Eq. 7 left factor), fp64.  q: [..., D], lam: [D]."""
+    q = np.asarray(q, dtype=np.float64)
+    D = q.shape[-1]
+    return (q * np.asarray(lam, dtype=np.float64)) @ hadamard(D)
+
+
+def transform_keys_exact(K: np.ndarray, lam: np.ndarray) -> np.ndarray:
+    """K~ = K diag(lambda)^-1 H_D (Eq. 7 right factor), fp64 (mathematical path)."""
+    K = np.asarray(K, dtype=np.float64)
+    D = K.shape[-1]
+    return (K / np.asarray(lam, dtype=np.float64)) @ hadamard(D)
+
+
+FIXED_POINT_BITS = 24          # reading R10: pinned exact fixed point, 2^-24 grid
+RANGE_LIMIT = 2.0 ** 32        # |k * inv_lambda| must stay below 2^32 (int64 headroom)
+
+
+def rn_float32_from_int(X: np.ndarray) -> np.ndarray:
+    """Round int64 values to the nearest float32 (ties to even), one rounding."""
+    return np.asarray(X, dtype=np.int64).astype(np.float32)
+
+
+def transform_key_pinned(k: np.ndarray, inv_lam: np.ndarray) -> np.ndarray:
+    """Key side of the dual transform, pinned so that codes are reproducible bit for bit.
+
+    Mathematically x = (k diag(lambda)^-1) H_D (Eq. 3 then Eq. 6; S+H order).  The paper
+    fixes no rounding, so (reading R10) the smoothed key is put on an exact 2^-24 fixed-point
+    grid and rotated exactly in integers:
+        A_l = rint_even(k_l * inv_lambda_l * 2^24)            (exact f64 product, < 53 bits)
+        X_j = sum_l H_pm[l, j] * A_l                           (exact int64, O(D^2))
+        x_j = RN32( RN32(X_j) * 2^-24 ) (*)32 RN32(1/sqrt(D))
+    k: [..., D] bf16-valued; inv_lam: [D] fp32.  Returns float32 [..., D].
+    """
+    k = np.asarray(k, dtype=np.float32)
+    D = k.shape[-1]
+    prod = k.astype(np.float64) * np.asarray(inv_lam, dtype=np.float32).astype(np.float64)
+    if np.any(np.abs(prod) >= RANGE_LIMIT):
+        raise OverflowError("|k * inv_lambda| >= 2^32: outside the pinned fixed-point range")
+    A = np.rint(prod * float(2 ** FIXED_POINT_BITS)).astype(np.int64)
+    X = A @ hadamard_pm(D)                                          # exact integer product
+    xs = rn_float32_from_int(X) * np.float32(2.0 ** -FIXED_POINT_BITS)
+    inv_sqrt_d = np.float32(1.0 / math.sqrt(D))
+    return (xs * inv_sqrt_d).astype(np.float32)
+
+
+# --------------------------------------------------------------------------------------------
+# Eq. 2: product vector quantisation, nearest centroid.
+# --------------------------------------------------------------------------------------------
+
+
+def vq_encode(x: np.ndarray, C: np.ndarray, chunk: int = 2048) -> np.ndarray:
+    """Codes j* = argmin_j ||x_i - C_j||^2 per contiguous sub-vector (Eq. 2).
+
+    x: [..., D] float32; C: [2^b, d] (bf16-valued).  Distance evaluated in fp32, every op
+    round-to-nearest, no fused multiply-add, summed in the fixed order ((e0^2+e1^2)+e2^2)+e3^2
+    (reading R9); ties -> lowest index (np.argmin returns the first minimum).
+    Returns int64 codes [..., D/d].
+    """
+    x = np.asarray(x, dtype=np.float32)
+    C = np.asarray(C, dtype=np.float32)
+    n_ent, d = C.shape
+    D = x.shape[-1]
+    if D % d:
+        raise ValueError("sub-vector dim must divide D")
+    lead = x.shape[:-1]
+    sub = x.reshape(-1, d)
+    codes = np.empty(sub.shape[0], dtype=np.int64)
+    step = max(1, chunk * 256 // n_ent)
+    for s0 in range(0, sub.shape[0], step):
+        blk = sub[s0:s0 + step]
+        dist = None
+        for t in range(d):
+            e = blk[:, None, t] - C[None, :, t]            # fp32 RN subtract
+            e2 = e * e                                       # fp32 RN multiply
+            dist = e2 if dist is None else dist + e2         # fp32 RN add, left to right
+        codes[s0:s0 + step] = np.argmin(dist, axis=1)
+    return codes.reshape(*lead, D // d)
+
+
+def vq_decode(codes: np.ndarray, C: np.ndarray) -> np.ndarray:
+    """VQ^-1: concatenate the selected centroids (Eq. 10), fp64 [..., M*d]."""
+    codes = np.asarray(codes, dtype=np.int64)
+    C = np.asarray(C, dtype=np.float64)
+    out = C[codes]                                            # [..., M, d]
+    return out.reshape(*codes.shape[:-1], codes.shape[-1] * C.shape[1])
+
+
+def encode_kv(k: np.ndarray, v: np.ndarray, inv_lam: np.ndarray, Ck: np.ndarray, Cv: np.ndarray):
+    """Prefill (Eq. 8) / decode append (Eq. 9) for one KV head.
+
+    K~_q = VQ(K diag(lambda)^-1 H_D, C_k) (pinned transform), V_q = VQ(V, C_v) (values are not
+    transformed).  k, v: [..., D].  Returns (k_codes, v_codes) int64 [..., M].
+    """
+    x = transform_key_pinned(k, inv_lam)
+    return vq_encode(x, Ck), vq_encode(np.asarray(v, dtype=np.float32), Cv)
+
+
+# --------------------------------------------------------------------------------------------
+# Eq. 1 / Eq. 10 and Alg. 1 outputs.
+# --------------------------------------------------------------------------------------------
+
+
+def attention_full(q: np.ndarray, K: np.ndarray, V: np.ndarray):
+    """Eq. 1: s = q K^T / sqrt(D), p = softmax(s), o = p V; also L = logsumexp(s).  fp64.
+
+    q: [G, D]; K, V: [N, D].  Empty N -> (o = 0, L = -inf) (SURVEY §8(b) empty-shard rule).
+    """
+    q = np.asarray(q, dtype=np.float64)
+    K = np.asarray(K, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    G, D = q.shape
+    if K.shape[0] == 0:
+        return np.zeros((G, V.shape[1])), np.full(G, -np.inf)
+    s = q @ K.T / math.sqrt(D)
+    m = s.max(axis=1, keepdims=True)
+    p = np.exp(s - m)
+    ell = p.sum(axis=1, keepdims=True)
+    o = (p @ V) / ell
+    L = (m + np.log(ell))[:, 0]
+    return o, L
+
+
+def attention_vq(q: np.ndarray, lam: np.ndarray, Ck: np.ndarray, Cv: np.ndarray,
+                 k_codes: np.ndarray, v_codes: np.ndarray):
+    """Decode attention over the VQ cache, Eq. 10 with Alg. 1's (o, L).
+
+    q: [G, D] raw query heads sharing one KV head (GQA, reading R15); lam: [D];
+    k_codes, v_codes: [N, M].  q~ = q diag(lambda) H_D (Eq. 7); s = q~ VQ^-1(K~_q)^T / sqrt(D);
+    o = softmax(s) VQ^-1(V_q); L = logsumexp(s) (natural log, reading R12).  fp64.
+    """
+    qt = transform_query(q, lam)
+    Kh = vq_decode(k_codes, Ck)
+    Vh = vq_decode(v_codes, Cv)
+    return attention_full(qt, Kh, Vh)
+
+
+def build_lut(q_tilde: np.ndarray, Ck: np.ndarray) -> np.ndarray:
+    """Alg. 1 line 4: q~' = reshape(q~, (M, D/M)); lut = q~' C_k^T  -> [M, 2^b] fp64."""
+    q_tilde = np.asarray(q_tilde, dtype=np.float64)
+    Ck = np.asarray(Ck, dtype=np.float64)
+    d = Ck.shape[1]
+    return q_tilde.reshape(-1, d) @ Ck.T
+
+
+def merge_lse(o_parts: np.ndarray, L_parts: np.ndarray):
+    """Merge split partials (o_s normalised, L_s) over axis 0: L = logsumexp_s L_s,
+    o = sum_s exp(L_s - L) o_s (the online-softmax recurrence of P:745-757 applied to whole
+    splits).  Partials with L_s = -inf carry zero weight; all -inf -> (0, -inf).
+    """
+    o_parts = np.asarray(o_parts, dtype=np.float64)
+    L_parts = np.asarray(L_parts, dtype=np.float64)
+    Lmax = L_parts.max(axis=0)
+    finite = np.isfinite(Lmax)
+    safe = np.where(finite, Lmax, 0.0)
+    w = np.where(np.isfinite(L_parts), np.exp(L_parts - safe[None]), 0.0)
+    tot = w.sum(axis=0)
+    L = np.where(finite, safe + np.log(np.where(finite, tot, 1.0)), -np.inf)
+    o = (w[..., None] * o_parts).sum(axis=0) / np.where(finite, tot, 1.0)[..., None]
+    o = np.where(finite[..., None], o, 0.0)
+    return o, L
+
+
+def attention_decode_batch(q: np.ndarray, lam: np.ndarray, Ck: np.ndarray, Cv: np.ndarray,
+                           k_codes: np.ndarray, v_codes: np.ndarray, seq_lens, tok_begin: int = 0,
+                           tok_end: int | None = None):
+    """One decode-attention layer call over a batch (the §8(b) vecinfer_attn_decode contract).
+
+    q: [B, H_q, D]; lam: [H_kv, D]; Ck/Cv: [H_kv, 2^b, d] (or [2^b, d] shared);
+    k_codes/v_codes: [B, H_kv, n_cap, M]; token range [tok_begin, min(tok_end, seq_len)).
+    Query head i reads KV head i // (H_q/H_kv) (GQA).  Returns o [B, H_q, D], L [B, H_q] fp64.
+    """
+    B, Hq, D = q.shape
+    Hkv = k_codes.shape[1]
+    G = Hq // Hkv
+    o = np.zeros((B, Hq, D))
+    L = np.full((B, Hq), -np.inf)
+    for b in range(B):
+        n = int(seq_lens[b])
+        e = n if tok_end is None else min(int(tok_end), n)
+        s = min(int(tok_begin), e)
+        for h in range(Hkv):
+            ck = Ck[h] if np.ndim(Ck) == 3 else Ck
+            cv = Cv[h] if np.ndim(Cv) == 3 else Cv
+            oo, LL = attention_vq(q[b, h * G:(h + 1) * G], lam[h], ck, cv,
+                                  k_codes[b, h, s:e], v_codes[b, h, s:e])
+            o[b, h * G:(h + 1) * G] = oo
+            L[b, h * G:(h + 1) * G] = LL
+    return o, L
+
+
+# --------------------------------------------------------------------------------------------
+# Code packing (reading R11) and byte accounting.
+# --------------------------------------------------------------------------------------------
+
+
+def pack_codes(codes: np.ndarray, code_bits: int) -> np.ndarray:
+    """Token-major packed rows: 8-bit one byte per code; 4-bit sub-vector 2i in the low nibble,
+    2i+1 in the high nibble; 16-bit little-endian u16.  codes: [..., M] -> uint8 [..., M*b/8]."""
+    codes = np.asarray(codes, dtype=np.int64)
+    if code_bits == 8:
+        return codes.astype(np.uint8)
+    if code_bits == 4:
+        lo = codes[..., 0::2]
+        hi = codes[..., 1::2]
+        return (lo | (hi << 4)).astype(np.uint8)
+    if code_bits == 16:
+        u = codes.astype(np.uint16)
+        return u.view(np.uint8).reshape(*codes.shape[:-1], codes.shape[-1] * 2)
+    raise ValueError("code_bits must be 4, 8 or 16")
+
+
+def unpack_codes(packed: np.ndarray, code_bits: int) -> np.ndarray:
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    if code_bits == 8:
+        return packed.astype(np.int64)
+    if code_bits == 4:
+        lo = (packed & 0xF).astype(np.int64)
+        hi = (packed >> 4).astype(np.int64)
+        out = np.empty(packed.shape[:-1] + (packed.shape[-1] * 2,), dtype=np.int64)
+        out[..., 0::2] = lo
+        out[..., 1::2] = hi
+        return out
+    if code_bits == 16:
+        return packed.view(np.uint16).astype(np.int64)
+    raise ValueError("code_bits must be 4, 8 or 16")
+
+
+def codebook_bytes(sub_dim: int, code_bits: int) -> int:
+    """2^b x d x 2 bytes."""
+    return (1 << code_bits) * sub_dim * 2
+
+
+def index_bytes_per_vector(head_dim: int, sub_dim: int, code_bits: int) -> float:
+    """(d_h / d) x (b / 8) bytes per cached vector."""
+    return (head_dim // sub_dim) * code_bits / 8.0
+
+
+def avg_bits(sub_dim: int, code_bits: int) -> float:
+    """b / d bits per element ("Avg. bit" column of Table 2, e.g. d4b8 -> 2)."""
+    return code_bits / sub_dim
+
+
+# --------------------------------------------------------------------------------------------
+# Codebook fitting (harness only): K-means, <= 30 iterations.
+# --------------------------------------------------------------------------------------------
+
+
+def _sqdist(X: np.ndarray, C: np.ndarray) -> np.ndarray:
+    X = np.asarray(X, dtype=np.float64)
+    C = np.asarray(C, dtype=np.float64)
+    return (X * X).sum(1)[:, None] - 2.0 * X @ C.T + (C * C).sum(1)[None, :]
+
+
+def kmeans(X: np.ndarray, n_clusters: int, max_iters: int = 30, seed: int = 0):
+    """K-means with k-means++ seeding and Lloyd iterations ("maximum number of iterations
+    set to 30"); empty clusters re-seeded at the current worst-distortion point.
+    Returns (centroids fp64 [n_clusters, d], objective history)."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    if n < n_clusters:
+        raise ValueError("insufficient data for k-means")
+    rng = np.random.default_rng(seed)
+    C = np.empty((n_clusters, X.shape[1]))
+    C[0] = X[rng.integers(n)]
+    d2 = ((X - C[0]) ** 2).sum(1)
+    for c in range(1, n_clusters):
+        tot = d2.sum()
+        if tot <= 0:
+            C[c] = X[rng.integers(n)]
+        else:
+            C[c] = X[rng.choice(n, p=d2 / tot)]
+        d2 = np.minimum(d2, ((X - C[c]) ** 2).sum(1))
+    hist = []
+    for _ in range(max_iters):
+        assign = np.empty(n, dtype=np.int64)
+        best = np.empty(n)
+        for s0 in range(0, n, 65536):
+            dd = _sqdist(X[s0:s0 + 65536], C)
+            assign[s0:s0 + 65536] = dd.argmin(1)
+            best[s0:s0 + 65536] = dd[np.arange(dd.shape[0]), assign[s0:s0 + 65536]]
+        hist.append(float(np.maximum(best, 0).sum()))
+        counts = np.bincount(assign, minlength=n_clusters)
+        sums = np.zeros_like(C)
+        np.add.at(sums, assign, X)
+        newC = C.copy()
+        nz = counts > 0
+        newC[nz] = sums[nz] / counts[nz, None]
+        order = np.argsort(-best, kind="stable")
+        k = 0
+        for c in np.nonzero(~nz)[0]:
+            newC[c] = X[order[k]]
+            k += 1
+        if np.array_equal(newC, C):
+            break
+        C = newC
+    return C, hist
