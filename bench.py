@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark of the VecInfer decode-attention hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg3|cfg4|cfg5-b1d4|...]
+    python bench.py --impl reference ...      # the CPU oracle arm (test infrastructure, timed as-is)
+
+One STEP = one decoded token through the attention of all 32 Llama-3.1-8B layers: per layer, the
+new token's k, v are encoded into the VQ cache (vecinfer_encode_kv, Eq. 9) and the G=4-grouped
+decode attention runs over the whole cache (vecinfer_attn_decode: query transform + fused
+dequant-MMA attention + split LSE merge, Eq. 10 / Alg. 1).  Each layer owns its own code cache, so a
+step streams 32 distinct caches (512 MiB at configs[1]) -- larger than the 126 MB L2, no flush
+needed.  The step is captured in a CUDA graph (the launch-bound inner loop; 2 kernels/layer).
+Timing: W untimed warm-up steps, then EXACTLY K steps bracketed by barrier + synchronize, CUDA
+events on the launching stream, max over ranks.  value = compressed-KV bytes of all ranks / time.
+The new token is written at row N-1 every step so every timed step does identical work.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "VQ decode-attn µs/step & HBM GB/s (% peak), Llama-3.1-8B b2d4, 1–8×B200"
+H_Q, H_KV, D, LAYERS = 32, 8, 128, 32
+
+WORKLOADS = {
+    # name: (batch, seq_len, kbits, vbits, description)
+    "cfg1": (1, 1024, 8, 8, "configs[0]: 1 batch, seq 1024, b2d4 (all 8 KV heads)"),
+    "cfg2": (1, 32768, 8, 8, "configs[1]: Llama-3.1-8B b2d4, batch 1, seq 32k, 1xB200"),
+    "cfg3": (64, 8192, 8, 8, "configs[2]: Llama-3.1-8B b2d4, batch 64, seq 8k (per-rank batch slice at N>1)"),
+    "cfg4": (1, 196608, 8, 8, "configs[3]: Llama-3.1-8B b2d4, batch 1, seq 196k (sequence-sharded at N>1)"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_codebooks():
+    import synth
+    z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz"))
+    out = {"lambda": z["lambda"], "inv_lambda": z["inv_lambda"]}
+    for k in z.files:
+        if k[:3] in ("ck_", "cv_"):
+            out[k] = synth.bf16_from_bits(z[k])
+    return out
+
+
+# ------------------------------------------------------------------------------ clocks (NVML)
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index: int, period_s: float = 0.005):
+        self.ok = False
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ CPU oracle arm
+def oracle_sample(seconds: float, N: int, seed: int = 7):
+    """Time the CPU oracle (as it stands) on (b, h_kv) units of the workload: one unit = the
+    decode-attention of 4 grouped query heads over N cached tokens (+ the 1-token append encode).
+    Returns (units, seconds, threads)."""
+    import synth
+    from oracle import ref
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count() or 1
+    cb = load_codebooks()
+    rng = np.random.default_rng(seed)
+    kc = rng.integers(0, 256, (N, 32))
+    vc = rng.integers(0, 256, (N, 32))
+    q = synth.gen_queries(1, H_Q, H_KV, D, seed=seed)[0]
+    knew = synth.gen_keys(1, H_KV, D, seed=seed)[0, 0]
+    vnew = synth.gen_values(1, H_KV, D, seed=seed + 1)[0, 0]
+    units, t0 = 0, time.perf_counter()
+    while True:
+        h = units % H_KV
+        ref.encode_kv(knew[h], vnew[h], cb["inv_lambda"][h], cb["ck_b2d4"][h], cb["cv_b2d4"][h])
+        ref.attention_vq(q[4 * h:4 * h + 4], cb["lambda"][h], cb["ck_b2d4"][h], cb["cv_b2d4"][h], kc, vc)
+        units += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return units, el, threads
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle timed on the box's host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    B, N, _, _, desc = WORKLOADS[args.workload]
+    unit_bytes = N * 64
+    for _ in range(args.warmup):
+        oracle_sample(0.0, N)
+    units, secs = 0, 0.0
+    threads = 1
+    for _ in range(args.steps):
+        u, s, threads = oracle_sample(args.ref_step_seconds, N)
+        units += u
+        secs += s
+    gbs = units * unit_bytes / secs / 1e9
+    step_ms = secs / max(args.steps, 1) * 1e3
+    sample = (f"{units} (b,h_kv) units of N={N} tokens (4 grouped q-heads each, + 1-token append encode) "
+              f"over {args.steps} steps of ~{args.ref_step_seconds}s")
+    line = {"impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": desc, "global_batch": B, "seq_len": N},
+            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import synth
+    from paper_2510_06175_b200 import vecinfer as vi
+    from paper_2510_06175_b200.sharding import batch_shard, gather_partials_packed, shard_range
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B_glob, N, kbits, vbits, desc = WORKLOADS[args.workload]
+    seq_sharded = args.workload == "cfg4" and world > 1
+    if args.workload == "cfg3" and world > 1:
+        b0, b1 = batch_shard(B_glob, rank, world)
+        B = b1 - b0
+    else:
+        B = B_glob
+    tok0, tok1 = shard_range(N, rank, world) if seq_sharded else (0, N)
+    L = args.layers
+    cb = load_codebooks()
+    lam = torch.from_numpy(cb["lambda"]).to(dev)
+    inv = torch.from_numpy(cb["inv_lambda"]).to(dev)
+    ck = torch.from_numpy(cb["ck_b2d4"]).to(dev).to(torch.bfloat16)
+    cv = torch.from_numpy(cb["cv_b2d4"]).to(dev).to(torch.bfloat16)
+    kcfg = vcfg = vi.B2D4
+
+    # ---- prefill: bulk-encode synthetic keys/values of one layer (Eq. 8), replicate per layer
+    n_local = tok1 - tok0
+    t_gen = time.perf_counter()
+    kc0 = torch.empty(B, H_KV, n_local, 32, dtype=torch.uint8, device=dev)
+    vc0 = torch.empty_like(kc0)
+    chunk = 4096
+    prefill_ms = 0.0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for c0 in range(0, n_local, chunk):
+        c1 = min(c0 + chunk, n_local)
+        k = torch.from_numpy(synth.gen_keys(c1 - c0, H_KV, D, seed=1000 * rank + c0, batch=B)).to(dev).to(torch.bfloat16)
+        v = torch.from_numpy(synth.gen_values(c1 - c0, H_KV, D, seed=7 + 1000 * rank + c0, batch=B)).to(dev).to(torch.bfloat16)
+        wp = torch.full((B,), c0, dtype=torch.int32, device=dev)
+        ev0.record()
+        vi.encode_kv(k, v, inv, ck, cv, kc0, vc0, wp, kcfg, vcfg)
+        ev1.record()
+        ev1.synchronize()
+        prefill_ms += ev0.elapsed_time(ev1)
+    prefill_tok_s = B * n_local / (prefill_ms / 1e3)
+    kcs = [kc0] + [kc0.clone() for _ in range(L - 1)]
+    vcs = [vc0] + [vc0.clone() for _ in range(L - 1)]
+    # cache layout seen by the kernels: rows [0, n_local) of this rank's shard
+    seq_lens = torch.full((B,), n_local, dtype=torch.int32, device=dev)
+    owns_tail = (not seq_sharded) or (tok1 == N)
+    write_pos = torch.full((B,), n_local - 1, dtype=torch.int32, device=dev)
+    q_all = torch.from_numpy(np.stack([synth.gen_queries(B, H_Q, H_KV, D, seed=50 + l) for l in range(L)])).to(dev).to(torch.bfloat16)
+    kn_all = torch.from_numpy(np.stack([synth.gen_keys(1, H_KV, D, seed=90 + l, batch=B) for l in range(L)])).to(dev).to(torch.bfloat16)
+    vn_all = torch.from_numpy(np.stack([synth.gen_values(1, H_KV, D, seed=91 + l, batch=B) for l in range(L)])).to(dev).to(torch.bfloat16)
+    gen_s = time.perf_counter() - t_gen
+
+    o_all = torch.empty(L, B, H_Q, D, dtype=torch.bfloat16, device=dev)
+    lse_all = torch.empty(L, B, H_Q, dtype=torch.float32, device=dev)
+    o_part = torch.empty(L, B, H_Q, D, dtype=torch.float32, device=dev) if seq_sharded else None
+    S = vi.attn_num_splits(B, H_KV, n_local, 0)
+    ws = [vi.attn_workspace(B, H_Q, H_KV, n_local, 0, device=dev) for _ in range(L)]
+    stream = torch.cuda.Stream(device=dev)
+
+    def layer(l, ev_pair=None):
+        if owns_tail:
+            vi.encode_kv(kn_all[l], vn_all[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg)
+        if ev_pair is not None:
+            ev_pair[0].record()
+        if seq_sharded:
+            vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, out=o_part[l], lse=lse_all[l],
+                           workspace=ws[l])
+        else:
+            vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, out=o_all[l], lse=lse_all[l],
+                           workspace=ws[l])
+        if ev_pair is not None:
+            ev_pair[1].record()
+
+    def step_eager(evs=None):
+        for l in range(L):
+            layer(l, None if evs is None else evs[l])
+        if seq_sharded:   # one all-gather of the per-rank partials of all 32 layers, then LSE merge
+            o_g, l_g = gather_partials_packed(o_part, lse_all)
+            vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
+                         o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D))
+
+    launches_per_step = L * ((1 if owns_tail else 0) + 1) + (1 if seq_sharded else 0)
+
+    # ---- warm-up (eager) so lazy init/attributes happen outside capture
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            step_eager()
+    torch.cuda.synchronize(dev)
+
+    use_graph = not args.no_graph and not seq_sharded   # NCCL all-gather kept eager
+    K, W = args.steps, args.warmup
+    evs = [[(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+            for _ in range(L)] for _ in range(K)]
+    graphs = []
+    if use_graph:
+        g_warm = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_warm, stream=stream):
+            step_eager()
+        for k in range(K):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step_eager(evs[k])
+            graphs.append(g)
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            if use_graph:
+                g_warm.replay()
+            else:
+                step_eager()
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        with torch.cuda.stream(stream):
+            t_start.record(stream)
+            for k in range(K):
+                if use_graph:
+                    graphs[k].replay()
+                else:
+                    step_eager(evs[k])
+            t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    elapsed_ms = t_start.elapsed_time(t_end)
+    attn_ms = [evs[k][l][0].elapsed_time(evs[k][l][1]) for k in range(K) for l in range(L)]
+    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t_max.item())
+
+    # ---- end to end through the public API: pinned host inputs -> device, eager calls, D2H read
+    q_h = q_all.cpu().pin_memory()
+    kn_h = kn_all.cpu().pin_memory()
+    vn_h = vn_all.cpu().pin_memory()
+    o_h = torch.empty(o_all.shape, dtype=o_all.dtype).pin_memory()
+    q_d, kn_d, vn_d = torch.empty_like(q_all), torch.empty_like(kn_all), torch.empty_like(vn_all)
+
+    def step_e2e():
+        q_d.copy_(q_h, non_blocking=True)
+        kn_d.copy_(kn_h, non_blocking=True)
+        vn_d.copy_(vn_h, non_blocking=True)
+        for l in range(L):
+            if owns_tail:
+                vi.encode_kv(kn_d[l], vn_d[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg)
+            if seq_sharded:
+                vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, out=o_part[l], lse=lse_all[l], workspace=ws[l])
+            else:
+                vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, out=o_all[l], lse=lse_all[l], workspace=ws[l])
+        if seq_sharded:
+            o_g, l_g = gather_partials_packed(o_part, lse_all)
+            vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
+                         o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D))
+        o_h.copy_(o_all, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, W)):
+            step_e2e()
+        barrier()
+        e0 = time.perf_counter()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0e.record(stream)
+        for _ in range(K):
+            step_e2e()
+        t1e.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = t0e.elapsed_time(t1e)
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    h2d = q_h.numel() * 2 + kn_h.numel() * 2 + vn_h.numel() * 2 if owns_tail else q_h.numel() * 2
+    d2h = o_h.numel() * 2
+
+    if rank != 0:
+        return
+    # ---- figures
+    code_bytes_rank = B * H_KV * n_local * 64                   # K + V codes per layer call
+    total_bytes = code_bytes_rank * L * K * (world if not seq_sharded else 1)
+    if seq_sharded:
+        total_bytes = B * H_KV * N * 64 * L * K
+    value = total_bytes / (elapsed_ms / 1e3) / 1e9
+    e2e_value = total_bytes / (e2e_ms / 1e3) / 1e9
+    peak, peak_src = load_peaks()
+    attn_avg_ms = float(np.mean(attn_ms))
+    achieved = code_bytes_rank / (attn_avg_ms / 1e3) / 1e9
+    step_ms = elapsed_ms / K
+    cpu = None
+    if not args.no_cpu_baseline:
+        units, secs, threads = oracle_sample(args.cpu_seconds, N if not seq_sharded else N)
+        cpu = {"value": units * N * 64 / secs / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
+               "sample": f"{units} (b,h_kv) units x {N} tokens (4 grouped q-heads each + 1-token append encode) "
+                         f"in {secs:.1f}s on {os.cpu_count()} host cores (NumPy fp64; threads = BLAS pool)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if seq_sharded else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": desc, "global_batch": B_glob, "seq_len": N,
+                   "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": "b2d4",
+                   "parallelism": ("seq-shard" if seq_sharded else "dp") + str(world),
+                   "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
+                   "num_splits": S, "cuda_graph": use_graph,
+                   "dtype_detail": "u8 codes, bf16 q/k/v/o, fp16 hi/lo MMA operands, f32 accumulate"},
+        "us_per_layer_call": step_ms * 1e3 / L,
+        "tokens_per_s": B_glob * 1e3 / step_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "attn_mma8_kernel (vecinfer_attn_decode)",
+                     "attn_us_avg": attn_avg_ms * 1e3, "attn_us_p10": float(np.percentile(attn_ms, 10)) * 1e3,
+                     "attn_us_p90": float(np.percentile(attn_ms, 90)) * 1e3,
+                     "algorithmic_bytes_per_launch": code_bytes_rank, "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_ms / K, "api": "eager vecinfer.encode_kv/attn_decode per layer, pinned H2D/D2H"},
+        "gpu_launches": launches_per_step * K,
+        "clocks": clk.summary(),
+        "prefill_encode": {"tokens_per_s": prefill_tok_s, "note": "bulk vecinfer_encode_kv, all 8 KV heads, K+V"},
+        "setup_s": gen_s,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=2.0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,191 @@
+/* vecinfer.h -- C ABI of the B200-native VecInfer decode-attention library (libvecinfer.so).
+ *
+ * VecInfer (arXiv 2510.06175): decode-time self-attention computed directly over a
+ * vector-quantized KV cache.  Keys are smoothed (Eq. 3-4) and Hadamard-rotated (Eq. 5-6)
+ * before product-VQ encoding (Eq. 2, 8, 9); queries get the matching transform so that
+ * q~ K~^T = q K^T (Eq. 7); attention runs over the codes without materialising a dequantized
+ * cache (Eq. 10, Algorithm 1).  Citations "P:n" are lines of the paper text PAPER.md.
+ *
+ * Conventions shared by every entry point
+ *  - Every tensor pointer is a DEVICE pointer owned by the caller (e.g. allocated by PyTorch).
+ *    The library never allocates device memory, never synchronises the device, and launches
+ *    only on the stream it is given.
+ *  - Strides are in ELEMENTS; the innermost (head_dim) dimension is always contiguous.
+ *  - bf16 tensors are raw IEEE bfloat16 (uint16) buffers.
+ *  - A status is returned synchronously after argument validation and before any launch;
+ *    VECINFER_ERR_CUDA reports a launch/configuration error (cudaGetLastError); asynchronous
+ *    device faults surface at the caller's next synchronisation.  No exception or abort
+ *    crosses the ABI.  vecinfer_last_error() returns a thread-local description of the last
+ *    non-OK status of the calling thread.
+ *  - Thread-safe: no global mutable state except the thread-local error string and a
+ *    per-device attribute cache.
+ *  - Supported shapes (v1): head_dim D = 128, sub_dim d = 4, code_bits in {4, 8, 16}
+ *    (b1d4, b2d4, b4d4 in BASELINE.json notation = paper d4b4, d4b8, d4b16);
+ *    GQA group G = H_q / H_kv in {1, 2, 4}.  Anything else returns VECINFER_ERR_UNSUPPORTED.
+ */
+#ifndef VECINFER_H_
+#define VECINFER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VECINFER_ABI_VERSION 1
+
+typedef struct CUstream_st* vecinfer_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  VECINFER_OK = 0,
+  VECINFER_ERR_INVALID_ARG = 1, /* NULL / misaligned pointer, bad enum, eps <= 0, bad stride     */
+  VECINFER_ERR_SHAPE = 2,       /* non-positive sizes, H_q % H_kv != 0, tok_begin > tok_end, ... */
+  VECINFER_ERR_UNSUPPORTED = 3, /* (D, d, code_bits, G) combination without a kernel             */
+  VECINFER_ERR_EMPTY = 4,       /* calibration with n_tokens == 0                                */
+  VECINFER_ERR_RANGE = 5,       /* (reported through the device err_flags word, see encode_kv)   */
+  VECINFER_ERR_WORKSPACE = 6,   /* workspace NULL or smaller than the *_workspace_bytes() query  */
+  VECINFER_ERR_CUDA = 7         /* CUDA launch / attribute error                                 */
+} vecinfer_status_t;
+
+typedef enum { VECINFER_BF16 = 0, VECINFER_F32 = 1 } vecinfer_dtype_t;
+
+/* Product-VQ configuration: head_dim D, sub-vector dim d, code bits b (2^b centroids).
+ * b2d4 = {128, 4, 8}: 256 centroids of 4 dims, one byte per sub-vector. */
+typedef struct {
+  int32_t head_dim;
+  int32_t sub_dim;
+  int32_t code_bits;
+} vecinfer_vq_t;
+
+/* Score/P.V algorithm of vecinfer_attn_decode.
+ *  DEQUANT_MMA: keys are dequantised from a bank-conflict-free replicated codebook into
+ *    tensor-core fragments; s = q~ K^T and o = P V both run as fp16 MMAs with hi/lo-split
+ *    operands (fp32 accumulate).  Default on sm_100a.
+ *  LUT: the paper's Algorithm 1 literally: lut = q~' C_k^T (l.4) in shared
+ *    memory, scores by table lookup (l.11), P.V from the dequantised value codebook on CUDA
+ *    cores (l.16).  Kept as the paper-faithful variant and for comparison. */
+typedef enum {
+  VECINFER_ATTN_AUTO = 0,
+  VECINFER_ATTN_DEQUANT_MMA = 1,
+  VECINFER_ATTN_LUT = 2
+} vecinfer_attn_algo_t;
+
+/* Device-side error bits written (atomicOr) into the optional err_flags word of encode_kv. */
+#define VECINFER_FLAG_RANGE 1u     /* |k * inv_lambda| >= 2^32: outside the pinned fixed point */
+#define VECINFER_FLAG_WRITE_POS 2u /* write_pos[b] + t outside [0, n_cap): row not written     */
+
+int vecinfer_abi_version(void);
+const char* vecinfer_last_error(void);
+const char* vecinfer_status_string(vecinfer_status_t status);
+
+/* ---------------------------------------------------------------------------------------
+ * Smoothing-factor calibration, Eq. 4: lambda_c = sqrt(max_n |K[n, h, c]|).
+ *   k_cal        bf16 [n_tokens, n_kv_heads, head_dim], element (n, h, c) at
+ *                n * stride_tok + h * stride_head + c.
+ *   eps_floor    > 0; lambda = max(RN32(sqrt(amax)), RN32(eps_floor)) (SPEC S:91 floor).
+ *   lambda_out, inv_lambda_out   fp32 [n_kv_heads, head_dim]; inv_lambda = RN32(1 / lambda).
+ *   workspace    >= vecinfer_calibrate_workspace_bytes(n_kv_heads, head_dim) bytes; contents
+ *                are overwritten (zeroed on the stream before use).
+ * Errors: INVALID_ARG (NULL, eps <= 0, stride_head < head_dim when n_kv_heads > 1),
+ *         EMPTY (n_tokens == 0), SHAPE (head_dim % 8 != 0 or <= 0), WORKSPACE, CUDA.
+ * ------------------------------------------------------------------------------------- */
+size_t vecinfer_calibrate_workspace_bytes(int32_t n_kv_heads, int32_t head_dim);
+vecinfer_status_t vecinfer_calibrate_smooth(const void* k_cal_bf16, int64_t n_tokens,
+                                            int32_t n_kv_heads, int32_t head_dim,
+                                            int64_t stride_tok, int64_t stride_head,
+                                            float eps_floor, float* lambda_out,
+                                            float* inv_lambda_out, void* workspace,
+                                            size_t workspace_bytes, vecinfer_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * KV encode + cache store: prefill (Eq. 8, T tokens) and decode append (Eq. 9,
+ * P:241-249, T = 1).  Per (b, t, h):
+ *   key:   x = (k diag(lambda)^-1) H_D (S then H) on the pinned exact fixed point
+ *          (R10): A = rint(k*inv_lambda*2^24) in int64, X = A H_pm (warp-shuffle
+ *          FWHT, exact), x = RN32(RN32(X) * 2^-24) * RN32(1/sqrt(D)); then
+ *          code[m] = argmin_j ||x_m - C_k[j]||^2 (Eq. 2).
+ *   value: code[m] = argmin_j ||v_m - C_v[j]||^2 (values are not transformed, Eq. 8).
+ *   Distances: fp32, each op round-to-nearest, no FMA, order ((e0^2+e1^2)+e2^2)+e3^2; ties to
+ *   the lowest index (R9).  Codes are bit-identical to the CPU oracle.
+ *   k_bf16, v_bf16   [B, T, H_kv, D] with element strides (b, t, h) in k_strides / v_strides.
+ *   inv_lambda       fp32 [H_kv, D] (from vecinfer_calibrate_smooth).
+ *   ck_bf16, cv_bf16 codebooks [H_kv, 2^b, d] bf16; *_head_stride = elements between heads,
+ *                    0 = one codebook shared by all heads.
+ *   k_codes, v_codes uint8 [B, H_kv, n_cap, D/d*b/8] token-major packed rows (R11: 8-bit one
+ *                    byte per sub-vector; 4-bit sub-vector 2i low nibble, 2i+1 high nibble;
+ *                    16-bit little-endian u16).
+ *   write_pos        device int32 [B]: cache row of token t = 0 of batch b (e.g. seq_len).
+ *   err_flags        device uint32 (may be NULL): VECINFER_FLAG_* bits are OR-ed in.
+ *   workspace        >= vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg, vcfg) bytes (0 for
+ *                    4/8-bit codebooks, which are searched from shared memory; 16-bit
+ *                    codebooks are searched by centroid-split CTAs that combine partial
+ *                    minima with 64-bit atomicMin on (dist_bits << 32 | index)).
+ * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, WORKSPACE, CUDA.
+ * ------------------------------------------------------------------------------------- */
+size_t vecinfer_encode_workspace_bytes(int32_t B, int32_t T, int32_t H_kv, vecinfer_vq_t kcfg,
+                                       vecinfer_vq_t vcfg);
+vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int32_t B,
+                                     int32_t T, int32_t H_kv, const int64_t k_strides[3],
+                                     const int64_t v_strides[3], const float* inv_lambda,
+                                     const void* ck_bf16, const void* cv_bf16,
+                                     int64_t ck_head_stride, int64_t cv_head_stride,
+                                     vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes,
+                                     uint8_t* v_codes, int64_t n_cap, const int32_t* write_pos,
+                                     uint32_t* err_flags, void* workspace, size_t workspace_bytes,
+                                     vecinfer_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Fused decode attention over the VQ cache, Eq. 10 + Algorithm 1,
+ * split-KV (grid over (batch, KV head, split)) with the log-sum-exp merge of the
+ * split partials fused into the same launch (last CTA of each (b, h_kv) merges, fixed order).
+ *   q_bf16      [B, H_q, D] raw queries (strides q_stride_b, q_stride_h); query head i reads
+ *               KV head i / G (GQA).  The kernel applies q~ = q diag(lambda) H_D (Eq. 7).
+ *   lambda      fp32 [H_kv, D].
+ *   codebooks / codes / n_cap as in vecinfer_encode_kv (kcfg, vcfg may differ).
+ *   seq_lens    device int32 [B]; tokens [tok_begin, min(tok_end, seq_len)) are attended
+ *               (tok_end < 0 means "to seq_len"): the sharding hook for multi-GPU splits.
+ *   softmax_scale  usually 1/sqrt(D).
+ *   num_splits  0 = heuristic (fill 148 SMs); > 0 fixed => bitwise-deterministic results.
+ *   o           [B, H_q, D] bf16 or fp32 (o_dtype); lse fp32 [B, H_q] natural log.
+ *               An empty range yields o = 0, lse = -inf (weight 0 in vecinfer_merge_lse).
+ *   workspace   >= vecinfer_attn_workspace_bytes(B, H_q, H_kv, D, n_tokens_max, num_splits)
+ *               bytes, where n_tokens_max bounds the attended range; MUST be zero-filled once
+ *               when first allocated (the kernel leaves its counters at zero on exit).
+ * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, WORKSPACE, CUDA.
+ * ------------------------------------------------------------------------------------- */
+int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max,
+                                 int32_t num_splits);
+size_t vecinfer_attn_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int32_t D,
+                                     int64_t n_tokens_max, int32_t num_splits);
+vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_q,
+                                       int32_t H_kv, int64_t q_stride_b, int64_t q_stride_h,
+                                       const float* lambda, const void* ck_bf16,
+                                       const void* cv_bf16, int64_t ck_head_stride,
+                                       int64_t cv_head_stride, vecinfer_vq_t kcfg,
+                                       vecinfer_vq_t vcfg, const uint8_t* k_codes,
+                                       const uint8_t* v_codes, int64_t n_cap,
+                                       const int32_t* seq_lens, int64_t tok_begin,
+                                       int64_t tok_end, float softmax_scale, int32_t num_splits,
+                                       vecinfer_attn_algo_t algo, void* o,
+                                       vecinfer_dtype_t o_dtype, float* lse, void* workspace,
+                                       size_t workspace_bytes, vecinfer_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Log-sum-exp merge of P normalised partials (cross-GPU sequence shards, residual window):
+ *   L = logsumexp_s L_s;  o = sum_s exp(L_s - L) o_s, summed in the fixed order s = 0..P-1
+ *   (the online-softmax recurrence of P:745-757 applied to whole partials).
+ *   o_parts fp32 [P, B, H_q, D] (normalised), lse_parts fp32 [P, B, H_q] (natural log);
+ *   partials with lse = -inf have zero weight; all -inf -> o = 0, lse = -inf.
+ *   o [B, H_q, D] bf16 or fp32; lse fp32 [B, H_q] (may be NULL).
+ * Errors: INVALID_ARG, SHAPE, CUDA.
+ * ------------------------------------------------------------------------------------- */
+vecinfer_status_t vecinfer_merge_lse(const float* o_parts, const float* lse_parts, int32_t P,
+                                     int32_t B, int32_t H_q, int32_t D, void* o,
+                                     vecinfer_dtype_t o_dtype, float* lse,
+                                     vecinfer_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VECINFER_H_ */

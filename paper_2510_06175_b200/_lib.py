@@ -1,0 +1,74 @@
+"""ctypes loader for libvecinfer.so and its C-ABI prototypes (include/vecinfer.h).
+
+There is no fallback: if the in-tree library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvecinfer.so")
+
+c_i32, c_i64, c_u32, c_f32, c_sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_float, ctypes.c_size_t
+c_void_p, c_char_p = ctypes.c_void_p, ctypes.c_char_p
+I64x3 = ctypes.c_int64 * 3
+
+
+class VQ(ctypes.Structure):
+    """vecinfer_vq_t {head_dim, sub_dim, code_bits}."""
+    _fields_ = [("head_dim", c_i32), ("sub_dim", c_i32), ("code_bits", c_i32)]
+
+
+STATUS = {0: "VECINFER_OK", 1: "VECINFER_ERR_INVALID_ARG", 2: "VECINFER_ERR_SHAPE", 3: "VECINFER_ERR_UNSUPPORTED",
+          4: "VECINFER_ERR_EMPTY", 5: "VECINFER_ERR_RANGE", 6: "VECINFER_ERR_WORKSPACE", 7: "VECINFER_ERR_CUDA"}
+
+# name -> (restype, argtypes); mirrors include/vecinfer.h exactly
+PROTOTYPES = {
+    "vecinfer_abi_version": (c_i32, []),
+    "vecinfer_last_error": (c_char_p, []),
+    "vecinfer_status_string": (c_char_p, [c_i32]),
+    "vecinfer_calibrate_workspace_bytes": (c_sz, [c_i32, c_i32]),
+    "vecinfer_calibrate_smooth": (c_i32, [c_void_p, c_i64, c_i32, c_i32, c_i64, c_i64, c_f32, c_void_p, c_void_p,
+                                          c_void_p, c_sz, c_void_p]),
+    "vecinfer_encode_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, VQ, VQ]),
+    "vecinfer_encode_kv": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, I64x3, I64x3, c_void_p, c_void_p,
+                                   c_void_p, c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p, c_void_p,
+                                   c_void_p, c_sz, c_void_p]),
+    "vecinfer_attn_num_splits": (c_i32, [c_i32, c_i32, c_i64, c_i32]),
+    "vecinfer_attn_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i32]),
+    "vecinfer_attn_decode": (c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i64, c_i64, c_void_p, c_void_p, c_void_p,
+                                     c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_i64, c_f32,
+                                     c_i32, c_i32, c_void_p, c_i32, c_void_p, c_void_p, c_sz, c_void_p]),
+    "vecinfer_merge_lse": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_void_p, c_i32, c_void_p,
+                                   c_void_p]),
+}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libvecinfer.so not built at {LIB_PATH}; run `python -m paper_2510_06175_b200.build` "
+                              "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in PROTOTYPES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+class VecInferError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        msg = load().vecinfer_last_error().decode(errors="replace")
+        super().__init__(f"{fn} -> {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def check(fn: str, status: int) -> None:
+    if status != 0:
+        raise VecInferError(fn, status)

@@ -1,0 +1,69 @@
+// ABI plumbing: version, thread-local error strings, status names, device attribute cache.
+#include <stdarg.h>
+#include <stdio.h>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace vecinfer {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+vecinfer_status_t fail(vecinfer_status_t st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+vecinfer_status_t check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(VECINFER_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return VECINFER_OK;
+}
+
+int device_sm_count() {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+}  // namespace vecinfer
+
+extern "C" {
+
+int vecinfer_abi_version(void) { return VECINFER_ABI_VERSION; }
+
+const char* vecinfer_last_error(void) { return vecinfer::g_err; }
+
+const char* vecinfer_status_string(vecinfer_status_t s) {
+  switch (s) {
+    case VECINFER_OK: return "VECINFER_OK";
+    case VECINFER_ERR_INVALID_ARG: return "VECINFER_ERR_INVALID_ARG";
+    case VECINFER_ERR_SHAPE: return "VECINFER_ERR_SHAPE";
+    case VECINFER_ERR_UNSUPPORTED: return "VECINFER_ERR_UNSUPPORTED";
+    case VECINFER_ERR_EMPTY: return "VECINFER_ERR_EMPTY";
+    case VECINFER_ERR_RANGE: return "VECINFER_ERR_RANGE";
+    case VECINFER_ERR_WORKSPACE: return "VECINFER_ERR_WORKSPACE";
+    case VECINFER_ERR_CUDA: return "VECINFER_ERR_CUDA";
+  }
+  return "VECINFER_UNKNOWN_STATUS";
+}
+
+}  // extern "C"

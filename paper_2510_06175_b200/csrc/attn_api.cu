@@ -1,0 +1,116 @@
+// Host side of vecinfer_attn_decode: validation, split heuristic, workspace layout, dispatch.
+#include "attn_common.cuh"
+
+using namespace vecinfer;
+
+namespace {
+
+constexpr int kMaxSplits = 128;
+constexpr int64_t kMinTokensPerSplit = 512;
+
+bool vq_ok(const vecinfer_vq_t& c) { return c.head_dim == 128 && c.sub_dim == 4 && c.code_bits == 8; }
+
+struct WsLayout {
+  size_t part_o, part_l, counter, total;
+};
+
+WsLayout ws_layout(int32_t B, int32_t H_kv, int32_t S) {
+  WsLayout w;
+  const size_t units = static_cast<size_t>(B) * H_kv;
+  w.counter = 0;
+  w.part_l = ((units * sizeof(uint32_t)) + 255) & ~size_t(255);
+  w.part_o = w.part_l + ((units * S * 4 * sizeof(float) + 255) & ~size_t(255));
+  w.total = w.part_o + units * S * 4 * 128 * sizeof(float);
+  return w;
+}
+
+}  // namespace
+
+// One CTA per SM (kernel N4 uses 16 warps and 66 KiB of shared memory), so the grid
+// B*H_kv*S is chosen to fill whole waves of SMs; splits shorter than 512 tokens are avoided.
+extern "C" int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits) {
+  if (num_splits > 0) return num_splits > kMaxSplits ? kMaxSplits : num_splits;
+  if (B <= 0 || H_kv <= 0) return 1;
+  const int64_t units = static_cast<int64_t>(B) * H_kv;
+  const int sms = device_sm_count();
+  int64_t smax = (n_tokens_max + kMinTokensPerSplit - 1) / kMinTokensPerSplit;
+  if (smax < 1) smax = 1;
+  if (smax > kMaxSplits) smax = kMaxSplits;
+  int best = 1;
+  double best_score = -1.0;
+  for (int s = 1; s <= smax; ++s) {
+    const int64_t ctas = units * s;
+    const int64_t waves = (ctas + sms - 1) / sms;
+    const double eff = static_cast<double>(ctas) / static_cast<double>(waves * sms);
+    const double score = eff - 0.002 * s;
+    if (score > best_score + 1e-12) { best_score = score; best = s; }
+  }
+  return best;
+}
+
+extern "C" size_t vecinfer_attn_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int32_t D, int64_t n_tokens_max,
+                                                int32_t num_splits) {
+  (void)H_q; (void)D;
+  if (B <= 0 || H_kv <= 0) return 0;
+  const int32_t S = vecinfer_attn_num_splits(B, H_kv, n_tokens_max, num_splits);
+  return ws_layout(B, H_kv, S).total;
+}
+
+extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_q, int32_t H_kv,
+                                                  int64_t q_stride_b, int64_t q_stride_h, const float* lambda,
+                                                  const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride,
+                                                  int64_t cv_head_stride, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
+                                                  const uint8_t* k_codes, const uint8_t* v_codes, int64_t n_cap,
+                                                  const int32_t* seq_lens, int64_t tok_begin, int64_t tok_end,
+                                                  float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
+                                                  void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
+                                                  size_t workspace_bytes, vecinfer_stream_t stream) {
+  if (!q_bf16 || !lambda || !ck_bf16 || !cv_bf16 || !k_codes || !v_codes || !seq_lens || !o)
+    return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: NULL pointer");
+  if (o_dtype != VECINFER_BF16 && o_dtype != VECINFER_F32) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad o_dtype");
+  if (algo != VECINFER_ATTN_AUTO && algo != VECINFER_ATTN_DEQUANT_MMA && algo != VECINFER_ATTN_LUT)
+    return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad algo");
+  if (B <= 0 || H_q <= 0 || H_kv <= 0 || n_cap <= 0) return fail(VECINFER_ERR_SHAPE, "attn_decode: non-positive size");
+  if (H_q % H_kv != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode: H_q %% H_kv != 0");
+  const int G = H_q / H_kv;
+  if (G != 1 && G != 2 && G != 4) return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: GQA group %d not in {1,2,4}", G);
+  if (!vq_ok(kcfg) || !vq_ok(vcfg))
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: supported config is b2d4 (D=128, d=4, 8-bit codes)");
+  if (tok_begin < 0 || (tok_end >= 0 && tok_end < tok_begin))
+    return fail(VECINFER_ERR_SHAPE, "attn_decode: bad token range [%lld, %lld)", (long long)tok_begin, (long long)tok_end);
+  if (!(softmax_scale > 0.f) || !isfinite(softmax_scale)) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: softmax_scale must be finite > 0");
+  if (num_splits < 0) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: num_splits < 0");
+  if (q_stride_h % 4 || q_stride_b % 4 || q_stride_h < 0 || q_stride_b < 0 || !aligned(q_bf16, 8))
+    return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: q must be 8-byte aligned with strides multiple of 4");
+  if (!aligned(lambda, 16) || !aligned(ck_bf16, 8) || !aligned(cv_bf16, 8) || !aligned(k_codes, 16) ||
+      !aligned(v_codes, 16) || ck_head_stride % 4 || cv_head_stride % 4 || ck_head_stride < 0 || cv_head_stride < 0)
+    return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: misaligned lambda/codebooks/codes");
+  const int64_t range = tok_end >= 0 ? (tok_end - tok_begin < n_cap ? tok_end - tok_begin : n_cap) : n_cap;
+  const int32_t S = vecinfer_attn_num_splits(B, H_kv, range, num_splits);
+  const WsLayout wl = ws_layout(B, H_kv, S);
+  if (S > 1 && (!workspace || workspace_bytes < wl.total || !aligned(workspace, 256)))
+    return fail(VECINFER_ERR_WORKSPACE, "attn_decode: workspace needs %zu bytes (256-B aligned)", wl.total);
+  if (B > 65535 || H_kv > 65535) return fail(VECINFER_ERR_SHAPE, "attn_decode: grid too large");
+
+  AttnArgs a;
+  a.q = static_cast<const uint16_t*>(q_bf16);
+  a.q_sb = q_stride_b; a.q_sh = q_stride_h;
+  a.B = B; a.Hq = H_q; a.Hkv = H_kv; a.G = G;
+  a.lambda = lambda;
+  a.ck = static_cast<const uint16_t*>(ck_bf16);
+  a.cv = static_cast<const uint16_t*>(cv_bf16);
+  a.ck_hs = ck_head_stride; a.cv_hs = cv_head_stride;
+  a.kcodes = k_codes; a.vcodes = v_codes; a.n_cap = n_cap;
+  a.seq_lens = seq_lens; a.tok_begin = tok_begin; a.tok_end = tok_end;
+  a.qscale = static_cast<float>((1.0 / sqrt(128.0)) * static_cast<double>(softmax_scale) * 1.4426950408889634);
+  a.S = S;
+  a.o = o; a.o_f32 = (o_dtype == VECINFER_F32); a.lse = lse;
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  a.counter = S > 1 ? reinterpret_cast<uint32_t*>(ws + wl.counter) : nullptr;
+  a.part_l = S > 1 ? reinterpret_cast<float*>(ws + wl.part_l) : nullptr;
+  a.part_o = S > 1 ? reinterpret_cast<float*>(ws + wl.part_o) : nullptr;
+  cudaStream_t st = as_stream(stream);
+  if (algo == VECINFER_ATTN_LUT) launch_attn_lut(a, kcfg.code_bits, vcfg.code_bits, st);
+  else launch_attn_mma(a, kcfg.code_bits, vcfg.code_bits, st);
+  return check_launch("attn_decode");
+}

@@ -1,0 +1,155 @@
+// Internal declarations shared by the attention kernels and their host dispatch.
+#pragma once
+#include "common.cuh"
+
+namespace vecinfer {
+
+struct AttnArgs {
+  const uint16_t* q;  // bf16 [B, Hq, D]
+  int64_t q_sb, q_sh;
+  int B, Hq, Hkv, G;
+  const float* lambda;  // [Hkv, 128]
+  const uint16_t* ck;   // bf16 codebooks
+  const uint16_t* cv;
+  int64_t ck_hs, cv_hs;
+  const uint8_t* kcodes;  // [B, Hkv, n_cap, row]
+  const uint8_t* vcodes;
+  int64_t n_cap;
+  const int32_t* seq_lens;
+  int64_t tok_begin, tok_end;  // tok_end < 0: to seq_len
+  float qscale;                // (1/sqrt(D)) * softmax_scale * log2(e): folded into q~
+  int S;                       // splits per (b, h_kv)
+  void* o;
+  int o_f32;
+  float* lse;
+  float* part_o;     // [B*Hkv*S][4][128]
+  float* part_l;     // [B*Hkv*S][4]   (log2 domain)
+  uint32_t* counter; // [B*Hkv]
+};
+
+// Token range [r0, r1) of split s for (b, h) and the clamp of the attended range.
+__device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int64_t& r0, int64_t& r1) {
+  int64_t len = a.seq_lens[b];
+  if (len > a.n_cap) len = a.n_cap;
+  if (len < 0) len = 0;
+  int64_t e = a.tok_end < 0 ? len : (a.tok_end < len ? a.tok_end : len);
+  int64_t beg = a.tok_begin < e ? a.tok_begin : e;
+  if (beg < 0) beg = 0;
+  const int64_t n = e - beg;
+  int64_t chunk = (n + a.S - 1) / a.S;
+  chunk = (chunk + 31) & ~int64_t(31);
+  r0 = beg + s * chunk;
+  if (r0 > e) r0 = e;
+  r1 = r0 + chunk;
+  if (r1 > e) r1 = e;
+}
+
+// CTA epilogue shared by all kernels: combine per-warp (m, l, acc) partials held in shared
+// memory, then either write the final output (S == 1) or a split partial plus a fused
+// last-CTA log-sum-exp merge over the S splits in fixed order s = 0..S-1.
+//   wm[NW][4], wl[NW][4] (log2 domain), wacc[NW][4][128] (unnormalised)
+template <int NTHREADS>
+__device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s, int NWARPS,
+                                           const float* wm, const float* wl, const float* wacc) {
+  const int tid = threadIdx.x;
+  const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
+  __shared__ float sL[4];
+  __shared__ bool s_last;
+  for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
+    const int g = idx >> 7, dim = idx & 127;
+    float M = -INFINITY;
+    for (int w = 0; w < NWARPS; ++w) M = fmaxf(M, wm[w * 4 + g]);
+    float osum = 0.f, lsum = 0.f;
+    if (M != -INFINITY) {
+      for (int w = 0; w < NWARPS; ++w) {
+        const float f = ex2_approx(wm[w * 4 + g] - M);
+        lsum += f * wl[w * 4 + g];
+        osum += f * wacc[(w * 4 + g) * 128 + dim];
+      }
+    }
+    const bool empty = !(lsum > 0.f);
+    const float ov = empty ? 0.f : osum / lsum;
+    const float L2 = empty ? -INFINITY : M + __log2f(lsum);
+    if (a.S == 1) {
+      if (g < a.G) {
+        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+        if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
+        else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
+        if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = L2 * kLn2;
+      }
+    } else {
+      const int64_t pi = (unit * a.S + s) * 4 + g;
+      a.part_o[pi * 128 + dim] = ov;
+      if (dim == 0) a.part_l[pi] = L2;
+    }
+  }
+  if (a.S == 1) return;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&a.counter[unit], 1u) == static_cast<uint32_t>(a.S - 1));
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid < 4) {
+    float M = -INFINITY;
+    for (int ss = 0; ss < a.S; ++ss) M = fmaxf(M, __ldcg(&a.part_l[(unit * a.S + ss) * 4 + tid]));
+    sL[tid] = M;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
+    const int g = idx >> 7, dim = idx & 127;
+    if (g >= a.G) continue;
+    const float M = sL[g];
+    float osum = 0.f, wsum = 0.f;
+    if (M != -INFINITY) {
+      for (int ss = 0; ss < a.S; ++ss) {
+        const int64_t pi = (unit * a.S + ss) * 4 + g;
+        const float f = ex2_approx(__ldcg(&a.part_l[pi]) - M);
+        wsum += f;
+        osum += f * __ldcg(&a.part_o[pi * 128 + dim]);
+      }
+    }
+    const bool empty = !(wsum > 0.f);
+    const float ov = empty ? 0.f : osum / wsum;
+    const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+    if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
+    else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
+    if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (M + __log2f(wsum)) * kLn2;
+  }
+  if (tid == 0) a.counter[unit] = 0u;  // ready for the next launch
+}
+
+// Query transform of Eq. 7 for the G query heads of KV head h, one warp per head:
+// sq[g][:] = ((q_g * lambda) H_pm) * qscale  (fp32 FWHT: 2 register + 5 shuffle stages).
+// Heads g >= G are zero (padding of the 4-wide GQA group).
+__device__ __forceinline__ void query_transform_warp(const AttnArgs& a, int b, int h, int g, float* sq_g) {
+  const int lane = threadIdx.x & 31;
+  float x[4] = {0.f, 0.f, 0.f, 0.f};
+  if (g < a.G) {
+    const uint16_t* qp = a.q + b * a.q_sb + (h * a.G + g) * a.q_sh + 4 * lane;
+    const uint2 w = *reinterpret_cast<const uint2*>(qp);
+    const float4 l = *reinterpret_cast<const float4*>(a.lambda + h * 128 + 4 * lane);
+    x[0] = __uint_as_float(w.x << 16) * l.x;
+    x[1] = __uint_as_float(w.x & 0xFFFF0000u) * l.y;
+    x[2] = __uint_as_float(w.y << 16) * l.z;
+    x[3] = __uint_as_float(w.y & 0xFFFF0000u) * l.w;
+  }
+  float s0 = x[0] + x[1], s1 = x[0] - x[1], s2 = x[2] + x[3], s3 = x[2] - x[3];
+  x[0] = s0 + s2; x[2] = s0 - s2; x[1] = s1 + s3; x[3] = s1 - s3;
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float o = __shfl_xor_sync(0xffffffffu, x[i], m);
+      x[i] = upper ? (o - x[i]) : (x[i] + o);
+    }
+  }
+  *reinterpret_cast<float4*>(sq_g + 4 * lane) =
+      make_float4(x[0] * a.qscale, x[1] * a.qscale, x[2] * a.qscale, x[3] * a.qscale);
+}
+
+void launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
+void launch_attn_lut(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
+
+}  // namespace vecinfer

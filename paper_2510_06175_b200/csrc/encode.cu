@@ -1,0 +1,315 @@
+// N2: KV encode + cache store (Eq. 8 prefill / Eq. 9 decode append).
+//
+// One warp per (b, t, h) token-head; lane l owns dims [4l, 4l+4) = sub-vector l (d = 4).
+//  key:   A = rint(k * inv_lambda * 2^24) (exact f64 product -> int64)       [smooth, Eq. 3]
+//         X = A H_pm: 2 in-register butterfly stages + 5 warp-shuffle stages, int64 (exact,
+//             so the result is independent of the butterfly order)            [Hadamard, Eq. 6]
+//         x = RN32(RN32(X) * 2^-24) * RN32(1/sqrt(D))                         [reading R10]
+//         code = argmin_j pinned_dist(x, C_k[j])  (lowest index on ties)      [Eq. 2, R9]
+//  value: code = argmin_j pinned_dist(v, C_v[j])                                [Eq. 8]
+// 4/8-bit codebooks live in shared memory as fp32 (all lanes read the same centroid ->
+// broadcast, conflict-free).  16-bit codebooks (65536 entries, 512 KiB bf16) are scanned by
+// centroid-split CTAs (1024 centroids staged per CTA) whose per-lane minima are combined
+// with 64-bit atomicMin on (dist_bits << 32 | j) -- exact argmin with lowest-index ties,
+// since dist >= 0 makes the fp32 bit pattern order-preserving.
+#include "common.cuh"
+
+namespace vecinfer {
+namespace {
+
+constexpr int kEncWarps = 8;
+constexpr int kChunk16 = 1024;  // centroids per CTA for 16-bit codebooks
+
+struct EncArgs {
+  const uint16_t* k;
+  const uint16_t* v;
+  int B, T, H;
+  int64_t ks_b, ks_t, ks_h, vs_b, vs_t, vs_h;
+  const float* inv_lambda;
+  const uint16_t* ck;
+  const uint16_t* cv;
+  int64_t ck_hs, cv_hs;
+  int kbits, vbits;
+  uint8_t* kcodes;
+  uint8_t* vcodes;
+  int64_t n_cap;
+  const int32_t* write_pos;
+  uint32_t* err;
+  float inv_sqrt_d;
+  unsigned long long* ws;  // 16-bit path: [B*T*H][2][32] packed minima
+};
+
+// Smoothing + exact integer FWHT + fixed-point -> fp32, for the 4 dims of this lane.
+__device__ __forceinline__ void transform_key_lane(const EncArgs& a, int b, int t, int h, int lane,
+                                                   float (&x)[4]) {
+  const uint16_t* kp = a.k + b * a.ks_b + t * a.ks_t + h * a.ks_h + 4 * lane;
+  const uint2 kw = *reinterpret_cast<const uint2*>(kp);
+  const float kf[4] = {__uint_as_float(kw.x << 16), __uint_as_float(kw.x & 0xFFFF0000u),
+                       __uint_as_float(kw.y << 16), __uint_as_float(kw.y & 0xFFFF0000u)};
+  const float4 il = *reinterpret_cast<const float4*>(a.inv_lambda + h * 128 + 4 * lane);
+  const float ilv[4] = {il.x, il.y, il.z, il.w};
+  long long A[4];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double p = __dmul_rn(static_cast<double>(kf[i]), static_cast<double>(ilv[i]));  // exact
+    bad |= !(fabs(p) < 4294967296.0);
+    A[i] = __double2ll_rn(__dmul_rn(p, 16777216.0));  // ties-to-even, exact scaling
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
+  // in-register stages (element strides 1, 2)
+  long long s0 = A[0] + A[1], s1 = A[0] - A[1], s2 = A[2] + A[3], s3 = A[2] - A[3];
+  A[0] = s0 + s2; A[2] = s0 - s2; A[1] = s1 + s3; A[3] = s1 - s3;
+  // warp-shuffle stages (element strides 4 .. 64 <-> lane strides 1 .. 16)
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const long long o = __shfl_xor_sync(0xffffffffu, A[i], m);
+      A[i] = upper ? (o - A[i]) : (A[i] + o);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    x[i] = __fmul_rn(__fmul_rn(__ll2float_rn(A[i]), 5.9604644775390625e-08f), a.inv_sqrt_d);
+}
+
+__device__ __forceinline__ void load_value_lane(const EncArgs& a, int b, int t, int h, int lane, float (&x)[4]) {
+  const uint16_t* vp = a.v + b * a.vs_b + t * a.vs_t + h * a.vs_h + 4 * lane;
+  const uint2 w = *reinterpret_cast<const uint2*>(vp);
+  x[0] = __uint_as_float(w.x << 16);
+  x[1] = __uint_as_float(w.x & 0xFFFF0000u);
+  x[2] = __uint_as_float(w.y << 16);
+  x[3] = __uint_as_float(w.y & 0xFFFF0000u);
+}
+
+__device__ __forceinline__ void store_code(uint8_t* codes, int bits, int64_t row, int lane, uint32_t code) {
+  const int row_bytes = 32 * bits / 8;
+  uint8_t* p = codes + row * row_bytes;
+  if (bits == 8) {
+    p[lane] = static_cast<uint8_t>(code);
+  } else if (bits == 4) {
+    const uint32_t hi = __shfl_xor_sync(0xffffffffu, code, 1);
+    if ((lane & 1) == 0) p[lane >> 1] = static_cast<uint8_t>(code | (hi << 4));
+  } else {
+    reinterpret_cast<uint16_t*>(p)[lane] = static_cast<uint16_t>(code);
+  }
+}
+
+__device__ __forceinline__ bool cache_row(const EncArgs& a, int b, int t, int h, int lane, int64_t& row) {
+  const int64_t pos = static_cast<int64_t>(a.write_pos[b]) + t;
+  if (pos < 0 || pos >= a.n_cap) {
+    if (lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
+    return false;
+  }
+  row = (static_cast<int64_t>(b) * a.H + h) * a.n_cap + pos;
+  return true;
+}
+
+// ------------------------------------------------------------------ 4/8-bit: smem codebooks
+template <int KBITS, int VBITS>
+__global__ void __launch_bounds__(kEncWarps * 32) encode_small_kernel(EncArgs a) {
+  constexpr int NK = 1 << KBITS, NV = 1 << VBITS;
+  __shared__ float4 sck[NK];
+  __shared__ float4 scv[NV];
+  const int h = blockIdx.y;
+  const uint16_t* ck = a.ck + h * a.ck_hs;
+  const uint16_t* cv = a.cv + h * a.cv_hs;
+  for (int j = threadIdx.x; j < NK; j += blockDim.x) {
+    const uint2 w = *reinterpret_cast<const uint2*>(ck + 4 * j);
+    sck[j] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                         __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+  }
+  for (int j = threadIdx.x; j < NV; j += blockDim.x) {
+    const uint2 w = *reinterpret_cast<const uint2*>(cv + 4 * j);
+    scv[j] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                         __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t bt = static_cast<int64_t>(blockIdx.x) * kEncWarps + (threadIdx.x >> 5);
+  if (bt >= static_cast<int64_t>(a.B) * a.T) return;
+  const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
+  int64_t row;
+  if (!cache_row(a, b, t, h, lane, row)) return;
+  float x[4];
+  transform_key_lane(a, b, t, h, lane, x);
+  float best = __int_as_float(0x7f800000);
+  uint32_t bi = 0;
+#pragma unroll 4
+  for (int j = 0; j < NK; ++j) {
+    const float4 c = sck[j];
+    const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
+    if (dd < best) { best = dd; bi = j; }
+  }
+  store_code(a.kcodes, KBITS, row, lane, bi);
+  load_value_lane(a, b, t, h, lane, x);
+  best = __int_as_float(0x7f800000);
+  bi = 0;
+#pragma unroll 4
+  for (int j = 0; j < NV; ++j) {
+    const float4 c = scv[j];
+    const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
+    if (dd < best) { best = dd; bi = j; }
+  }
+  store_code(a.vcodes, VBITS, row, lane, bi);
+}
+
+// ------------------------------------------------------------------ 16-bit: centroid split
+// grid (ceil(B*T / kEncWarps), 65536 / kChunk16, H); stage one chunk of C_k and C_v.
+__global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) {
+  __shared__ float4 sc[kChunk16];
+  const int h = blockIdx.z;
+  const int j0 = blockIdx.y * kChunk16;
+  const int lane = threadIdx.x & 31;
+  const int64_t bt = static_cast<int64_t>(blockIdx.x) * kEncWarps + (threadIdx.x >> 5);
+  const bool live = bt < static_cast<int64_t>(a.B) * a.T;
+  const int b = live ? static_cast<int>(bt / a.T) : 0, t = live ? static_cast<int>(bt % a.T) : 0;
+  for (int which = 0; which < 2; ++which) {
+    const int bits = which ? a.vbits : a.kbits;
+    const int n_ent = 1 << bits;
+    __syncthreads();
+    if (j0 < n_ent) {
+      const uint16_t* cb = which ? (a.cv + h * a.cv_hs) : (a.ck + h * a.ck_hs);
+      for (int j = threadIdx.x; j < kChunk16; j += blockDim.x) {
+        const uint2 w = *reinterpret_cast<const uint2*>(cb + 4 * (j0 + j));
+        sc[j] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                            __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+      }
+    }
+    __syncthreads();
+    if (!live || j0 >= n_ent || bits != 16) continue;
+    float x[4];
+    if (which == 0) transform_key_lane(a, b, t, h, lane, x);
+    else load_value_lane(a, b, t, h, lane, x);
+    float best = __int_as_float(0x7f800000);
+    uint32_t bi = 0;
+#pragma unroll 4
+    for (int j = 0; j < kChunk16; ++j) {
+      const float4 c = sc[j];
+      const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
+      if (dd < best) { best = dd; bi = j; }
+    }
+    const unsigned long long packed =
+        (static_cast<unsigned long long>(__float_as_uint(best)) << 32) | static_cast<unsigned long long>(j0 + bi);
+    atomicMin(a.ws + ((bt * a.H + h) * 2 + which) * 32 + lane, packed);
+  }
+}
+
+// finalize 16-bit codes (and encode the other stream if it is 4/8-bit)
+template <int OBITS>
+__device__ __forceinline__ void small_nn_global(const uint16_t* cb, const float (&x)[4], uint32_t& bi) {
+  float best = __int_as_float(0x7f800000);
+  bi = 0;
+  for (int j = 0; j < (1 << OBITS); ++j) {
+    const uint2 w = *reinterpret_cast<const uint2*>(cb + 4 * j);
+    const float dd = pinned_dist4(x[0], x[1], x[2], x[3], __uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                                  __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+    if (dd < best) { best = dd; bi = j; }
+  }
+}
+
+__global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_finalize(EncArgs a) {
+  const int h = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int64_t bt = static_cast<int64_t>(blockIdx.x) * kEncWarps + (threadIdx.x >> 5);
+  if (bt >= static_cast<int64_t>(a.B) * a.T) return;
+  const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
+  int64_t row;
+  if (!cache_row(a, b, t, h, lane, row)) return;
+  for (int which = 0; which < 2; ++which) {
+    const int bits = which ? a.vbits : a.kbits;
+    uint8_t* codes = which ? a.vcodes : a.kcodes;
+    uint32_t code;
+    if (bits == 16) {
+      unsigned long long* slot = a.ws + ((bt * a.H + h) * 2 + which) * 32 + lane;
+      code = static_cast<uint32_t>(*slot & 0xFFFFFFFFull);
+      *slot = ~0ull;  // leave the workspace ready for the next call
+    } else {
+      float x[4];
+      if (which == 0) transform_key_lane(a, b, t, h, lane, x);
+      else load_value_lane(a, b, t, h, lane, x);
+      const uint16_t* cb = which ? (a.cv + h * a.cv_hs) : (a.ck + h * a.ck_hs);
+      if (bits == 8) small_nn_global<8>(cb, x, code);
+      else small_nn_global<4>(cb, x, code);
+    }
+    store_code(codes, bits, row, lane, code);
+  }
+}
+
+bool vq_supported(const vecinfer_vq_t& c) {
+  return c.head_dim == 128 && c.sub_dim == 4 && (c.code_bits == 4 || c.code_bits == 8 || c.code_bits == 16);
+}
+
+}  // namespace
+}  // namespace vecinfer
+
+using namespace vecinfer;
+
+extern "C" size_t vecinfer_encode_workspace_bytes(int32_t B, int32_t T, int32_t H_kv, vecinfer_vq_t kcfg,
+                                                  vecinfer_vq_t vcfg) {
+  if (B <= 0 || T <= 0 || H_kv <= 0) return 0;
+  if (kcfg.code_bits != 16 && vcfg.code_bits != 16) return 0;
+  return static_cast<size_t>(B) * T * H_kv * 2 * 32 * sizeof(unsigned long long);
+}
+
+extern "C" vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int32_t B, int32_t T,
+                                                int32_t H_kv, const int64_t k_strides[3], const int64_t v_strides[3],
+                                                const float* inv_lambda, const void* ck_bf16, const void* cv_bf16,
+                                                int64_t ck_head_stride, int64_t cv_head_stride, vecinfer_vq_t kcfg,
+                                                vecinfer_vq_t vcfg, uint8_t* k_codes, uint8_t* v_codes, int64_t n_cap,
+                                                const int32_t* write_pos, uint32_t* err_flags, void* workspace,
+                                                size_t workspace_bytes, vecinfer_stream_t stream) {
+  if (!k_bf16 || !v_bf16 || !k_strides || !v_strides || !inv_lambda || !ck_bf16 || !cv_bf16 || !k_codes ||
+      !v_codes || !write_pos)
+    return fail(VECINFER_ERR_INVALID_ARG, "encode_kv: NULL pointer");
+  if (B <= 0 || T <= 0 || H_kv <= 0 || n_cap <= 0) return fail(VECINFER_ERR_SHAPE, "encode_kv: non-positive size");
+  if (!vq_supported(kcfg) || !vq_supported(vcfg))
+    return fail(VECINFER_ERR_UNSUPPORTED, "encode_kv: supported configs are D=128, d=4, code_bits in {4,8,16}");
+  if (!aligned(k_bf16, 8) || !aligned(v_bf16, 8) || !aligned(inv_lambda, 16) || !aligned(ck_bf16, 8) ||
+      !aligned(cv_bf16, 8) || !aligned(k_codes, 2) || !aligned(v_codes, 2))
+    return fail(VECINFER_ERR_INVALID_ARG, "encode_kv: misaligned pointer (k/v/codebooks 8 B, inv_lambda 16 B)");
+  for (int i = 0; i < 3; ++i)
+    if (k_strides[i] % 4 != 0 || v_strides[i] % 4 != 0 || k_strides[i] < 0 || v_strides[i] < 0)
+      return fail(VECINFER_ERR_INVALID_ARG, "encode_kv: strides must be non-negative multiples of 4 elements");
+  if (ck_head_stride < 0 || cv_head_stride < 0 || ck_head_stride % 4 || cv_head_stride % 4)
+    return fail(VECINFER_ERR_INVALID_ARG, "encode_kv: codebook head stride must be a non-negative multiple of 4");
+  EncArgs a;
+  a.k = static_cast<const uint16_t*>(k_bf16);
+  a.v = static_cast<const uint16_t*>(v_bf16);
+  a.B = B; a.T = T; a.H = H_kv;
+  a.ks_b = k_strides[0]; a.ks_t = k_strides[1]; a.ks_h = k_strides[2];
+  a.vs_b = v_strides[0]; a.vs_t = v_strides[1]; a.vs_h = v_strides[2];
+  a.inv_lambda = inv_lambda;
+  a.ck = static_cast<const uint16_t*>(ck_bf16);
+  a.cv = static_cast<const uint16_t*>(cv_bf16);
+  a.ck_hs = ck_head_stride; a.cv_hs = cv_head_stride;
+  a.kbits = kcfg.code_bits; a.vbits = vcfg.code_bits;
+  a.kcodes = k_codes; a.vcodes = v_codes;
+  a.n_cap = n_cap; a.write_pos = write_pos; a.err = err_flags;
+  a.inv_sqrt_d = static_cast<float>(1.0 / sqrt(static_cast<double>(kcfg.head_dim)));
+  a.ws = static_cast<unsigned long long*>(workspace);
+  cudaStream_t st = as_stream(stream);
+  const int64_t nbt = static_cast<int64_t>(B) * T;
+  const int64_t gx = (nbt + kEncWarps - 1) / kEncWarps;
+  if (gx > 2147483647) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many tokens");
+  if (H_kv > 65535) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many heads");
+  if (kcfg.code_bits == 16 || vcfg.code_bits == 16) {
+    const size_t need = vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg, vcfg);
+    if (!workspace || workspace_bytes < need || !aligned(workspace, 8))
+      return fail(VECINFER_ERR_WORKSPACE, "encode_kv: 16-bit codebooks need %zu bytes of workspace", need);
+    if (cudaMemsetAsync(workspace, 0xFF, need, st) != cudaSuccess) return check_launch("encode_kv memset");
+    encode_nn16_kernel<<<dim3(static_cast<unsigned>(gx), 65536 / kChunk16, H_kv), kEncWarps * 32, 0, st>>>(a);
+    vecinfer_status_t s = check_launch("encode_nn16_kernel");
+    if (s != VECINFER_OK) return s;
+    encode_nn16_finalize<<<dim3(static_cast<unsigned>(gx), H_kv), kEncWarps * 32, 0, st>>>(a);
+    return check_launch("encode_nn16_finalize");
+  }
+  dim3 grid(static_cast<unsigned>(gx), H_kv);
+  if (kcfg.code_bits == 8 && vcfg.code_bits == 8) encode_small_kernel<8, 8><<<grid, kEncWarps * 32, 0, st>>>(a);
+  else if (kcfg.code_bits == 4 && vcfg.code_bits == 4) encode_small_kernel<4, 4><<<grid, kEncWarps * 32, 0, st>>>(a);
+  else if (kcfg.code_bits == 8 && vcfg.code_bits == 4) encode_small_kernel<8, 4><<<grid, kEncWarps * 32, 0, st>>>(a);
+  else encode_small_kernel<4, 8><<<grid, kEncWarps * 32, 0, st>>>(a);
+  return check_launch("encode_small_kernel");
+}

@@ -1,0 +1,178 @@
+"""Thin PyTorch binding of the libvecinfer C ABI (argument marshalling only).
+
+Every step of the hot path runs in the CUDA kernels behind include/vecinfer.h; this module only
+checks dtypes/devices, allocates outputs/workspaces with torch (device memory is PyTorch's job),
+and passes raw pointers plus torch's current CUDA stream.  There is no CPU fallback: CPU tensors
+are rejected and a missing library raises at import.
+Names follow the C ABI: calibrate_smooth, encode_kv, attn_decode, merge_lse.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import VQ, I64x3, check
+
+_lib.load()   # fail loudly at import if the native library is missing
+
+BF16, F32 = 0, 1
+ALGOS = {"auto": 0, "mma": 1, "dequant_mma": 1, "lut": 2}
+
+
+@dataclass(frozen=True)
+class VQConfig:
+    """Product-VQ config; b2d4 = VQConfig(128, 4, 8) (BASELINE notation bXdY = paper d{Y}b{X*Y})."""
+    head_dim: int = 128
+    sub_dim: int = 4
+    code_bits: int = 8
+
+    @property
+    def n_sub(self) -> int:
+        return self.head_dim // self.sub_dim
+
+    @property
+    def row_bytes(self) -> int:
+        return self.n_sub * self.code_bits // 8
+
+    @property
+    def n_entries(self) -> int:
+        return 1 << self.code_bits
+
+    def c(self) -> VQ:
+        return VQ(self.head_dim, self.sub_dim, self.code_bits)
+
+
+B1D4, B2D4, B4D4 = VQConfig(128, 4, 4), VQConfig(128, 4, 8), VQConfig(128, 4, 16)
+
+
+def _stream(dev: torch.device):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _need(t: torch.Tensor, name: str, dtype=None):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.stride(-1) != 1:
+        raise ValueError(f"{name}: innermost dimension must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _cb_stride(cb: torch.Tensor) -> int:
+    """[H_kv, 2^b, d] -> elements between heads; [2^b, d] (shared) -> 0."""
+    return 0 if cb.dim() == 2 else cb.stride(0)
+
+
+def calibrate_smooth(k_cal: torch.Tensor, eps: float = 1e-6):
+    """lambda = sqrt(max |K|) per (KV head, channel) (Eq. 4).  k_cal bf16 [N, H_kv, D]."""
+    N, H, D = k_cal.shape
+    lam = torch.empty(H, D, dtype=torch.float32, device=k_cal.device)
+    inv = torch.empty_like(lam)
+    lib = _lib.load()
+    nws = lib.vecinfer_calibrate_workspace_bytes(H, D)
+    ws = torch.empty(max(nws, 4), dtype=torch.uint8, device=k_cal.device)
+    check("vecinfer_calibrate_smooth", lib.vecinfer_calibrate_smooth(
+        _need(k_cal, "k_cal", torch.bfloat16), N, H, D, k_cal.stride(0), k_cal.stride(1), eps,
+        _need(lam, "lambda"), _need(inv, "inv_lambda"), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+        _stream(k_cal.device)))
+    return lam, inv
+
+
+def encode_workspace(B: int, T: int, H_kv: int, kcfg: VQConfig = B2D4, vcfg: VQConfig = B2D4, device="cuda"):
+    n = _lib.load().vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg.c(), vcfg.c())
+    return torch.empty(max(n, 8), dtype=torch.uint8, device=device)
+
+
+def encode_kv(k: torch.Tensor, v: torch.Tensor, inv_lambda: torch.Tensor, ck: torch.Tensor, cv: torch.Tensor,
+              k_codes: torch.Tensor, v_codes: torch.Tensor, write_pos: torch.Tensor, kcfg: VQConfig = B2D4,
+              vcfg: VQConfig = B2D4, err_flags: torch.Tensor | None = None,
+              workspace: torch.Tensor | None = None) -> None:
+    """Encode k, v [B, T, H_kv, D] (bf16) into the packed code caches [B, H_kv, n_cap, row] (uint8)
+    at rows write_pos[b] + t (Eq. 8 prefill / Eq. 9 append)."""
+    B, T, H, D = k.shape
+    if v.shape != k.shape:
+        raise ValueError("k and v shapes differ")
+    n_cap = k_codes.shape[2]
+    if tuple(k_codes.shape) != (B, H, n_cap, kcfg.row_bytes) or tuple(v_codes.shape) != (B, H, n_cap, vcfg.row_bytes):
+        raise ValueError("code cache shape mismatch")
+    if not (k_codes.is_contiguous() and v_codes.is_contiguous()):
+        raise ValueError("code caches must be contiguous")
+    lib = _lib.load()
+    nws = lib.vecinfer_encode_workspace_bytes(B, T, H, kcfg.c(), vcfg.c())
+    if nws and (workspace is None or workspace.numel() < nws):
+        workspace = torch.empty(nws, dtype=torch.uint8, device=k.device)
+    wsp = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else ctypes.c_void_p(0)
+    wsn = workspace.numel() if workspace is not None else 0
+    check("vecinfer_encode_kv", lib.vecinfer_encode_kv(
+        _need(k, "k", torch.bfloat16), _need(v, "v", torch.bfloat16), B, T, H,
+        I64x3(*k.stride()[:3]), I64x3(*v.stride()[:3]), _need(inv_lambda, "inv_lambda", torch.float32),
+        _need(ck, "ck", torch.bfloat16), _need(cv, "cv", torch.bfloat16), _cb_stride(ck), _cb_stride(cv),
+        kcfg.c(), vcfg.c(), _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
+        _need(write_pos, "write_pos", torch.int32),
+        ctypes.c_void_p(err_flags.data_ptr()) if err_flags is not None else ctypes.c_void_p(0),
+        wsp, wsn, _stream(k.device)))
+
+
+def attn_num_splits(B: int, H_kv: int, n_tokens_max: int, num_splits: int = 0) -> int:
+    return _lib.load().vecinfer_attn_num_splits(B, H_kv, n_tokens_max, num_splits)
+
+
+def attn_workspace(B: int, H_q: int, H_kv: int, n_tokens_max: int, num_splits: int = 0, device="cuda"):
+    """Zero-filled workspace for attn_decode (counters must start at zero; the kernel resets them)."""
+    n = _lib.load().vecinfer_attn_workspace_bytes(B, H_q, H_kv, 128, n_tokens_max, num_splits)
+    return torch.zeros(max(n, 256), dtype=torch.uint8, device=device)
+
+
+def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.Tensor, k_codes: torch.Tensor,
+                v_codes: torch.Tensor, seq_lens: torch.Tensor, tok_begin: int = 0, tok_end: int = -1,
+                softmax_scale: float | None = None, num_splits: int = 0, algo: str = "auto",
+                kcfg: VQConfig = B2D4, vcfg: VQConfig = B2D4, o_dtype: torch.dtype = torch.float32,
+                out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
+                workspace: torch.Tensor | None = None):
+    """Decode attention of q [B, H_q, D] (bf16) over the VQ cache (Eq. 10 / Alg. 1).
+    Returns (o [B, H_q, D] o_dtype, lse [B, H_q] fp32, natural log)."""
+    B, Hq, D = q.shape
+    Hkv, n_cap = k_codes.shape[1], k_codes.shape[2]
+    if softmax_scale is None:
+        softmax_scale = D ** -0.5
+    rng = n_cap if tok_end < 0 else max(0, min(tok_end - tok_begin, n_cap))
+    if out is None:
+        out = torch.empty(B, Hq, D, dtype=o_dtype, device=q.device)
+    if lse is None:
+        lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device)
+    lib = _lib.load()
+    need = lib.vecinfer_attn_workspace_bytes(B, Hq, Hkv, D, rng, num_splits)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.zeros(max(need, 256), dtype=torch.uint8, device=q.device)
+    odt = F32 if out.dtype == torch.float32 else BF16
+    if out.dtype not in (torch.float32, torch.bfloat16) or not out.is_contiguous():
+        raise TypeError("out must be a contiguous float32 or bfloat16 tensor")
+    check("vecinfer_attn_decode", lib.vecinfer_attn_decode(
+        _need(q, "q", torch.bfloat16), B, Hq, Hkv, q.stride(0), q.stride(1), _need(lam, "lambda", torch.float32),
+        _need(ck, "ck", torch.bfloat16), _need(cv, "cv", torch.bfloat16), _cb_stride(ck), _cb_stride(cv),
+        kcfg.c(), vcfg.c(), _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
+        _need(seq_lens, "seq_lens", torch.int32), tok_begin, tok_end, softmax_scale, num_splits, ALGOS[algo],
+        _need(out, "out"), odt, _need(lse, "lse", torch.float32), ctypes.c_void_p(workspace.data_ptr()),
+        workspace.numel(), _stream(q.device)))
+    return out, lse
+
+
+def merge_lse(o_parts: torch.Tensor, lse_parts: torch.Tensor, o_dtype: torch.dtype = torch.float32,
+              out: torch.Tensor | None = None, lse: torch.Tensor | None = None):
+    """Merge P partials o_parts [P, B, H_q, D] fp32 / lse_parts [P, B, H_q] by log-sum-exp."""
+    P, B, Hq, D = o_parts.shape
+    if not (o_parts.is_contiguous() and lse_parts.is_contiguous()):
+        raise ValueError("partials must be contiguous")
+    if out is None:
+        out = torch.empty(B, Hq, D, dtype=o_dtype, device=o_parts.device)
+    if lse is None:
+        lse = torch.empty(B, Hq, dtype=torch.float32, device=o_parts.device)
+    check("vecinfer_merge_lse", _lib.load().vecinfer_merge_lse(
+        _need(o_parts, "o_parts", torch.float32), _need(lse_parts, "lse_parts", torch.float32), P, B, Hq, D,
+        _need(out, "out"), F32 if out.dtype == torch.float32 else BF16, _need(lse, "lse", torch.float32),
+        _stream(o_parts.device)))
+    return out, lse

@@ -144,3 +144,13 @@ def dyadic_points(n: int, sub_dim: int, n_levels: int, step: float, seed: int, d
     hi = (n_levels / 2.0) * step + step
     k = rng.integers(int(lo * denom), int(hi * denom) + 1, size=(n, sub_dim))
     return (k / denom).astype(np.float32)
+
+
+def gen_codes_torch(shape, code_bits: int, seed: int, device="cuda"):
+    """Uniform random PACKED code bytes (uint8) generated with torch's seeded RNG on `device`, for
+    full-size (GiB-scale) attention workloads where a NumPy draw would dominate the run time.
+    Every byte pattern is a valid code at 4/8/16 bits, so uniform bytes = uniform codes."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return torch.randint(0, 256, tuple(shape), dtype=torch.uint8, device=device, generator=g)

@@ -1,0 +1,331 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bars (BASELINE north_star): codes bit-exact; attention outputs within 2e-3 max-abs relative
+error per (b, h_q) row on the fp32 output, |dL| <= 2e-3; calibration bit-exact.
+Inputs: seeded synthetic (synth/) + frozen oracle-fitted codebooks; nothing the oracle sees comes
+from the CUDA path.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import ref
+from helpers import TOL_L, TOL_O, load_codebooks, row_rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2510_06175_b200 import vecinfer as vi  # noqa: E402
+
+DEV = "cuda"
+CB = load_codebooks()
+
+
+def t_bf16(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(DEV).to(torch.bfloat16)
+
+
+def t_f32(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(DEV)
+
+
+def t_u8(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint8)).to(DEV)
+
+
+def t_i32(x):
+    return torch.tensor(np.asarray(x, dtype=np.int32), device=DEV)
+
+
+# ------------------------------------------------------------------------ calibrate (Eq. 4)
+@pytest.mark.parametrize("n_tok", [1, 7, 4096, 131072])
+def test_calibrate_bit_exact(n_tok):
+    k = synth.gen_calibration_keys(8, 128, n_samples=1, sample_len=n_tok, seed_base=50)
+    if n_tok == 7:
+        k[:, 3, 5] = 0.0                                  # zero channel -> eps floor
+    lam_ref, inv_ref = ref.calibrate_smooth(k)
+    lam, inv = vi.calibrate_smooth(t_bf16(k))
+    assert np.array_equal(lam.cpu().numpy().view(np.uint32), lam_ref.view(np.uint32))
+    assert np.array_equal(inv.cpu().numpy().view(np.uint32), inv_ref.view(np.uint32))
+
+
+def test_calibrate_strided_input():
+    k = synth.gen_calibration_keys(4, 128, n_samples=1, sample_len=300, seed_base=60)
+    big = torch.zeros(300, 6, 136, dtype=torch.bfloat16, device=DEV)
+    big[:, 1:5, 4:132] = t_bf16(k)
+    view = big[:, 1:5, 4:132]                               # non-16B-aligned strides -> scalar path
+    lam, inv = vi.calibrate_smooth(view)
+    lam_ref, _ = ref.calibrate_smooth(k)
+    assert np.array_equal(lam.cpu().numpy(), lam_ref)
+
+
+def test_calibrate_frozen_lambda_matches():
+    """The frozen lambda (oracle, scripts/fit_codebooks.py) is reproduced bit-exactly on the GPU."""
+    kcal = synth.gen_calibration_keys(8, 128)
+    lam, inv = vi.calibrate_smooth(t_bf16(kcal))
+    assert np.array_equal(lam.cpu().numpy(), CB["lambda"])
+    assert np.array_equal(inv.cpu().numpy(), CB["inv_lambda"])
+
+
+# ----------------------------------------------------------------- encode (Eq. 2, 8, 9)
+def _encode_gpu(k, v, inv, ck, cv, n_cap, write_pos, kcfg, vcfg, err=None):
+    B, T, H, D = k.shape
+    kc = torch.zeros(B, H, n_cap, kcfg.row_bytes, dtype=torch.uint8, device=DEV)
+    vc = torch.zeros(B, H, n_cap, vcfg.row_bytes, dtype=torch.uint8, device=DEV)
+    vi.encode_kv(t_bf16(k), t_bf16(v), t_f32(inv), t_bf16(ck), t_bf16(cv), kc, vc, t_i32(write_pos), kcfg, vcfg,
+                 err_flags=err)
+    return kc.cpu().numpy(), vc.cpu().numpy()
+
+
+def _encode_ref(k, v, inv, ck, cv, n_cap, write_pos, kcfg, vcfg):
+    B, T, H, D = k.shape
+    kc = np.zeros((B, H, n_cap, kcfg.row_bytes), np.uint8)
+    vc = np.zeros((B, H, n_cap, vcfg.row_bytes), np.uint8)
+    for h in range(H):
+        ckh = ck[h] if ck.ndim == 3 else ck
+        cvh = cv[h] if cv.ndim == 3 else cv
+        kk, vv = ref.encode_kv(k[:, :, h], v[:, :, h], inv[h], ckh, cvh)
+        for b in range(B):
+            p = write_pos[b]
+            kc[b, h, p:p + T] = ref.pack_codes(kk[b], kcfg.code_bits)
+            vc[b, h, p:p + T] = ref.pack_codes(vv[b], vcfg.code_bits)
+    return kc, vc
+
+
+@pytest.mark.parametrize("name,cfg", [("b2d4", vi.B2D4), ("b1d4", vi.B1D4)])
+@pytest.mark.parametrize("B,T", [(1, 1), (2, 37), (1, 300)])
+def test_encode_bit_exact(name, cfg, B, T):
+    k = synth.gen_keys(T, 8, 128, seed=100 + T, batch=B)
+    v = synth.gen_values(T, 8, 128, seed=200 + T, batch=B)
+    n_cap = T + 10
+    wp = [3 + b for b in range(B)]
+    ck, cv = CB[f"ck_{name}"], CB[f"cv_{name}"]
+    got = _encode_gpu(k, v, CB["inv_lambda"], ck, cv, n_cap, wp, cfg, cfg)
+    want = _encode_ref(k, v, CB["inv_lambda"], ck, cv, n_cap, wp, cfg, cfg)
+    assert np.array_equal(got[0], want[0]), "key codes differ"
+    assert np.array_equal(got[1], want[1]), "value codes differ"
+
+
+def test_encode_b4d4_bit_exact_shared_codebook():
+    T = 24
+    k = synth.gen_keys(T, 2, 128, seed=300)
+    v = synth.gen_values(T, 2, 128, seed=301)
+    ck, cv = CB["ck_b4d4"], CB["cv_b4d4"]                  # one codebook for all heads (stride 0)
+    got = _encode_gpu(k, v, CB["inv_lambda"][:2], ck, cv, T, [0], vi.B4D4, vi.B4D4)
+    want = _encode_ref(k, v, CB["inv_lambda"][:2], ck, cv, T, [0], vi.B4D4, vi.B4D4)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_encode_mixed_bits_bit_exact():
+    T = 20
+    k = synth.gen_keys(T, 2, 128, seed=310)
+    v = synth.gen_values(T, 2, 128, seed=311)
+    got = _encode_gpu(k, v, CB["inv_lambda"][:2], CB["ck_b2d4"][:2], CB["cv_b1d4"][:2], T, [0], vi.B2D4, vi.B1D4)
+    want = _encode_ref(k, v, CB["inv_lambda"][:2], CB["ck_b2d4"][:2], CB["cv_b1d4"][:2], T, [0], vi.B2D4, vi.B1D4)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("n_levels,cfg", [(2, vi.B1D4), (4, vi.B2D4), (16, vi.B4D4)])
+def test_encode_product_grid_ties(n_levels, cfg):
+    """Closed-form NN with genuine fp32 ties through the untransformed V path: lowest index wins
+    (16 / 256 / 65536 entries)."""
+    cb = synth.product_grid_codebook(n_levels, 4, step=0.5)
+    T = 8 if n_levels == 16 else 64
+    pts = synth.dyadic_points(T * 32, 4, n_levels, 0.5, seed=n_levels).reshape(1, T, 1, 128)
+    lv = synth.grid_levels(n_levels, 0.5)
+    digit = np.argmin(np.abs(pts.reshape(-1, 4)[:, :, None].astype(np.float64) - lv), axis=2)
+    want = (digit * (n_levels ** np.arange(4))).sum(1).reshape(T, 32)
+    k = np.zeros_like(pts)
+    _, vc = _encode_gpu(k, pts, np.ones((1, 128), np.float32), cb, cb, T, [0], cfg, cfg)
+    assert np.array_equal(ref.unpack_codes(vc[0, 0], cfg.code_bits), want)
+
+
+def test_encode_flags_range_and_write_pos():
+    k = np.zeros((1, 2, 1, 128), np.float32)
+    k[0, 0, 0, 0] = 2.0 ** 40                                 # |k * inv_lambda| >= 2^32
+    v = np.zeros_like(k)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    _encode_gpu(k, v, np.ones((1, 128), np.float32), CB["ck_b2d4"][:1], CB["cv_b2d4"][:1], 2, [0], vi.B2D4, vi.B2D4,
+                err=err)
+    assert int(err.item()) & 1
+    err.zero_()
+    _encode_gpu(np.zeros_like(k), v, np.ones((1, 128), np.float32), CB["ck_b2d4"][:1], CB["cv_b2d4"][:1], 2, [1],
+                vi.B2D4, vi.B2D4, err=err)                    # row 1 + t=1 == n_cap -> flagged
+    assert int(err.item()) & 2
+
+
+# ------------------------------------------------------------------- attention (Eq. 10)
+def _attn_case(B, Hkv, G, n_cap, seq_lens, seed, codes_from="random"):
+    rng = np.random.default_rng(seed)
+    heads = rng.choice(8, size=Hkv, replace=False) if Hkv < 8 else np.arange(8)
+    lam = CB["lambda"][heads]
+    ck, cv = CB["ck_b2d4"][heads], CB["cv_b2d4"][heads]
+    if codes_from == "random":
+        kc = synth.gen_codes(n_cap, Hkv, 32, 8, seed=seed, batch=B)
+        vc = synth.gen_codes(n_cap, Hkv, 32, 8, seed=seed + 1, batch=B)
+    else:   # codes of realistic synthetic keys, encoded by the ORACLE
+        k = synth.gen_keys(n_cap, 8, 128, seed=seed, batch=B)[:, :, heads]
+        v = synth.gen_values(n_cap, 8, 128, seed=seed + 1, batch=B)[:, :, heads]
+        kc = np.zeros((B, Hkv, n_cap, 32), np.int64)
+        vc = np.zeros_like(kc)
+        for i in range(Hkv):
+            kk, vv = ref.encode_kv(k[:, :, i], v[:, :, i], CB["inv_lambda"][heads[i]], ck[i], cv[i])
+            kc[:, i], vc[:, i] = kk, vv
+    q = synth.gen_queries(B, 8 * G, 8, 128, seed=seed + 2).reshape(B, 8, G, 128)[:, heads].reshape(B, Hkv * G, 128)
+    return dict(q=q, lam=lam, ck=ck, cv=cv, kc=kc, vc=vc, seq_lens=np.asarray(seq_lens))
+
+
+def _run_gpu(c, **kw):
+    o, L = vi.attn_decode(t_bf16(c["q"]), t_f32(c["lam"]), t_bf16(c["ck"]), t_bf16(c["cv"]),
+                          t_u8(c["kc"]), t_u8(c["vc"]), t_i32(c["seq_lens"]), **kw)
+    return o.float().cpu().numpy(), L.cpu().numpy()
+
+
+def _run_ref(c, tok_begin=0, tok_end=None):
+    return ref.attention_decode_batch(c["q"], c["lam"], c["ck"], c["cv"], c["kc"], c["vc"], c["seq_lens"],
+                                      tok_begin, tok_end)
+
+
+def _assert_close(o, L, o_ref, L_ref):
+    err = row_rel_err(o, o_ref)
+    assert err.max() <= TOL_O, f"max row rel err {err.max():.3e}"
+    fin = np.isfinite(L_ref)
+    assert np.array_equal(np.isfinite(L), fin)
+    assert np.all(np.abs(L[fin] - L_ref[fin]) <= TOL_L), f"max |dL| {np.abs(L[fin] - L_ref[fin]).max():.3e}"
+    assert np.all(o[~fin] == 0)
+
+
+@pytest.mark.parametrize("algo", ["mma", "lut"])
+def test_attn_cfg1_oracle_encoded(algo):
+    """BASELINE configs[0]: 1 batch, 1 KV head (G = 4), seq 1024, b2d4, codes from the oracle encoder."""
+    c = _attn_case(1, 1, 4, 1024, [1024], seed=0, codes_from="oracle")
+    o, L = _run_gpu(c, algo=algo)
+    _assert_close(o, L, *_run_ref(c))
+
+
+@pytest.mark.parametrize("algo", ["mma", "lut"])
+@pytest.mark.parametrize("n", [1, 2, 15, 16, 17, 31, 33, 100, 513, 2047, 4097])
+def test_attn_ragged_lengths(algo, n):
+    c = _attn_case(2, 2, 4, 4200, [n, max(1, n // 3)], seed=n)
+    o, L = _run_gpu(c, algo=algo)
+    _assert_close(o, L, *_run_ref(c))
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 7, 40])
+def test_attn_fixed_splits_and_determinism(splits):
+    c = _attn_case(1, 4, 4, 3000, [2999], seed=splits)
+    o1, L1 = _run_gpu(c, num_splits=splits)
+    o2, L2 = _run_gpu(c, num_splits=splits)
+    assert np.array_equal(o1, o2) and np.array_equal(L1, L2)      # bitwise deterministic
+    _assert_close(o1, L1, *_run_ref(c))
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_attn_gqa_groups(G):
+    c = _attn_case(2, 3, G, 700, [700, 450], seed=10 + G)
+    o, L = _run_gpu(c)
+    _assert_close(o, L, *_run_ref(c))
+
+
+@pytest.mark.parametrize("rng_", [(0, 500), (500, -1), (100, 101), (1000, 3000), (250, 250)])
+def test_attn_token_ranges(rng_):
+    """Sharding hook: tokens [tok_begin, min(tok_end, seq_len)); empty shard -> o = 0, L = -inf."""
+    a, e = rng_
+    c = _attn_case(2, 2, 4, 1200, [1200, 700], seed=21)
+    o, L = _run_gpu(c, tok_begin=a, tok_end=e)
+    _assert_close(o, L, *_run_ref(c, a, None if e < 0 else e))
+
+
+def test_attn_empty_sequence():
+    c = _attn_case(1, 2, 4, 64, [0], seed=22)
+    o, L = _run_gpu(c)
+    assert np.all(o == 0) and np.all(np.isneginf(L))
+
+
+def test_attn_bf16_output_is_rounded_fp32():
+    c = _attn_case(1, 2, 4, 900, [900], seed=23)
+    of, Lf = _run_gpu(c, num_splits=3)
+    ob, Lb = _run_gpu(c, num_splits=3, o_dtype=torch.bfloat16)
+    assert np.array_equal(synth.round_to_bf16(of.astype(np.float32)), ob.astype(np.float32))
+    assert np.array_equal(Lf, Lb)
+
+
+def test_attn_identity_codebook_equals_full_precision():
+    """If every transformed key sub-vector is a centroid, VQ attention = Eq. 1 attention on the
+    ORIGINAL keys (Eq. 7 invariance); GPU vs the fp64 full-precision Eq. 1 oracle."""
+    c = _attn_case(1, 1, 4, 512, [512], seed=24)
+    H = ref.hadamard(128)
+    K = ref.vq_decode(c["kc"][0, 0], c["ck"][0]) @ H.T * c["lam"][0][None].astype(np.float64)
+    V = ref.vq_decode(c["vc"][0, 0], c["cv"][0])
+    o_ref, L_ref = ref.attention_full(c["q"][0], K, V)
+    o, L = _run_gpu(c)
+    _assert_close(o[0], L[0], o_ref, L_ref)
+
+
+def test_attn_single_token_and_identical_keys():
+    c = _attn_case(1, 1, 4, 40, [1], seed=25)
+    o, L = _run_gpu(c)
+    assert np.max(row_rel_err(o[0], np.repeat(ref.vq_decode(c["vc"][0, 0, :1], c["cv"][0]), 4, 0))) <= TOL_O
+    c["kc"][:] = c["kc"][:, :, :1]                                  # all keys identical
+    c["seq_lens"] = np.array([40])
+    o, L = _run_gpu(c)
+    want = ref.vq_decode(c["vc"][0, 0, :40], c["cv"][0]).mean(0)
+    assert np.max(row_rel_err(o[0], np.tile(want, (4, 1)))) <= TOL_O
+
+
+# ----------------------------------------------------------------------- merge (LSE)
+def test_merge_lse_vs_oracle():
+    rng = np.random.default_rng(30)
+    P, B, Hq = 5, 2, 32
+    o = rng.standard_normal((P, B, Hq, 128)).astype(np.float32)
+    L = (rng.standard_normal((P, B, Hq)) * 3).astype(np.float32)
+    L[2, 0, :4] = -np.inf
+    L[:, 1, 5] = -np.inf
+    got_o, got_L = vi.merge_lse(t_f32(o), t_f32(L))
+    want_o, want_L = ref.merge_lse(o, L)
+    _assert_close(got_o.cpu().numpy(), got_L.cpu().numpy(), want_o, want_L)
+
+
+def test_sharded_attention_plus_merge_equals_unsharded():
+    """Single-GPU emulation of the sequence-sharded multi-GPU path: attn_decode on P contiguous
+    token shards + merge_lse == oracle over the whole sequence."""
+    c = _attn_case(1, 8, 4, 6000, [5990], seed=31)
+    parts = [_run_gpu(c, tok_begin=a, tok_end=e) for a, e in ((0, 1500), (1500, 3000), (3000, 4500), (4500, 6000))]
+    o_p = np.stack([p[0] for p in parts]).astype(np.float32)
+    L_p = np.stack([p[1] for p in parts]).astype(np.float32)
+    mo, mL = vi.merge_lse(t_f32(o_p), t_f32(L_p))
+    _assert_close(mo.cpu().numpy(), mL.cpu().numpy(), *_run_ref(c))
+
+
+# ------------------------------------------------------ BASELINE configs at full size
+def _sampled_units_check(B, N, n_units, seed, **kw):
+    """Full-size launch (auto splits, as bench.py) checked on sampled (b, h_kv) units."""
+    rng = np.random.default_rng(seed)
+    q = synth.gen_queries(B, 32, 8, 128, seed=seed)
+    kc = synth.gen_codes_torch((B, 8, N, 32), 8, seed=seed, device=DEV)
+    vc = synth.gen_codes_torch((B, 8, N, 32), 8, seed=seed + 1, device=DEV)
+    o, L = vi.attn_decode(t_bf16(q), t_f32(CB["lambda"]), t_bf16(CB["ck_b2d4"]), t_bf16(CB["cv_b2d4"]), kc, vc,
+                          t_i32([N] * B), **kw)
+    o, L = o.cpu().numpy(), L.cpu().numpy()
+    for _ in range(n_units):
+        b, h = int(rng.integers(B)), int(rng.integers(8))
+        kk = kc[b, h].cpu().numpy().astype(np.int64)   # synthetic inputs (synth/), not CUDA results
+        vv = vc[b, h].cpu().numpy().astype(np.int64)
+        o_ref, L_ref = ref.attention_vq(q[b, 4 * h:4 * h + 4], CB["lambda"][h], CB["ck_b2d4"][h], CB["cv_b2d4"][h],
+                                        kk, vv)
+        _assert_close(o[b, 4 * h:4 * h + 4], L[b, 4 * h:4 * h + 4], o_ref, L_ref)
+
+
+def test_cfg2_full_size_all_units():
+    _sampled_units_check(1, 32768, 8, seed=40)
+
+
+def test_cfg3_full_size_sampled_units():
+    _sampled_units_check(64, 8192, 6, seed=41)
+
+
+def test_cfg4_full_size_sampled_units():
+    _sampled_units_check(1, 196608, 2, seed=42)
