@@ -47,13 +47,14 @@ __device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int
 // CTA epilogue shared by all kernels: combine per-warp (m, l, acc) partials held in shared
 // memory, then either write the final output (S == 1) or a split partial plus a fused
 // last-CTA log-sum-exp merge over the S splits in fixed order s = 0..S-1.
-//   wm[NW][4], wl[NW][4] (log2 domain), wacc[NW][4][128] (unnormalised)
+//   wm[NW][4], wl[NW][4] (log2 domain), wacc[NW][4][128] (unnormalised);
+//   scratch: >= 4*S + 8 floats of shared memory not aliased with wm/wl/wacc.
 template <int NTHREADS>
 __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s, int NWARPS,
-                                           const float* wm, const float* wl, const float* wacc) {
+                                           const float* wm, const float* wl, const float* wacc,
+                                           float* scratch) {
   const int tid = threadIdx.x;
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
-  __shared__ float sL[4];
   __shared__ bool s_last;
   for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
     const int g = idx >> 7, dim = idx & 127;
@@ -90,23 +91,29 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // stage the S x 4 split LSEs (parallel loads), then per-head maxima
+  float* sLs = scratch;           // [S][4]
+  float* sM = scratch + 4 * a.S;  // [4]
+  for (int i = tid; i < 4 * a.S; i += NTHREADS) sLs[i] = __ldcg(&a.part_l[unit * a.S * 4 + i]);
+  __syncthreads();
   if (tid < 4) {
     float M = -INFINITY;
-    for (int ss = 0; ss < a.S; ++ss) M = fmaxf(M, __ldcg(&a.part_l[(unit * a.S + ss) * 4 + tid]));
-    sL[tid] = M;
+    for (int ss = 0; ss < a.S; ++ss) M = fmaxf(M, sLs[ss * 4 + tid]);
+    sM[tid] = M;
   }
   __syncthreads();
   for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
     const int g = idx >> 7, dim = idx & 127;
     if (g >= a.G) continue;
-    const float M = sL[g];
+    const float M = sM[g];
     float osum = 0.f, wsum = 0.f;
     if (M != -INFINITY) {
+      const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
+#pragma unroll 8
       for (int ss = 0; ss < a.S; ++ss) {
-        const int64_t pi = (unit * a.S + ss) * 4 + g;
-        const float f = ex2_approx(__ldcg(&a.part_l[pi]) - M);
+        const float f = ex2_approx(sLs[ss * 4 + g] - M);
         wsum += f;
-        osum += f * __ldcg(&a.part_o[pi * 128 + dim]);
+        osum += f * __ldcg(po + static_cast<int64_t>(ss) * 4 * 128);
       }
     }
     const bool empty = !(wsum > 0.f);

@@ -169,11 +169,12 @@ __global__ void __launch_bounds__(kT, 1) attn_lut8_kernel(const AttnArgs a) {
   float* wm = reinterpret_cast<float*>(smem_raw);   // reuse the LUT region
   float* wl = wm + 4;
   float* wacc = wl + 4;
+  float* scratch = wacc + 4 * 128;
   if (tid < 4) { wm[tid] = m_run[tid]; wl[tid] = l_run[tid]; }
 #pragma unroll
   for (int g = 0; g < 4; ++g) wacc[g * 128 + tid] = o[g];
   __syncthreads();
-  cta_finish<kT>(a, b, h, s, 1, wm, wl, wacc);
+  cta_finish<kT>(a, b, h, s, 1, wm, wl, wacc, scratch);
 }
 
 }  // namespace

@@ -2,7 +2,7 @@
 //
 // Implements Eq. 10 with Algorithm 1's online softmax:
 //   s = q~ VQ^-1(K~_q)^T / sqrt(D),  o = softmax(s) VQ^-1(V_q),  L = logsumexp(s).
-// CTA = (split, KV head, batch); each of its NW warps streams 32-token tiles of packed codes
+// CTA = (split, KV head, batch); each of its 16 warps streams 32-token tiles of packed codes
 // straight from HBM into registers (LDG, one tile of prefetch) -- no dequantised cache, no
 // shared-memory staging of codes.  Per warp and 16-token sub-tile:
 //  score:  the key codes index a 16x-replicated fp16 copy of C_k in shared memory (lane l
@@ -15,8 +15,12 @@
 //          accumulator layout to the B-operand layout with movmatrix.trans.
 //  P.V:    V^T (16 dims x 16 tokens) built from replicated C_v gathers (PRMT pairs tokens)
 //          times P (16 tokens x 8 = 4 heads x {hi, lo}); fp32 accumulators in registers.
+// Shared-memory codebook rows are 256 B: [C_k copies 0..15 | C_v copies 0..15] for centroid c,
+// in a 64 KiB-aligned region, so a gather address is ONE byte-permute: PRMT places code byte k
+// of a code word into address bits 8..15 next to the per-lane base (bits 0..7, 16..31).
 // Epilogue: warps combine through shared memory; splits merge by log-sum-exp in the last CTA
-// of each (b, h_kv) (fixed order => deterministic).  See DESIGN.md "Kernel N4".
+// of each (b, h_kv), which stages all partials in shared memory first (fixed order s = 0..S-1
+// => deterministic).  See DESIGN.md "Kernel N4".
 #include "attn_common.cuh"
 
 namespace vecinfer {
@@ -25,30 +29,35 @@ namespace {
 constexpr int kNW = 16;            // warps per CTA (1 CTA per SM)
 constexpr int kThreads = kNW * 32;
 constexpr float kTau = 8.0f;       // lazy-rescale threshold (log2 units): p <= 2^8
-constexpr int kRep = 16;           // codebook replicas (one per half-warp lane)
 constexpr int kRowBytes = 32;      // 8-bit codes, D/d = 32 sub-vectors
+constexpr int kTab = 65536;        // [256 centroids][256 B] codebook table, 64 KiB-aligned
+// misc region (below the table): q~ [4][128] f32, warp partials, staged split partials
+constexpr int kMiscQ = 0;
+constexpr int kMiscW = 2048;                         // wm[16][4], wl[16][4], wacc[16][4][128]
+constexpr int kMiscBytes = kMiscW + (kNW * 8 + kNW * 4 * 128) * 4;   // 35328
+constexpr int kSmemBytes = kTab + 65536 + 1024;      // table + worst-case alignment pad + slack
 
-struct Smem8 {
-  uint2 ck[256 * kRep];  // fp16x4 centroids, entry j copy c at [j*16 + c]
-  uint2 cv[256 * kRep];
-  float q[4][128];
-};
-
-__device__ __forceinline__ void fill_codebook(uint2* dst, const uint16_t* src, int tid) {
-  // thread j converts centroid j (bf16 -> fp16, exact for |c| in the fp16 normal range) and
-  // writes its 16 replicas as 8 x 16-byte stores, rotated so a quarter-warp hits 8 banks groups
-  if (tid < 256) {
-    const uint2 w = *reinterpret_cast<const uint2*>(src + 4 * tid);
-    uint2 e;
-    e.x = pack_half2(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u));
-    e.y = pack_half2(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
-    uint4 v = make_uint4(e.x, e.y, e.x, e.y);
+__device__ __forceinline__ void fill_tables(unsigned char* tab, const uint16_t* ck, const uint16_t* cv, int tid) {
+  // thread t: centroid j = t/2 of C_k (t even) or C_v (t odd); 16 replicas = 8 x 16-byte stores,
+  // rotated so that the 8 threads of a quarter-warp hit 8 different bank groups
+  const int j = tid >> 1, which = tid & 1;
+  const uint16_t* src = (which ? cv : ck) + 4 * j;
+  const uint2 w = *reinterpret_cast<const uint2*>(src);
+  const uint32_t e0 = pack_half2(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u));
+  const uint32_t e1 = pack_half2(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+  const uint4 v = make_uint4(e0, e1, e0, e1);
+  unsigned char* row = tab + j * 256 + which * 128;
 #pragma unroll
-    for (int u0 = 0; u0 < 8; ++u0) {
-      const int u = (u0 + tid) & 7;
-      *reinterpret_cast<uint4*>(&dst[tid * kRep + 2 * u]) = v;
-    }
+  for (int u0 = 0; u0 < 8; ++u0) {
+    const int u = (u0 + tid) & 7;
+    *reinterpret_cast<uint4*>(row + 16 * u) = v;
   }
+}
+
+// shared address of centroid (byte k of w) for this lane: one PRMT
+template <int K>
+__device__ __forceinline__ uint32_t gaddr(uint32_t w, uint32_t base) {
+  return prmt(w, base, 0x7604u | (K << 4));
 }
 
 struct TileCodes {
@@ -56,51 +65,68 @@ struct TileCodes {
   uint32_t v[2][4];  // [sub-tile][token 2j, 2j+1, 2j+8, 2j+9]: 4 value codes (sub-vectors 4r..4r+3)
 };
 
-__device__ __forceinline__ void load_tile(TileCodes& tc, const uint8_t* kb, const uint8_t* vb, int64_t t0,
-                                          int64_t r1, int r, int j) {
+// kp/vp point at this lane's bytes of token (tile start + r) / (tile start + 2j) respectively
+__device__ __forceinline__ void load_tile_full(TileCodes& tc, const uint8_t* kp, const uint8_t* vp) {
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    const int64_t base = t0 + 16 * q;
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int64_t tok = base + r + 8 * hh;
-      tc.k[q][hh] = tok < r1 ? ldg_nc_u64(kb + tok * kRowBytes + 8 * j) : make_uint2(0u, 0u);
-    }
-    const int toks[4] = {2 * j, 2 * j + 1, 2 * j + 8, 2 * j + 9};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t tok = base + toks[i];
-      tc.v[q][i] = tok < r1 ? ldg_nc_u32(vb + tok * kRowBytes + 4 * r) : 0u;
-    }
+    tc.k[q][0] = ldg_nc_u64(kp + (16 * q) * kRowBytes);
+    tc.k[q][1] = ldg_nc_u64(kp + (16 * q + 8) * kRowBytes);
+    tc.v[q][0] = ldg_nc_u32(vp + (16 * q) * kRowBytes);
+    tc.v[q][1] = ldg_nc_u32(vp + (16 * q + 1) * kRowBytes);
+    tc.v[q][2] = ldg_nc_u32(vp + (16 * q + 8) * kRowBytes);
+    tc.v[q][3] = ldg_nc_u32(vp + (16 * q + 9) * kRowBytes);
   }
 }
 
-// byte t of a code word pair -> shared-memory byte offset of that centroid's replica row
-__device__ __forceinline__ uint32_t code_off(uint32_t w, int byte) {
-  return byte == 0 ? ((w << 7) & 0x7f80u) : ((w >> (8 * byte - 7)) & 0x7f80u);
+// ragged last tile: rem = tokens left in the split (1..31), rows beyond it read as code 0
+__device__ __forceinline__ void load_tile_tail(TileCodes& tc, const uint8_t* kp, const uint8_t* vp, int rem, int r,
+                                               int j) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    tc.k[q][0] = (16 * q + r < rem) ? ldg_nc_u64(kp + (16 * q) * kRowBytes) : make_uint2(0u, 0u);
+    tc.k[q][1] = (16 * q + r + 8 < rem) ? ldg_nc_u64(kp + (16 * q + 8) * kRowBytes) : make_uint2(0u, 0u);
+    const int t0 = 16 * q + 2 * j;
+    tc.v[q][0] = (t0 < rem) ? ldg_nc_u32(vp + (16 * q) * kRowBytes) : 0u;
+    tc.v[q][1] = (t0 + 1 < rem) ? ldg_nc_u32(vp + (16 * q + 1) * kRowBytes) : 0u;
+    tc.v[q][2] = (t0 + 8 < rem) ? ldg_nc_u32(vp + (16 * q + 8) * kRowBytes) : 0u;
+    tc.v[q][3] = (t0 + 9 < rem) ? ldg_nc_u32(vp + (16 * q + 9) * kRowBytes) : 0u;
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem8& sm = *reinterpret_cast<Smem8*>(smem_raw);
   const int s = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
 
+  // shared layout: misc at the bottom, the codebook table at the next 64 KiB boundary
+  const uint32_t raw_s = smem_u32(smem_raw);
+  uint32_t tab_off = ((raw_s + 65535u) & ~65535u) - raw_s;
+  if (tab_off < static_cast<uint32_t>(kMiscBytes)) tab_off += 65536u;
+  unsigned char* tab = smem_raw + tab_off;
+  float* sq = reinterpret_cast<float*>(smem_raw + kMiscQ);
+  const uint32_t tab_s = raw_s + tab_off;
+
   int64_t r0, r1;
   split_range(a, b, s, r0, r1);
-  const int64_t ntile = (r1 - r0 + 31) / 32;
+  const int ntok = static_cast<int>(r1 - r0);
+  const int ntile = (ntok + 31) >> 5;
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
-  const uint8_t* kb = a.kcodes + unit * a.n_cap * kRowBytes;
-  const uint8_t* vb = a.vcodes + unit * a.n_cap * kRowBytes;
+  // lane-resolved code pointers of this warp's first tile
+  const uint8_t* kp = a.kcodes + (unit * a.n_cap + r0 + 32 * warp + r) * kRowBytes + 8 * j;
+  const uint8_t* vp = a.vcodes + (unit * a.n_cap + r0 + 32 * warp + 2 * j) * kRowBytes + 4 * r;
+  constexpr int kStep = 32 * kNW * kRowBytes;  // bytes between a warp's consecutive tiles
 
   // issue the first tile's loads before the prologue so HBM latency overlaps it
   TileCodes nxt;
-  if (warp < ntile) load_tile(nxt, kb, vb, r0 + 32 * warp, r1, r, j);
+  if (warp < ntile) {
+    const int rem = ntok - 32 * warp;
+    if (rem >= 32) load_tile_full(nxt, kp, vp);
+    else load_tile_tail(nxt, kp, vp, rem, r, j);
+  }
 
-  fill_codebook(sm.ck, a.ck + h * a.ck_hs, tid);
-  if (tid >= 256) fill_codebook(sm.cv, a.cv + h * a.cv_hs, tid - 256);
-  if (warp < 4) query_transform_warp(a, b, h, warp, sm.q[warp]);
+  fill_tables(tab, a.ck + h * a.ck_hs, a.cv + h * a.cv_hs, tid);
+  if (warp < 4) query_transform_warp(a, b, h, warp, sq + 128 * warp);
   __syncthreads();
 
   // B fragments of the score MMA: column n = lane/4 <-> (head n/2, part n%2); rows k
@@ -110,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
     const int gq = r >> 1, part = r & 1;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const float4 v = *reinterpret_cast<const float4*>(&sm.q[gq][4 * (8 * j + t)]);
+      const float4 v = *reinterpret_cast<const float4*>(sq + 128 * gq + 4 * (8 * j + t));
       const float in[4] = {v.x, v.y, v.z, v.w};
       float o[4];
 #pragma unroll
@@ -123,20 +149,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
     }
   }
 
-  const uint32_t ck_base = smem_u32(sm.ck) + (lane & 15) * 8;
-  const uint32_t cv_base = smem_u32(sm.cv) + (lane & 15) * 8;
+  const uint32_t kbase = tab_s + (lane & 15) * 8;
+  const uint32_t vbase = kbase + 128;
 
   float acc[8][4];
 #pragma unroll
   for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
   float m_run = -INFINITY, l_run = 0.f;
 
-  for (int64_t it = warp; it < ntile; it += kNW) {
+  for (int it = warp; it < ntile; it += kNW) {
     const TileCodes cur = nxt;
-    const int64_t t0 = r0 + 32 * it;
-    if (it + kNW < ntile) load_tile(nxt, kb, vb, t0 + 32 * kNW, r1, r, j);
+    const int rem_cur = ntok - 32 * it;
+    if (it + kNW < ntile) {
+      kp += kStep;
+      vp += kStep;
+      const int rem = rem_cur - 32 * kNW;
+      if (rem >= 32) load_tile_full(nxt, kp, vp);
+      else load_tile_tail(nxt, kp, vp, rem, r, j);
+    }
 
-    // ---- scores (log2 units) for tokens t0 + 16q + {r, r+8}, head j
+    // ---- scores (log2 units) for tile tokens 16q + {r, r+8}, head j
     float sc[2][2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -145,13 +177,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
       for (int t = 0; t < 8; ++t) {
         const uint32_t wa = t < 4 ? cur.k[q][0].x : cur.k[q][0].y;
         const uint32_t wb = t < 4 ? cur.k[q][1].x : cur.k[q][1].y;
-        const uint2 ea = lds_u64(ck_base + code_off(wa, t & 3));
-        const uint2 eb = lds_u64(ck_base + code_off(wb, t & 3));
+        uint2 ea, eb;
+        switch (t & 3) {
+          case 0: ea = lds_u64(gaddr<0>(wa, kbase)); eb = lds_u64(gaddr<0>(wb, kbase)); break;
+          case 1: ea = lds_u64(gaddr<1>(wa, kbase)); eb = lds_u64(gaddr<1>(wb, kbase)); break;
+          case 2: ea = lds_u64(gaddr<2>(wa, kbase)); eb = lds_u64(gaddr<2>(wb, kbase)); break;
+          default: ea = lds_u64(gaddr<3>(wa, kbase)); eb = lds_u64(gaddr<3>(wb, kbase)); break;
+        }
         mma_16816(d, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
       }
-      const int64_t tok = t0 + 16 * q + r;
-      sc[q][0] = tok < r1 ? d[0] + d[1] : -INFINITY;
-      sc[q][1] = tok + 8 < r1 ? d[2] + d[3] : -INFINITY;
+      sc[q][0] = d[0] + d[1];
+      sc[q][1] = d[2] + d[3];
+    }
+    if (rem_cur < 32) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (16 * q + r >= rem_cur) sc[q][0] = -INFINITY;
+        if (16 * q + r + 8 >= rem_cur) sc[q][1] = -INFINITY;
+      }
     }
 
     // ---- online softmax (Alg. 1 l.12-13, 18), lazy rescale
@@ -177,21 +220,33 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
       const float p0 = ex2_approx(sc[q][0] - m_use);
       const float p1 = ex2_approx(sc[q][1] - m_use);
       l_run += p0 + p1;
-      const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
-      const __half l0 = __float2half_rn(p0 - __half2float(h0));
-      const __half l1 = __float2half_rn(p1 - __half2float(h1));
-      const uint32_t x0 = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(l0)) << 16);
-      const uint32_t x1 = static_cast<uint32_t>(__half_as_ushort(h1)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
-      const uint32_t bp0 = movmatrix_trans(x0);  // P^T rows (slots) x tokens 0..7
-      const uint32_t bp1 = movmatrix_trans(x1);  // tokens 8..15
+      // hi/lo fp16 split: hi = RN16(p), lo = RN16(p - hi)
+      const __half2 hh = __floats2half2_rn(p0, p1);
+      const float2 hf = __half22float2(hh);
+      const __half2 ll = __floats2half2_rn(p0 - hf.x, p1 - hf.y);
+      const uint32_t hb = *reinterpret_cast<const uint32_t*>(&hh);
+      const uint32_t lb = *reinterpret_cast<const uint32_t*>(&ll);
+      const uint32_t bp0 = movmatrix_trans(prmt(hb, lb, 0x5410));  // (hi, lo) of token r
+      const uint32_t bp1 = movmatrix_trans(prmt(hb, lb, 0x7632));  // (hi, lo) of token r + 8
 
       // ---- P.V (Alg. 1 l.16): m-tile t <-> sub-vector 4r + t/2, components 2(t%2) + {0,1}
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint2 g0 = lds_u64(cv_base + code_off(cur.v[q][0], u));
-        const uint2 g1 = lds_u64(cv_base + code_off(cur.v[q][1], u));
-        const uint2 g2 = lds_u64(cv_base + code_off(cur.v[q][2], u));
-        const uint2 g3 = lds_u64(cv_base + code_off(cur.v[q][3], u));
+        uint2 g0, g1, g2, g3;
+        switch (u) {
+          case 0:
+            g0 = lds_u64(gaddr<0>(cur.v[q][0], vbase)); g1 = lds_u64(gaddr<0>(cur.v[q][1], vbase));
+            g2 = lds_u64(gaddr<0>(cur.v[q][2], vbase)); g3 = lds_u64(gaddr<0>(cur.v[q][3], vbase)); break;
+          case 1:
+            g0 = lds_u64(gaddr<1>(cur.v[q][0], vbase)); g1 = lds_u64(gaddr<1>(cur.v[q][1], vbase));
+            g2 = lds_u64(gaddr<1>(cur.v[q][2], vbase)); g3 = lds_u64(gaddr<1>(cur.v[q][3], vbase)); break;
+          case 2:
+            g0 = lds_u64(gaddr<2>(cur.v[q][0], vbase)); g1 = lds_u64(gaddr<2>(cur.v[q][1], vbase));
+            g2 = lds_u64(gaddr<2>(cur.v[q][2], vbase)); g3 = lds_u64(gaddr<2>(cur.v[q][3], vbase)); break;
+          default:
+            g0 = lds_u64(gaddr<3>(cur.v[q][0], vbase)); g1 = lds_u64(gaddr<3>(cur.v[q][1], vbase));
+            g2 = lds_u64(gaddr<3>(cur.v[q][2], vbase)); g3 = lds_u64(gaddr<3>(cur.v[q][3], vbase)); break;
+        }
         mma_16816(acc[2 * u], prmt(g0.x, g1.x, 0x5410), prmt(g0.x, g1.x, 0x7632), prmt(g2.x, g3.x, 0x5410),
                   prmt(g2.x, g3.x, 0x7632), bp0, bp1);
         mma_16816(acc[2 * u + 1], prmt(g0.y, g1.y, 0x5410), prmt(g0.y, g1.y, 0x7632), prmt(g2.y, g3.y, 0x5410),
@@ -200,12 +255,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
     }
   }
 
-  // ---- warp partials -> shared memory (reusing the codebook region)
+  // ---- warp partials -> shared memory
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 4);
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 8);
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);
-  __syncthreads();
-  float* wm = reinterpret_cast<float*>(smem_raw);
+  float* wm = reinterpret_cast<float*>(smem_raw + kMiscW);
   float* wl = wm + kNW * 4;
   float* wacc = wl + kNW * 4;
   if (r == 0) {
@@ -219,20 +273,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
     dst[2 * t + 1] = acc[t][2] + acc[t][3];  // dim 16r + 2t + 1 (h = 1)
   }
   __syncthreads();
-  cta_finish<kThreads>(a, b, h, s, kNW, wm, wl, wacc);
+  cta_finish<kThreads>(a, b, h, s, kNW, wm, wl, wacc, reinterpret_cast<float*>(tab));
 }
 
 }  // namespace
 
 void launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st) {
   (void)kbits; (void)vbits;  // dispatch validated by the caller (8/8 only in v1)
-  const size_t smem = sizeof(Smem8);
   static bool attr_set = false;  // benign race: idempotent attribute
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_mma8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(attn_mma8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     attr_set = true;
   }
-  attn_mma8_kernel<<<dim3(a.S, a.Hkv, a.B), kThreads, smem, st>>>(a);
+  attn_mma8_kernel<<<dim3(a.S, a.Hkv, a.B), kThreads, kSmemBytes, st>>>(a);
 }
 
 }  // namespace vecinfer

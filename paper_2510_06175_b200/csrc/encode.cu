@@ -156,6 +156,65 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_small_kernel(EncArgs a)
   store_code(a.vcodes, VBITS, row, lane, bi);
 }
 
+// ------------------------------------------------------------------ 4/8-bit decode append
+// Few token-heads (decode append, T = 1): one CTA of 16 warps per token-head.  Warps 0-7 search
+// C_k, warps 8-15 search C_v, each over 1/8 of the centroids (staged by that warp only, so no
+// CTA barrier before the scan); per-lane (dist, index) minima are reduced in warp order, which
+// keeps the lowest-index tie rule (strict < within a warp, ascending centroid ranges across).
+template <int KBITS, int VBITS>
+__global__ void __launch_bounds__(512) encode_append_kernel(EncArgs a) {
+  constexpr int NK = 1 << KBITS, NV = 1 << VBITS;
+  constexpr int PK = (NK + 7) / 8, PV = (NV + 7) / 8;  // centroids per warp
+  __shared__ float4 sc[8 * (PK > PV ? PK : PV) * 2];
+  __shared__ float sbest[16][32];
+  __shared__ uint32_t sidx[16][32];
+  const int h = blockIdx.y;
+  const int64_t bt = blockIdx.x;
+  const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool isv = warp >= 8;
+  const int w8 = warp & 7;
+  const int P = isv ? PV : PK;
+  const int n_ent = isv ? NV : NK;
+  const int j0 = w8 * P;
+  float4* mine = sc + (isv ? 8 * PK : 0) + w8 * P;
+  const uint16_t* cb = isv ? (a.cv + h * a.cv_hs) : (a.ck + h * a.ck_hs);
+  for (int i = lane; i < P; i += 32) {
+    if (j0 + i < n_ent) {
+      const uint2 w = *reinterpret_cast<const uint2*>(cb + 4 * (j0 + i));
+      mine[i] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                            __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+    }
+  }
+  float x[4];
+  if (isv) load_value_lane(a, b, t, h, lane, x);
+  else transform_key_lane(a, b, t, h, lane, x);
+  __syncwarp();
+  float best = __int_as_float(0x7f800000);
+  uint32_t bi = 0;
+  const int cnt = min(P, n_ent - j0);
+#pragma unroll 8
+  for (int i = 0; i < cnt; ++i) {
+    const float4 c = mine[i];
+    const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
+    if (dd < best) { best = dd; bi = j0 + i; }
+  }
+  sbest[warp][lane] = best;
+  sidx[warp][lane] = bi;
+  __syncthreads();
+  if (warp == 0 || warp == 8) {
+    float bb = sbest[warp][lane];
+    uint32_t ii = sidx[warp][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      const float c = sbest[warp + w][lane];
+      if (c < bb) { bb = c; ii = sidx[warp + w][lane]; }
+    }
+    int64_t row;
+    if (cache_row(a, b, t, h, lane, row)) store_code(isv ? a.vcodes : a.kcodes, isv ? VBITS : KBITS, row, lane, ii);
+  }
+}
+
 // ------------------------------------------------------------------ 16-bit: centroid split
 // grid (ceil(B*T / kEncWarps), 65536 / kChunk16, H); stage one chunk of C_k and C_v.
 __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) {
@@ -305,6 +364,14 @@ extern "C" vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* 
     if (s != VECINFER_OK) return s;
     encode_nn16_finalize<<<dim3(static_cast<unsigned>(gx), H_kv), kEncWarps * 32, 0, st>>>(a);
     return check_launch("encode_nn16_finalize");
+  }
+  if (nbt * H_kv <= 4096) {   // decode append: centroid-split search, 16 warps per token-head
+    dim3 g2(static_cast<unsigned>(nbt), H_kv);
+    if (kcfg.code_bits == 8 && vcfg.code_bits == 8) encode_append_kernel<8, 8><<<g2, 512, 0, st>>>(a);
+    else if (kcfg.code_bits == 4 && vcfg.code_bits == 4) encode_append_kernel<4, 4><<<g2, 512, 0, st>>>(a);
+    else if (kcfg.code_bits == 8 && vcfg.code_bits == 4) encode_append_kernel<8, 4><<<g2, 512, 0, st>>>(a);
+    else encode_append_kernel<4, 8><<<g2, 512, 0, st>>>(a);
+    return check_launch("encode_append_kernel");
   }
   dim3 grid(static_cast<unsigned>(gx), H_kv);
   if (kcfg.code_bits == 8 && vcfg.code_bits == 8) encode_small_kernel<8, 8><<<grid, kEncWarps * 32, 0, st>>>(a);

@@ -96,7 +96,7 @@ def _encode_ref(k, v, inv, ck, cv, n_cap, write_pos, kcfg, vcfg):
 
 
 @pytest.mark.parametrize("name,cfg", [("b2d4", vi.B2D4), ("b1d4", vi.B1D4)])
-@pytest.mark.parametrize("B,T", [(1, 1), (2, 37), (1, 300)])
+@pytest.mark.parametrize("B,T", [(1, 1), (2, 37), (1, 300), (1, 600)])  # 600 x 8 heads > 4096: bulk kernel
 def test_encode_bit_exact(name, cfg, B, T):
     k = synth.gen_keys(T, 8, 128, seed=100 + T, batch=B)
     v = synth.gen_values(T, 8, 128, seed=200 + T, batch=B)
