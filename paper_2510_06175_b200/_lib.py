@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvecinfer.so")
+LIB_PATH = os.environ.get("VECINFER_LIB") or os.path.join(_HERE, "libvecinfer.so")
 
 c_i32, c_i64, c_u32, c_f32, c_sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_float, ctypes.c_size_t
 c_void_p, c_char_p = ctypes.c_void_p, ctypes.c_char_p

@@ -20,6 +20,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "vecinfer")
 LIB = os.path.join(PKG, "libvecinfer.so")
+# profiling variant (phase timestamps), built only on request: python -m paper_2510_06175_b200.build --phase-timing
+LIB_PHASE = os.path.join(PKG, "libvecinfer_phase.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -41,7 +43,11 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, phase_timing: bool = False) -> str:
+    global BUILD, LIB
+    if phase_timing:
+        BUILD, LIB = BUILD + "_phase", LIB_PHASE
+        FLAGS.append("-DVECINFER_PHASE_TIMING")
     os.makedirs(BUILD, exist_ok=True)
     srcs = _sources()
     headers = [d for d in _deps() if not d.endswith(".cu")]
@@ -81,5 +87,6 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--phase-timing", action="store_true")
     args = ap.parse_args()
-    print(build(force=args.force, verbose=args.verbose))
+    print(build(force=args.force, verbose=args.verbose, phase_timing=args.phase_timing))

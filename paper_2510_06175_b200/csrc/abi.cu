@@ -46,6 +46,18 @@ int device_sm_count() {
 
 }  // namespace vecinfer
 
+namespace vecinfer {
+static unsigned long long* g_phase = nullptr;
+unsigned long long* phase_buffer() { return g_phase; }
+}  // namespace vecinfer
+#ifdef VECINFER_PHASE_TIMING
+// profiling builds only: device buffer of [n_cta][8] u64 globaltimer stamps
+extern "C" int vecinfer_debug_set_phase_buffer(void* p) {
+  vecinfer::g_phase = static_cast<unsigned long long*>(p);
+  return 0;
+}
+#endif
+
 extern "C" {
 
 int vecinfer_abi_version(void) { return VECINFER_ABI_VERSION; }

@@ -26,26 +26,50 @@ WsLayout ws_layout(int32_t B, int32_t H_kv, int32_t S) {
 
 }  // namespace
 
-// One CTA per SM (kernel N4 uses 16 warps and 66 KiB of shared memory), so the grid
-// B*H_kv*S is chosen to fill whole waves of SMs; splits shorter than 512 tokens are avoided.
-extern "C" int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits) {
-  if (num_splits > 0) return num_splits > kMaxSplits ? kMaxSplits : num_splits;
-  if (B <= 0 || H_kv <= 0) return 1;
+// Split plan: one CTA per SM (kernel N4: 16 warps, all 64K registers), so the grid B*H_kv*S
+// is sized in waves of SMs.  Cost model in "tokens of one CTA" (calibrated from the phase
+// timeline on B200, scripts/phase_attn.py): prologue ~370, DSMEM cluster merge ~250, global
+// fence/atomic/last-CTA merge ~1200, single split ~125.  Cluster path: the S <= 16 splits of a
+// (b, h_kv) form one thread-block cluster (limited by cudaOccupancyMaxActiveClusters).
+struct SplitPlan {
+  int S;
+  int cluster;
+};
+
+static SplitPlan plan_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits) {
   const int64_t units = static_cast<int64_t>(B) * H_kv;
   const int sms = device_sm_count();
+  if (num_splits > 0) {
+    const int S = num_splits > kMaxSplits ? kMaxSplits : num_splits;
+    const bool cl = S > 1 && S <= 16 && attn_mma_max_active_clusters(S) > 0;
+    return {S, cl ? 1 : 0};
+  }
   int64_t smax = (n_tokens_max + kMinTokensPerSplit - 1) / kMinTokensPerSplit;
   if (smax < 1) smax = 1;
   if (smax > kMaxSplits) smax = kMaxSplits;
-  int best = 1;
-  double best_score = -1.0;
+  SplitPlan best{1, 0};
+  double best_cost = 1e300;
   for (int s = 1; s <= smax; ++s) {
-    const int64_t ctas = units * s;
-    const int64_t waves = (ctas + sms - 1) / sms;
-    const double eff = static_cast<double>(ctas) / static_cast<double>(waves * sms);
-    const double score = eff - 0.002 * s;
-    if (score > best_score + 1e-12) { best_score = score; best = s; }
+    const double per = static_cast<double>((n_tokens_max + s - 1) / s) + 370.0;
+    // global-merge (or single-split) path
+    const int64_t waves = (units * s + sms - 1) / sms;
+    const double cg = static_cast<double>(waves) * (per + (s == 1 ? 125.0 : 1200.0));
+    if (cg < best_cost - 1e-9) { best_cost = cg; best = {s, 0}; }
+    if (s >= 2 && s <= 16) {
+      const int mac = attn_mma_max_active_clusters(s);
+      if (mac > 0) {
+        const int64_t wc = (units + mac - 1) / mac;
+        const double cc = static_cast<double>(wc) * (per + 250.0);
+        if (cc < best_cost - 1e-9) { best_cost = cc; best = {s, 1}; }
+      }
+    }
   }
   return best;
+}
+
+extern "C" int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits) {
+  if (B <= 0 || H_kv <= 0) return 1;
+  return plan_splits(B, H_kv, n_tokens_max, num_splits).S;
 }
 
 extern "C" size_t vecinfer_attn_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int32_t D, int64_t n_tokens_max,
@@ -86,9 +110,11 @@ extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B,
       !aligned(v_codes, 16) || ck_head_stride % 4 || cv_head_stride % 4 || ck_head_stride < 0 || cv_head_stride < 0)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: misaligned lambda/codebooks/codes");
   const int64_t range = tok_end >= 0 ? (tok_end - tok_begin < n_cap ? tok_end - tok_begin : n_cap) : n_cap;
-  const int32_t S = vecinfer_attn_num_splits(B, H_kv, range, num_splits);
+  const SplitPlan plan = algo == VECINFER_ATTN_LUT ? SplitPlan{vecinfer_attn_num_splits(B, H_kv, range, num_splits), 0}
+                                                  : plan_splits(B, H_kv, range, num_splits);
+  const int32_t S = plan.S;
   const WsLayout wl = ws_layout(B, H_kv, S);
-  if (S > 1 && (!workspace || workspace_bytes < wl.total || !aligned(workspace, 256)))
+  if (S > 1 && !plan.cluster && (!workspace || workspace_bytes < wl.total || !aligned(workspace, 256)))
     return fail(VECINFER_ERR_WORKSPACE, "attn_decode: workspace needs %zu bytes (256-B aligned)", wl.total);
   if (B > 65535 || H_kv > 65535) return fail(VECINFER_ERR_SHAPE, "attn_decode: grid too large");
 
@@ -104,13 +130,22 @@ extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B,
   a.seq_lens = seq_lens; a.tok_begin = tok_begin; a.tok_end = tok_end;
   a.qscale = static_cast<float>((1.0 / sqrt(128.0)) * static_cast<double>(softmax_scale) * 1.4426950408889634);
   a.S = S;
+  a.cluster = plan.cluster;
   a.o = o; a.o_f32 = (o_dtype == VECINFER_F32); a.lse = lse;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   a.counter = S > 1 ? reinterpret_cast<uint32_t*>(ws + wl.counter) : nullptr;
   a.part_l = S > 1 ? reinterpret_cast<float*>(ws + wl.part_l) : nullptr;
   a.part_o = S > 1 ? reinterpret_cast<float*>(ws + wl.part_o) : nullptr;
+  a.phase = phase_buffer();
   cudaStream_t st = as_stream(stream);
-  if (algo == VECINFER_ATTN_LUT) launch_attn_lut(a, kcfg.code_bits, vcfg.code_bits, st);
-  else launch_attn_mma(a, kcfg.code_bits, vcfg.code_bits, st);
+  if (algo == VECINFER_ATTN_LUT) {
+    launch_attn_lut(a, kcfg.code_bits, vcfg.code_bits, st);
+    return check_launch("attn_decode (lut)");
+  }
+  const cudaError_t e = launch_attn_mma(a, kcfg.code_bits, vcfg.code_bits, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(VECINFER_ERR_CUDA, "attn_decode: launch failed: %s", cudaGetErrorString(e));
+  }
   return check_launch("attn_decode");
 }

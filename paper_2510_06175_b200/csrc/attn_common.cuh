@@ -19,12 +19,14 @@ struct AttnArgs {
   int64_t tok_begin, tok_end;  // tok_end < 0: to seq_len
   float qscale;                // (1/sqrt(D)) * softmax_scale * log2(e): folded into q~
   int S;                       // splits per (b, h_kv)
+  int cluster;                 // 1: the S splits of a (b, h_kv) form one cluster, merged over DSMEM
   void* o;
   int o_f32;
   float* lse;
   float* part_o;     // [B*Hkv*S][4][128]
   float* part_l;     // [B*Hkv*S][4]   (log2 domain)
   uint32_t* counter; // [B*Hkv]
+  unsigned long long* phase;  // profiling builds: per-CTA phase stamps (else null)
 };
 
 // Token range [r0, r1) of split s for (b, h) and the clamp of the attended range.
@@ -89,6 +91,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   __syncthreads();
   if (tid == 0) s_last = (atomicAdd(&a.counter[unit], 1u) == static_cast<uint32_t>(a.S - 1));
   __syncthreads();
+  phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
   if (!s_last) return;
   __threadfence();
   // stage the S x 4 split LSEs (parallel loads), then per-head maxima
@@ -156,7 +159,8 @@ __device__ __forceinline__ void query_transform_warp(const AttnArgs& a, int b, i
       make_float4(x[0] * a.qscale, x[1] * a.qscale, x[2] * a.qscale, x[3] * a.qscale);
 }
 
-void launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
+cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
+int attn_mma_max_active_clusters(int cluster_size);  // 0 if not schedulable
 void launch_attn_lut(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
 
 }  // namespace vecinfer

@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kT, 1) attn_lut8_kernel(const AttnArgs a) {
   SmemLut& sm = *reinterpret_cast<SmemLut*>(smem_raw);
   const int s = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  griddep_wait();
   int64_t r0, r1;
   split_range(a, b, s, r0, r1);
   const int64_t ntile = (r1 - r0 + kT - 1) / kT;

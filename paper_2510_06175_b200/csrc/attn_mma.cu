@@ -35,7 +35,9 @@ constexpr int kTab = 65536;        // [256 centroids][256 B] codebook table, 64 
 constexpr int kMiscQ = 0;
 constexpr int kMiscW = 2048;                         // wm[16][4], wl[16][4], wacc[16][4][128]
 constexpr int kMiscBytes = kMiscW + (kNW * 8 + kNW * 4 * 128) * 4;   // 35328
-constexpr int kSmemBytes = kTab + 65536 + 1024;      // table + worst-case alignment pad + slack
+constexpr int kClusterMax = 16;                      // DSMEM merge buffer: [16][4][128] + m, l
+constexpr int kCbufBytes = kClusterMax * 4 * 130 * 4;
+constexpr int kSmemBytes = 65536 + kTab + kCbufBytes + 1024;  // pad + table + cluster buffer + slack
 
 __device__ __forceinline__ void fill_tables(unsigned char* tab, const uint16_t* ck, const uint16_t* cv, int tid) {
   // thread t: centroid j = t/2 of C_k (t even) or C_v (t odd); 16 replicas = 8 x 16-byte stores,
@@ -98,6 +100,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   const int s = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
+  const int cta_id = (b * gridDim.y + h) * gridDim.x + s;
+  phase_mark(a.phase, cta_id, 0);
 
   // shared layout: misc at the bottom, the codebook table at the next 64 KiB boundary
   const uint32_t raw_s = smem_u32(smem_raw);
@@ -106,6 +110,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   unsigned char* tab = smem_raw + tab_off;
   float* sq = reinterpret_cast<float*>(smem_raw + kMiscQ);
   const uint32_t tab_s = raw_s + tab_off;
+
+  // static weights first (codebooks): with programmatic dependent launch this overlaps the
+  // tail of the previous kernel on the stream; everything dynamic is read after the wait
+  fill_tables(tab, a.ck + h * a.ck_hs, a.cv + h * a.cv_hs, tid);
+  griddep_wait();
 
   int64_t r0, r1;
   split_range(a, b, s, r0, r1);
@@ -117,17 +126,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   const uint8_t* vp = a.vcodes + (unit * a.n_cap + r0 + 32 * warp + 2 * j) * kRowBytes + 4 * r;
   constexpr int kStep = 32 * kNW * kRowBytes;  // bytes between a warp's consecutive tiles
 
-  // issue the first tile's loads before the prologue so HBM latency overlaps it
+  // first tile's loads go out before the query transform so HBM latency overlaps it
   TileCodes nxt;
   if (warp < ntile) {
     const int rem = ntok - 32 * warp;
     if (rem >= 32) load_tile_full(nxt, kp, vp);
     else load_tile_tail(nxt, kp, vp, rem, r, j);
   }
-
-  fill_tables(tab, a.ck + h * a.ck_hs, a.cv + h * a.cv_hs, tid);
   if (warp < 4) query_transform_warp(a, b, h, warp, sq + 128 * warp);
   __syncthreads();
+  phase_mark(a.phase, cta_id, 1);
 
   // B fragments of the score MMA: column n = lane/4 <-> (head n/2, part n%2); rows k
   // <-> sub-vector 8j+t, components {0,1} (b0) and {2,3} (b1)
@@ -256,6 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   }
 
   // ---- warp partials -> shared memory
+  phase_mark(a.phase, cta_id, 2);
+  griddep_launch_dependents();   // the next kernel may start its (static) prologue
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 4);
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 8);
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);
@@ -273,19 +283,123 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
     dst[2 * t + 1] = acc[t][2] + acc[t][3];  // dim 16r + 2t + 1 (h = 1)
   }
   __syncthreads();
-  cta_finish<kThreads>(a, b, h, s, kNW, wm, wl, wacc, reinterpret_cast<float*>(tab));
+  phase_mark(a.phase, cta_id, 3);
+  if (!a.cluster) {
+    cta_finish<kThreads>(a, b, h, s, kNW, wm, wl, wacc, reinterpret_cast<float*>(tab));
+    phase_mark(a.phase, cta_id, 4);
+    return;
+  }
+  // ---- cluster path: the S splits of (b, h) are one cluster; each CTA combines its warps and
+  // pushes (M, l, acc[4][128]) into the leader's buffer over DSMEM; one cluster barrier; the
+  // leader merges the S partials in rank order (deterministic) and writes o and the LSE.
+  {
+    const int g = tid >> 7, dim = tid & 127;     // 512 threads <-> 4 heads x 128 dims
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) M = fmaxf(M, wm[w * 4 + g]);
+    float osum = 0.f, lsum = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kNW; ++w) {
+        const float f = ex2_approx(wm[w * 4 + g] - M);
+        lsum += f * wl[w * 4 + g];
+        osum += f * wacc[(w * 4 + g) * 128 + dim];
+      }
+    }
+    const uint32_t rank = cluster_ctarank();
+    float* cbuf = reinterpret_cast<float*>(tab + kTab);     // [16][4][128] acc, [16][4] M, [16][4] l
+    float* cM = cbuf + kClusterMax * 4 * 128;
+    float* cL = cM + kClusterMax * 4;
+    const uint32_t cb_s = smem_u32(cbuf);
+    st_cluster_f32(mapa_shared(cb_s + 4u * ((rank * 4 + g) * 128 + dim), 0), osum);
+    if (dim == 0) {
+      st_cluster_f32(mapa_shared(smem_u32(cM + rank * 4 + g), 0), M);
+      st_cluster_f32(mapa_shared(smem_u32(cL + rank * 4 + g), 0), lsum);
+    }
+    cluster_sync_all();
+    phase_mark(a.phase, cta_id, 5);
+    if (rank == 0 && g < a.G) {
+      float Mx = -INFINITY;
+      for (int q = 0; q < a.S; ++q) Mx = fmaxf(Mx, cM[q * 4 + g]);
+      float os = 0.f, ls = 0.f;
+      if (Mx != -INFINITY) {
+        for (int q = 0; q < a.S; ++q) {
+          const float f = ex2_approx(cM[q * 4 + g] - Mx);
+          ls += f * cL[q * 4 + g];
+          os += f * cbuf[(q * 4 + g) * 128 + dim];
+        }
+      }
+      const bool empty = !(ls > 0.f);
+      const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+      const float ov = empty ? 0.f : os / ls;
+      if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
+      else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
+      if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (Mx + __log2f(ls)) * kLn2;
+    }
+  }
+  phase_mark(a.phase, cta_id, 4);
 }
 
 }  // namespace
 
-void launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st) {
-  (void)kbits; (void)vbits;  // dispatch validated by the caller (8/8 only in v1)
-  static bool attr_set = false;  // benign race: idempotent attribute
-  if (!attr_set) {
+static void set_attrs_once() {
+  static bool done = false;  // benign race: idempotent attributes
+  if (!done) {
     cudaFuncSetAttribute(attn_mma8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    attr_set = true;
+    cudaFuncSetAttribute(attn_mma8_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    done = true;
   }
-  attn_mma8_kernel<<<dim3(a.S, a.Hkv, a.B), kThreads, kSmemBytes, st>>>(a);
+}
+
+int attn_mma_max_active_clusters(int cluster_size) {
+  static int cache[kClusterMax + 1] = {0};
+  if (cluster_size < 1 || cluster_size > kClusterMax) return 0;
+  if (cache[cluster_size] == 0) {
+    set_attrs_once();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cluster_size, 64, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cluster_size;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, attn_mma8_kernel, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    cache[cluster_size] = n > 0 ? n : -1;
+  }
+  return cache[cluster_size] > 0 ? cache[cluster_size] : 0;
+}
+
+cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st) {
+  (void)kbits; (void)vbits;  // dispatch validated by the caller (8/8 only in v1)
+  set_attrs_once();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.S, a.Hkv, a.B);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[n].val.programmaticStreamSerializationAllowed = 1;
+  ++n;
+  if (a.cluster) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = a.S;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, attn_mma8_kernel, a);
 }
 
 }  // namespace vecinfer

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <math.h>
+#include <utility>
 
 #include "../../include/vecinfer.h"
 
@@ -18,6 +19,25 @@ vecinfer_status_t check_launch(const char* what);
 int device_sm_count();  // cached per device
 
 inline cudaStream_t as_stream(vecinfer_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+// Launch with programmatic dependent launch enabled: the kernel may start while its predecessor
+// on the stream drains; it must call griddep_wait() before touching anything the predecessor
+// may write (our kernels read only static weights -- codebooks, lambda -- before the wait).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 // ------------------------------------------------------------------ device helpers
@@ -87,6 +107,27 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ---- thread-block clusters / distributed shared memory
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// ---- programmatic dependent launch (no-ops when the launch did not enable PDL)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // Pinned fp32 squared distance of reading R9: ((e0^2 + e1^2) + e2^2) + e3^2, RN, no FMA.
 __device__ __forceinline__ float pinned_dist4(float x0, float x1, float x2, float x3, float c0,
                                               float c1, float c2, float c3) {
@@ -96,6 +137,21 @@ __device__ __forceinline__ float pinned_dist4(float x0, float x1, float x2, floa
   s = __fadd_rn(s, __fmul_rn(e2, e2));
   return __fadd_rn(s, __fmul_rn(e3, e3));
 }
+
+// Phase timestamps for profiling builds (-DVECINFER_PHASE_TIMING): thread 0 of each CTA writes
+// %globaltimer (ns) at phase boundaries into a device buffer set with vecinfer_debug_set_phase_buffer.
+unsigned long long* phase_buffer();  // host: set by vecinfer_debug_set_phase_buffer (profiling builds)
+#ifdef VECINFER_PHASE_TIMING
+__device__ __forceinline__ void phase_mark(unsigned long long* buf, int cta, int slot) {
+  if (threadIdx.x == 0 && buf) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    buf[cta * 8 + slot] = t;
+  }
+}
+#else
+__device__ __forceinline__ void phase_mark(unsigned long long*, int, int) {}
+#endif
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;

@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_small_kernel(EncArgs a)
   constexpr int NK = 1 << KBITS, NV = 1 << VBITS;
   __shared__ float4 sck[NK];
   __shared__ float4 scv[NV];
+  griddep_launch_dependents();
   const int h = blockIdx.y;
   const uint16_t* ck = a.ck + h * a.ck_hs;
   const uint16_t* cv = a.cv + h * a.cv_hs;
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_small_kernel(EncArgs a)
                          __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
   }
   __syncthreads();
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   const int64_t bt = static_cast<int64_t>(blockIdx.x) * kEncWarps + (threadIdx.x >> 5);
   if (bt >= static_cast<int64_t>(a.B) * a.T) return;
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(512) encode_append_kernel(EncArgs a) {
   __shared__ float4 sc[8 * (PK > PV ? PK : PV) * 2];
   __shared__ float sbest[16][32];
   __shared__ uint32_t sidx[16][32];
+  griddep_launch_dependents();
   const int h = blockIdx.y;
   const int64_t bt = blockIdx.x;
   const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
@@ -186,6 +189,7 @@ __global__ void __launch_bounds__(512) encode_append_kernel(EncArgs a) {
                             __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
     }
   }
+  griddep_wait();
   float x[4];
   if (isv) load_value_lane(a, b, t, h, lane, x);
   else transform_key_lane(a, b, t, h, lane, x);
@@ -219,6 +223,7 @@ __global__ void __launch_bounds__(512) encode_append_kernel(EncArgs a) {
 // grid (ceil(B*T / kEncWarps), 65536 / kChunk16, H); stage one chunk of C_k and C_v.
 __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) {
   __shared__ float4 sc[kChunk16];
+  griddep_wait();
   const int h = blockIdx.z;
   const int j0 = blockIdx.y * kChunk16;
   const int lane = threadIdx.x & 31;
@@ -270,6 +275,7 @@ __device__ __forceinline__ void small_nn_global(const uint16_t* cb, const float 
 }
 
 __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_finalize(EncArgs a) {
+  griddep_wait();
   const int h = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int64_t bt = static_cast<int64_t>(blockIdx.x) * kEncWarps + (threadIdx.x >> 5);
@@ -367,16 +373,21 @@ extern "C" vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* 
   }
   if (nbt * H_kv <= 4096) {   // decode append: centroid-split search, 16 warps per token-head
     dim3 g2(static_cast<unsigned>(nbt), H_kv);
-    if (kcfg.code_bits == 8 && vcfg.code_bits == 8) encode_append_kernel<8, 8><<<g2, 512, 0, st>>>(a);
-    else if (kcfg.code_bits == 4 && vcfg.code_bits == 4) encode_append_kernel<4, 4><<<g2, 512, 0, st>>>(a);
-    else if (kcfg.code_bits == 8 && vcfg.code_bits == 4) encode_append_kernel<8, 4><<<g2, 512, 0, st>>>(a);
-    else encode_append_kernel<4, 8><<<g2, 512, 0, st>>>(a);
+    cudaError_t e;
+    if (kcfg.code_bits == 8 && vcfg.code_bits == 8) e = launch_pdl(encode_append_kernel<8, 8>, g2, dim3(512), 0, st, a);
+    else if (kcfg.code_bits == 4 && vcfg.code_bits == 4) e = launch_pdl(encode_append_kernel<4, 4>, g2, dim3(512), 0, st, a);
+    else if (kcfg.code_bits == 8 && vcfg.code_bits == 4) e = launch_pdl(encode_append_kernel<8, 4>, g2, dim3(512), 0, st, a);
+    else e = launch_pdl(encode_append_kernel<4, 8>, g2, dim3(512), 0, st, a);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_append_kernel: %s", cudaGetErrorString(e)); }
     return check_launch("encode_append_kernel");
   }
   dim3 grid(static_cast<unsigned>(gx), H_kv);
-  if (kcfg.code_bits == 8 && vcfg.code_bits == 8) encode_small_kernel<8, 8><<<grid, kEncWarps * 32, 0, st>>>(a);
-  else if (kcfg.code_bits == 4 && vcfg.code_bits == 4) encode_small_kernel<4, 4><<<grid, kEncWarps * 32, 0, st>>>(a);
-  else if (kcfg.code_bits == 8 && vcfg.code_bits == 4) encode_small_kernel<8, 4><<<grid, kEncWarps * 32, 0, st>>>(a);
-  else encode_small_kernel<4, 8><<<grid, kEncWarps * 32, 0, st>>>(a);
+  const dim3 blk(kEncWarps * 32);
+  cudaError_t e;
+  if (kcfg.code_bits == 8 && vcfg.code_bits == 8) e = launch_pdl(encode_small_kernel<8, 8>, grid, blk, 0, st, a);
+  else if (kcfg.code_bits == 4 && vcfg.code_bits == 4) e = launch_pdl(encode_small_kernel<4, 4>, grid, blk, 0, st, a);
+  else if (kcfg.code_bits == 8 && vcfg.code_bits == 4) e = launch_pdl(encode_small_kernel<8, 4>, grid, blk, 0, st, a);
+  else e = launch_pdl(encode_small_kernel<4, 8>, grid, blk, 0, st, a);
+  if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_small_kernel: %s", cudaGetErrorString(e)); }
   return check_launch("encode_small_kernel");
 }

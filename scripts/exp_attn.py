@@ -1,0 +1,67 @@
+"""Attention-kernel timing experiments (CUDA-graph replay of back-to-back launches, events).
+
+    python scripts/exp_attn.py --case B,N,splits[,algo] ...
+Prints µs per launch and GB/s on compressed bytes; rotates over enough cache copies to exceed L2.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+from paper_2510_06175_b200 import vecinfer as vi  # noqa: E402
+
+
+def run(B, N, splits, algo, reps=20):
+    dev = torch.device("cuda", 0)
+    z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz"))
+    lam = torch.from_numpy(z["lambda"]).to(dev)
+    ck = torch.from_numpy(synth.bf16_from_bits(z["ck_b2d4"])).to(dev).to(torch.bfloat16)
+    cv = torch.from_numpy(synth.bf16_from_bits(z["cv_b2d4"])).to(dev).to(torch.bfloat16)
+    nbytes = B * 8 * N * 64
+    copies = max(1, int(np.ceil(400e6 / nbytes)))
+    kcs = [synth.gen_codes_torch((B, 8, N, 32), 8, seed=2 * i, device=dev) for i in range(copies)]
+    vcs = [synth.gen_codes_torch((B, 8, N, 32), 8, seed=2 * i + 1, device=dev) for i in range(copies)]
+    q = torch.from_numpy(synth.gen_queries(B, 32, 8, 128, seed=3)).to(dev).to(torch.bfloat16)
+    seq = torch.full((B,), N, dtype=torch.int32, device=dev)
+    ws = [vi.attn_workspace(B, 32, 8, N, splits, device=dev) for _ in range(copies)]
+    o = torch.empty(B, 32, 128, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(B, 32, dtype=torch.float32, device=dev)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for i in range(copies):
+            vi.attn_decode(q, lam, ck, cv, kcs[i], vcs[i], seq, num_splits=splits, algo=algo, out=o, lse=lse, workspace=ws[i])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    n_l = max(copies, 8)
+    with torch.cuda.graph(g, stream=s):
+        for i in range(n_l):
+            vi.attn_decode(q, lam, ck, cv, kcs[i % copies], vcs[i % copies], seq, num_splits=splits, algo=algo,
+                           out=o, lse=lse, workspace=ws[i % copies])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):      # CUDAGraph.replay() launches on the CURRENT stream
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(reps):
+            g.replay()
+        e1.record(s)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / (reps * n_l)
+    S = vi.attn_num_splits(B, 8, N, splits)
+    print(f"B={B:3d} N={N:7d} S={S:3d} algo={algo:4s}: {us:8.2f} us/launch  {nbytes / us / 1e3:7.0f} GB/s  "
+          f"({100 * nbytes / us / 1e3 / 6553.6:.1f}% of 6553.6)  cyc/token-head@1.9GHz/SM={us * 1.9e3 * 148 / (B * 8 * N):.2f}",
+          flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", action="append", required=True)
+    args = ap.parse_args()
+    for c in args.case:
+        p = c.split(",")
+        run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma")

@@ -1,0 +1,69 @@
+"""Per-CTA phase timeline of the attention kernel (profiling build libvecinfer_phase.so).
+
+    python -m paper_2510_06175_b200.build --phase-timing
+    VECINFER_LIB=paper_2510_06175_b200/libvecinfer_phase.so python scripts/phase_attn.py --case 1,32768,0
+Stamps (globaltimer ns, thread 0 of each CTA): 0 start, 1 prologue done, 2 main loop done,
+3 warp partials in smem, 5 split partial published (atomic done), 4 exit.
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+from paper_2510_06175_b200 import _lib, vecinfer as vi  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", action="append", required=True)
+    args = ap.parse_args()
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz"))
+    lam = torch.from_numpy(z["lambda"]).to(dev)
+    ck = torch.from_numpy(synth.bf16_from_bits(z["ck_b2d4"])).to(dev).to(torch.bfloat16)
+    cv = torch.from_numpy(synth.bf16_from_bits(z["cv_b2d4"])).to(dev).to(torch.bfloat16)
+    for c in args.case:
+        B, N, splits = map(int, c.split(",")[:3])
+        S = vi.attn_num_splits(B, 8, N, splits)
+        nct = B * 8 * S
+        buf = torch.zeros(nct * 8, dtype=torch.int64, device=dev)
+        lib.vecinfer_debug_set_phase_buffer.argtypes = [ctypes.c_void_p]
+        lib.vecinfer_debug_set_phase_buffer(ctypes.c_void_p(buf.data_ptr()))
+        kc = synth.gen_codes_torch((B, 8, N, 32), 8, seed=1, device=dev)
+        vc = synth.gen_codes_torch((B, 8, N, 32), 8, seed=2, device=dev)
+        q = torch.from_numpy(synth.gen_queries(B, 32, 8, 128, seed=3)).to(dev).to(torch.bfloat16)
+        seq = torch.full((B,), N, dtype=torch.int32, device=dev)
+        ws = vi.attn_workspace(B, 32, 8, N, splits, device=dev)
+        for _ in range(5):
+            buf.zero_()
+            vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, workspace=ws)
+            torch.cuda.synchronize()
+        t = buf.view(nct, 8).cpu().numpy().astype(np.float64)
+        t0 = t[:, 0].min()
+        rel = (t - t0) / 1e3
+        span = (t[:, 4].max() - t0) / 1e3
+        print(f"B={B} N={N} S={S} CTAs={nct}: span {span:.2f} us")
+
+        def st(x, name):
+            print(f"   {name:32s} min {x.min():7.2f}  med {np.median(x):7.2f}  max {x.max():7.2f} us")
+        st(rel[:, 0], "CTA start (rel)")
+        st(rel[:, 1] - rel[:, 0], "prologue (fill+q~+sync)")
+        st(rel[:, 2] - rel[:, 1], "main loop (incl. bq frags)")
+        st(rel[:, 3] - rel[:, 2], "warp partials -> smem")
+        if S > 1:
+            st(rel[:, 5] - rel[:, 3], "combine+publish+fence+atomic")
+            last = t[:, 4] - t[:, 5] > 0
+            st((rel[:, 4] - rel[:, 5]), "merge (all CTAs)")
+            print(f"   last-CTA merges: {int(last.sum())}, exit max {rel[:, 4].max():.2f}")
+        st(rel[:, 4], "CTA end (rel)")
+
+
+if __name__ == "__main__":
+    main()

@@ -214,7 +214,7 @@ def test_attn_ragged_lengths(algo, n):
     _assert_close(o, L, *_run_ref(c))
 
 
-@pytest.mark.parametrize("splits", [1, 2, 3, 7, 40])
+@pytest.mark.parametrize("splits", [1, 2, 3, 7, 16, 18, 40])  # <= 16: DSMEM cluster merge; else global
 def test_attn_fixed_splits_and_determinism(splits):
     c = _attn_case(1, 4, 4, 3000, [2999], seed=splits)
     o1, L1 = _run_gpu(c, num_splits=splits)
