@@ -67,6 +67,11 @@ static SplitPlan plan_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int3
   return best;
 }
 
+// diagnostics: max co-resident clusters of the attention kernel for a cluster size (0 = none)
+extern "C" int32_t vecinfer_debug_attn_max_clusters(int32_t cluster_size) {
+  return attn_mma_max_active_clusters(cluster_size);
+}
+
 extern "C" int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits) {
   if (B <= 0 || H_kv <= 0) return 1;
   return plan_splits(B, H_kv, n_tokens_max, num_splits).S;

@@ -16,7 +16,7 @@ import synth  # noqa: E402
 from paper_2510_06175_b200 import vecinfer as vi  # noqa: E402
 
 
-def run(B, N, splits, algo, reps=20):
+def run(B, N, splits, algo, reps=20, with_encode=False):
     dev = torch.device("cuda", 0)
     z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz"))
     lam = torch.from_numpy(z["lambda"]).to(dev)
@@ -34,12 +34,25 @@ def run(B, N, splits, algo, reps=20):
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         for i in range(copies):
-            vi.attn_decode(q, lam, ck, cv, kcs[i], vcs[i], seq, num_splits=splits, algo=algo, out=o, lse=lse, workspace=ws[i])
+            if algo != "none":
+                vi.attn_decode(q, lam, ck, cv, kcs[i], vcs[i], seq, num_splits=splits, algo=algo, out=o, lse=lse,
+                               workspace=ws[i])
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     n_l = max(copies, 8)
+    inv = torch.from_numpy(z["inv_lambda"]).to(dev)
+    kn = torch.from_numpy(synth.gen_keys(1, 8, 128, seed=4, batch=B)).to(dev).to(torch.bfloat16)
+    vn = torch.from_numpy(synth.gen_values(1, 8, 128, seed=5, batch=B)).to(dev).to(torch.bfloat16)
+    wp = torch.full((B,), N - 1, dtype=torch.int32, device=dev)
+    with torch.cuda.stream(s):
+        vi.encode_kv(kn, vn, inv, ck, cv, kcs[0], vcs[0], wp)
+    torch.cuda.synchronize()
     with torch.cuda.graph(g, stream=s):
         for i in range(n_l):
+            if with_encode:
+                vi.encode_kv(kn, vn, inv, ck, cv, kcs[i % copies], vcs[i % copies], wp)
+            if algo == "none":
+                continue
             vi.attn_decode(q, lam, ck, cv, kcs[i % copies], vcs[i % copies], seq, num_splits=splits, algo=algo,
                            out=o, lse=lse, workspace=ws[i % copies])
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -53,7 +66,7 @@ def run(B, N, splits, algo, reps=20):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (reps * n_l)
     S = vi.attn_num_splits(B, 8, N, splits)
-    print(f"B={B:3d} N={N:7d} S={S:3d} algo={algo:4s}: {us:8.2f} us/launch  {nbytes / us / 1e3:7.0f} GB/s  "
+    print(f"B={B:3d} N={N:7d} S={S:3d} algo={algo:4s} enc={int(with_encode)}: {us:8.2f} us/launch  {nbytes / us / 1e3:7.0f} GB/s  "
           f"({100 * nbytes / us / 1e3 / 6553.6:.1f}% of 6553.6)  cyc/token-head@1.9GHz/SM={us * 1.9e3 * 148 / (B * 8 * N):.2f}",
           flush=True)
 
@@ -64,4 +77,7 @@ if __name__ == "__main__":
     args = ap.parse_args()
     for c in args.case:
         p = c.split(",")
-        run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma")
+        run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma", with_encode=len(p) > 4 and p[4] == "enc")
+    from paper_2510_06175_b200 import _lib
+    lib = _lib.load()
+    print("max active clusters (size: n):", {c: lib.vecinfer_debug_attn_max_clusters(c) for c in (2, 4, 8, 12, 16)})
