@@ -51,19 +51,22 @@ __device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int
 // last-CTA log-sum-exp merge over the S splits in fixed order s = 0..S-1.
 //   wm[NW][4], wl[NW][4] (log2 domain), wacc[NW][4][128] (unnormalised);
 //   scratch: >= 4*S + 8 floats of shared memory not aliased with wm/wl/wacc.
-template <int NTHREADS>
-__device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s, int NWARPS,
+template <int NTHREADS, int NWARPS>
+__device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s,
                                            const float* wm, const float* wl, const float* wacc,
                                            float* scratch) {
+  (void)scratch;
   const int tid = threadIdx.x;
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
   __shared__ bool s_last;
   for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
     const int g = idx >> 7, dim = idx & 127;
     float M = -INFINITY;
+#pragma unroll
     for (int w = 0; w < NWARPS; ++w) M = fmaxf(M, wm[w * 4 + g]);
     float osum = 0.f, lsum = 0.f;
     if (M != -INFINITY) {
+#pragma unroll
       for (int w = 0; w < NWARPS; ++w) {
         const float f = ex2_approx(wm[w * 4 + g] - M);
         lsum += f * wl[w * 4 + g];
@@ -94,29 +97,27 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
   if (!s_last) return;
   __threadfence();
-  // stage the S x 4 split LSEs (parallel loads), then per-head maxima
-  float* sLs = scratch;           // [S][4]
-  float* sM = scratch + 4 * a.S;  // [4]
-  for (int i = tid; i < 4 * a.S; i += NTHREADS) sLs[i] = __ldcg(&a.part_l[unit * a.S * 4 + i]);
-  __syncthreads();
-  if (tid < 4) {
-    float M = -INFINITY;
-    for (int ss = 0; ss < a.S; ++ss) M = fmaxf(M, sLs[ss * 4 + tid]);
-    sM[tid] = M;
-  }
-  __syncthreads();
+  // one pass, one memory round trip: every (L_s, o_s) load is independent of the arithmetic,
+  // the running-max merge folds them in the fixed order s = 0..S-1
   for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
     const int g = idx >> 7, dim = idx & 127;
     if (g >= a.G) continue;
-    const float M = sM[g];
-    float osum = 0.f, wsum = 0.f;
-    if (M != -INFINITY) {
-      const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
+    const float* pl = a.part_l + unit * a.S * 4 + g;
+    const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
+    float m = -INFINITY, wsum = 0.f, osum = 0.f;
 #pragma unroll 8
-      for (int ss = 0; ss < a.S; ++ss) {
-        const float f = ex2_approx(sLs[ss * 4 + g] - M);
+    for (int ss = 0; ss < a.S; ++ss) {
+      const float L = __ldcg(pl + 4 * ss);
+      const float x = __ldcg(po + static_cast<int64_t>(ss) * 512);
+      if (L > m) {
+        const float sc = ex2_approx(m - L);   // 0 when m == -inf
+        osum = osum * sc + x;
+        wsum = wsum * sc + 1.f;
+        m = L;
+      } else {
+        const float f = L == -INFINITY ? 0.f : ex2_approx(L - m);   // empty split: weight 0
+        osum += f * x;
         wsum += f;
-        osum += f * __ldcg(po + static_cast<int64_t>(ss) * 4 * 128);
       }
     }
     const bool empty = !(wsum > 0.f);
@@ -124,7 +125,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
     if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
     else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-    if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (M + __log2f(wsum)) * kLn2;
+    if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
   }
   if (tid == 0) a.counter[unit] = 0u;  // ready for the next launch
 }

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kT, 1) attn_lut8_kernel(const AttnArgs a) {
 #pragma unroll
   for (int g = 0; g < 4; ++g) wacc[g * 128 + tid] = o[g];
   __syncthreads();
-  cta_finish<kT>(a, b, h, s, 1, wm, wl, wacc, scratch);
+  cta_finish<kT, 1>(a, b, h, s, wm, wl, wacc, scratch);
 }
 
 }  // namespace

@@ -30,6 +30,7 @@ constexpr int kNW = 16;            // warps per CTA (1 CTA per SM)
 constexpr int kThreads = kNW * 32;
 constexpr float kTau = 8.0f;       // lazy-rescale threshold (log2 units): p <= 2^8
 constexpr int kRowBytes = 32;      // 8-bit codes, D/d = 32 sub-vectors
+constexpr int kPfd = 4;            // L2 bulk-prefetch distance, in this warp's tiles
 constexpr int kTab = 65536;        // [256 centroids][256 B] codebook table, 64 KiB-aligned
 // misc region (below the table): q~ [4][128] f32, warp partials, staged split partials
 constexpr int kMiscQ = 0;
@@ -126,7 +127,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   const uint8_t* vp = a.vcodes + (unit * a.n_cap + r0 + 32 * warp + 2 * j) * kRowBytes + 4 * r;
   constexpr int kStep = 32 * kNW * kRowBytes;  // bytes between a warp's consecutive tiles
 
-  // first tile's loads go out before the query transform so HBM latency overlaps it
+  // L2 bulk prefetch of this warp's next kPfd tiles (K and V rows are contiguous per tile), then
+  // the first tile's register loads; both overlap the query transform
+  const uint8_t* kb_unit = a.kcodes + (unit * a.n_cap + r0) * kRowBytes;
+  const uint8_t* vb_unit = a.vcodes + (unit * a.n_cap + r0) * kRowBytes;
+  if (lane == 0) {
+#pragma unroll
+    for (int pf = 1; pf <= kPfd; ++pf) {
+      const int tt = warp + pf * kNW;
+      if (tt < ntile) {
+        const int nt = min(32, ntok - 32 * tt);
+        prefetch_l2_bulk(kb_unit + tt * 32 * kRowBytes, nt * kRowBytes);
+        prefetch_l2_bulk(vb_unit + tt * 32 * kRowBytes, nt * kRowBytes);
+      }
+    }
+  }
   TileCodes nxt;
   if (warp < ntile) {
     const int rem = ntok - 32 * warp;
@@ -168,6 +183,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   for (int it = warp; it < ntile; it += kNW) {
     const TileCodes cur = nxt;
     const int rem_cur = ntok - 32 * it;
+    if (lane == 0 && it + (kPfd + 1) * kNW < ntile) {
+      const int tt = it + (kPfd + 1) * kNW;
+      const int nt = min(32, ntok - 32 * tt);
+      prefetch_l2_bulk(kb_unit + tt * 32 * kRowBytes, nt * kRowBytes);
+      prefetch_l2_bulk(vb_unit + tt * 32 * kRowBytes, nt * kRowBytes);
+    }
     if (it + kNW < ntile) {
       kp += kStep;
       vp += kStep;
@@ -285,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   __syncthreads();
   phase_mark(a.phase, cta_id, 3);
   if (!a.cluster) {
-    cta_finish<kThreads>(a, b, h, s, kNW, wm, wl, wacc, reinterpret_cast<float*>(tab));
+    cta_finish<kThreads, kNW>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
     phase_mark(a.phase, cta_id, 4);
     return;
   }
