@@ -230,7 +230,13 @@ def run_ours(args, rank, world, local_rank):
     ws = [vi.attn_workspace(B, H_Q, H_KV, n_local, 0, device=dev) for _ in range(L)]
     stream = torch.cuda.Stream(device=dev)
 
+    fused = not args.unfused and not seq_sharded
+
     def layer(l, ev_pair=None):
+        if fused:   # one launch: append-encode of the new token + attention (vecinfer_decode_step)
+            vi.decode_step(q_all[l], kn_all[l][:, 0], vn_all[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
+                           seq_lens, out=o_all[l], lse=lse_all[l], workspace=ws[l])
+            return
         if owns_tail:
             vi.encode_kv(kn_all[l], vn_all[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg)
         if ev_pair is not None:
@@ -252,7 +258,7 @@ def run_ours(args, rank, world, local_rank):
             vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
                          o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D))
 
-    launches_per_step = L * ((1 if owns_tail else 0) + 1) + (1 if seq_sharded else 0)
+    launches_per_step = L if fused else L * ((1 if owns_tail else 0) + 1) + (1 if seq_sharded else 0)
 
     # ---- warm-up (eager) so lazy init/attributes happen outside capture
     with torch.cuda.stream(stream):
@@ -334,6 +340,10 @@ def run_ours(args, rank, world, local_rank):
         kn_d.copy_(kn_h, non_blocking=True)
         vn_d.copy_(vn_h, non_blocking=True)
         for l in range(L):
+            if fused:
+                vi.decode_step(q_d[l], kn_d[l][:, 0], vn_d[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
+                               seq_lens, out=o_all[l], lse=lse_all[l], workspace=ws[l])
+                continue
             if owns_tail:
                 vi.encode_kv(kn_d[l], vn_d[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg)
             if seq_sharded:
@@ -393,7 +403,7 @@ def run_ours(args, rank, world, local_rank):
                    "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": "b2d4",
                    "parallelism": ("seq-shard" if seq_sharded else "dp") + str(world),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
-                   "num_splits": S, "cuda_graph": use_graph,
+                   "num_splits": S, "cuda_graph": use_graph, "fused_append": fused,
                    "dtype_detail": "u8 codes, bf16 q/k/v/o, fp16 hi/lo MMA operands, f32 accumulate"},
         "us_per_layer_call": step_ms * 1e3 / L,
         "tokens_per_s": B_glob * 1e3 / step_ms,
@@ -424,6 +434,7 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--unfused", action="store_true", help="separate encode_kv + attn_decode launches per layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=2.0)

@@ -75,6 +75,10 @@ typedef enum {
 #define VECINFER_FLAG_RANGE 1u     /* |k * inv_lambda| >= 2^32: outside the pinned fixed point */
 #define VECINFER_FLAG_WRITE_POS 2u /* write_pos[b] + t outside [0, n_cap): row not written     */
 
+/* Programmatic dependent launch: every kernel is launched with PDL and reads only the static
+ * weights (codebooks) before griddepcontrol.wait, so codebooks must not be produced by the
+ * kernel immediately preceding a call on the same stream.  All other inputs may be. */
+
 int vecinfer_abi_version(void);
 const char* vecinfer_last_error(void);
 const char* vecinfer_status_string(vecinfer_status_t status);
@@ -172,6 +176,32 @@ vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_
                                        size_t workspace_bytes, vecinfer_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Fused decode step for one layer: EXACTLY vecinfer_encode_kv(T = 1) of the new token followed
+ * by vecinfer_attn_decode over [0, seq_lens[b]) (Eq. 9 then Eq. 10), in one launch.
+ * The split of each (b, h_kv) whose range holds row write_pos[b] (else split 0) encodes the new
+ * k, v in its prologue (centroid scan split over its 16 warps, bit-identical codes), writes them
+ * to the cache and uses them for that row; all other work is the plain attention kernel.
+ *   q_bf16     [B, H_q, D] (strides q_strides = {b, h});  k_new_bf16, v_new_bf16 [B, H_kv, D]
+ *              (strides {b, h}); inv_lambda as in encode_kv; lambda as in attn_decode.
+ *   k_codes, v_codes  the code caches (written at row write_pos[b], read over [0, seq_lens[b])).
+ *   Other arguments as in vecinfer_attn_decode (token range = whole sequence) and
+ *   vecinfer_encode_kv (err_flags).  The codebooks must be b2d4 for the fused launch; with
+ *   algo = VECINFER_ATTN_LUT the call is executed as the two separate launches.
+ * Errors: as vecinfer_encode_kv and vecinfer_attn_decode.
+ * ------------------------------------------------------------------------------------- */
+vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,
+                                       int32_t B, int32_t H_q, int32_t H_kv, const int64_t q_strides[2],
+                                       const int64_t k_new_strides[2], const int64_t v_new_strides[2],
+                                       const float* lambda, const float* inv_lambda, const void* ck_bf16,
+                                       const void* cv_bf16, int64_t ck_head_stride, int64_t cv_head_stride,
+                                       vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes,
+                                       uint8_t* v_codes, int64_t n_cap, const int32_t* write_pos,
+                                       const int32_t* seq_lens, float softmax_scale, int32_t num_splits,
+                                       vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype,
+                                       float* lse, uint32_t* err_flags, void* workspace,
+                                       size_t workspace_bytes, vecinfer_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
  * Log-sum-exp merge of P normalised partials (cross-GPU sequence shards, residual window):
  *   L = logsumexp_s L_s;  o = sum_s exp(L_s - L) o_s, summed in the fixed order s = 0..P-1
  *   (the online-softmax recurrence of P:745-757 applied to whole partials).
@@ -184,6 +214,10 @@ vecinfer_status_t vecinfer_merge_lse(const float* o_parts, const float* lse_part
                                      int32_t B, int32_t H_q, int32_t D, void* o,
                                      vecinfer_dtype_t o_dtype, float* lse,
                                      vecinfer_stream_t stream);
+
+/* Diagnostics: how many thread-block clusters of `cluster_size` CTAs of the attention kernel can
+ * be co-resident on the current device (0 = not schedulable); used by the split planner. */
+int32_t vecinfer_debug_attn_max_clusters(int32_t cluster_size);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,7 @@ LIB_PATH = os.environ.get("VECINFER_LIB") or os.path.join(_HERE, "libvecinfer.so
 c_i32, c_i64, c_u32, c_f32, c_sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_float, ctypes.c_size_t
 c_void_p, c_char_p = ctypes.c_void_p, ctypes.c_char_p
 I64x3 = ctypes.c_int64 * 3
+I64x2 = ctypes.c_int64 * 2
 
 
 class VQ(ctypes.Structure):
@@ -40,6 +41,11 @@ PROTOTYPES = {
     "vecinfer_attn_decode": (c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i64, c_i64, c_void_p, c_void_p, c_void_p,
                                      c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_i64, c_f32,
                                      c_i32, c_i32, c_void_p, c_i32, c_void_p, c_void_p, c_sz, c_void_p]),
+    "vecinfer_decode_step": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, I64x2, I64x2, I64x2,
+                                     c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, VQ, VQ, c_void_p,
+                                     c_void_p, c_i64, c_void_p, c_void_p, c_f32, c_i32, c_i32, c_void_p, c_i32,
+                                     c_void_p, c_void_p, c_void_p, c_sz, c_void_p]),
+    "vecinfer_debug_attn_max_clusters": (c_i32, [c_i32]),
     "vecinfer_merge_lse": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_void_p, c_i32, c_void_p,
                                    c_void_p]),
 }

@@ -85,15 +85,24 @@ extern "C" size_t vecinfer_attn_workspace_bytes(int32_t B, int32_t H_q, int32_t 
   return ws_layout(B, H_kv, S).total;
 }
 
-extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_q, int32_t H_kv,
-                                                  int64_t q_stride_b, int64_t q_stride_h, const float* lambda,
-                                                  const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride,
-                                                  int64_t cv_head_stride, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
-                                                  const uint8_t* k_codes, const uint8_t* v_codes, int64_t n_cap,
-                                                  const int32_t* seq_lens, int64_t tok_begin, int64_t tok_end,
-                                                  float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
-                                                  void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
-                                                  size_t workspace_bytes, vecinfer_stream_t stream) {
+struct AppendArgs {
+  const void* k_new;
+  const void* v_new;
+  int64_t kn_sb, kn_sh, vn_sb, vn_sh;
+  const float* inv_lambda;
+  const int32_t* write_pos;
+  uint32_t* err;
+};
+
+static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, int32_t H_kv,
+                                   int64_t q_stride_b, int64_t q_stride_h, const float* lambda,
+                                   const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride,
+                                   int64_t cv_head_stride, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
+                                   const uint8_t* k_codes, const uint8_t* v_codes, int64_t n_cap,
+                                   const int32_t* seq_lens, int64_t tok_begin, int64_t tok_end,
+                                   float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
+                                   void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
+                                   size_t workspace_bytes, vecinfer_stream_t stream, const AppendArgs* app) {
   if (!q_bf16 || !lambda || !ck_bf16 || !cv_bf16 || !k_codes || !v_codes || !seq_lens || !o)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: NULL pointer");
   if (o_dtype != VECINFER_BF16 && o_dtype != VECINFER_F32) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad o_dtype");
@@ -142,6 +151,17 @@ extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B,
   a.part_l = S > 1 ? reinterpret_cast<float*>(ws + wl.part_l) : nullptr;
   a.part_o = S > 1 ? reinterpret_cast<float*>(ws + wl.part_o) : nullptr;
   a.phase = phase_buffer();
+  a.append = app != nullptr;
+  a.knew = app ? static_cast<const uint16_t*>(app->k_new) : nullptr;
+  a.vnew = app ? static_cast<const uint16_t*>(app->v_new) : nullptr;
+  a.kn_sb = app ? app->kn_sb : 0; a.kn_sh = app ? app->kn_sh : 0;
+  a.vn_sb = app ? app->vn_sb : 0; a.vn_sh = app ? app->vn_sh : 0;
+  a.inv_lambda = app ? app->inv_lambda : nullptr;
+  a.write_pos = app ? app->write_pos : nullptr;
+  a.err = app ? app->err : nullptr;
+  a.kcodes_w = const_cast<uint8_t*>(k_codes);
+  a.vcodes_w = const_cast<uint8_t*>(v_codes);
+  a.inv_sqrt_d = static_cast<float>(1.0 / sqrt(128.0));
   cudaStream_t st = as_stream(stream);
   if (algo == VECINFER_ATTN_LUT) {
     launch_attn_lut(a, kcfg.code_bits, vcfg.code_bits, st);
@@ -153,4 +173,54 @@ extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B,
     return fail(VECINFER_ERR_CUDA, "attn_decode: launch failed: %s", cudaGetErrorString(e));
   }
   return check_launch("attn_decode");
+}
+
+extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_q, int32_t H_kv,
+                                                  int64_t q_stride_b, int64_t q_stride_h, const float* lambda,
+                                                  const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride,
+                                                  int64_t cv_head_stride, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
+                                                  const uint8_t* k_codes, const uint8_t* v_codes, int64_t n_cap,
+                                                  const int32_t* seq_lens, int64_t tok_begin, int64_t tok_end,
+                                                  float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
+                                                  void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
+                                                  size_t workspace_bytes, vecinfer_stream_t stream) {
+  return attn_impl(q_bf16, B, H_q, H_kv, q_stride_b, q_stride_h, lambda, ck_bf16, cv_bf16, ck_head_stride,
+                   cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, tok_begin, tok_end, softmax_scale,
+                   num_splits, algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr);
+}
+
+extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,
+                                                  int32_t B, int32_t H_q, int32_t H_kv, const int64_t q_strides[2],
+                                                  const int64_t k_new_strides[2], const int64_t v_new_strides[2],
+                                                  const float* lambda, const float* inv_lambda, const void* ck_bf16,
+                                                  const void* cv_bf16, int64_t ck_head_stride, int64_t cv_head_stride,
+                                                  vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes,
+                                                  uint8_t* v_codes, int64_t n_cap, const int32_t* write_pos,
+                                                  const int32_t* seq_lens, float softmax_scale, int32_t num_splits,
+                                                  vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype,
+                                                  float* lse, uint32_t* err_flags, void* workspace,
+                                                  size_t workspace_bytes, vecinfer_stream_t stream) {
+  if (!k_new_bf16 || !v_new_bf16 || !inv_lambda || !write_pos || !q_strides || !k_new_strides || !v_new_strides)
+    return fail(VECINFER_ERR_INVALID_ARG, "decode_step: NULL pointer");
+  for (int i = 0; i < 2; ++i)
+    if (k_new_strides[i] % 4 || v_new_strides[i] % 4 || k_new_strides[i] < 0 || v_new_strides[i] < 0)
+      return fail(VECINFER_ERR_INVALID_ARG, "decode_step: k_new/v_new strides must be non-negative multiples of 4");
+  if (!aligned(k_new_bf16, 8) || !aligned(v_new_bf16, 8) || !aligned(inv_lambda, 16))
+    return fail(VECINFER_ERR_INVALID_ARG, "decode_step: misaligned k_new/v_new/inv_lambda");
+  if (algo == VECINFER_ATTN_LUT) {   // paper-faithful variant: separate append + LUT attention launches
+    const int64_t ks[3] = {k_new_strides[0], 0, k_new_strides[1]};
+    const int64_t vs[3] = {v_new_strides[0], 0, v_new_strides[1]};
+    vecinfer_status_t st = vecinfer_encode_kv(k_new_bf16, v_new_bf16, B, 1, H_kv, ks, vs, inv_lambda, ck_bf16, cv_bf16,
+                                              ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap,
+                                              write_pos, err_flags, nullptr, 0, stream);
+    if (st != VECINFER_OK) return st;
+    return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
+                     cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
+                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr);
+  }
+  AppendArgs app{k_new_bf16, v_new_bf16, k_new_strides[0], k_new_strides[1], v_new_strides[0], v_new_strides[1],
+                 inv_lambda, write_pos, err_flags};
+  return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
+                   cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
+                   algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app);
 }

@@ -27,18 +27,37 @@ struct AttnArgs {
   float* part_l;     // [B*Hkv*S][4]   (log2 domain)
   uint32_t* counter; // [B*Hkv]
   unsigned long long* phase;  // profiling builds: per-CTA phase stamps (else null)
+  // fused decode append (vecinfer_decode_step): encode the new token's k, v of each (b, h_kv)
+  // into cache row write_pos[b] inside the attention launch (append == 0: plain attention)
+  int append;
+  const uint16_t* knew;  // bf16 [B, H_kv, 128] (strides kn_sb, kn_sh)
+  const uint16_t* vnew;
+  int64_t kn_sb, kn_sh, vn_sb, vn_sh;
+  const float* inv_lambda;  // [H_kv, 128]
+  const int32_t* write_pos; // [B]
+  uint32_t* err;            // optional VECINFER_FLAG_* word
+  uint8_t* kcodes_w;        // writable views of the code caches
+  uint8_t* vcodes_w;
+  float inv_sqrt_d;
 };
 
-// Token range [r0, r1) of split s for (b, h) and the clamp of the attended range.
-__device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int64_t& r0, int64_t& r1) {
+// extra tokens' worth of work the split owning the appended row does (its encode), used to
+// shorten that split so it does not become the straggler
+constexpr int64_t kAppendTokenCost = 160;
+
+// Token range [r0, r1) of split s for (b, h) within the attended range [beg, e).
+__device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int64_t& r0, int64_t& r1,
+                                            int64_t* pbeg = nullptr, int64_t* pend = nullptr) {
   int64_t len = a.seq_lens[b];
   if (len > a.n_cap) len = a.n_cap;
   if (len < 0) len = 0;
   int64_t e = a.tok_end < 0 ? len : (a.tok_end < len ? a.tok_end : len);
   int64_t beg = a.tok_begin < e ? a.tok_begin : e;
   if (beg < 0) beg = 0;
+  if (pbeg) *pbeg = beg;
+  if (pend) *pend = e;
   const int64_t n = e - beg;
-  int64_t chunk = (n + a.S - 1) / a.S;
+  int64_t chunk = (n + (a.append && a.S > 1 ? kAppendTokenCost : 0) + a.S - 1) / a.S;
   chunk = (chunk + 31) & ~int64_t(31);
   r0 = beg + s * chunk;
   if (r0 > e) r0 = e;
@@ -97,28 +116,37 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
   if (!s_last) return;
   __threadfence();
-  // one pass, one memory round trip: every (L_s, o_s) load is independent of the arithmetic,
-  // the running-max merge folds them in the fixed order s = 0..S-1
+  // merge in chunks of 32 splits: all 2 x 32 loads of a chunk are issued before any use (one
+  // memory round trip per chunk), then the fixed-order log-sum-exp combine s = 0..S-1
   for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
     const int g = idx >> 7, dim = idx & 127;
     if (g >= a.G) continue;
     const float* pl = a.part_l + unit * a.S * 4 + g;
     const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
     float m = -INFINITY, wsum = 0.f, osum = 0.f;
-#pragma unroll 8
-    for (int ss = 0; ss < a.S; ++ss) {
-      const float L = __ldcg(pl + 4 * ss);
-      const float x = __ldcg(po + static_cast<int64_t>(ss) * 512);
-      if (L > m) {
-        const float sc = ex2_approx(m - L);   // 0 when m == -inf
-        osum = osum * sc + x;
-        wsum = wsum * sc + 1.f;
-        m = L;
-      } else {
-        const float f = L == -INFINITY ? 0.f : ex2_approx(L - m);   // empty split: weight 0
-        osum += f * x;
-        wsum += f;
+    for (int s0 = 0; s0 < a.S; s0 += 32) {
+      float lv[32], xv[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const bool ok = s0 + k < a.S;
+        lv[k] = ok ? __ldcg(pl + 4 * (s0 + k)) : -INFINITY;
+        xv[k] = ok ? __ldcg(po + static_cast<int64_t>(s0 + k) * 512) : 0.f;
       }
+      float mc = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) mc = fmaxf(mc, lv[k]);
+      const float mn = fmaxf(m, mc);
+      if (mn == -INFINITY) continue;
+      const float sc = m == -INFINITY ? 0.f : ex2_approx(m - mn);
+      osum *= sc;
+      wsum *= sc;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float f = lv[k] == -INFINITY ? 0.f : ex2_approx(lv[k] - mn);
+        wsum += f;
+        osum += f * xv[k];
+      }
+      m = mn;
     }
     const bool empty = !(wsum > 0.f);
     const float ov = empty ? 0.f : osum / wsum;

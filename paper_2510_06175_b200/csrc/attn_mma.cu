@@ -30,11 +30,11 @@ constexpr int kNW = 16;            // warps per CTA (1 CTA per SM)
 constexpr int kThreads = kNW * 32;
 constexpr float kTau = 8.0f;       // lazy-rescale threshold (log2 units): p <= 2^8
 constexpr int kRowBytes = 32;      // 8-bit codes, D/d = 32 sub-vectors
-constexpr int kPfd = 4;            // L2 bulk-prefetch distance, in this warp's tiles
 constexpr int kTab = 65536;        // [256 centroids][256 B] codebook table, 64 KiB-aligned
 // misc region (below the table): q~ [4][128] f32, warp partials, staged split partials
 constexpr int kMiscQ = 0;
-constexpr int kMiscW = 2048;                         // wm[16][4], wl[16][4], wacc[16][4][128]
+constexpr int kMiscNew = 2048;                       // 64 B: codes of the appended token (fused append)
+constexpr int kMiscW = 2176;                         // wm[16][4], wl[16][4], wacc[16][4][128]
 constexpr int kMiscBytes = kMiscW + (kNW * 8 + kNW * 4 * 128) * 4;   // 35328
 constexpr int kClusterMax = 16;                      // DSMEM merge buffer: [16][4][128] + m, l
 constexpr int kCbufBytes = kClusterMax * 4 * 130 * 4;
@@ -117,39 +117,91 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   fill_tables(tab, a.ck + h * a.ck_hs, a.cv + h * a.cv_hs, tid);
   griddep_wait();
 
-  int64_t r0, r1;
-  split_range(a, b, s, r0, r1);
+  int64_t r0, r1, beg, e;
+  split_range(a, b, s, r0, r1, &beg, &e);
   const int ntok = static_cast<int>(r1 - r0);
   const int ntile = (ntok + 31) >> 5;
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
+  // fused decode append: the split holding row p = write_pos[b] (else split 0) encodes the new token
+  bool owner = false;
+  int patch_tile = -1, patch_row = 0;
+  int64_t p_row = 0;
+  if (a.append) {
+    p_row = a.write_pos[b];
+    const bool in_range = p_row >= beg && p_row < e;
+    owner = in_range ? (p_row >= r0 && p_row < r1) : (s == 0);
+    if (owner && in_range) {
+      patch_tile = static_cast<int>((p_row - r0) >> 5);
+      patch_row = static_cast<int>((p_row - r0) & 31);
+    }
+  }
   // lane-resolved code pointers of this warp's first tile
   const uint8_t* kp = a.kcodes + (unit * a.n_cap + r0 + 32 * warp + r) * kRowBytes + 8 * j;
   const uint8_t* vp = a.vcodes + (unit * a.n_cap + r0 + 32 * warp + 2 * j) * kRowBytes + 4 * r;
   constexpr int kStep = 32 * kNW * kRowBytes;  // bytes between a warp's consecutive tiles
 
-  // L2 bulk prefetch of this warp's next kPfd tiles (K and V rows are contiguous per tile), then
-  // the first tile's register loads; both overlap the query transform
-  const uint8_t* kb_unit = a.kcodes + (unit * a.n_cap + r0) * kRowBytes;
-  const uint8_t* vb_unit = a.vcodes + (unit * a.n_cap + r0) * kRowBytes;
-  if (lane == 0) {
-#pragma unroll
-    for (int pf = 1; pf <= kPfd; ++pf) {
-      const int tt = warp + pf * kNW;
-      if (tt < ntile) {
-        const int nt = min(32, ntok - 32 * tt);
-        prefetch_l2_bulk(kb_unit + tt * 32 * kRowBytes, nt * kRowBytes);
-        prefetch_l2_bulk(vb_unit + tt * 32 * kRowBytes, nt * kRowBytes);
-      }
-    }
-  }
+  // first tile's loads go out before the query transform so HBM latency overlaps it
   TileCodes nxt;
   if (warp < ntile) {
     const int rem = ntok - 32 * warp;
     if (rem >= 32) load_tile_full(nxt, kp, vp);
     else load_tile_tail(nxt, kp, vp, rem, r, j);
   }
+  unsigned char* newcodes = smem_raw + kMiscNew;   // [0,32): K codes, [32,64): V codes
+  if (owner) {
+    // Eq. 9: encode the new token (S then H on the key, VQ on both), 8 warps per stream, each
+    // scanning 32 centroids (bf16 codebook -> fp32, pinned distance, lowest index on ties)
+    const bool isv = warp >= 8;
+    const int w8 = warp & 7;
+    float4* stage = reinterpret_cast<float4*>(smem_raw + kMiscW);
+    float* sbest = reinterpret_cast<float*>(smem_raw + kMiscW + 8192);
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(smem_raw + kMiscW + 10240);
+    const uint16_t* cb = isv ? (a.cv + h * a.cv_hs) : (a.ck + h * a.ck_hs);
+    stage[warp * 32 + lane] = bf16x4_to_float4(*reinterpret_cast<const uint2*>(cb + 4 * (32 * w8 + lane)));
+    float x[4];
+    if (!isv) {
+      const bool bad = key_transform_lane(a.knew + b * a.kn_sb + h * a.kn_sh + 4 * lane,
+                                          a.inv_lambda + h * 128 + 4 * lane, a.inv_sqrt_d, lane, x);
+      if (bad && warp == 0 && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
+    } else {
+      const float4 v = bf16x4_to_float4(*reinterpret_cast<const uint2*>(a.vnew + b * a.vn_sb + h * a.vn_sh + 4 * lane));
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    }
+    __syncwarp();
+    float best = __int_as_float(0x7f800000);
+    uint32_t bi = 0;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) {
+      const float4 c = stage[warp * 32 + i];
+      const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
+      if (dd < best) { best = dd; bi = 32 * w8 + i; }
+    }
+    sbest[warp * 32 + lane] = best;
+    sidx[warp * 32 + lane] = bi;
+  }
   if (warp < 4) query_transform_warp(a, b, h, warp, sq + 128 * warp);
   __syncthreads();
+  if (owner) {
+    if (warp == 0 || warp == 8) {
+      const float* sbest = reinterpret_cast<const float*>(smem_raw + kMiscW + 8192);
+      const uint32_t* sidx = reinterpret_cast<const uint32_t*>(smem_raw + kMiscW + 10240);
+      float bb = sbest[warp * 32 + lane];
+      uint32_t ii = sidx[warp * 32 + lane];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) {
+        const float c = sbest[(warp + w) * 32 + lane];
+        if (c < bb) { bb = c; ii = sidx[(warp + w) * 32 + lane]; }
+      }
+      newcodes[(warp >> 3) * 32 + lane] = static_cast<uint8_t>(ii);
+      if (p_row >= 0 && p_row < a.n_cap) {
+        uint8_t* dst = (warp == 0 ? a.kcodes_w : a.vcodes_w) + (unit * a.n_cap + p_row) * kRowBytes;
+        dst[lane] = static_cast<uint8_t>(ii);
+      } else if (lane == 0 && a.err) {
+        atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
+      }
+    }
+    __syncthreads();
+  }
   phase_mark(a.phase, cta_id, 1);
 
   // B fragments of the score MMA: column n = lane/4 <-> (head n/2, part n%2); rows k
@@ -181,14 +233,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   float m_run = -INFINITY, l_run = 0.f;
 
   for (int it = warp; it < ntile; it += kNW) {
-    const TileCodes cur = nxt;
-    const int rem_cur = ntok - 32 * it;
-    if (lane == 0 && it + (kPfd + 1) * kNW < ntile) {
-      const int tt = it + (kPfd + 1) * kNW;
-      const int nt = min(32, ntok - 32 * tt);
-      prefetch_l2_bulk(kb_unit + tt * 32 * kRowBytes, nt * kRowBytes);
-      prefetch_l2_bulk(vb_unit + tt * 32 * kRowBytes, nt * kRowBytes);
+    TileCodes cur = nxt;
+    if (it == patch_tile) {   // the appended row: use the codes just encoded (not the stale load)
+      const uint2 nk = *reinterpret_cast<const uint2*>(newcodes + 8 * j);
+      const uint32_t nv = *reinterpret_cast<const uint32_t*>(newcodes + 32 + 4 * r);
+      const int qp = patch_row >> 4, rr = patch_row & 15;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (q != qp) continue;
+        if (r == rr) cur.k[q][0] = nk;
+        if (r + 8 == rr) cur.k[q][1] = nk;
+        if (2 * j == rr) cur.v[q][0] = nv;
+        if (2 * j + 1 == rr) cur.v[q][1] = nv;
+        if (2 * j + 8 == rr) cur.v[q][2] = nv;
+        if (2 * j + 9 == rr) cur.v[q][3] = nv;
+      }
     }
+    const int rem_cur = ntok - 32 * it;
     if (it + kNW < ntile) {
       kp += kStep;
       vp += kStep;

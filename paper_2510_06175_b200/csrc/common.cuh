@@ -143,6 +143,49 @@ __device__ __forceinline__ float pinned_dist4(float x0, float x1, float x2, floa
   return __fadd_rn(s, __fmul_rn(e3, e3));
 }
 
+// Key side of the dual transform for the 4 dims [4*lane, 4*lane+4) held by this lane (one warp =
+// one 128-dim key), on the pinned exact fixed point (R10):
+//   A = rint_even(k * inv_lambda * 2^24) in int64 (the f64 product bf16 x fp32 is exact),
+//   X = A H_pm  (2 in-register + 5 warp-shuffle butterfly stages, exact integer arithmetic),
+//   x = RN32(RN32(X) * 2^-24) * RN32(1/sqrt(D)).
+// krow4/inv4 point at this lane's 4 elements.  Returns true (warp-uniform) if any |k*inv| >= 2^32.
+__device__ __forceinline__ bool key_transform_lane(const uint16_t* krow4, const float* inv4, float inv_sqrt_d,
+                                                   int lane, float (&x)[4]) {
+  const uint2 kw = *reinterpret_cast<const uint2*>(krow4);
+  const float kf[4] = {__uint_as_float(kw.x << 16), __uint_as_float(kw.x & 0xFFFF0000u),
+                       __uint_as_float(kw.y << 16), __uint_as_float(kw.y & 0xFFFF0000u)};
+  const float4 il = *reinterpret_cast<const float4*>(inv4);
+  const float ilv[4] = {il.x, il.y, il.z, il.w};
+  long long A[4];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double p = __dmul_rn(static_cast<double>(kf[i]), static_cast<double>(ilv[i]));  // exact
+    bad |= !(fabs(p) < 4294967296.0);
+    A[i] = __double2ll_rn(__dmul_rn(p, 16777216.0));  // ties-to-even, exact scaling
+  }
+  long long s0 = A[0] + A[1], s1 = A[0] - A[1], s2 = A[2] + A[3], s3 = A[2] - A[3];
+  A[0] = s0 + s2; A[2] = s0 - s2; A[1] = s1 + s3; A[3] = s1 - s3;
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const long long o = __shfl_xor_sync(0xffffffffu, A[i], m);
+      A[i] = upper ? (o - A[i]) : (A[i] + o);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    x[i] = __fmul_rn(__fmul_rn(__ll2float_rn(A[i]), 5.9604644775390625e-08f), inv_sqrt_d);
+  return __any_sync(0xffffffffu, bad);
+}
+
+__device__ __forceinline__ float4 bf16x4_to_float4(uint2 w) {
+  return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u), __uint_as_float(w.y << 16),
+                     __uint_as_float(w.y & 0xFFFF0000u));
+}
+
 // Phase timestamps for profiling builds (-DVECINFER_PHASE_TIMING): thread 0 of each CTA writes
 // %globaltimer (ns) at phase boundaries into a device buffer set with vecinfer_debug_set_phase_buffer.
 unsigned long long* phase_buffer();  // host: set by vecinfer_debug_set_phase_buffer (profiling builds)

@@ -39,40 +39,12 @@ struct EncArgs {
   unsigned long long* ws;  // 16-bit path: [B*T*H][2][32] packed minima
 };
 
-// Smoothing + exact integer FWHT + fixed-point -> fp32, for the 4 dims of this lane.
+// Smoothing + exact integer FWHT + fixed-point -> fp32 (key_transform_lane), flags range errors.
 __device__ __forceinline__ void transform_key_lane(const EncArgs& a, int b, int t, int h, int lane,
                                                    float (&x)[4]) {
-  const uint16_t* kp = a.k + b * a.ks_b + t * a.ks_t + h * a.ks_h + 4 * lane;
-  const uint2 kw = *reinterpret_cast<const uint2*>(kp);
-  const float kf[4] = {__uint_as_float(kw.x << 16), __uint_as_float(kw.x & 0xFFFF0000u),
-                       __uint_as_float(kw.y << 16), __uint_as_float(kw.y & 0xFFFF0000u)};
-  const float4 il = *reinterpret_cast<const float4*>(a.inv_lambda + h * 128 + 4 * lane);
-  const float ilv[4] = {il.x, il.y, il.z, il.w};
-  long long A[4];
-  bool bad = false;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double p = __dmul_rn(static_cast<double>(kf[i]), static_cast<double>(ilv[i]));  // exact
-    bad |= !(fabs(p) < 4294967296.0);
-    A[i] = __double2ll_rn(__dmul_rn(p, 16777216.0));  // ties-to-even, exact scaling
-  }
-  if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
-  // in-register stages (element strides 1, 2)
-  long long s0 = A[0] + A[1], s1 = A[0] - A[1], s2 = A[2] + A[3], s3 = A[2] - A[3];
-  A[0] = s0 + s2; A[2] = s0 - s2; A[1] = s1 + s3; A[3] = s1 - s3;
-  // warp-shuffle stages (element strides 4 .. 64 <-> lane strides 1 .. 16)
-#pragma unroll
-  for (int m = 1; m < 32; m <<= 1) {
-    const bool upper = (lane & m) != 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const long long o = __shfl_xor_sync(0xffffffffu, A[i], m);
-      A[i] = upper ? (o - A[i]) : (A[i] + o);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    x[i] = __fmul_rn(__fmul_rn(__ll2float_rn(A[i]), 5.9604644775390625e-08f), a.inv_sqrt_d);
+  const bool bad = key_transform_lane(a.k + b * a.ks_b + t * a.ks_t + h * a.ks_h + 4 * lane,
+                                      a.inv_lambda + h * 128 + 4 * lane, a.inv_sqrt_d, lane, x);
+  if (bad && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
 }
 
 __device__ __forceinline__ void load_value_lane(const EncArgs& a, int b, int t, int h, int lane, float (&x)[4]) {

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import VQ, I64x3, check
+from ._lib import VQ, I64x2, I64x3, check
 
 _lib.load()   # fail loudly at import if the native library is missing
 
@@ -158,6 +158,44 @@ def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.
         _need(seq_lens, "seq_lens", torch.int32), tok_begin, tok_end, softmax_scale, num_splits, ALGOS[algo],
         _need(out, "out"), odt, _need(lse, "lse", torch.float32), ctypes.c_void_p(workspace.data_ptr()),
         workspace.numel(), _stream(q.device)))
+    return out, lse
+
+
+def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: torch.Tensor,
+                inv_lambda: torch.Tensor, ck: torch.Tensor, cv: torch.Tensor, k_codes: torch.Tensor,
+                v_codes: torch.Tensor, write_pos: torch.Tensor, seq_lens: torch.Tensor,
+                softmax_scale: float | None = None, num_splits: int = 0, algo: str = "auto",
+                kcfg: VQConfig = B2D4, vcfg: VQConfig = B2D4, o_dtype: torch.dtype = torch.float32,
+                out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
+                err_flags: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+    """Fused layer decode step = encode_kv(T=1) of k_new/v_new [B, H_kv, D] at row write_pos[b]
+    followed by attn_decode over [0, seq_lens[b]) -- one launch (vecinfer_decode_step)."""
+    B, Hq, D = q.shape
+    Hkv, n_cap = k_codes.shape[1], k_codes.shape[2]
+    if softmax_scale is None:
+        softmax_scale = D ** -0.5
+    if tuple(k_new.shape) != (B, Hkv, D) or tuple(v_new.shape) != (B, Hkv, D):
+        raise ValueError("k_new/v_new must be [B, H_kv, D]")
+    if out is None:
+        out = torch.empty(B, Hq, D, dtype=o_dtype, device=q.device)
+    if lse is None:
+        lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device)
+    lib = _lib.load()
+    need = lib.vecinfer_attn_workspace_bytes(B, Hq, Hkv, D, n_cap, num_splits)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.zeros(max(need, 256), dtype=torch.uint8, device=q.device)
+    check("vecinfer_decode_step", lib.vecinfer_decode_step(
+        _need(q, "q", torch.bfloat16), _need(k_new, "k_new", torch.bfloat16), _need(v_new, "v_new", torch.bfloat16),
+        B, Hq, Hkv, I64x2(q.stride(0), q.stride(1)), I64x2(k_new.stride(0), k_new.stride(1)),
+        I64x2(v_new.stride(0), v_new.stride(1)), _need(lam, "lambda", torch.float32),
+        _need(inv_lambda, "inv_lambda", torch.float32), _need(ck, "ck", torch.bfloat16),
+        _need(cv, "cv", torch.bfloat16), _cb_stride(ck), _cb_stride(cv), kcfg.c(), vcfg.c(),
+        _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
+        _need(write_pos, "write_pos", torch.int32), _need(seq_lens, "seq_lens", torch.int32), softmax_scale,
+        num_splits, ALGOS[algo], _need(out, "out"), F32 if out.dtype == torch.float32 else BF16,
+        _need(lse, "lse", torch.float32),
+        ctypes.c_void_p(err_flags.data_ptr()) if err_flags is not None else ctypes.c_void_p(0),
+        ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream(q.device)))
     return out, lse
 
 

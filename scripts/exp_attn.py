@@ -49,6 +49,10 @@ def run(B, N, splits, algo, reps=20, with_encode=False):
     torch.cuda.synchronize()
     with torch.cuda.graph(g, stream=s):
         for i in range(n_l):
+            if with_encode == "fused":
+                vi.decode_step(q, kn[:, 0], vn[:, 0], lam, inv, ck, cv, kcs[i % copies], vcs[i % copies], wp, seq,
+                               num_splits=splits, out=o, lse=lse, workspace=ws[i % copies])
+                continue
             if with_encode:
                 vi.encode_kv(kn, vn, inv, ck, cv, kcs[i % copies], vcs[i % copies], wp)
             if algo == "none":
@@ -66,7 +70,7 @@ def run(B, N, splits, algo, reps=20, with_encode=False):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (reps * n_l)
     S = vi.attn_num_splits(B, 8, N, splits)
-    print(f"B={B:3d} N={N:7d} S={S:3d} algo={algo:4s} enc={int(with_encode)}: {us:8.2f} us/launch  {nbytes / us / 1e3:7.0f} GB/s  "
+    print(f"B={B:3d} N={N:7d} S={S:3d} algo={algo:4s} enc={with_encode}: {us:8.2f} us/launch  {nbytes / us / 1e3:7.0f} GB/s  "
           f"({100 * nbytes / us / 1e3 / 6553.6:.1f}% of 6553.6)  cyc/token-head@1.9GHz/SM={us * 1.9e3 * 148 / (B * 8 * N):.2f}",
           flush=True)
 
@@ -77,7 +81,8 @@ if __name__ == "__main__":
     args = ap.parse_args()
     for c in args.case:
         p = c.split(",")
-        run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma", with_encode=len(p) > 4 and p[4] == "enc")
+        run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma",
+            with_encode=(p[4] if p[4] == "fused" else True) if len(p) > 4 else False)
     from paper_2510_06175_b200 import _lib
     lib = _lib.load()
     print("max active clusters (size: n):", {c: lib.vecinfer_debug_attn_max_clusters(c) for c in (2, 4, 8, 12, 16)})

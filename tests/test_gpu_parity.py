@@ -329,3 +329,44 @@ def test_cfg3_full_size_sampled_units():
 
 def test_cfg4_full_size_sampled_units():
     _sampled_units_check(1, 196608, 2, seed=42)
+
+
+# ------------------------------------------------- fused decode step (append + attention)
+@pytest.mark.parametrize("splits", [0, 1, 3, 8, 18])
+@pytest.mark.parametrize("lens", [[2048], [1500, 37], [33, 1]])
+def test_decode_step_fused_equals_encode_then_attend(splits, lens):
+    """vecinfer_decode_step == encode_kv(T=1) + attn_decode: the appended row's codes are the
+    oracle's, bit for bit, and the output matches the oracle over the updated cache."""
+    B = len(lens)
+    n_cap = max(lens) + 5
+    c = _attn_case(B, 8, 4, n_cap, lens, seed=60 + splits + len(lens))
+    kn = synth.gen_keys(1, 8, 128, seed=70, batch=B)[:, 0]        # [B, H_kv, D]
+    vn = synth.gen_values(1, 8, 128, seed=71, batch=B)[:, 0]
+    wp = [n - 1 for n in lens]
+    kcodes, vcodes = t_u8(c["kc"]), t_u8(c["vc"])
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(c["ck"]), t_bf16(c["cv"]), kcodes, vcodes, t_i32(wp), t_i32(lens),
+                          num_splits=splits, err_flags=err)
+    assert int(err.item()) == 0
+    for b in range(B):
+        for h in range(8):
+            kk, vv = ref.encode_kv(kn[b, h], vn[b, h], CB["inv_lambda"][h], c["ck"][h], c["cv"][h])
+            c["kc"][b, h, wp[b]] = kk
+            c["vc"][b, h, wp[b]] = vv
+    assert np.array_equal(kcodes.cpu().numpy(), c["kc"].astype(np.uint8))
+    assert np.array_equal(vcodes.cpu().numpy(), c["vc"].astype(np.uint8))
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))
+
+
+def test_decode_step_append_outside_attended_range():
+    """write_pos beyond seq_len: the row is written (by split 0) but not attended."""
+    c = _attn_case(1, 8, 4, 600, [500], seed=80)
+    kn = synth.gen_keys(1, 8, 128, seed=81)[:, 0]
+    vn = synth.gen_values(1, 8, 128, seed=82)[:, 0]
+    kcodes, vcodes = t_u8(c["kc"]), t_u8(c["vc"])
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(c["ck"]), t_bf16(c["cv"]), kcodes, vcodes, t_i32([550]), t_i32([500]))
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))      # old cache attended
+    kk, _ = ref.encode_kv(kn[0, 3], vn[0, 3], CB["inv_lambda"][3], c["ck"][3], c["cv"][3])
+    assert np.array_equal(kcodes[0, 3, 550].cpu().numpy(), kk.astype(np.uint8))
