@@ -1,9 +1,32 @@
 // Host side of vecinfer_attn_decode: validation, split heuristic, workspace layout, dispatch.
+#include <stdlib.h>
+
 #include "attn_common.cuh"
 
 using namespace vecinfer;
 
+namespace vecinfer {
+// Separate split-merge kernel (PDL): launched right behind the attention kernel, it waits for the
+// attention grid to complete (griddepcontrol.wait gives completion + visibility of the partials,
+// so the attention CTAs need no fence/atomic), then merges the S partials of one (b, h_kv) unit.
+__global__ void __launch_bounds__(512) split_merge_kernel(const AttnArgs a) {
+  griddep_launch_dependents();
+  griddep_wait();
+  merge_splits<512>(a, blockIdx.x % a.B, blockIdx.x / a.B);
+}
+}  // namespace vecinfer
+
 namespace {
+
+// VECINFER_MERGE=kernel selects the separate merge kernel, =fused the last-CTA merge (default)
+int merge_mode_from_env() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("VECINFER_MERGE");
+    mode = (e && e[0] == 'k') ? 1 : 0;
+  }
+  return mode;
+}
 
 constexpr int kMaxSplits = 128;
 constexpr int64_t kMinTokensPerSplit = 512;
@@ -145,6 +168,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.qscale = static_cast<float>((1.0 / sqrt(128.0)) * static_cast<double>(softmax_scale) * 1.4426950408889634);
   a.S = S;
   a.cluster = plan.cluster;
+  a.merge_kernel = (S > 1 && !plan.cluster && algo != VECINFER_ATTN_LUT) ? merge_mode_from_env() : 0;
   a.o = o; a.o_f32 = (o_dtype == VECINFER_F32); a.lse = lse;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   a.counter = S > 1 ? reinterpret_cast<uint32_t*>(ws + wl.counter) : nullptr;
@@ -171,6 +195,13 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(VECINFER_ERR_CUDA, "attn_decode: launch failed: %s", cudaGetErrorString(e));
+  }
+  if (a.merge_kernel) {
+    const cudaError_t e2 = launch_pdl(split_merge_kernel, dim3(static_cast<unsigned>(B) * H_kv), dim3(512), 0, st, a);
+    if (e2 != cudaSuccess) {
+      cudaGetLastError();
+      return fail(VECINFER_ERR_CUDA, "attn_decode: merge launch failed: %s", cudaGetErrorString(e2));
+    }
   }
   return check_launch("attn_decode");
 }
@@ -207,7 +238,19 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
       return fail(VECINFER_ERR_INVALID_ARG, "decode_step: k_new/v_new strides must be non-negative multiples of 4");
   if (!aligned(k_new_bf16, 8) || !aligned(v_new_bf16, 8) || !aligned(inv_lambda, 16))
     return fail(VECINFER_ERR_INVALID_ARG, "decode_step: misaligned k_new/v_new/inv_lambda");
-  if (algo == VECINFER_ATTN_LUT) {   // paper-faithful variant: separate append + LUT attention launches
+  // Fuse only when the grid is one wave: the owner CTA's encode latency (~1-2 us) then hides
+  // behind the other CTAs' longer splits; with several waves every wave would carry it, and a
+  // separate append launch (latency ~3 us, once) is cheaper.
+  bool fuse = algo != VECINFER_ATTN_LUT;
+  if (fuse && B > 0 && H_kv > 0) {
+    const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
+    const int64_t units = static_cast<int64_t>(B) * H_kv;
+    const int64_t waves = plan.cluster ? (units + attn_mma_max_active_clusters(plan.S) - 1) /
+                                             (attn_mma_max_active_clusters(plan.S) > 0 ? attn_mma_max_active_clusters(plan.S) : 1)
+                                       : (units * plan.S + device_sm_count() - 1) / device_sm_count();
+    fuse = waves <= 1;
+  }
+  if (!fuse) {   // separate append + attention launches (always for the paper-faithful LUT variant)
     const int64_t ks[3] = {k_new_strides[0], 0, k_new_strides[1]};
     const int64_t vs[3] = {v_new_strides[0], 0, v_new_strides[1]};
     vecinfer_status_t st = vecinfer_encode_kv(k_new_bf16, v_new_bf16, B, 1, H_kv, ks, vs, inv_lambda, ck_bf16, cv_bf16,

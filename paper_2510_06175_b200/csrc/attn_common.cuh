@@ -20,6 +20,7 @@ struct AttnArgs {
   float qscale;                // (1/sqrt(D)) * softmax_scale * log2(e): folded into q~
   int S;                       // splits per (b, h_kv)
   int cluster;                 // 1: the S splits of a (b, h_kv) form one cluster, merged over DSMEM
+  int merge_kernel;            // 1: split partials are merged by a separate PDL-launched kernel
   void* o;
   int o_f32;
   float* lse;
@@ -70,6 +71,51 @@ __device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int
 // last-CTA log-sum-exp merge over the S splits in fixed order s = 0..S-1.
 //   wm[NW][4], wl[NW][4] (log2 domain), wacc[NW][4][128] (unnormalised);
 //   scratch: >= 4*S + 8 floats of shared memory not aliased with wm/wl/wacc.
+// Fixed-order log-sum-exp merge of the S split partials of unit (b, h) into o and lse, in chunks
+// of 32 splits: all 2 x 32 loads of a chunk are issued before any use (one memory round trip per
+// chunk), then the running-max combine over s = 0..S-1.
+template <int NTHREADS>
+__device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
+  const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
+  for (int idx = threadIdx.x; idx < 4 * 128; idx += NTHREADS) {
+    const int g = idx >> 7, dim = idx & 127;
+    if (g >= a.G) continue;
+    const float* pl = a.part_l + unit * a.S * 4 + g;
+    const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
+    float m = -INFINITY, wsum = 0.f, osum = 0.f;
+    for (int s0 = 0; s0 < a.S; s0 += 32) {
+      float lv[32], xv[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const bool ok = s0 + k < a.S;
+        lv[k] = ok ? __ldcg(pl + 4 * (s0 + k)) : -INFINITY;
+        xv[k] = ok ? __ldcg(po + static_cast<int64_t>(s0 + k) * 512) : 0.f;
+      }
+      float mc = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) mc = fmaxf(mc, lv[k]);
+      const float mn = fmaxf(m, mc);
+      if (mn == -INFINITY) continue;
+      const float sc = m == -INFINITY ? 0.f : ex2_approx(m - mn);
+      osum *= sc;
+      wsum *= sc;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float f = lv[k] == -INFINITY ? 0.f : ex2_approx(lv[k] - mn);
+        wsum += f;
+        osum += f * xv[k];
+      }
+      m = mn;
+    }
+    const bool empty = !(wsum > 0.f);
+    const float ov = empty ? 0.f : osum / wsum;
+    const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+    if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
+    else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
+    if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
+  }
+}
+
 template <int NTHREADS, int NWARPS>
 __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s,
                                            const float* wm, const float* wl, const float* wacc,
@@ -108,7 +154,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
       if (dim == 0) a.part_l[pi] = L2;
     }
   }
-  if (a.S == 1) return;
+  if (a.S == 1 || a.merge_kernel) return;
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = (atomicAdd(&a.counter[unit], 1u) == static_cast<uint32_t>(a.S - 1));
@@ -116,45 +162,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
   if (!s_last) return;
   __threadfence();
-  // merge in chunks of 32 splits: all 2 x 32 loads of a chunk are issued before any use (one
-  // memory round trip per chunk), then the fixed-order log-sum-exp combine s = 0..S-1
-  for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
-    const int g = idx >> 7, dim = idx & 127;
-    if (g >= a.G) continue;
-    const float* pl = a.part_l + unit * a.S * 4 + g;
-    const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
-    float m = -INFINITY, wsum = 0.f, osum = 0.f;
-    for (int s0 = 0; s0 < a.S; s0 += 32) {
-      float lv[32], xv[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const bool ok = s0 + k < a.S;
-        lv[k] = ok ? __ldcg(pl + 4 * (s0 + k)) : -INFINITY;
-        xv[k] = ok ? __ldcg(po + static_cast<int64_t>(s0 + k) * 512) : 0.f;
-      }
-      float mc = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) mc = fmaxf(mc, lv[k]);
-      const float mn = fmaxf(m, mc);
-      if (mn == -INFINITY) continue;
-      const float sc = m == -INFINITY ? 0.f : ex2_approx(m - mn);
-      osum *= sc;
-      wsum *= sc;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const float f = lv[k] == -INFINITY ? 0.f : ex2_approx(lv[k] - mn);
-        wsum += f;
-        osum += f * xv[k];
-      }
-      m = mn;
-    }
-    const bool empty = !(wsum > 0.f);
-    const float ov = empty ? 0.f : osum / wsum;
-    const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
-    if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
-    else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-    if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
-  }
+  merge_splits<NTHREADS>(a, b, h);
   if (tid == 0) a.counter[unit] = 0u;  // ready for the next launch
 }
 

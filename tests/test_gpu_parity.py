@@ -370,3 +370,20 @@ def test_decode_step_append_outside_attended_range():
     _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))      # old cache attended
     kk, _ = ref.encode_kv(kn[0, 3], vn[0, 3], CB["inv_lambda"][3], c["ck"][3], c["cv"][3])
     assert np.array_equal(kcodes[0, 3, 550].cpu().numpy(), kk.astype(np.uint8))
+
+
+def test_decode_step_many_units_uses_separate_append():
+    """Multi-wave grids run the append as its own launch inside vecinfer_decode_step; same result."""
+    B, n = 40, 64
+    c = _attn_case(B, 8, 4, n + 2, [n] * B, seed=90)
+    kn = synth.gen_keys(1, 8, 128, seed=91, batch=B)[:, 0]
+    vn = synth.gen_values(1, 8, 128, seed=92, batch=B)[:, 0]
+    kcodes, vcodes = t_u8(c["kc"]), t_u8(c["vc"])
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(c["ck"]), t_bf16(c["cv"]), kcodes, vcodes, t_i32([n - 1] * B), t_i32([n] * B))
+    for b in range(B):
+        for h in range(8):
+            kk, vv = ref.encode_kv(kn[b, h], vn[b, h], CB["inv_lambda"][h], c["ck"][h], c["cv"][h])
+            c["kc"][b, h, n - 1], c["vc"][b, h, n - 1] = kk, vv
+    assert np.array_equal(kcodes.cpu().numpy(), c["kc"].astype(np.uint8))
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))
