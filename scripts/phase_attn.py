@@ -57,12 +57,19 @@ def main():
         st(rel[:, 1] - rel[:, 0], "prologue (fill+q~+sync)")
         st(rel[:, 2] - rel[:, 1], "main loop (incl. bq frags)")
         st(rel[:, 3] - rel[:, 2], "warp partials -> smem")
+        if S > 1 and t[:, 6].max() > 0:
+            st(rel[:, 6] - rel[:, 3], "combine + partial store")
+            st(rel[:, 7] - rel[:, 6], "threadfence + syncthreads")
+            st(rel[:, 5] - rel[:, 7], "atomic + syncthreads")
         if S > 1:
             st(rel[:, 5] - rel[:, 3], "combine+publish+fence+atomic")
             last = t[:, 4] - t[:, 5] > 0
             st((rel[:, 4] - rel[:, 5]), "merge (all CTAs)")
             print(f"   last-CTA merges: {int(last.sum())}, exit max {rel[:, 4].max():.2f}")
         st(rel[:, 4], "CTA end (rel)")
+        if S > 1:
+            last = rel[:, 4] > rel[:, 5]
+            print(f"   last CTAs: atomic done at {np.sort(rel[last, 5])[-3:]}, exit at {np.sort(rel[last, 4])[-3:]}")
 
 
 if __name__ == "__main__":
