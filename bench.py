@@ -387,6 +387,11 @@ def run_ours(args, rank, world, local_rank):
     e2e_value = total_bytes / (e2e_ms / 1e3) / 1e9
     peak, peak_src = load_peaks()
     attn_avg_ms = float(np.mean(attn_ms))
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r01", f"attn_{args.workload}_traffic.json")
+    if os.path.exists(tp):   # dram__bytes_read.sum + dram__bytes_write.sum per launch, committed ncu capture
+        with open(tp) as f:
+            traffic = json.load(f)["traffic_per_launch"]
     achieved = code_bytes_rank / (attn_avg_ms / 1e3) / 1e9
     step_ms = elapsed_ms / K
     cpu = None
@@ -408,7 +413,7 @@ def run_ours(args, rank, world, local_rank):
         "us_per_layer_call": step_ms * 1e3 / L,
         "tokens_per_s": B_glob * 1e3 / step_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "attn_mma8_kernel (vecinfer_attn_decode)",
+                     "traffic": traffic, "kernel": "attn_mma8_kernel (vecinfer_attn_decode)",
                      "attn_us_avg": attn_avg_ms * 1e3, "attn_us_p10": float(np.percentile(attn_ms, 10)) * 1e3,
                      "attn_us_p90": float(np.percentile(attn_ms, 90)) * 1e3,
                      "timing": "CUDA events around K replays of a graph of the 32 layers' vecinfer_attn_decode launches "
