@@ -156,14 +156,12 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   }
   if (a.S == 1 || a.merge_kernel) return;
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 6);
-  __threadfence();
   __syncthreads();
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 7);
-  if (tid == 0) s_last = (atomicAdd(&a.counter[unit], 1u) == static_cast<uint32_t>(a.S - 1));
+  if (tid == 0) s_last = (atom_add_acq_rel_gpu(&a.counter[unit], 1u) == static_cast<uint32_t>(a.S - 1));
   __syncthreads();
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
   if (!s_last) return;
-  __threadfence();
   merge_splits<NTHREADS>(a, b, h);
   if (tid == 0) a.counter[unit] = 0u;  // ready for the next launch
 }

@@ -258,11 +258,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
       else load_tile_tail(nxt, kp, vp, rem, r, j);
     }
 
-    // ---- scores (log2 units) for tile tokens 16q + {r, r+8}, head j
+    // ---- scores (log2 units) for tile tokens 16q + {r, r+8}, head j; two independent MMA
+    // accumulator chains per sub-tile (k-steps 0-3 and 4-7) halve the dependent HMMA latency
     float sc[2][2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      float d[4] = {0.f, 0.f, 0.f, 0.f};
+      float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const uint32_t wa = t < 4 ? cur.k[q][0].x : cur.k[q][0].y;
@@ -274,10 +275,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
           case 2: ea = lds_u64(gaddr<2>(wa, kbase)); eb = lds_u64(gaddr<2>(wb, kbase)); break;
           default: ea = lds_u64(gaddr<3>(wa, kbase)); eb = lds_u64(gaddr<3>(wb, kbase)); break;
         }
-        mma_16816(d, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
+        if (t < 4) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
+        else mma_16816(d1, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
       }
-      sc[q][0] = d[0] + d[1];
-      sc[q][1] = d[2] + d[3];
+      sc[q][0] = (d0[0] + d1[0]) + (d0[1] + d1[1]);
+      sc[q][1] = (d0[2] + d1[2]) + (d0[3] + d1[3]);
     }
     if (rem_cur < 32) {
 #pragma unroll
@@ -287,13 +289,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
       }
     }
 
-    // ---- online softmax (Alg. 1 l.12-13, 18), lazy rescale
+    // ---- online softmax (Alg. 1 l.12-13, 18), lazy rescale.  Common path: every lane checks its
+    // own 4 scores against m_run + tau (p <= 2^tau) -- no cross-lane traffic; only when some lane
+    // exceeds it are the per-head tile maxima reduced and the accumulators rescaled.
     float mx = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-    const bool need = mx > m_run + kTau;
-    if (__any_sync(0xffffffffu, need)) {
+    if (__any_sync(0xffffffffu, mx > m_run + kTau)) {
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      const bool need = mx > m_run + kTau;           // uniform across the 8 lanes of head j
       const float m_new = need ? mx : m_run;
       const float alpha = need ? ex2_approx(m_run - m_new) : 1.f;  // 0 when m_run was -inf
 #pragma unroll
