@@ -31,7 +31,9 @@ int merge_mode_from_env() {
 constexpr int kMaxSplits = 128;
 constexpr int64_t kMinTokensPerSplit = 512;
 
-bool vq_ok(const vecinfer_vq_t& c) { return c.head_dim == 128 && c.sub_dim == 4 && c.code_bits == 8; }
+bool vq_ok(const vecinfer_vq_t& c) {
+  return c.head_dim == 128 && c.sub_dim == 4 && (c.code_bits == 4 || c.code_bits == 8 || c.code_bits == 16);
+}
 
 struct WsLayout {
   size_t part_o, part_l, counter, total;
@@ -136,7 +138,9 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   const int G = H_q / H_kv;
   if (G != 1 && G != 2 && G != 4) return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: GQA group %d not in {1,2,4}", G);
   if (!vq_ok(kcfg) || !vq_ok(vcfg))
-    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: supported config is b2d4 (D=128, d=4, 8-bit codes)");
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: supported configs are D=128, d=4, code_bits in {4,8,16}");
+  if (algo == VECINFER_ATTN_LUT && (kcfg.code_bits != 8 || vcfg.code_bits != 8))
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: the LUT variant is implemented for b2d4 only");
   if (tok_begin < 0 || (tok_end >= 0 && tok_end < tok_begin))
     return fail(VECINFER_ERR_SHAPE, "attn_decode: bad token range [%lld, %lld)", (long long)tok_begin, (long long)tok_end);
   if (!(softmax_scale > 0.f) || !isfinite(softmax_scale)) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: softmax_scale must be finite > 0");
@@ -241,7 +245,7 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
   // Fuse only when the grid is one wave: the owner CTA's encode latency (~1-2 us) then hides
   // behind the other CTAs' longer splits; with several waves every wave would carry it, and a
   // separate append launch (latency ~3 us, once) is cheaper.
-  bool fuse = algo != VECINFER_ATTN_LUT;
+  bool fuse = algo != VECINFER_ATTN_LUT && kcfg.code_bits <= 8 && vcfg.code_bits <= 8;
   if (fuse && B > 0 && H_kv > 0) {
     const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
     const int64_t units = static_cast<int64_t>(B) * H_kv;

@@ -29,26 +29,100 @@ namespace {
 constexpr int kNW = 16;            // warps per CTA (1 CTA per SM)
 constexpr int kThreads = kNW * 32;
 constexpr float kTau = 8.0f;       // lazy-rescale threshold (log2 units): p <= 2^8
-constexpr int kRowBytes = 32;      // 8-bit codes, D/d = 32 sub-vectors
 constexpr int kTab = 65536;        // [256 centroids][256 B] codebook table, 64 KiB-aligned
 // misc region (below the table): q~ [4][128] f32, warp partials, staged split partials
 constexpr int kMiscQ = 0;
-constexpr int kMiscNew = 2048;                       // 64 B: codes of the appended token (fused append)
+constexpr int kMiscNew = 2048;                       // 128 B: codes of the appended token (K at +0, V at +64)
 constexpr int kMiscW = 2176;                         // wm[16][4], wl[16][4], wacc[16][4][128]
 constexpr int kMiscBytes = kMiscW + (kNW * 8 + kNW * 4 * 128) * 4;   // 35328
 constexpr int kClusterMax = 16;                      // DSMEM merge buffer: [16][4][128] + m, l
 constexpr int kCbufBytes = kClusterMax * 4 * 130 * 4;
 constexpr int kSmemBytes = 65536 + kTab + kCbufBytes + 1024;  // pad + table + cluster buffer + slack
 
+// ---- code-width traits.  Per lane and token: the K chunk holds sub-vectors 8j..8j+7 (score MMA
+// k-steps), the V chunk sub-vectors 4r..4r+3 (P.V m-tiles).  4/8-bit codebooks are gathered from the
+// shared table (rows of 256 B: [16 K replicas | 16 V replicas]); 16-bit codebooks (65536 x 4 bf16 =
+// 512 KiB) do not fit shared memory and are gathered from global memory (L2/L1 resident).
+template <int BITS> struct Fmt;
+template <> struct Fmt<8> {
+  static constexpr int kRow = 32, kOffK = 8, kOffV = 4;
+  static constexpr bool kSmem = true;
+  using K = uint2;
+  using V = uint32_t;
+  static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u64(p); }
+  static __device__ __forceinline__ V ldv(const uint8_t* p) { return ldg_nc_u32(p); }
+  static __device__ __forceinline__ K zk() { return make_uint2(0u, 0u); }
+  // shared address of the centroid of code T of the chunk: code byte -> address bits 8..15 (PRMT)
+  template <int T> static __device__ __forceinline__ uint32_t kaddr(const K& c, uint32_t base) {
+    return prmt(T < 4 ? c.x : c.y, base, 0x7604u | ((T & 3) << 4));
+  }
+  template <int U> static __device__ __forceinline__ uint32_t vaddr(V c, uint32_t base) {
+    return prmt(c, base, 0x7604u | (U << 4));
+  }
+};
+template <> struct Fmt<4> {
+  static constexpr int kRow = 16, kOffK = 4, kOffV = 2;
+  static constexpr bool kSmem = true;
+  using K = uint32_t;
+  using V = uint32_t;   // low 16 bits
+  static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u32(p); }
+  static __device__ __forceinline__ V ldv(const uint8_t* p) { return ldg_nc_u16(p); }
+  static __device__ __forceinline__ K zk() { return 0u; }
+  template <int T> static __device__ __forceinline__ uint32_t nib8(uint32_t w) {   // nibble T -> bits 8..11
+    return T >= 2 ? ((w >> (4 * T - 8)) & 0xF00u) : ((w << (8 - 4 * T)) & 0xF00u);
+  }
+  template <int T> static __device__ __forceinline__ uint32_t kaddr(K c, uint32_t base) { return nib8<T>(c) | base; }
+  template <int U> static __device__ __forceinline__ uint32_t vaddr(V c, uint32_t base) { return nib8<U>(c) | base; }
+};
+template <> struct Fmt<16> {
+  static constexpr int kRow = 64, kOffK = 16, kOffV = 8;
+  static constexpr bool kSmem = false;
+  using K = uint4;
+  using V = uint2;
+  static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u128(p); }
+  static __device__ __forceinline__ V ldv(const uint8_t* p) { return ldg_nc_u64(p); }
+  static __device__ __forceinline__ K zk() { return make_uint4(0u, 0u, 0u, 0u); }
+  template <int T> static __device__ __forceinline__ uint32_t kidx(const K& c) {
+    const uint32_t w = T < 2 ? c.x : T < 4 ? c.y : T < 6 ? c.z : c.w;
+    return (T & 1) ? (w >> 16) : (w & 0xFFFFu);
+  }
+  template <int U> static __device__ __forceinline__ uint32_t vidx(const V& c) {
+    const uint32_t w = U < 2 ? c.x : c.y;
+    return (U & 1) ? (w >> 16) : (w & 0xFFFFu);
+  }
+};
+template <int BITS> using KCode = typename Fmt<BITS>::K;
+template <int BITS> using VCode = typename Fmt<BITS>::V;
+
+// bf16x4 centroid (global) -> fp16x4 MMA operand pair (exact for |c| in the fp16 normal range)
+__device__ __forceinline__ uint2 bf16x4_to_f16x4(uint2 w) {
+  uint2 e;
+  e.x = pack_half2(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u));
+  e.y = pack_half2(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+  return e;
+}
+
+template <int KB, int T>
+__device__ __forceinline__ uint2 gather_k(const KCode<KB>& c, uint32_t kbase, const uint16_t* cbk) {
+  if constexpr (Fmt<KB>::kSmem) return lds_u64(Fmt<KB>::template kaddr<T>(c, kbase));
+  else return bf16x4_to_f16x4(ldg_ro_u64(cbk + 4 * Fmt<KB>::template kidx<T>(c)));
+}
+template <int VB, int U>
+__device__ __forceinline__ uint2 gather_v(const VCode<VB>& c, uint32_t vbase, const uint16_t* cbv) {
+  if constexpr (Fmt<VB>::kSmem) return lds_u64(Fmt<VB>::template vaddr<U>(c, vbase));
+  else return bf16x4_to_f16x4(ldg_ro_u64(cbv + 4 * Fmt<VB>::template vidx<U>(c)));
+}
+
+template <int KB, int VB>
 __device__ __forceinline__ void fill_tables(unsigned char* tab, const uint16_t* ck, const uint16_t* cv, int tid) {
   // thread t: centroid j = t/2 of C_k (t even) or C_v (t odd); 16 replicas = 8 x 16-byte stores,
   // rotated so that the 8 threads of a quarter-warp hit 8 different bank groups
   const int j = tid >> 1, which = tid & 1;
+  const int n = which ? (VB <= 8 ? (1 << VB) : 0) : (KB <= 8 ? (1 << KB) : 0);
+  if (j >= n) return;
   const uint16_t* src = (which ? cv : ck) + 4 * j;
-  const uint2 w = *reinterpret_cast<const uint2*>(src);
-  const uint32_t e0 = pack_half2(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u));
-  const uint32_t e1 = pack_half2(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
-  const uint4 v = make_uint4(e0, e1, e0, e1);
+  const uint2 e = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(src));
+  const uint4 v = make_uint4(e.x, e.y, e.x, e.y);
   unsigned char* row = tab + j * 256 + which * 128;
 #pragma unroll
   for (int u0 = 0; u0 < 8; ++u0) {
@@ -57,46 +131,59 @@ __device__ __forceinline__ void fill_tables(unsigned char* tab, const uint16_t* 
   }
 }
 
-// shared address of centroid (byte k of w) for this lane: one PRMT
-template <int K>
-__device__ __forceinline__ uint32_t gaddr(uint32_t w, uint32_t base) {
-  return prmt(w, base, 0x7604u | (K << 4));
-}
-
+template <int KB, int VB>
 struct TileCodes {
-  uint2 k[2][2];     // [sub-tile][row r / r+8]: 8 key codes (sub-vectors 8j..8j+7)
-  uint32_t v[2][4];  // [sub-tile][token 2j, 2j+1, 2j+8, 2j+9]: 4 value codes (sub-vectors 4r..4r+3)
+  KCode<KB> k[2][2];  // [sub-tile][row r / r+8]
+  VCode<VB> v[2][4];  // [sub-tile][token 2j, 2j+1, 2j+8, 2j+9]
 };
 
 // kp/vp point at this lane's bytes of token (tile start + r) / (tile start + 2j) respectively
-__device__ __forceinline__ void load_tile_full(TileCodes& tc, const uint8_t* kp, const uint8_t* vp) {
+template <int KB, int VB>
+__device__ __forceinline__ void load_tile_full(TileCodes<KB, VB>& tc, const uint8_t* kp, const uint8_t* vp) {
+  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    tc.k[q][0] = ldg_nc_u64(kp + (16 * q) * kRowBytes);
-    tc.k[q][1] = ldg_nc_u64(kp + (16 * q + 8) * kRowBytes);
-    tc.v[q][0] = ldg_nc_u32(vp + (16 * q) * kRowBytes);
-    tc.v[q][1] = ldg_nc_u32(vp + (16 * q + 1) * kRowBytes);
-    tc.v[q][2] = ldg_nc_u32(vp + (16 * q + 8) * kRowBytes);
-    tc.v[q][3] = ldg_nc_u32(vp + (16 * q + 9) * kRowBytes);
+    tc.k[q][0] = Fmt<KB>::ldk(kp + (16 * q) * KR);
+    tc.k[q][1] = Fmt<KB>::ldk(kp + (16 * q + 8) * KR);
+    tc.v[q][0] = Fmt<VB>::ldv(vp + (16 * q) * VR);
+    tc.v[q][1] = Fmt<VB>::ldv(vp + (16 * q + 1) * VR);
+    tc.v[q][2] = Fmt<VB>::ldv(vp + (16 * q + 8) * VR);
+    tc.v[q][3] = Fmt<VB>::ldv(vp + (16 * q + 9) * VR);
   }
 }
 
 // ragged last tile: rem = tokens left in the split (1..31), rows beyond it read as code 0
-__device__ __forceinline__ void load_tile_tail(TileCodes& tc, const uint8_t* kp, const uint8_t* vp, int rem, int r,
-                                               int j) {
+template <int KB, int VB>
+__device__ __forceinline__ void load_tile_tail(TileCodes<KB, VB>& tc, const uint8_t* kp, const uint8_t* vp, int rem,
+                                               int r, int j) {
+  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    tc.k[q][0] = (16 * q + r < rem) ? ldg_nc_u64(kp + (16 * q) * kRowBytes) : make_uint2(0u, 0u);
-    tc.k[q][1] = (16 * q + r + 8 < rem) ? ldg_nc_u64(kp + (16 * q + 8) * kRowBytes) : make_uint2(0u, 0u);
+    tc.k[q][0] = (16 * q + r < rem) ? Fmt<KB>::ldk(kp + (16 * q) * KR) : Fmt<KB>::zk();
+    tc.k[q][1] = (16 * q + r + 8 < rem) ? Fmt<KB>::ldk(kp + (16 * q + 8) * KR) : Fmt<KB>::zk();
     const int t0 = 16 * q + 2 * j;
-    tc.v[q][0] = (t0 < rem) ? ldg_nc_u32(vp + (16 * q) * kRowBytes) : 0u;
-    tc.v[q][1] = (t0 + 1 < rem) ? ldg_nc_u32(vp + (16 * q + 1) * kRowBytes) : 0u;
-    tc.v[q][2] = (t0 + 8 < rem) ? ldg_nc_u32(vp + (16 * q + 8) * kRowBytes) : 0u;
-    tc.v[q][3] = (t0 + 9 < rem) ? ldg_nc_u32(vp + (16 * q + 9) * kRowBytes) : 0u;
+    tc.v[q][0] = (t0 < rem) ? Fmt<VB>::ldv(vp + (16 * q) * VR) : VCode<VB>{};
+    tc.v[q][1] = (t0 + 1 < rem) ? Fmt<VB>::ldv(vp + (16 * q + 1) * VR) : VCode<VB>{};
+    tc.v[q][2] = (t0 + 8 < rem) ? Fmt<VB>::ldv(vp + (16 * q + 8) * VR) : VCode<VB>{};
+    tc.v[q][3] = (t0 + 9 < rem) ? Fmt<VB>::ldv(vp + (16 * q + 9) * VR) : VCode<VB>{};
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a) {
+// store the packed code of sub-vector `lane` (4/8-bit) for the fused append
+template <int BITS>
+__device__ __forceinline__ void put_code(unsigned char* row, int lane, uint32_t code) {
+  if constexpr (BITS == 8) {
+    row[lane] = static_cast<uint8_t>(code);
+  } else {
+    const uint32_t hi = __shfl_xor_sync(0xffffffffu, code, 1);
+    if ((lane & 1) == 0) row[lane >> 1] = static_cast<uint8_t>(code | (hi << 4));
+  }
+}
+
+template <int KB, int VB>
+__global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
+  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
+  constexpr bool kCanAppend = KB <= 8 && VB <= 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -114,7 +201,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
 
   // static weights first (codebooks): with programmatic dependent launch this overlaps the
   // tail of the previous kernel on the stream; everything dynamic is read after the wait
-  fill_tables(tab, a.ck + h * a.ck_hs, a.cv + h * a.cv_hs, tid);
+  const uint16_t* cbk = a.ck + h * a.ck_hs;
+  const uint16_t* cbv = a.cv + h * a.cv_hs;
+  fill_tables<KB, VB>(tab, cbk, cbv, tid);
   griddep_wait();
 
   int64_t r0, r1, beg, e;
@@ -126,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   bool owner = false;
   int patch_tile = -1, patch_row = 0;
   int64_t p_row = 0;
-  if (a.append) {
+  if (kCanAppend && a.append) {
     p_row = a.write_pos[b];
     const bool in_range = p_row >= beg && p_row < e;
     owner = in_range ? (p_row >= r0 && p_row < r1) : (s == 0);
@@ -136,28 +225,29 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
     }
   }
   // lane-resolved code pointers of this warp's first tile
-  const uint8_t* kp = a.kcodes + (unit * a.n_cap + r0 + 32 * warp + r) * kRowBytes + 8 * j;
-  const uint8_t* vp = a.vcodes + (unit * a.n_cap + r0 + 32 * warp + 2 * j) * kRowBytes + 4 * r;
-  constexpr int kStep = 32 * kNW * kRowBytes;  // bytes between a warp's consecutive tiles
+  const uint8_t* kp = a.kcodes + (unit * a.n_cap + r0 + 32 * warp + r) * KR + Fmt<KB>::kOffK * j;
+  const uint8_t* vp = a.vcodes + (unit * a.n_cap + r0 + 32 * warp + 2 * j) * VR + Fmt<VB>::kOffV * r;
+  constexpr int kStepK = 32 * kNW * KR, kStepV = 32 * kNW * VR;  // bytes between a warp's tiles
 
   // first tile's loads go out before the query transform so HBM latency overlaps it
-  TileCodes nxt;
+  TileCodes<KB, VB> nxt;
   if (warp < ntile) {
     const int rem = ntok - 32 * warp;
     if (rem >= 32) load_tile_full(nxt, kp, vp);
     else load_tile_tail(nxt, kp, vp, rem, r, j);
   }
-  unsigned char* newcodes = smem_raw + kMiscNew;   // [0,32): K codes, [32,64): V codes
-  if (owner) {
+  unsigned char* newcodes = smem_raw + kMiscNew;   // [0,64): K code row, [64,128): V code row
+  if (kCanAppend && owner) {
     // Eq. 9: encode the new token (S then H on the key, VQ on both), 8 warps per stream, each
-    // scanning 32 centroids (bf16 codebook -> fp32, pinned distance, lowest index on ties)
+    // scanning 1/8 of the centroids (bf16 codebook -> fp32, pinned distance, lowest index on ties)
     const bool isv = warp >= 8;
     const int w8 = warp & 7;
+    const int P = (isv ? (1 << (VB <= 8 ? VB : 8)) : (1 << (KB <= 8 ? KB : 8))) / 8;   // centroids per warp
     float4* stage = reinterpret_cast<float4*>(smem_raw + kMiscW);
     float* sbest = reinterpret_cast<float*>(smem_raw + kMiscW + 8192);
     uint32_t* sidx = reinterpret_cast<uint32_t*>(smem_raw + kMiscW + 10240);
-    const uint16_t* cb = isv ? (a.cv + h * a.cv_hs) : (a.ck + h * a.ck_hs);
-    stage[warp * 32 + lane] = bf16x4_to_float4(*reinterpret_cast<const uint2*>(cb + 4 * (32 * w8 + lane)));
+    const uint16_t* cb = isv ? cbv : cbk;
+    if (lane < P) stage[warp * 32 + lane] = bf16x4_to_float4(*reinterpret_cast<const uint2*>(cb + 4 * (P * w8 + lane)));
     float x[4];
     if (!isv) {
       const bool bad = key_transform_lane(a.knew + b * a.kn_sb + h * a.kn_sh + 4 * lane,
@@ -171,17 +261,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
     float best = __int_as_float(0x7f800000);
     uint32_t bi = 0;
 #pragma unroll 8
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < P; ++i) {
       const float4 c = stage[warp * 32 + i];
       const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
-      if (dd < best) { best = dd; bi = 32 * w8 + i; }
+      if (dd < best) { best = dd; bi = P * w8 + i; }
     }
     sbest[warp * 32 + lane] = best;
     sidx[warp * 32 + lane] = bi;
   }
   if (warp < 4) query_transform_warp(a, b, h, warp, sq + 128 * warp);
   __syncthreads();
-  if (owner) {
+  if (kCanAppend && owner) {
     if (warp == 0 || warp == 8) {
       const float* sbest = reinterpret_cast<const float*>(smem_raw + kMiscW + 8192);
       const uint32_t* sidx = reinterpret_cast<const uint32_t*>(smem_raw + kMiscW + 10240);
@@ -192,10 +282,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
         const float c = sbest[(warp + w) * 32 + lane];
         if (c < bb) { bb = c; ii = sidx[(warp + w) * 32 + lane]; }
       }
-      newcodes[(warp >> 3) * 32 + lane] = static_cast<uint8_t>(ii);
+      if (warp == 0) put_code<(KB <= 8 ? KB : 8)>(newcodes, lane, ii);
+      else put_code<(VB <= 8 ? VB : 8)>(newcodes + 64, lane, ii);
       if (p_row >= 0 && p_row < a.n_cap) {
-        uint8_t* dst = (warp == 0 ? a.kcodes_w : a.vcodes_w) + (unit * a.n_cap + p_row) * kRowBytes;
-        dst[lane] = static_cast<uint8_t>(ii);
+        if (warp == 0) put_code<(KB <= 8 ? KB : 8)>(a.kcodes_w + (unit * a.n_cap + p_row) * KR, lane, ii);
+        else put_code<(VB <= 8 ? VB : 8)>(a.vcodes_w + (unit * a.n_cap + p_row) * VR, lane, ii);
       } else if (lane == 0 && a.err) {
         atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
       }
@@ -233,10 +324,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
   float m_run = -INFINITY, l_run = 0.f;
 
   for (int it = warp; it < ntile; it += kNW) {
-    TileCodes cur = nxt;
-    if (it == patch_tile) {   // the appended row: use the codes just encoded (not the stale load)
-      const uint2 nk = *reinterpret_cast<const uint2*>(newcodes + 8 * j);
-      const uint32_t nv = *reinterpret_cast<const uint32_t*>(newcodes + 32 + 4 * r);
+    TileCodes<KB, VB> cur = nxt;
+    if constexpr (kCanAppend) {
+    if (it == patch_tile) {   // the appended row: codes just encoded, not the stale load
+      KCode<KB> nk;
+      VCode<VB> nv;
+      if constexpr (KB == 8) nk = *reinterpret_cast<const uint2*>(newcodes + 8 * j);
+      else nk = *reinterpret_cast<const uint32_t*>(newcodes + Fmt<(KB <= 8 ? KB : 8)>::kOffK * j);
+      if constexpr (VB == 8) nv = *reinterpret_cast<const uint32_t*>(newcodes + 64 + 4 * r);
+      else nv = *reinterpret_cast<const uint16_t*>(newcodes + 64 + Fmt<(VB <= 8 ? VB : 8)>::kOffV * r);
       const int qp = patch_row >> 4, rr = patch_row & 15;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -249,10 +345,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
         if (2 * j + 9 == rr) cur.v[q][3] = nv;
       }
     }
+    }
     const int rem_cur = ntok - 32 * it;
     if (it + kNW < ntile) {
-      kp += kStep;
-      vp += kStep;
+      kp += kStepK;
+      vp += kStepV;
       const int rem = rem_cur - 32 * kNW;
       if (rem >= 32) load_tile_full(nxt, kp, vp);
       else load_tile_tail(nxt, kp, vp, rem, r, j);
@@ -264,20 +361,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const uint32_t wa = t < 4 ? cur.k[q][0].x : cur.k[q][0].y;
-        const uint32_t wb = t < 4 ? cur.k[q][1].x : cur.k[q][1].y;
-        uint2 ea, eb;
-        switch (t & 3) {
-          case 0: ea = lds_u64(gaddr<0>(wa, kbase)); eb = lds_u64(gaddr<0>(wb, kbase)); break;
-          case 1: ea = lds_u64(gaddr<1>(wa, kbase)); eb = lds_u64(gaddr<1>(wb, kbase)); break;
-          case 2: ea = lds_u64(gaddr<2>(wa, kbase)); eb = lds_u64(gaddr<2>(wb, kbase)); break;
-          default: ea = lds_u64(gaddr<3>(wa, kbase)); eb = lds_u64(gaddr<3>(wb, kbase)); break;
-        }
+      static_for<0, 8>([&](auto T) {
+        constexpr int t = decltype(T)::value;
+        const uint2 ea = gather_k<KB, t>(cur.k[q][0], kbase, cbk);
+        const uint2 eb = gather_k<KB, t>(cur.k[q][1], kbase, cbk);
         if (t < 4) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
         else mma_16816(d1, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
-      }
+      });
       sc[q][0] = (d0[0] + d1[0]) + (d0[1] + d1[1]);
       sc[q][1] = (d0[2] + d1[2]) + (d0[3] + d1[3]);
     }
@@ -324,28 +414,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
       const uint32_t bp1 = movmatrix_trans(prmt(hb, lb, 0x7632));  // (hi, lo) of token r + 8
 
       // ---- P.V (Alg. 1 l.16): m-tile t <-> sub-vector 4r + t/2, components 2(t%2) + {0,1}
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        uint2 g0, g1, g2, g3;
-        switch (u) {
-          case 0:
-            g0 = lds_u64(gaddr<0>(cur.v[q][0], vbase)); g1 = lds_u64(gaddr<0>(cur.v[q][1], vbase));
-            g2 = lds_u64(gaddr<0>(cur.v[q][2], vbase)); g3 = lds_u64(gaddr<0>(cur.v[q][3], vbase)); break;
-          case 1:
-            g0 = lds_u64(gaddr<1>(cur.v[q][0], vbase)); g1 = lds_u64(gaddr<1>(cur.v[q][1], vbase));
-            g2 = lds_u64(gaddr<1>(cur.v[q][2], vbase)); g3 = lds_u64(gaddr<1>(cur.v[q][3], vbase)); break;
-          case 2:
-            g0 = lds_u64(gaddr<2>(cur.v[q][0], vbase)); g1 = lds_u64(gaddr<2>(cur.v[q][1], vbase));
-            g2 = lds_u64(gaddr<2>(cur.v[q][2], vbase)); g3 = lds_u64(gaddr<2>(cur.v[q][3], vbase)); break;
-          default:
-            g0 = lds_u64(gaddr<3>(cur.v[q][0], vbase)); g1 = lds_u64(gaddr<3>(cur.v[q][1], vbase));
-            g2 = lds_u64(gaddr<3>(cur.v[q][2], vbase)); g3 = lds_u64(gaddr<3>(cur.v[q][3], vbase)); break;
-        }
+      static_for<0, 4>([&](auto U) {
+        constexpr int u = decltype(U)::value;
+        const uint2 g0 = gather_v<VB, u>(cur.v[q][0], vbase, cbv);
+        const uint2 g1 = gather_v<VB, u>(cur.v[q][1], vbase, cbv);
+        const uint2 g2 = gather_v<VB, u>(cur.v[q][2], vbase, cbv);
+        const uint2 g3 = gather_v<VB, u>(cur.v[q][3], vbase, cbv);
         mma_16816(acc[2 * u], prmt(g0.x, g1.x, 0x5410), prmt(g0.x, g1.x, 0x7632), prmt(g2.x, g3.x, 0x5410),
                   prmt(g2.x, g3.x, 0x7632), bp0, bp1);
         mma_16816(acc[2 * u + 1], prmt(g0.y, g1.y, 0x5410), prmt(g0.y, g1.y, 0x7632), prmt(g2.y, g3.y, 0x5410),
                   prmt(g2.y, g3.y, 0x7632), bp0, bp1);
-      }
+      });
     }
   }
 
@@ -428,11 +507,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma8_kernel(const AttnArgs a
 
 }  // namespace
 
+using AttnKernel = void (*)(const AttnArgs);
+
+static AttnKernel kernel_for(int kb, int vb) {
+  const int ki = kb == 4 ? 0 : kb == 8 ? 1 : 2, vi = vb == 4 ? 0 : vb == 8 ? 1 : 2;
+  static const AttnKernel table[3][3] = {
+      {attn_mma_kernel<4, 4>, attn_mma_kernel<4, 8>, attn_mma_kernel<4, 16>},
+      {attn_mma_kernel<8, 4>, attn_mma_kernel<8, 8>, attn_mma_kernel<8, 16>},
+      {attn_mma_kernel<16, 4>, attn_mma_kernel<16, 8>, attn_mma_kernel<16, 16>}};
+  return table[ki][vi];
+}
+
 static void set_attrs_once() {
   static bool done = false;  // benign race: idempotent attributes
   if (!done) {
-    cudaFuncSetAttribute(attn_mma8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    cudaFuncSetAttribute(attn_mma8_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int kb : {4, 8, 16})
+      for (int vb : {4, 8, 16}) {
+        cudaFuncSetAttribute(kernel_for(kb, vb), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(kernel_for(kb, vb), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      }
     done = true;
   }
 }
@@ -454,7 +547,7 @@ int attn_mma_max_active_clusters(int cluster_size) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, attn_mma8_kernel, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, kernel_for(8, 8), &cfg) != cudaSuccess) {
       cudaGetLastError();
       n = 0;
     }
@@ -464,7 +557,6 @@ int attn_mma_max_active_clusters(int cluster_size) {
 }
 
 cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st) {
-  (void)kbits; (void)vbits;  // dispatch validated by the caller (8/8 only in v1)
   set_attrs_once();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.S, a.Hkv, a.B);
@@ -485,7 +577,7 @@ cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_
   }
   cfg.attrs = at;
   cfg.numAttrs = n;
-  return cudaLaunchKernelEx(&cfg, attn_mma8_kernel, a);
+  return cudaLaunchKernelEx(&cfg, kernel_for(kbits, vbits), a);
 }
 
 }  // namespace vecinfer

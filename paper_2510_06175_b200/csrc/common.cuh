@@ -7,6 +7,7 @@
 #include <stdint.h>
 #include <math.h>
 #include <utility>
+#include <type_traits>
 
 #include "../../include/vecinfer.h"
 
@@ -95,6 +96,27 @@ __device__ __forceinline__ uint4 ldg_nc_u128(const void* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
+}
+
+__device__ __forceinline__ uint32_t ldg_nc_u16(const void* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return static_cast<uint32_t>(v);
+}
+// read-only load that may allocate in L1 (codebook gathers)
+__device__ __forceinline__ uint2 ldg_ro_u64(const void* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+// compile-time unrolled loop: f(std::integral_constant<int, I>) for I in [B, E)
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
 }
 
 __device__ __forceinline__ uint2 lds_u64(uint32_t saddr) {

@@ -387,3 +387,75 @@ def test_decode_step_many_units_uses_separate_append():
             c["kc"][b, h, n - 1], c["vc"][b, h, n - 1] = kk, vv
     assert np.array_equal(kcodes.cpu().numpy(), c["kc"].astype(np.uint8))
     _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))
+
+
+# ------------------------------------------- bit-width sweep (BASELINE configs[4]) + mixed K/V
+CFGS = {4: vi.B1D4, 8: vi.B2D4, 16: vi.B4D4}
+CBNAME = {4: "b1d4", 8: "b2d4", 16: "b4d4"}
+
+
+def _bits_case(B, kb, vb, n_cap, lens, seed, G=4):
+    """Random codes at the given widths; per-head codebooks (b1d4/b2d4) or the shared b4d4 one."""
+    heads = np.arange(8)
+    ck = CB[f"ck_{CBNAME[kb]}"]
+    cv = CB[f"cv_{CBNAME[vb]}"]
+    kc = synth.gen_codes(n_cap, 8, 32, kb, seed=seed, batch=B)
+    vc = synth.gen_codes(n_cap, 8, 32, vb, seed=seed + 1, batch=B)
+    q = synth.gen_queries(B, 8 * G, 8, 128, seed=seed + 2)
+    return dict(q=q, lam=CB["lambda"][heads], ck=ck, cv=cv, kc=kc, vc=vc, seq_lens=np.asarray(lens), kb=kb, vb=vb)
+
+
+def _run_gpu_bits(c, **kw):
+    o, L = vi.attn_decode(t_bf16(c["q"]), t_f32(c["lam"]), t_bf16(c["ck"]), t_bf16(c["cv"]),
+                          t_u8(ref.pack_codes(c["kc"], c["kb"])), t_u8(ref.pack_codes(c["vc"], c["vb"])),
+                          t_i32(c["seq_lens"]), kcfg=CFGS[c["kb"]], vcfg=CFGS[c["vb"]], **kw)
+    return o.float().cpu().numpy(), L.cpu().numpy()
+
+
+@pytest.mark.parametrize("kb,vb", [(4, 4), (16, 16), (8, 4), (4, 8), (16, 8), (8, 16), (4, 16), (16, 4)])
+@pytest.mark.parametrize("splits", [0, 3])
+def test_attn_bitwidths(kb, vb, splits):
+    c = _bits_case(2, kb, vb, 800, [777, 100], seed=100 + kb + vb + splits)
+    o, L = _run_gpu_bits(c, num_splits=splits)
+    _assert_close(o, L, *_run_ref(c))
+
+
+@pytest.mark.parametrize("kb,vb", [(4, 4), (8, 4), (4, 8)])
+def test_decode_step_fused_bitwidths(kb, vb):
+    B, lens = 1, [1000]
+    c = _bits_case(B, kb, vb, 1003, lens, seed=120 + kb * vb)
+    kn = synth.gen_keys(1, 8, 128, seed=121, batch=B)[:, 0]
+    vn = synth.gen_values(1, 8, 128, seed=122, batch=B)[:, 0]
+    kcodes = t_u8(ref.pack_codes(c["kc"], kb))
+    vcodes = t_u8(ref.pack_codes(c["vc"], vb))
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(c["ck"]), t_bf16(c["cv"]), kcodes, vcodes, t_i32([999]), t_i32(lens),
+                          kcfg=CFGS[kb], vcfg=CFGS[vb])
+    for h in range(8):
+        kk, vv = ref.encode_kv(kn[0, h], vn[0, h], CB["inv_lambda"][h], c["ck"][h], c["cv"][h])
+        c["kc"][0, h, 999], c["vc"][0, h, 999] = kk, vv
+    assert np.array_equal(kcodes.cpu().numpy(), ref.pack_codes(c["kc"], kb))
+    assert np.array_equal(vcodes.cpu().numpy(), ref.pack_codes(c["vc"], vb))
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))
+
+
+@pytest.mark.parametrize("bits", [4, 16])
+def test_cfg5_full_size_sampled_units(bits):
+    """BASELINE configs[4] at full size (N = 65536, 8 KV heads) for b1d4 / b4d4, sampled units."""
+    N = 65536
+    rng = np.random.default_rng(bits)
+    row = 32 * bits // 8
+    kc = synth.gen_codes_torch((1, 8, N, row), bits, seed=bits, device=DEV)
+    vc = synth.gen_codes_torch((1, 8, N, row), bits, seed=bits + 1, device=DEV)
+    q = synth.gen_queries(1, 32, 8, 128, seed=bits + 2)
+    ck, cv = CB[f"ck_{CBNAME[bits]}"], CB[f"cv_{CBNAME[bits]}"]
+    o, L = vi.attn_decode(t_bf16(q), t_f32(CB["lambda"]), t_bf16(ck), t_bf16(cv), kc, vc, t_i32([N]),
+                          kcfg=CFGS[bits], vcfg=CFGS[bits])
+    o, L = o.cpu().numpy(), L.cpu().numpy()
+    for h in rng.choice(8, size=2, replace=False):
+        kk = ref.unpack_codes(kc[0, h].cpu().numpy(), bits)
+        vv = ref.unpack_codes(vc[0, h].cpu().numpy(), bits)
+        ckh = ck[h] if ck.ndim == 3 else ck
+        cvh = cv[h] if cv.ndim == 3 else cv
+        o_ref, L_ref = ref.attention_vq(q[0, 4 * h:4 * h + 4], CB["lambda"][h], ckh, cvh, kk, vv)
+        _assert_close(o[0, 4 * h:4 * h + 4], L[0, 4 * h:4 * h + 4], o_ref, L_ref)
