@@ -37,7 +37,11 @@ WORKLOADS = {
     "cfg2": (1, 32768, 8, 8, "configs[1]: Llama-3.1-8B b2d4, batch 1, seq 32k, 1xB200"),
     "cfg3": (64, 8192, 8, 8, "configs[2]: Llama-3.1-8B b2d4, batch 64, seq 8k (per-rank batch slice at N>1)"),
     "cfg4": (1, 196608, 8, 8, "configs[3]: Llama-3.1-8B b2d4, batch 1, seq 196k (sequence-sharded at N>1)"),
+    "cfg5-b1d4": (1, 65536, 4, 4, "configs[4]: bit-width sweep, b1d4 (16 centroids), seq 64k"),
+    "cfg5-b2d4": (1, 65536, 8, 8, "configs[4]: bit-width sweep, b2d4 (256 centroids), seq 64k"),
+    "cfg5-b4d4": (1, 65536, 16, 16, "configs[4]: bit-width sweep, b4d4 (65536 centroids, shared codebook), seq 64k"),
 }
+CB_NAME = {4: "b1d4", 8: "b2d4", 16: "b4d4"}
 
 
 def load_peaks():
@@ -111,7 +115,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ CPU oracle arm
-def oracle_sample(seconds: float, N: int, seed: int = 7):
+def oracle_sample(seconds: float, N: int, seed: int = 7, kbits: int = 8, vbits: int = 8):
     """Time the CPU oracle (as it stands) on (b, h_kv) units of the workload: one unit = the
     decode-attention of 4 grouped query heads over N cached tokens (+ the 1-token append encode).
     Returns (units, seconds, threads)."""
@@ -124,16 +128,20 @@ def oracle_sample(seconds: float, N: int, seed: int = 7):
         threads = os.cpu_count() or 1
     cb = load_codebooks()
     rng = np.random.default_rng(seed)
-    kc = rng.integers(0, 256, (N, 32))
-    vc = rng.integers(0, 256, (N, 32))
+    kc = rng.integers(0, 1 << kbits, (N, 32))
+    vc = rng.integers(0, 1 << vbits, (N, 32))
+    ckn, cvn = f"ck_{CB_NAME[kbits]}", f"cv_{CB_NAME[vbits]}"
+
+    def head_cb(name, h):
+        return cb[name][h] if cb[name].ndim == 3 else cb[name]
     q = synth.gen_queries(1, H_Q, H_KV, D, seed=seed)[0]
     knew = synth.gen_keys(1, H_KV, D, seed=seed)[0, 0]
     vnew = synth.gen_values(1, H_KV, D, seed=seed + 1)[0, 0]
     units, t0 = 0, time.perf_counter()
     while True:
         h = units % H_KV
-        ref.encode_kv(knew[h], vnew[h], cb["inv_lambda"][h], cb["ck_b2d4"][h], cb["cv_b2d4"][h])
-        ref.attention_vq(q[4 * h:4 * h + 4], cb["lambda"][h], cb["ck_b2d4"][h], cb["cv_b2d4"][h], kc, vc)
+        ref.encode_kv(knew[h], vnew[h], cb["inv_lambda"][h], head_cb(ckn, h), head_cb(cvn, h))
+        ref.attention_vq(q[4 * h:4 * h + 4], cb["lambda"][h], head_cb(ckn, h), head_cb(cvn, h), kc, vc)
         units += 1
         el = time.perf_counter() - t0
         if el >= seconds:
@@ -144,14 +152,14 @@ def run_reference(args, rank, world):
     """--impl reference: the oracle timed on the box's host cores (rank 0 only)."""
     if rank != 0:
         return
-    B, N, _, _, desc = WORKLOADS[args.workload]
-    unit_bytes = N * 64
+    B, N, kbits, vbits, desc = WORKLOADS[args.workload]
+    unit_bytes = N * (4 * kbits + 4 * vbits)
     for _ in range(args.warmup):
-        oracle_sample(0.0, N)
+        oracle_sample(0.0, N, kbits=kbits, vbits=vbits)
     units, secs = 0, 0.0
     threads = 1
     for _ in range(args.steps):
-        u, s, threads = oracle_sample(args.ref_step_seconds, N)
+        u, s, threads = oracle_sample(args.ref_step_seconds, N, kbits=kbits, vbits=vbits)
         units += u
         secs += s
     gbs = units * unit_bytes / secs / 1e9
@@ -189,15 +197,18 @@ def run_ours(args, rank, world, local_rank):
     cb = load_codebooks()
     lam = torch.from_numpy(cb["lambda"]).to(dev)
     inv = torch.from_numpy(cb["inv_lambda"]).to(dev)
-    ck = torch.from_numpy(cb["ck_b2d4"]).to(dev).to(torch.bfloat16)
-    cv = torch.from_numpy(cb["cv_b2d4"]).to(dev).to(torch.bfloat16)
-    kcfg = vcfg = vi.B2D4
+    ck = torch.from_numpy(cb[f"ck_{CB_NAME[kbits]}"]).to(dev).to(torch.bfloat16)
+    cv = torch.from_numpy(cb[f"cv_{CB_NAME[vbits]}"]).to(dev).to(torch.bfloat16)
+    cfgs = {4: vi.B1D4, 8: vi.B2D4, 16: vi.B4D4}
+    kcfg, vcfg = cfgs[kbits], cfgs[vbits]
+    unit_bytes = 4 * kbits + 4 * vbits          # K + V code bytes per cached (token, KV head)
 
     # ---- prefill: bulk-encode synthetic keys/values of one layer (Eq. 8), replicate per layer
     n_local = tok1 - tok0
     t_gen = time.perf_counter()
-    kc0 = torch.empty(B, H_KV, n_local, 32, dtype=torch.uint8, device=dev)
-    vc0 = torch.empty_like(kc0)
+    kc0 = torch.empty(B, H_KV, n_local, kcfg.row_bytes, dtype=torch.uint8, device=dev)
+    vc0 = torch.empty(B, H_KV, n_local, vcfg.row_bytes, dtype=torch.uint8, device=dev)
+    enc_ws = vi.encode_workspace(B, 4096, H_KV, kcfg, vcfg, device=dev)
     chunk = 4096
     prefill_ms = 0.0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -207,7 +218,7 @@ def run_ours(args, rank, world, local_rank):
         v = torch.from_numpy(synth.gen_values(c1 - c0, H_KV, D, seed=7 + 1000 * rank + c0, batch=B)).to(dev).to(torch.bfloat16)
         wp = torch.full((B,), c0, dtype=torch.int32, device=dev)
         ev0.record()
-        vi.encode_kv(k, v, inv, ck, cv, kc0, vc0, wp, kcfg, vcfg)
+        vi.encode_kv(k, v, inv, ck, cv, kc0, vc0, wp, kcfg, vcfg, workspace=enc_ws)
         ev1.record()
         ev1.synchronize()
         prefill_ms += ev0.elapsed_time(ev1)
@@ -227,7 +238,7 @@ def run_ours(args, rank, world, local_rank):
     lse_all = torch.empty(L, B, H_Q, dtype=torch.float32, device=dev)
     o_part = torch.empty(L, B, H_Q, D, dtype=torch.float32, device=dev) if seq_sharded else None
     S = vi.attn_num_splits(B, H_KV, n_local, 0)
-    ws = [vi.attn_workspace(B, H_Q, H_KV, n_local, 0, device=dev) for _ in range(L)]
+    ws = [vi.decode_step_workspace(B, H_Q, H_KV, n_local, kcfg, vcfg, device=dev) for _ in range(L)]
     stream = torch.cuda.Stream(device=dev)
 
     fused = not args.unfused and not seq_sharded
@@ -235,18 +246,18 @@ def run_ours(args, rank, world, local_rank):
     def layer(l, ev_pair=None):
         if fused:   # one launch: append-encode of the new token + attention (vecinfer_decode_step)
             vi.decode_step(q_all[l], kn_all[l][:, 0], vn_all[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
-                           seq_lens, out=o_all[l], lse=lse_all[l], workspace=ws[l])
+                           seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l])
             return
         if owns_tail:
-            vi.encode_kv(kn_all[l], vn_all[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg)
+            vi.encode_kv(kn_all[l], vn_all[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg, workspace=enc_ws)
         if ev_pair is not None:
             ev_pair[0].record()
         if seq_sharded:
-            vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, out=o_part[l], lse=lse_all[l],
-                           workspace=ws[l])
+            vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_part[l],
+                           lse=lse_all[l], workspace=ws[l])
         else:
-            vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, out=o_all[l], lse=lse_all[l],
-                           workspace=ws[l])
+            vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
+                           lse=lse_all[l], workspace=ws[l])
         if ev_pair is not None:
             ev_pair[1].record()
 
@@ -276,8 +287,8 @@ def run_ours(args, rank, world, local_rank):
         g_attn = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_attn, stream=stream):
             for l in range(L):
-                vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, out=o_all[l], lse=lse_all[l],
-                               workspace=ws[l])
+                vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
+                               lse=lse_all[l], workspace=ws[l])
     torch.cuda.synchronize(dev)
 
     def barrier():
@@ -342,14 +353,16 @@ def run_ours(args, rank, world, local_rank):
         for l in range(L):
             if fused:
                 vi.decode_step(q_d[l], kn_d[l][:, 0], vn_d[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
-                               seq_lens, out=o_all[l], lse=lse_all[l], workspace=ws[l])
+                               seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l])
                 continue
             if owns_tail:
-                vi.encode_kv(kn_d[l], vn_d[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg)
+                vi.encode_kv(kn_d[l], vn_d[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg, workspace=enc_ws)
             if seq_sharded:
-                vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, out=o_part[l], lse=lse_all[l], workspace=ws[l])
+                vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_part[l],
+                               lse=lse_all[l], workspace=ws[l])
             else:
-                vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, out=o_all[l], lse=lse_all[l], workspace=ws[l])
+                vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
+                               lse=lse_all[l], workspace=ws[l])
         if seq_sharded:
             o_g, l_g = gather_partials_packed(o_part, lse_all)
             vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
@@ -379,10 +392,10 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     # ---- figures
-    code_bytes_rank = B * H_KV * n_local * 64                   # K + V codes per layer call
+    code_bytes_rank = B * H_KV * n_local * unit_bytes           # K + V codes per layer call
     total_bytes = code_bytes_rank * L * K * (world if not seq_sharded else 1)
     if seq_sharded:
-        total_bytes = B * H_KV * N * 64 * L * K
+        total_bytes = B * H_KV * N * unit_bytes * L * K
     value = total_bytes / (elapsed_ms / 1e3) / 1e9
     e2e_value = total_bytes / (e2e_ms / 1e3) / 1e9
     peak, peak_src = load_peaks()
@@ -396,8 +409,8 @@ def run_ours(args, rank, world, local_rank):
     step_ms = elapsed_ms / K
     cpu = None
     if not args.no_cpu_baseline:
-        units, secs, threads = oracle_sample(args.cpu_seconds, N if not seq_sharded else N)
-        cpu = {"value": units * N * 64 / secs / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
+        units, secs, threads = oracle_sample(args.cpu_seconds, N, kbits=kbits, vbits=vbits)
+        cpu = {"value": units * N * unit_bytes / secs / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
                "sample": f"{units} (b,h_kv) units x {N} tokens (4 grouped q-heads each + 1-token append encode) "
                          f"in {secs:.1f}s on {os.cpu_count()} host cores (NumPy fp64; threads = BLAS pool)"}
     line = {
@@ -405,7 +418,7 @@ def run_ours(args, rank, world, local_rank):
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if seq_sharded else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.workload, "desc": desc, "global_batch": B_glob, "seq_len": N,
-                   "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": "b2d4",
+                   "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": f"K-{CB_NAME[kbits]}/V-{CB_NAME[vbits]}",
                    "parallelism": ("seq-shard" if seq_sharded else "dp") + str(world),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
                    "num_splits": S, "cuda_graph": use_graph, "fused_append": fused,

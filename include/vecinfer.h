@@ -185,10 +185,14 @@ vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_
  *              (strides {b, h}); inv_lambda as in encode_kv; lambda as in attn_decode.
  *   k_codes, v_codes  the code caches (written at row write_pos[b], read over [0, seq_lens[b])).
  *   Other arguments as in vecinfer_attn_decode (token range = whole sequence) and
- *   vecinfer_encode_kv (err_flags).  The codebooks must be b2d4 for the fused launch; with
+ *   vecinfer_encode_kv (err_flags); workspace >= vecinfer_decode_step_workspace_bytes(...), zero-
+ *   filled once.  Grids of more than one wave, 16-bit codebooks and the LUT variant run the
+ *   append as its own launch first (same results).  The codebooks must be b2d4 for the fused launch; with
  *   algo = VECINFER_ATTN_LUT the call is executed as the two separate launches.
  * Errors: as vecinfer_encode_kv and vecinfer_attn_decode.
  * ------------------------------------------------------------------------------------- */
+size_t vecinfer_decode_step_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int64_t n_cap,
+                                            vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, int32_t num_splits);
 vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,
                                        int32_t B, int32_t H_q, int32_t H_kv, const int64_t q_strides[2],
                                        const int64_t k_new_strides[2], const int64_t v_new_strides[2],

@@ -46,6 +46,7 @@ PROTOTYPES = {
                                      c_void_p, c_i64, c_void_p, c_void_p, c_f32, c_i32, c_i32, c_void_p, c_i32,
                                      c_void_p, c_void_p, c_void_p, c_sz, c_void_p]),
     "vecinfer_debug_attn_max_clusters": (c_i32, [c_i32]),
+    "vecinfer_decode_step_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i64, VQ, VQ, c_i32]),
     "vecinfer_merge_lse": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_void_p, c_i32, c_void_p,
                                    c_void_p]),
 }

@@ -224,6 +224,12 @@ extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B,
                    num_splits, algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr);
 }
 
+extern "C" size_t vecinfer_decode_step_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int64_t n_cap,
+                                                       vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, int32_t num_splits) {
+  const size_t a = (vecinfer_attn_workspace_bytes(B, H_q, H_kv, 128, n_cap, num_splits) + 255) & ~size_t(255);
+  return a + vecinfer_encode_workspace_bytes(B, 1, H_kv, kcfg, vcfg);
+}
+
 extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,
                                                   int32_t B, int32_t H_q, int32_t H_kv, const int64_t q_strides[2],
                                                   const int64_t k_new_strides[2], const int64_t v_new_strides[2],
@@ -257,9 +263,15 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
   if (!fuse) {   // separate append + attention launches (always for the paper-faithful LUT variant)
     const int64_t ks[3] = {k_new_strides[0], 0, k_new_strides[1]};
     const int64_t vs[3] = {v_new_strides[0], 0, v_new_strides[1]};
+    // encode workspace (16-bit codebooks) lives behind the attention workspace
+    const size_t aw = (vecinfer_attn_workspace_bytes(B, H_q, H_kv, 128, n_cap, num_splits) + 255) & ~size_t(255);
+    const size_t ew = vecinfer_encode_workspace_bytes(B, 1, H_kv, kcfg, vcfg);
+    if (ew && (!workspace || workspace_bytes < aw + ew))
+      return fail(VECINFER_ERR_WORKSPACE, "decode_step: workspace needs %zu bytes", aw + ew);
+    void* ews = ew ? static_cast<void*>(static_cast<unsigned char*>(workspace) + aw) : nullptr;
     vecinfer_status_t st = vecinfer_encode_kv(k_new_bf16, v_new_bf16, B, 1, H_kv, ks, vs, inv_lambda, ck_bf16, cv_bf16,
                                               ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap,
-                                              write_pos, err_flags, nullptr, 0, stream);
+                                              write_pos, err_flags, ews, ew, stream);
     if (st != VECINFER_OK) return st;
     return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,

@@ -181,7 +181,7 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
     if lse is None:
         lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device)
     lib = _lib.load()
-    need = lib.vecinfer_attn_workspace_bytes(B, Hq, Hkv, D, n_cap, num_splits)
+    need = lib.vecinfer_decode_step_workspace_bytes(B, Hq, Hkv, n_cap, kcfg.c(), vcfg.c(), num_splits)
     if workspace is None or workspace.numel() < need:
         workspace = torch.zeros(max(need, 256), dtype=torch.uint8, device=q.device)
     check("vecinfer_decode_step", lib.vecinfer_decode_step(
@@ -197,6 +197,12 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
         ctypes.c_void_p(err_flags.data_ptr()) if err_flags is not None else ctypes.c_void_p(0),
         ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream(q.device)))
     return out, lse
+
+
+def decode_step_workspace(B: int, H_q: int, H_kv: int, n_cap: int, kcfg: VQConfig = B2D4, vcfg: VQConfig = B2D4,
+                          num_splits: int = 0, device="cuda"):
+    n = _lib.load().vecinfer_decode_step_workspace_bytes(B, H_q, H_kv, n_cap, kcfg.c(), vcfg.c(), num_splits)
+    return torch.zeros(max(n, 256), dtype=torch.uint8, device=device)
 
 
 def merge_lse(o_parts: torch.Tensor, lse_parts: torch.Tensor, o_dtype: torch.dtype = torch.float32,
