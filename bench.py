@@ -242,6 +242,8 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(device=dev)
 
     fused = not args.unfused and not seq_sharded
+    # vecinfer_decode_step itself fuses only single-wave grids with <= 8-bit codes
+    fused_launch = fused and kbits <= 8 and vbits <= 8 and vi.attn_num_splits(B, H_KV, n_local, 0) * B * H_KV <= 148
 
     def layer(l, ev_pair=None):
         if fused:   # one launch: append-encode of the new token + attention (vecinfer_decode_step)
@@ -269,7 +271,11 @@ def run_ours(args, rank, world, local_rank):
             vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
                          o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D))
 
-    launches_per_step = L if fused else L * ((1 if owns_tail else 0) + 1) + (1 if seq_sharded else 0)
+    append_kernels = 2 if max(kbits, vbits) == 16 else 1      # 16-bit: centroid-split search + finalize
+    if fused_launch:
+        launches_per_step = L
+    else:
+        launches_per_step = L * ((append_kernels if owns_tail else 0) + 1) + (1 if seq_sharded else 0)
 
     # ---- warm-up (eager) so lazy init/attributes happen outside capture
     with torch.cuda.stream(stream):
@@ -421,7 +427,7 @@ def run_ours(args, rank, world, local_rank):
                    "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": f"K-{CB_NAME[kbits]}/V-{CB_NAME[vbits]}",
                    "parallelism": ("seq-shard" if seq_sharded else "dp") + str(world),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
-                   "num_splits": S, "cuda_graph": use_graph, "fused_append": fused,
+                   "num_splits": S, "cuda_graph": use_graph, "fused_append": fused_launch,
                    "dtype_detail": "u8 codes, bf16 q/k/v/o, fp16 hi/lo MMA operands, f32 accumulate"},
         "us_per_layer_call": step_ms * 1e3 / L,
         "tokens_per_s": B_glob * 1e3 / step_ms,

@@ -38,6 +38,11 @@ constexpr int kMiscBytes = kMiscW + (kNW * 8 + kNW * 4 * 128) * 4;   // 35328
 constexpr int kClusterMax = 16;                      // DSMEM merge buffer: [16][4][128] + m, l
 constexpr int kCbufBytes = kClusterMax * 4 * 130 * 4;
 constexpr int kSmemBytes = 65536 + kTab + kCbufBytes + 1024;  // pad + table + cluster buffer + slack
+// 16-bit K and V: no shared table -> only misc + cluster buffer, leaving the L1 to the global
+// codebook gathers
+constexpr int kSmemBytesNoTab = kMiscBytes + 1024 + kCbufBytes + 1024;
+template <int KB, int VB>
+constexpr int smem_bytes() { return (KB > 8 && VB > 8) ? kSmemBytesNoTab : kSmemBytes; }
 
 // ---- code-width traits.  Per lane and token: the K chunk holds sub-vectors 8j..8j+7 (score MMA
 // k-steps), the V chunk sub-vectors 4r..4r+3 (P.V m-tiles).  4/8-bit codebooks are gathered from the
@@ -193,8 +198,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   // shared layout: misc at the bottom, the codebook table at the next 64 KiB boundary
   const uint32_t raw_s = smem_u32(smem_raw);
-  uint32_t tab_off = ((raw_s + 65535u) & ~65535u) - raw_s;
-  if (tab_off < static_cast<uint32_t>(kMiscBytes)) tab_off += 65536u;
+  uint32_t tab_off;
+  if constexpr (KB > 8 && VB > 8) {
+    tab_off = (kMiscBytes + 1023) & ~1023;   // no table: the "table" base only anchors the cluster buffer
+  } else {
+    tab_off = ((raw_s + 65535u) & ~65535u) - raw_s;
+    if (tab_off < static_cast<uint32_t>(kMiscBytes)) tab_off += 65536u;
+  }
   unsigned char* tab = smem_raw + tab_off;
   float* sq = reinterpret_cast<float*>(smem_raw + kMiscQ);
   const uint32_t tab_s = raw_s + tab_off;
@@ -472,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       }
     }
     const uint32_t rank = cluster_ctarank();
-    float* cbuf = reinterpret_cast<float*>(tab + kTab);     // [16][4][128] acc, [16][4] M, [16][4] l
+    float* cbuf = reinterpret_cast<float*>(tab + ((KB > 8 && VB > 8) ? 0 : kTab));   // [16][4][128] acc, [16][4] M, l
     float* cM = cbuf + kClusterMax * 4 * 128;
     float* cL = cM + kClusterMax * 4;
     const uint32_t cb_s = smem_u32(cbuf);
@@ -509,6 +519,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
 using AttnKernel = void (*)(const AttnArgs);
 
+static int smem_for(int kb, int vb) { return (kb > 8 && vb > 8) ? kSmemBytesNoTab : kSmemBytes; }
+
 static AttnKernel kernel_for(int kb, int vb) {
   const int ki = kb == 4 ? 0 : kb == 8 ? 1 : 2, vi = vb == 4 ? 0 : vb == 8 ? 1 : 2;
   static const AttnKernel table[3][3] = {
@@ -523,7 +535,7 @@ static void set_attrs_once() {
   if (!done) {
     for (int kb : {4, 8, 16})
       for (int vb : {4, 8, 16}) {
-        cudaFuncSetAttribute(kernel_for(kb, vb), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(kernel_for(kb, vb), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(kb, vb));
         cudaFuncSetAttribute(kernel_for(kb, vb), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       }
     done = true;
@@ -561,7 +573,7 @@ cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.S, a.Hkv, a.B);
   cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.dynamicSmemBytes = smem_for(kbits, vbits);
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   int n = 0;

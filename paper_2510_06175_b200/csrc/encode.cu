@@ -193,13 +193,19 @@ __global__ void __launch_bounds__(512) encode_append_kernel(EncArgs a) {
 
 // ------------------------------------------------------------------ 16-bit: centroid split
 // grid (ceil(B*T / kEncWarps), 65536 / kChunk16, H); stage one chunk of C_k and C_v.
+// kSplit (few token-heads, e.g. the decode append): one token-head per CTA and its 8 warps split
+// the chunk (128 centroids each); otherwise one token-head per warp scanning the whole chunk.
+template <bool kSplit>
 __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) {
   __shared__ float4 sc[kChunk16];
   griddep_wait();
   const int h = blockIdx.z;
   const int j0 = blockIdx.y * kChunk16;
   const int lane = threadIdx.x & 31;
-  const int64_t bt = static_cast<int64_t>(blockIdx.x) * kEncWarps + (threadIdx.x >> 5);
+  const int warp = threadIdx.x >> 5;
+  const int64_t bt = kSplit ? static_cast<int64_t>(blockIdx.x) : static_cast<int64_t>(blockIdx.x) * kEncWarps + warp;
+  constexpr int kSpan = kSplit ? kChunk16 / kEncWarps : kChunk16;
+  const int jw = kSplit ? warp * kSpan : 0;
   const bool live = bt < static_cast<int64_t>(a.B) * a.T;
   const int b = live ? static_cast<int>(bt / a.T) : 0, t = live ? static_cast<int>(bt % a.T) : 0;
   for (int which = 0; which < 2; ++which) {
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) 
     float best = __int_as_float(0x7f800000);
     uint32_t bi = 0;
 #pragma unroll 4
-    for (int j = 0; j < kChunk16; ++j) {
+    for (int j = jw; j < jw + kSpan; ++j) {
       const float4 c = sc[j];
       const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
       if (dd < best) { best = dd; bi = j; }
@@ -337,7 +343,10 @@ extern "C" vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* 
     if (!workspace || workspace_bytes < need || !aligned(workspace, 8))
       return fail(VECINFER_ERR_WORKSPACE, "encode_kv: 16-bit codebooks need %zu bytes of workspace", need);
     if (cudaMemsetAsync(workspace, 0xFF, need, st) != cudaSuccess) return check_launch("encode_kv memset");
-    encode_nn16_kernel<<<dim3(static_cast<unsigned>(gx), 65536 / kChunk16, H_kv), kEncWarps * 32, 0, st>>>(a);
+    if (nbt * H_kv <= 4096)
+      encode_nn16_kernel<true><<<dim3(static_cast<unsigned>(nbt), 65536 / kChunk16, H_kv), kEncWarps * 32, 0, st>>>(a);
+    else
+      encode_nn16_kernel<false><<<dim3(static_cast<unsigned>(gx), 65536 / kChunk16, H_kv), kEncWarps * 32, 0, st>>>(a);
     vecinfer_status_t s = check_launch("encode_nn16_kernel");
     if (s != VECINFER_OK) return s;
     encode_nn16_finalize<<<dim3(static_cast<unsigned>(gx), H_kv), kEncWarps * 32, 0, st>>>(a);
