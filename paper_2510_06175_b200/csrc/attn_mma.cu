@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   const int r = lane >> 2, j = lane & 3;
   const int cta_id = (b * gridDim.y + h) * gridDim.x + s;
   phase_mark(a.phase, cta_id, 0);
+  if (a.cluster) cluster_arrive_relaxed();   // paired with cluster_wait() before the DSMEM pushes
 
   // shared layout: misc at the bottom, the codebook table at the next 64 KiB boundary
   const uint32_t raw_s = smem_u32(smem_raw);
@@ -481,6 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         osum += f * wacc[(w * 4 + g) * 128 + dim];
       }
     }
+    cluster_wait();   // every CTA of the cluster has started: DSMEM of the leader is valid
     const uint32_t rank = cluster_ctarank();
     float* cbuf = reinterpret_cast<float*>(tab + ((KB > 8 && VB > 8) ? 0 : kTab));   // [16][4][128] acc, [16][4] M, l
     float* cM = cbuf + kClusterMax * 4 * 128;
