@@ -183,7 +183,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2510_06175_b200 import vecinfer as vi
     from paper_2510_06175_b200.sharding import batch_shard, gather_partials_packed, shard_range
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank if args.backend == "nccl" else local_rank % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
     B_glob, N, kbits, vbits, desc = WORKLOADS[args.workload]
     seq_sharded = args.workload == "cfg4" and world > 1
@@ -267,7 +267,11 @@ def run_ours(args, rank, world, local_rank):
         for l in range(L):
             layer(l, None if evs is None else evs[l])
         if seq_sharded:   # one all-gather of the per-rank partials of all 32 layers, then LSE merge
-            o_g, l_g = gather_partials_packed(o_part, lse_all)
+            if args.backend == "gloo":
+                o_g, l_g = gather_partials_packed(o_part.cpu(), lse_all.cpu())
+                o_g, l_g = o_g.to(dev), l_g.to(dev)
+            else:
+                o_g, l_g = gather_partials_packed(o_part, lse_all)
             vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
                          o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D))
 
@@ -323,10 +327,13 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize(dev)
     elapsed_ms = t_start.elapsed_time(t_end)
-    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t_max.item())
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    elapsed_ms = max_over_ranks(elapsed_ms)
 
     # ---- dominant kernel (vecinfer_attn_decode) timed alone: K replays of the 32-layer attention
     # graph on the launching stream; per-launch time = total / (K * L) (inter-kernel gaps included)
@@ -370,7 +377,11 @@ def run_ours(args, rank, world, local_rank):
                 vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
                                lse=lse_all[l], workspace=ws[l])
         if seq_sharded:
-            o_g, l_g = gather_partials_packed(o_part, lse_all)
+            if args.backend == "gloo":
+                o_g, l_g = gather_partials_packed(o_part.cpu(), lse_all.cpu())
+                o_g, l_g = o_g.to(dev), l_g.to(dev)
+            else:
+                o_g, l_g = gather_partials_packed(o_part, lse_all)
             vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
                          o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D))
         o_h.copy_(o_all, non_blocking=True)
@@ -388,10 +399,7 @@ def run_ours(args, rank, world, local_rank):
         t1e.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = t0e.elapsed_time(t1e)
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item())
+    e2e_ms = max_over_ranks(e2e_ms)
     h2d = q_h.numel() * 2 + kn_h.numel() * 2 + vn_h.numel() * 2 if owns_tail else q_h.numel() * 2
     d2h = o_h.numel() * 2
 
@@ -458,6 +466,8 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N>1 (gloo: ranks may share one GPU; functional check)")
     ap.add_argument("--unfused", action="store_true", help="separate encode_kv + attn_decode launches per layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -472,8 +482,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev_idx = local_rank if args.backend == "nccl" else local_rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev_idx)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:   # gloo: functional check of the multi-rank paths on a single-GPU box
+            dist.init_process_group("gloo")
     try:
         run_ours(args, rank, world, local_rank)
     finally:
