@@ -440,7 +440,7 @@ def run_ours(args, rank, world, local_rank):
         "us_per_layer_call": step_ms * 1e3 / L,
         "tokens_per_s": B_glob * 1e3 / step_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "attn_mma8_kernel (vecinfer_attn_decode)",
+                     "traffic": traffic, "kernel": "attn_mma_kernel<KB,VB> (vecinfer_attn_decode / vecinfer_decode_step)",
                      "attn_us_avg": attn_avg_ms * 1e3, "attn_us_p10": float(np.percentile(attn_ms, 10)) * 1e3,
                      "attn_us_p90": float(np.percentile(attn_ms, 90)) * 1e3,
                      "timing": "CUDA events around K replays of a graph of the 32 layers' vecinfer_attn_decode launches "
