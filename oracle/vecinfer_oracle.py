@@ -212,6 +212,29 @@ def attention_vq(q: np.ndarray, lam: np.ndarray, Ck: np.ndarray, Cv: np.ndarray,
     return attention_full(qt, Kh, Vh)
 
 
+def attention_vq_residual(q: np.ndarray, lam: np.ndarray, Ck: np.ndarray, Cv: np.ndarray,
+                          k_codes: np.ndarray, v_codes: np.ndarray, K_res: np.ndarray, V_res: np.ndarray):
+    """VQ cache plus a full-precision residual window ("the residual length for all methods
+    is set to 128"): one softmax over the union of the quantised tokens and the residual tokens.
+    Quantised scores use q~ and VQ^-1(K~_q) (Eq. 10); residual scores use the raw q and raw keys,
+    equal to q~ k~^T by Eq. 7.  q: [G, D]; K_res, V_res: [R, D] (R may be 0).  fp64."""
+    qt = transform_query(q, lam)
+    Kh = vq_decode(k_codes, Ck)
+    Vh = vq_decode(v_codes, Cv)
+    D = q.shape[-1]
+    q = np.asarray(q, dtype=np.float64)
+    K_res = np.asarray(K_res, dtype=np.float64).reshape(-1, D)
+    V_res = np.asarray(V_res, dtype=np.float64).reshape(-1, D)
+    s = np.concatenate([qt @ Kh.T, q @ K_res.T], axis=1) / math.sqrt(D)
+    V = np.concatenate([Vh, V_res], axis=0)
+    if s.shape[1] == 0:
+        return np.zeros((q.shape[0], D)), np.full(q.shape[0], -np.inf)
+    m = s.max(axis=1, keepdims=True)
+    p = np.exp(s - m)
+    ell = p.sum(axis=1, keepdims=True)
+    return (p @ V) / ell, (m + np.log(ell))[:, 0]
+
+
 def build_lut(q_tilde: np.ndarray, Ck: np.ndarray) -> np.ndarray:
     """Alg. 1 line 4: q~' = reshape(q~, (M, D/M)); lut = q~' C_k^T  -> [M, 2^b] fp64."""
     q_tilde = np.asarray(q_tilde, dtype=np.float64)
@@ -240,12 +263,13 @@ def merge_lse(o_parts: np.ndarray, L_parts: np.ndarray):
 
 def attention_decode_batch(q: np.ndarray, lam: np.ndarray, Ck: np.ndarray, Cv: np.ndarray,
                            k_codes: np.ndarray, v_codes: np.ndarray, seq_lens, tok_begin: int = 0,
-                           tok_end: int | None = None):
+                           tok_end: int | None = None, K_res=None, V_res=None, res_lens=None):
     """One decode-attention layer call over a batch (the §8(b) vecinfer_attn_decode contract).
 
     q: [B, H_q, D]; lam: [H_kv, D]; Ck/Cv: [H_kv, 2^b, d] (or [2^b, d] shared);
     k_codes/v_codes: [B, H_kv, n_cap, M]; token range [tok_begin, min(tok_end, seq_len)).
-    Query head i reads KV head i // (H_q/H_kv) (GQA).  Returns o [B, H_q, D], L [B, H_q] fp64.
+    Query head i reads KV head i // (H_q/H_kv) (GQA).  Optional residual window K_res/V_res
+    [B, H_kv, R_cap, D] with res_lens [B] (attention_vq_residual).  Returns o [B, H_q, D], L [B, H_q].
     """
     B, Hq, D = q.shape
     Hkv = k_codes.shape[1]
@@ -259,8 +283,13 @@ def attention_decode_batch(q: np.ndarray, lam: np.ndarray, Ck: np.ndarray, Cv: n
         for h in range(Hkv):
             ck = Ck[h] if np.ndim(Ck) == 3 else Ck
             cv = Cv[h] if np.ndim(Cv) == 3 else Cv
-            oo, LL = attention_vq(q[b, h * G:(h + 1) * G], lam[h], ck, cv,
-                                  k_codes[b, h, s:e], v_codes[b, h, s:e])
+            if K_res is None:
+                oo, LL = attention_vq(q[b, h * G:(h + 1) * G], lam[h], ck, cv,
+                                      k_codes[b, h, s:e], v_codes[b, h, s:e])
+            else:
+                r = int(res_lens[b])
+                oo, LL = attention_vq_residual(q[b, h * G:(h + 1) * G], lam[h], ck, cv, k_codes[b, h, s:e],
+                                               v_codes[b, h, s:e], K_res[b, h, :r], V_res[b, h, :r])
             o[b, h * G:(h + 1) * G] = oo
             L[b, h * G:(h + 1) * G] = LL
     return o, L

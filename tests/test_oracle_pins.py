@@ -429,3 +429,42 @@ def test_kmeans_examples(golden):
     assert np.array_equal(Ca, Cb)                                  # deterministic
     assert all(b <= a + 1e-9 for a, b in zip(ha, ha[1:]))          # objective non-increasing
     assert len(ha) <= 30                                           # P:501 iteration cap
+
+
+# ------------------------------------------------------------ residual window (NEXT-1)
+def test_residual_window_special_cases():
+    """Residual-window attention: empty residual == Eq. 10 VQ attention; empty VQ part == Eq. 1 on
+    the residual; and in general == the LSE merge of the two separate attentions (exact algebra)."""
+    rng = np.random.default_rng(40)
+    Ck = synth.gen_codebook(256, 4, seed=41)
+    Cv = synth.gen_codebook(256, 4, seed=42)
+    kc, vc = rng.integers(0, 256, (300, 32)), rng.integers(0, 256, (300, 32))
+    lam = np.exp(rng.uniform(-1, 1, 128))
+    q = rng.standard_normal((4, 128))
+    Kr, Vr = rng.standard_normal((77, 128)), rng.standard_normal((77, 128))
+    o0, L0 = ref.attention_vq_residual(q, lam, Ck, Cv, kc, vc, Kr[:0], Vr[:0])
+    o1, L1 = ref.attention_vq(q, lam, Ck, Cv, kc, vc)
+    assert np.allclose(o0, o1, rtol=1e-12) and np.allclose(L0, L1, rtol=1e-12)
+    o0, L0 = ref.attention_vq_residual(q, lam, Ck, Cv, kc[:0], vc[:0], Kr, Vr)
+    o1, L1 = ref.attention_full(q, Kr, Vr)
+    assert np.allclose(o0, o1, rtol=1e-12) and np.allclose(L0, L1, rtol=1e-12)
+    o, L = ref.attention_vq_residual(q, lam, Ck, Cv, kc, vc, Kr, Vr)
+    pa, pb = ref.attention_vq(q, lam, Ck, Cv, kc, vc), ref.attention_full(q, Kr, Vr)
+    mo, mL = ref.merge_lse(np.stack([pa[0], pb[0]]), np.stack([pa[1], pb[1]]))
+    assert np.allclose(o, mo, rtol=1e-12, atol=1e-14) and np.allclose(L, mL, rtol=1e-12)
+
+
+def test_residual_window_equals_unquantised_keys_when_exact():
+    """If the quantised tokens are exactly representable (codes decode to the transformed keys), the
+    residual + VQ attention equals Eq. 1 over all ORIGINAL keys (invariance, Eq. 7)."""
+    rng = np.random.default_rng(43)
+    Ck = synth.gen_codebook(256, 4, seed=44)
+    Cv = synth.gen_codebook(256, 4, seed=45)
+    kc, vc = rng.integers(0, 256, (100, 32)), rng.integers(0, 256, (100, 32))
+    lam = np.exp(rng.uniform(-1, 1, 128))
+    q = rng.standard_normal((4, 128))
+    Kq = ref.vq_decode(kc, Ck) @ ref.hadamard(128).T * lam[None]
+    Kr, Vr = rng.standard_normal((20, 128)), rng.standard_normal((20, 128))
+    o, L = ref.attention_vq_residual(q, lam, Ck, Cv, kc, vc, Kr, Vr)
+    o2, L2 = ref.attention_full(q, np.concatenate([Kq, Kr]), np.concatenate([ref.vq_decode(vc, Cv), Vr]))
+    assert np.allclose(o, o2, rtol=1e-10, atol=1e-12) and np.allclose(L, L2, rtol=1e-10)
