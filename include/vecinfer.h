@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define VECINFER_ABI_VERSION 1
+#define VECINFER_ABI_VERSION 2
 
 typedef struct CUstream_st* vecinfer_stream_t; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -70,6 +70,24 @@ typedef enum {
   VECINFER_ATTN_DEQUANT_MMA = 1,
   VECINFER_ATTN_LUT = 2
 } vecinfer_attn_algo_t;
+
+/* Full-precision residual window ("the residual length for all methods is set to 128";
+ * SURVEY §8(f) NEXT-1): the newest tokens of each sequence kept as raw bf16 k, v rows next to the
+ * VQ cache.  Attention runs one softmax over the quantised tokens [tok range of seq_lens] and the
+ * residual rows [0, lens[b]); residual scores use the raw q (q k^T = q~ k~^T, Eq. 7).
+ *   k, v        bf16 [B, H_kv, r_cap, D]; element (b, h, t, c) at b*stride_b + h*stride_h + t*D + c.
+ *   lens        device int32 [B] rows in use (0 = none).
+ *   append_new  vecinfer_decode_step only: 1 = the new token is written to residual row lens[b]-1
+ *               (raw bf16 copy, no encode) instead of being encoded into the codes.
+ * The caller flushes old residual rows into the codes (vecinfer_encode_kv) when the window fills. */
+typedef struct {
+  const void* k;
+  const void* v;
+  int64_t stride_b, stride_h;
+  int64_t r_cap;
+  const int32_t* lens;
+  int32_t append_new;
+} vecinfer_residual_t;
 
 /* Device-side error bits written (atomicOr) into the optional err_flags word of encode_kv. */
 #define VECINFER_FLAG_RANGE 1u     /* |k * inv_lambda| >= 2^32: outside the pinned fixed point */
@@ -153,6 +171,8 @@ vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int
  *   num_splits  0 = heuristic (fill 148 SMs); > 0 fixed => bitwise-deterministic results.
  *   o           [B, H_q, D] bf16 or fp32 (o_dtype); lse fp32 [B, H_q] natural log.
  *               An empty range yields o = 0, lse = -inf (weight 0 in vecinfer_merge_lse).
+ *   residual    optional full-precision window (NULL = none), attended by the last split;
+ *               LUT variant: not supported (VECINFER_ERR_UNSUPPORTED).
  *   workspace   >= vecinfer_attn_workspace_bytes(B, H_q, H_kv, D, n_tokens_max, num_splits)
  *               bytes, where n_tokens_max bounds the attended range; MUST be zero-filled once
  *               when first allocated (the kernel leaves its counters at zero on exit).
@@ -173,7 +193,8 @@ vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_
                                        int64_t tok_end, float softmax_scale, int32_t num_splits,
                                        vecinfer_attn_algo_t algo, void* o,
                                        vecinfer_dtype_t o_dtype, float* lse, void* workspace,
-                                       size_t workspace_bytes, vecinfer_stream_t stream);
+                                       size_t workspace_bytes, vecinfer_stream_t stream,
+                                       const vecinfer_residual_t* residual);
 
 /* ---------------------------------------------------------------------------------------
  * Fused decode step for one layer: EXACTLY vecinfer_encode_kv(T = 1) of the new token followed
@@ -203,7 +224,8 @@ vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf1
                                        const int32_t* seq_lens, float softmax_scale, int32_t num_splits,
                                        vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype,
                                        float* lse, uint32_t* err_flags, void* workspace,
-                                       size_t workspace_bytes, vecinfer_stream_t stream);
+                                       size_t workspace_bytes, vecinfer_stream_t stream,
+                                       const vecinfer_residual_t* residual);
 
 /* ---------------------------------------------------------------------------------------
  * Log-sum-exp merge of P normalised partials (cross-GPU sequence shards, residual window):

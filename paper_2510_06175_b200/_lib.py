@@ -16,6 +16,13 @@ I64x3 = ctypes.c_int64 * 3
 I64x2 = ctypes.c_int64 * 2
 
 
+class Residual(ctypes.Structure):
+    """vecinfer_residual_t: full-precision residual window (NEXT-1)."""
+    _fields_ = [("k", ctypes.c_void_p), ("v", ctypes.c_void_p), ("stride_b", ctypes.c_int64),
+                ("stride_h", ctypes.c_int64), ("r_cap", ctypes.c_int64), ("lens", ctypes.c_void_p),
+                ("append_new", ctypes.c_int32)]
+
+
 class VQ(ctypes.Structure):
     """vecinfer_vq_t {head_dim, sub_dim, code_bits}."""
     _fields_ = [("head_dim", c_i32), ("sub_dim", c_i32), ("code_bits", c_i32)]
@@ -44,7 +51,7 @@ PROTOTYPES = {
     "vecinfer_decode_step": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, I64x2, I64x2, I64x2,
                                      c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, VQ, VQ, c_void_p,
                                      c_void_p, c_i64, c_void_p, c_void_p, c_f32, c_i32, c_i32, c_void_p, c_i32,
-                                     c_void_p, c_void_p, c_void_p, c_sz, c_void_p]),
+                                     c_void_p, c_void_p, c_void_p, c_sz, c_void_p, ctypes.POINTER(Residual)]),
     "vecinfer_debug_attn_max_clusters": (c_i32, [c_i32]),
     "vecinfer_decode_step_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i64, VQ, VQ, c_i32]),
     "vecinfer_merge_lse": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_void_p, c_i32, c_void_p,

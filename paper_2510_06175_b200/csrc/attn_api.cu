@@ -127,7 +127,8 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
                                    const int32_t* seq_lens, int64_t tok_begin, int64_t tok_end,
                                    float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
                                    void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
-                                   size_t workspace_bytes, vecinfer_stream_t stream, const AppendArgs* app) {
+                                   size_t workspace_bytes, vecinfer_stream_t stream, const AppendArgs* app,
+                                   const vecinfer_residual_t* res, bool res_append) {
   if (!q_bf16 || !lambda || !ck_bf16 || !cv_bf16 || !k_codes || !v_codes || !seq_lens || !o)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: NULL pointer");
   if (o_dtype != VECINFER_BF16 && o_dtype != VECINFER_F32) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad o_dtype");
@@ -158,6 +159,14 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   if (S > 1 && !plan.cluster && (!workspace || workspace_bytes < wl.total || !aligned(workspace, 256)))
     return fail(VECINFER_ERR_WORKSPACE, "attn_decode: workspace needs %zu bytes (256-B aligned)", wl.total);
   if (B > 65535 || H_kv > 65535) return fail(VECINFER_ERR_SHAPE, "attn_decode: grid too large");
+  if (res) {
+    if (algo == VECINFER_ATTN_LUT) return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: residual window needs the MMA kernel");
+    if (!res->k || !res->v || !res->lens) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: residual NULL pointer");
+    if (res->r_cap <= 0) return fail(VECINFER_ERR_SHAPE, "attn_decode: residual r_cap <= 0");
+    if (!aligned(res->k, 16) || !aligned(res->v, 16) || res->stride_b % 8 || res->stride_h % 8 || res->stride_b < 0 ||
+        res->stride_h < 0)
+      return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: residual rows must be 16-byte aligned (strides multiple of 8)");
+  }
 
   AttnArgs a;
   a.q = static_cast<const uint16_t*>(q_bf16);
@@ -179,7 +188,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.part_l = S > 1 ? reinterpret_cast<float*>(ws + wl.part_l) : nullptr;
   a.part_o = S > 1 ? reinterpret_cast<float*>(ws + wl.part_o) : nullptr;
   a.phase = phase_buffer();
-  a.append = app != nullptr;
+  a.append = app != nullptr && !res_append;   // encode into the codes (not a residual append)
   a.knew = app ? static_cast<const uint16_t*>(app->k_new) : nullptr;
   a.vnew = app ? static_cast<const uint16_t*>(app->v_new) : nullptr;
   a.kn_sb = app ? app->kn_sb : 0; a.kn_sh = app ? app->kn_sh : 0;
@@ -190,6 +199,15 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.kcodes_w = const_cast<uint8_t*>(k_codes);
   a.vcodes_w = const_cast<uint8_t*>(v_codes);
   a.inv_sqrt_d = static_cast<float>(1.0 / sqrt(128.0));
+  a.res = res != nullptr;
+  a.kres = res ? static_cast<const uint16_t*>(res->k) : nullptr;
+  a.vres = res ? static_cast<const uint16_t*>(res->v) : nullptr;
+  a.res_sb = res ? res->stride_b : 0;
+  a.res_sh = res ? res->stride_h : 0;
+  a.r_cap = res ? res->r_cap : 0;
+  a.res_lens = res ? res->lens : nullptr;
+  a.res_append = res_append ? 1 : 0;
+  a.qscale_raw = static_cast<float>(static_cast<double>(softmax_scale) * 1.4426950408889634);
   cudaStream_t st = as_stream(stream);
   if (algo == VECINFER_ATTN_LUT) {
     launch_attn_lut(a, kcfg.code_bits, vcfg.code_bits, st);
@@ -218,10 +236,11 @@ extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B,
                                                   const int32_t* seq_lens, int64_t tok_begin, int64_t tok_end,
                                                   float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
                                                   void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
-                                                  size_t workspace_bytes, vecinfer_stream_t stream) {
+                                                  size_t workspace_bytes, vecinfer_stream_t stream,
+                                                  const vecinfer_residual_t* residual) {
   return attn_impl(q_bf16, B, H_q, H_kv, q_stride_b, q_stride_h, lambda, ck_bf16, cv_bf16, ck_head_stride,
                    cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, tok_begin, tok_end, softmax_scale,
-                   num_splits, algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr);
+                   num_splits, algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false);
 }
 
 extern "C" size_t vecinfer_decode_step_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int64_t n_cap,
@@ -240,7 +259,8 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
                                                   const int32_t* seq_lens, float softmax_scale, int32_t num_splits,
                                                   vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype,
                                                   float* lse, uint32_t* err_flags, void* workspace,
-                                                  size_t workspace_bytes, vecinfer_stream_t stream) {
+                                                  size_t workspace_bytes, vecinfer_stream_t stream,
+                                                  const vecinfer_residual_t* residual) {
   if (!k_new_bf16 || !v_new_bf16 || !inv_lambda || !write_pos || !q_strides || !k_new_strides || !v_new_strides)
     return fail(VECINFER_ERR_INVALID_ARG, "decode_step: NULL pointer");
   for (int i = 0; i < 2; ++i)
@@ -248,6 +268,14 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
       return fail(VECINFER_ERR_INVALID_ARG, "decode_step: k_new/v_new strides must be non-negative multiples of 4");
   if (!aligned(k_new_bf16, 8) || !aligned(v_new_bf16, 8) || !aligned(inv_lambda, 16))
     return fail(VECINFER_ERR_INVALID_ARG, "decode_step: misaligned k_new/v_new/inv_lambda");
+  if (residual && residual->append_new) {   // the new token goes to the residual window (raw copy)
+    if (algo == VECINFER_ATTN_LUT) return fail(VECINFER_ERR_UNSUPPORTED, "decode_step: residual needs the MMA kernel");
+    AppendArgs app{k_new_bf16, v_new_bf16, k_new_strides[0], k_new_strides[1], v_new_strides[0], v_new_strides[1],
+                   inv_lambda, write_pos, err_flags};
+    return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
+                     cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
+                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, true);
+  }
   // Fuse only when the grid is one wave: the owner CTA's encode latency (~1-2 us) then hides
   // behind the other CTAs' longer splits; with several waves every wave would carry it, and a
   // separate append launch (latency ~3 us, once) is cheaper.
@@ -275,11 +303,11 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
     if (st != VECINFER_OK) return st;
     return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
-                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr);
+                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false);
   }
   AppendArgs app{k_new_bf16, v_new_bf16, k_new_strides[0], k_new_strides[1], v_new_strides[0], v_new_strides[1],
                  inv_lambda, write_pos, err_flags};
   return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                    cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
-                   algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app);
+                   algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, false);
 }

@@ -280,6 +280,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     sbest[warp * 32 + lane] = best;
     sidx[warp * 32 + lane] = bi;
   }
+  const bool res_cta = a.res && s == a.S - 1;   // this CTA attends the residual window
+  if (res_cta && a.res_append && warp < 2) {
+    // decode step into the residual window: raw bf16 copy of the new k (warp 0) / v (warp 1)
+    const int64_t pr = static_cast<int64_t>(a.res_lens[b]) - 1;
+    if (pr >= 0 && pr < a.r_cap) {
+      const uint16_t* src = (warp == 0 ? a.knew + b * a.kn_sb + h * a.kn_sh : a.vnew + b * a.vn_sb + h * a.vn_sh);
+      uint16_t* dst = const_cast<uint16_t*>(warp == 0 ? a.kres : a.vres) + b * a.res_sb + h * a.res_sh + pr * 128;
+      reinterpret_cast<uint2*>(dst)[lane] = reinterpret_cast<const uint2*>(src)[lane];
+    } else if (lane == 0 && a.err) {
+      atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
+    }
+  }
   if (warp < 4) query_transform_warp(a, b, h, warp, sq + 128 * warp);
   __syncthreads();
   if (kCanAppend && owner) {
@@ -436,6 +448,63 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         mma_16816(acc[2 * u + 1], prmt(g0.y, g1.y, 0x5410), prmt(g0.y, g1.y, 0x7632), prmt(g2.y, g3.y, 0x5410),
                   prmt(g2.y, g3.y, 0x7632), bp0, bp1);
       });
+    }
+  }
+
+  // ---- residual window (NEXT-1): tokens t = warp, warp + 16, ... of the raw bf16 rows, scored
+  // with the raw q (q k^T = q~ k~^T, Eq. 7) and folded into this warp's online-softmax state; the
+  // P.V goes straight into the hi slots of the MMA accumulator layout (thread (r, j) owns head j,
+  // dims 16r + 2t + {0, 1}).  Plain (coherent) loads: rows may have been appended by this CTA.
+  if (res_cta) {
+    const int rlen = min(a.res_lens[b], static_cast<int32_t>(a.r_cap));
+    if (rlen > 0) {
+      float qr[4][4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        if (g < a.G) {
+          const float4 v = bf16x4_to_float4(
+              *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (h * a.G + g) * a.q_sh + 4 * lane));
+          qr[g][0] = v.x * a.qscale_raw; qr[g][1] = v.y * a.qscale_raw;
+          qr[g][2] = v.z * a.qscale_raw; qr[g][3] = v.w * a.qscale_raw;
+        } else {
+          qr[g][0] = qr[g][1] = qr[g][2] = qr[g][3] = 0.f;
+        }
+      }
+      const uint16_t* kr = a.kres + b * a.res_sb + h * a.res_sh;
+      const uint16_t* vr = a.vres + b * a.res_sb + h * a.res_sh;
+      for (int t = warp; t < rlen; t += kNW) {
+        const float4 kv = bf16x4_to_float4(*reinterpret_cast<const uint2*>(kr + t * 128 + 4 * lane));
+        float sg[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float v = qr[g][0] * kv.x + qr[g][1] * kv.y + qr[g][2] * kv.z + qr[g][3] * kv.w;
+#pragma unroll
+          for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+          sg[g] = v;
+        }
+        const float sj = j == 0 ? sg[0] : j == 1 ? sg[1] : j == 2 ? sg[2] : sg[3];
+        if (__any_sync(0xffffffffu, sj > m_run + kTau)) {
+          const bool need = sj > m_run + kTau;       // uniform over the 8 lanes of head j
+          const float m_new = need ? sj : m_run;
+          const float alpha = need ? ex2_approx(m_run - m_new) : 1.f;
+#pragma unroll
+          for (int tt = 0; tt < 8; ++tt) {
+            acc[tt][0] *= alpha; acc[tt][1] *= alpha; acc[tt][2] *= alpha; acc[tt][3] *= alpha;
+          }
+          l_run *= alpha;
+          m_run = m_new;
+        }
+        const float p = ex2_approx(sj - (m_run == -INFINITY ? 0.f : m_run));
+        if (r == 0) l_run += p;                         // once per head (lanes r=0 of each j)
+        const uint4 v0 = *reinterpret_cast<const uint4*>(vr + t * 128 + 16 * r);
+        const uint4 v1 = *reinterpret_cast<const uint4*>(vr + t * 128 + 16 * r + 8);
+        const uint32_t vw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) {
+          acc[tt][0] += p * __uint_as_float(vw[tt] << 16);             // dim 16r + 2tt
+          acc[tt][2] += p * __uint_as_float(vw[tt] & 0xFFFF0000u);     // dim 16r + 2tt + 1
+        }
+      }
     }
   }
 

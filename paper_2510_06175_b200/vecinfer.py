@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import VQ, I64x2, I64x3, check
+from ._lib import VQ, I64x2, I64x3, Residual, check
 
 _lib.load()   # fail loudly at import if the native library is missing
 
@@ -65,6 +65,18 @@ def _need(t: torch.Tensor, name: str, dtype=None):
 def _cb_stride(cb: torch.Tensor) -> int:
     """[H_kv, 2^b, d] -> elements between heads; [2^b, d] (shared) -> 0."""
     return 0 if cb.dim() == 2 else cb.stride(0)
+
+
+def _residual(k_res, v_res, res_lens, append_new=False):
+    """vecinfer_residual_t for bf16 [B, H_kv, r_cap, D] residual windows (None -> NULL)."""
+    if k_res is None:
+        return None
+    if k_res.shape != v_res.shape or k_res.stride() != v_res.stride() or k_res.stride(2) != k_res.shape[3]:
+        raise ValueError("k_res/v_res must be [B, H_kv, r_cap, D] with identical strides and contiguous rows")
+    r = Residual(_need(k_res, "k_res", torch.bfloat16).value, _need(v_res, "v_res", torch.bfloat16).value,
+                 k_res.stride(0), k_res.stride(1), k_res.shape[2], _need(res_lens, "res_lens", torch.int32).value,
+                 1 if append_new else 0)
+    return ctypes.pointer(r)
 
 
 def calibrate_smooth(k_cal: torch.Tensor, eps: float = 1e-6):
@@ -132,8 +144,10 @@ def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.
                 softmax_scale: float | None = None, num_splits: int = 0, algo: str = "auto",
                 kcfg: VQConfig = B2D4, vcfg: VQConfig = B2D4, o_dtype: torch.dtype = torch.float32,
                 out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
-                workspace: torch.Tensor | None = None):
-    """Decode attention of q [B, H_q, D] (bf16) over the VQ cache (Eq. 10 / Alg. 1).
+                workspace: torch.Tensor | None = None, k_res: torch.Tensor | None = None,
+                v_res: torch.Tensor | None = None, res_lens: torch.Tensor | None = None):
+    """Decode attention of q [B, H_q, D] (bf16) over the VQ cache (Eq. 10 / Alg. 1), plus an optional
+    full-precision residual window k_res/v_res [B, H_kv, r_cap, D] with res_lens [B].
     Returns (o [B, H_q, D] o_dtype, lse [B, H_q] fp32, natural log)."""
     B, Hq, D = q.shape
     Hkv, n_cap = k_codes.shape[1], k_codes.shape[2]
@@ -157,7 +171,7 @@ def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.
         kcfg.c(), vcfg.c(), _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
         _need(seq_lens, "seq_lens", torch.int32), tok_begin, tok_end, softmax_scale, num_splits, ALGOS[algo],
         _need(out, "out"), odt, _need(lse, "lse", torch.float32), ctypes.c_void_p(workspace.data_ptr()),
-        workspace.numel(), _stream(q.device)))
+        workspace.numel(), _stream(q.device), _residual(k_res, v_res, res_lens)))
     return out, lse
 
 
@@ -167,9 +181,13 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
                 softmax_scale: float | None = None, num_splits: int = 0, algo: str = "auto",
                 kcfg: VQConfig = B2D4, vcfg: VQConfig = B2D4, o_dtype: torch.dtype = torch.float32,
                 out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
-                err_flags: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+                err_flags: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                k_res: torch.Tensor | None = None, v_res: torch.Tensor | None = None,
+                res_lens: torch.Tensor | None = None, append_to_residual: bool = False):
     """Fused layer decode step = encode_kv(T=1) of k_new/v_new [B, H_kv, D] at row write_pos[b]
-    followed by attn_decode over [0, seq_lens[b]) -- one launch (vecinfer_decode_step)."""
+    followed by attn_decode over [0, seq_lens[b]) -- one launch (vecinfer_decode_step).  With a
+    residual window and append_to_residual, the new token is copied to residual row res_lens[b]-1
+    instead (no encode) and attended from there."""
     B, Hq, D = q.shape
     Hkv, n_cap = k_codes.shape[1], k_codes.shape[2]
     if softmax_scale is None:
@@ -195,7 +213,8 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
         num_splits, ALGOS[algo], _need(out, "out"), F32 if out.dtype == torch.float32 else BF16,
         _need(lse, "lse", torch.float32),
         ctypes.c_void_p(err_flags.data_ptr()) if err_flags is not None else ctypes.c_void_p(0),
-        ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream(q.device)))
+        ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream(q.device),
+        _residual(k_res, v_res, res_lens, append_to_residual)))
     return out, lse
 
 

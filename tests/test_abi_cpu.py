@@ -38,7 +38,7 @@ def test_every_declared_symbol_is_exported(lib):
     for name in declared_functions():
         assert hasattr(lib, name), f"{name} not exported"
         assert name in _lib.PROTOTYPES, f"{name} missing from the Python prototypes"
-    assert lib.vecinfer_abi_version() == 1
+    assert lib.vecinfer_abi_version() == 2
 
 
 def test_library_contains_sm100a_code(lib):
@@ -55,7 +55,7 @@ def test_argument_validation_without_cuda(lib):
     from paper_2510_06175_b200._lib import VQ, I64x3
     cfg = VQ(128, 4, 8)
     st = lib.vecinfer_attn_decode(None, 1, 32, 8, 0, 0, None, None, None, 0, 0, cfg, cfg, None, None, 16, None, 0, -1,
-                                  0.088, 0, 0, None, 1, None, None, 0, None)
+                                  0.088, 0, 0, None, 1, None, None, 0, None, None)
     assert st == 1 and b"NULL" in lib.vecinfer_last_error()
     st = lib.vecinfer_merge_lse(None, None, 1, 1, 1, 128, None, 1, None, None)
     assert st == 1

@@ -459,3 +459,77 @@ def test_cfg5_full_size_sampled_units(bits):
         cvh = cv[h] if cv.ndim == 3 else cv
         o_ref, L_ref = ref.attention_vq(q[0, 4 * h:4 * h + 4], CB["lambda"][h], ckh, cvh, kk, vv)
         _assert_close(o[0, 4 * h:4 * h + 4], L[0, 4 * h:4 * h + 4], o_ref, L_ref)
+
+
+# ----------------------------------------------- residual window
+def _res_case(B, n_q, r_lens, r_cap, seed):
+    c = _attn_case(B, 8, 4, max(n_q) + 4, n_q, seed=seed)
+    c["K_res"] = synth.gen_keys(r_cap, 8, 128, seed=seed + 7, batch=B).transpose(0, 2, 1, 3).copy()
+    c["V_res"] = synth.gen_values(r_cap, 8, 128, seed=seed + 8, batch=B).transpose(0, 2, 1, 3).copy()
+    c["res_lens"] = np.asarray(r_lens)
+    return c
+
+
+def _run_ref_res(c):
+    return ref.attention_decode_batch(c["q"], c["lam"], c["ck"], c["cv"], c["kc"], c["vc"], c["seq_lens"],
+                                      K_res=c["K_res"], V_res=c["V_res"], res_lens=c["res_lens"])
+
+
+@pytest.mark.parametrize("splits", [0, 1, 3, 8, 18])
+@pytest.mark.parametrize("n_q,r_lens", [([3000, 700], [128, 5]), ([0, 1000], [17, 0]), ([64, 64], [1, 256])])
+def test_attn_residual_window(splits, n_q, r_lens):
+    c = _res_case(2, n_q, r_lens, 256, seed=130 + splits)
+    o, L = vi.attn_decode(t_bf16(c["q"]), t_f32(c["lam"]), t_bf16(c["ck"]), t_bf16(c["cv"]), t_u8(c["kc"]),
+                          t_u8(c["vc"]), t_i32(c["seq_lens"]), num_splits=splits, k_res=t_bf16(c["K_res"]),
+                          v_res=t_bf16(c["V_res"]), res_lens=t_i32(c["res_lens"]))
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref_res(c))
+
+
+def test_decode_step_appends_to_residual():
+    c = _res_case(2, [2000, 300], [40, 1], 128, seed=140)
+    kn = synth.gen_keys(1, 8, 128, seed=141, batch=2)[:, 0]
+    vn = synth.gen_values(1, 8, 128, seed=142, batch=2)[:, 0]
+    kr, vr = t_bf16(c["K_res"]), t_bf16(c["V_res"])
+    lens = np.array([41, 2])                       # the new token becomes row lens-1
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(c["ck"]), t_bf16(c["cv"]), t_u8(c["kc"]), t_u8(c["vc"]), t_i32([0, 0]),
+                          t_i32(c["seq_lens"]), k_res=kr, v_res=vr, res_lens=t_i32(lens), append_to_residual=True)
+    for b in range(2):
+        c["K_res"][b, :, lens[b] - 1] = kn[b]
+        c["V_res"][b, :, lens[b] - 1] = vn[b]
+    assert np.array_equal(kr.float().cpu().numpy(), c["K_res"]) and np.array_equal(vr.float().cpu().numpy(), c["V_res"])
+    c["res_lens"] = lens
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref_res(c))
+
+
+def test_vqkv_cache_protocol_replay():
+    """Cache manager (residual R = 8, flush of the oldest 8 rows when 16 are held) over 40 decode
+    steps vs the oracle replay: flushed tokens are the ORACLE's codes, the window is raw."""
+    from paper_2510_06175_b200.cache import VQKVCache
+    B, R, steps = 2, 8, 40
+    cache = VQKVCache(B, 8, 256, t_f32(CB["lambda"]), t_f32(CB["inv_lambda"]), t_bf16(CB["ck_b2d4"]),
+                      t_bf16(CB["cv_b2d4"]), residual=R)
+    ks = synth.gen_keys(steps, 8, 128, seed=150, batch=B)          # [B, steps, H, D]
+    vs = synth.gen_values(steps, 8, 128, seed=151, batch=B)
+    qs = [synth.gen_queries(B, 32, 8, 128, seed=200 + i) for i in range(steps)]
+    n_q = 0
+    for i in range(steps):
+        o, L = cache.step(t_bf16(qs[i]), t_bf16(ks[:, i]), t_bf16(vs[:, i]))
+        n_tot = i + 1
+        if n_tot - n_q > 2 * R:     # the cache flushed before this step's append
+            n_q += R
+        kc = np.zeros((B, 8, max(n_q, 1), 32), np.int64)
+        vc = np.zeros_like(kc)
+        for b in range(B):
+            for h in range(8):
+                if n_q:
+                    kk, vv = ref.encode_kv(ks[b, :n_q, h], vs[b, :n_q, h], CB["inv_lambda"][h], CB["ck_b2d4"][h],
+                                           CB["cv_b2d4"][h])
+                    kc[b, h, :n_q], vc[b, h, :n_q] = kk, vv
+        o_ref, L_ref = ref.attention_decode_batch(
+            qs[i], CB["lambda"], CB["ck_b2d4"], CB["cv_b2d4"], kc, vc, [n_q] * B,
+            K_res=ks[:, n_q:n_tot].transpose(0, 2, 1, 3), V_res=vs[:, n_q:n_tot].transpose(0, 2, 1, 3),
+            res_lens=[n_tot - n_q] * B)
+        _assert_close(o.cpu().numpy(), L.cpu().numpy(), o_ref, L_ref)
+    assert cache.n_q == n_q == 24 and cache.n_r == 16
+    assert np.array_equal(cache.kc[:, :, :n_q].cpu().numpy(), kc.astype(np.uint8))
