@@ -226,7 +226,14 @@ def run_ours(args, rank, world, local_rank):
     kcs = [kc0] + [kc0.clone() for _ in range(L - 1)]
     vcs = [vc0] + [vc0.clone() for _ in range(L - 1)]
     # cache layout seen by the kernels: rows [0, n_local) of this rank's shard
-    seq_lens = torch.full((B,), n_local, dtype=torch.int32, device=dev)
+    R = args.residual if not seq_sharded else 0
+    seq_lens = torch.full((B,), n_local - R, dtype=torch.int32, device=dev)
+    if R:   # full-precision window: the newest R tokens as raw bf16 rows (per layer), kept at R rows
+        kres = [torch.from_numpy(synth.gen_keys(R, H_KV, D, seed=500 + l, batch=B)).to(dev).to(torch.bfloat16)
+                .permute(0, 2, 1, 3).contiguous() for l in range(L)]
+        vres = [torch.from_numpy(synth.gen_values(R, H_KV, D, seed=600 + l, batch=B)).to(dev).to(torch.bfloat16)
+                .permute(0, 2, 1, 3).contiguous() for l in range(L)]
+        res_lens = torch.full((B,), R, dtype=torch.int32, device=dev)
     owns_tail = (not seq_sharded) or (tok1 == N)
     write_pos = torch.full((B,), n_local - 1, dtype=torch.int32, device=dev)
     q_all = torch.from_numpy(np.stack([synth.gen_queries(B, H_Q, H_KV, D, seed=50 + l) for l in range(L)])).to(dev).to(torch.bfloat16)
@@ -243,9 +250,15 @@ def run_ours(args, rank, world, local_rank):
 
     fused = not args.unfused and not seq_sharded
     # vecinfer_decode_step itself fuses only single-wave grids with <= 8-bit codes
-    fused_launch = fused and kbits <= 8 and vbits <= 8 and vi.attn_num_splits(B, H_KV, n_local, 0) * B * H_KV <= 148
+    fused_launch = fused and (bool(R) or (kbits <= 8 and vbits <= 8 and
+                                          vi.attn_num_splits(B, H_KV, n_local, 0) * B * H_KV <= 148))
 
     def layer(l, ev_pair=None):
+        if fused and R:   # one launch: the new token goes to residual row R-1, attention over codes + window
+            vi.decode_step(q_all[l], kn_all[l][:, 0], vn_all[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
+                           seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l],
+                           k_res=kres[l], v_res=vres[l], res_lens=res_lens, append_to_residual=True)
+            return
         if fused:   # one launch: append-encode of the new token + attention (vecinfer_decode_step)
             vi.decode_step(q_all[l], kn_all[l][:, 0], vn_all[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
                            seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l])
@@ -366,7 +379,9 @@ def run_ours(args, rank, world, local_rank):
         for l in range(L):
             if fused:
                 vi.decode_step(q_d[l], kn_d[l][:, 0], vn_d[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
-                               seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l])
+                               seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l],
+                               **({"k_res": kres[l], "v_res": vres[l], "res_lens": res_lens,
+                                   "append_to_residual": True} if R else {}))
                 continue
             if owns_tail:
                 vi.encode_kv(kn_d[l], vn_d[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg, workspace=enc_ws)
@@ -406,7 +421,8 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     # ---- figures
-    code_bytes_rank = B * H_KV * n_local * unit_bytes           # K + V codes per layer call
+    # K + V bytes per layer call: codes of the quantised tokens + raw bf16 rows of the residual window
+    code_bytes_rank = B * H_KV * ((n_local - R) * unit_bytes + R * 2 * D * 2)
     total_bytes = code_bytes_rank * L * K * (world if not seq_sharded else 1)
     if seq_sharded:
         total_bytes = B * H_KV * N * unit_bytes * L * K
@@ -435,7 +451,7 @@ def run_ours(args, rank, world, local_rank):
                    "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": f"K-{CB_NAME[kbits]}/V-{CB_NAME[vbits]}",
                    "parallelism": ("seq-shard" if seq_sharded else "dp") + str(world),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
-                   "num_splits": S, "cuda_graph": use_graph, "fused_append": fused_launch,
+                   "num_splits": S, "cuda_graph": use_graph, "residual_window": R, "fused_append": fused_launch,
                    "dtype_detail": "u8 codes, bf16 q/k/v/o, fp16 hi/lo MMA operands, f32 accumulate"},
         "us_per_layer_call": step_ms * 1e3 / L,
         "tokens_per_s": B_glob * 1e3 / step_ms,
@@ -469,6 +485,8 @@ def main():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N>1 (gloo: ranks may share one GPU; functional check)")
     ap.add_argument("--unfused", action="store_true", help="separate encode_kv + attn_decode launches per layer")
+    ap.add_argument("--residual", type=int, default=0,
+                    help="full-precision residual window of R tokens (P:494: 128); the step appends into it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=2.0)

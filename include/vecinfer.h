@@ -171,7 +171,7 @@ vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int
  *   num_splits  0 = heuristic (fill 148 SMs); > 0 fixed => bitwise-deterministic results.
  *   o           [B, H_q, D] bf16 or fp32 (o_dtype); lse fp32 [B, H_q] natural log.
  *               An empty range yields o = 0, lse = -inf (weight 0 in vecinfer_merge_lse).
- *   residual    optional full-precision window (NULL = none), attended by the last split;
+ *   residual    optional full-precision window (NULL = none); row t is attended by split t % S;
  *               LUT variant: not supported (VECINFER_ERR_UNSUPPORTED).
  *   workspace   >= vecinfer_attn_workspace_bytes(B, H_q, H_kv, D, n_tokens_max, num_splits)
  *               bytes, where n_tokens_max bounds the attended range; MUST be zero-filled once

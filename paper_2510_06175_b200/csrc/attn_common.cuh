@@ -40,8 +40,8 @@ struct AttnArgs {
   uint8_t* kcodes_w;        // writable views of the code caches
   uint8_t* vcodes_w;
   float inv_sqrt_d;
-  // full-precision residual window (NEXT-1), attended by the last split; res_append: the new token
-  // goes to residual row res_lens[b]-1 (raw bf16 copy) instead of the codes
+  // full-precision residual window (NEXT-1): row t is attended by split t % S, warp (t / S) % 16;
+  // res_append: the new token goes to residual row res_lens[b]-1 (raw bf16 copy), not the codes
   int res;
   const uint16_t* kres;  // bf16 [B, H_kv, r_cap, 128]
   const uint16_t* vres;
@@ -51,8 +51,6 @@ struct AttnArgs {
   float qscale_raw;      // softmax_scale * log2(e): raw-query scale for the residual scores
 };
 
-// extra tokens' worth of work of the split that attends the residual window
-constexpr int64_t kResidualTokenCost = 256;
 
 // extra tokens' worth of work the split owning the appended row does (its encode), used to
 // shorten that split so it does not become the straggler
@@ -70,7 +68,7 @@ __device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int
   if (pbeg) *pbeg = beg;
   if (pend) *pend = e;
   const int64_t n = e - beg;
-  const int64_t extra = a.S > 1 ? ((a.append ? kAppendTokenCost : 0) + (a.res ? kResidualTokenCost : 0)) : 0;
+  const int64_t extra = a.S > 1 && a.append ? kAppendTokenCost : 0;
   int64_t chunk = (n + extra + a.S - 1) / a.S;
   chunk = (chunk + 31) & ~int64_t(31);
   r0 = beg + s * chunk;

@@ -280,16 +280,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     sbest[warp * 32 + lane] = best;
     sidx[warp * 32 + lane] = bi;
   }
-  const bool res_cta = a.res && s == a.S - 1;   // this CTA attends the residual window
-  if (res_cta && a.res_append && warp < 2) {
-    // decode step into the residual window: raw bf16 copy of the new k (warp 0) / v (warp 1)
-    const int64_t pr = static_cast<int64_t>(a.res_lens[b]) - 1;
-    if (pr >= 0 && pr < a.r_cap) {
-      const uint16_t* src = (warp == 0 ? a.knew + b * a.kn_sb + h * a.kn_sh : a.vnew + b * a.vn_sb + h * a.vn_sh);
-      uint16_t* dst = const_cast<uint16_t*>(warp == 0 ? a.kres : a.vres) + b * a.res_sb + h * a.res_sh + pr * 128;
-      reinterpret_cast<uint2*>(dst)[lane] = reinterpret_cast<const uint2*>(src)[lane];
-    } else if (lane == 0 && a.err) {
-      atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
+  // residual window rows handled by this warp: t = s + S * (warp + kNW * k), first one preloaded
+  // here so its latency hides behind the prologue; the appended row (decode step into the
+  // window) is taken from k_new / v_new by its owner warp, which also writes it to the window
+  const int rlen = a.res ? min(a.res_lens[b], static_cast<int32_t>(a.r_cap)) : 0;
+  const int t_res0 = s + a.S * warp;
+  const int64_t res_off = a.res ? b * a.res_sb + h * a.res_sh : 0;
+  uint2 rk = make_uint2(0u, 0u);
+  uint4 rv0 = make_uint4(0u, 0u, 0u, 0u), rv1 = rv0;
+  if (t_res0 < rlen) {
+    const bool is_new = a.res_append && t_res0 == rlen - 1;
+    const uint16_t* krow = is_new ? a.knew + b * a.kn_sb + h * a.kn_sh : a.kres + res_off + t_res0 * 128;
+    const uint16_t* vrow = is_new ? a.vnew + b * a.vn_sb + h * a.vn_sh : a.vres + res_off + t_res0 * 128;
+    rk = *reinterpret_cast<const uint2*>(krow + 4 * lane);
+    rv0 = *reinterpret_cast<const uint4*>(vrow + 16 * r);
+    rv1 = *reinterpret_cast<const uint4*>(vrow + 16 * r + 8);
+    if (is_new) {   // write the new token's raw rows into the window (this warp is the only writer)
+      reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.kres) + res_off + t_res0 * 128)[lane] = rk;
+      reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.vres) + res_off + t_res0 * 128)[lane] =
+          *reinterpret_cast<const uint2*>(vrow + 4 * lane);
     }
   }
   if (warp < 4) query_transform_warp(a, b, h, warp, sq + 128 * warp);
@@ -345,6 +354,64 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 #pragma unroll
   for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
   float m_run = -INFINITY, l_run = 0.f;
+
+  // ---- residual window (NEXT-1): raw bf16 rows scored with the raw q (q k^T = q~ k~^T, Eq. 7),
+  // folded into this warp's online-softmax state before the code tiles; the P.V goes into the hi
+  // slots of the MMA accumulator layout (thread (r, j) owns head j, dims 16r + 2t + {0, 1})
+  if (t_res0 < rlen) {
+    float qr[4][4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const float4 v = g < a.G ? bf16x4_to_float4(*reinterpret_cast<const uint2*>(
+                                     a.q + b * a.q_sb + (h * a.G + g) * a.q_sh + 4 * lane))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      qr[g][0] = v.x * a.qscale_raw; qr[g][1] = v.y * a.qscale_raw;
+      qr[g][2] = v.z * a.qscale_raw; qr[g][3] = v.w * a.qscale_raw;
+    }
+    for (int t = t_res0; t < rlen; t += a.S * kNW) {
+      if (t != t_res0) {   // rows beyond the first (long windows, few splits)
+        const uint16_t* krow = a.kres + res_off + t * 128;
+        const uint16_t* vrow = a.vres + res_off + t * 128;
+        const bool is_new = a.res_append && t == rlen - 1;
+        rk = *reinterpret_cast<const uint2*>((is_new ? a.knew + b * a.kn_sb + h * a.kn_sh : krow) + 4 * lane);
+        const uint16_t* vsrc = is_new ? a.vnew + b * a.vn_sb + h * a.vn_sh : vrow;
+        rv0 = *reinterpret_cast<const uint4*>(vsrc + 16 * r);
+        rv1 = *reinterpret_cast<const uint4*>(vsrc + 16 * r + 8);
+        if (is_new) {
+          reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.kres) + res_off + t * 128)[lane] = rk;
+          reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.vres) + res_off + t * 128)[lane] =
+              *reinterpret_cast<const uint2*>(vsrc + 4 * lane);
+        }
+      }
+      const float4 kv = bf16x4_to_float4(rk);
+      float sg[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        float v = qr[g][0] * kv.x + qr[g][1] * kv.y + qr[g][2] * kv.z + qr[g][3] * kv.w;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        sg[g] = v;
+      }
+      const float sj = j == 0 ? sg[0] : j == 1 ? sg[1] : j == 2 ? sg[2] : sg[3];
+      if (sj > m_run + kTau) {   // per-lane: all 8 lanes of head j agree
+        const float alpha = ex2_approx(m_run - sj);
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) {
+          acc[tt][0] *= alpha; acc[tt][1] *= alpha; acc[tt][2] *= alpha; acc[tt][3] *= alpha;
+        }
+        l_run *= alpha;
+        m_run = sj;
+      }
+      const float p = ex2_approx(sj - m_run);
+      if (r == 0) l_run += p;                         // once per head (lanes r = 0 of each j)
+      const uint32_t vw[8] = {rv0.x, rv0.y, rv0.z, rv0.w, rv1.x, rv1.y, rv1.z, rv1.w};
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt) {
+        acc[tt][0] += p * __uint_as_float(vw[tt] << 16);             // dim 16r + 2tt
+        acc[tt][2] += p * __uint_as_float(vw[tt] & 0xFFFF0000u);     // dim 16r + 2tt + 1
+      }
+    }
+  }
 
   for (int it = warp; it < ntile; it += kNW) {
     TileCodes<KB, VB> cur = nxt;
@@ -448,63 +515,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         mma_16816(acc[2 * u + 1], prmt(g0.y, g1.y, 0x5410), prmt(g0.y, g1.y, 0x7632), prmt(g2.y, g3.y, 0x5410),
                   prmt(g2.y, g3.y, 0x7632), bp0, bp1);
       });
-    }
-  }
-
-  // ---- residual window (NEXT-1): tokens t = warp, warp + 16, ... of the raw bf16 rows, scored
-  // with the raw q (q k^T = q~ k~^T, Eq. 7) and folded into this warp's online-softmax state; the
-  // P.V goes straight into the hi slots of the MMA accumulator layout (thread (r, j) owns head j,
-  // dims 16r + 2t + {0, 1}).  Plain (coherent) loads: rows may have been appended by this CTA.
-  if (res_cta) {
-    const int rlen = min(a.res_lens[b], static_cast<int32_t>(a.r_cap));
-    if (rlen > 0) {
-      float qr[4][4];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        if (g < a.G) {
-          const float4 v = bf16x4_to_float4(
-              *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (h * a.G + g) * a.q_sh + 4 * lane));
-          qr[g][0] = v.x * a.qscale_raw; qr[g][1] = v.y * a.qscale_raw;
-          qr[g][2] = v.z * a.qscale_raw; qr[g][3] = v.w * a.qscale_raw;
-        } else {
-          qr[g][0] = qr[g][1] = qr[g][2] = qr[g][3] = 0.f;
-        }
-      }
-      const uint16_t* kr = a.kres + b * a.res_sb + h * a.res_sh;
-      const uint16_t* vr = a.vres + b * a.res_sb + h * a.res_sh;
-      for (int t = warp; t < rlen; t += kNW) {
-        const float4 kv = bf16x4_to_float4(*reinterpret_cast<const uint2*>(kr + t * 128 + 4 * lane));
-        float sg[4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          float v = qr[g][0] * kv.x + qr[g][1] * kv.y + qr[g][2] * kv.z + qr[g][3] * kv.w;
-#pragma unroll
-          for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-          sg[g] = v;
-        }
-        const float sj = j == 0 ? sg[0] : j == 1 ? sg[1] : j == 2 ? sg[2] : sg[3];
-        if (__any_sync(0xffffffffu, sj > m_run + kTau)) {
-          const bool need = sj > m_run + kTau;       // uniform over the 8 lanes of head j
-          const float m_new = need ? sj : m_run;
-          const float alpha = need ? ex2_approx(m_run - m_new) : 1.f;
-#pragma unroll
-          for (int tt = 0; tt < 8; ++tt) {
-            acc[tt][0] *= alpha; acc[tt][1] *= alpha; acc[tt][2] *= alpha; acc[tt][3] *= alpha;
-          }
-          l_run *= alpha;
-          m_run = m_new;
-        }
-        const float p = ex2_approx(sj - (m_run == -INFINITY ? 0.f : m_run));
-        if (r == 0) l_run += p;                         // once per head (lanes r=0 of each j)
-        const uint4 v0 = *reinterpret_cast<const uint4*>(vr + t * 128 + 16 * r);
-        const uint4 v1 = *reinterpret_cast<const uint4*>(vr + t * 128 + 16 * r + 8);
-        const uint32_t vw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-        for (int tt = 0; tt < 8; ++tt) {
-          acc[tt][0] += p * __uint_as_float(vw[tt] << 16);             // dim 16r + 2tt
-          acc[tt][2] += p * __uint_as_float(vw[tt] & 0xFFFF0000u);     // dim 16r + 2tt + 1
-        }
-      }
     }
   }
 
