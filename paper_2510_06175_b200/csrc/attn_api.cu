@@ -43,7 +43,7 @@ WsLayout ws_layout(int32_t B, int32_t H_kv, int32_t S) {
   WsLayout w;
   const size_t units = static_cast<size_t>(B) * H_kv;
   w.counter = 0;
-  w.part_l = ((units * sizeof(uint32_t)) + 255) & ~size_t(255);
+  w.part_l = ((2 * units * sizeof(uint32_t)) + 255) & ~size_t(255);   // arrive + depart counters
   w.part_o = w.part_l + ((units * S * 4 * sizeof(float) + 255) & ~size_t(255));
   w.total = w.part_o + units * S * 4 * 128 * sizeof(float);
   return w;
@@ -182,6 +182,9 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.S = S;
   a.cluster = plan.cluster;
   a.merge_kernel = (S > 1 && !plan.cluster && algo != VECINFER_ATTN_LUT) ? merge_mode_from_env() : 0;
+  // every CTA co-resident (one CTA per SM, grid <= SMs): spin-barrier + sliced merge
+  a.merge_spin = (S > 1 && !plan.cluster && !a.merge_kernel && algo != VECINFER_ATTN_LUT &&
+                  static_cast<int64_t>(B) * H_kv * S <= device_sm_count() && !getenv("VECINFER_NO_SPIN")) ? 1 : 0;
   a.o = o; a.o_f32 = (o_dtype == VECINFER_F32); a.lse = lse;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   a.counter = S > 1 ? reinterpret_cast<uint32_t*>(ws + wl.counter) : nullptr;

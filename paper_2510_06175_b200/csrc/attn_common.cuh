@@ -21,12 +21,13 @@ struct AttnArgs {
   int S;                       // splits per (b, h_kv)
   int cluster;                 // 1: the S splits of a (b, h_kv) form one cluster, merged over DSMEM
   int merge_kernel;            // 1: split partials are merged by a separate PDL-launched kernel
+  int merge_spin;              // 1: single-wave grid, every CTA merges a slice after an arrival barrier
   void* o;
   int o_f32;
   float* lse;
   float* part_o;     // [B*Hkv*S][4][128]
   float* part_l;     // [B*Hkv*S][4]   (log2 domain)
-  uint32_t* counter; // [B*Hkv]
+  uint32_t* counter; // [B*Hkv] arrivals (+ [B*Hkv] departures for merge_spin)
   unsigned long long* phase;  // profiling builds: per-CTA phase stamps (else null)
   // fused decode append (vecinfer_decode_step): encode the new token's k, v of each (b, h_kv)
   // into cache row write_pos[b] inside the attention launch (append == 0: plain attention)
@@ -166,6 +167,67 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     }
   }
   if (a.S == 1 || a.merge_kernel) return;
+  if (a.merge_spin) {
+    // Single-wave grid (all S CTAs of the unit are co-resident): publish, wait until all S arrived,
+    // then every CTA merges a 1/S slice of the 4 x 128 outputs (fixed order s = 0..S-1).  The last
+    // CTA to depart resets both counters for the next launch.
+    uint32_t* arrive = a.counter + unit;
+    uint32_t* depart = a.counter + static_cast<int64_t>(a.B) * a.Hkv + unit;
+    __syncthreads();
+    if (tid == 0) {
+      atom_add_acq_rel_gpu(arrive, 1u);
+      while (ld_acquire_gpu(arrive) < static_cast<uint32_t>(a.S)) __nanosleep(64);
+    }
+    __syncthreads();
+    phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
+    const int per = (4 * 128 + a.S - 1) / a.S;
+    const int idx = s * per + tid;
+    if (tid < per && idx < 4 * 128) {
+      const int g = idx >> 7, dim = idx & 127;
+      if (g < a.G) {
+        const float* pl = a.part_l + unit * a.S * 4 + g;
+        const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
+        float m = -INFINITY, wsum = 0.f, osum = 0.f;
+        for (int s0 = 0; s0 < a.S; s0 += 32) {
+          float lv[32], xv[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const bool ok = s0 + k < a.S;
+            lv[k] = ok ? __ldcg(pl + 4 * (s0 + k)) : -INFINITY;
+            xv[k] = ok ? __ldcg(po + static_cast<int64_t>(s0 + k) * 512) : 0.f;
+          }
+          float mc = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) mc = fmaxf(mc, lv[k]);
+          const float mn = fmaxf(m, mc);
+          if (mn == -INFINITY) continue;
+          const float sc = m == -INFINITY ? 0.f : ex2_approx(m - mn);
+          osum *= sc;
+          wsum *= sc;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float f = lv[k] == -INFINITY ? 0.f : ex2_approx(lv[k] - mn);
+            wsum += f;
+            osum += f * xv[k];
+          }
+          m = mn;
+        }
+        const bool empty = !(wsum > 0.f);
+        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+        const float ov = empty ? 0.f : osum / wsum;
+        if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
+        else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
+        if (dim == 0 && a.lse)
+          a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && atom_add_acq_rel_gpu(depart, 1u) == static_cast<uint32_t>(a.S - 1)) {
+      st_relaxed_gpu(arrive, 0u);
+      st_relaxed_gpu(depart, 0u);
+    }
+    return;
+  }
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 6);
   __syncthreads();
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 7);
