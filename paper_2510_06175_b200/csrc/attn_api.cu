@@ -43,7 +43,7 @@ WsLayout ws_layout(int32_t B, int32_t H_kv, int32_t S) {
   WsLayout w;
   const size_t units = static_cast<size_t>(B) * H_kv;
   w.counter = 0;
-  w.part_l = ((2 * units * sizeof(uint32_t)) + 255) & ~size_t(255);   // arrive + depart counters
+  w.part_l = ((units * sizeof(unsigned long long)) + 255) & ~size_t(255);   // 64-bit counters / barriers
   w.part_o = w.part_l + ((units * S * 4 * sizeof(float) + 255) & ~size_t(255));
   w.total = w.part_o + units * S * 4 * 128 * sizeof(float);
   return w;

@@ -27,7 +27,7 @@ struct AttnArgs {
   float* lse;
   float* part_o;     // [B*Hkv*S][4][128]
   float* part_l;     // [B*Hkv*S][4]   (log2 domain)
-  uint32_t* counter; // [B*Hkv] arrivals (+ [B*Hkv] departures for merge_spin)
+  uint32_t* counter; // [B*Hkv] 64-bit words: low half = last-CTA count, high half = spin epoch
   unsigned long long* phase;  // profiling builds: per-CTA phase stamps (else null)
   // fused decode append (vecinfer_decode_step): encode the new token's k, v of each (b, h_kv)
   // into cache row write_pos[b] inside the attention launch (append == 0: plain attention)
@@ -168,15 +168,19 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   }
   if (a.S == 1 || a.merge_kernel) return;
   if (a.merge_spin) {
-    // Single-wave grid (all S CTAs of the unit are co-resident): publish, wait until all S arrived,
-    // then every CTA merges a 1/S slice of the 4 x 128 outputs (fixed order s = 0..S-1).  The last
-    // CTA to depart resets both counters for the next launch.
-    uint32_t* arrive = a.counter + unit;
-    uint32_t* depart = a.counter + static_cast<int64_t>(a.B) * a.Hkv + unit;
+    // Single-wave grid (all S CTAs of the unit are co-resident): publish, then a sense-reversing
+    // barrier on a 64-bit word (high 32 bits: epoch, low 32: arrivals).  The last arriver resets
+    // the count and bumps the epoch with one release-add; the others wait for the epoch to change.
+    // Then every CTA merges a 1/S slice of the 4 x 128 outputs (fixed order s = 0..S-1).
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(a.counter) + unit;
     __syncthreads();
     if (tid == 0) {
-      atom_add_acq_rel_gpu(arrive, 1u);
-      while (ld_acquire_gpu(arrive) < static_cast<uint32_t>(a.S)) __nanosleep(64);
+      const unsigned long long old = atom_add_acq_rel_gpu_u64(bar, 1ull);
+      if ((old & 0xFFFFFFFFull) == static_cast<unsigned long long>(a.S - 1)) {
+        red_add_release_gpu_u64(bar, (1ull << 32) - static_cast<unsigned long long>(a.S));
+      } else {
+        while ((ld_acquire_gpu_u64(bar) >> 32) == (old >> 32)) __nanosleep(32);
+      }
     }
     __syncthreads();
     phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
@@ -193,8 +197,8 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
             const bool ok = s0 + k < a.S;
-            lv[k] = ok ? __ldcg(pl + 4 * (s0 + k)) : -INFINITY;
-            xv[k] = ok ? __ldcg(po + static_cast<int64_t>(s0 + k) * 512) : 0.f;
+            lv[k] = ok ? ld_na_f32(pl + 4 * (s0 + k)) : -INFINITY;
+            xv[k] = ok ? ld_na_f32(po + static_cast<int64_t>(s0 + k) * 512) : 0.f;
           }
           float mc = -INFINITY;
 #pragma unroll
@@ -221,22 +225,18 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
           a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
       }
     }
-    __syncthreads();
-    if (tid == 0 && atom_add_acq_rel_gpu(depart, 1u) == static_cast<uint32_t>(a.S - 1)) {
-      st_relaxed_gpu(arrive, 0u);
-      st_relaxed_gpu(depart, 0u);
-    }
     return;
   }
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 6);
   __syncthreads();
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 7);
-  if (tid == 0) s_last = (atom_add_acq_rel_gpu(&a.counter[unit], 1u) == static_cast<uint32_t>(a.S - 1));
+  // low 32-bit half of the unit's 64-bit barrier word (the high half holds the spin-merge epoch)
+  if (tid == 0) s_last = (atom_add_acq_rel_gpu(&a.counter[2 * unit], 1u) == static_cast<uint32_t>(a.S - 1));
   __syncthreads();
   phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
   if (!s_last) return;
   merge_splits<NTHREADS>(a, b, h);
-  if (tid == 0) a.counter[unit] = 0u;  // ready for the next launch
+  if (tid == 0) a.counter[2 * unit] = 0u;  // ready for the next launch
 }
 
 // Query transform of Eq. 7 for the G query heads of KV head h, one warp per head:
