@@ -180,6 +180,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.seq_lens = seq_lens; a.tok_begin = tok_begin; a.tok_end = tok_end;
   a.qscale = static_cast<float>((1.0 / sqrt(128.0)) * static_cast<double>(softmax_scale) * 1.4426950408889634);
   a.S = S;
+  a.n_items = B * H_kv * S;
   a.cluster = plan.cluster;
   a.merge_kernel = (S > 1 && !plan.cluster && algo != VECINFER_ATTN_LUT) ? merge_mode_from_env() : 0;
   // every CTA co-resident (one CTA per SM, grid <= SMs): spin-barrier + sliced merge

@@ -19,6 +19,7 @@ struct AttnArgs {
   int64_t tok_begin, tok_end;  // tok_end < 0: to seq_len
   float qscale;                // (1/sqrt(D)) * softmax_scale * log2(e): folded into q~
   int S;                       // splits per (b, h_kv)
+  int n_items;                 // B * H_kv * S work items
   int cluster;                 // 1: the S splits of a (b, h_kv) form one cluster, merged over DSMEM
   int merge_kernel;            // 1: split partials are merged by a separate PDL-launched kernel
   int merge_spin;              // 1: single-wave grid, every CTA merges a slice after an arrival barrier
@@ -183,7 +184,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
       }
     }
     __syncthreads();
-    phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
+    phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);
     const int per = (4 * 128 + a.S - 1) / a.S;
     const int idx = s * per + tid;
     if (tid < per && idx < 4 * 128) {
@@ -227,13 +228,13 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     }
     return;
   }
-  phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 6);
+  phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 6);
   __syncthreads();
-  phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 7);
+  phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 7);
   // low 32-bit half of the unit's 64-bit barrier word (the high half holds the spin-merge epoch)
   if (tid == 0) s_last = (atom_add_acq_rel_gpu(&a.counter[2 * unit], 1u) == static_cast<uint32_t>(a.S - 1));
   __syncthreads();
-  phase_mark(a.phase, (b * gridDim.y + h) * gridDim.x + s, 5);
+  phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);
   if (!s_last) return;
   merge_splits<NTHREADS>(a, b, h);
   if (tid == 0) a.counter[2 * unit] = 0u;  // ready for the next launch

@@ -52,7 +52,7 @@ __device__ __forceinline__ void issue_tile(uint8_t* dst, const uint8_t* src, int
 __global__ void __launch_bounds__(kT, 1) attn_lut8_kernel(const AttnArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemLut& sm = *reinterpret_cast<SmemLut*>(smem_raw);
-  const int s = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int s = blockIdx.x, h = blockIdx.y, b = blockIdx.z;   // (non-persistent grid)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   griddep_wait();
   int64_t r0, r1;

@@ -190,11 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
   constexpr bool kCanAppend = KB <= 8 && VB <= 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int s = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
-  const int cta_id = (b * gridDim.y + h) * gridDim.x + s;
-  phase_mark(a.phase, cta_id, 0);
   if (a.cluster) cluster_arrive_relaxed();   // paired with cluster_wait() before the DSMEM pushes
 
   // shared layout: misc at the bottom, the codebook table at the next 64 KiB boundary
@@ -210,12 +207,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   float* sq = reinterpret_cast<float*>(smem_raw + kMiscQ);
   const uint32_t tab_s = raw_s + tab_off;
 
+  // Work items = (split s, KV head h, batch b), s fastest.  Grids of up to one wave map one item
+  // to each CTA; larger problems run persistent CTAs (one per SM) over items, so the per-CTA
+  // prologue/epilogue and the wave ramp are paid once per item instead of once per wave.
+  const int nblk = gridDim.x * gridDim.y * gridDim.z;
+  bool first = true;
+  for (int item = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); item < a.n_items; item += nblk) {
+  const int s = item % a.S, h = (item / a.S) % a.Hkv, b = item / (a.S * a.Hkv);
+  const int cta_id = item;
+  phase_mark(a.phase, cta_id, 0);
+  if (!first) __syncthreads();   // previous item is done with the table and the misc region
+
   // static weights first (codebooks): with programmatic dependent launch this overlaps the
   // tail of the previous kernel on the stream; everything dynamic is read after the wait
   const uint16_t* cbk = a.ck + h * a.ck_hs;
   const uint16_t* cbv = a.cv + h * a.cv_hs;
   fill_tables<KB, VB>(tab, cbk, cbv, tid);
-  griddep_wait();
+  if (first) griddep_wait();
+  first = false;
 
   int64_t r0, r1, beg, e;
   split_range(a, b, s, r0, r1, &beg, &e);
@@ -542,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   if (!a.cluster) {
     cta_finish<kThreads, kNW>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
     phase_mark(a.phase, cta_id, 4);
-    return;
+    continue;
   }
   // ---- cluster path: the S splits of (b, h) are one cluster; each CTA combines its warps and
   // pushes (M, l, acc[4][128]) into the leader's buffer over DSMEM; one cluster barrier; the
@@ -594,6 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
   }
   phase_mark(a.phase, cta_id, 4);
+  }  // item loop
 }
 
 }  // namespace
@@ -652,7 +662,12 @@ int attn_mma_max_active_clusters(int cluster_size) {
 cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st) {
   set_attrs_once();
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.S, a.Hkv, a.B);
+  if (a.cluster) {
+    cfg.gridDim = dim3(a.S, a.Hkv, a.B);
+  } else {
+    const int sms = device_sm_count();
+    cfg.gridDim = dim3(a.n_items < sms ? a.n_items : sms, 1, 1);   // persistent beyond one wave
+  }
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem_for(kbits, vbits);
   cfg.stream = st;
