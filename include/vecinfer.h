@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define VECINFER_ABI_VERSION 2
+#define VECINFER_ABI_VERSION 3
 
 typedef struct CUstream_st* vecinfer_stream_t; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -64,11 +64,16 @@ typedef struct {
  *    operands (fp32 accumulate).  Default on sm_100a.
  *  LUT: the paper's Algorithm 1 literally: lut = q~' C_k^T (l.4) in shared
  *    memory, scores by table lookup (l.11), P.V from the dequantised value codebook on CUDA
- *    cores (l.16).  Kept as the paper-faithful variant and for comparison. */
+ *    cores (l.16).  Kept as the paper-faithful variant and for comparison.
+ *  DEQUANT_MMA_STREAM: DEQUANT_MMA with the stream partition (units cut into pieces so every
+ *    CTA gets the same number of tokens; pieces merged in fixed order).  AUTO selects it for
+ *    B*H_kv >= #SMs (batch decode); forcing it here with num_splits = S > 0 gives exactly S
+ *    pieces per unit (grid min(B*H_kv*S, #SMs) persistent CTAs). */
 typedef enum {
   VECINFER_ATTN_AUTO = 0,
   VECINFER_ATTN_DEQUANT_MMA = 1,
-  VECINFER_ATTN_LUT = 2
+  VECINFER_ATTN_LUT = 2,
+  VECINFER_ATTN_DEQUANT_MMA_STREAM = 3
 } vecinfer_attn_algo_t;
 
 /* Full-precision residual window ("the residual length for all methods is set to 128";
@@ -159,8 +164,9 @@ vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int
 
 /* ---------------------------------------------------------------------------------------
  * Fused decode attention over the VQ cache, Eq. 10 + Algorithm 1,
- * split-KV (grid over (batch, KV head, split)) with the log-sum-exp merge of the
- * split partials fused into the same launch (last CTA of each (b, h_kv) merges, fixed order).
+ * split-KV generalised to a stream partition: the B*H_kv units (b, h_kv) are cut into
+ * pieces so that every CTA (one per SM) gets the same number of tokens; the log-sum-exp merge
+ * of the pieces of a split unit is fused into the same launch (fixed piece order).
  *   q_bf16      [B, H_q, D] raw queries (strides q_stride_b, q_stride_h); query head i reads
  *               KV head i / G (GQA).  The kernel applies q~ = q diag(lambda) H_D (Eq. 7).
  *   lambda      fp32 [H_kv, D].
@@ -168,18 +174,24 @@ vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int
  *   seq_lens    device int32 [B]; tokens [tok_begin, min(tok_end, seq_len)) are attended
  *               (tok_end < 0 means "to seq_len"): the sharding hook for multi-GPU splits.
  *   softmax_scale  usually 1/sqrt(D).
- *   num_splits  0 = heuristic (fill 148 SMs); > 0 fixed => bitwise-deterministic results.
+ *   num_splits  0 = heuristic (fill the SMs); S > 0 = exactly S pieces per unit.  Results are
+ *               bitwise reproducible for a fixed (shape, num_splits, device SM count).
  *   o           [B, H_q, D] bf16 or fp32 (o_dtype); lse fp32 [B, H_q] natural log.
  *               An empty range yields o = 0, lse = -inf (weight 0 in vecinfer_merge_lse).
- *   residual    optional full-precision window (NULL = none); row t is attended by split t % S;
+ *   residual    optional full-precision window (NULL = none); row t of a unit is attended by
+ *               its piece t % P (P = pieces of the unit);
  *               LUT variant: not supported (VECINFER_ERR_UNSUPPORTED).
  *   workspace   >= vecinfer_attn_workspace_bytes(B, H_q, H_kv, D, n_tokens_max, num_splits)
  *               bytes, where n_tokens_max bounds the attended range; MUST be zero-filled once
  *               when first allocated (the kernel leaves its counters at zero on exit).
  * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, WORKSPACE, CUDA.
  * ------------------------------------------------------------------------------------- */
+/* pieces per unit (num_splits if > 0, else the heuristic's upper bound), and the number of
+ * virtual CTAs V of the partition (the grid is min(V, #SMs) persistent CTAs) */
 int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max,
                                  int32_t num_splits);
+int32_t vecinfer_attn_num_ctas(int32_t B, int32_t H_kv, int64_t n_tokens_max,
+                               int32_t num_splits);
 size_t vecinfer_attn_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int32_t D,
                                      int64_t n_tokens_max, int32_t num_splits);
 vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_q,

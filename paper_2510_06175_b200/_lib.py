@@ -44,6 +44,7 @@ PROTOTYPES = {
                                    c_void_p, c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p, c_void_p,
                                    c_void_p, c_sz, c_void_p]),
     "vecinfer_attn_num_splits": (c_i32, [c_i32, c_i32, c_i64, c_i32]),
+    "vecinfer_attn_num_ctas": (c_i32, [c_i32, c_i32, c_i64, c_i32]),
     "vecinfer_attn_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i32]),
     "vecinfer_attn_decode": (c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i64, c_i64, c_void_p, c_void_p, c_void_p,
                                      c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_i64, c_f32,
@@ -69,6 +70,8 @@ def load() -> ctypes.CDLL:
                               "(there is no CPU fallback)")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in PROTOTYPES.items():
+            if os.environ.get("VECINFER_LIB") and not hasattr(lib, name):
+                continue   # experiment builds (VECINFER_LIB override) may predate a symbol
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -36,17 +36,44 @@ bool vq_ok(const vecinfer_vq_t& c) {
 }
 
 struct WsLayout {
-  size_t part_o, part_l, counter, total;
+  size_t part_o, part_l, counter, elem, total;
 };
 
-WsLayout ws_layout(int32_t B, int32_t H_kv, int32_t S) {
+// counters: one 64-bit word per unit; split partials (split/LUT kernels): U*S x (L [4], o [4][128])
+// fp32; stream elements (stream kernel, auto mode only): (U + #SMs) x [4][128] 64-bit words.  The
+// two partial regions are disjoint, so a workspace shared by both kernels keeps the stream region
+// zero (its "empty" value) whatever the split kernel wrote.
+WsLayout ws_layout(int32_t B, int32_t H_kv, int32_t S, bool stream_region) {
   WsLayout w;
   const size_t units = static_cast<size_t>(B) * H_kv;
   w.counter = 0;
   w.part_l = ((units * sizeof(unsigned long long)) + 255) & ~size_t(255);   // 64-bit counters / barriers
   w.part_o = w.part_l + ((units * S * 4 * sizeof(float) + 255) & ~size_t(255));
-  w.total = w.part_o + units * S * 4 * 128 * sizeof(float);
+  w.elem = w.part_o + ((units * S * 4 * 128 * sizeof(float) + 255) & ~size_t(255));
+  // (explicit S with the forced stream algo: U*S pieces)
+  const size_t v = static_cast<size_t>(device_sm_count()) > units * S ? device_sm_count() : units * S;
+  const size_t slots = stream_region ? units + v : 0;
+  w.total = w.elem + slots * 4 * 128 * sizeof(unsigned long long);
   return w;
+}
+
+// Stream kernel (attn_stream.cu) for batch decode: B*H_kv >= #SMs units over V = #SMs CTAs (a
+// unit crossing a CTA boundary is split in two and merged).  VECINFER_STREAM=0 disables it,
+// =1 forces it for any auto-split call (experiments).
+static int stream_mode_from_env() {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("VECINFER_STREAM");
+    mode = e ? (e[0] == '1' ? 1 : 0) : -1;
+  }
+  return mode;
+}
+static bool use_stream(int32_t B, int32_t H_kv, int32_t num_splits, bool lut, bool forced = false) {
+  if (forced) return true;
+  if (lut || num_splits > 0) return false;
+  const int m = stream_mode_from_env();
+  if (m >= 0) return m == 1;
+  return static_cast<int64_t>(B) * H_kv >= device_sm_count();
 }
 
 }  // namespace
@@ -99,15 +126,25 @@ extern "C" int32_t vecinfer_debug_attn_max_clusters(int32_t cluster_size) {
 
 extern "C" int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits) {
   if (B <= 0 || H_kv <= 0) return 1;
+  if (use_stream(B, H_kv, num_splits, false)) {
+    const int64_t U = static_cast<int64_t>(B) * H_kv, V = device_sm_count();
+    return static_cast<int32_t>((V + U - 1) / U);   // pieces per unit (upper bound)
+  }
   return plan_splits(B, H_kv, n_tokens_max, num_splits).S;
+}
+
+extern "C" int32_t vecinfer_attn_num_ctas(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits) {
+  if (B <= 0 || H_kv <= 0) return 0;
+  if (use_stream(B, H_kv, num_splits, false)) return device_sm_count();
+  return B * H_kv * plan_splits(B, H_kv, n_tokens_max, num_splits).S;
 }
 
 extern "C" size_t vecinfer_attn_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int32_t D, int64_t n_tokens_max,
                                                 int32_t num_splits) {
   (void)H_q; (void)D;
   if (B <= 0 || H_kv <= 0) return 0;
-  const int32_t S = vecinfer_attn_num_splits(B, H_kv, n_tokens_max, num_splits);
-  return ws_layout(B, H_kv, S).total;
+  const int32_t S = plan_splits(B, H_kv, n_tokens_max, num_splits).S;
+  return ws_layout(B, H_kv, S, true).total;
 }
 
 struct AppendArgs {
@@ -132,7 +169,8 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   if (!q_bf16 || !lambda || !ck_bf16 || !cv_bf16 || !k_codes || !v_codes || !seq_lens || !o)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: NULL pointer");
   if (o_dtype != VECINFER_BF16 && o_dtype != VECINFER_F32) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad o_dtype");
-  if (algo != VECINFER_ATTN_AUTO && algo != VECINFER_ATTN_DEQUANT_MMA && algo != VECINFER_ATTN_LUT)
+  if (algo != VECINFER_ATTN_AUTO && algo != VECINFER_ATTN_DEQUANT_MMA && algo != VECINFER_ATTN_LUT &&
+      algo != VECINFER_ATTN_DEQUANT_MMA_STREAM)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad algo");
   if (B <= 0 || H_q <= 0 || H_kv <= 0 || n_cap <= 0) return fail(VECINFER_ERR_SHAPE, "attn_decode: non-positive size");
   if (H_q % H_kv != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode: H_q %% H_kv != 0");
@@ -152,11 +190,18 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
       !aligned(v_codes, 16) || ck_head_stride % 4 || cv_head_stride % 4 || ck_head_stride < 0 || cv_head_stride < 0)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: misaligned lambda/codebooks/codes");
   const int64_t range = tok_end >= 0 ? (tok_end - tok_begin < n_cap ? tok_end - tok_begin : n_cap) : n_cap;
-  const SplitPlan plan = algo == VECINFER_ATTN_LUT ? SplitPlan{vecinfer_attn_num_splits(B, H_kv, range, num_splits), 0}
-                                                  : plan_splits(B, H_kv, range, num_splits);
+  const bool lut = algo == VECINFER_ATTN_LUT;
+  const bool use_sk = use_stream(B, H_kv, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
+  const SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
   const int32_t S = plan.S;
-  const WsLayout wl = ws_layout(B, H_kv, S);
-  if (S > 1 && !plan.cluster && (!workspace || workspace_bytes < wl.total || !aligned(workspace, 256)))
+  const WsLayout wl = ws_layout(B, H_kv, plan_splits(B, H_kv, range, num_splits).S, true);
+  const int64_t U = static_cast<int64_t>(B) * H_kv;
+  const int64_t sms = device_sm_count();
+  const int64_t V = use_sk ? (num_splits > 0 ? U * (num_splits > kMaxSplits ? kMaxSplits : num_splits) : sms) : U * S;
+  if (use_sk && U * V >= (int64_t(1) << 42))
+    return fail(VECINFER_ERR_SHAPE, "attn_decode: B*H_kv*num_splits too large for the stream partition");
+  const bool stream_split = use_sk && (V > U || U % V != 0);
+  if (((S > 1 && !plan.cluster) || stream_split) && (!workspace || workspace_bytes < wl.total || !aligned(workspace, 256)))
     return fail(VECINFER_ERR_WORKSPACE, "attn_decode: workspace needs %zu bytes (256-B aligned)", wl.total);
   if (B > 65535 || H_kv > 65535) return fail(VECINFER_ERR_SHAPE, "attn_decode: grid too large");
   if (res) {
@@ -181,6 +226,11 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.qscale = static_cast<float>((1.0 / sqrt(128.0)) * static_cast<double>(softmax_scale) * 1.4426950408889634);
   a.S = S;
   a.n_items = B * H_kv * S;
+  a.U = static_cast<int>(U);
+  a.V = static_cast<int>(V);
+  a.rcpU = 1.0 / static_cast<double>(U);
+  a.rcpV = 1.0 / static_cast<double>(V);
+  a.merge = !stream_split ? kMergeNone : (V <= sms ? kMergeSpin : kMergeLast);
   a.cluster = plan.cluster;
   a.merge_kernel = (S > 1 && !plan.cluster && algo != VECINFER_ATTN_LUT) ? merge_mode_from_env() : 0;
   // every CTA co-resident (one CTA per SM, grid <= SMs): spin-barrier + sliced merge
@@ -191,6 +241,8 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.counter = S > 1 ? reinterpret_cast<uint32_t*>(ws + wl.counter) : nullptr;
   a.part_l = S > 1 ? reinterpret_cast<float*>(ws + wl.part_l) : nullptr;
   a.part_o = S > 1 ? reinterpret_cast<float*>(ws + wl.part_o) : nullptr;
+  a.part_elem = stream_split ? reinterpret_cast<unsigned long long*>(ws + wl.elem) : nullptr;
+  if (stream_split) a.counter = reinterpret_cast<uint32_t*>(ws + wl.counter);
   a.phase = phase_buffer();
   a.append = app != nullptr && !res_append;   // encode into the codes (not a residual append)
   a.knew = app ? static_cast<const uint16_t*>(app->k_new) : nullptr;
@@ -213,11 +265,12 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.res_append = res_append ? 1 : 0;
   a.qscale_raw = static_cast<float>(static_cast<double>(softmax_scale) * 1.4426950408889634);
   cudaStream_t st = as_stream(stream);
-  if (algo == VECINFER_ATTN_LUT) {
+  if (lut) {
     launch_attn_lut(a, kcfg.code_bits, vcfg.code_bits, st);
     return check_launch("attn_decode (lut)");
   }
-  const cudaError_t e = launch_attn_mma(a, kcfg.code_bits, vcfg.code_bits, st);
+  const cudaError_t e = use_sk ? launch_attn_stream(a, kcfg.code_bits, vcfg.code_bits, st)
+                               : launch_attn_mma(a, kcfg.code_bits, vcfg.code_bits, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(VECINFER_ERR_CUDA, "attn_decode: launch failed: %s", cudaGetErrorString(e));
@@ -284,7 +337,10 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
   // behind the other CTAs' longer splits; with several waves every wave would carry it, and a
   // separate append launch (latency ~3 us, once) is cheaper.
   bool fuse = algo != VECINFER_ATTN_LUT && kcfg.code_bits <= 8 && vcfg.code_bits <= 8;
-  if (fuse && B > 0 && H_kv > 0) {
+  const bool forced_stream = algo == VECINFER_ATTN_DEQUANT_MMA_STREAM;
+  if (fuse && forced_stream) fuse = num_splits == 0 ||
+      static_cast<int64_t>(B) * H_kv * num_splits <= device_sm_count();   // persistent grids: separate append
+  else if (fuse && B > 0 && H_kv > 0 && !use_stream(B, H_kv, num_splits, false)) {   // (stream: V <= #SMs)
     const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
     const int64_t units = static_cast<int64_t>(B) * H_kv;
     const int64_t waves = plan.cluster ? (units + attn_mma_max_active_clusters(plan.S) - 1) /

@@ -23,6 +23,12 @@ struct AttnArgs {
   int cluster;                 // 1: the S splits of a (b, h_kv) form one cluster, merged over DSMEM
   int merge_kernel;            // 1: split partials are merged by a separate PDL-launched kernel
   int merge_spin;              // 1: single-wave grid, every CTA merges a slice after an arrival barrier
+  // stream kernel (attn_stream.cu): U = B*H_kv units and V virtual CTAs tile one line of U*V ticks
+  // (unit u = [u*V, (u+1)*V), CTA c = [c*U, (c+1)*U))
+  int U, V;
+  double rcpU, rcpV;           // 1/U, 1/V (host, double): division-free tick arithmetic
+  int merge;                   // kMergeNone / kMergeSpin / kMergeLast
+  unsigned long long* part_elem;   // [U + V][4][128] published (o, L) elements (zero = empty)
   void* o;
   int o_f32;
   float* lse;
@@ -57,6 +63,21 @@ struct AttnArgs {
 // extra tokens' worth of work the split owning the appended row does (its encode), used to
 // shorten that split so it does not become the straggler
 constexpr int64_t kAppendTokenCost = 160;
+
+// merge of the pieces of a unit split over several CTAs (stream kernel)
+constexpr int kMergeNone = 0;   // every unit is processed by one CTA
+constexpr int kMergeSpin = 1;   // all CTAs co-resident: publish, then each piece merges a slice
+constexpr int kMergeLast = 2;   // persistent grid: the last-arriving piece merges the unit
+
+// floor(x / d) for 0 <= x < 2^53, 1 <= d < 2^31: the double estimate x * (1/d) is within one of the
+// quotient (x is exact in double), so one integer fix-up step either way makes it exact
+__device__ __forceinline__ int64_t div_fix(int64_t x, int64_t d, double rcp) {
+  int64_t q = __double2ll_rz(static_cast<double>(x) * rcp);
+  const int64_t r = x - q * d;
+  q += (r >= d) ? 1 : 0;
+  q -= (r < 0) ? 1 : 0;
+  return q;
+}
 
 // Token range [r0, r1) of split s for (b, h) within the attended range [beg, e).
 __device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int64_t& r0, int64_t& r1,
@@ -271,6 +292,7 @@ __device__ __forceinline__ void query_transform_warp(const AttnArgs& a, int b, i
 }
 
 cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
+cudaError_t launch_attn_stream(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
 int attn_mma_max_active_clusters(int cluster_size);  // 0 if not schedulable
 void launch_attn_lut(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
 

@@ -21,15 +21,11 @@
 // Epilogue: warps combine through shared memory; splits merge by log-sum-exp in the last CTA
 // of each (b, h_kv), which stages all partials in shared memory first (fixed order s = 0..S-1
 // => deterministic).  See DESIGN.md "Kernel N4".
-#include "attn_common.cuh"
+#include "attn_tiles.cuh"
 
 namespace vecinfer {
 namespace {
 
-constexpr int kNW = 16;            // warps per CTA (1 CTA per SM)
-constexpr int kThreads = kNW * 32;
-constexpr float kTau = 8.0f;       // lazy-rescale threshold (log2 units): p <= 2^8
-constexpr int kTab = 65536;        // [256 centroids][256 B] codebook table, 64 KiB-aligned
 // misc region (below the table): q~ [4][128] f32, warp partials, staged split partials
 constexpr int kMiscQ = 0;
 constexpr int kMiscNew = 2048;                       // 128 B: codes of the appended token (K at +0, V at +64)
@@ -44,146 +40,6 @@ constexpr int kSmemBytesNoTab = kMiscBytes + 1024 + kCbufBytes + 1024;
 template <int KB, int VB>
 constexpr int smem_bytes() { return (KB > 8 && VB > 8) ? kSmemBytesNoTab : kSmemBytes; }
 
-// ---- code-width traits.  Per lane and token: the K chunk holds sub-vectors 8j..8j+7 (score MMA
-// k-steps), the V chunk sub-vectors 4r..4r+3 (P.V m-tiles).  4/8-bit codebooks are gathered from the
-// shared table (rows of 256 B: [16 K replicas | 16 V replicas]); 16-bit codebooks (65536 x 4 bf16 =
-// 512 KiB) do not fit shared memory and are gathered from global memory (L2/L1 resident).
-template <int BITS> struct Fmt;
-template <> struct Fmt<8> {
-  static constexpr int kRow = 32, kOffK = 8, kOffV = 4;
-  static constexpr bool kSmem = true;
-  using K = uint2;
-  using V = uint32_t;
-  static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u64(p); }
-  static __device__ __forceinline__ V ldv(const uint8_t* p) { return ldg_nc_u32(p); }
-  static __device__ __forceinline__ K zk() { return make_uint2(0u, 0u); }
-  // shared address of the centroid of code T of the chunk: code byte -> address bits 8..15 (PRMT)
-  template <int T> static __device__ __forceinline__ uint32_t kaddr(const K& c, uint32_t base) {
-    return prmt(T < 4 ? c.x : c.y, base, 0x7604u | ((T & 3) << 4));
-  }
-  template <int U> static __device__ __forceinline__ uint32_t vaddr(V c, uint32_t base) {
-    return prmt(c, base, 0x7604u | (U << 4));
-  }
-};
-template <> struct Fmt<4> {
-  static constexpr int kRow = 16, kOffK = 4, kOffV = 2;
-  static constexpr bool kSmem = true;
-  using K = uint32_t;
-  using V = uint32_t;   // low 16 bits
-  static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u32(p); }
-  static __device__ __forceinline__ V ldv(const uint8_t* p) { return ldg_nc_u16(p); }
-  static __device__ __forceinline__ K zk() { return 0u; }
-  template <int T> static __device__ __forceinline__ uint32_t nib8(uint32_t w) {   // nibble T -> bits 8..11
-    return T >= 2 ? ((w >> (4 * T - 8)) & 0xF00u) : ((w << (8 - 4 * T)) & 0xF00u);
-  }
-  template <int T> static __device__ __forceinline__ uint32_t kaddr(K c, uint32_t base) { return nib8<T>(c) | base; }
-  template <int U> static __device__ __forceinline__ uint32_t vaddr(V c, uint32_t base) { return nib8<U>(c) | base; }
-};
-template <> struct Fmt<16> {
-  static constexpr int kRow = 64, kOffK = 16, kOffV = 8;
-  static constexpr bool kSmem = false;
-  using K = uint4;
-  using V = uint2;
-  static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u128(p); }
-  static __device__ __forceinline__ V ldv(const uint8_t* p) { return ldg_nc_u64(p); }
-  static __device__ __forceinline__ K zk() { return make_uint4(0u, 0u, 0u, 0u); }
-  template <int T> static __device__ __forceinline__ uint32_t kidx(const K& c) {
-    const uint32_t w = T < 2 ? c.x : T < 4 ? c.y : T < 6 ? c.z : c.w;
-    return (T & 1) ? (w >> 16) : (w & 0xFFFFu);
-  }
-  template <int U> static __device__ __forceinline__ uint32_t vidx(const V& c) {
-    const uint32_t w = U < 2 ? c.x : c.y;
-    return (U & 1) ? (w >> 16) : (w & 0xFFFFu);
-  }
-};
-template <int BITS> using KCode = typename Fmt<BITS>::K;
-template <int BITS> using VCode = typename Fmt<BITS>::V;
-
-// bf16x4 centroid (global) -> fp16x4 MMA operand pair (exact for |c| in the fp16 normal range)
-__device__ __forceinline__ uint2 bf16x4_to_f16x4(uint2 w) {
-  uint2 e;
-  e.x = pack_half2(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u));
-  e.y = pack_half2(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
-  return e;
-}
-
-template <int KB, int T>
-__device__ __forceinline__ uint2 gather_k(const KCode<KB>& c, uint32_t kbase, const uint16_t* cbk) {
-  if constexpr (Fmt<KB>::kSmem) return lds_u64(Fmt<KB>::template kaddr<T>(c, kbase));
-  else return bf16x4_to_f16x4(ldg_ro_u64(cbk + 4 * Fmt<KB>::template kidx<T>(c)));
-}
-template <int VB, int U>
-__device__ __forceinline__ uint2 gather_v(const VCode<VB>& c, uint32_t vbase, const uint16_t* cbv) {
-  if constexpr (Fmt<VB>::kSmem) return lds_u64(Fmt<VB>::template vaddr<U>(c, vbase));
-  else return bf16x4_to_f16x4(ldg_ro_u64(cbv + 4 * Fmt<VB>::template vidx<U>(c)));
-}
-
-template <int KB, int VB>
-__device__ __forceinline__ void fill_tables(unsigned char* tab, const uint16_t* ck, const uint16_t* cv, int tid) {
-  // thread t: centroid j = t/2 of C_k (t even) or C_v (t odd); 16 replicas = 8 x 16-byte stores,
-  // rotated so that the 8 threads of a quarter-warp hit 8 different bank groups
-  const int j = tid >> 1, which = tid & 1;
-  const int n = which ? (VB <= 8 ? (1 << VB) : 0) : (KB <= 8 ? (1 << KB) : 0);
-  if (j >= n) return;
-  const uint16_t* src = (which ? cv : ck) + 4 * j;
-  const uint2 e = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(src));
-  const uint4 v = make_uint4(e.x, e.y, e.x, e.y);
-  unsigned char* row = tab + j * 256 + which * 128;
-#pragma unroll
-  for (int u0 = 0; u0 < 8; ++u0) {
-    const int u = (u0 + tid) & 7;
-    *reinterpret_cast<uint4*>(row + 16 * u) = v;
-  }
-}
-
-template <int KB, int VB>
-struct TileCodes {
-  KCode<KB> k[2][2];  // [sub-tile][row r / r+8]
-  VCode<VB> v[2][4];  // [sub-tile][token 2j, 2j+1, 2j+8, 2j+9]
-};
-
-// kp/vp point at this lane's bytes of token (tile start + r) / (tile start + 2j) respectively
-template <int KB, int VB>
-__device__ __forceinline__ void load_tile_full(TileCodes<KB, VB>& tc, const uint8_t* kp, const uint8_t* vp) {
-  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    tc.k[q][0] = Fmt<KB>::ldk(kp + (16 * q) * KR);
-    tc.k[q][1] = Fmt<KB>::ldk(kp + (16 * q + 8) * KR);
-    tc.v[q][0] = Fmt<VB>::ldv(vp + (16 * q) * VR);
-    tc.v[q][1] = Fmt<VB>::ldv(vp + (16 * q + 1) * VR);
-    tc.v[q][2] = Fmt<VB>::ldv(vp + (16 * q + 8) * VR);
-    tc.v[q][3] = Fmt<VB>::ldv(vp + (16 * q + 9) * VR);
-  }
-}
-
-// ragged last tile: rem = tokens left in the split (1..31), rows beyond it read as code 0
-template <int KB, int VB>
-__device__ __forceinline__ void load_tile_tail(TileCodes<KB, VB>& tc, const uint8_t* kp, const uint8_t* vp, int rem,
-                                               int r, int j) {
-  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    tc.k[q][0] = (16 * q + r < rem) ? Fmt<KB>::ldk(kp + (16 * q) * KR) : Fmt<KB>::zk();
-    tc.k[q][1] = (16 * q + r + 8 < rem) ? Fmt<KB>::ldk(kp + (16 * q + 8) * KR) : Fmt<KB>::zk();
-    const int t0 = 16 * q + 2 * j;
-    tc.v[q][0] = (t0 < rem) ? Fmt<VB>::ldv(vp + (16 * q) * VR) : VCode<VB>{};
-    tc.v[q][1] = (t0 + 1 < rem) ? Fmt<VB>::ldv(vp + (16 * q + 1) * VR) : VCode<VB>{};
-    tc.v[q][2] = (t0 + 8 < rem) ? Fmt<VB>::ldv(vp + (16 * q + 8) * VR) : VCode<VB>{};
-    tc.v[q][3] = (t0 + 9 < rem) ? Fmt<VB>::ldv(vp + (16 * q + 9) * VR) : VCode<VB>{};
-  }
-}
-
-// store the packed code of sub-vector `lane` (4/8-bit) for the fused append
-template <int BITS>
-__device__ __forceinline__ void put_code(unsigned char* row, int lane, uint32_t code) {
-  if constexpr (BITS == 8) {
-    row[lane] = static_cast<uint8_t>(code);
-  } else {
-    const uint32_t hi = __shfl_xor_sync(0xffffffffu, code, 1);
-    if ((lane & 1) == 0) row[lane >> 1] = static_cast<uint8_t>(code | (hi << 4));
-  }
-}
 
 template <int KB, int VB>
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {

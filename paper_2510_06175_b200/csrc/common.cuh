@@ -160,6 +160,22 @@ __device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu_u64(unsigned 
 __device__ __forceinline__ void red_add_release_gpu_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// floor(x / d) for 0 <= x < 2^24, 1 <= d < 2^24: float reciprocal estimate + exact fix-up
+__device__ __forceinline__ int div_small(int x, int d) {
+  int q = __float2int_rz(__int2float_rn(x) * __frcp_rn(__int2float_rn(d)));
+  int rr = x - q * d;
+  while (rr < 0) { --q; rr += d; }
+  while (rr >= d) { ++q; rr -= d; }
+  return q;
+}
 __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -262,7 +278,7 @@ __device__ __forceinline__ void phase_mark(unsigned long long* buf, int cta, int
   if (threadIdx.x == 0 && buf) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    buf[cta * 8 + slot] = t;
+    buf[cta * 16 + slot] = t;   // 16 slots per CTA
   }
 }
 #else

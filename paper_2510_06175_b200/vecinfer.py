@@ -19,7 +19,7 @@ from ._lib import VQ, I64x2, I64x3, Residual, check
 _lib.load()   # fail loudly at import if the native library is missing
 
 BF16, F32 = 0, 1
-ALGOS = {"auto": 0, "mma": 1, "dequant_mma": 1, "lut": 2}
+ALGOS = {"auto": 0, "mma": 1, "dequant_mma": 1, "lut": 2, "stream": 3, "dequant_mma_stream": 3}
 
 
 @dataclass(frozen=True)
@@ -131,6 +131,11 @@ def encode_kv(k: torch.Tensor, v: torch.Tensor, inv_lambda: torch.Tensor, ck: to
 
 def attn_num_splits(B: int, H_kv: int, n_tokens_max: int, num_splits: int = 0) -> int:
     return _lib.load().vecinfer_attn_num_splits(B, H_kv, n_tokens_max, num_splits)
+
+
+def attn_num_ctas(B: int, H_kv: int, n_tokens_max: int, num_splits: int = 0) -> int:
+    """Virtual CTAs V of the stream partition (the grid is min(V, #SMs) persistent CTAs)."""
+    return _lib.load().vecinfer_attn_num_ctas(B, H_kv, n_tokens_max, num_splits)
 
 
 def attn_workspace(B: int, H_q: int, H_kv: int, n_tokens_max: int, num_splits: int = 0, device="cuda"):

@@ -70,7 +70,11 @@ def run(B, N, splits, algo, reps=20, with_encode=False):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (reps * n_l)
     S = vi.attn_num_splits(B, 8, N, splits)
-    print(f"B={B:3d} N={N:7d} S={S:3d} algo={algo:4s} enc={with_encode}: {us:8.2f} us/launch  {nbytes / us / 1e3:7.0f} GB/s  "
+    try:
+        V = vi.attn_num_ctas(B, 8, N, splits)
+    except Exception:
+        V = -1
+    print(f"B={B:3d} N={N:7d} S={S:3d} V={V:4d} algo={algo:4s} enc={with_encode}: {us:8.2f} us/launch  {nbytes / us / 1e3:7.0f} GB/s  "
           f"({100 * nbytes / us / 1e3 / 6553.6:.1f}% of 6553.6)  cyc/token-head@1.9GHz/SM={us * 1.9e3 * 148 / (B * 8 * N):.2f}",
           flush=True)
 

@@ -32,8 +32,8 @@ def main():
     for c in args.case:
         B, N, splits = map(int, c.split(",")[:3])
         S = vi.attn_num_splits(B, 8, N, splits)
-        nct = B * 8 * S
-        buf = torch.zeros(nct * 8, dtype=torch.int64, device=dev)
+        nct = vi.attn_num_ctas(B, 8, N, splits)
+        buf = torch.zeros(nct * 16, dtype=torch.int64, device=dev)
         lib.vecinfer_debug_set_phase_buffer.argtypes = [ctypes.c_void_p]
         lib.vecinfer_debug_set_phase_buffer(ctypes.c_void_p(buf.data_ptr()))
         kc = synth.gen_codes_torch((B, 8, N, 32), 8, seed=1, device=dev)
@@ -45,7 +45,7 @@ def main():
             buf.zero_()
             vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, workspace=ws)
             torch.cuda.synchronize()
-        t = buf.view(nct, 8).cpu().numpy().astype(np.float64)
+        t = buf.view(nct, 16).cpu().numpy().astype(np.float64)
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3
         span = (t[:, 4].max() - t0) / 1e3
@@ -53,24 +53,25 @@ def main():
 
         def st(x, name):
             print(f"   {name:32s} min {x.min():7.2f}  med {np.median(x):7.2f}  max {x.max():7.2f} us")
-        st(rel[:, 0], "CTA start (rel)")
-        st(rel[:, 1] - rel[:, 0], "prologue (fill+q~+sync)")
-        st(rel[:, 2] - rel[:, 1], "main loop (incl. bq frags)")
-        st(rel[:, 3] - rel[:, 2], "warp partials -> smem")
-        if S > 1 and t[:, 6].max() > 0:
-            st(rel[:, 6] - rel[:, 3], "combine + partial store")
-            st(rel[:, 7] - rel[:, 6], "threadfence + syncthreads")
-            st(rel[:, 5] - rel[:, 7], "atomic + syncthreads")
-        if S > 1:
-            st(rel[:, 5] - rel[:, 3], "combine+publish+fence+atomic")
-            last = t[:, 4] - t[:, 5] > 0
-            st((rel[:, 4] - rel[:, 5]), "merge (all CTAs)")
-            print(f"   last-CTA merges: {int(last.sum())}, exit max {rel[:, 4].max():.2f}")
-        st(rel[:, 4], "CTA end (rel)")
-        if S > 1:
-            last = rel[:, 4] > rel[:, 5]
-            print(f"   last CTAs: atomic done at {np.sort(rel[last, 5])[-3:]}, exit at {np.sort(rel[last, 4])[-3:]}")
+        rel[t == 0] = np.nan   # stamps a CTA did not write (e.g. no deferred merge)
 
+        def st(x, name):   # noqa: F811
+            x = x[~np.isnan(x)]
+            if x.size:
+                print(f"   {name:32s} min {x.min():7.2f}  med {np.median(x):7.2f}  max {x.max():7.2f} us  (n={x.size})")
+        st(rel[:, 0], "CTA start (rel)")
+        st(rel[:, 6] - rel[:, 0], "prologue: fill+wait+segs")
+        st(rel[:, 12] - rel[:, 6], "prologue: piece setup (loads)")
+        st(rel[:, 11] - rel[:, 12], "prologue: q~ transform")
+        st(rel[:, 1] - rel[:, 11], "prologue: encode + sync")
+        st(rel[:, 2] - rel[:, 1], "main loop warp 0 (last round)")
+        st(rel[:, 7] - rel[:, 2], "wait for slowest warp")
+        st(rel[:, 9] - rel[:, 7], "combine + store")
+        st(rel[:, 10] - rel[:, 9], "sync")
+        st(rel[:, 3] - rel[:, 10], "arrive")
+        st(rel[:, 5] - rel[:, 3], "spin wait (deferred merges)")
+        st(rel[:, 4] - rel[:, 5], "slice merge")
+        st(rel[:, 4], "CTA end (rel)")
 
 if __name__ == "__main__":
     main()

@@ -373,7 +373,7 @@ def test_decode_step_append_outside_attended_range():
 
 
 def test_decode_step_many_units_uses_separate_append():
-    """Multi-wave grids run the append as its own launch inside vecinfer_decode_step; same result."""
+    """320 units (>= #SMs): AUTO runs the stream kernel with the append fused; same result as the oracle."""
     B, n = 40, 64
     c = _attn_case(B, 8, 4, n + 2, [n] * B, seed=90)
     kn = synth.gen_keys(1, 8, 128, seed=91, batch=B)[:, 0]
