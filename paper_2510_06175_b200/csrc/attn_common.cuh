@@ -103,7 +103,7 @@ __device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int
 // CTA epilogue shared by all kernels: combine per-warp (m, l, acc) partials held in shared
 // memory, then either write the final output (S == 1) or a split partial plus a fused
 // last-CTA log-sum-exp merge over the S splits in fixed order s = 0..S-1.
-//   wm[NW][4], wl[NW][4] (log2 domain), wacc[NW][4][128] (unnormalised);
+//   wm[NW][4], wl[NW][4] (log2 domain), wacc[NW][4][WROW] (unnormalised, rows WROW floats apart);
 //   scratch: >= 4*S + 8 floats of shared memory not aliased with wm/wl/wacc.
 // Fixed-order log-sum-exp merge of the S split partials of unit (b, h) into o and lse, in chunks
 // of 32 splits: all 2 x 32 loads of a chunk are issued before any use (one memory round trip per
@@ -150,7 +150,7 @@ __device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
   }
 }
 
-template <int NTHREADS, int NWARPS>
+template <int NTHREADS, int NWARPS, int WROW = 128>
 __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s,
                                            const float* wm, const float* wl, const float* wacc,
                                            float* scratch) {
@@ -169,7 +169,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
       for (int w = 0; w < NWARPS; ++w) {
         const float f = ex2_approx(wm[w * 4 + g] - M);
         lsum += f * wl[w * 4 + g];
-        osum += f * wacc[(w * 4 + g) * 128 + dim];
+        osum += f * wacc[(w * 4 + g) * WROW + dim];
       }
     }
     const bool empty = !(lsum > 0.f);
@@ -261,10 +261,18 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   if (tid == 0) a.counter[2 * unit] = 0u;  // ready for the next launch
 }
 
+// q~ rows in shared memory: sub-vector m of a head at float offset 4m + 8(m/8), heads kQRow = 164
+// floats apart.  The MMA kernels' B-fragment loads (lanes (r, j) read head r/2, sub-vectors 8j+t)
+// then hit 8 distinct 16-byte bank groups instead of one (a 16-way conflict with dense rows).
+constexpr int kQRow = 164;
+__device__ __forceinline__ int qoff(int m) { return 4 * m + 8 * (m >> 3); }
+
 // Query transform of Eq. 7 for the G query heads of KV head h, one warp per head:
 // sq[g][:] = ((q_g * lambda) H_pm) * qscale  (fp32 FWHT: 2 register + 5 shuffle stages).
 // Heads g >= G are zero (padding of the 4-wide GQA group).
-__device__ __forceinline__ void query_transform_warp(const AttnArgs& a, int b, int h, int g, float* sq_g) {
+// padded: write in the qoff() layout (MMA kernels), else dense (LUT kernel).
+__device__ __forceinline__ void query_transform_warp(const AttnArgs& a, int b, int h, int g, float* sq_g,
+                                                     bool padded = false) {
   const int lane = threadIdx.x & 31;
   float x[4] = {0.f, 0.f, 0.f, 0.f};
   if (g < a.G) {
@@ -287,7 +295,7 @@ __device__ __forceinline__ void query_transform_warp(const AttnArgs& a, int b, i
       x[i] = upper ? (o - x[i]) : (x[i] + o);
     }
   }
-  *reinterpret_cast<float4*>(sq_g + 4 * lane) =
+  *reinterpret_cast<float4*>(sq_g + (padded ? qoff(lane) : 4 * lane)) =
       make_float4(x[0] * a.qscale, x[1] * a.qscale, x[2] * a.qscale, x[3] * a.qscale);
 }
 

@@ -26,11 +26,13 @@
 namespace vecinfer {
 namespace {
 
-// misc region (below the table): q~ [4][128] f32, warp partials, staged split partials
+// misc region (below the table): q~ [4][kQRow] f32, warp partials, staged split partials
 constexpr int kMiscQ = 0;
-constexpr int kMiscNew = 2048;                       // 128 B: codes of the appended token (K at +0, V at +64)
-constexpr int kMiscW = 2176;                         // wm[16][4], wl[16][4], wacc[16][4][128]
-constexpr int kMiscBytes = kMiscW + (kNW * 8 + kNW * 4 * 128) * 4;   // 35328
+constexpr int kMiscNew = 2688;                       // 128 B: codes of the appended token (K at +0, V at +64)
+constexpr int kMiscW = 2816;                         // wm[16][4], wl[16][4], wacc[16][4][kWRow]
+constexpr int kWRow = 132;   // warp-partial row stride: the 16-byte stores of a warp spread over all banks
+constexpr int kMiscBytes = kMiscW + (kNW * 8 + kNW * 4 * kWRow) * 4;   // 37120
+static_assert(4 * kQRow * 4 <= kMiscNew, "q~ rows");
 constexpr int kClusterMax = 16;                      // DSMEM merge buffer: [16][4][128] + m, l
 constexpr int kCbufBytes = kClusterMax * 4 * 130 * 4;
 constexpr int kSmemBytes = 65536 + kTab + kCbufBytes + 1024;  // pad + table + cluster buffer + slack
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           *reinterpret_cast<const uint2*>(vrow + 4 * lane);
     }
   }
-  if (warp < 4) query_transform_warp(a, b, h, warp, sq + 128 * warp);
+  if (warp < 4) query_transform_warp(a, b, h, warp, sq + kQRow * warp, true);
   __syncthreads();
   if (kCanAppend && owner) {
     if (warp == 0 || warp == 8) {
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     const int gq = r >> 1, part = r & 1;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const float4 v = *reinterpret_cast<const float4*>(sq + 128 * gq + 4 * (8 * j + t));
+      const float4 v = *reinterpret_cast<const float4*>(sq + kQRow * gq + qoff(8 * j + t));
       const float in[4] = {v.x, v.y, v.z, v.w};
       float o[4];
 #pragma unroll
@@ -396,16 +398,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     wm[warp * 4 + j] = m_run;
     wl[warp * 4 + j] = l_run;
   }
-  float* dst = wacc + (warp * 4 + j) * 128 + 16 * r;
+  // thread (r, j): head j, dims 16r..16r+15; MMA slots [t][0] + [t][1] hold dim 16r+2t, [t][2] + [t][3]
+  // dim 16r+2t+1 (hi + lo parts)
+  float* dst = wacc + (warp * 4 + j) * kWRow + 16 * r;
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    dst[2 * t] = acc[t][0] + acc[t][1];      // dim 16r + 2t     (h = 0: hi + lo slot)
-    dst[2 * t + 1] = acc[t][2] + acc[t][3];  // dim 16r + 2t + 1 (h = 1)
-  }
+  for (int k = 0; k < 4; ++k)
+    *reinterpret_cast<float4*>(dst + 4 * k) =
+        make_float4(acc[2 * k][0] + acc[2 * k][1], acc[2 * k][2] + acc[2 * k][3],
+                    acc[2 * k + 1][0] + acc[2 * k + 1][1], acc[2 * k + 1][2] + acc[2 * k + 1][3]);
   __syncthreads();
   phase_mark(a.phase, cta_id, 3);
   if (!a.cluster) {
-    cta_finish<kThreads, kNW>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
+    cta_finish<kThreads, kNW, kWRow>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
     phase_mark(a.phase, cta_id, 4);
     continue;
   }
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       for (int w = 0; w < kNW; ++w) {
         const float f = ex2_approx(wm[w * 4 + g] - M);
         lsum += f * wl[w * 4 + g];
-        osum += f * wacc[(w * 4 + g) * 128 + dim];
+        osum += f * wacc[(w * 4 + g) * kWRow + dim];
       }
     }
     cluster_wait();   // every CTA of the cluster has started: DSMEM of the leader is valid

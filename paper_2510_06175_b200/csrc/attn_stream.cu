@@ -40,11 +40,7 @@ namespace {
 // misc region (below the tables, which start at the next 64 KiB boundary of the shared window)
 constexpr int kWRow = 132;         // row stride (floats) of the warp partials: conflict-free 16-B stores
 constexpr int kSlots = 17;         // warp partial slots: warp w's last piece -> w, the straddler's first -> 16
-// q~ rows: sub-vector m of head g at float offset g*kQRow + 4m + 8(m/8): the B-fragment loads
-// (lanes (r, j) read head r/2, sub-vectors 8j + t) then hit 8 distinct 16-byte bank groups
-constexpr int kQRow = 164;
-constexpr int kQSeg = 4 * kQRow;
-__device__ __forceinline__ int qoff(int m) { return 4 * m + 8 * (m >> 3); }
+constexpr int kQSeg = 4 * kQRow;   // q~ rows of a segment (kQRow, qoff: attn_common.cuh)
 constexpr int kMiscQ = 0;          // q~ [2 segments][4][kQRow] f32
 constexpr int kMiscNew = 5376;     // appended-token codes [2][128 B] (K at +0, V at +64)
 constexpr int kMiscWM = 5632;      // wm [17][4] f32 (log2-domain running max per warp piece)
