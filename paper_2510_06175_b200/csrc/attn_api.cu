@@ -241,7 +241,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.counter = S > 1 ? reinterpret_cast<uint32_t*>(ws + wl.counter) : nullptr;
   a.part_l = S > 1 ? reinterpret_cast<float*>(ws + wl.part_l) : nullptr;
   a.part_o = S > 1 ? reinterpret_cast<float*>(ws + wl.part_o) : nullptr;
-  a.part_elem = stream_split ? reinterpret_cast<unsigned long long*>(ws + wl.elem) : nullptr;
+  a.part_elem = (stream_split || a.merge_spin) ? reinterpret_cast<unsigned long long*>(ws + wl.elem) : nullptr;
   if (stream_split) a.counter = reinterpret_cast<uint32_t*>(ws + wl.counter);
   a.phase = phase_buffer();
   a.append = app != nullptr && !res_append;   // encode into the codes (not a residual append)

@@ -154,7 +154,6 @@ template <int NTHREADS, int NWARPS, int WROW = 128>
 __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s,
                                            const float* wm, const float* wl, const float* wacc,
                                            float* scratch) {
-  (void)scratch;
   const int tid = threadIdx.x;
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
   __shared__ bool s_last;
@@ -182,6 +181,11 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
         else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
         if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = L2 * kLn2;
       }
+    } else if (a.merge_spin) {
+      // publish (o_s, L_s) as one 64-bit relaxed store of ~(L_s << 32 | o_s) (zero = empty)
+      const int64_t pi = ((unit * a.S + s) * 4 + g) * 128 + dim;
+      st_relaxed_gpu_u64(a.part_elem + pi, ~((static_cast<unsigned long long>(__float_as_uint(L2)) << 32) |
+                                             __float_as_uint(ov)));
     } else {
       const int64_t pi = (unit * a.S + s) * 4 + g;
       a.part_o[pi * 128 + dim] = ov;
@@ -190,62 +194,51 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   }
   if (a.S == 1 || a.merge_kernel) return;
   if (a.merge_spin) {
-    // Single-wave grid (all S CTAs of the unit are co-resident): publish, then a sense-reversing
-    // barrier on a 64-bit word (high 32 bits: epoch, low 32: arrivals).  The last arriver resets
-    // the count and bumps the epoch with one release-add; the others wait for the epoch to change.
-    // Then every CTA merges a 1/S slice of the 4 x 128 outputs (fixed order s = 0..S-1).
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(a.counter) + unit;
-    __syncthreads();
-    if (tid == 0) {
-      const unsigned long long old = atom_add_acq_rel_gpu_u64(bar, 1ull);
-      if ((old & 0xFFFFFFFFull) == static_cast<unsigned long long>(a.S - 1)) {
-        red_add_release_gpu_u64(bar, (1ull << 32) - static_cast<unsigned long long>(a.S));
-      } else {
-        while ((ld_acquire_gpu_u64(bar) >> 32) == (old >> 32)) __nanosleep(32);
+    // Single-wave grid (all S CTAs of the unit are co-resident), no fence and no atomic: split s
+    // merges outputs [s*per, (s+1)*per) of the unit, per = ceil(512/S).  One thread per (output,
+    // split) element polls it until published (non-zero), consumes it (stores zero back: every
+    // element is read exactly once, so the workspace is clean for the next launch) and stages it
+    // in shared memory; then one thread per output combines its S splits in order s = 0..S-1.
+    const int S = a.S;
+    const int per = (4 * 128 + S - 1) / S;
+    const int o0 = s * per, nout = max(0, min(4 * 128, o0 + per) - o0);
+    float2* stage = reinterpret_cast<float2*>(scratch);
+    for (int e = tid; e < nout * S; e += NTHREADS) {
+      const int oo = e / S, p = e - oo * S, o = o0 + oo;
+      float2 v = make_float2(0.f, -INFINITY);
+      if ((o >> 7) < a.G) {
+        unsigned long long* pp = a.part_elem + (unit * S + p) * 512 + o;
+        unsigned long long w;
+        while ((w = ld_relaxed_gpu_u64(pp)) == 0ull) __nanosleep(20);
+        st_relaxed_gpu_u64(pp, 0ull);
+        w = ~w;
+        v = make_float2(__uint_as_float(static_cast<uint32_t>(w)), __uint_as_float(static_cast<uint32_t>(w >> 32)));
       }
+      stage[e] = v;
     }
     __syncthreads();
     phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);
-    const int per = (4 * 128 + a.S - 1) / a.S;
-    const int idx = s * per + tid;
-    if (tid < per && idx < 4 * 128) {
-      const int g = idx >> 7, dim = idx & 127;
-      if (g < a.G) {
-        const float* pl = a.part_l + unit * a.S * 4 + g;
-        const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
-        float m = -INFINITY, wsum = 0.f, osum = 0.f;
-        for (int s0 = 0; s0 < a.S; s0 += 32) {
-          float lv[32], xv[32];
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const bool ok = s0 + k < a.S;
-            lv[k] = ok ? ld_na_f32(pl + 4 * (s0 + k)) : -INFINITY;
-            xv[k] = ok ? ld_na_f32(po + static_cast<int64_t>(s0 + k) * 512) : 0.f;
-          }
-          float mc = -INFINITY;
-#pragma unroll
-          for (int k = 0; k < 32; ++k) mc = fmaxf(mc, lv[k]);
-          const float mn = fmaxf(m, mc);
-          if (mn == -INFINITY) continue;
-          const float sc = m == -INFINITY ? 0.f : ex2_approx(m - mn);
-          osum *= sc;
-          wsum *= sc;
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const float f = lv[k] == -INFINITY ? 0.f : ex2_approx(lv[k] - mn);
-            wsum += f;
-            osum += f * xv[k];
-          }
-          m = mn;
+    for (int t = tid; t < nout; t += NTHREADS) {
+      const int o = o0 + t, g = o >> 7, dim = o & 127;
+      if (g >= a.G) continue;
+      const float2* sv = stage + t * S;
+      float m = -INFINITY;
+      for (int p = 0; p < S; ++p) m = fmaxf(m, sv[p].y);
+      float wsum = 0.f, osum = 0.f;
+      if (m != -INFINITY) {
+        for (int p = 0; p < S; ++p) {
+          const float f = sv[p].y == -INFINITY ? 0.f : ex2_approx(sv[p].y - m);
+          wsum += f;
+          osum += f * sv[p].x;
         }
-        const bool empty = !(wsum > 0.f);
-        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
-        const float ov = empty ? 0.f : osum / wsum;
-        if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
-        else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-        if (dim == 0 && a.lse)
-          a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
       }
+      const bool empty = !(wsum > 0.f);
+      const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+      const float ov = empty ? 0.f : osum * __frcp_rn(wsum);
+      if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
+      else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
+      if (dim == 0 && a.lse)
+        a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
     }
     return;
   }
