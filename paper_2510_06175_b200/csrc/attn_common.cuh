@@ -199,6 +199,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     // split) element polls it until published (non-zero), consumes it (stores zero back: every
     // element is read exactly once, so the workspace is clean for the next launch) and stages it
     // in shared memory; then one thread per output combines its S splits in order s = 0..S-1.
+    phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 8);
     const int S = a.S;
     const int per = (4 * 128 + S - 1) / S;
     const int o0 = s * per, nout = max(0, min(4 * 128, o0 + per) - o0);

@@ -81,8 +81,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   const uint16_t* cbk = a.ck + h * a.ck_hs;
   const uint16_t* cbv = a.cv + h * a.cv_hs;
   fill_tables<KB, VB>(tab, cbk, cbv, tid);
+  float4 lam4 = make_float4(0.f, 0.f, 0.f, 0.f);   // warps 0..3: lambda of head h (static)
+  if (warp < 4) lam4 = *reinterpret_cast<const float4*>(a.lambda + h * 128 + 4 * lane);
   if (first) griddep_wait();
   first = false;
+  // q of the warp's query head goes out right after the wait, next to the seq_lens read below
+  uint2 qw = make_uint2(0u, 0u);
+  if (warp < a.G) qw = *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (h * a.G + warp) * a.q_sh + 4 * lane);
 
   int64_t r0, r1, beg, e;
   split_range(a, b, s, r0, r1, &beg, &e);
@@ -168,7 +173,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           *reinterpret_cast<const uint2*>(vrow + 4 * lane);
     }
   }
-  if (warp < 4) query_transform_warp(a, b, h, warp, sq + kQRow * warp, true);
+  if (warp < 4) {   // Eq. 7 query transform (heads g >= G are zero padding)
+    float* dq = sq + kQRow * warp + qoff(lane);
+    if (warp < a.G) qtransform_lane(qw, lam4, a.qscale, lane, dq);
+    else *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   __syncthreads();
   if (kCanAppend && owner) {
     if (warp == 0 || warp == 8) {

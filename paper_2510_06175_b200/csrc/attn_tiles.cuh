@@ -152,4 +152,27 @@ __device__ __forceinline__ void put_code(unsigned char* row, int lane, uint32_t 
   }
 }
 
+// Query transform of Eq. 7 for one head (one warp): ((q * lambda) H_pm) * qscale, fp32 FWHT
+// (2 register + 5 shuffle stages); q (4 bf16) and lambda (float4) are this lane's 4 channels;
+// dst = this lane's 4 outputs (sub-vector `lane`).
+__device__ __forceinline__ void qtransform_lane(uint2 w, float4 l, float qscale, int lane, float* dst) {
+  float x[4];
+  x[0] = __uint_as_float(w.x << 16) * l.x;
+  x[1] = __uint_as_float(w.x & 0xFFFF0000u) * l.y;
+  x[2] = __uint_as_float(w.y << 16) * l.z;
+  x[3] = __uint_as_float(w.y & 0xFFFF0000u) * l.w;
+  float s0 = x[0] + x[1], s1 = x[0] - x[1], s2 = x[2] + x[3], s3 = x[2] - x[3];
+  x[0] = s0 + s2; x[2] = s0 - s2; x[1] = s1 + s3; x[3] = s1 - s3;
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float o = __shfl_xor_sync(0xffffffffu, x[i], m);
+      x[i] = upper ? (o - x[i]) : (x[i] + o);
+    }
+  }
+  *reinterpret_cast<float4*>(dst) = make_float4(x[0] * qscale, x[1] * qscale, x[2] * qscale, x[3] * qscale);
+}
+
 }  // namespace vecinfer

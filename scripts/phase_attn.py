@@ -60,17 +60,23 @@ def main():
             if x.size:
                 print(f"   {name:32s} min {x.min():7.2f}  med {np.median(x):7.2f}  max {x.max():7.2f} us  (n={x.size})")
         st(rel[:, 0], "CTA start (rel)")
-        st(rel[:, 6] - rel[:, 0], "prologue: fill+wait+segs")
-        st(rel[:, 12] - rel[:, 6], "prologue: piece setup (loads)")
-        st(rel[:, 11] - rel[:, 12], "prologue: q~ transform")
-        st(rel[:, 1] - rel[:, 11], "prologue: encode + sync")
-        st(rel[:, 2] - rel[:, 1], "main loop warp 0 (last round)")
-        st(rel[:, 7] - rel[:, 2], "wait for slowest warp")
-        st(rel[:, 9] - rel[:, 7], "combine + store")
-        st(rel[:, 10] - rel[:, 9], "sync")
-        st(rel[:, 3] - rel[:, 10], "arrive")
-        st(rel[:, 5] - rel[:, 3], "spin wait (deferred merges)")
-        st(rel[:, 4] - rel[:, 5], "slice merge")
+        if np.isfinite(rel[:, 12]).any():   # stream kernel (attn_stream.cu) stamps
+            st(rel[:, 6] - rel[:, 0], "prologue: fill+wait+segs")
+            st(rel[:, 12] - rel[:, 6], "prologue: piece setup (loads)")
+            st(rel[:, 11] - rel[:, 12], "prologue: q~ transform")
+            st(rel[:, 1] - rel[:, 11], "prologue: encode + sync")
+            st(rel[:, 2] - rel[:, 1], "main loop warp 0 (last round)")
+            st(rel[:, 7] - rel[:, 2], "wait for slowest warp")
+            st(rel[:, 9] - rel[:, 7], "combine + store")
+            st(rel[:, 5] - rel[:, 3], "spin wait (deferred merges)")
+            st(rel[:, 4] - rel[:, 5], "slice merge")
+        else:                                # split kernel (attn_mma.cu) stamps
+            st(rel[:, 1] - rel[:, 0], "prologue (fill+q~+sync)")
+            st(rel[:, 2] - rel[:, 1], "main loop warp 0 (incl. bq)")
+            st(rel[:, 3] - rel[:, 2], "warp partials -> smem + sync")
+            st(rel[:, 8] - rel[:, 3], "combine + publish")
+            st(rel[:, 5] - rel[:, 8], "poll + stage (wait for splits)")
+            st(rel[:, 4] - rel[:, 5], "slice merge")
         st(rel[:, 4], "CTA end (rel)")
 
 if __name__ == "__main__":
