@@ -249,9 +249,9 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(device=dev)
 
     fused = not args.unfused and not seq_sharded
-    # vecinfer_decode_step itself fuses only single-wave grids with <= 8-bit codes
-    fused_launch = fused and (bool(R) or (kbits <= 8 and vbits <= 8 and
-                                          vi.attn_num_splits(B, H_KV, n_local, 0) * B * H_KV <= 148))
+    # launches of one vecinfer_decode_step (the library decides whether the append is fused)
+    fused_launch = fused and vi.decode_step_launches(B, H_KV, n_local, kcfg, vcfg, residual_append=bool(R)) == 1
+    kernel_kind = vi.attn_kernel_kind(B, H_KV)
 
     def layer(l, ev_pair=None):
         if fused and R:   # one launch: the new token goes to residual row R-1, attention over codes + window
@@ -289,8 +289,8 @@ def run_ours(args, rank, world, local_rank):
                          o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D))
 
     append_kernels = 2 if max(kbits, vbits) == 16 else 1      # 16-bit: centroid-split search + finalize
-    if fused_launch:
-        launches_per_step = L
+    if fused:
+        launches_per_step = L * vi.decode_step_launches(B, H_KV, n_local, kcfg, vcfg, residual_append=bool(R))
     else:
         launches_per_step = L * ((append_kernels if owns_tail else 0) + 1) + (1 if seq_sharded else 0)
 
@@ -467,12 +467,15 @@ def run_ours(args, rank, world, local_rank):
                    "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": f"K-{CB_NAME[kbits]}/V-{CB_NAME[vbits]}",
                    "parallelism": ("seq-shard" if seq_sharded else "dp") + str(world),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
-                   "num_splits": S, "cuda_graph": use_graph, "residual_window": R, "fused_append": fused_launch,
+                   "num_splits": S, "attn_kernel": kernel_kind, "cuda_graph": use_graph, "residual_window": R, "fused_append": fused_launch,
                    "dtype_detail": "u8 codes, bf16 q/k/v/o, fp16 hi/lo MMA operands, f32 accumulate"},
         "us_per_layer_call": step_ms * 1e3 / L,
         "tokens_per_s": B_glob * 1e3 / step_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "attn_mma_kernel<KB,VB> (vecinfer_attn_decode / vecinfer_decode_step)",
+                     "traffic": traffic,
+                     "kernel": ("attn_stream_kernel<KB,VB> (stream partition, attn_stream.cu)" if kernel_kind == "stream"
+                                else "attn_mma_kernel<KB,VB> (split-KV, attn_mma.cu)") +
+                               " via vecinfer_attn_decode / vecinfer_decode_step",
                      "attn_us_avg": attn_avg_ms * 1e3, "attn_us_p10": float(np.percentile(attn_ms, 10)) * 1e3,
                      "attn_us_p90": float(np.percentile(attn_ms, 90)) * 1e3,
                      "timing": "CUDA events around K replays of a graph of the 32 layers' vecinfer_attn_decode launches "

@@ -192,6 +192,9 @@ int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max,
                                  int32_t num_splits);
 int32_t vecinfer_attn_num_ctas(int32_t B, int32_t H_kv, int64_t n_tokens_max,
                                int32_t num_splits);
+/* which kernel a call with these arguments runs: 0 = split kernel, 1 = stream kernel, 2 = LUT */
+int32_t vecinfer_attn_kernel_kind(int32_t B, int32_t H_kv, int32_t num_splits,
+                                  vecinfer_attn_algo_t algo);
 size_t vecinfer_attn_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int32_t D,
                                      int64_t n_tokens_max, int32_t num_splits);
 vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_q,
@@ -224,6 +227,10 @@ vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_
  *   algo = VECINFER_ATTN_LUT the call is executed as the two separate launches.
  * Errors: as vecinfer_encode_kv and vecinfer_attn_decode.
  * ------------------------------------------------------------------------------------- */
+/* kernel launches one vecinfer_decode_step call makes (1: the append is fused into attention) */
+int32_t vecinfer_decode_step_launches(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t kcfg,
+                                      vecinfer_vq_t vcfg, int32_t num_splits,
+                                      vecinfer_attn_algo_t algo, int32_t residual_append);
 size_t vecinfer_decode_step_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int64_t n_cap,
                                             vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, int32_t num_splits);
 vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,

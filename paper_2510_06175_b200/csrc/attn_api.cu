@@ -300,6 +300,40 @@ extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B,
                    num_splits, algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false);
 }
 
+// Whether vecinfer_decode_step runs the append-encode inside the attention launch.  Split kernel:
+// only single-wave grids (the owner CTA's encode then hides behind the other CTAs' longer splits;
+// with several waves every wave would carry it, and one separate append launch is cheaper).
+// Stream kernel: always when every CTA is resident (the partition budgets the encode).  Never for
+// 16-bit codebooks or the LUT variant.
+static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
+                         int32_t num_splits, vecinfer_attn_algo_t algo) {
+  if (algo == VECINFER_ATTN_LUT || kcfg.code_bits > 8 || vcfg.code_bits > 8 || B <= 0 || H_kv <= 0) return false;
+  const int64_t units = static_cast<int64_t>(B) * H_kv;
+  if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
+    return num_splits == 0 || units * num_splits <= device_sm_count();   // persistent grids: separate append
+  if (use_stream(B, H_kv, num_splits, false)) return true;
+  const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
+  const int mac = plan.cluster ? attn_mma_max_active_clusters(plan.S) : 0;
+  const int64_t waves = plan.cluster ? (units + (mac > 0 ? mac : 1) - 1) / (mac > 0 ? mac : 1)
+                                     : (units * plan.S + device_sm_count() - 1) / device_sm_count();
+  return waves <= 1;
+}
+
+// which attention kernel a call runs: 0 split (attn_mma.cu), 1 stream (attn_stream.cu), 2 LUT
+extern "C" int32_t vecinfer_attn_kernel_kind(int32_t B, int32_t H_kv, int32_t num_splits, vecinfer_attn_algo_t algo) {
+  if (algo == VECINFER_ATTN_LUT) return 2;
+  return use_stream(B, H_kv, num_splits, false, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM) ? 1 : 0;
+}
+
+// kernel launches of one vecinfer_decode_step call (1 = append fused into the attention launch)
+extern "C" int32_t vecinfer_decode_step_launches(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t kcfg,
+                                                 vecinfer_vq_t vcfg, int32_t num_splits, vecinfer_attn_algo_t algo,
+                                                 int32_t residual_append) {
+  if (residual_append) return 1;
+  if (decode_fuses(B, H_kv, n_cap, kcfg, vcfg, num_splits, algo)) return 1;
+  return 1 + ((kcfg.code_bits == 16 || vcfg.code_bits == 16) ? 2 : 1);   // 16-bit: split search + finalize
+}
+
 extern "C" size_t vecinfer_decode_step_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int64_t n_cap,
                                                        vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, int32_t num_splits) {
   const size_t a = (vecinfer_attn_workspace_bytes(B, H_q, H_kv, 128, n_cap, num_splits) + 255) & ~size_t(255);
@@ -333,21 +367,7 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
                      algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, true);
   }
-  // Fuse only when the grid is one wave: the owner CTA's encode latency (~1-2 us) then hides
-  // behind the other CTAs' longer splits; with several waves every wave would carry it, and a
-  // separate append launch (latency ~3 us, once) is cheaper.
-  bool fuse = algo != VECINFER_ATTN_LUT && kcfg.code_bits <= 8 && vcfg.code_bits <= 8;
-  const bool forced_stream = algo == VECINFER_ATTN_DEQUANT_MMA_STREAM;
-  if (fuse && forced_stream) fuse = num_splits == 0 ||
-      static_cast<int64_t>(B) * H_kv * num_splits <= device_sm_count();   // persistent grids: separate append
-  else if (fuse && B > 0 && H_kv > 0 && !use_stream(B, H_kv, num_splits, false)) {   // (stream: V <= #SMs)
-    const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
-    const int64_t units = static_cast<int64_t>(B) * H_kv;
-    const int64_t waves = plan.cluster ? (units + attn_mma_max_active_clusters(plan.S) - 1) /
-                                             (attn_mma_max_active_clusters(plan.S) > 0 ? attn_mma_max_active_clusters(plan.S) : 1)
-                                       : (units * plan.S + device_sm_count() - 1) / device_sm_count();
-    fuse = waves <= 1;
-  }
+  const bool fuse = decode_fuses(B, H_kv, n_cap, kcfg, vcfg, num_splits, algo);
   if (!fuse) {   // separate append + attention launches (always for the paper-faithful LUT variant)
     const int64_t ks[3] = {k_new_strides[0], 0, k_new_strides[1]};
     const int64_t vs[3] = {v_new_strides[0], 0, v_new_strides[1]};

@@ -138,6 +138,21 @@ def attn_num_ctas(B: int, H_kv: int, n_tokens_max: int, num_splits: int = 0) -> 
     return _lib.load().vecinfer_attn_num_ctas(B, H_kv, n_tokens_max, num_splits)
 
 
+def attn_kernel_kind(B: int, H_kv: int, num_splits: int = 0, algo: str = "auto") -> str:
+    """Which attention kernel a call runs: "split" (attn_mma.cu), "stream" (attn_stream.cu) or "lut"."""
+    k = _lib.load().vecinfer_attn_kernel_kind(B, H_kv, num_splits, ALGOS[algo])
+    return ("split", "stream", "lut")[k]
+
+
+def decode_step_launches(B: int, H_kv: int, n_cap: int, kcfg: VQConfig = None, vcfg: VQConfig = None,
+                         num_splits: int = 0, algo: str = "auto", residual_append: bool = False) -> int:
+    """Kernel launches of one decode_step call (1: the append-encode is fused into attention)."""
+    kcfg = kcfg or B2D4
+    vcfg = vcfg or B2D4
+    return _lib.load().vecinfer_decode_step_launches(B, H_kv, n_cap, kcfg.c(), vcfg.c(), num_splits, ALGOS[algo],
+                                                     int(residual_append))
+
+
 def attn_workspace(B: int, H_q: int, H_kv: int, n_tokens_max: int, num_splits: int = 0, device="cuda"):
     """Zero-filled workspace for attn_decode (counters must start at zero; the kernel resets them)."""
     n = _lib.load().vecinfer_attn_workspace_bytes(B, H_q, H_kv, 128, n_tokens_max, num_splits)

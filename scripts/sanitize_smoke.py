@@ -28,9 +28,14 @@ for name, cfg in (("b1d4", vi.B1D4), ("b2d4", vi.B2D4), ("b4d4", vi.B4D4)):
     seq = torch.tensor([N, N // 3], dtype=torch.int32, device=dev)
     for splits in (0, 1, 3, 20):
         vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, kcfg=cfg, vcfg=cfg)
+    # stream kernel: straddling pieces (auto), fixed pieces, persistent last-arriver merge (80 x 16 > #SMs)
+    for splits in (0, 3, 80):
+        vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, kcfg=cfg, vcfg=cfg, algo="stream")
     kn, vn = k[:, 0].contiguous(), v[:, 0].contiguous()
     vi.decode_step(q, kn, vn, lam, inv, ck, cv, kc, vc, torch.tensor([N, N // 3], dtype=torch.int32, device=dev),
                    seq + 1, kcfg=cfg, vcfg=cfg)
+    vi.decode_step(q, kn, vn, lam, inv, ck, cv, kc, vc, torch.tensor([N, N // 3], dtype=torch.int32, device=dev),
+                   seq + 1, kcfg=cfg, vcfg=cfg, algo="stream")
 ck = T(synth.bf16_from_bits(z["ck_b2d4"])).to(torch.bfloat16)
 vi.attn_decode(q, lam, ck, ck, kc[..., :32].contiguous() if kc.shape[-1] >= 32 else kc, vc[..., :32].contiguous(),
                seq, algo="lut") if False else None
