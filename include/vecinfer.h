@@ -168,7 +168,9 @@ vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int
  * pieces so that every CTA (one per SM) gets the same number of tokens; the log-sum-exp merge
  * of the pieces of a split unit is fused into the same launch (fixed piece order).
  *   q_bf16      [B, H_q, D] raw queries (strides q_stride_b, q_stride_h); query head i reads
- *               KV head i / G (GQA).  The kernel applies q~ = q diag(lambda) H_D (Eq. 7).
+ *               KV head i / G (GQA, G = H_q / H_kv in 1..8; groups of 5..8 run as two virtual KV
+ *               heads of <= 4 query heads that share the codes).  The kernel applies
+ *               q~ = q diag(lambda) H_D (Eq. 7).
  *   lambda      fp32 [H_kv, D].
  *   codebooks / codes / n_cap as in vecinfer_encode_kv (kcfg, vcfg may differ).
  *   seq_lens    device int32 [B]; tokens [tok_begin, min(tok_end, seq_len)) are attended
@@ -187,7 +189,9 @@ vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int
  * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, WORKSPACE, CUDA.
  * ------------------------------------------------------------------------------------- */
 /* pieces per unit (num_splits if > 0, else the heuristic's upper bound), and the number of
- * virtual CTAs V of the partition (the grid is min(V, #SMs) persistent CTAs) */
+ * virtual CTAs V of the partition (the grid is min(V, #SMs) persistent CTAs).  These queries and
+ * vecinfer_attn_kernel_kind / vecinfer_decode_step_launches take the number of attention units per
+ * batch row as H_kv: pass 2 * H_kv when H_q / H_kv > 4 (virtual KV heads). */
 int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max,
                                  int32_t num_splits);
 int32_t vecinfer_attn_num_ctas(int32_t B, int32_t H_kv, int64_t n_tokens_max,

@@ -57,6 +57,12 @@ WsLayout ws_layout(int32_t B, int32_t H_kv, int32_t S, bool stream_region) {
   return w;
 }
 
+// GQA groups of 5..8 query heads run as two virtual KV heads per KV head (head_map in
+// attn_common.cuh); every plan below is made over the virtual heads.
+static int hsplit_of(int32_t H_q, int32_t H_kv) {
+  return (H_kv > 0 && H_q % H_kv == 0 && H_q / H_kv > 4) ? 2 : 1;
+}
+
 // Stream kernel (attn_stream.cu) for batch decode: B*H_kv >= #SMs units over V = #SMs CTAs (a
 // unit crossing a CTA boundary is split in two and merged).  VECINFER_STREAM=0 disables it,
 // =1 forces it for any auto-split call (experiments).
@@ -143,8 +149,9 @@ extern "C" size_t vecinfer_attn_workspace_bytes(int32_t B, int32_t H_q, int32_t 
                                                 int32_t num_splits) {
   (void)H_q; (void)D;
   if (B <= 0 || H_kv <= 0) return 0;
-  const int32_t S = plan_splits(B, H_kv, n_tokens_max, num_splits).S;
-  return ws_layout(B, H_kv, S, true).total;
+  const int32_t Hv = H_kv * hsplit_of(H_q, H_kv);
+  const int32_t S = plan_splits(B, Hv, n_tokens_max, num_splits).S;
+  return ws_layout(B, Hv, S, true).total;
 }
 
 struct AppendArgs {
@@ -174,8 +181,14 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad algo");
   if (B <= 0 || H_q <= 0 || H_kv <= 0 || n_cap <= 0) return fail(VECINFER_ERR_SHAPE, "attn_decode: non-positive size");
   if (H_q % H_kv != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode: H_q %% H_kv != 0");
-  const int G = H_q / H_kv;
-  if (G != 1 && G != 2 && G != 4) return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: GQA group %d not in {1,2,4}", G);
+  const int Gfull = H_q / H_kv;
+  if (Gfull > 8) return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: GQA group %d > 8", Gfull);
+  if (Gfull > 4 && algo == VECINFER_ATTN_LUT)
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: the LUT variant supports GQA groups <= 4");
+  const int hsplit = hsplit_of(H_q, H_kv);
+  const int G = hsplit == 1 ? Gfull : 4;   // query heads per virtual head (the last may hold fewer)
+  const int32_t H_kv_real = H_kv;
+  H_kv *= hsplit;                          // from here on: virtual KV heads
   if (!vq_ok(kcfg) || !vq_ok(vcfg))
     return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: supported configs are D=128, d=4, code_bits in {4,8,16}");
   if (algo == VECINFER_ATTN_LUT && (kcfg.code_bits != 8 || vcfg.code_bits != 8))
@@ -217,6 +230,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.q = static_cast<const uint16_t*>(q_bf16);
   a.q_sb = q_stride_b; a.q_sh = q_stride_h;
   a.B = B; a.Hq = H_q; a.Hkv = H_kv; a.G = G;
+  a.Hc = H_kv_real; a.hsplit = hsplit; a.Gfull = Gfull;
   a.lambda = lambda;
   a.ck = static_cast<const uint16_t*>(ck_bf16);
   a.cv = static_cast<const uint16_t*>(cv_bf16);
@@ -367,7 +381,7 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
                      algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, true);
   }
-  const bool fuse = decode_fuses(B, H_kv, n_cap, kcfg, vcfg, num_splits, algo);
+  const bool fuse = decode_fuses(B, H_kv * hsplit_of(H_q, H_kv), n_cap, kcfg, vcfg, num_splits, algo);
   if (!fuse) {   // separate append + attention launches (always for the paper-faithful LUT variant)
     const int64_t ks[3] = {k_new_strides[0], 0, k_new_strides[1]};
     const int64_t vs[3] = {v_new_strides[0], 0, v_new_strides[1]};

@@ -7,7 +7,8 @@ namespace vecinfer {
 struct AttnArgs {
   const uint16_t* q;  // bf16 [B, Hq, D]
   int64_t q_sb, q_sh;
-  int B, Hq, Hkv, G;
+  int B, Hq, Hkv, G;   // Hkv: VIRTUAL KV heads (= Hc * hsplit); G: query heads per virtual head (<= 4)
+  int Hc, hsplit, Gfull;   // code/cache KV heads, virtual heads per KV head (GQA group > 4), full group
   const float* lambda;  // [Hkv, 128]
   const uint16_t* ck;   // bf16 codebooks
   const uint16_t* cv;
@@ -64,6 +65,27 @@ struct AttnArgs {
 // shorten that split so it does not become the straggler
 constexpr int64_t kAppendTokenCost = 160;
 
+// GQA groups of up to 8 query heads run as hsplit = ceil(G/4) virtual KV heads of <= 4 query
+// heads each: virtual head h reads the codes, codebooks and lambda of KV head hc = h / hsplit and
+// serves query heads hq0 .. hq0 + gp - 1.  (hsplit = 1: h == hc, hq0 = h * G, gp = G.)
+struct HeadMap {
+  int hc;    // KV head (codes, codebooks, lambda, k_new/v_new, residual rows)
+  int hq0;   // first query head
+  int gp;    // query heads in this virtual head (<= 4)
+};
+__device__ __forceinline__ HeadMap head_map(const AttnArgs& a, int h) {
+  HeadMap m;
+  if (a.hsplit == 1) {
+    m.hc = h; m.hq0 = h * a.G; m.gp = a.G;
+  } else {
+    m.hc = h >> 1;
+    const int half = h & 1;
+    m.hq0 = m.hc * a.Gfull + 4 * half;
+    m.gp = half ? a.Gfull - 4 : 4;
+  }
+  return m;
+}
+
 // merge of the pieces of a unit split over several CTAs (stream kernel)
 constexpr int kMergeNone = 0;   // every unit is processed by one CTA
 constexpr int kMergeSpin = 1;   // all CTAs co-resident: publish, then each piece merges a slice
@@ -111,9 +133,10 @@ __device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int
 template <int NTHREADS>
 __device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
+  const HeadMap hm = head_map(a, h);
   for (int idx = threadIdx.x; idx < 4 * 128; idx += NTHREADS) {
     const int g = idx >> 7, dim = idx & 127;
-    if (g >= a.G) continue;
+    if (g >= hm.gp) continue;
     const float* pl = a.part_l + unit * a.S * 4 + g;
     const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
     float m = -INFINITY, wsum = 0.f, osum = 0.f;
@@ -143,10 +166,10 @@ __device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
     }
     const bool empty = !(wsum > 0.f);
     const float ov = empty ? 0.f : osum / wsum;
-    const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+    const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * 128 + dim;
     if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
     else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-    if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
+    if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
   }
 }
 
@@ -156,6 +179,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
                                            float* scratch) {
   const int tid = threadIdx.x;
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
+  const HeadMap hm = head_map(a, h);
   __shared__ bool s_last;
   for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
     const int g = idx >> 7, dim = idx & 127;
@@ -175,11 +199,11 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     const float ov = empty ? 0.f : osum / lsum;
     const float L2 = empty ? -INFINITY : M + __log2f(lsum);
     if (a.S == 1) {
-      if (g < a.G) {
-        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+      if (g < hm.gp) {
+        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * 128 + dim;
         if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
         else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-        if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = L2 * kLn2;
+        if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = L2 * kLn2;
       }
     } else if (a.merge_spin) {
       // publish (o_s, L_s) as one 64-bit relaxed store of ~(L_s << 32 | o_s) (zero = empty)
@@ -207,7 +231,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     for (int e = tid; e < nout * S; e += NTHREADS) {
       const int oo = e / S, p = e - oo * S, o = o0 + oo;
       float2 v = make_float2(0.f, -INFINITY);
-      if ((o >> 7) < a.G) {
+      if ((o >> 7) < hm.gp) {
         unsigned long long* pp = a.part_elem + (unit * S + p) * 512 + o;
         unsigned long long w;
         while ((w = ld_relaxed_gpu_u64(pp)) == 0ull) __nanosleep(20);
@@ -221,7 +245,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);
     for (int t = tid; t < nout; t += NTHREADS) {
       const int o = o0 + t, g = o >> 7, dim = o & 127;
-      if (g >= a.G) continue;
+      if (g >= hm.gp) continue;
       const float2* sv = stage + t * S;
       float m = -INFINITY;
       for (int p = 0; p < S; ++p) m = fmaxf(m, sv[p].y);
@@ -234,12 +258,12 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
         }
       }
       const bool empty = !(wsum > 0.f);
-      const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+      const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * 128 + dim;
       const float ov = empty ? 0.f : osum * __frcp_rn(wsum);
       if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
       else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
       if (dim == 0 && a.lse)
-        a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
+        a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
     }
     return;
   }
@@ -269,10 +293,11 @@ __device__ __forceinline__ void query_transform_warp(const AttnArgs& a, int b, i
                                                      bool padded = false) {
   const int lane = threadIdx.x & 31;
   float x[4] = {0.f, 0.f, 0.f, 0.f};
-  if (g < a.G) {
-    const uint16_t* qp = a.q + b * a.q_sb + (h * a.G + g) * a.q_sh + 4 * lane;
+  const HeadMap hm = head_map(a, h);
+  if (g < hm.gp) {
+    const uint16_t* qp = a.q + b * a.q_sb + (hm.hq0 + g) * a.q_sh + 4 * lane;
     const uint2 w = *reinterpret_cast<const uint2*>(qp);
-    const float4 l = *reinterpret_cast<const float4*>(a.lambda + h * 128 + 4 * lane);
+    const float4 l = *reinterpret_cast<const float4*>(a.lambda + hm.hc * 128 + 4 * lane);
     x[0] = __uint_as_float(w.x << 16) * l.x;
     x[1] = __uint_as_float(w.x & 0xFFFF0000u) * l.y;
     x[2] = __uint_as_float(w.y << 16) * l.z;

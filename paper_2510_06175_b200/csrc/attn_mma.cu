@@ -78,22 +78,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   // static weights first (codebooks): with programmatic dependent launch this overlaps the
   // tail of the previous kernel on the stream; everything dynamic is read after the wait
-  const uint16_t* cbk = a.ck + h * a.ck_hs;
-  const uint16_t* cbv = a.cv + h * a.cv_hs;
+  const HeadMap hm = head_map(a, h);   // virtual head h -> KV head hm.hc, query heads hm.hq0 ..
+  const int hc = hm.hc;
+  const uint16_t* cbk = a.ck + hc * a.ck_hs;
+  const uint16_t* cbv = a.cv + hc * a.cv_hs;
   fill_tables<KB, VB>(tab, cbk, cbv, tid);
   float4 lam4 = make_float4(0.f, 0.f, 0.f, 0.f);   // warps 0..3: lambda of head h (static)
-  if (warp < 4) lam4 = *reinterpret_cast<const float4*>(a.lambda + h * 128 + 4 * lane);
+  if (warp < 4) lam4 = *reinterpret_cast<const float4*>(a.lambda + hc * 128 + 4 * lane);
   if (first) griddep_wait();
   first = false;
   // q of the warp's query head goes out right after the wait, next to the seq_lens read below
   uint2 qw = make_uint2(0u, 0u);
-  if (warp < a.G) qw = *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (h * a.G + warp) * a.q_sh + 4 * lane);
+  if (warp < hm.gp) qw = *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (hm.hq0 + warp) * a.q_sh + 4 * lane);
 
   int64_t r0, r1, beg, e;
   split_range(a, b, s, r0, r1, &beg, &e);
   const int ntok = static_cast<int>(r1 - r0);
   const int ntile = (ntok + 31) >> 5;
-  const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
+  const int64_t unit = static_cast<int64_t>(b) * a.Hc + hc;   // cache unit of the codes
   // fused decode append: the split holding row p = write_pos[b] (else split 0) encodes the new token
   bool owner = false;
   int patch_tile = -1, patch_row = 0;
@@ -133,11 +135,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     if (lane < P) stage[warp * 32 + lane] = bf16x4_to_float4(*reinterpret_cast<const uint2*>(cb + 4 * (P * w8 + lane)));
     float x[4];
     if (!isv) {
-      const bool bad = key_transform_lane(a.knew + b * a.kn_sb + h * a.kn_sh + 4 * lane,
-                                          a.inv_lambda + h * 128 + 4 * lane, a.inv_sqrt_d, lane, x);
+      const bool bad = key_transform_lane(a.knew + b * a.kn_sb + hc * a.kn_sh + 4 * lane,
+                                          a.inv_lambda + hc * 128 + 4 * lane, a.inv_sqrt_d, lane, x);
       if (bad && warp == 0 && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
     } else {
-      const float4 v = bf16x4_to_float4(*reinterpret_cast<const uint2*>(a.vnew + b * a.vn_sb + h * a.vn_sh + 4 * lane));
+      const float4 v = bf16x4_to_float4(*reinterpret_cast<const uint2*>(a.vnew + b * a.vn_sb + hc * a.vn_sh + 4 * lane));
       x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
     }
     __syncwarp();
@@ -157,13 +159,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   // window) is taken from k_new / v_new by its owner warp, which also writes it to the window
   const int rlen = a.res ? min(a.res_lens[b], static_cast<int32_t>(a.r_cap)) : 0;
   const int t_res0 = s + a.S * warp;
-  const int64_t res_off = a.res ? b * a.res_sb + h * a.res_sh : 0;
+  const int64_t res_off = a.res ? b * a.res_sb + hc * a.res_sh : 0;
   uint2 rk = make_uint2(0u, 0u);
   uint4 rv0 = make_uint4(0u, 0u, 0u, 0u), rv1 = rv0;
   if (t_res0 < rlen) {
     const bool is_new = a.res_append && t_res0 == rlen - 1;
-    const uint16_t* krow = is_new ? a.knew + b * a.kn_sb + h * a.kn_sh : a.kres + res_off + t_res0 * 128;
-    const uint16_t* vrow = is_new ? a.vnew + b * a.vn_sb + h * a.vn_sh : a.vres + res_off + t_res0 * 128;
+    const uint16_t* krow = is_new ? a.knew + b * a.kn_sb + hc * a.kn_sh : a.kres + res_off + t_res0 * 128;
+    const uint16_t* vrow = is_new ? a.vnew + b * a.vn_sb + hc * a.vn_sh : a.vres + res_off + t_res0 * 128;
     rk = *reinterpret_cast<const uint2*>(krow + 4 * lane);
     rv0 = *reinterpret_cast<const uint4*>(vrow + 16 * r);
     rv1 = *reinterpret_cast<const uint4*>(vrow + 16 * r + 8);
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   }
   if (warp < 4) {   // Eq. 7 query transform (heads g >= G are zero padding)
     float* dq = sq + kQRow * warp + qoff(lane);
-    if (warp < a.G) qtransform_lane(qw, lam4, a.qscale, lane, dq);
+    if (warp < hm.gp) qtransform_lane(qw, lam4, a.qscale, lane, dq);
     else *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncthreads();
@@ -238,8 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     float qr[4][4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-      const float4 v = g < a.G ? bf16x4_to_float4(*reinterpret_cast<const uint2*>(
-                                     a.q + b * a.q_sb + (h * a.G + g) * a.q_sh + 4 * lane))
+      const float4 v = g < hm.gp ? bf16x4_to_float4(*reinterpret_cast<const uint2*>(
+                                       a.q + b * a.q_sb + (hm.hq0 + g) * a.q_sh + 4 * lane))
                                : make_float4(0.f, 0.f, 0.f, 0.f);
       qr[g][0] = v.x * a.qscale_raw; qr[g][1] = v.y * a.qscale_raw;
       qr[g][2] = v.z * a.qscale_raw; qr[g][3] = v.w * a.qscale_raw;
@@ -249,8 +251,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         const uint16_t* krow = a.kres + res_off + t * 128;
         const uint16_t* vrow = a.vres + res_off + t * 128;
         const bool is_new = a.res_append && t == rlen - 1;
-        rk = *reinterpret_cast<const uint2*>((is_new ? a.knew + b * a.kn_sb + h * a.kn_sh : krow) + 4 * lane);
-        const uint16_t* vsrc = is_new ? a.vnew + b * a.vn_sb + h * a.vn_sh : vrow;
+        rk = *reinterpret_cast<const uint2*>((is_new ? a.knew + b * a.kn_sb + hc * a.kn_sh : krow) + 4 * lane);
+        const uint16_t* vsrc = is_new ? a.vnew + b * a.vn_sb + hc * a.vn_sh : vrow;
         rv0 = *reinterpret_cast<const uint4*>(vsrc + 16 * r);
         rv1 = *reinterpret_cast<const uint4*>(vsrc + 16 * r + 8);
         if (is_new) {
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
     cluster_sync_all();
     phase_mark(a.phase, cta_id, 5);
-    if (rank == 0 && g < a.G) {
+    if (rank == 0 && g < hm.gp) {
       float Mx = -INFINITY;
       for (int q = 0; q < a.S; ++q) Mx = fmaxf(Mx, cM[q * 4 + g]);
       float os = 0.f, ls = 0.f;
@@ -464,11 +466,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         }
       }
       const bool empty = !(ls > 0.f);
-      const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+      const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * 128 + dim;
       const float ov = empty ? 0.f : os / ls;
       if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
       else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-      if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (Mx + __log2f(ls)) * kLn2;
+      if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = empty ? -INFINITY : (Mx + __log2f(ls)) * kLn2;
     }
   }
   phase_mark(a.phase, cta_id, 4);

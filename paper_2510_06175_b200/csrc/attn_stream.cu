@@ -62,7 +62,9 @@ struct SegSh {
   long long t0, t1;    // token rows [t0, t1) of the unit handled by this piece
   long long p_row;     // append row (write_pos[b]) when appending
   long long res_off;   // element offset of the unit's residual rows
-  int u, b, h;         // unit, batch, KV head
+  int u, b, h;         // unit, batch, virtual KV head (head_map: GQA groups > 4)
+  int hc, hq0, gp;     // KV head of the codes, first query head, query heads (<= 4)
+  int cu;              // cache unit b * Hc + hc (code rows)
   int k, P;            // piece index and number of pieces of the unit
   int rlen;            // residual rows of the unit
   int owner;           // this piece encodes the appended token
@@ -108,6 +110,9 @@ __device__ __forceinline__ void compute_seg(const AttnArgs& a, int vc, int u, Se
   o.t0 = beg + piece_tok(tau0, V, a.rcpV, e - beg, X);
   o.t1 = beg + piece_tok(tau1, V, a.rcpV, e - beg, X);
   o.u = u; o.b = b; o.h = h;
+  const HeadMap hm = head_map(a, h);
+  o.hc = hm.hc; o.hq0 = hm.hq0; o.gp = hm.gp;
+  o.cu = b * a.Hc + hm.hc;
   o.k = static_cast<int>(vc - c1);
   o.P = P;
   o.owner = 0; o.patch = 0; o.p_row = -1;
@@ -124,7 +129,7 @@ __device__ __forceinline__ void compute_seg(const AttnArgs& a, int vc, int u, Se
     rl = static_cast<int>(x < 0 ? 0 : (x > a.r_cap ? a.r_cap : x));
   }
   o.rlen = rl;
-  o.res_off = a.res ? b * a.res_sb + h * a.res_sh : 0;
+  o.res_off = a.res ? b * a.res_sb + hm.hc * a.res_sh : 0;
 }
 
 
@@ -147,7 +152,7 @@ __device__ __forceinline__ void store_state(float* dacc, float* dm, float* dl, i
 // Last-arriver merge (persistent grids): the P published pieces (slots slot0 .. slot0+P-1) of output
 // element (b, h, g, dim), combined in slot order by log-sum-exp (Alg. 1 l.729-730) and consumed
 // (zeroed) for the next launch.  Chunks of 8 loads in flight.
-__device__ __noinline__ void merge_consume(const AttnArgs& a, unsigned long long* part, int b, int h, int g, int dim,
+__device__ __noinline__ void merge_consume(const AttnArgs& a, unsigned long long* part, int b, int hq0, int g, int dim,
                                            int64_t slot0, int P) {
   unsigned long long* pp = part + (slot0 * 4 + g) * 128 + dim;
   float m = -INFINITY, wsum = 0.f, osum = 0.f;
@@ -181,10 +186,10 @@ __device__ __noinline__ void merge_consume(const AttnArgs& a, unsigned long long
   }
   const bool empty = !(wsum > 0.f);
   const float ov = empty ? 0.f : osum / wsum;
-  const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+  const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hq0 + g) * 128 + dim;
   if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
   else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-  if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
+  if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
 }
 
 template <int KB, int VB>
@@ -227,12 +232,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
 
       // ---- static inputs (codebooks, lambda) first: with programmatic dependent launch this
       // overlaps the tail of the previous kernel; everything dynamic is read after the wait
-      const int bA = div_small(ua, a.Hkv), hA = ua - bA * a.Hkv;
+      const int bA = div_small(ua, a.Hkv), hA = ua - bA * a.Hkv;   // virtual heads of the round's units
       const int hB = hA + 1 == a.Hkv ? 0 : hA + 1;
-      const uint16_t* cbkA = a.ck + hA * a.ck_hs;
-      const uint16_t* cbvA = a.cv + hA * a.cv_hs;
-      const uint16_t* cbkB = a.ck + hB * a.ck_hs;
-      const uint16_t* cbvB = a.cv + hB * a.cv_hs;
+      const HeadMap hmA = head_map(a, hA), hmB = head_map(a, hB);
+      const uint16_t* cbkA = a.ck + hmA.hc * a.ck_hs;
+      const uint16_t* cbvA = a.cv + hmA.hc * a.cv_hs;
+      const uint16_t* cbkB = a.ck + hmB.hc * a.ck_hs;
+      const uint16_t* cbvB = a.cv + hmB.hc * a.cv_hs;
       const bool sameB = nseg == 1 || (cbkB == cbkA && cbvB == cbvA);   // B reuses table A
       // warp 0 skips the fill: it goes straight to the (dynamic) segment computation below
       if constexpr (kTable) {
@@ -246,15 +252,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       const int qseg = (warp - 8) >> 2, qg = warp & 3;   // warps 8..11: heads of segment A, 12..15: of B
       const bool qwarp = warp >= 8 && warp < 8 + 4 * nseg;
       float4 lam4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (qwarp) lam4 = *reinterpret_cast<const float4*>(a.lambda + (qseg ? hB : hA) * 128 + 4 * lane);
+      if (qwarp) lam4 = *reinterpret_cast<const float4*>(a.lambda + (qseg ? hmB.hc : hmA.hc) * 128 + 4 * lane);
+      const int q_gp = qseg ? hmB.gp : hmA.gp;
       if (first) griddep_wait();
       first = false;
 
       // ---- dynamic inputs
       uint2 qw = make_uint2(0u, 0u);
-      if (qwarp && qg < a.G) {
-        const int bq = qseg && hB == 0 ? bA + 1 : bA, hq = qseg ? hB : hA;
-        qw = *reinterpret_cast<const uint2*>(a.q + bq * a.q_sb + (hq * a.G + qg) * a.q_sh + 4 * lane);
+      if (qwarp && qg < q_gp) {
+        const int bq = qseg && hB == 0 ? bA + 1 : bA, hq0 = qseg ? hmB.hq0 : hmA.hq0;
+        qw = *reinterpret_cast<const uint2*>(a.q + bq * a.q_sb + (hq0 + qg) * a.q_sh + 4 * lane);
       }
       // ---- segments and warp assignment: the round's 16-token sub-tiles (A's, then B's) go to
       // the warps in contiguous balanced ranges [w*ns/16, (w+1)*ns/16); segment A = warps
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         const int64_t tend = sg.t0 + 16 * static_cast<int64_t>(s1);
         ntok = static_cast<int>(max(int64_t(0), min(tend, static_cast<int64_t>(sg.t1)) - tok0));
         ntile = (ntok + 31) >> 5;
-        const int64_t unit = sg.u;
+        const int64_t unit = sg.cu;   // cache unit of the codes
         kp = a.kcodes + (unit * a.n_cap + tok0 + r) * KR + Fmt<KB>::kOffK * j;
         vp = a.vcodes + (unit * a.n_cap + tok0 + 2 * j) * VR + Fmt<VB>::kOffV * r;
         patch_tile = -1;
@@ -338,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       // ---- query transform (Eq. 7): sq[seg][g] = ((q_g * lambda) H) * qscale
       if (qwarp) {
         float* dq = sq + kQSeg * qseg + kQRow * qg + qoff(lane);
-        if (qg < a.G) qtransform_lane(qw, lam4, a.qscale, lane, dq);
+        if (qg < q_gp) qtransform_lane(qw, lam4, a.qscale, lane, dq);
         else *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
 
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
             if (!segs[sgi].owner) continue;
             if (synced) __syncthreads();   // the previous encode's staging is consumed
             const SegSh& sg = segs[sgi];
-            const int bb = sg.b, hh = sg.h;
+            const int bb = sg.b, hh = sg.hc;
             const bool isv = warp >= 8;
             const int w8 = warp & 7;
             const int P8 = (isv ? (1 << VB) : (1 << KB)) / 8;   // centroids per warp
@@ -398,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
               else put_code<VB>(nc + 64, lane, ii);
               const int64_t p = sg.p_row;
               if (p >= 0 && p < a.n_cap) {
-                const int64_t row = static_cast<int64_t>(sg.u) * a.n_cap + p;
+                const int64_t row = static_cast<int64_t>(sg.cu) * a.n_cap + p;
                 if (warp == 0) put_code<KB>(a.kcodes_w + row * KR, lane, ii);
                 else put_code<VB>(a.vcodes_w + row * VR, lane, ii);
               } else if (lane == 0 && a.err) {
@@ -460,12 +467,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         // 16r + 2t + {0, 1})
         if (t_res < rlen) {
           const SegSh& sgr = segs[seg];
-          const int bb = sgr.b, hh = sgr.h;
+          const int bb = sgr.b, hh = sgr.hc;
           float qr[4][4];
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
-            const float4 v = g < a.G ? bf16x4_to_float4(*reinterpret_cast<const uint2*>(
-                                           a.q + bb * a.q_sb + (hh * a.G + g) * a.q_sh + 4 * lane))
+            const float4 v = g < sgr.gp ? bf16x4_to_float4(*reinterpret_cast<const uint2*>(
+                                              a.q + bb * a.q_sb + (sgr.hq0 + g) * a.q_sh + 4 * lane))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
             qr[g][0] = v.x * a.qscale_raw; qr[g][1] = v.y * a.qscale_raw;
             qr[g][2] = v.z * a.qscale_raw; qr[g][3] = v.w * a.qscale_raw;
@@ -686,11 +693,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         const float L2 = empty ? -INFINITY : M + __log2f(lsum);
         const SegSh& sg = segs[sgi];
         if (sg.P == 1) {
-          if (g < a.G) {
-            const int64_t oi = (static_cast<int64_t>(sg.b) * a.Hq + sg.h * a.G + g) * 128 + dim;
+          if (g < sg.gp) {
+            const int64_t oi = (static_cast<int64_t>(sg.b) * a.Hq + sg.hq0 + g) * 128 + dim;
             if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
             else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-            if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(sg.b) * a.Hq + sg.h * a.G + g] = L2 * kLn2;
+            if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(sg.b) * a.Hq + sg.hq0 + g] = L2 * kLn2;
           }
         } else {
           const int64_t pi = ((static_cast<int64_t>(vc) + sg.u) * 4 + g) * 128 + dim;
@@ -721,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           const SegSh& sg = segs[sgi];
           const int64_t c1 = div_fix(static_cast<int64_t>(sg.u) * a.V, a.U, a.rcpU);
           const int g = tid >> 7, dim = tid & 127;
-          if (g < a.G) merge_consume(a, part, sg.b, sg.h, g, dim, c1 + sg.u, sg.P);
+          if (g < sg.gp) merge_consume(a, part, sg.b, sg.hq0, g, dim, c1 + sg.u, sg.P);
         }
       }
       if (ua + 2 > u_last) phase_mark(a.phase, vc, 3);
@@ -753,7 +760,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         const int oo = ee / P, p = ee - oo * P;
         const int o = k * per[i] + oo;   // g * 128 + dim
         float2 v = make_float2(0.f, -INFINITY);
-        if ((o >> 7) < a.G) {
+        const int bu = div_small(u, a.Hkv);
+        if ((o >> 7) < head_map(a, u - bu * a.Hkv).gp) {
           const int64_t c1 = div_fix(static_cast<int64_t>(u) * a.V, a.U, a.rcpU);
           unsigned long long* pp = part + (c1 + u + p) * 512 + o;
           unsigned long long w;
@@ -772,7 +780,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         const int* rec = sflag + 4 + 4 * i;
         const int u = rec[0], k = rec[1], P = rec[2];
         const int o = k * per[i] + tt, g = o >> 7, dim = o & 127;
-        if (g >= a.G) continue;
+        const int b = div_small(u, a.Hkv);
+        const HeadMap hmu = head_map(a, u - b * a.Hkv);
+        if (g >= hmu.gp) continue;
         const float2* sv = stage + (i ? E[0] : 0) + tt * P;
         float M = -INFINITY;
         for (int p = 0; p < P; ++p) M = fmaxf(M, sv[p].y);
@@ -785,12 +795,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           }
         }
         const bool empty = !(wsum > 0.f);
-        const int b = div_small(u, a.Hkv), h = u - b * a.Hkv;
-        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + h * a.G + g) * 128 + dim;
+        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hmu.hq0 + g) * 128 + dim;
         const float ov = empty ? 0.f : osum * __frcp_rn(wsum);
         if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
         else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-        if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + h * a.G + g] = empty ? -INFINITY : (M + __log2f(wsum)) * kLn2;
+        if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hmu.hq0 + g] = empty ? -INFINITY : (M + __log2f(wsum)) * kLn2;
       }
     }
   }

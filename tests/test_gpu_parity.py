@@ -223,11 +223,34 @@ def test_attn_fixed_splits_and_determinism(splits):
     _assert_close(o1, L1, *_run_ref(c))
 
 
-@pytest.mark.parametrize("G", [1, 2, 4])
-def test_attn_gqa_groups(G):
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 5, 6, 7, 8])   # > 4: two virtual KV heads per KV head
+@pytest.mark.parametrize("splits", [0, 3])
+def test_attn_gqa_groups(G, splits):
     c = _attn_case(2, 3, G, 700, [700, 450], seed=10 + G)
-    o, L = _run_gpu(c)
+    o, L = _run_gpu(c, num_splits=splits)
     _assert_close(o, L, *_run_ref(c))
+
+
+@pytest.mark.parametrize("G", [5, 8])
+def test_decode_step_fused_gqa_over_4(G):
+    """Qwen2.5-14B-like group (40 q / 8 kv = 5) and G = 8: both virtual heads of a KV head run the
+    owner encode and write identical codes; codes bit-exact, output vs the oracle."""
+    lens = [900, 333]
+    B = len(lens)
+    c = _attn_case(B, 8, G, max(lens) + 2, lens, seed=30 + G)
+    kn = synth.gen_keys(1, 8, 128, seed=31, batch=B)[:, 0]
+    vn = synth.gen_values(1, 8, 128, seed=32, batch=B)[:, 0]
+    wp = [n - 1 for n in lens]
+    kcodes, vcodes = t_u8(c["kc"]), t_u8(c["vc"])
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(c["ck"]), t_bf16(c["cv"]), kcodes, vcodes, t_i32(wp), t_i32(lens))
+    for b in range(B):
+        for h in range(8):
+            kk, vv = ref.encode_kv(kn[b, h], vn[b, h], CB["inv_lambda"][h], c["ck"][h], c["cv"][h])
+            c["kc"][b, h, wp[b]], c["vc"][b, h, wp[b]] = kk, vv
+    assert np.array_equal(kcodes.cpu().numpy(), c["kc"].astype(np.uint8))
+    assert np.array_equal(vcodes.cpu().numpy(), c["vc"].astype(np.uint8))
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))
 
 
 @pytest.mark.parametrize("rng_", [(0, 500), (500, -1), (100, 101), (1000, 3000), (250, 250)])

@@ -62,6 +62,14 @@ def test_stream_auto_many_units():
     _assert_close(o, L, *_run_ref(c))
 
 
+def test_stream_gqa_groups_over_4():
+    """G = 5 / 8 through the stream kernel (two virtual heads per KV head share one table)."""
+    for G in (5, 8):
+        c = _attn_case(3, 8, G, 1500, [1500, 77, 900], seed=345 + G)
+        o, L = _run_gpu(c, algo="stream")
+        _assert_close(o, L, *_run_ref(c))
+
+
 @pytest.mark.parametrize("rng_", [(0, 500), (500, -1), (100, 101), (250, 250)])
 def test_stream_token_ranges(rng_):
     a, e = rng_
