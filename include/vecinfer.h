@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define VECINFER_ABI_VERSION 3
+#define VECINFER_ABI_VERSION 4
 
 typedef struct CUstream_st* vecinfer_stream_t; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -75,6 +75,21 @@ typedef enum {
   VECINFER_ATTN_LUT = 2,
   VECINFER_ATTN_DEQUANT_MMA_STREAM = 3
 } vecinfer_attn_algo_t;
+
+/* Paged code cache (serving integration): k_codes / v_codes are a pool of
+ * n_pages pages laid out [n_pages, H_kv, page_size, row_bytes]; token t of batch row b lives in
+ * page block_table[b * bt_stride + t / page_size] at row t % page_size.  page_size is a power of
+ * two >= 32; n_cap (the per-sequence capacity) must not exceed bt_stride * page_size.  Entries
+ * outside [0, n_pages) are flagged as VECINFER_FLAG_WRITE_POS by the encoders and must not be
+ * reached by attended tokens.  Token ranges must start at a multiple of 32.  The *_paged entry
+ * points run the split attention kernel (the stream kernel and the LUT variant are contiguous-only).
+ *   block_table  device int32 [B, bt_stride] (caller owned).                                   */
+typedef struct {
+  const int32_t* block_table;
+  int64_t bt_stride;
+  int32_t page_size;
+  int32_t n_pages;
+} vecinfer_paged_t;
 
 /* Full-precision residual window ("the residual length for all methods is set to 128";
  * SURVEY §8(f) NEXT-1): the newest tokens of each sequence kept as raw bf16 k, v rows next to the
@@ -161,6 +176,17 @@ vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int
                                      uint8_t* v_codes, int64_t n_cap, const int32_t* write_pos,
                                      uint32_t* err_flags, void* workspace, size_t workspace_bytes,
                                      vecinfer_stream_t stream);
+/* vecinfer_encode_kv into a paged code cache (vecinfer_paged_t; same arguments otherwise). */
+vecinfer_status_t vecinfer_encode_kv_paged(const void* k_bf16, const void* v_bf16, int32_t B,
+                                           int32_t T, int32_t H_kv, const int64_t k_strides[3],
+                                           const int64_t v_strides[3], const float* inv_lambda,
+                                           const void* ck_bf16, const void* cv_bf16,
+                                           int64_t ck_head_stride, int64_t cv_head_stride,
+                                           vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes,
+                                           uint8_t* v_codes, int64_t n_cap, const int32_t* write_pos,
+                                           uint32_t* err_flags, void* workspace,
+                                           size_t workspace_bytes, vecinfer_stream_t stream,
+                                           const vecinfer_paged_t* paged);
 
 /* ---------------------------------------------------------------------------------------
  * Fused decode attention over the VQ cache, Eq. 10 + Algorithm 1,
@@ -214,6 +240,21 @@ vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_
                                        vecinfer_dtype_t o_dtype, float* lse, void* workspace,
                                        size_t workspace_bytes, vecinfer_stream_t stream,
                                        const vecinfer_residual_t* residual);
+/* vecinfer_attn_decode over a paged code cache (split kernel; tok_begin % 32 == 0). */
+vecinfer_status_t vecinfer_attn_decode_paged(const void* q_bf16, int32_t B, int32_t H_q,
+                                             int32_t H_kv, int64_t q_stride_b, int64_t q_stride_h,
+                                             const float* lambda, const void* ck_bf16,
+                                             const void* cv_bf16, int64_t ck_head_stride,
+                                             int64_t cv_head_stride, vecinfer_vq_t kcfg,
+                                             vecinfer_vq_t vcfg, const uint8_t* k_codes,
+                                             const uint8_t* v_codes, int64_t n_cap,
+                                             const int32_t* seq_lens, int64_t tok_begin,
+                                             int64_t tok_end, float softmax_scale,
+                                             int32_t num_splits, vecinfer_attn_algo_t algo, void* o,
+                                             vecinfer_dtype_t o_dtype, float* lse, void* workspace,
+                                             size_t workspace_bytes, vecinfer_stream_t stream,
+                                             const vecinfer_residual_t* residual,
+                                             const vecinfer_paged_t* paged);
 
 /* ---------------------------------------------------------------------------------------
  * Fused decode step for one layer: EXACTLY vecinfer_encode_kv(T = 1) of the new token followed
@@ -249,6 +290,18 @@ vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf1
                                        float* lse, uint32_t* err_flags, void* workspace,
                                        size_t workspace_bytes, vecinfer_stream_t stream,
                                        const vecinfer_residual_t* residual);
+/* vecinfer_decode_step over a paged code cache (append row write_pos[b] translated through the
+ * block table; split kernel). */
+vecinfer_status_t vecinfer_decode_step_paged(
+    const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16, int32_t B, int32_t H_q,
+    int32_t H_kv, const int64_t q_strides[2], const int64_t k_new_strides[2],
+    const int64_t v_new_strides[2], const float* lambda, const float* inv_lambda,
+    const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride, int64_t cv_head_stride,
+    vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes, uint8_t* v_codes, int64_t n_cap,
+    const int32_t* write_pos, const int32_t* seq_lens, float softmax_scale, int32_t num_splits,
+    vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype, float* lse, uint32_t* err_flags,
+    void* workspace, size_t workspace_bytes, vecinfer_stream_t stream,
+    const vecinfer_residual_t* residual, const vecinfer_paged_t* paged);
 
 /* ---------------------------------------------------------------------------------------
  * Log-sum-exp merge of P normalised partials (cross-GPU sequence shards, residual window):

@@ -23,6 +23,12 @@ class Residual(ctypes.Structure):
                 ("append_new", ctypes.c_int32)]
 
 
+class Paged(ctypes.Structure):
+    """vecinfer_paged_t: paged code cache [n_pages, H_kv, page_size, row] + block table."""
+    _fields_ = [("block_table", ctypes.c_void_p), ("bt_stride", ctypes.c_int64), ("page_size", ctypes.c_int32),
+                ("n_pages", ctypes.c_int32)]
+
+
 class VQ(ctypes.Structure):
     """vecinfer_vq_t {head_dim, sub_dim, code_bits}."""
     _fields_ = [("head_dim", c_i32), ("sub_dim", c_i32), ("code_bits", c_i32)]
@@ -43,6 +49,9 @@ PROTOTYPES = {
     "vecinfer_encode_kv": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, I64x3, I64x3, c_void_p, c_void_p,
                                    c_void_p, c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p, c_void_p,
                                    c_void_p, c_sz, c_void_p]),
+    "vecinfer_encode_kv_paged": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, I64x3, I64x3, c_void_p, c_void_p,
+                                         c_void_p, c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p,
+                                         c_void_p, c_void_p, c_sz, c_void_p, ctypes.POINTER(Paged)]),
     "vecinfer_attn_num_splits": (c_i32, [c_i32, c_i32, c_i64, c_i32]),
     "vecinfer_attn_num_ctas": (c_i32, [c_i32, c_i32, c_i64, c_i32]),
     "vecinfer_attn_kernel_kind": (c_i32, [c_i32, c_i32, c_i32, c_i32]),
@@ -50,11 +59,21 @@ PROTOTYPES = {
     "vecinfer_attn_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i32]),
     "vecinfer_attn_decode": (c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i64, c_i64, c_void_p, c_void_p, c_void_p,
                                      c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_i64, c_f32,
-                                     c_i32, c_i32, c_void_p, c_i32, c_void_p, c_void_p, c_sz, c_void_p]),
+                                     c_i32, c_i32, c_void_p, c_i32, c_void_p, c_void_p, c_sz, c_void_p,
+                                     ctypes.POINTER(Residual)]),
+    "vecinfer_attn_decode_paged": (c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i64, c_i64, c_void_p, c_void_p,
+                                           c_void_p, c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p,
+                                           c_i64, c_i64, c_f32, c_i32, c_i32, c_void_p, c_i32, c_void_p, c_void_p,
+                                           c_sz, c_void_p, ctypes.POINTER(Residual), ctypes.POINTER(Paged)]),
     "vecinfer_decode_step": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, I64x2, I64x2, I64x2,
                                      c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, VQ, VQ, c_void_p,
                                      c_void_p, c_i64, c_void_p, c_void_p, c_f32, c_i32, c_i32, c_void_p, c_i32,
                                      c_void_p, c_void_p, c_void_p, c_sz, c_void_p, ctypes.POINTER(Residual)]),
+    "vecinfer_decode_step_paged": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, I64x2, I64x2, I64x2,
+                                           c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, VQ, VQ, c_void_p,
+                                           c_void_p, c_i64, c_void_p, c_void_p, c_f32, c_i32, c_i32, c_void_p,
+                                           c_i32, c_void_p, c_void_p, c_void_p, c_sz, c_void_p,
+                                           ctypes.POINTER(Residual), ctypes.POINTER(Paged)]),
     "vecinfer_debug_attn_max_clusters": (c_i32, [c_i32]),
     "vecinfer_decode_step_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i64, VQ, VQ, c_i32]),
     "vecinfer_merge_lse": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_void_p, c_i32, c_void_p,

@@ -24,6 +24,17 @@ vecinfer_status_t fail(vecinfer_status_t st, const char* fmt, ...) {
   return st;
 }
 
+vecinfer_status_t check_paged(const vecinfer_paged_t* pg, int64_t n_cap, const char* who) {
+  if (!pg->block_table) return fail(VECINFER_ERR_INVALID_ARG, "%s: paged cache without block_table", who);
+  const int ps = pg->page_size;
+  if (ps < 32 || (ps & (ps - 1)) != 0)
+    return fail(VECINFER_ERR_INVALID_ARG, "%s: page_size %d must be a power of two >= 32", who, ps);
+  if (pg->n_pages <= 0) return fail(VECINFER_ERR_SHAPE, "%s: n_pages must be > 0", who);
+  if (pg->bt_stride <= 0 || pg->bt_stride * static_cast<int64_t>(ps) < n_cap)
+    return fail(VECINFER_ERR_SHAPE, "%s: bt_stride * page_size must cover n_cap", who);
+  return VECINFER_OK;
+}
+
 vecinfer_status_t check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(VECINFER_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));

@@ -172,7 +172,8 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
                                    float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
                                    void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
                                    size_t workspace_bytes, vecinfer_stream_t stream, const AppendArgs* app,
-                                   const vecinfer_residual_t* res, bool res_append) {
+                                   const vecinfer_residual_t* res, bool res_append,
+                                   const vecinfer_paged_t* pg = nullptr) {
   if (!q_bf16 || !lambda || !ck_bf16 || !cv_bf16 || !k_codes || !v_codes || !seq_lens || !o)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: NULL pointer");
   if (o_dtype != VECINFER_BF16 && o_dtype != VECINFER_F32) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad o_dtype");
@@ -204,7 +205,14 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: misaligned lambda/codebooks/codes");
   const int64_t range = tok_end >= 0 ? (tok_end - tok_begin < n_cap ? tok_end - tok_begin : n_cap) : n_cap;
   const bool lut = algo == VECINFER_ATTN_LUT;
-  const bool use_sk = use_stream(B, H_kv, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
+  if (pg) {   // paged code cache: split kernel only, 32-aligned token ranges
+    const vecinfer_status_t v = check_paged(pg, n_cap, "attn_decode_paged");
+    if (v != VECINFER_OK) return v;
+    if (lut || algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
+      return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_paged: paged caches run the split DEQUANT_MMA kernel only");
+    if (tok_begin % 32 != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode_paged: tok_begin must be a multiple of 32");
+  }
+  const bool use_sk = !pg && use_stream(B, H_kv, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
   const SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
   const int32_t S = plan.S;
   const WsLayout wl = ws_layout(B, H_kv, plan_splits(B, H_kv, range, num_splits).S, true);
@@ -236,6 +244,10 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.cv = static_cast<const uint16_t*>(cv_bf16);
   a.ck_hs = ck_head_stride; a.cv_hs = cv_head_stride;
   a.kcodes = k_codes; a.vcodes = v_codes; a.n_cap = n_cap;
+  a.bt = pg ? pg->block_table : nullptr;
+  a.bt_stride = pg ? pg->bt_stride : 0;
+  a.page_shift = pg ? __builtin_ctz(static_cast<unsigned>(pg->page_size)) : 0;
+  a.n_pages = pg ? pg->n_pages : 0;
   a.seq_lens = seq_lens; a.tok_begin = tok_begin; a.tok_end = tok_end;
   a.qscale = static_cast<float>((1.0 / sqrt(128.0)) * static_cast<double>(softmax_scale) * 1.4426950408889634);
   a.S = S;
@@ -314,18 +326,34 @@ extern "C" vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B,
                    num_splits, algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false);
 }
 
+extern "C" vecinfer_status_t vecinfer_attn_decode_paged(const void* q_bf16, int32_t B, int32_t H_q, int32_t H_kv,
+                                                  int64_t q_stride_b, int64_t q_stride_h, const float* lambda,
+                                                  const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride,
+                                                  int64_t cv_head_stride, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
+                                                  const uint8_t* k_codes, const uint8_t* v_codes, int64_t n_cap,
+                                                  const int32_t* seq_lens, int64_t tok_begin, int64_t tok_end,
+                                                  float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
+                                                  void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
+                                                  size_t workspace_bytes, vecinfer_stream_t stream,
+                                                  const vecinfer_residual_t* residual, const vecinfer_paged_t* paged) {
+  if (!paged) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode_paged: NULL paged descriptor");
+  return attn_impl(q_bf16, B, H_q, H_kv, q_stride_b, q_stride_h, lambda, ck_bf16, cv_bf16, ck_head_stride,
+                   cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, tok_begin, tok_end, softmax_scale,
+                   num_splits, algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false, paged);
+}
+
 // Whether vecinfer_decode_step runs the append-encode inside the attention launch.  Split kernel:
 // only single-wave grids (the owner CTA's encode then hides behind the other CTAs' longer splits;
 // with several waves every wave would carry it, and one separate append launch is cheaper).
 // Stream kernel: always when every CTA is resident (the partition budgets the encode).  Never for
 // 16-bit codebooks or the LUT variant.
 static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
-                         int32_t num_splits, vecinfer_attn_algo_t algo) {
+                         int32_t num_splits, vecinfer_attn_algo_t algo, bool paged = false) {
   if (algo == VECINFER_ATTN_LUT || kcfg.code_bits > 8 || vcfg.code_bits > 8 || B <= 0 || H_kv <= 0) return false;
   const int64_t units = static_cast<int64_t>(B) * H_kv;
   if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
     return num_splits == 0 || units * num_splits <= device_sm_count();   // persistent grids: separate append
-  if (use_stream(B, H_kv, num_splits, false)) return true;
+  if (!paged && use_stream(B, H_kv, num_splits, false)) return true;
   const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
   const int mac = plan.cluster ? attn_mma_max_active_clusters(plan.S) : 0;
   const int64_t waves = plan.cluster ? (units + (mac > 0 ? mac : 1) - 1) / (mac > 0 ? mac : 1)
@@ -354,7 +382,7 @@ extern "C" size_t vecinfer_decode_step_workspace_bytes(int32_t B, int32_t H_q, i
   return a + vecinfer_encode_workspace_bytes(B, 1, H_kv, kcfg, vcfg);
 }
 
-extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,
+static vecinfer_status_t decode_step_impl(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,
                                                   int32_t B, int32_t H_q, int32_t H_kv, const int64_t q_strides[2],
                                                   const int64_t k_new_strides[2], const int64_t v_new_strides[2],
                                                   const float* lambda, const float* inv_lambda, const void* ck_bf16,
@@ -365,7 +393,7 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
                                                   vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype,
                                                   float* lse, uint32_t* err_flags, void* workspace,
                                                   size_t workspace_bytes, vecinfer_stream_t stream,
-                                                  const vecinfer_residual_t* residual) {
+                                                  const vecinfer_residual_t* residual, const vecinfer_paged_t* pg) {
   if (!k_new_bf16 || !v_new_bf16 || !inv_lambda || !write_pos || !q_strides || !k_new_strides || !v_new_strides)
     return fail(VECINFER_ERR_INVALID_ARG, "decode_step: NULL pointer");
   for (int i = 0; i < 2; ++i)
@@ -379,9 +407,9 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
                    inv_lambda, write_pos, err_flags};
     return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
-                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, true);
+                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, true, pg);
   }
-  const bool fuse = decode_fuses(B, H_kv * hsplit_of(H_q, H_kv), n_cap, kcfg, vcfg, num_splits, algo);
+  const bool fuse = decode_fuses(B, H_kv * hsplit_of(H_q, H_kv), n_cap, kcfg, vcfg, num_splits, algo, pg != nullptr);
   if (!fuse) {   // separate append + attention launches (always for the paper-faithful LUT variant)
     const int64_t ks[3] = {k_new_strides[0], 0, k_new_strides[1]};
     const int64_t vs[3] = {v_new_strides[0], 0, v_new_strides[1]};
@@ -391,17 +419,55 @@ extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void
     if (ew && (!workspace || workspace_bytes < aw + ew))
       return fail(VECINFER_ERR_WORKSPACE, "decode_step: workspace needs %zu bytes", aw + ew);
     void* ews = ew ? static_cast<void*>(static_cast<unsigned char*>(workspace) + aw) : nullptr;
-    vecinfer_status_t st = vecinfer_encode_kv(k_new_bf16, v_new_bf16, B, 1, H_kv, ks, vs, inv_lambda, ck_bf16, cv_bf16,
-                                              ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap,
-                                              write_pos, err_flags, ews, ew, stream);
+    vecinfer_status_t st =
+        pg ? vecinfer_encode_kv_paged(k_new_bf16, v_new_bf16, B, 1, H_kv, ks, vs, inv_lambda, ck_bf16, cv_bf16,
+                                      ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, write_pos,
+                                      err_flags, ews, ew, stream, pg)
+           : vecinfer_encode_kv(k_new_bf16, v_new_bf16, B, 1, H_kv, ks, vs, inv_lambda, ck_bf16, cv_bf16,
+                                ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, write_pos,
+                                err_flags, ews, ew, stream);
     if (st != VECINFER_OK) return st;
     return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
-                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false);
+                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false, pg);
   }
   AppendArgs app{k_new_bf16, v_new_bf16, k_new_strides[0], k_new_strides[1], v_new_strides[0], v_new_strides[1],
                  inv_lambda, write_pos, err_flags};
   return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                    cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
-                   algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, false);
+                   algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, false, pg);
+}
+
+extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,
+                                                  int32_t B, int32_t H_q, int32_t H_kv, const int64_t q_strides[2],
+                                                  const int64_t k_new_strides[2], const int64_t v_new_strides[2],
+                                                  const float* lambda, const float* inv_lambda, const void* ck_bf16,
+                                                  const void* cv_bf16, int64_t ck_head_stride, int64_t cv_head_stride,
+                                                  vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes,
+                                                  uint8_t* v_codes, int64_t n_cap, const int32_t* write_pos,
+                                                  const int32_t* seq_lens, float softmax_scale, int32_t num_splits,
+                                                  vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype,
+                                                  float* lse, uint32_t* err_flags, void* workspace,
+                                                  size_t workspace_bytes, vecinfer_stream_t stream,
+                                                  const vecinfer_residual_t* residual) {
+  return decode_step_impl(q_bf16, k_new_bf16, v_new_bf16, B, H_q, H_kv, q_strides, k_new_strides, v_new_strides,
+                          lambda, inv_lambda, ck_bf16, cv_bf16, ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes,
+                          v_codes, n_cap, write_pos, seq_lens, softmax_scale, num_splits, algo, o, o_dtype, lse,
+                          err_flags, workspace, workspace_bytes, stream, residual, nullptr);
+}
+
+extern "C" vecinfer_status_t vecinfer_decode_step_paged(
+    const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16, int32_t B, int32_t H_q, int32_t H_kv,
+    const int64_t q_strides[2], const int64_t k_new_strides[2], const int64_t v_new_strides[2], const float* lambda,
+    const float* inv_lambda, const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride, int64_t cv_head_stride,
+    vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes, uint8_t* v_codes, int64_t n_cap,
+    const int32_t* write_pos, const int32_t* seq_lens, float softmax_scale, int32_t num_splits,
+    vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype, float* lse, uint32_t* err_flags, void* workspace,
+    size_t workspace_bytes, vecinfer_stream_t stream, const vecinfer_residual_t* residual,
+    const vecinfer_paged_t* paged) {
+  if (!paged) return fail(VECINFER_ERR_INVALID_ARG, "decode_step_paged: NULL paged descriptor");
+  return decode_step_impl(q_bf16, k_new_bf16, v_new_bf16, B, H_q, H_kv, q_strides, k_new_strides, v_new_strides,
+                          lambda, inv_lambda, ck_bf16, cv_bf16, ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes,
+                          v_codes, n_cap, write_pos, seq_lens, softmax_scale, num_splits, algo, o, o_dtype, lse,
+                          err_flags, workspace, workspace_bytes, stream, residual, paged);
 }

@@ -16,6 +16,9 @@ struct AttnArgs {
   const uint8_t* kcodes;  // [B, Hkv, n_cap, row]
   const uint8_t* vcodes;
   int64_t n_cap;
+  const int32_t* bt;           // paged code cache (split kernel): block table, NULL = contiguous
+  int64_t bt_stride;
+  int page_shift, n_pages;
   const int32_t* seq_lens;
   int64_t tok_begin, tok_end;  // tok_end < 0: to seq_len
   float qscale;                // (1/sqrt(D)) * softmax_scale * log2(e): folded into q~

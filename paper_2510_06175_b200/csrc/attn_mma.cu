@@ -109,9 +109,27 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       patch_row = static_cast<int>((p_row - r0) & 31);
     }
   }
-  // lane-resolved code pointers of this warp's first tile
-  const uint8_t* kp = a.kcodes + (unit * a.n_cap + r0 + 32 * warp + r) * KR + Fmt<KB>::kOffK * j;
-  const uint8_t* vp = a.vcodes + (unit * a.n_cap + r0 + 32 * warp + 2 * j) * VR + Fmt<VB>::kOffV * r;
+  // lane-resolved code pointers of this warp's first tile.  Paged caches: tiles are 32-aligned
+  // (tok_begin % 32 == 0, chunks of 32) so a tile never crosses a page; the page of the tile after
+  // next is read one tile ahead so its latency hides behind the current tile.
+  const bool paged = a.bt != nullptr;
+  const uint8_t* kcb = a.kcodes + static_cast<int64_t>(r) * KR + Fmt<KB>::kOffK * j;
+  const uint8_t* vcb = a.vcodes + static_cast<int64_t>(2 * j) * VR + Fmt<VB>::kOffV * r;
+  const int64_t pmask = (int64_t(1) << a.page_shift) - 1;
+  auto page_of = [&](int64_t tok) -> int { return a.bt[b * a.bt_stride + (tok >> a.page_shift)]; };
+  auto row_in = [&](int pg, int64_t tok) -> int64_t {   // cache row of token tok given its page
+    return paged ? ((static_cast<int64_t>(pg) * a.Hc + hc) << a.page_shift) + (tok & pmask) : unit * a.n_cap + tok;
+  };
+  int pg_ahead = 0;
+  const uint8_t* kp;
+  const uint8_t* vp;
+  {
+    const int64_t tok = r0 + 32 * warp;
+    const int64_t rw = row_in(paged && warp < ntile ? page_of(tok) : 0, tok);
+    kp = kcb + rw * KR;
+    vp = vcb + rw * VR;
+    if (paged && warp + kNW < ntile) pg_ahead = page_of(tok + 32 * kNW);
+  }
   constexpr int kStepK = 32 * kNW * KR, kStepV = 32 * kNW * VR;  // bytes between a warp's tiles
 
   // first tile's loads go out before the query transform so HBM latency overlaps it
@@ -194,9 +212,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       }
       if (warp == 0) put_code<(KB <= 8 ? KB : 8)>(newcodes, lane, ii);
       else put_code<(VB <= 8 ? VB : 8)>(newcodes + 64, lane, ii);
-      if (p_row >= 0 && p_row < a.n_cap) {
-        if (warp == 0) put_code<(KB <= 8 ? KB : 8)>(a.kcodes_w + (unit * a.n_cap + p_row) * KR, lane, ii);
-        else put_code<(VB <= 8 ? VB : 8)>(a.vcodes_w + (unit * a.n_cap + p_row) * VR, lane, ii);
+      int pgw = 0;
+      const bool pok = p_row >= 0 && p_row < a.n_cap && (!paged || ((pgw = page_of(p_row)) >= 0 && pgw < a.n_pages));
+      if (pok) {
+        const int64_t rw = row_in(pgw, p_row);
+        if (warp == 0) put_code<(KB <= 8 ? KB : 8)>(a.kcodes_w + rw * KR, lane, ii);
+        else put_code<(VB <= 8 ? VB : 8)>(a.vcodes_w + rw * VR, lane, ii);
       } else if (lane == 0 && a.err) {
         atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
       }
@@ -316,8 +337,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
     const int rem_cur = ntok - 32 * it;
     if (it + kNW < ntile) {
-      kp += kStepK;
-      vp += kStepV;
+      if (paged) {
+        const int64_t tok = r0 + 32 * static_cast<int64_t>(it + kNW);
+        const int64_t rw = row_in(pg_ahead, tok);
+        kp = kcb + rw * KR;
+        vp = vcb + rw * VR;
+        if (it + 2 * kNW < ntile) pg_ahead = page_of(tok + 32 * kNW);
+      } else {
+        kp += kStepK;
+        vp += kStepV;
+      }
       const int rem = rem_cur - 32 * kNW;
       if (rem >= 32) load_tile_full(nxt, kp, vp);
       else load_tile_tail(nxt, kp, vp, rem, r, j);

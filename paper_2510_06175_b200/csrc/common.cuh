@@ -41,6 +41,9 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+// validation of a paged-cache descriptor (include/vecinfer.h, vecinfer_paged_t)
+vecinfer_status_t check_paged(const vecinfer_paged_t* pg, int64_t n_cap, const char* who);
+
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t b) {
   return __uint_as_float(static_cast<uint32_t>(b) << 16);

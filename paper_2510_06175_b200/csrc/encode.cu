@@ -33,6 +33,9 @@ struct EncArgs {
   uint8_t* kcodes;
   uint8_t* vcodes;
   int64_t n_cap;
+  const int32_t* bt;          // paged cache: block table (NULL: contiguous [B, H, n_cap, row])
+  int64_t bt_stride;
+  int page_shift, n_pages;
   const int32_t* write_pos;
   uint32_t* err;
   float inv_sqrt_d;
@@ -74,6 +77,15 @@ __device__ __forceinline__ bool cache_row(const EncArgs& a, int b, int t, int h,
   if (pos < 0 || pos >= a.n_cap) {
     if (lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
     return false;
+  }
+  if (a.bt) {   // paged: [n_pages, H, page_size, row]
+    const int pg = a.bt[b * a.bt_stride + (pos >> a.page_shift)];
+    if (pg < 0 || pg >= a.n_pages) {
+      if (lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
+      return false;
+    }
+    row = ((static_cast<int64_t>(pg) * a.H + h) << a.page_shift) + (pos & ((int64_t(1) << a.page_shift) - 1));
+    return true;
   }
   row = (static_cast<int64_t>(b) * a.H + h) * a.n_cap + pos;
   return true;
@@ -297,13 +309,13 @@ extern "C" size_t vecinfer_encode_workspace_bytes(int32_t B, int32_t T, int32_t 
   return static_cast<size_t>(B) * T * H_kv * 2 * 32 * sizeof(unsigned long long);
 }
 
-extern "C" vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int32_t B, int32_t T,
-                                                int32_t H_kv, const int64_t k_strides[3], const int64_t v_strides[3],
-                                                const float* inv_lambda, const void* ck_bf16, const void* cv_bf16,
-                                                int64_t ck_head_stride, int64_t cv_head_stride, vecinfer_vq_t kcfg,
-                                                vecinfer_vq_t vcfg, uint8_t* k_codes, uint8_t* v_codes, int64_t n_cap,
-                                                const int32_t* write_pos, uint32_t* err_flags, void* workspace,
-                                                size_t workspace_bytes, vecinfer_stream_t stream) {
+static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int32_t B, int32_t T,
+                                     int32_t H_kv, const int64_t k_strides[3], const int64_t v_strides[3],
+                                     const float* inv_lambda, const void* ck_bf16, const void* cv_bf16,
+                                     int64_t ck_head_stride, int64_t cv_head_stride, vecinfer_vq_t kcfg,
+                                     vecinfer_vq_t vcfg, uint8_t* k_codes, uint8_t* v_codes, int64_t n_cap,
+                                     const int32_t* write_pos, uint32_t* err_flags, void* workspace,
+                                     size_t workspace_bytes, vecinfer_stream_t stream, const vecinfer_paged_t* pg) {
   if (!k_bf16 || !v_bf16 || !k_strides || !v_strides || !inv_lambda || !ck_bf16 || !cv_bf16 || !k_codes ||
       !v_codes || !write_pos)
     return fail(VECINFER_ERR_INVALID_ARG, "encode_kv: NULL pointer");
@@ -331,6 +343,13 @@ extern "C" vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* 
   a.kbits = kcfg.code_bits; a.vbits = vcfg.code_bits;
   a.kcodes = k_codes; a.vcodes = v_codes;
   a.n_cap = n_cap; a.write_pos = write_pos; a.err = err_flags;
+  a.bt = nullptr; a.bt_stride = 0; a.page_shift = 0; a.n_pages = 0;
+  if (pg) {
+    const vecinfer_status_t v = check_paged(pg, n_cap, "encode_kv");
+    if (v != VECINFER_OK) return v;
+    a.bt = pg->block_table; a.bt_stride = pg->bt_stride; a.n_pages = pg->n_pages;
+    a.page_shift = __builtin_ctz(static_cast<unsigned>(pg->page_size));
+  }
   a.inv_sqrt_d = static_cast<float>(1.0 / sqrt(static_cast<double>(kcfg.head_dim)));
   a.ws = static_cast<unsigned long long*>(workspace);
   cudaStream_t st = as_stream(stream);
@@ -371,4 +390,31 @@ extern "C" vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* 
   else e = launch_pdl(encode_small_kernel<4, 8>, grid, blk, 0, st, a);
   if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_small_kernel: %s", cudaGetErrorString(e)); }
   return check_launch("encode_small_kernel");
+}
+
+extern "C" vecinfer_status_t vecinfer_encode_kv(const void* k_bf16, const void* v_bf16, int32_t B, int32_t T,
+                                                int32_t H_kv, const int64_t k_strides[3], const int64_t v_strides[3],
+                                                const float* inv_lambda, const void* ck_bf16, const void* cv_bf16,
+                                                int64_t ck_head_stride, int64_t cv_head_stride, vecinfer_vq_t kcfg,
+                                                vecinfer_vq_t vcfg, uint8_t* k_codes, uint8_t* v_codes, int64_t n_cap,
+                                                const int32_t* write_pos, uint32_t* err_flags, void* workspace,
+                                                size_t workspace_bytes, vecinfer_stream_t stream) {
+  return encode_impl(k_bf16, v_bf16, B, T, H_kv, k_strides, v_strides, inv_lambda, ck_bf16, cv_bf16, ck_head_stride,
+                     cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, write_pos, err_flags, workspace,
+                     workspace_bytes, stream, nullptr);
+}
+
+extern "C" vecinfer_status_t vecinfer_encode_kv_paged(const void* k_bf16, const void* v_bf16, int32_t B, int32_t T,
+                                                      int32_t H_kv, const int64_t k_strides[3],
+                                                      const int64_t v_strides[3], const float* inv_lambda,
+                                                      const void* ck_bf16, const void* cv_bf16,
+                                                      int64_t ck_head_stride, int64_t cv_head_stride,
+                                                      vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes,
+                                                      uint8_t* v_codes, int64_t n_cap, const int32_t* write_pos,
+                                                      uint32_t* err_flags, void* workspace, size_t workspace_bytes,
+                                                      vecinfer_stream_t stream, const vecinfer_paged_t* paged) {
+  if (!paged) return fail(VECINFER_ERR_INVALID_ARG, "encode_kv_paged: NULL paged descriptor");
+  return encode_impl(k_bf16, v_bf16, B, T, H_kv, k_strides, v_strides, inv_lambda, ck_bf16, cv_bf16, ck_head_stride,
+                     cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, write_pos, err_flags, workspace,
+                     workspace_bytes, stream, paged);
 }

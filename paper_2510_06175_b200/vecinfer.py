@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import VQ, I64x2, I64x3, Residual, check
+from ._lib import VQ, I64x2, I64x3, Paged, Residual, check
 
 _lib.load()   # fail loudly at import if the native library is missing
 
@@ -67,6 +67,16 @@ def _cb_stride(cb: torch.Tensor) -> int:
     return 0 if cb.dim() == 2 else cb.stride(0)
 
 
+def _paged(block_table, codes):
+    """vecinfer_paged_t for a paged code pool codes [n_pages, H_kv, page_size, row] and an int32
+    block table [B, pages_per_seq]; returns (pointer, n_cap)."""
+    if block_table.dim() != 2 or block_table.stride(1) != 1:
+        raise ValueError("block_table must be [B, pages_per_seq] with contiguous rows")
+    n_pages, _, page_size, _ = codes.shape
+    pg = Paged(_need(block_table, "block_table", torch.int32).value, block_table.stride(0), page_size, n_pages)
+    return ctypes.pointer(pg), block_table.shape[1] * page_size
+
+
 def _residual(k_res, v_res, res_lens, append_new=False):
     """vecinfer_residual_t for bf16 [B, H_kv, r_cap, D] residual windows (None -> NULL)."""
     if k_res is None:
@@ -102,15 +112,23 @@ def encode_workspace(B: int, T: int, H_kv: int, kcfg: VQConfig = B2D4, vcfg: VQC
 def encode_kv(k: torch.Tensor, v: torch.Tensor, inv_lambda: torch.Tensor, ck: torch.Tensor, cv: torch.Tensor,
               k_codes: torch.Tensor, v_codes: torch.Tensor, write_pos: torch.Tensor, kcfg: VQConfig = B2D4,
               vcfg: VQConfig = B2D4, err_flags: torch.Tensor | None = None,
-              workspace: torch.Tensor | None = None) -> None:
+              workspace: torch.Tensor | None = None, block_table: torch.Tensor | None = None) -> None:
     """Encode k, v [B, T, H_kv, D] (bf16) into the packed code caches [B, H_kv, n_cap, row] (uint8)
-    at rows write_pos[b] + t (Eq. 8 prefill / Eq. 9 append)."""
+    at rows write_pos[b] + t (Eq. 8 prefill / Eq. 9 append).  With block_table [B, pages_per_seq]
+    (int32) the caches are page pools [n_pages, H_kv, page_size, row] (vecinfer_encode_kv_paged)."""
     B, T, H, D = k.shape
     if v.shape != k.shape:
         raise ValueError("k and v shapes differ")
-    n_cap = k_codes.shape[2]
-    if tuple(k_codes.shape) != (B, H, n_cap, kcfg.row_bytes) or tuple(v_codes.shape) != (B, H, n_cap, vcfg.row_bytes):
-        raise ValueError("code cache shape mismatch")
+    pg = None
+    if block_table is not None:
+        pg, n_cap = _paged(block_table, k_codes)
+        if k_codes.shape[1] != H or k_codes.shape[3] != kcfg.row_bytes or v_codes.shape != (
+                k_codes.shape[0], H, k_codes.shape[2], vcfg.row_bytes):
+            raise ValueError("paged code pool shape mismatch")
+    else:
+        n_cap = k_codes.shape[2]
+        if tuple(k_codes.shape) != (B, H, n_cap, kcfg.row_bytes) or tuple(v_codes.shape) != (B, H, n_cap, vcfg.row_bytes):
+            raise ValueError("code cache shape mismatch")
     if not (k_codes.is_contiguous() and v_codes.is_contiguous()):
         raise ValueError("code caches must be contiguous")
     lib = _lib.load()
@@ -119,14 +137,17 @@ def encode_kv(k: torch.Tensor, v: torch.Tensor, inv_lambda: torch.Tensor, ck: to
         workspace = torch.empty(nws, dtype=torch.uint8, device=k.device)
     wsp = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else ctypes.c_void_p(0)
     wsn = workspace.numel() if workspace is not None else 0
-    check("vecinfer_encode_kv", lib.vecinfer_encode_kv(
-        _need(k, "k", torch.bfloat16), _need(v, "v", torch.bfloat16), B, T, H,
-        I64x3(*k.stride()[:3]), I64x3(*v.stride()[:3]), _need(inv_lambda, "inv_lambda", torch.float32),
-        _need(ck, "ck", torch.bfloat16), _need(cv, "cv", torch.bfloat16), _cb_stride(ck), _cb_stride(cv),
-        kcfg.c(), vcfg.c(), _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
-        _need(write_pos, "write_pos", torch.int32),
-        ctypes.c_void_p(err_flags.data_ptr()) if err_flags is not None else ctypes.c_void_p(0),
-        wsp, wsn, _stream(k.device)))
+    args = (_need(k, "k", torch.bfloat16), _need(v, "v", torch.bfloat16), B, T, H,
+            I64x3(*k.stride()[:3]), I64x3(*v.stride()[:3]), _need(inv_lambda, "inv_lambda", torch.float32),
+            _need(ck, "ck", torch.bfloat16), _need(cv, "cv", torch.bfloat16), _cb_stride(ck), _cb_stride(cv),
+            kcfg.c(), vcfg.c(), _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
+            _need(write_pos, "write_pos", torch.int32),
+            ctypes.c_void_p(err_flags.data_ptr()) if err_flags is not None else ctypes.c_void_p(0),
+            wsp, wsn, _stream(k.device))
+    if pg is not None:
+        check("vecinfer_encode_kv_paged", lib.vecinfer_encode_kv_paged(*args, pg))
+    else:
+        check("vecinfer_encode_kv", lib.vecinfer_encode_kv(*args))
 
 
 def attn_num_splits(B: int, H_kv: int, n_tokens_max: int, num_splits: int = 0) -> int:
@@ -165,12 +186,17 @@ def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.
                 kcfg: VQConfig = B2D4, vcfg: VQConfig = B2D4, o_dtype: torch.dtype = torch.float32,
                 out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
                 workspace: torch.Tensor | None = None, k_res: torch.Tensor | None = None,
-                v_res: torch.Tensor | None = None, res_lens: torch.Tensor | None = None):
+                v_res: torch.Tensor | None = None, res_lens: torch.Tensor | None = None,
+                block_table: torch.Tensor | None = None):
     """Decode attention of q [B, H_q, D] (bf16) over the VQ cache (Eq. 10 / Alg. 1), plus an optional
     full-precision residual window k_res/v_res [B, H_kv, r_cap, D] with res_lens [B].
+    With block_table [B, pages_per_seq] the code caches are page pools [n_pages, H_kv, page_size, row].
     Returns (o [B, H_q, D] o_dtype, lse [B, H_q] fp32, natural log)."""
     B, Hq, D = q.shape
     Hkv, n_cap = k_codes.shape[1], k_codes.shape[2]
+    pg = None
+    if block_table is not None:
+        pg, n_cap = _paged(block_table, k_codes)
     if softmax_scale is None:
         softmax_scale = D ** -0.5
     rng = n_cap if tok_end < 0 else max(0, min(tok_end - tok_begin, n_cap))
@@ -185,13 +211,16 @@ def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.
     odt = F32 if out.dtype == torch.float32 else BF16
     if out.dtype not in (torch.float32, torch.bfloat16) or not out.is_contiguous():
         raise TypeError("out must be a contiguous float32 or bfloat16 tensor")
-    check("vecinfer_attn_decode", lib.vecinfer_attn_decode(
-        _need(q, "q", torch.bfloat16), B, Hq, Hkv, q.stride(0), q.stride(1), _need(lam, "lambda", torch.float32),
-        _need(ck, "ck", torch.bfloat16), _need(cv, "cv", torch.bfloat16), _cb_stride(ck), _cb_stride(cv),
-        kcfg.c(), vcfg.c(), _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
-        _need(seq_lens, "seq_lens", torch.int32), tok_begin, tok_end, softmax_scale, num_splits, ALGOS[algo],
-        _need(out, "out"), odt, _need(lse, "lse", torch.float32), ctypes.c_void_p(workspace.data_ptr()),
-        workspace.numel(), _stream(q.device), _residual(k_res, v_res, res_lens)))
+    args = (_need(q, "q", torch.bfloat16), B, Hq, Hkv, q.stride(0), q.stride(1), _need(lam, "lambda", torch.float32),
+            _need(ck, "ck", torch.bfloat16), _need(cv, "cv", torch.bfloat16), _cb_stride(ck), _cb_stride(cv),
+            kcfg.c(), vcfg.c(), _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
+            _need(seq_lens, "seq_lens", torch.int32), tok_begin, tok_end, softmax_scale, num_splits, ALGOS[algo],
+            _need(out, "out"), odt, _need(lse, "lse", torch.float32), ctypes.c_void_p(workspace.data_ptr()),
+            workspace.numel(), _stream(q.device), _residual(k_res, v_res, res_lens))
+    if pg is not None:
+        check("vecinfer_attn_decode_paged", lib.vecinfer_attn_decode_paged(*args, pg))
+    else:
+        check("vecinfer_attn_decode", lib.vecinfer_attn_decode(*args))
     return out, lse
 
 
@@ -203,13 +232,17 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
                 out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
                 err_flags: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
                 k_res: torch.Tensor | None = None, v_res: torch.Tensor | None = None,
-                res_lens: torch.Tensor | None = None, append_to_residual: bool = False):
+                res_lens: torch.Tensor | None = None, append_to_residual: bool = False,
+                block_table: torch.Tensor | None = None):
     """Fused layer decode step = encode_kv(T=1) of k_new/v_new [B, H_kv, D] at row write_pos[b]
     followed by attn_decode over [0, seq_lens[b]) -- one launch (vecinfer_decode_step).  With a
     residual window and append_to_residual, the new token is copied to residual row res_lens[b]-1
     instead (no encode) and attended from there."""
     B, Hq, D = q.shape
     Hkv, n_cap = k_codes.shape[1], k_codes.shape[2]
+    pg = None
+    if block_table is not None:   # page pools [n_pages, H_kv, page_size, row]
+        pg, n_cap = _paged(block_table, k_codes)
     if softmax_scale is None:
         softmax_scale = D ** -0.5
     if tuple(k_new.shape) != (B, Hkv, D) or tuple(v_new.shape) != (B, Hkv, D):
@@ -222,7 +255,9 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
     need = lib.vecinfer_decode_step_workspace_bytes(B, Hq, Hkv, n_cap, kcfg.c(), vcfg.c(), num_splits)
     if workspace is None or workspace.numel() < need:
         workspace = torch.zeros(max(need, 256), dtype=torch.uint8, device=q.device)
-    check("vecinfer_decode_step", lib.vecinfer_decode_step(
+    fn = lib.vecinfer_decode_step_paged if pg is not None else lib.vecinfer_decode_step
+    extra = (pg,) if pg is not None else ()
+    check("vecinfer_decode_step", fn(
         _need(q, "q", torch.bfloat16), _need(k_new, "k_new", torch.bfloat16), _need(v_new, "v_new", torch.bfloat16),
         B, Hq, Hkv, I64x2(q.stride(0), q.stride(1)), I64x2(k_new.stride(0), k_new.stride(1)),
         I64x2(v_new.stride(0), v_new.stride(1)), _need(lam, "lambda", torch.float32),
@@ -234,7 +269,7 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
         _need(lse, "lse", torch.float32),
         ctypes.c_void_p(err_flags.data_ptr()) if err_flags is not None else ctypes.c_void_p(0),
         ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream(q.device),
-        _residual(k_res, v_res, res_lens, append_to_residual)))
+        _residual(k_res, v_res, res_lens, append_to_residual), *extra))
     return out, lse
 
 

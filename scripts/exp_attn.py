@@ -16,7 +16,19 @@ import synth  # noqa: E402
 from paper_2510_06175_b200 import vecinfer as vi  # noqa: E402
 
 
-def run(B, N, splits, algo, reps=20, with_encode=False):
+def _paginate(kc, ps, seed):
+    """[B, H, N, row] -> random-permuted page pool [n_pages, H, ps, row] and block table [B, N/ps]."""
+    B, H, N, row = kc.shape
+    npb = N // ps
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    perm = torch.randperm(B * npb, generator=g).to(kc.device)
+    blocks = kc.view(B, H, npb, ps, row).permute(0, 2, 1, 3, 4).reshape(B * npb, H, ps, row)
+    pool = torch.empty(blocks.shape, dtype=blocks.dtype, device=blocks.device)
+    pool[perm] = blocks
+    return pool, perm.view(B, npb).to(torch.int32)
+
+
+def run(B, N, splits, algo, reps=20, with_encode=False, paged=0):
     dev = torch.device("cuda", 0)
     z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz"))
     lam = torch.from_numpy(z["lambda"]).to(dev)
@@ -26,6 +38,11 @@ def run(B, N, splits, algo, reps=20, with_encode=False):
     copies = max(1, int(np.ceil(400e6 / nbytes)))
     kcs = [synth.gen_codes_torch((B, 8, N, 32), 8, seed=2 * i, device=dev) for i in range(copies)]
     vcs = [synth.gen_codes_torch((B, 8, N, 32), 8, seed=2 * i + 1, device=dev) for i in range(copies)]
+    bt = None
+    if paged:
+        pk = [_paginate(k, paged, 7 + i) for i, k in enumerate(kcs)]
+        pv = [_paginate(v, paged, 7 + i) for i, v in enumerate(vcs)]
+        kcs, vcs, bt = [p[0] for p in pk], [p[0] for p in pv], pk[0][1]   # same permutation for K and V
     q = torch.from_numpy(synth.gen_queries(B, 32, 8, 128, seed=3)).to(dev).to(torch.bfloat16)
     seq = torch.full((B,), N, dtype=torch.int32, device=dev)
     ws = [vi.attn_workspace(B, 32, 8, N, splits, device=dev) for _ in range(copies)]
@@ -36,7 +53,7 @@ def run(B, N, splits, algo, reps=20, with_encode=False):
         for i in range(copies):
             if algo != "none":
                 vi.attn_decode(q, lam, ck, cv, kcs[i], vcs[i], seq, num_splits=splits, algo=algo, out=o, lse=lse,
-                               workspace=ws[i])
+                               workspace=ws[i], block_table=bt)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     n_l = max(copies, 8)
@@ -45,7 +62,7 @@ def run(B, N, splits, algo, reps=20, with_encode=False):
     vn = torch.from_numpy(synth.gen_values(1, 8, 128, seed=5, batch=B)).to(dev).to(torch.bfloat16)
     wp = torch.full((B,), N - 1, dtype=torch.int32, device=dev)
     with torch.cuda.stream(s):
-        vi.encode_kv(kn, vn, inv, ck, cv, kcs[0], vcs[0], wp)
+        vi.encode_kv(kn, vn, inv, ck, cv, kcs[0], vcs[0], wp, block_table=bt)
     torch.cuda.synchronize()
     with torch.cuda.graph(g, stream=s):
         for i in range(n_l):
@@ -54,11 +71,11 @@ def run(B, N, splits, algo, reps=20, with_encode=False):
                                num_splits=splits, out=o, lse=lse, workspace=ws[i % copies])
                 continue
             if with_encode:
-                vi.encode_kv(kn, vn, inv, ck, cv, kcs[i % copies], vcs[i % copies], wp)
+                vi.encode_kv(kn, vn, inv, ck, cv, kcs[i % copies], vcs[i % copies], wp, block_table=bt)
             if algo == "none":
                 continue
             vi.attn_decode(q, lam, ck, cv, kcs[i % copies], vcs[i % copies], seq, num_splits=splits, algo=algo,
-                           out=o, lse=lse, workspace=ws[i % copies])
+                           out=o, lse=lse, workspace=ws[i % copies], block_table=bt)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(s):      # CUDAGraph.replay() launches on the CURRENT stream
         g.replay()
@@ -82,10 +99,11 @@ def run(B, N, splits, algo, reps=20, with_encode=False):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", action="append", required=True)
+    ap.add_argument("--paged", type=int, default=0, help="page size of a random-permuted paged cache (0: contiguous)")
     args = ap.parse_args()
     for c in args.case:
         p = c.split(",")
-        run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma",
+        run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma", paged=args.paged,
             with_encode=(p[4] if p[4] == "fused" else True) if len(p) > 4 else False)
     from paper_2510_06175_b200 import _lib
     lib = _lib.load()
