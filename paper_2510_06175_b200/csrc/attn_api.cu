@@ -32,7 +32,8 @@ constexpr int kMaxSplits = 128;
 constexpr int64_t kMinTokensPerSplit = 512;
 
 bool vq_ok(const vecinfer_vq_t& c) {
-  return c.head_dim == 128 && c.sub_dim == 4 && (c.code_bits == 4 || c.code_bits == 8 || c.code_bits == 16);
+  return (c.head_dim == 128 || c.head_dim == 64) && c.sub_dim == 4 &&
+         (c.code_bits == 4 || c.code_bits == 8 || c.code_bits == 16);
 }
 
 struct WsLayout {
@@ -191,7 +192,11 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   const int32_t H_kv_real = H_kv;
   H_kv *= hsplit;                          // from here on: virtual KV heads
   if (!vq_ok(kcfg) || !vq_ok(vcfg))
-    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: supported configs are D=128, d=4, code_bits in {4,8,16}");
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: supported configs are D in {64, 128}, d=4, code_bits in {4,8,16}");
+  if (kcfg.head_dim != vcfg.head_dim) return fail(VECINFER_ERR_SHAPE, "attn_decode: K and V head_dim differ");
+  const int D = kcfg.head_dim;
+  if (D == 64 && (algo == VECINFER_ATTN_LUT || algo == VECINFER_ATTN_DEQUANT_MMA_STREAM || res))
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: head_dim 64 runs the split DEQUANT_MMA kernel without a residual window");
   if (algo == VECINFER_ATTN_LUT && (kcfg.code_bits != 8 || vcfg.code_bits != 8))
     return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: the LUT variant is implemented for b2d4 only");
   if (tok_begin < 0 || (tok_end >= 0 && tok_end < tok_begin))
@@ -212,8 +217,9 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
       return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_paged: paged caches run the split DEQUANT_MMA kernel only");
     if (tok_begin % 32 != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode_paged: tok_begin must be a multiple of 32");
   }
-  const bool use_sk = !pg && use_stream(B, H_kv, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
-  const SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
+  const bool use_sk = !pg && D == 128 && use_stream(B, H_kv, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
+  SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
+  if (D == 64) plan.cluster = 0;   // the DSMEM cluster merge is written for 128-dim rows
   const int32_t S = plan.S;
   const WsLayout wl = ws_layout(B, H_kv, plan_splits(B, H_kv, range, num_splits).S, true);
   const int64_t U = static_cast<int64_t>(B) * H_kv;
@@ -249,7 +255,9 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.page_shift = pg ? __builtin_ctz(static_cast<unsigned>(pg->page_size)) : 0;
   a.n_pages = pg ? pg->n_pages : 0;
   a.seq_lens = seq_lens; a.tok_begin = tok_begin; a.tok_end = tok_end;
-  a.qscale = static_cast<float>((1.0 / sqrt(128.0)) * static_cast<double>(softmax_scale) * 1.4426950408889634);
+  a.D = D;
+  a.qscale = static_cast<float>((1.0 / sqrt(static_cast<double>(D))) * static_cast<double>(softmax_scale) *
+                                1.4426950408889634);
   a.S = S;
   a.n_items = B * H_kv * S;
   a.U = static_cast<int>(U);
@@ -258,7 +266,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.rcpV = 1.0 / static_cast<double>(V);
   a.merge = !stream_split ? kMergeNone : (V <= sms ? kMergeSpin : kMergeLast);
   a.cluster = plan.cluster;
-  a.merge_kernel = (S > 1 && !plan.cluster && algo != VECINFER_ATTN_LUT) ? merge_mode_from_env() : 0;
+  a.merge_kernel = (S > 1 && !plan.cluster && algo != VECINFER_ATTN_LUT && D == 128) ? merge_mode_from_env() : 0;
   // every CTA co-resident (one CTA per SM, grid <= SMs): spin-barrier + sliced merge
   a.merge_spin = (S > 1 && !plan.cluster && !a.merge_kernel && algo != VECINFER_ATTN_LUT &&
                   static_cast<int64_t>(B) * H_kv * S <= device_sm_count() && !getenv("VECINFER_NO_SPIN")) ? 1 : 0;
@@ -280,7 +288,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.err = app ? app->err : nullptr;
   a.kcodes_w = const_cast<uint8_t*>(k_codes);
   a.vcodes_w = const_cast<uint8_t*>(v_codes);
-  a.inv_sqrt_d = static_cast<float>(1.0 / sqrt(128.0));
+  a.inv_sqrt_d = static_cast<float>(1.0 / sqrt(static_cast<double>(D)));
   a.res = res != nullptr;
   a.kres = res ? static_cast<const uint16_t*>(res->k) : nullptr;
   a.vres = res ? static_cast<const uint16_t*>(res->v) : nullptr;
@@ -350,6 +358,7 @@ extern "C" vecinfer_status_t vecinfer_attn_decode_paged(const void* q_bf16, int3
 static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
                          int32_t num_splits, vecinfer_attn_algo_t algo, bool paged = false) {
   if (algo == VECINFER_ATTN_LUT || kcfg.code_bits > 8 || vcfg.code_bits > 8 || B <= 0 || H_kv <= 0) return false;
+  if (kcfg.head_dim != 128) return false;   // the fused encode is written for 128-dim keys
   const int64_t units = static_cast<int64_t>(B) * H_kv;
   if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
     return num_splits == 0 || units * num_splits <= device_sm_count();   // persistent grids: separate append

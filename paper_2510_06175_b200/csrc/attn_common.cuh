@@ -9,6 +9,7 @@ struct AttnArgs {
   int64_t q_sb, q_sh;
   int B, Hq, Hkv, G;   // Hkv: VIRTUAL KV heads (= Hc * hsplit); G: query heads per virtual head (<= 4)
   int Hc, hsplit, Gfull;   // code/cache KV heads, virtual heads per KV head (GQA group > 4), full group
+  int D;                   // head dim: 128, or 64 (split kernel only)
   const float* lambda;  // [Hkv, 128]
   const uint16_t* ck;   // bf16 codebooks
   const uint16_t* cv;
@@ -133,12 +134,12 @@ __device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int
 // Fixed-order log-sum-exp merge of the S split partials of unit (b, h) into o and lse, in chunks
 // of 32 splits: all 2 x 32 loads of a chunk are issued before any use (one memory round trip per
 // chunk), then the running-max combine over s = 0..S-1.
-template <int NTHREADS>
+template <int NTHREADS, int DH = 128>
 __device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
   const HeadMap hm = head_map(a, h);
-  for (int idx = threadIdx.x; idx < 4 * 128; idx += NTHREADS) {
-    const int g = idx >> 7, dim = idx & 127;
+  for (int idx = threadIdx.x; idx < 4 * DH; idx += NTHREADS) {
+    const int g = idx / DH, dim = idx % DH;   // partials keep a 128-float row per head
     if (g >= hm.gp) continue;
     const float* pl = a.part_l + unit * a.S * 4 + g;
     const float* po = a.part_o + (unit * a.S * 4 + g) * 128 + dim;
@@ -169,14 +170,14 @@ __device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
     }
     const bool empty = !(wsum > 0.f);
     const float ov = empty ? 0.f : osum / wsum;
-    const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * 128 + dim;
+    const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * DH + dim;
     if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
     else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
     if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
   }
 }
 
-template <int NTHREADS, int NWARPS, int WROW = 128>
+template <int NTHREADS, int NWARPS, int WROW = 128, int DH = 128>
 __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s,
                                            const float* wm, const float* wl, const float* wacc,
                                            float* scratch) {
@@ -184,8 +185,9 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
   const HeadMap hm = head_map(a, h);
   __shared__ bool s_last;
-  for (int idx = tid; idx < 4 * 128; idx += NTHREADS) {
-    const int g = idx >> 7, dim = idx & 127;
+  // outputs o = g * DH + dim; partials are stored with a 128-float row per head
+  for (int idx = tid; idx < 4 * DH; idx += NTHREADS) {
+    const int g = idx / DH, dim = idx % DH;
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < NWARPS; ++w) M = fmaxf(M, wm[w * 4 + g]);
@@ -203,7 +205,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     const float L2 = empty ? -INFINITY : M + __log2f(lsum);
     if (a.S == 1) {
       if (g < hm.gp) {
-        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * 128 + dim;
+        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * DH + dim;
         if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
         else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
         if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = L2 * kLn2;
@@ -228,14 +230,14 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     // in shared memory; then one thread per output combines its S splits in order s = 0..S-1.
     phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 8);
     const int S = a.S;
-    const int per = (4 * 128 + S - 1) / S;
-    const int o0 = s * per, nout = max(0, min(4 * 128, o0 + per) - o0);
+    const int per = (4 * DH + S - 1) / S;
+    const int o0 = s * per, nout = max(0, min(4 * DH, o0 + per) - o0);
     float2* stage = reinterpret_cast<float2*>(scratch);
     for (int e = tid; e < nout * S; e += NTHREADS) {
       const int oo = e / S, p = e - oo * S, o = o0 + oo;
       float2 v = make_float2(0.f, -INFINITY);
-      if ((o >> 7) < hm.gp) {
-        unsigned long long* pp = a.part_elem + (unit * S + p) * 512 + o;
+      if (o / DH < hm.gp) {
+        unsigned long long* pp = a.part_elem + (unit * S + p) * 512 + (o / DH) * 128 + o % DH;
         unsigned long long w;
         while ((w = ld_relaxed_gpu_u64(pp)) == 0ull) __nanosleep(20);
         st_relaxed_gpu_u64(pp, 0ull);
@@ -247,7 +249,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     __syncthreads();
     phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);
     for (int t = tid; t < nout; t += NTHREADS) {
-      const int o = o0 + t, g = o >> 7, dim = o & 127;
+      const int o = o0 + t, g = o / DH, dim = o % DH;
       if (g >= hm.gp) continue;
       const float2* sv = stage + t * S;
       float m = -INFINITY;
@@ -261,7 +263,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
         }
       }
       const bool empty = !(wsum > 0.f);
-      const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * 128 + dim;
+      const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * DH + dim;
       const float ov = empty ? 0.f : osum * __frcp_rn(wsum);
       if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
       else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
@@ -278,7 +280,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   __syncthreads();
   phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);
   if (!s_last) return;
-  merge_splits<NTHREADS>(a, b, h);
+  merge_splits<NTHREADS, DH>(a, b, h);
   if (tid == 0) a.counter[2 * unit] = 0u;  // ready for the next launch
 }
 

@@ -43,10 +43,15 @@ template <int KB, int VB>
 constexpr int smem_bytes() { return (KB > 8 && VB > 8) ? kSmemBytesNoTab : kSmemBytes; }
 
 
-template <int KB, int VB>
+template <int KB, int VB, int DH>
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
-  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
-  constexpr bool kCanAppend = KB <= 8 && VB <= 8;
+  // DH = head dim (128, or 64: NEXT-4).  KS score k-steps (4 sub-vectors each) per 16 tokens,
+  // VS V sub-vectors per lane r (2 P.V m-tiles each), NL lanes holding a q~ row.
+  using FK = FmtD<KB, DH>;
+  using FV = FmtD<VB, DH>;
+  constexpr int KR = FK::kRow, VR = FV::kRow;
+  constexpr int KS = DH / 16, VS = DH / 32, NL = DH / 4;
+  constexpr bool kCanAppend = KB <= 8 && VB <= 8 && DH == 128;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
@@ -84,12 +89,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   const uint16_t* cbv = a.cv + hc * a.cv_hs;
   fill_tables<KB, VB>(tab, cbk, cbv, tid);
   float4 lam4 = make_float4(0.f, 0.f, 0.f, 0.f);   // warps 0..3: lambda of head h (static)
-  if (warp < 4) lam4 = *reinterpret_cast<const float4*>(a.lambda + hc * 128 + 4 * lane);
+  if (warp < 4) lam4 = *reinterpret_cast<const float4*>(a.lambda + hc * DH + 4 * (lane & (NL - 1)));
   if (first) griddep_wait();
   first = false;
   // q of the warp's query head goes out right after the wait, next to the seq_lens read below
   uint2 qw = make_uint2(0u, 0u);
-  if (warp < hm.gp) qw = *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (hm.hq0 + warp) * a.q_sh + 4 * lane);
+  if (warp < hm.gp)
+    qw = *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (hm.hq0 + warp) * a.q_sh + 4 * (lane & (NL - 1)));
 
   int64_t r0, r1, beg, e;
   split_range(a, b, s, r0, r1, &beg, &e);
@@ -113,8 +119,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   // (tok_begin % 32 == 0, chunks of 32) so a tile never crosses a page; the page of the tile after
   // next is read one tile ahead so its latency hides behind the current tile.
   const bool paged = a.bt != nullptr;
-  const uint8_t* kcb = a.kcodes + static_cast<int64_t>(r) * KR + Fmt<KB>::kOffK * j;
-  const uint8_t* vcb = a.vcodes + static_cast<int64_t>(2 * j) * VR + Fmt<VB>::kOffV * r;
+  const uint8_t* kcb = a.kcodes + static_cast<int64_t>(r) * KR + FK::kOffK * j;
+  const uint8_t* vcb = a.vcodes + static_cast<int64_t>(2 * j) * VR + FV::kOffV * r;
   const int64_t pmask = (int64_t(1) << a.page_shift) - 1;
   auto page_of = [&](int64_t tok) -> int { return a.bt[b * a.bt_stride + (tok >> a.page_shift)]; };
   auto row_in = [&](int pg, int64_t tok) -> int64_t {   // cache row of token tok given its page
@@ -136,8 +142,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   TileCodes<KB, VB> nxt;
   if (warp < ntile) {
     const int rem = ntok - 32 * warp;
-    if (rem >= 32) load_tile_full(nxt, kp, vp);
-    else load_tile_tail(nxt, kp, vp, rem, r, j);
+    if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
+    else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
   }
   unsigned char* newcodes = smem_raw + kMiscNew;   // [0,64): K code row, [64,128): V code row
   if (kCanAppend && owner) {
@@ -195,8 +201,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   }
   if (warp < 4) {   // Eq. 7 query transform (heads g >= G are zero padding)
     float* dq = sq + kQRow * warp + qoff(lane);
-    if (warp < hm.gp) qtransform_lane(qw, lam4, a.qscale, lane, dq);
-    else *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (warp < hm.gp) qtransform_lane(qw, lam4, a.qscale, lane, dq, NL);
+    else if (lane < NL) *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncthreads();
   if (kCanAppend && owner) {
@@ -228,12 +234,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   // B fragments of the score MMA: column n = lane/4 <-> (head n/2, part n%2); rows k
   // <-> sub-vector 8j+t, components {0,1} (b0) and {2,3} (b1)
-  uint32_t bq0[8], bq1[8];
+  uint32_t bq0[KS], bq1[KS];
   {
     const int gq = r >> 1, part = r & 1;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const float4 v = *reinterpret_cast<const float4*>(sq + kQRow * gq + qoff(8 * j + t));
+    for (int t = 0; t < KS; ++t) {
+      const float4 v = *reinterpret_cast<const float4*>(sq + kQRow * gq + qoff(KS * j + t));
       const float in[4] = {v.x, v.y, v.z, v.w};
       float o[4];
 #pragma unroll
@@ -249,15 +255,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   const uint32_t kbase = tab_s + (lane & 15) * 8;
   const uint32_t vbase = kbase + 128;
 
-  float acc[8][4];
+  float acc[2 * VS][4];
 #pragma unroll
-  for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+  for (int t = 0; t < 2 * VS; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
   float m_run = -INFINITY, l_run = 0.f;
 
   // ---- residual window (NEXT-1): raw bf16 rows scored with the raw q (q k^T = q~ k~^T, Eq. 7),
   // folded into this warp's online-softmax state before the code tiles; the P.V goes into the hi
   // slots of the MMA accumulator layout (thread (r, j) owns head j, dims 16r + 2t + {0, 1})
-  if (t_res0 < rlen) {
+  if constexpr (DH == 128) if (t_res0 < rlen) {
     float qr[4][4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
@@ -348,8 +354,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         vp += kStepV;
       }
       const int rem = rem_cur - 32 * kNW;
-      if (rem >= 32) load_tile_full(nxt, kp, vp);
-      else load_tile_tail(nxt, kp, vp, rem, r, j);
+      if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
+      else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
     }
 
     // ---- scores (log2 units) for tile tokens 16q + {r, r+8}, head j; two independent MMA
@@ -358,11 +364,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-      static_for<0, 8>([&](auto T) {
+      static_for<0, KS>([&](auto T) {
         constexpr int t = decltype(T)::value;
         const uint2 ea = gather_k<KB, t>(cur.k[q][0], kbase, cbk);
         const uint2 eb = gather_k<KB, t>(cur.k[q][1], kbase, cbk);
-        if (t < 4) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
+        if (t < KS / 2) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
         else mma_16816(d1, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
       });
       sc[q][0] = (d0[0] + d1[0]) + (d0[1] + d1[1]);
@@ -388,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       const float m_new = need ? mx : m_run;
       const float alpha = need ? ex2_approx(m_run - m_new) : 1.f;  // 0 when m_run was -inf
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+      for (int t = 0; t < 2 * VS; ++t) {
         acc[t][0] *= alpha; acc[t][1] *= alpha; acc[t][2] *= alpha; acc[t][3] *= alpha;
       }
       l_run *= alpha;
@@ -410,8 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       const uint32_t bp0 = movmatrix_trans(prmt(hb, lb, 0x5410));  // (hi, lo) of token r
       const uint32_t bp1 = movmatrix_trans(prmt(hb, lb, 0x7632));  // (hi, lo) of token r + 8
 
-      // ---- P.V (Alg. 1 l.16): m-tile t <-> sub-vector 4r + t/2, components 2(t%2) + {0,1}
-      static_for<0, 4>([&](auto U) {
+      // ---- P.V (Alg. 1 l.16): m-tile t <-> sub-vector VS*r + t/2, components 2(t%2) + {0,1}
+      static_for<0, VS>([&](auto U) {
         constexpr int u = decltype(U)::value;
         const uint2 g0 = gather_v<VB, u>(cur.v[q][0], vbase, cbv);
         const uint2 g1 = gather_v<VB, u>(cur.v[q][1], vbase, cbv);
@@ -438,18 +444,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     wm[warp * 4 + j] = m_run;
     wl[warp * 4 + j] = l_run;
   }
-  // thread (r, j): head j, dims 16r..16r+15; MMA slots [t][0] + [t][1] hold dim 16r+2t, [t][2] + [t][3]
-  // dim 16r+2t+1 (hi + lo parts)
-  float* dst = wacc + (warp * 4 + j) * kWRow + 16 * r;
+  // thread (r, j): head j, dims (DH/8)r .. (DH/8)r + DH/8 - 1; MMA slots [t][0] + [t][1] hold dim
+  // (DH/8)r + 2t, [t][2] + [t][3] dim (DH/8)r + 2t + 1 (hi + lo parts)
+  float* dst = wacc + (warp * 4 + j) * kWRow + (DH / 8) * r;
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < VS; ++k)
     *reinterpret_cast<float4*>(dst + 4 * k) =
         make_float4(acc[2 * k][0] + acc[2 * k][1], acc[2 * k][2] + acc[2 * k][3],
                     acc[2 * k + 1][0] + acc[2 * k + 1][1], acc[2 * k + 1][2] + acc[2 * k + 1][3]);
   __syncthreads();
   phase_mark(a.phase, cta_id, 3);
   if (!a.cluster) {
-    cta_finish<kThreads, kNW, kWRow>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
+    cta_finish<kThreads, kNW, kWRow, DH>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
     phase_mark(a.phase, cta_id, 4);
     continue;
   }
@@ -512,23 +518,27 @@ using AttnKernel = void (*)(const AttnArgs);
 
 static int smem_for(int kb, int vb) { return (kb > 8 && vb > 8) ? kSmemBytesNoTab : kSmemBytes; }
 
-static AttnKernel kernel_for(int kb, int vb) {
+static AttnKernel kernel_for(int kb, int vb, int dh = 128) {
   const int ki = kb == 4 ? 0 : kb == 8 ? 1 : 2, vi = vb == 4 ? 0 : vb == 8 ? 1 : 2;
-  static const AttnKernel table[3][3] = {
-      {attn_mma_kernel<4, 4>, attn_mma_kernel<4, 8>, attn_mma_kernel<4, 16>},
-      {attn_mma_kernel<8, 4>, attn_mma_kernel<8, 8>, attn_mma_kernel<8, 16>},
-      {attn_mma_kernel<16, 4>, attn_mma_kernel<16, 8>, attn_mma_kernel<16, 16>}};
-  return table[ki][vi];
+  static const AttnKernel table[2][3][3] = {
+      {{attn_mma_kernel<4, 4, 128>, attn_mma_kernel<4, 8, 128>, attn_mma_kernel<4, 16, 128>},
+       {attn_mma_kernel<8, 4, 128>, attn_mma_kernel<8, 8, 128>, attn_mma_kernel<8, 16, 128>},
+       {attn_mma_kernel<16, 4, 128>, attn_mma_kernel<16, 8, 128>, attn_mma_kernel<16, 16, 128>}},
+      {{attn_mma_kernel<4, 4, 64>, attn_mma_kernel<4, 8, 64>, attn_mma_kernel<4, 16, 64>},
+       {attn_mma_kernel<8, 4, 64>, attn_mma_kernel<8, 8, 64>, attn_mma_kernel<8, 16, 64>},
+       {attn_mma_kernel<16, 4, 64>, attn_mma_kernel<16, 8, 64>, attn_mma_kernel<16, 16, 64>}}};
+  return table[dh == 64 ? 1 : 0][ki][vi];
 }
 
 static void set_attrs_once() {
   static bool done = false;  // benign race: idempotent attributes
   if (!done) {
-    for (int kb : {4, 8, 16})
-      for (int vb : {4, 8, 16}) {
-        cudaFuncSetAttribute(kernel_for(kb, vb), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(kb, vb));
-        cudaFuncSetAttribute(kernel_for(kb, vb), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      }
+    for (int dh : {128, 64})
+      for (int kb : {4, 8, 16})
+        for (int vb : {4, 8, 16}) {
+          cudaFuncSetAttribute(kernel_for(kb, vb, dh), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(kb, vb));
+          cudaFuncSetAttribute(kernel_for(kb, vb, dh), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        }
     done = true;
   }
 }
@@ -585,7 +595,7 @@ cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_
   }
   cfg.attrs = at;
   cfg.numAttrs = n;
-  return cudaLaunchKernelEx(&cfg, kernel_for(kbits, vbits), a);
+  return cudaLaunchKernelEx(&cfg, kernel_for(kbits, vbits, a.D), a);
 }
 
 }  // namespace vecinfer

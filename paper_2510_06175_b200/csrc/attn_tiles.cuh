@@ -66,6 +66,29 @@ template <> struct Fmt<16> {
 template <int BITS> using KCode = typename Fmt<BITS>::K;
 template <int BITS> using VCode = typename Fmt<BITS>::V;
 
+// head-dim variants of the traits: D = 128 is Fmt<BITS>; D = 64 (16 sub-vectors, NEXT-4) keeps the
+// register types and gather selectors but halves the row and the per-lane chunks: lane j's K chunk
+// is sub-vectors 4j..4j+3 (4 score k-steps), lane r's V chunk sub-vectors 2r, 2r+1 (4 m-tiles).
+template <int BITS, int DH> struct FmtD : Fmt<BITS> {};
+template <> struct FmtD<8, 64> : Fmt<8> {
+  static constexpr int kRow = 16, kOffK = 4, kOffV = 2;
+  static __device__ __forceinline__ uint2 ldk(const uint8_t* p) { return make_uint2(ldg_nc_u32(p), 0u); }
+  static __device__ __forceinline__ uint32_t ldv(const uint8_t* p) { return ldg_nc_u16(p); }
+};
+template <> struct FmtD<4, 64> : Fmt<4> {
+  static constexpr int kRow = 8, kOffK = 2, kOffV = 1;
+  static __device__ __forceinline__ uint32_t ldk(const uint8_t* p) { return ldg_nc_u16(p); }
+  static __device__ __forceinline__ uint32_t ldv(const uint8_t* p) { return ldg_nc_u8(p); }
+};
+template <> struct FmtD<16, 64> : Fmt<16> {
+  static constexpr int kRow = 32, kOffK = 8, kOffV = 4;
+  static __device__ __forceinline__ uint4 ldk(const uint8_t* p) {
+    const uint2 w = ldg_nc_u64(p);
+    return make_uint4(w.x, w.y, 0u, 0u);
+  }
+  static __device__ __forceinline__ uint2 ldv(const uint8_t* p) { return make_uint2(ldg_nc_u32(p), 0u); }
+};
+
 // bf16x4 centroid (global) -> fp16x4 MMA operand pair (exact for |c| in the fp16 normal range)
 __device__ __forceinline__ uint2 bf16x4_to_f16x4(uint2 w) {
   uint2 e;
@@ -110,34 +133,38 @@ struct TileCodes {
 };
 
 // kp/vp point at this lane's bytes of token (tile start + r) / (tile start + 2j) respectively
-template <int KB, int VB>
+template <int KB, int VB, int DH = 128>
 __device__ __forceinline__ void load_tile_full(TileCodes<KB, VB>& tc, const uint8_t* kp, const uint8_t* vp) {
-  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
+  using FK = FmtD<KB, DH>;
+  using FV = FmtD<VB, DH>;
+  constexpr int KR = FK::kRow, VR = FV::kRow;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    tc.k[q][0] = Fmt<KB>::ldk(kp + (16 * q) * KR);
-    tc.k[q][1] = Fmt<KB>::ldk(kp + (16 * q + 8) * KR);
-    tc.v[q][0] = Fmt<VB>::ldv(vp + (16 * q) * VR);
-    tc.v[q][1] = Fmt<VB>::ldv(vp + (16 * q + 1) * VR);
-    tc.v[q][2] = Fmt<VB>::ldv(vp + (16 * q + 8) * VR);
-    tc.v[q][3] = Fmt<VB>::ldv(vp + (16 * q + 9) * VR);
+    tc.k[q][0] = FK::ldk(kp + (16 * q) * KR);
+    tc.k[q][1] = FK::ldk(kp + (16 * q + 8) * KR);
+    tc.v[q][0] = FV::ldv(vp + (16 * q) * VR);
+    tc.v[q][1] = FV::ldv(vp + (16 * q + 1) * VR);
+    tc.v[q][2] = FV::ldv(vp + (16 * q + 8) * VR);
+    tc.v[q][3] = FV::ldv(vp + (16 * q + 9) * VR);
   }
 }
 
 // ragged last tile: rem = tokens left in the split (1..31), rows beyond it read as code 0
-template <int KB, int VB>
+template <int KB, int VB, int DH = 128>
 __device__ __forceinline__ void load_tile_tail(TileCodes<KB, VB>& tc, const uint8_t* kp, const uint8_t* vp, int rem,
                                                int r, int j) {
-  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
+  using FK = FmtD<KB, DH>;
+  using FV = FmtD<VB, DH>;
+  constexpr int KR = FK::kRow, VR = FV::kRow;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    tc.k[q][0] = (16 * q + r < rem) ? Fmt<KB>::ldk(kp + (16 * q) * KR) : Fmt<KB>::zk();
-    tc.k[q][1] = (16 * q + r + 8 < rem) ? Fmt<KB>::ldk(kp + (16 * q + 8) * KR) : Fmt<KB>::zk();
+    tc.k[q][0] = (16 * q + r < rem) ? FK::ldk(kp + (16 * q) * KR) : Fmt<KB>::zk();
+    tc.k[q][1] = (16 * q + r + 8 < rem) ? FK::ldk(kp + (16 * q + 8) * KR) : Fmt<KB>::zk();
     const int t0 = 16 * q + 2 * j;
-    tc.v[q][0] = (t0 < rem) ? Fmt<VB>::ldv(vp + (16 * q) * VR) : VCode<VB>{};
-    tc.v[q][1] = (t0 + 1 < rem) ? Fmt<VB>::ldv(vp + (16 * q + 1) * VR) : VCode<VB>{};
-    tc.v[q][2] = (t0 + 8 < rem) ? Fmt<VB>::ldv(vp + (16 * q + 8) * VR) : VCode<VB>{};
-    tc.v[q][3] = (t0 + 9 < rem) ? Fmt<VB>::ldv(vp + (16 * q + 9) * VR) : VCode<VB>{};
+    tc.v[q][0] = (t0 < rem) ? FV::ldv(vp + (16 * q) * VR) : VCode<VB>{};
+    tc.v[q][1] = (t0 + 1 < rem) ? FV::ldv(vp + (16 * q + 1) * VR) : VCode<VB>{};
+    tc.v[q][2] = (t0 + 8 < rem) ? FV::ldv(vp + (16 * q + 8) * VR) : VCode<VB>{};
+    tc.v[q][3] = (t0 + 9 < rem) ? FV::ldv(vp + (16 * q + 9) * VR) : VCode<VB>{};
   }
 }
 
@@ -155,7 +182,8 @@ __device__ __forceinline__ void put_code(unsigned char* row, int lane, uint32_t 
 // Query transform of Eq. 7 for one head (one warp): ((q * lambda) H_pm) * qscale, fp32 FWHT
 // (2 register + 5 shuffle stages); q (4 bf16) and lambda (float4) are this lane's 4 channels;
 // dst = this lane's 4 outputs (sub-vector `lane`).
-__device__ __forceinline__ void qtransform_lane(uint2 w, float4 l, float qscale, int lane, float* dst) {
+__device__ __forceinline__ void qtransform_lane(uint2 w, float4 l, float qscale, int lane, float* dst,
+                                                int nlanes = 32) {
   float x[4];
   x[0] = __uint_as_float(w.x << 16) * l.x;
   x[1] = __uint_as_float(w.x & 0xFFFF0000u) * l.y;
@@ -165,6 +193,7 @@ __device__ __forceinline__ void qtransform_lane(uint2 w, float4 l, float qscale,
   x[0] = s0 + s2; x[2] = s0 - s2; x[1] = s1 + s3; x[3] = s1 - s3;
 #pragma unroll
   for (int m = 1; m < 32; m <<= 1) {
+    if (m >= nlanes) break;   // D = 64: 4 shuffle stages inside each half-warp
     const bool upper = (lane & m) != 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -172,7 +201,8 @@ __device__ __forceinline__ void qtransform_lane(uint2 w, float4 l, float qscale,
       x[i] = upper ? (o - x[i]) : (x[i] + o);
     }
   }
-  *reinterpret_cast<float4*>(dst) = make_float4(x[0] * qscale, x[1] * qscale, x[2] * qscale, x[3] * qscale);
+  if (lane < nlanes)
+    *reinterpret_cast<float4*>(dst) = make_float4(x[0] * qscale, x[1] * qscale, x[2] * qscale, x[3] * qscale);
 }
 
 }  // namespace vecinfer

@@ -106,6 +106,11 @@ __device__ __forceinline__ uint32_t ldg_nc_u16(const void* p) {
   asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
   return static_cast<uint32_t>(v);
 }
+__device__ __forceinline__ uint32_t ldg_nc_u8(const void* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return static_cast<uint32_t>(v);
+}
 // read-only load that may allocate in L1 (codebook gathers)
 __device__ __forceinline__ uint2 ldg_ro_u64(const void* p) {
   uint2 v;
@@ -236,8 +241,10 @@ __device__ __forceinline__ float pinned_dist4(float x0, float x1, float x2, floa
 //   X = A H_pm  (2 in-register + 5 warp-shuffle butterfly stages, exact integer arithmetic),
 //   x = RN32(RN32(X) * 2^-24) * RN32(1/sqrt(D)).
 // krow4/inv4 point at this lane's 4 elements.  Returns true (warp-uniform) if any |k*inv| >= 2^32.
+// nlanes = D / 4 lanes hold the key (32 for D = 128, 16 for D = 64; with 16 the upper half-warp
+// computes a duplicate of the lower one and the butterflies never cross the halves).
 __device__ __forceinline__ bool key_transform_lane(const uint16_t* krow4, const float* inv4, float inv_sqrt_d,
-                                                   int lane, float (&x)[4]) {
+                                                   int lane, float (&x)[4], int nlanes = 32) {
   const uint2 kw = *reinterpret_cast<const uint2*>(krow4);
   const float kf[4] = {__uint_as_float(kw.x << 16), __uint_as_float(kw.x & 0xFFFF0000u),
                        __uint_as_float(kw.y << 16), __uint_as_float(kw.y & 0xFFFF0000u)};
@@ -255,6 +262,7 @@ __device__ __forceinline__ bool key_transform_lane(const uint16_t* krow4, const 
   A[0] = s0 + s2; A[2] = s0 - s2; A[1] = s1 + s3; A[3] = s1 - s3;
 #pragma unroll
   for (int m = 1; m < 32; m <<= 1) {
+    if (m >= nlanes) break;
     const bool upper = (lane & m) != 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {

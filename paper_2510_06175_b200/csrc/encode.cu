@@ -39,19 +39,21 @@ struct EncArgs {
   const int32_t* write_pos;
   uint32_t* err;
   float inv_sqrt_d;
+  int D, nsub;             // head dim (64 or 128) and sub-vectors (lanes holding the key) = D / 4
   unsigned long long* ws;  // 16-bit path: [B*T*H][2][32] packed minima
 };
 
 // Smoothing + exact integer FWHT + fixed-point -> fp32 (key_transform_lane), flags range errors.
 __device__ __forceinline__ void transform_key_lane(const EncArgs& a, int b, int t, int h, int lane,
                                                    float (&x)[4]) {
-  const bool bad = key_transform_lane(a.k + b * a.ks_b + t * a.ks_t + h * a.ks_h + 4 * lane,
-                                      a.inv_lambda + h * 128 + 4 * lane, a.inv_sqrt_d, lane, x);
+  const int le = lane & (a.nsub - 1);   // D = 64: the upper half-warp duplicates the lower one
+  const bool bad = key_transform_lane(a.k + b * a.ks_b + t * a.ks_t + h * a.ks_h + 4 * le,
+                                      a.inv_lambda + h * a.D + 4 * le, a.inv_sqrt_d, lane, x, a.nsub);
   if (bad && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
 }
 
 __device__ __forceinline__ void load_value_lane(const EncArgs& a, int b, int t, int h, int lane, float (&x)[4]) {
-  const uint16_t* vp = a.v + b * a.vs_b + t * a.vs_t + h * a.vs_h + 4 * lane;
+  const uint16_t* vp = a.v + b * a.vs_b + t * a.vs_t + h * a.vs_h + 4 * (lane & (a.nsub - 1));
   const uint2 w = *reinterpret_cast<const uint2*>(vp);
   x[0] = __uint_as_float(w.x << 16);
   x[1] = __uint_as_float(w.x & 0xFFFF0000u);
@@ -59,16 +61,17 @@ __device__ __forceinline__ void load_value_lane(const EncArgs& a, int b, int t, 
   x[3] = __uint_as_float(w.y & 0xFFFF0000u);
 }
 
-__device__ __forceinline__ void store_code(uint8_t* codes, int bits, int64_t row, int lane, uint32_t code) {
-  const int row_bytes = 32 * bits / 8;
+__device__ __forceinline__ void store_code(uint8_t* codes, int bits, int64_t row, int lane, uint32_t code,
+                                           int nsub = 32) {
+  const int row_bytes = nsub * bits / 8;
   uint8_t* p = codes + row * row_bytes;
   if (bits == 8) {
-    p[lane] = static_cast<uint8_t>(code);
+    if (lane < nsub) p[lane] = static_cast<uint8_t>(code);
   } else if (bits == 4) {
     const uint32_t hi = __shfl_xor_sync(0xffffffffu, code, 1);
-    if ((lane & 1) == 0) p[lane >> 1] = static_cast<uint8_t>(code | (hi << 4));
+    if ((lane & 1) == 0 && lane < nsub) p[lane >> 1] = static_cast<uint8_t>(code | (hi << 4));
   } else {
-    reinterpret_cast<uint16_t*>(p)[lane] = static_cast<uint16_t>(code);
+    if (lane < nsub) reinterpret_cast<uint16_t*>(p)[lane] = static_cast<uint16_t>(code);
   }
 }
 
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_small_kernel(EncArgs a)
     const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
     if (dd < best) { best = dd; bi = j; }
   }
-  store_code(a.kcodes, KBITS, row, lane, bi);
+  store_code(a.kcodes, KBITS, row, lane, bi, a.nsub);
   load_value_lane(a, b, t, h, lane, x);
   best = __int_as_float(0x7f800000);
   bi = 0;
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_small_kernel(EncArgs a)
     const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
     if (dd < best) { best = dd; bi = j; }
   }
-  store_code(a.vcodes, VBITS, row, lane, bi);
+  store_code(a.vcodes, VBITS, row, lane, bi, a.nsub);
 }
 
 // ------------------------------------------------------------------ 4/8-bit decode append
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(512) encode_append_kernel(EncArgs a) {
       if (c < bb) { bb = c; ii = sidx[warp + w][lane]; }
     }
     int64_t row;
-    if (cache_row(a, b, t, h, lane, row)) store_code(isv ? a.vcodes : a.kcodes, isv ? VBITS : KBITS, row, lane, ii);
+    if (cache_row(a, b, t, h, lane, row)) store_code(isv ? a.vcodes : a.kcodes, isv ? VBITS : KBITS, row, lane, ii, a.nsub);
   }
 }
 
@@ -289,12 +292,13 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_finalize(EncArgs a
       if (bits == 8) small_nn_global<8>(cb, x, code);
       else small_nn_global<4>(cb, x, code);
     }
-    store_code(codes, bits, row, lane, code);
+    store_code(codes, bits, row, lane, code, a.nsub);
   }
 }
 
 bool vq_supported(const vecinfer_vq_t& c) {
-  return c.head_dim == 128 && c.sub_dim == 4 && (c.code_bits == 4 || c.code_bits == 8 || c.code_bits == 16);
+  return (c.head_dim == 128 || c.head_dim == 64) && c.sub_dim == 4 &&
+         (c.code_bits == 4 || c.code_bits == 8 || c.code_bits == 16);
 }
 
 }  // namespace
@@ -321,7 +325,8 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
     return fail(VECINFER_ERR_INVALID_ARG, "encode_kv: NULL pointer");
   if (B <= 0 || T <= 0 || H_kv <= 0 || n_cap <= 0) return fail(VECINFER_ERR_SHAPE, "encode_kv: non-positive size");
   if (!vq_supported(kcfg) || !vq_supported(vcfg))
-    return fail(VECINFER_ERR_UNSUPPORTED, "encode_kv: supported configs are D=128, d=4, code_bits in {4,8,16}");
+    return fail(VECINFER_ERR_UNSUPPORTED, "encode_kv: supported configs are D in {64, 128}, d=4, code_bits in {4,8,16}");
+  if (kcfg.head_dim != vcfg.head_dim) return fail(VECINFER_ERR_SHAPE, "encode_kv: K and V head_dim differ");
   if (!aligned(k_bf16, 8) || !aligned(v_bf16, 8) || !aligned(inv_lambda, 16) || !aligned(ck_bf16, 8) ||
       !aligned(cv_bf16, 8) || !aligned(k_codes, 2) || !aligned(v_codes, 2))
     return fail(VECINFER_ERR_INVALID_ARG, "encode_kv: misaligned pointer (k/v/codebooks 8 B, inv_lambda 16 B)");
@@ -351,6 +356,8 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
     a.page_shift = __builtin_ctz(static_cast<unsigned>(pg->page_size));
   }
   a.inv_sqrt_d = static_cast<float>(1.0 / sqrt(static_cast<double>(kcfg.head_dim)));
+  a.D = kcfg.head_dim;
+  a.nsub = kcfg.head_dim / 4;
   a.ws = static_cast<unsigned long long*>(workspace);
   cudaStream_t st = as_stream(stream);
   const int64_t nbt = static_cast<int64_t>(B) * T;

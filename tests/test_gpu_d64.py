@@ -1,0 +1,132 @@
+"""head_dim 64 (the paper's Fig. 10 variant): 16 sub-vectors of 4 dims per
+head.  Encode must match the oracle bit for bit (its pinned transform is written for any D: 64-point
+integer Hadamard, 1/sqrt(64) = 0.125), attention must match the oracle within the usual 2e-3.
+D = 64 runs the split kernel (no residual window, no fused append, no stream/LUT variant).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import ref
+from helpers import load_codebooks
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2510_06175_b200 import vecinfer as vi  # noqa: E402
+from paper_2510_06175_b200._lib import VecInferError  # noqa: E402
+from test_gpu_parity import _assert_close, t_bf16, t_f32, t_i32, t_u8  # noqa: E402
+
+CB = load_codebooks()
+D = 64
+CFG64 = {4: vi.VQConfig(64, 4, 4), 8: vi.VQConfig(64, 4, 8), 16: vi.VQConfig(64, 4, 16)}
+NAME = {4: "b1d4", 8: "b2d4", 16: "b4d4"}
+LAM, INV = CB["lambda"][:, :D].copy(), CB["inv_lambda"][:, :D].copy()
+
+
+def _case(B, G, n_cap, lens, seed, bits=8, Hkv=8):
+    ck, cv = CB[f"ck_{NAME[bits]}"], CB[f"cv_{NAME[bits]}"]
+    kc = synth.gen_codes(n_cap, Hkv, D // 4, bits, seed=seed, batch=B)
+    vc = synth.gen_codes(n_cap, Hkv, D // 4, bits, seed=seed + 1, batch=B)
+    q = synth.gen_queries(B, Hkv * G, Hkv, D, seed=seed + 2)
+    return dict(q=q, lam=LAM[:Hkv], ck=ck if ck.ndim == 2 else ck[:Hkv], cv=cv if cv.ndim == 2 else cv[:Hkv],
+                kc=kc, vc=vc, seq_lens=np.asarray(lens), bits=bits)
+
+
+def _run(c, **kw):
+    b = c["bits"]
+    o, L = vi.attn_decode(t_bf16(c["q"]), t_f32(c["lam"]), t_bf16(c["ck"]), t_bf16(c["cv"]),
+                          t_u8(ref.pack_codes(c["kc"], b)), t_u8(ref.pack_codes(c["vc"], b)), t_i32(c["seq_lens"]),
+                          kcfg=CFG64[b], vcfg=CFG64[b], **kw)
+    return o.float().cpu().numpy(), L.cpu().numpy()
+
+
+def _ref(c, tok_begin=0, tok_end=None):
+    return ref.attention_decode_batch(c["q"], c["lam"], c["ck"], c["cv"], c["kc"], c["vc"], c["seq_lens"],
+                                      tok_begin, tok_end)
+
+
+@pytest.mark.parametrize("bits", [4, 8, 16])
+@pytest.mark.parametrize("T", [1, 300])
+def test_d64_encode_bit_exact(bits, T):
+    B, H = 2, 8
+    k = synth.gen_keys(T, H, D, seed=600 + T, batch=B)
+    v = synth.gen_values(T, H, D, seed=601 + T, batch=B)
+    ck, cv = CB[f"ck_{NAME[bits]}"], CB[f"cv_{NAME[bits]}"]
+    cfg = CFG64[bits]
+    n_cap = T + 3
+    kcodes = torch.zeros(B, H, n_cap, cfg.row_bytes, dtype=torch.uint8, device="cuda")
+    vcodes = torch.zeros_like(kcodes)
+    wp = np.array([0, 3], np.int32)
+    vi.encode_kv(t_bf16(k), t_bf16(v), t_f32(INV), t_bf16(ck), t_bf16(cv), kcodes, vcodes, t_i32(wp), cfg, cfg)
+    for b in range(B):
+        for h in range(H):
+            ckh = ck if ck.ndim == 2 else ck[h]
+            cvh = cv if cv.ndim == 2 else cv[h]
+            kk, vv = ref.encode_kv(k[b, :, h], v[b, :, h], INV[h], ckh, cvh)
+            got_k = ref.unpack_codes(kcodes[b, h, wp[b]:wp[b] + T].cpu().numpy(), bits)
+            got_v = ref.unpack_codes(vcodes[b, h, wp[b]:wp[b] + T].cpu().numpy(), bits)
+            assert np.array_equal(got_k, kk) and np.array_equal(got_v, vv), (b, h)
+
+
+@pytest.mark.parametrize("splits", [0, 1, 3, 16, 40])
+@pytest.mark.parametrize("lens", [[2000, 17], [1, 4097]])
+def test_d64_attention(splits, lens):
+    c = _case(len(lens), 4, max(lens) + 2, lens, seed=610 + splits)
+    o, L = _run(c, num_splits=splits)
+    _assert_close(o, L, *_ref(c))
+
+
+@pytest.mark.parametrize("G,bits", [(1, 8), (2, 4), (8, 8), (5, 16)])
+def test_d64_gqa_and_bitwidths(G, bits):
+    c = _case(2, G, 900, [900, 450], seed=620 + G + bits, bits=bits)
+    o, L = _run(c)
+    _assert_close(o, L, *_ref(c))
+
+
+def test_d64_token_range_and_bf16():
+    c = _case(2, 4, 1200, [1200, 700], seed=630)
+    o, L = _run(c, tok_begin=100, tok_end=1000)
+    _assert_close(o, L, *_ref(c, 100, 1000))
+    of, Lf = _run(c, num_splits=3)
+    ob, Lb = _run(c, num_splits=3, o_dtype=torch.bfloat16)
+    assert np.array_equal(synth.round_to_bf16(of.astype(np.float32)), ob.astype(np.float32))
+
+
+def test_d64_decode_step():
+    """D = 64 decode step: separate append launch + attention; appended codes are the oracle's."""
+    lens = [700, 64]
+    B = len(lens)
+    c = _case(B, 4, 710, lens, seed=640)
+    kn = synth.gen_keys(1, 8, D, seed=641, batch=B)[:, 0]
+    vn = synth.gen_values(1, 8, D, seed=642, batch=B)[:, 0]
+    wp = [n - 1 for n in lens]
+    kcodes, vcodes = t_u8(ref.pack_codes(c["kc"], 8)), t_u8(ref.pack_codes(c["vc"], 8))
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(INV), t_bf16(c["ck"]),
+                          t_bf16(c["cv"]), kcodes, vcodes, t_i32(wp), t_i32(lens), kcfg=CFG64[8], vcfg=CFG64[8])
+    assert vi.decode_step_launches(B, 8, 710, CFG64[8], CFG64[8]) == 2
+    for b in range(B):
+        for h in range(8):
+            kk, vv = ref.encode_kv(kn[b, h], vn[b, h], INV[h], c["ck"][h], c["cv"][h])
+            c["kc"][b, h, wp[b]], c["vc"][b, h, wp[b]] = kk, vv
+    assert np.array_equal(kcodes.cpu().numpy(), ref.pack_codes(c["kc"], 8))
+    assert np.array_equal(vcodes.cpu().numpy(), ref.pack_codes(c["vc"], 8))
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_ref(c))
+
+
+def test_d64_unsupported_paths_fail_loudly():
+    c = _case(1, 4, 256, [256], seed=650)
+    with pytest.raises(VecInferError):
+        _run(c, algo="stream")
+    with pytest.raises(VecInferError):
+        _run(c, algo="lut")
+    kr = torch.zeros(1, 8, 16, D, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(VecInferError):
+        _run(c, k_res=kr, v_res=kr, res_lens=t_i32([4]))
+    with pytest.raises(VecInferError):   # K and V head dims must agree
+        vi.attn_decode(t_bf16(c["q"]), t_f32(c["lam"]), t_bf16(c["ck"]), t_bf16(c["cv"]),
+                       t_u8(ref.pack_codes(c["kc"], 8)), t_u8(ref.pack_codes(c["vc"], 8)), t_i32(c["seq_lens"]),
+                       kcfg=CFG64[8], vcfg=vi.B2D4)
