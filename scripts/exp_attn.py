@@ -28,41 +28,44 @@ def _paginate(kc, ps, seed):
     return pool, perm.view(B, npb).to(torch.int32)
 
 
-def run(B, N, splits, algo, reps=20, with_encode=False, paged=0):
+def run(B, N, splits, algo, reps=20, with_encode=False, paged=0, dh=128):
     dev = torch.device("cuda", 0)
     z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz"))
     lam = torch.from_numpy(z["lambda"]).to(dev)
     ck = torch.from_numpy(synth.bf16_from_bits(z["ck_b2d4"])).to(dev).to(torch.bfloat16)
     cv = torch.from_numpy(synth.bf16_from_bits(z["cv_b2d4"])).to(dev).to(torch.bfloat16)
-    nbytes = B * 8 * N * 64
+    nbytes = B * 8 * N * 64 * dh // 128
     copies = max(1, int(np.ceil(400e6 / nbytes)))
-    kcs = [synth.gen_codes_torch((B, 8, N, 32), 8, seed=2 * i, device=dev) for i in range(copies)]
-    vcs = [synth.gen_codes_torch((B, 8, N, 32), 8, seed=2 * i + 1, device=dev) for i in range(copies)]
+    kcs = [synth.gen_codes_torch((B, 8, N, dh // 4), 8, seed=2 * i, device=dev) for i in range(copies)]
+    vcs = [synth.gen_codes_torch((B, 8, N, dh // 4), 8, seed=2 * i + 1, device=dev) for i in range(copies)]
+    cfg = vi.VQConfig(dh, 4, 8)
+    if dh != 128:
+        lam = lam[:, :dh].contiguous()
     bt = None
     if paged:
         pk = [_paginate(k, paged, 7 + i) for i, k in enumerate(kcs)]
         pv = [_paginate(v, paged, 7 + i) for i, v in enumerate(vcs)]
         kcs, vcs, bt = [p[0] for p in pk], [p[0] for p in pv], pk[0][1]   # same permutation for K and V
-    q = torch.from_numpy(synth.gen_queries(B, 32, 8, 128, seed=3)).to(dev).to(torch.bfloat16)
+    q = torch.from_numpy(synth.gen_queries(B, 32, 8, dh, seed=3)).to(dev).to(torch.bfloat16)
     seq = torch.full((B,), N, dtype=torch.int32, device=dev)
     ws = [vi.attn_workspace(B, 32, 8, N, splits, device=dev) for _ in range(copies)]
-    o = torch.empty(B, 32, 128, dtype=torch.bfloat16, device=dev)
+    o = torch.empty(B, 32, dh, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(B, 32, dtype=torch.float32, device=dev)
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         for i in range(copies):
             if algo != "none":
                 vi.attn_decode(q, lam, ck, cv, kcs[i], vcs[i], seq, num_splits=splits, algo=algo, out=o, lse=lse,
-                               workspace=ws[i], block_table=bt)
+                               workspace=ws[i], block_table=bt, kcfg=cfg, vcfg=cfg)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     n_l = max(copies, 8)
-    inv = torch.from_numpy(z["inv_lambda"]).to(dev)
-    kn = torch.from_numpy(synth.gen_keys(1, 8, 128, seed=4, batch=B)).to(dev).to(torch.bfloat16)
-    vn = torch.from_numpy(synth.gen_values(1, 8, 128, seed=5, batch=B)).to(dev).to(torch.bfloat16)
+    inv = torch.from_numpy(z["inv_lambda"]).to(dev)[:, :dh].contiguous()
+    kn = torch.from_numpy(synth.gen_keys(1, 8, dh, seed=4, batch=B)).to(dev).to(torch.bfloat16)
+    vn = torch.from_numpy(synth.gen_values(1, 8, dh, seed=5, batch=B)).to(dev).to(torch.bfloat16)
     wp = torch.full((B,), N - 1, dtype=torch.int32, device=dev)
     with torch.cuda.stream(s):
-        vi.encode_kv(kn, vn, inv, ck, cv, kcs[0], vcs[0], wp, block_table=bt)
+        vi.encode_kv(kn, vn, inv, ck, cv, kcs[0], vcs[0], wp, cfg, cfg, block_table=bt)
     torch.cuda.synchronize()
     with torch.cuda.graph(g, stream=s):
         for i in range(n_l):
@@ -71,11 +74,11 @@ def run(B, N, splits, algo, reps=20, with_encode=False, paged=0):
                                num_splits=splits, out=o, lse=lse, workspace=ws[i % copies])
                 continue
             if with_encode:
-                vi.encode_kv(kn, vn, inv, ck, cv, kcs[i % copies], vcs[i % copies], wp, block_table=bt)
+                vi.encode_kv(kn, vn, inv, ck, cv, kcs[i % copies], vcs[i % copies], wp, cfg, cfg, block_table=bt)
             if algo == "none":
                 continue
             vi.attn_decode(q, lam, ck, cv, kcs[i % copies], vcs[i % copies], seq, num_splits=splits, algo=algo,
-                           out=o, lse=lse, workspace=ws[i % copies], block_table=bt)
+                           out=o, lse=lse, workspace=ws[i % copies], block_table=bt, kcfg=cfg, vcfg=cfg)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(s):      # CUDAGraph.replay() launches on the CURRENT stream
         g.replay()
@@ -100,10 +103,11 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", action="append", required=True)
     ap.add_argument("--paged", type=int, default=0, help="page size of a random-permuted paged cache (0: contiguous)")
+    ap.add_argument("--dh", type=int, default=128, help="head dim (128 or 64)")
     args = ap.parse_args()
     for c in args.case:
         p = c.split(",")
-        run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma", paged=args.paged,
+        run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma", paged=args.paged, dh=args.dh,
             with_encode=(p[4] if p[4] == "fused" else True) if len(p) > 4 else False)
     from paper_2510_06175_b200 import _lib
     lib = _lib.load()
