@@ -19,9 +19,11 @@
  *    non-OK status of the calling thread.
  *  - Thread-safe: no global mutable state except the thread-local error string and a
  *    per-device attribute cache.
- *  - Supported shapes (v1): head_dim D = 128, sub_dim d = 4, code_bits in {4, 8, 16}
- *    (b1d4, b2d4, b4d4 in BASELINE.json notation = paper d4b4, d4b8, d4b16);
- *    GQA group G = H_q / H_kv in {1, 2, 4}.  Anything else returns VECINFER_ERR_UNSUPPORTED.
+ *  - Supported shapes (ABI v4): head_dim D in {128, 64}, sub_dim d = 4, code_bits in {4, 8, 16}
+ *    (b1d4, b2d4, b4d4 in BASELINE.json notation = paper d4b4, d4b8, d4b16), K and V
+ *    widths independent; GQA group G = H_q / H_kv in 1..8; contiguous or paged code caches.
+ *    D = 64 runs the split attention kernel only (no residual window, no fused append).
+ *    Anything else returns VECINFER_ERR_UNSUPPORTED.
  */
 #ifndef VECINFER_H_
 #define VECINFER_H_
