@@ -23,6 +23,11 @@
  *    (b1d4, b2d4, b4d4 in BASELINE.json notation = paper d4b4, d4b8, d4b16), K and V
  *    widths independent; GQA group G = H_q / H_kv in 1..8; contiguous or paged code caches.
  *    D = 64 runs the split attention kernel only (no residual window, no fused append).
+ *    The paper's other configurations, D = 128 only:
+ *    d8b8 {128, 8, 8}, d8b12 {128, 8, 12}, d4b10 {128, 4, 10}, d2b8 {128, 2, 8}; attention pairs
+ *    (f, f) and the mixed K-d4b10 / V-d8b12 and K-d8b12 / V-d8b8 of Table 3, on the split
+ *    DEQUANT_MMA kernel (contiguous or paged, residual window allowed; no stream / LUT variant,
+ *    decode_step appends with a separate encode launch).
  *    Anything else returns VECINFER_ERR_UNSUPPORTED.
  */
 #ifndef VECINFER_H_
@@ -156,9 +161,13 @@ vecinfer_status_t vecinfer_calibrate_smooth(const void* k_cal_bf16, int64_t n_to
  *   inv_lambda       fp32 [H_kv, D] (from vecinfer_calibrate_smooth).
  *   ck_bf16, cv_bf16 codebooks [H_kv, 2^b, d] bf16; *_head_stride = elements between heads,
  *                    0 = one codebook shared by all heads.
- *   k_codes, v_codes uint8 [B, H_kv, n_cap, D/d*b/8] token-major packed rows (R11: 8-bit one
+ *   k_codes, v_codes uint8 [B, H_kv, n_cap, D/d*b/8] token-major packed rows (R11: the row is
+ *                    one little-endian bit string, code m in bits [m b, m b + b) -- 8-bit one
  *                    byte per sub-vector; 4-bit sub-vector 2i low nibble, 2i+1 high nibble;
- *                    16-bit little-endian u16).
+ *                    16-bit little-endian u16; 10/12-bit codes straddle bytes).
+ *   (d = 8 / 2 distances sum the d squared differences left to right in the same way; the
+ *    NEXT-2 formats are encoded by one CTA per (token-head, K or V) that scans the codebook
+ *    with all 256 threads and reduces (dist_bits << 32 | index) minima.)
  *   write_pos        device int32 [B]: cache row of token t = 0 of batch b (e.g. seq_len).
  *   err_flags        device uint32 (may be NULL): VECINFER_FLAG_* bits are OR-ed in.
  *   workspace        >= vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg, vcfg) bytes (0 for

@@ -301,8 +301,11 @@ def attention_decode_batch(q: np.ndarray, lam: np.ndarray, Ck: np.ndarray, Cv: n
 
 
 def pack_codes(codes: np.ndarray, code_bits: int) -> np.ndarray:
-    """Token-major packed rows: 8-bit one byte per code; 4-bit sub-vector 2i in the low nibble,
-    2i+1 in the high nibble; 16-bit little-endian u16.  codes: [..., M] -> uint8 [..., M*b/8]."""
+    """Token-major packed rows (reading R11): the M codes of a row form one little-endian bit
+    string, code m in bits [m*b, (m+1)*b) (bit i of the row = bit i%8 of byte i//8).  For b = 8
+    that is one byte per code, for b = 4 sub-vector 2i in the low nibble, for b = 16 little-endian
+    u16; b = 10 / 12 (d4b10, d8b12: P:338, 340, 993-999) are the same rule.  Row length
+    M*b/8 bytes.  codes: [..., M] -> uint8 [..., M*b/8]."""
     codes = np.asarray(codes, dtype=np.int64)
     if code_bits == 8:
         return codes.astype(np.uint8)
@@ -313,7 +316,40 @@ def pack_codes(codes: np.ndarray, code_bits: int) -> np.ndarray:
     if code_bits == 16:
         u = codes.astype(np.uint16)
         return u.view(np.uint8).reshape(*codes.shape[:-1], codes.shape[-1] * 2)
-    raise ValueError("code_bits must be 4, 8 or 16")
+    if code_bits not in (10, 12):
+        raise ValueError("code_bits must be 4, 8, 10, 12 or 16")
+    return pack_bitstream(codes, code_bits)
+
+
+def pack_bitstream(codes: np.ndarray, code_bits: int) -> np.ndarray:
+    """The R11 rule written bit by bit, for any b (pack_codes' 4/8/16-bit branches are its
+    special cases; tests/test_oracle_pins.py checks that they agree)."""
+    codes = np.asarray(codes, dtype=np.int64)
+    M = codes.shape[-1]
+    if (M * code_bits) % 8:
+        raise ValueError("a row of codes must fill whole bytes")
+    bits = np.zeros(codes.shape[:-1] + (M * code_bits,), dtype=np.uint8)
+    for m in range(M):                      # bit t of code m -> row bit m*b + t
+        for t in range(code_bits):
+            bits[..., m * code_bits + t] = (codes[..., m] >> t) & 1
+    out = np.zeros(codes.shape[:-1] + (M * code_bits // 8,), dtype=np.int64)
+    for i in range(8):
+        out |= bits[..., i::8].astype(np.int64) << i
+    return out.astype(np.uint8)
+
+
+def unpack_bitstream(packed: np.ndarray, code_bits: int) -> np.ndarray:
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    nbits = packed.shape[-1] * 8
+    bits = np.zeros(packed.shape[:-1] + (nbits,), dtype=np.int64)
+    for i in range(8):
+        bits[..., i::8] = (packed >> i) & 1
+    M = nbits // code_bits
+    out = np.zeros(packed.shape[:-1] + (M,), dtype=np.int64)
+    for m in range(M):
+        for t in range(code_bits):
+            out[..., m] |= bits[..., m * code_bits + t] << t
+    return out
 
 
 def unpack_codes(packed: np.ndarray, code_bits: int) -> np.ndarray:
@@ -329,7 +365,9 @@ def unpack_codes(packed: np.ndarray, code_bits: int) -> np.ndarray:
         return out
     if code_bits == 16:
         return packed.view(np.uint16).astype(np.int64)
-    raise ValueError("code_bits must be 4, 8 or 16")
+    if code_bits not in (10, 12):
+        raise ValueError("code_bits must be 4, 8, 10, 12 or 16")
+    return unpack_bitstream(packed, code_bits)
 
 
 def codebook_bytes(sub_dim: int, code_bits: int) -> int:

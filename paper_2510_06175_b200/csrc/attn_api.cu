@@ -31,10 +31,18 @@ int merge_mode_from_env() {
 constexpr int kMaxSplits = 128;
 constexpr int64_t kMinTokensPerSplit = 512;
 
-bool vq_ok(const vecinfer_vq_t& c) {
+bool vq_d4(const vecinfer_vq_t& c) {
   return (c.head_dim == 128 || c.head_dim == 64) && c.sub_dim == 4 &&
          (c.code_bits == 4 || c.code_bits == 8 || c.code_bits == 16);
 }
+// the paper's other configurations (NEXT-2): D = 128, d8b8, d8b12, d4b10, d2b8
+bool vq_next2(const vecinfer_vq_t& c) {
+  return c.head_dim == 128 && ((c.sub_dim == 8 && (c.code_bits == 8 || c.code_bits == 12)) ||
+                               (c.sub_dim == 4 && c.code_bits == 10) || (c.sub_dim == 2 && c.code_bits == 8));
+}
+bool vq_ok(const vecinfer_vq_t& c) { return vq_d4(c) || vq_next2(c); }
+// kernel format id: b for the d = 4 byte-aligned formats, else 100 d + b (attn_tiles.cuh)
+int fmt_id(const vecinfer_vq_t& c) { return vq_d4(c) ? c.code_bits : 100 * c.sub_dim + c.code_bits; }
 
 struct WsLayout {
   size_t part_o, part_l, counter, elem, total;
@@ -192,7 +200,14 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   const int32_t H_kv_real = H_kv;
   H_kv *= hsplit;                          // from here on: virtual KV heads
   if (!vq_ok(kcfg) || !vq_ok(vcfg))
-    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: supported configs are D in {64, 128}, d=4, code_bits in {4,8,16}");
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: supported configs are D in {64, 128} with d=4, code_bits in "
+                "{4,8,16}, and D = 128 d8b8 / d8b12 / d4b10 / d2b8");
+  const bool next2 = vq_next2(kcfg) || vq_next2(vcfg);
+  const int kf = fmt_id(kcfg), vf = fmt_id(vcfg);
+  if (next2 && (!attn_mma_supports(kf, vf, kcfg.head_dim) || algo == VECINFER_ATTN_LUT ||
+                algo == VECINFER_ATTN_DEQUANT_MMA_STREAM))
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: d8b8 / d8b12 / d4b10 / d2b8 run the split DEQUANT_MMA kernel for "
+                "the pairs (f, f), (d4b10, d8b12), (d8b12, d8b8)");
   if (kcfg.head_dim != vcfg.head_dim) return fail(VECINFER_ERR_SHAPE, "attn_decode: K and V head_dim differ");
   const int D = kcfg.head_dim;
   if (D == 64 && (algo == VECINFER_ATTN_LUT || algo == VECINFER_ATTN_DEQUANT_MMA_STREAM || res))
@@ -217,7 +232,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
       return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_paged: paged caches run the split DEQUANT_MMA kernel only");
     if (tok_begin % 32 != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode_paged: tok_begin must be a multiple of 32");
   }
-  const bool use_sk = !pg && D == 128 && use_stream(B, H_kv, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
+  const bool use_sk = !pg && !next2 && D == 128 && use_stream(B, H_kv, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
   SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
   if (D == 64) plan.cluster = 0;   // the DSMEM cluster merge is written for 128-dim rows
   const int32_t S = plan.S;
@@ -304,7 +319,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
     return check_launch("attn_decode (lut)");
   }
   const cudaError_t e = use_sk ? launch_attn_stream(a, kcfg.code_bits, vcfg.code_bits, st)
-                               : launch_attn_mma(a, kcfg.code_bits, vcfg.code_bits, st);
+                               : launch_attn_mma(a, kf, vf, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(VECINFER_ERR_CUDA, "attn_decode: launch failed: %s", cudaGetErrorString(e));
@@ -358,6 +373,7 @@ extern "C" vecinfer_status_t vecinfer_attn_decode_paged(const void* q_bf16, int3
 static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
                          int32_t num_splits, vecinfer_attn_algo_t algo, bool paged = false) {
   if (algo == VECINFER_ATTN_LUT || kcfg.code_bits > 8 || vcfg.code_bits > 8 || B <= 0 || H_kv <= 0) return false;
+  if (vq_next2(kcfg) || vq_next2(vcfg)) return false;   // NEXT-2 formats: separate encode launch
   if (kcfg.head_dim != 128) return false;   // the fused encode is written for 128-dim keys
   const int64_t units = static_cast<int64_t>(B) * H_kv;
   if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)

@@ -324,6 +324,7 @@ __device__ __forceinline__ void query_transform_warp(const AttnArgs& a, int b, i
 }
 
 cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
+bool attn_mma_supports(int kfmt, int vfmt, int dh);   // a split kernel exists for the format pair
 cudaError_t launch_attn_stream(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);
 int attn_mma_max_active_clusters(int cluster_size);  // 0 if not schedulable
 void launch_attn_lut(const AttnArgs& a, int kbits, int vbits, cudaStream_t st);

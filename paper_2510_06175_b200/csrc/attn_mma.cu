@@ -40,7 +40,7 @@ constexpr int kSmemBytes = 65536 + kTab + kCbufBytes + 1024;  // pad + table + c
 // codebook gathers
 constexpr int kSmemBytesNoTab = kMiscBytes + 1024 + kCbufBytes + 1024;
 template <int KB, int VB>
-constexpr int smem_bytes() { return (KB > 8 && VB > 8) ? kSmemBytesNoTab : kSmemBytes; }
+constexpr int smem_bytes() { return (!Fmt<KB>::kSmem && !Fmt<VB>::kSmem) ? kSmemBytesNoTab : kSmemBytes; }
 
 
 template <int KB, int VB, int DH>
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   using FV = FmtD<VB, DH>;
   constexpr int KR = FK::kRow, VR = FV::kRow;
   constexpr int KS = DH / 16, VS = DH / 32, NL = DH / 4;
-  constexpr bool kCanAppend = KB <= 8 && VB <= 8 && DH == 128;
+  constexpr bool kCanAppend = Fmt<KB>::kSmem && Fmt<VB>::kSmem && DH == 128;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   // shared layout: misc at the bottom, the codebook table at the next 64 KiB boundary
   const uint32_t raw_s = smem_u32(smem_raw);
   uint32_t tab_off;
-  if constexpr (KB > 8 && VB > 8) {
+  if constexpr (!Fmt<KB>::kSmem && !Fmt<VB>::kSmem) {
     tab_off = (kMiscBytes + 1023) & ~1023;   // no table: the "table" base only anchors the cluster buffer
   } else {
     tab_off = ((raw_s + 65535u) & ~65535u) - raw_s;
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
     cluster_wait();   // every CTA of the cluster has started: DSMEM of the leader is valid
     const uint32_t rank = cluster_ctarank();
-    float* cbuf = reinterpret_cast<float*>(tab + ((KB > 8 && VB > 8) ? 0 : kTab));   // [16][4][128] acc, [16][4] M, l
+    float* cbuf = reinterpret_cast<float*>(tab + ((!Fmt<KB>::kSmem && !Fmt<VB>::kSmem) ? 0 : kTab));   // [16][4][128] acc, [16][4] M, l
     float* cM = cbuf + kClusterMax * 4 * 128;
     float* cL = cM + kClusterMax * 4;
     const uint32_t cb_s = smem_u32(cbuf);
@@ -516,10 +516,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
 using AttnKernel = void (*)(const AttnArgs);
 
-static int smem_for(int kb, int vb) { return (kb > 8 && vb > 8) ? kSmemBytesNoTab : kSmemBytes; }
+static bool has_table(int f) { return f == 4 || f == 8; }
+static int smem_for(int kf, int vf) { return (!has_table(kf) && !has_table(vf)) ? kSmemBytesNoTab : kSmemBytes; }
 
-static AttnKernel kernel_for(int kb, int vb, int dh = 128) {
-  const int ki = kb == 4 ? 0 : kb == 8 ? 1 : 2, vi = vb == 4 ? 0 : vb == 8 ? 1 : 2;
+// the NEXT-2 (K, V) format pairs with a kernel: each format with itself and the paper's mixed
+// configurations K-d4b10 / V-d8b12 (2-bit) and K-d8b12 / V-d8b8 (1.25-bit), Table 3 / P:993-999
+#define VECINFER_NEXT2_PAIRS(X)                                                   \
+  X(kFmtD8B8, kFmtD8B8) X(kFmtD8B12, kFmtD8B12) X(kFmtD4B10, kFmtD4B10)           \
+  X(kFmtD2B8, kFmtD2B8) X(kFmtD4B10, kFmtD8B12) X(kFmtD8B12, kFmtD8B8)
+
+static AttnKernel kernel_for(int kf, int vf, int dh = 128) {
+#define VECINFER_PAIR(K, V) \
+  if (kf == K && vf == V) return dh == 128 ? attn_mma_kernel<K, V, 128> : nullptr;
+  VECINFER_NEXT2_PAIRS(VECINFER_PAIR)
+#undef VECINFER_PAIR
+  const int ki = kf == 4 ? 0 : kf == 8 ? 1 : kf == 16 ? 2 : -1, vi = vf == 4 ? 0 : vf == 8 ? 1 : vf == 16 ? 2 : -1;
+  if (ki < 0 || vi < 0) return nullptr;
   static const AttnKernel table[2][3][3] = {
       {{attn_mma_kernel<4, 4, 128>, attn_mma_kernel<4, 8, 128>, attn_mma_kernel<4, 16, 128>},
        {attn_mma_kernel<8, 4, 128>, attn_mma_kernel<8, 8, 128>, attn_mma_kernel<8, 16, 128>},
@@ -530,18 +542,25 @@ static AttnKernel kernel_for(int kb, int vb, int dh = 128) {
   return table[dh == 64 ? 1 : 0][ki][vi];
 }
 
+static void set_attr(AttnKernel k, int smem) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
+
 static void set_attrs_once() {
   static bool done = false;  // benign race: idempotent attributes
   if (!done) {
     for (int dh : {128, 64})
       for (int kb : {4, 8, 16})
-        for (int vb : {4, 8, 16}) {
-          cudaFuncSetAttribute(kernel_for(kb, vb, dh), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(kb, vb));
-          cudaFuncSetAttribute(kernel_for(kb, vb, dh), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        }
+        for (int vb : {4, 8, 16}) set_attr(kernel_for(kb, vb, dh), smem_for(kb, vb));
+#define VECINFER_PAIR(K, V) set_attr(kernel_for(K, V), smem_for(K, V));
+    VECINFER_NEXT2_PAIRS(VECINFER_PAIR)
+#undef VECINFER_PAIR
     done = true;
   }
 }
+
+bool attn_mma_supports(int kfmt, int vfmt, int dh) { return kernel_for(kfmt, vfmt, dh) != nullptr; }
 
 int attn_mma_max_active_clusters(int cluster_size) {
   static int cache[kClusterMax + 1] = {0};
@@ -570,6 +589,7 @@ int attn_mma_max_active_clusters(int cluster_size) {
 }
 
 cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_t st) {
+  // kbits / vbits: format ids (b for d = 4, else 100d + b)
   set_attrs_once();
   cudaLaunchConfig_t cfg = {};
   if (a.cluster) {

@@ -11,6 +11,14 @@ constexpr int kThreads = kNW * 32;
 constexpr float kTau = 8.0f;       // lazy-rescale threshold (log2 units): p <= 2^8
 constexpr int kTab = 65536;        // [256 centroids][256 B] codebook table, 64 KiB-aligned
 
+// bf16x4 centroid (global) -> fp16x4 MMA operand pair (exact for |c| in the fp16 normal range)
+__device__ __forceinline__ uint2 bf16x4_to_f16x4(uint2 w) {
+  uint2 e;
+  e.x = pack_half2(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u));
+  e.y = pack_half2(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+  return e;
+}
+
 // ---- code-width traits.  Per lane and token: the K chunk holds sub-vectors 8j..8j+7 (score MMA
 // k-steps), the V chunk sub-vectors 4r..4r+3 (P.V m-tiles).  4/8-bit codebooks are gathered from the
 // shared table (rows of 256 B: [16 K replicas | 16 V replicas]); 16-bit codebooks (65536 x 4 bf16 =
@@ -18,7 +26,7 @@ constexpr int kTab = 65536;        // [256 centroids][256 B] codebook table, 64 
 template <int BITS> struct Fmt;
 template <> struct Fmt<8> {
   static constexpr int kRow = 32, kOffK = 8, kOffV = 4;
-  static constexpr bool kSmem = true;
+  static constexpr bool kSmem = true, kGeneric = false;
   using K = uint2;
   using V = uint32_t;
   static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u64(p); }
@@ -34,7 +42,7 @@ template <> struct Fmt<8> {
 };
 template <> struct Fmt<4> {
   static constexpr int kRow = 16, kOffK = 4, kOffV = 2;
-  static constexpr bool kSmem = true;
+  static constexpr bool kSmem = true, kGeneric = false;
   using K = uint32_t;
   using V = uint32_t;   // low 16 bits
   static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u32(p); }
@@ -48,7 +56,7 @@ template <> struct Fmt<4> {
 };
 template <> struct Fmt<16> {
   static constexpr int kRow = 64, kOffK = 16, kOffV = 8;
-  static constexpr bool kSmem = false;
+  static constexpr bool kSmem = false, kGeneric = false;
   using K = uint4;
   using V = uint2;
   static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u128(p); }
@@ -63,6 +71,84 @@ template <> struct Fmt<16> {
     return (U & 1) ? (w >> 16) : (w & 0xFFFFu);
   }
 };
+
+// ---- the paper's other configurations (NEXT-2), D = 128: d-dim
+// sub-vectors with b-bit codes, rows = one little-endian bit string (code m in bits [mb, mb+b),
+// reading R11).  The kernels keep their 4-dim "virtual sub-vector" view (one gather = one MMA
+// fragment pair): lane j's K chunk is dims 32j..32j+31 (32b/d bits at byte 4jb/d), lane r's V
+// chunk dims 16r..16r+15.  Virtual sub-vector T of a chunk is half T&1 of code T/2 (d = 8), code T
+// (d = 4) or codes 2T, 2T+1 (d = 2).  Codebooks (bf16, <= 64 KiB) are gathered from global memory
+// through L1 like the 16-bit ones.  Format ids: d = 4 keeps id = b (4, 8, 16); else 100d + b.
+template <int NB, int AL>
+__device__ __forceinline__ void load_chunk(const uint8_t* p, uint32_t* w) {
+  // NB bytes at an AL-aligned address -> little-endian words w[0..(NB+3)/4)
+  if constexpr (AL >= 16 && NB == 16) {
+    const uint4 v = ldg_nc_u128(p);
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+  } else if constexpr (AL >= 8 && NB == 8) {
+    const uint2 v = ldg_nc_u64(p);
+    w[0] = v.x; w[1] = v.y;
+  } else if constexpr (AL >= 4 && NB % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < NB / 4; ++i) w[i] = ldg_ro_u32(p + 4 * i);
+  } else if constexpr (AL >= 2 && NB % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < (NB + 3) / 4; ++i) w[i] = 0u;
+#pragma unroll
+    for (int i = 0; i < NB / 2; ++i) w[i >> 1] |= ldg_ro_u16(p + 2 * i) << (16 * (i & 1));
+  } else {
+#pragma unroll
+    for (int i = 0; i < (NB + 3) / 4; ++i) w[i] = 0u;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) w[i >> 2] |= ldg_ro_u8(p + i) << (8 * (i & 3));
+  }
+}
+
+template <int SUB, int BITS>
+struct FmtG {
+  static constexpr int kRow = 128 / SUB * BITS / 8;        // bytes per cached row
+  static constexpr int kOffK = 32 / SUB * BITS / 8;        // K chunk bytes (= lane stride)
+  static constexpr int kOffV = 16 / SUB * BITS / 8;        // V chunk bytes
+  static constexpr bool kSmem = false, kGeneric = true;
+  static_assert(kOffV * 8 == 16 / SUB * BITS, "V chunk must be whole bytes");
+  static constexpr int kRowAl = (kRow % 16 == 0) ? 16 : (kRow % 8 == 0) ? 8 : 4;
+  static constexpr int gcd(int x, int y) { return y == 0 ? x : gcd(y, x % y); }
+  struct K { uint32_t w[(kOffK + 3) / 4]; };
+  struct V { uint32_t w[(kOffV + 3) / 4]; };
+  static __device__ __forceinline__ K ldk(const uint8_t* p) {
+    K c;
+    load_chunk<kOffK, gcd(kOffK, kRowAl)>(p, c.w);
+    return c;
+  }
+  static __device__ __forceinline__ V ldv(const uint8_t* p) {
+    V c;
+    load_chunk<kOffV, gcd(kOffV, kRowAl)>(p, c.w);
+    return c;
+  }
+  static __device__ __forceinline__ K zk() { return K{}; }
+  template <int I, int NW> static __device__ __forceinline__ uint32_t code(const uint32_t (&w)[NW]) {
+    constexpr int p = I * BITS, wi = p / 32, sh = p % 32;
+    uint32_t x = w[wi] >> sh;
+    if constexpr (sh + BITS > 32) x |= w[wi + 1] << (32 - sh);
+    return x & ((1u << BITS) - 1u);
+  }
+  // fp16x4 operand pair of virtual sub-vector T of a chunk (codebook cb: bf16 [2^b][SUB])
+  template <int T, int NW> static __device__ __forceinline__ uint2 gather(const uint32_t (&w)[NW], const uint16_t* cb) {
+    if constexpr (SUB == 8) {
+      return bf16x4_to_f16x4(ldg_ro_u64(cb + 8 * code<T / 2>(w) + 4 * (T & 1)));
+    } else if constexpr (SUB == 4) {
+      return bf16x4_to_f16x4(ldg_ro_u64(cb + 4 * code<T>(w)));
+    } else {
+      return bf16x4_to_f16x4(make_uint2(ldg_ro_u32(cb + 2 * code<2 * T>(w)), ldg_ro_u32(cb + 2 * code<2 * T + 1>(w))));
+    }
+  }
+};
+constexpr int kFmtD8B8 = 808, kFmtD8B12 = 812, kFmtD4B10 = 410, kFmtD2B8 = 208;
+template <> struct Fmt<kFmtD8B8> : FmtG<8, 8> {};
+template <> struct Fmt<kFmtD8B12> : FmtG<8, 12> {};
+template <> struct Fmt<kFmtD4B10> : FmtG<4, 10> {};
+template <> struct Fmt<kFmtD2B8> : FmtG<2, 8> {};
+
 template <int BITS> using KCode = typename Fmt<BITS>::K;
 template <int BITS> using VCode = typename Fmt<BITS>::V;
 
@@ -89,22 +175,17 @@ template <> struct FmtD<16, 64> : Fmt<16> {
   static __device__ __forceinline__ uint2 ldv(const uint8_t* p) { return make_uint2(ldg_nc_u32(p), 0u); }
 };
 
-// bf16x4 centroid (global) -> fp16x4 MMA operand pair (exact for |c| in the fp16 normal range)
-__device__ __forceinline__ uint2 bf16x4_to_f16x4(uint2 w) {
-  uint2 e;
-  e.x = pack_half2(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u));
-  e.y = pack_half2(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
-  return e;
-}
 
 template <int KB, int T>
 __device__ __forceinline__ uint2 gather_k(const KCode<KB>& c, uint32_t kbase, const uint16_t* cbk) {
   if constexpr (Fmt<KB>::kSmem) return lds_u64(Fmt<KB>::template kaddr<T>(c, kbase));
+  else if constexpr (Fmt<KB>::kGeneric) return Fmt<KB>::template gather<T>(c.w, cbk);
   else return bf16x4_to_f16x4(ldg_ro_u64(cbk + 4 * Fmt<KB>::template kidx<T>(c)));
 }
 template <int VB, int U>
 __device__ __forceinline__ uint2 gather_v(const VCode<VB>& c, uint32_t vbase, const uint16_t* cbv) {
   if constexpr (Fmt<VB>::kSmem) return lds_u64(Fmt<VB>::template vaddr<U>(c, vbase));
+  else if constexpr (Fmt<VB>::kGeneric) return Fmt<VB>::template gather<U>(c.w, cbv);
   else return bf16x4_to_f16x4(ldg_ro_u64(cbv + 4 * Fmt<VB>::template vidx<U>(c)));
 }
 
@@ -113,7 +194,7 @@ __device__ __forceinline__ void fill_tables(unsigned char* tab, const uint16_t* 
   // thread t: centroid j = t/2 of C_k (t even) or C_v (t odd); 16 replicas = 8 x 16-byte stores,
   // rotated so that the 8 threads of a quarter-warp hit 8 different bank groups
   const int j = tid >> 1, which = tid & 1;
-  const int n = which ? (VB <= 8 ? (1 << VB) : 0) : (KB <= 8 ? (1 << KB) : 0);
+  const int n = which ? (Fmt<VB>::kSmem ? (1 << (VB & 15)) : 0) : (Fmt<KB>::kSmem ? (1 << (KB & 15)) : 0);
   if (j >= n) return;
   const uint16_t* src = (which ? cv : ck) + 4 * j;
   const uint2 e = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(src));

@@ -118,6 +118,24 @@ __device__ __forceinline__ uint2 ldg_ro_u64(const void* p) {
   return v;
 }
 
+// read-only loads that may allocate in L1 (sub-word code chunks of the NEXT-2 formats: the bytes
+// of one chunk are fetched by several loads, the first brings the sector into L1)
+__device__ __forceinline__ uint32_t ldg_ro_u8(const void* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return static_cast<uint32_t>(v);
+}
+__device__ __forceinline__ uint32_t ldg_ro_u16(const void* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return static_cast<uint32_t>(v);
+}
+__device__ __forceinline__ uint32_t ldg_ro_u32(const void* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 // compile-time unrolled loop: f(std::integral_constant<int, I>) for I in [B, E)
 template <int B, int E, typename F>
 __device__ __forceinline__ void static_for(F&& f) {

@@ -30,6 +30,7 @@ struct EncArgs {
   const uint16_t* cv;
   int64_t ck_hs, cv_hs;
   int kbits, vbits;
+  int ksub, vsub;             // sub-vector dims (4; NEXT-2 formats: 8 / 4 / 2)
   uint8_t* kcodes;
   uint8_t* vcodes;
   int64_t n_cap;
@@ -296,10 +297,79 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_finalize(EncArgs a
   }
 }
 
-bool vq_supported(const vecinfer_vq_t& c) {
+// ------------------------------------------------------------------ NEXT-2 formats
+// d8b8 / d8b12 / d4b10 / d2b8, D = 128.  One CTA of 256 threads
+// per (token-head, K or V): warp 0 produces the row (key: the pinned smooth + integer FWHT above;
+// value: raw) into shared memory; for each sub-vector m every thread scans centroids j = tid,
+// tid + 256, ... with the pinned distance (fp32, RN, no FMA, summed left to right over the d
+// dims: reading R9), minima travel as (dist_bits << 32 | j) -- dist >= 0, so the minimum is the
+// nearest centroid with the lowest index on ties.  The codes are then packed into the row's
+// little-endian bit string (code m in bits [m b, m b + b), reading R11).
+constexpr int kGenThreads = 256;
+
+__global__ void __launch_bounds__(kGenThreads) encode_generic_kernel(EncArgs a) {
+  __shared__ __align__(16) float xs[128];
+  __shared__ unsigned long long best[64];
+  griddep_launch_dependents();
+  const int which = blockIdx.z, h = blockIdx.y;
+  const int64_t bt = blockIdx.x;
+  const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = which ? a.vsub : a.ksub, bits = which ? a.vbits : a.kbits;
+  const int M = 128 / sub, n_ent = 1 << bits;
+  const uint16_t* cb = which ? (a.cv + h * a.cv_hs) : (a.ck + h * a.ck_hs);
+  if (tid < 64) best[tid] = ~0ull;
+  griddep_wait();
+  int64_t row;
+  if (!cache_row(a, b, t, h, lane, row)) return;   // uniform over the CTA
+  if (warp == 0) {
+    float x[4];
+    if (which == 0) transform_key_lane(a, b, t, h, lane, x);
+    else load_value_lane(a, b, t, h, lane, x);
+    *reinterpret_cast<float4*>(xs + 4 * lane) = make_float4(x[0], x[1], x[2], x[3]);
+  }
+  __syncthreads();
+  for (int m = 0; m < M; ++m) {
+    const float* xm = xs + m * sub;
+    unsigned long long key = ~0ull;
+    for (int j = tid; j < n_ent; j += kGenThreads) {
+      const uint16_t* c = cb + static_cast<int64_t>(j) * sub;
+      float e = __fsub_rn(xm[0], __uint_as_float(static_cast<uint32_t>(c[0]) << 16));
+      float dsum = __fmul_rn(e, e);
+      for (int u = 1; u < sub; ++u) {
+        e = __fsub_rn(xm[u], __uint_as_float(static_cast<uint32_t>(c[u]) << 16));
+        dsum = __fadd_rn(dsum, __fmul_rn(e, e));
+      }
+      const unsigned long long k = (static_cast<unsigned long long>(__float_as_uint(dsum)) << 32) | static_cast<uint32_t>(j);
+      key = k < key ? k : key;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, off);
+      key = o < key ? o : key;
+    }
+    if (lane == 0) atomicMin(&best[m], key);
+  }
+  __syncthreads();
+  const int rb = M * bits / 8;
+  uint8_t* dst = (which ? a.vcodes : a.kcodes) + row * rb;
+  for (int i = tid; i < rb; i += kGenThreads) {   // byte i = row bits [8i, 8i + 8): <= 2 codes (b >= 8)
+    const int p = 8 * i, c0 = p / bits, off = p - c0 * bits;
+    uint32_t w = static_cast<uint32_t>(best[c0] & 0xFFFFFFFFull);
+    if (c0 + 1 < M) w |= static_cast<uint32_t>(best[c0 + 1] & 0xFFFFFFFFull) << bits;
+    dst[i] = static_cast<uint8_t>(w >> off);
+  }
+}
+
+bool vq_d4(const vecinfer_vq_t& c) {
   return (c.head_dim == 128 || c.head_dim == 64) && c.sub_dim == 4 &&
          (c.code_bits == 4 || c.code_bits == 8 || c.code_bits == 16);
 }
+bool vq_next2(const vecinfer_vq_t& c) {
+  return c.head_dim == 128 && ((c.sub_dim == 8 && (c.code_bits == 8 || c.code_bits == 12)) ||
+                               (c.sub_dim == 4 && c.code_bits == 10) || (c.sub_dim == 2 && c.code_bits == 8));
+}
+bool vq_supported(const vecinfer_vq_t& c) { return vq_d4(c) || vq_next2(c); }
 
 }  // namespace
 }  // namespace vecinfer
@@ -325,7 +395,8 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
     return fail(VECINFER_ERR_INVALID_ARG, "encode_kv: NULL pointer");
   if (B <= 0 || T <= 0 || H_kv <= 0 || n_cap <= 0) return fail(VECINFER_ERR_SHAPE, "encode_kv: non-positive size");
   if (!vq_supported(kcfg) || !vq_supported(vcfg))
-    return fail(VECINFER_ERR_UNSUPPORTED, "encode_kv: supported configs are D in {64, 128}, d=4, code_bits in {4,8,16}");
+    return fail(VECINFER_ERR_UNSUPPORTED, "encode_kv: supported configs are D in {64, 128} with d=4, code_bits in "
+                "{4,8,16}, and D = 128 d8b8 / d8b12 / d4b10 / d2b8");
   if (kcfg.head_dim != vcfg.head_dim) return fail(VECINFER_ERR_SHAPE, "encode_kv: K and V head_dim differ");
   if (!aligned(k_bf16, 8) || !aligned(v_bf16, 8) || !aligned(inv_lambda, 16) || !aligned(ck_bf16, 8) ||
       !aligned(cv_bf16, 8) || !aligned(k_codes, 2) || !aligned(v_codes, 2))
@@ -346,6 +417,7 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
   a.cv = static_cast<const uint16_t*>(cv_bf16);
   a.ck_hs = ck_head_stride; a.cv_hs = cv_head_stride;
   a.kbits = kcfg.code_bits; a.vbits = vcfg.code_bits;
+  a.ksub = kcfg.sub_dim; a.vsub = vcfg.sub_dim;
   a.kcodes = k_codes; a.vcodes = v_codes;
   a.n_cap = n_cap; a.write_pos = write_pos; a.err = err_flags;
   a.bt = nullptr; a.bt_stride = 0; a.page_shift = 0; a.n_pages = 0;
@@ -364,6 +436,13 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
   const int64_t gx = (nbt + kEncWarps - 1) / kEncWarps;
   if (gx > 2147483647) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many tokens");
   if (H_kv > 65535) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many heads");
+  if (vq_next2(kcfg) || vq_next2(vcfg)) {   // one generic launch encodes both streams
+    if (nbt > 2147483647) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many tokens");
+    const cudaError_t e = launch_pdl(encode_generic_kernel, dim3(static_cast<unsigned>(nbt), H_kv, 2),
+                                     dim3(kGenThreads), 0, st, a);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_generic_kernel: %s", cudaGetErrorString(e)); }
+    return check_launch("encode_generic_kernel");
+  }
   if (kcfg.code_bits == 16 || vcfg.code_bits == 16) {
     const size_t need = vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg, vcfg);
     if (!workspace || workspace_bytes < need || !aligned(workspace, 8))

@@ -7,6 +7,7 @@ import synth
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CODEBOOKS = os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz")
+CODEBOOKS_NEXT2 = os.path.join(ROOT, "data", "next2_codebooks.npz")   # d8b8, d8b12, d4b10, d2b8
 
 # north_star: outputs within 2e-3 max-abs relative error (bf16 I/O, fp32 accumulation);
 # measured per (b, h_q) row on the fp32 output (reading R13)
@@ -19,9 +20,13 @@ def load_codebooks():
     as bf16-exact float32 arrays."""
     z = np.load(CODEBOOKS)
     out = {"lambda": z["lambda"], "inv_lambda": z["inv_lambda"]}
-    for k in z.files:
-        if k.startswith("ck_") or k.startswith("cv_"):
-            out[k] = synth.bf16_from_bits(z[k])
+    for path in (CODEBOOKS, CODEBOOKS_NEXT2):
+        if not os.path.exists(path):
+            continue
+        z = np.load(path)
+        for k in z.files:
+            if k.startswith("ck_") or k.startswith("cv_"):
+                out[k] = synth.bf16_from_bits(z[k])
     return out
 
 

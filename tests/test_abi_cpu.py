@@ -65,12 +65,12 @@ def test_argument_validation_without_cuda(lib):
     st = lib.vecinfer_calibrate_smooth(ctypes.c_void_p(16), 5, 8, 128, 1024, 128, 0.0, ctypes.c_void_p(16),
                                        ctypes.c_void_p(16), ctypes.c_void_p(256), 1 << 20, None)
     assert st == 1     # eps <= 0
-    bad = VQ(128, 8, 8)
+    bad = VQ(128, 16, 8)   # d = 16: no kernel (d8b8 / d8b12 / d4b10 / d2b8 are NEXT-2 formats)
     st = lib.vecinfer_encode_kv(ctypes.c_void_p(256), ctypes.c_void_p(256), 1, 1, 8, I64x3(0, 1024, 128),
                                 I64x3(0, 1024, 128), ctypes.c_void_p(256), ctypes.c_void_p(256), ctypes.c_void_p(256),
                                 0, 0, bad, cfg, ctypes.c_void_p(256), ctypes.c_void_p(256), 16, ctypes.c_void_p(256),
                                 None, None, 0, None)
-    assert st == 3     # UNSUPPORTED (d = 8)
+    assert st == 3     # UNSUPPORTED (d = 16)
     assert lib.vecinfer_status_string(3) == b"VECINFER_ERR_UNSUPPORTED"
 
 

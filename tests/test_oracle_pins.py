@@ -415,6 +415,71 @@ def test_pack_roundtrip_and_order(bits):
         assert packed[0, 0, 0] == codes[0, 0, 0] & 0xFF and packed[0, 0, 1] == codes[0, 0, 0] >> 8
 
 
+def test_pack_bitstream_hand_examples():
+    """Reading R11 for non-byte-aligned codes, worked by hand: b = 10 codes 0x3FF, 0x001, 0x155,
+    0x2AA occupy row bits 0-9, 10-19, 20-29, 30-39 -> bytes FF 07 50 95 AA; b = 12 codes 0xABC,
+    0x123 -> the 24-bit value 0x123ABC little-endian -> BC 3A 12."""
+    assert ref.pack_codes(np.array([[0x3FF, 0x001, 0x155, 0x2AA]]), 10).tolist() == [[0xFF, 0x07, 0x50, 0x95, 0xAA]]
+    assert ref.pack_codes(np.array([[0xABC, 0x123]]), 12).tolist() == [[0xBC, 0x3A, 0x12]]
+    assert ref.unpack_codes(np.array([[0xBC, 0x3A, 0x12]], np.uint8), 12).tolist() == [[0xABC, 0x123]]
+
+
+@pytest.mark.parametrize("bits", [4, 8, 16])
+def test_pack_byte_widths_are_the_bitstream(bits):
+    """The 4/8/16-bit branches of pack_codes (written separately) are special cases of the
+    bit-by-bit rule (same bytes both ways)."""
+    codes = np.random.default_rng(40 + bits).integers(0, 1 << bits, (4, 32))
+    assert np.array_equal(ref.pack_codes(codes, bits), ref.pack_bitstream(codes, bits))
+    assert np.array_equal(ref.unpack_bitstream(ref.pack_codes(codes, bits), bits), codes)
+
+
+@pytest.mark.parametrize("sub_dim,bits", [(4, 10), (8, 12), (8, 8), (2, 8)])
+def test_pack_roundtrip_next2_formats(sub_dim, bits):
+    """d4b10 / d8b12 / d8b8 / d2b8 rows: M = 128/d codes, M*b/8 bytes
+    (P:143), lossless."""
+    M = 128 // sub_dim
+    codes = np.random.default_rng(sub_dim * bits).integers(0, 1 << bits, (3, 2, M))
+    packed = ref.pack_codes(codes, bits)
+    assert packed.shape[-1] == ref.index_bytes_per_vector(128, sub_dim, bits)
+    assert np.array_equal(ref.unpack_codes(packed, bits), codes)
+    extremes = np.full((1, M), (1 << bits) - 1)
+    assert np.all(ref.pack_codes(extremes, bits) == 0xFF) and np.all(ref.pack_codes(0 * extremes, bits) == 0)
+
+
+@pytest.mark.parametrize("sub_dim,n_levels", [(8, 2), (2, 16), (8, 3)])
+def test_encode_product_grid_other_sub_dims(sub_dim, n_levels):
+    """Eq. 2 with d = 8 (2^8 and 3^8 = 6561 entries) and d = 2 (16^2): the separable closed form
+    of test_encode_product_grid_closed_form at the other sub-vector sizes."""
+    cb = synth.product_grid_codebook(n_levels, sub_dim, step=0.5)
+    n = 400
+    X = synth.dyadic_points(n, sub_dim, n_levels, 0.5, seed=sub_dim * 7 + n_levels)
+    lv = synth.grid_levels(n_levels, 0.5)
+    dist = np.abs(X[:, :, None].astype(np.float64) - lv[None, None, :])
+    digit = np.argmin(dist, axis=2)
+    want = (digit * (n_levels ** np.arange(sub_dim))[None, :]).sum(1)
+    got = ref.vq_encode(X.reshape(n, sub_dim), cb)[:, 0]
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dk,nk,dv,nv", [(8, 4096, 8, 256), (4, 1024, 2, 256)])
+def test_vq_attention_identity_other_formats(dk, nk, dv, nv):
+    """The exhaustive-codebook identity pin at K-d8b12 / V-d8b8 and K-d4b10 / V-d2b8 (Table 3
+    mixed configurations): Eq. 10 over codes = Eq. 1 over the reconstructed keys."""
+    rng = np.random.default_rng(dk * 100 + dv)
+    D, N, G = 128, 150, 4
+    Ck = synth.gen_codebook(nk, dk, seed=15)
+    Cv = synth.gen_codebook(nv, dv, seed=16)
+    kc = rng.integers(0, nk, (N, D // dk))
+    vc = rng.integers(0, nv, (N, D // dv))
+    lam = np.exp(rng.uniform(-1, 1, D))
+    q = rng.standard_normal((G, D))
+    K_orig = ref.vq_decode(kc, Ck) @ ref.hadamard(D).T * lam[None]
+    o1, L1 = ref.attention_vq(q, lam, Ck, Cv, kc, vc)
+    o2, L2 = ref.attention_full(q, K_orig, ref.vq_decode(vc, Cv))
+    assert np.max(np.abs(o1 - o2)) <= 1e-10 * np.max(np.abs(o2))
+    assert np.max(np.abs(L1 - L2)) <= 1e-10 * np.max(np.abs(L2))
+
+
 # ------------------------------------------------------------------------- k-means (harness)
 def test_kmeans_examples(golden):
     ex = golden["kmeans_example"]
