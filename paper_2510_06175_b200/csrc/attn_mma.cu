@@ -40,7 +40,7 @@ constexpr int kSmemBytes = 65536 + kTab + kCbufBytes + 1024;  // pad + table + c
 // codebook gathers
 constexpr int kSmemBytesNoTab = kMiscBytes + 1024 + kCbufBytes + 1024;
 template <int KB, int VB>
-constexpr int smem_bytes() { return (!Fmt<KB>::kSmem && !Fmt<VB>::kSmem) ? kSmemBytesNoTab : kSmemBytes; }
+constexpr int smem_bytes() { return (!Fmt<KB>::kSmem && !Fmt<VB>::kSmem) ? kSmemBytesNoTab : kSmemBytes; }   // (== smem_for)
 
 
 template <int KB, int VB, int DH>
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   using FV = FmtD<VB, DH>;
   constexpr int KR = FK::kRow, VR = FV::kRow;
   constexpr int KS = DH / 16, VS = DH / 32, NL = DH / 4;
-  constexpr bool kCanAppend = Fmt<KB>::kSmem && Fmt<VB>::kSmem && DH == 128;
+  constexpr bool kCanAppend = KB <= 8 && VB <= 8 && DH == 128;   // d = 4, 4/8-bit codebooks
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
@@ -252,8 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
   }
 
-  const uint32_t kbase = tab_s + (lane & 15) * 8;
-  const uint32_t vbase = kbase + 128;
+  const uint32_t kbase = tab_s + table_lane_off<KB>(lane);
+  const uint32_t vbase = tab_s + 128 + table_lane_off<VB>(lane);
 
   float acc[2 * VS][4];
 #pragma unroll
@@ -364,13 +364,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-      static_for<0, KS>([&](auto T) {
-        constexpr int t = decltype(T)::value;
-        const uint2 ea = gather_k<KB, t>(cur.k[q][0], kbase, cbk);
-        const uint2 eb = gather_k<KB, t>(cur.k[q][1], kbase, cbk);
-        if (t < KS / 2) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
-        else mma_16816(d1, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
-      });
+      if constexpr (Fmt<KB>::kWide) {   // d8b8: one 16-byte gather = virtual sub-vectors 2i, 2i+1
+        static_for<0, KS / 2>([&](auto I) {
+          constexpr int i = decltype(I)::value, t = 2 * i;
+          const uint4 wa = lds_u128(Fmt<KB>::template kaddr<i>(cur.k[q][0], kbase));
+          const uint4 wb = lds_u128(Fmt<KB>::template kaddr<i>(cur.k[q][1], kbase));
+          if (t < KS / 2) {
+            mma_16816(d0, wa.x, wb.x, wa.y, wb.y, bq0[t], bq1[t]);
+            mma_16816(d0, wa.z, wb.z, wa.w, wb.w, bq0[t + 1], bq1[t + 1]);
+          } else {
+            mma_16816(d1, wa.x, wb.x, wa.y, wb.y, bq0[t], bq1[t]);
+            mma_16816(d1, wa.z, wb.z, wa.w, wb.w, bq0[t + 1], bq1[t + 1]);
+          }
+        });
+      } else {
+        static_for<0, KS>([&](auto T) {
+          constexpr int t = decltype(T)::value;
+          const uint2 ea = gather_k<KB, t>(cur.k[q][0], kbase, cbk);
+          const uint2 eb = gather_k<KB, t>(cur.k[q][1], kbase, cbk);
+          if (t < KS / 2) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
+          else mma_16816(d1, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
+        });
+      }
       sc[q][0] = (d0[0] + d1[0]) + (d0[1] + d1[1]);
       sc[q][1] = (d0[2] + d1[2]) + (d0[3] + d1[3]);
     }
@@ -417,17 +432,31 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       const uint32_t bp1 = movmatrix_trans(prmt(hb, lb, 0x7632));  // (hi, lo) of token r + 8
 
       // ---- P.V (Alg. 1 l.16): m-tile t <-> sub-vector VS*r + t/2, components 2(t%2) + {0,1}
-      static_for<0, VS>([&](auto U) {
+      auto pv = [&](auto U, const uint2& g0, const uint2& g1, const uint2& g2, const uint2& g3) {
         constexpr int u = decltype(U)::value;
-        const uint2 g0 = gather_v<VB, u>(cur.v[q][0], vbase, cbv);
-        const uint2 g1 = gather_v<VB, u>(cur.v[q][1], vbase, cbv);
-        const uint2 g2 = gather_v<VB, u>(cur.v[q][2], vbase, cbv);
-        const uint2 g3 = gather_v<VB, u>(cur.v[q][3], vbase, cbv);
         mma_16816(acc[2 * u], prmt(g0.x, g1.x, 0x5410), prmt(g0.x, g1.x, 0x7632), prmt(g2.x, g3.x, 0x5410),
                   prmt(g2.x, g3.x, 0x7632), bp0, bp1);
         mma_16816(acc[2 * u + 1], prmt(g0.y, g1.y, 0x5410), prmt(g0.y, g1.y, 0x7632), prmt(g2.y, g3.y, 0x5410),
                   prmt(g2.y, g3.y, 0x7632), bp0, bp1);
-      });
+      };
+      if constexpr (Fmt<VB>::kWide) {   // d8b8: code i of the V chunk = virtual sub-vectors 2i, 2i+1
+        static_for<0, VS / 2>([&](auto I) {
+          constexpr int i = decltype(I)::value;
+          const uint4 w0 = lds_u128(Fmt<VB>::template vaddr<i>(cur.v[q][0], vbase));
+          const uint4 w1 = lds_u128(Fmt<VB>::template vaddr<i>(cur.v[q][1], vbase));
+          const uint4 w2 = lds_u128(Fmt<VB>::template vaddr<i>(cur.v[q][2], vbase));
+          const uint4 w3 = lds_u128(Fmt<VB>::template vaddr<i>(cur.v[q][3], vbase));
+          pv(std::integral_constant<int, 2 * i>{}, make_uint2(w0.x, w0.y), make_uint2(w1.x, w1.y), make_uint2(w2.x, w2.y),
+             make_uint2(w3.x, w3.y));
+          pv(std::integral_constant<int, 2 * i + 1>{}, make_uint2(w0.z, w0.w), make_uint2(w1.z, w1.w), make_uint2(w2.z, w2.w), make_uint2(w3.z, w3.w));
+        });
+      } else {
+        static_for<0, VS>([&](auto U) {
+          constexpr int u = decltype(U)::value;
+          pv(U, gather_v<VB, u>(cur.v[q][0], vbase, cbv), gather_v<VB, u>(cur.v[q][1], vbase, cbv),
+             gather_v<VB, u>(cur.v[q][2], vbase, cbv), gather_v<VB, u>(cur.v[q][3], vbase, cbv));
+        });
+      }
     }
   }
 
@@ -516,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
 using AttnKernel = void (*)(const AttnArgs);
 
-static bool has_table(int f) { return f == 4 || f == 8; }
+static bool has_table(int f) { return f == 4 || f == 8 || f == kFmtD8B8 || f == kFmtD2B8; }
 static int smem_for(int kf, int vf) { return (!has_table(kf) && !has_table(vf)) ? kSmemBytesNoTab : kSmemBytes; }
 
 // the NEXT-2 (K, V) format pairs with a kernel: each format with itself and the paper's mixed

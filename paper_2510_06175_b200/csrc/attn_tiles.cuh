@@ -26,7 +26,8 @@ __device__ __forceinline__ uint2 bf16x4_to_f16x4(uint2 w) {
 template <int BITS> struct Fmt;
 template <> struct Fmt<8> {
   static constexpr int kRow = 32, kOffK = 8, kOffV = 4;
-  static constexpr bool kSmem = true, kGeneric = false;
+  static constexpr bool kSmem = true, kGeneric = false, kWide = false;
+  static __device__ __forceinline__ uint32_t lane_off(int lane) { return (lane & 15) * 8; }   // copy lane % 16
   using K = uint2;
   using V = uint32_t;
   static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u64(p); }
@@ -42,7 +43,8 @@ template <> struct Fmt<8> {
 };
 template <> struct Fmt<4> {
   static constexpr int kRow = 16, kOffK = 4, kOffV = 2;
-  static constexpr bool kSmem = true, kGeneric = false;
+  static constexpr bool kSmem = true, kGeneric = false, kWide = false;
+  static __device__ __forceinline__ uint32_t lane_off(int lane) { return (lane & 15) * 8; }
   using K = uint32_t;
   using V = uint32_t;   // low 16 bits
   static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u32(p); }
@@ -56,7 +58,7 @@ template <> struct Fmt<4> {
 };
 template <> struct Fmt<16> {
   static constexpr int kRow = 64, kOffK = 16, kOffV = 8;
-  static constexpr bool kSmem = false, kGeneric = false;
+  static constexpr bool kSmem = false, kGeneric = false, kWide = false;
   using K = uint4;
   using V = uint2;
   static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u128(p); }
@@ -109,7 +111,7 @@ struct FmtG {
   static constexpr int kRow = 128 / SUB * BITS / 8;        // bytes per cached row
   static constexpr int kOffK = 32 / SUB * BITS / 8;        // K chunk bytes (= lane stride)
   static constexpr int kOffV = 16 / SUB * BITS / 8;        // V chunk bytes
-  static constexpr bool kSmem = false, kGeneric = true;
+  static constexpr bool kSmem = false, kGeneric = true, kWide = false;
   static_assert(kOffV * 8 == 16 / SUB * BITS, "V chunk must be whole bytes");
   static constexpr int kRowAl = (kRow % 16 == 0) ? 16 : (kRow % 8 == 0) ? 8 : 4;
   static constexpr int gcd(int x, int y) { return y == 0 ? x : gcd(y, x % y); }
@@ -144,10 +146,50 @@ struct FmtG {
   }
 };
 constexpr int kFmtD8B8 = 808, kFmtD8B12 = 812, kFmtD4B10 = 410, kFmtD2B8 = 208;
-template <> struct Fmt<kFmtD8B8> : FmtG<8, 8> {};
 template <> struct Fmt<kFmtD8B12> : FmtG<8, 12> {};
 template <> struct Fmt<kFmtD4B10> : FmtG<4, 10> {};
-template <> struct Fmt<kFmtD2B8> : FmtG<2, 8> {};
+// 256-entry books live in the shared table like b2d4 (code byte -> address bits 8..15, rows of
+// 256 B = [K half | V half]).  d8b8: the 16-byte centroid in 8 copies per half (lane l reads copy
+// l % 8: one LDS.128 per quarter-warp phase hits 8 distinct 16-byte bank groups) and one 16-byte
+// gather feeds two virtual sub-vectors ("wide").  d2b8: the 4-byte centroid in 32 copies per half
+// (one LDS.32 per lane, all 32 banks); a virtual sub-vector is two gathers.
+template <> struct Fmt<kFmtD8B8> {
+  static constexpr int kRow = 16, kOffK = 4, kOffV = 2;   // K chunk: codes 4j..4j+3, V: 2r, 2r+1
+  static constexpr bool kSmem = true, kGeneric = false, kWide = true;
+  static __device__ __forceinline__ uint32_t lane_off(int lane) { return (lane & 7) * 16; }
+  using K = uint32_t;
+  using V = uint32_t;   // low 16 bits
+  static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u32(p); }
+  static __device__ __forceinline__ V ldv(const uint8_t* p) { return ldg_nc_u16(p); }
+  static __device__ __forceinline__ K zk() { return 0u; }
+  template <int I> static __device__ __forceinline__ uint32_t kaddr(K c, uint32_t base) {
+    return prmt(c, base, 0x7604u | (I << 4));
+  }
+  template <int I> static __device__ __forceinline__ uint32_t vaddr(V c, uint32_t base) {
+    return prmt(c, base, 0x7604u | (I << 4));
+  }
+};
+template <> struct Fmt<kFmtD2B8> {
+  static constexpr int kRow = 64, kOffK = 16, kOffV = 8;  // K chunk: codes 16j..16j+15, V: 8r..8r+7
+  static constexpr bool kSmem = true, kGeneric = false, kWide = false;
+  static __device__ __forceinline__ uint32_t lane_off(int lane) { return lane * 4; }
+  using K = uint4;
+  using V = uint2;
+  static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u128(p); }
+  static __device__ __forceinline__ V ldv(const uint8_t* p) { return ldg_nc_u64(p); }
+  static __device__ __forceinline__ K zk() { return make_uint4(0u, 0u, 0u, 0u); }
+  template <int I> static __device__ __forceinline__ uint32_t byte_addr(uint32_t w, uint32_t base) {
+    return prmt(w, base, 0x7604u | ((I & 3) << 4));
+  }
+  template <int T> static __device__ __forceinline__ uint2 gk(const K& c, uint32_t base) {
+    const uint32_t w = T < 2 ? c.x : T < 4 ? c.y : T < 6 ? c.z : c.w;   // codes 2T, 2T+1
+    return make_uint2(lds_u32(byte_addr<2 * T>(w, base)), lds_u32(byte_addr<2 * T + 1>(w, base)));
+  }
+  template <int U> static __device__ __forceinline__ uint2 gv(const V& c, uint32_t base) {
+    const uint32_t w = U < 2 ? c.x : c.y;
+    return make_uint2(lds_u32(byte_addr<2 * U>(w, base)), lds_u32(byte_addr<2 * U + 1>(w, base)));
+  }
+};
 
 template <int BITS> using KCode = typename Fmt<BITS>::K;
 template <int BITS> using VCode = typename Fmt<BITS>::V;
@@ -178,27 +220,55 @@ template <> struct FmtD<16, 64> : Fmt<16> {
 
 template <int KB, int T>
 __device__ __forceinline__ uint2 gather_k(const KCode<KB>& c, uint32_t kbase, const uint16_t* cbk) {
-  if constexpr (Fmt<KB>::kSmem) return lds_u64(Fmt<KB>::template kaddr<T>(c, kbase));
+  if constexpr (KB == kFmtD2B8) return Fmt<KB>::template gk<T>(c, kbase);
+  else if constexpr (Fmt<KB>::kSmem) return lds_u64(Fmt<KB>::template kaddr<T>(c, kbase));
   else if constexpr (Fmt<KB>::kGeneric) return Fmt<KB>::template gather<T>(c.w, cbk);
   else return bf16x4_to_f16x4(ldg_ro_u64(cbk + 4 * Fmt<KB>::template kidx<T>(c)));
 }
 template <int VB, int U>
 __device__ __forceinline__ uint2 gather_v(const VCode<VB>& c, uint32_t vbase, const uint16_t* cbv) {
-  if constexpr (Fmt<VB>::kSmem) return lds_u64(Fmt<VB>::template vaddr<U>(c, vbase));
+  if constexpr (VB == kFmtD2B8) return Fmt<VB>::template gv<U>(c, vbase);
+  else if constexpr (Fmt<VB>::kSmem) return lds_u64(Fmt<VB>::template vaddr<U>(c, vbase));
   else if constexpr (Fmt<VB>::kGeneric) return Fmt<VB>::template gather<U>(c.w, cbv);
   else return bf16x4_to_f16x4(ldg_ro_u64(cbv + 4 * Fmt<VB>::template vidx<U>(c)));
 }
 
+// entries of a format's shared-table half (0: no shared table) and the 16-byte store pattern of
+// centroid j (fp16): d = 4 -> the 8-byte centroid twice, d8b8 -> the 16-byte centroid, d2b8 -> the
+// 4-byte centroid four times; 8 such stores fill the 128-byte half-row
+template <int F> constexpr int smem_entries() {
+  return F == 4 ? 16 : (F == 8 || F == kFmtD8B8 || F == kFmtD2B8) ? 256 : 0;
+}
+template <int F>
+__device__ __forceinline__ uint4 table_pattern(const uint16_t* cb, int j) {
+  if constexpr (F == kFmtD8B8) {
+    const uint2 lo = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(cb + 8 * j));
+    const uint2 hi = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(cb + 8 * j + 4));
+    return make_uint4(lo.x, lo.y, hi.x, hi.y);
+  } else if constexpr (F == kFmtD2B8) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(cb + 2 * j);
+    const uint32_t h = pack_half2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+    return make_uint4(h, h, h, h);
+  } else {
+    const uint2 e = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(cb + 4 * j));
+    return make_uint4(e.x, e.y, e.x, e.y);
+  }
+}
+
+template <int F>
+__device__ __forceinline__ uint32_t table_lane_off(int lane) {
+  if constexpr (Fmt<F>::kSmem) return Fmt<F>::lane_off(lane);
+  else return 0u;
+}
+
 template <int KB, int VB>
 __device__ __forceinline__ void fill_tables(unsigned char* tab, const uint16_t* ck, const uint16_t* cv, int tid) {
-  // thread t: centroid j = t/2 of C_k (t even) or C_v (t odd); 16 replicas = 8 x 16-byte stores,
+  // thread t: centroid j = t/2 of C_k (t even) or C_v (t odd); 8 x 16-byte stores per half-row,
   // rotated so that the 8 threads of a quarter-warp hit 8 different bank groups
   const int j = tid >> 1, which = tid & 1;
-  const int n = which ? (Fmt<VB>::kSmem ? (1 << (VB & 15)) : 0) : (Fmt<KB>::kSmem ? (1 << (KB & 15)) : 0);
+  const int n = which ? smem_entries<VB>() : smem_entries<KB>();
   if (j >= n) return;
-  const uint16_t* src = (which ? cv : ck) + 4 * j;
-  const uint2 e = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(src));
-  const uint4 v = make_uint4(e.x, e.y, e.x, e.y);
+  const uint4 v = which ? table_pattern<VB>(cv, j) : table_pattern<KB>(ck, j);
   unsigned char* row = tab + j * 256 + which * 128;
 #pragma unroll
   for (int u0 = 0; u0 < 8; ++u0) {
