@@ -1,7 +1,7 @@
 """Seeded random-configuration sweep of vecinfer_attn_decode against the CPU oracle.
 
 Each case draws a combination the targeted tests cover only one axis at a time: batch, KV heads,
-GQA group (1..8), head dim (64/128), K/V code widths, ragged lengths (incl. 0), token ranges,
+GQA group (1..8), head dim (64/128), K/V code widths (every 4th case a NEXT-2 format pair), ragged lengths (incl. 0), token ranges,
 fixed or automatic splits, algorithm (auto / split / stream), paged or contiguous codes and a
 residual window, then checks the output against attention_decode_batch (same 2e-3 bars).
 """
@@ -23,6 +23,10 @@ from test_gpu_parity import _assert_close, t_bf16, t_f32, t_i32, t_u8  # noqa: E
 
 CB = load_codebooks()
 NAME = {4: "b1d4", 8: "b2d4", 16: "b4d4"}
+# NEXT-2 pairs (D = 128, split kernel): name -> (sub_dim, code_bits)
+N2 = {"d8b8": (8, 8), "d8b12": (8, 12), "d4b10": (4, 10), "d2b8": (2, 8)}
+N2_PAIRS = [("d8b8", "d8b8"), ("d8b12", "d8b12"), ("d4b10", "d4b10"), ("d2b8", "d2b8"), ("d4b10", "d8b12"),
+            ("d8b12", "d8b8")]
 
 
 def _paginate(codes, ps, rng):
@@ -56,16 +60,25 @@ def test_random_configuration(case):
     tok_begin = 32 * int(rng.integers(0, 4)) if rng.integers(0, 3) == 0 else 0
     tok_end = int(rng.integers(tok_begin, n_cap + 1)) if rng.integers(0, 3) == 0 else -1
     use_res = D == 128 and rng.integers(0, 3) == 0
+    if case % 4 == 3:
+        use_res = bool(rng.integers(0, 3) == 0)
 
+    kname, vname = NAME[kb], NAME[vb]
+    ksub = vsub = 4
+    if case % 4 == 3:   # every 4th case: a NEXT-2 format pair (D = 128, split kernel)
+        D = 128
+        kname, vname = N2_PAIRS[int(rng.integers(0, len(N2_PAIRS)))]
+        (ksub, kb), (vsub, vb) = N2[kname], N2[vname]
+        algo = "auto" if algo == "stream" else algo
     heads = np.arange(Hkv)
     lam = CB["lambda"][heads, :D].copy()
-    ck, cv = CB[f"ck_{NAME[kb]}"], CB[f"cv_{NAME[vb]}"]
+    ck, cv = CB[f"ck_{kname}"], CB[f"cv_{vname}"]
     ck = ck if ck.ndim == 2 else ck[heads]
     cv = cv if cv.ndim == 2 else cv[heads]
-    kc = synth.gen_codes(n_cap, Hkv, D // 4, kb, seed=701 + case, batch=B)
-    vc = synth.gen_codes(n_cap, Hkv, D // 4, vb, seed=702 + case, batch=B)
+    kc = synth.gen_codes(n_cap, Hkv, D // ksub, kb, seed=701 + case, batch=B)
+    vc = synth.gen_codes(n_cap, Hkv, D // vsub, vb, seed=702 + case, batch=B)
     q = synth.gen_queries(B, Hkv * G, Hkv, D, seed=703 + case)
-    kcfg, vcfg = vi.VQConfig(D, 4, kb), vi.VQConfig(D, 4, vb)
+    kcfg, vcfg = vi.VQConfig(D, ksub, kb), vi.VQConfig(D, vsub, vb)
     kp, vp = ref.pack_codes(kc, kb), ref.pack_codes(vc, vb)
     kw = dict(num_splits=splits, algo=algo, tok_begin=tok_begin, tok_end=tok_end, kcfg=kcfg, vcfg=vcfg)
     if paged:   # the same page permutation for K and V
