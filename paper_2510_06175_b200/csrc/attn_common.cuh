@@ -177,10 +177,12 @@ __device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
   }
 }
 
-template <int NTHREADS, int NWARPS, int WROW = 128, int DH = 128>
+template <int NTHREADS, int NWARPS, int WROW = 128, int DH = 128, bool PRESCALED = false>
 __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s,
                                            const float* wm, const float* wl, const float* wacc,
                                            float* scratch) {
+  // PRESCALED: the warps already rescaled their partials to the CTA-wide running max of each head
+  // (wm[w][g] == that max for every w), so the combine is a plain sum over the warps.
   const int tid = threadIdx.x;
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
   const HeadMap hm = head_map(a, h);
@@ -189,18 +191,27 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   for (int idx = tid; idx < 4 * DH; idx += NTHREADS) {
     const int g = idx / DH, dim = idx % DH;
     float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < NWARPS; ++w) M = fmaxf(M, wm[w * 4 + g]);
     float osum = 0.f, lsum = 0.f;
-    if (M != -INFINITY) {
+    if constexpr (PRESCALED) {
+      M = wm[g];
 #pragma unroll
       for (int w = 0; w < NWARPS; ++w) {
-        const float f = ex2_approx(wm[w * 4 + g] - M);
-        lsum += f * wl[w * 4 + g];
-        osum += f * wacc[(w * 4 + g) * WROW + dim];
+        lsum += wl[w * 4 + g];
+        osum += wacc[(w * 4 + g) * WROW + dim];
+      }
+    } else {
+#pragma unroll
+      for (int w = 0; w < NWARPS; ++w) M = fmaxf(M, wm[w * 4 + g]);
+      if (M != -INFINITY) {
+#pragma unroll
+        for (int w = 0; w < NWARPS; ++w) {
+          const float f = ex2_approx(wm[w * 4 + g] - M);
+          lsum += f * wl[w * 4 + g];
+          osum += f * wacc[(w * 4 + g) * WROW + dim];
+        }
       }
     }
-    const bool empty = !(lsum > 0.f);
+    const bool empty = !(lsum > 0.f) || M == -INFINITY;
     const float ov = empty ? 0.f : osum / lsum;
     const float L2 = empty ? -INFINITY : M + __log2f(lsum);
     if (a.S == 1) {
@@ -224,52 +235,80 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   if (a.S == 1 || a.merge_kernel) return;
   if (a.merge_spin) {
     // Single-wave grid (all S CTAs of the unit are co-resident), no fence and no atomic: split s
-    // merges outputs [s*per, (s+1)*per) of the unit, per = ceil(512/S).  One thread per (output,
-    // split) element polls it until published (non-zero), consumes it (stores zero back: every
-    // element is read exactly once, so the workspace is clean for the next launch) and stages it
-    // in shared memory; then one thread per output combines its S splits in order s = 0..S-1.
+    // merges outputs [s*per, (s+1)*per) of the unit, per = ceil(4*DH/S).  Each output is merged by
+    // a group of L lanes (L = the largest power of two <= min(S, 32)); lane l of a group owns
+    // splits l, l+L, l+2L, ...  Every lane first issues the loads of all its elements, then polls
+    // the ones not yet published (non-zero), consumes them (stores zero back: each element is read
+    // exactly once, so the workspace is clean for the next launch) and folds them in split order;
+    // the group combines its lanes with a fixed butterfly (deterministic).  One memory round trip
+    // once the last split has published; no shared-memory staging, no __syncthreads.
     phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 8);
+    (void)scratch;
     const int S = a.S;
     const int per = (4 * DH + S - 1) / S;
     const int o0 = s * per, nout = max(0, min(4 * DH, o0 + per) - o0);
-    float2* stage = reinterpret_cast<float2*>(scratch);
-    for (int e = tid; e < nout * S; e += NTHREADS) {
-      const int oo = e / S, p = e - oo * S, o = o0 + oo;
-      float2 v = make_float2(0.f, -INFINITY);
-      if (o / DH < hm.gp) {
-        unsigned long long* pp = a.part_elem + (unit * S + p) * 512 + (o / DH) * 128 + o % DH;
-        unsigned long long w;
-        while ((w = ld_relaxed_gpu_u64(pp)) == 0ull) __nanosleep(20);
-        st_relaxed_gpu_u64(pp, 0ull);
-        w = ~w;
-        v = make_float2(__uint_as_float(static_cast<uint32_t>(w)), __uint_as_float(static_cast<uint32_t>(w >> 32)));
-      }
-      stage[e] = v;
-    }
-    __syncthreads();
-    phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);
-    for (int t = tid; t < nout; t += NTHREADS) {
+    const int L = S >= 32 ? 32 : (1 << (31 - __clz(S)));
+    const int groups = NTHREADS / L, lg = tid / L, ll = tid % L;
+    constexpr int kMaxPer = 8;   // splits per lane: S <= 256
+    for (int t0 = 0; t0 < nout; t0 += groups) {   // one pass unless S is tiny and DH... (uniform)
+      const int t = t0 + lg;
       const int o = o0 + t, g = o / DH, dim = o % DH;
-      if (g >= hm.gp) continue;
-      const float2* sv = stage + t * S;
-      float m = -INFINITY;
-      for (int p = 0; p < S; ++p) m = fmaxf(m, sv[p].y);
-      float wsum = 0.f, osum = 0.f;
-      if (m != -INFINITY) {
-        for (int p = 0; p < S; ++p) {
-          const float f = sv[p].y == -INFINITY ? 0.f : ex2_approx(sv[p].y - m);
-          wsum += f;
-          osum += f * sv[p].x;
+      const bool act = t < nout && g < hm.gp;
+      unsigned long long* pp = a.part_elem + (unit * S) * 512 + g * 128 + dim;
+      unsigned long long w[kMaxPer];
+#pragma unroll
+      for (int k = 0; k < kMaxPer; ++k) {
+        const int p = ll + k * L;
+        w[k] = (act && p < S) ? ld_relaxed_gpu_u64(pp + static_cast<int64_t>(p) * 512) : ~0ull;
+      }
+#pragma unroll
+      for (int k = 0; k < kMaxPer; ++k) {
+        const int p = ll + k * L;
+        if (act && p < S) {
+          while (w[k] == 0ull) {
+            __nanosleep(20);
+            w[k] = ld_relaxed_gpu_u64(pp + static_cast<int64_t>(p) * 512);
+          }
+          st_relaxed_gpu_u64(pp + static_cast<int64_t>(p) * 512, 0ull);
         }
       }
-      const bool empty = !(wsum > 0.f);
-      const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * DH + dim;
-      const float ov = empty ? 0.f : osum * __frcp_rn(wsum);
-      if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
-      else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
-      if (dim == 0 && a.lse)
-        a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
+      // ~w = (L_s << 32 | o_s); the neutral element ~0 decodes to (o, L) = (0, bits 0) -> mark it
+      float lv[kMaxPer], xv[kMaxPer];
+      float m = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kMaxPer; ++k) {
+        const int p = ll + k * L;
+        const unsigned long long v = ~w[k];
+        const bool has = act && p < S;
+        xv[k] = has ? __uint_as_float(static_cast<uint32_t>(v)) : 0.f;
+        lv[k] = has ? __uint_as_float(static_cast<uint32_t>(v >> 32)) : -INFINITY;
+        m = fmaxf(m, lv[k]);
+      }
+      for (int off = 1; off < L; off <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      float wsum = 0.f, osum = 0.f;
+      if (m != -INFINITY) {
+#pragma unroll
+        for (int k = 0; k < kMaxPer; ++k) {
+          const float f = lv[k] == -INFINITY ? 0.f : ex2_approx(lv[k] - m);
+          wsum += f;
+          osum += f * xv[k];
+        }
+      }
+      for (int off = 1; off < L; off <<= 1) {
+        wsum += __shfl_xor_sync(0xffffffffu, wsum, off);
+        osum += __shfl_xor_sync(0xffffffffu, osum, off);
+      }
+      if (act && ll == 0) {
+        const bool empty = !(wsum > 0.f);
+        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * DH + dim;
+        const float ov = empty ? 0.f : osum * __frcp_rn(wsum);
+        if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
+        else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
+        if (dim == 0 && a.lse)
+          a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
+      }
     }
+    phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);
     return;
   }
   phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 6);

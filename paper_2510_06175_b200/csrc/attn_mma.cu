@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   const int hc = hm.hc;
   const uint16_t* cbk = a.ck + hc * a.ck_hs;
   const uint16_t* cbv = a.cv + hc * a.cv_hs;
-  fill_tables<KB, VB>(tab, cbk, cbv, tid);
+  const uint4 tabv = table_load<KB, VB>(cbk, cbv, tid);   // stored after the first tile's loads
   float4 lam4 = make_float4(0.f, 0.f, 0.f, 0.f);   // warps 0..3: lambda of head h (static)
   if (warp < 4) lam4 = *reinterpret_cast<const float4*>(a.lambda + hc * DH + 4 * (lane & (NL - 1)));
   if (first) griddep_wait();
@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
     else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
   }
+  table_store<KB, VB>(tab, tabv, tid);
   unsigned char* newcodes = smem_raw + kMiscNew;   // [0,64): K code row, [64,128): V code row
   if (kCanAppend && owner) {
     // Eq. 9: encode the new token (S then H on the key, VQ on both), 8 warps per stream, each
@@ -460,7 +461,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
   }
 
-  // ---- warp partials -> shared memory
+  // ---- warp partials -> shared memory, rescaled to the CTA-wide running max of each head: every
+  // warp posts m_run, reads the 16 maxima back (a warp that overwrote its slot with the max already
+  // leaves the max unchanged) and stores f*acc, f*l with f = 2^(m_run - M); wm then holds M for
+  // every warp, so the combine (cta_finish<PRESCALED>, or the cluster path's generic one with
+  // f = 1) is a plain sum over the warps
   phase_mark(a.phase, cta_id, 2);
   griddep_launch_dependents();   // the next kernel may start its (static) prologue
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 4);
@@ -469,9 +474,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   float* wm = reinterpret_cast<float*>(smem_raw + kMiscW);
   float* wl = wm + kNW * 4;
   float* wacc = wl + kNW * 4;
+  if (r == 0) wm[warp * 4 + j] = m_run;
+  __syncthreads();
+  float Mh = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < kNW; ++w) Mh = fmaxf(Mh, wm[w * 4 + j]);
+  const float fsc = m_run == -INFINITY ? 0.f : ex2_approx(m_run - Mh);
   if (r == 0) {
-    wm[warp * 4 + j] = m_run;
-    wl[warp * 4 + j] = l_run;
+    wm[warp * 4 + j] = Mh;
+    wl[warp * 4 + j] = l_run * fsc;
   }
   // thread (r, j): head j, dims (DH/8)r .. (DH/8)r + DH/8 - 1; MMA slots [t][0] + [t][1] hold dim
   // (DH/8)r + 2t, [t][2] + [t][3] dim (DH/8)r + 2t + 1 (hi + lo parts)
@@ -479,12 +490,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 #pragma unroll
   for (int k = 0; k < VS; ++k)
     *reinterpret_cast<float4*>(dst + 4 * k) =
-        make_float4(acc[2 * k][0] + acc[2 * k][1], acc[2 * k][2] + acc[2 * k][3],
-                    acc[2 * k + 1][0] + acc[2 * k + 1][1], acc[2 * k + 1][2] + acc[2 * k + 1][3]);
+        make_float4((acc[2 * k][0] + acc[2 * k][1]) * fsc, (acc[2 * k][2] + acc[2 * k][3]) * fsc,
+                    (acc[2 * k + 1][0] + acc[2 * k + 1][1]) * fsc, (acc[2 * k + 1][2] + acc[2 * k + 1][3]) * fsc);
   __syncthreads();
   phase_mark(a.phase, cta_id, 3);
   if (!a.cluster) {
-    cta_finish<kThreads, kNW, kWRow, DH>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
+    cta_finish<kThreads, kNW, kWRow, DH, true>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
     phase_mark(a.phase, cta_id, 4);
     continue;
   }

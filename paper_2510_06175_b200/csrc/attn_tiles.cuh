@@ -261,20 +261,33 @@ __device__ __forceinline__ uint32_t table_lane_off(int lane) {
   else return 0u;
 }
 
+// codebook table fill in two halves, so the codebook loads can be issued first and the shared
+// stores placed after the (dependent) first code-tile loads: thread t owns centroid j = t/2 of
+// C_k (t even) or C_v (t odd)
 template <int KB, int VB>
-__device__ __forceinline__ void fill_tables(unsigned char* tab, const uint16_t* ck, const uint16_t* cv, int tid) {
-  // thread t: centroid j = t/2 of C_k (t even) or C_v (t odd); 8 x 16-byte stores per half-row,
-  // rotated so that the 8 threads of a quarter-warp hit 8 different bank groups
+__device__ __forceinline__ uint4 table_load(const uint16_t* ck, const uint16_t* cv, int tid) {
+  const int j = tid >> 1, which = tid & 1;
+  const int n = which ? smem_entries<VB>() : smem_entries<KB>();
+  if (j >= n) return make_uint4(0u, 0u, 0u, 0u);
+  return which ? table_pattern<VB>(cv, j) : table_pattern<KB>(ck, j);
+}
+template <int KB, int VB>
+__device__ __forceinline__ void table_store(unsigned char* tab, const uint4 v, int tid) {
+  // 8 x 16-byte stores per half-row, rotated so that the 8 threads of a quarter-warp hit 8
+  // different bank groups
   const int j = tid >> 1, which = tid & 1;
   const int n = which ? smem_entries<VB>() : smem_entries<KB>();
   if (j >= n) return;
-  const uint4 v = which ? table_pattern<VB>(cv, j) : table_pattern<KB>(ck, j);
   unsigned char* row = tab + j * 256 + which * 128;
 #pragma unroll
   for (int u0 = 0; u0 < 8; ++u0) {
     const int u = (u0 + tid) & 7;
     *reinterpret_cast<uint4*>(row + 16 * u) = v;
   }
+}
+template <int KB, int VB>
+__device__ __forceinline__ void fill_tables(unsigned char* tab, const uint16_t* ck, const uint16_t* cv, int tid) {
+  table_store<KB, VB>(tab, table_load<KB, VB>(ck, cv, tid), tid);
 }
 
 template <int KB, int VB>

@@ -15,7 +15,8 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 from paper_2510_06175_b200 import vecinfer as vi  # noqa: E402
 
-CFG = {"cfg2": (1, 32768), "cfg3": (64, 8192), "cfg4": (1, 196608), "cfg1": (1, 1024)}
+CFG = {"cfg2": (1, 32768), "cfg3": (64, 8192), "cfg4": (1, 196608), "cfg1": (1, 1024),
+       "steady": (18, 65536)}   # steady: 144 units of 65536 tokens, use --splits 1 --copies 2
 
 
 def main():
