@@ -251,7 +251,7 @@ def run_ours(args, rank, world, local_rank):
     fused = not args.unfused and not seq_sharded
     # launches of one vecinfer_decode_step (the library decides whether the append is fused)
     fused_launch = fused and vi.decode_step_launches(B, H_KV, n_local, kcfg, vcfg, residual_append=bool(R)) == 1
-    kernel_kind = vi.attn_kernel_kind(B, H_KV)
+    kernel_kind = vi.attn_kernel_kind(B, H_KV, n_local)
 
     def layer(l, ev_pair=None):
         if fused and R:   # one launch: the new token goes to residual row R-1, attention over codes + window

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define VECINFER_ABI_VERSION 4
+#define VECINFER_ABI_VERSION 5
 
 typedef struct CUstream_st* vecinfer_stream_t; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -233,8 +233,12 @@ int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max,
                                  int32_t num_splits);
 int32_t vecinfer_attn_num_ctas(int32_t B, int32_t H_kv, int64_t n_tokens_max,
                                int32_t num_splits);
-/* which kernel a call with these arguments runs: 0 = split kernel, 1 = stream kernel, 2 = LUT */
-int32_t vecinfer_attn_kernel_kind(int32_t B, int32_t H_kv, int32_t num_splits,
+/* which kernel a call with these arguments runs: 0 = split kernel, 1 = stream kernel, 2 = LUT.
+ * AUTO picks the stream partition when B*H_kv >= #SMs, and below that when a cost model over
+ * n_tokens_max (the attended range) says the split plan's waves leave more SMs idle than the
+ * stream partition's fixed costs (e.g. B = 8..16 at 32k tokens, 8 KV heads).  (ABI v5: n_tokens_max
+ * added.) */
+int32_t vecinfer_attn_kernel_kind(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits,
                                   vecinfer_attn_algo_t algo);
 size_t vecinfer_attn_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int32_t D,
                                      int64_t n_tokens_max, int32_t num_splits);

@@ -54,7 +54,7 @@ PROTOTYPES = {
                                          c_void_p, c_void_p, c_sz, c_void_p, ctypes.POINTER(Paged)]),
     "vecinfer_attn_num_splits": (c_i32, [c_i32, c_i32, c_i64, c_i32]),
     "vecinfer_attn_num_ctas": (c_i32, [c_i32, c_i32, c_i64, c_i32]),
-    "vecinfer_attn_kernel_kind": (c_i32, [c_i32, c_i32, c_i32, c_i32]),
+    "vecinfer_attn_kernel_kind": (c_i32, [c_i32, c_i32, c_i64, c_i32, c_i32]),
     "vecinfer_decode_step_launches": (c_i32, [c_i32, c_i32, c_i64, VQ, VQ, c_i32, c_i32, c_i32]),
     "vecinfer_attn_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i32]),
     "vecinfer_attn_decode": (c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i64, c_i64, c_void_p, c_void_p, c_void_p,

@@ -83,15 +83,20 @@ static int stream_mode_from_env() {
   }
   return mode;
 }
-static bool use_stream(int32_t B, int32_t H_kv, int32_t num_splits, bool lut, bool forced = false) {
-  if (forced) return true;
-  if (lut || num_splits > 0) return false;
-  const int m = stream_mode_from_env();
-  if (m >= 0) return m == 1;
-  return static_cast<int64_t>(B) * H_kv >= device_sm_count();
-}
-
 }  // namespace
+
+struct SplitPlan;
+static SplitPlan plan_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits);
+
+// Stream partition (attn_stream.cu) or split kernel (attn_mma.cu)?  With B*H_kv >= #SMs the split
+// kernel's whole-unit waves leave SMs idle, so the stream partition runs.  With fewer units the
+// split plan may still leave SMs idle (units * S CTAs rounded to waves) while the stream partition
+// gives every SM the same token count but pays more per CTA (segment setup, one more piece merge):
+// a cost model in tokens of one CTA picks the cheaper (steady state ~2.98 ns per token and CTA on
+// B200; fixed costs ~6.5 us split with merge, ~4 us single split, ~10 us stream -- fitted to the
+// B = 2..16 x N = 8k..128k timings in DESIGN.md).
+static bool use_stream(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits, bool lut,
+                       bool forced = false);
 
 // Split plan: one CTA per SM (kernel N4: 16 warps, all 64K registers), so the grid B*H_kv*S
 // is sized in waves of SMs.  Cost model in "tokens of one CTA" (calibrated from the phase
@@ -134,6 +139,29 @@ static SplitPlan plan_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int3
   return best;
 }
 
+static bool use_stream(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits, bool lut, bool forced) {
+  if (forced) return true;
+  if (lut || num_splits > 0) return false;
+  const int m = stream_mode_from_env();
+  if (m >= 0) return m == 1;
+  const int64_t U = static_cast<int64_t>(B) * H_kv;
+  const int sms = device_sm_count();
+  if (U >= sms) return true;
+  if (n_tokens_max <= 0) return false;
+  const SplitPlan p = plan_splits(B, H_kv, n_tokens_max, 0);
+  int64_t waves;
+  if (p.cluster) {
+    const int mac = attn_mma_max_active_clusters(p.S);
+    waves = (U + (mac > 0 ? mac : 1) - 1) / (mac > 0 ? mac : 1);
+  } else {
+    waves = (U * p.S + sms - 1) / sms;
+  }
+  const double chunk = static_cast<double>((n_tokens_max + p.S - 1) / p.S);
+  const double t_split = static_cast<double>(waves) * (chunk + (p.S > 1 ? 2200.0 : 1350.0));
+  const double t_stream = static_cast<double>(U) * static_cast<double>(n_tokens_max) / sms + 3350.0;
+  return t_stream < t_split;
+}
+
 // diagnostics: max co-resident clusters of the attention kernel for a cluster size (0 = none)
 extern "C" int32_t vecinfer_debug_attn_max_clusters(int32_t cluster_size) {
   return attn_mma_max_active_clusters(cluster_size);
@@ -141,7 +169,7 @@ extern "C" int32_t vecinfer_debug_attn_max_clusters(int32_t cluster_size) {
 
 extern "C" int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits) {
   if (B <= 0 || H_kv <= 0) return 1;
-  if (use_stream(B, H_kv, num_splits, false)) {
+  if (use_stream(B, H_kv, n_tokens_max, num_splits, false)) {
     const int64_t U = static_cast<int64_t>(B) * H_kv, V = device_sm_count();
     return static_cast<int32_t>((V + U - 1) / U);   // pieces per unit (upper bound)
   }
@@ -150,7 +178,7 @@ extern "C" int32_t vecinfer_attn_num_splits(int32_t B, int32_t H_kv, int64_t n_t
 
 extern "C" int32_t vecinfer_attn_num_ctas(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits) {
   if (B <= 0 || H_kv <= 0) return 0;
-  if (use_stream(B, H_kv, num_splits, false)) return device_sm_count();
+  if (use_stream(B, H_kv, n_tokens_max, num_splits, false)) return device_sm_count();
   return B * H_kv * plan_splits(B, H_kv, n_tokens_max, num_splits).S;
 }
 
@@ -232,7 +260,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
       return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_paged: paged caches run the split DEQUANT_MMA kernel only");
     if (tok_begin % 32 != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode_paged: tok_begin must be a multiple of 32");
   }
-  const bool use_sk = !pg && !next2 && D == 128 && use_stream(B, H_kv, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
+  const bool use_sk = !pg && !next2 && D == 128 && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
   SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
   if (D == 64) plan.cluster = 0;   // the DSMEM cluster merge is written for 128-dim rows
   const int32_t S = plan.S;
@@ -378,7 +406,7 @@ static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t k
   const int64_t units = static_cast<int64_t>(B) * H_kv;
   if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
     return num_splits == 0 || units * num_splits <= device_sm_count();   // persistent grids: separate append
-  if (!paged && use_stream(B, H_kv, num_splits, false)) return true;
+  if (!paged && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
   const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
   const int mac = plan.cluster ? attn_mma_max_active_clusters(plan.S) : 0;
   const int64_t waves = plan.cluster ? (units + (mac > 0 ? mac : 1) - 1) / (mac > 0 ? mac : 1)
@@ -387,9 +415,10 @@ static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t k
 }
 
 // which attention kernel a call runs: 0 split (attn_mma.cu), 1 stream (attn_stream.cu), 2 LUT
-extern "C" int32_t vecinfer_attn_kernel_kind(int32_t B, int32_t H_kv, int32_t num_splits, vecinfer_attn_algo_t algo) {
+extern "C" int32_t vecinfer_attn_kernel_kind(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits,
+                                             vecinfer_attn_algo_t algo) {
   if (algo == VECINFER_ATTN_LUT) return 2;
-  return use_stream(B, H_kv, num_splits, false, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM) ? 1 : 0;
+  return use_stream(B, H_kv, n_tokens_max, num_splits, false, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM) ? 1 : 0;
 }
 
 // kernel launches of one vecinfer_decode_step call (1 = append fused into the attention launch)

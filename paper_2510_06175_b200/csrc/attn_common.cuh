@@ -1,5 +1,8 @@
 // Internal declarations shared by the attention kernels and their host dispatch.
 #pragma once
+#ifndef VECINFER_SPIN_NS
+#define VECINFER_SPIN_NS 0    // back-off between polls of an unpublished split partial (ns; measured: 0 >= 20 > 100)
+#endif
 #include "common.cuh"
 
 namespace vecinfer {
@@ -266,7 +269,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
         const int p = ll + k * L;
         if (act && p < S) {
           while (w[k] == 0ull) {
-            __nanosleep(20);
+            if (VECINFER_SPIN_NS > 0) __nanosleep(VECINFER_SPIN_NS);
             w[k] = ld_relaxed_gpu_u64(pp + static_cast<int64_t>(p) * 512);
           }
           st_relaxed_gpu_u64(pp + static_cast<int64_t>(p) * 512, 0ull);

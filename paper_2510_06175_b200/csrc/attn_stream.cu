@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           const int64_t c1 = div_fix(static_cast<int64_t>(u) * a.V, a.U, a.rcpU);
           unsigned long long* pp = part + (c1 + u + p) * 512 + o;
           unsigned long long w;
-          while ((w = ld_relaxed_gpu_u64(pp)) == 0ull) __nanosleep(20);
+          while ((w = ld_relaxed_gpu_u64(pp)) == 0ull) if (VECINFER_SPIN_NS > 0) __nanosleep(VECINFER_SPIN_NS);
           st_relaxed_gpu_u64(pp, 0ull);
           w = ~w;
           v = make_float2(__uint_as_float(static_cast<uint32_t>(w)), __uint_as_float(static_cast<uint32_t>(w >> 32)));

@@ -162,9 +162,9 @@ def attn_num_ctas(B: int, H_kv: int, n_tokens_max: int, num_splits: int = 0) -> 
     return _lib.load().vecinfer_attn_num_ctas(B, H_kv, n_tokens_max, num_splits)
 
 
-def attn_kernel_kind(B: int, H_kv: int, num_splits: int = 0, algo: str = "auto") -> str:
+def attn_kernel_kind(B: int, H_kv: int, n_tokens_max: int, num_splits: int = 0, algo: str = "auto") -> str:
     """Which attention kernel a call runs: "split" (attn_mma.cu), "stream" (attn_stream.cu) or "lut"."""
-    k = _lib.load().vecinfer_attn_kernel_kind(B, H_kv, num_splits, ALGOS[algo])
+    k = _lib.load().vecinfer_attn_kernel_kind(B, H_kv, n_tokens_max, num_splits, ALGOS[algo])
     return ("split", "stream", "lut")[k]
 
 

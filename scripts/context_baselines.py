@@ -85,7 +85,7 @@ def main():
         res["vecinfer_us"] = time_graph(
             lambda i: vi.attn_decode(q, lam, ck, cv, kcs[i], vcs[i], seq, out=o, lse=lse, workspace=ws[i]),
             copies_vq, args.reps, stream)
-        res["vecinfer_kernel"] = vi.attn_kernel_kind(B, HKV)
+        res["vecinfer_kernel"] = vi.attn_kernel_kind(B, HKV, N)
 
         # ---- dequantise-then-attend: K~ = C_k[codes] (transformed space, Eq. 7), V^ = C_v[codes]
         hidx = torch.arange(HKV, device=dev).view(1, HKV, 1, 1)
