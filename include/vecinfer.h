@@ -332,6 +332,32 @@ vecinfer_status_t vecinfer_merge_lse(const float* o_parts, const float* lse_part
                                      vecinfer_dtype_t o_dtype, float* lse,
                                      vecinfer_stream_t stream);
 
+/* ---------------------------------------------------------------------------------------
+ * vecinfer_kmeans_step -- one Lloyd iteration of the codebook k-means (offline step of the
+ * method: "C_k ... via K-means"; "K-means ... maximum number of iterations set to 30",
+ * P:501; empty-cluster re-seeding at the largest-distortion points).  NEXT-3.
+ *   X          fp32 [n, d] points (row-major, contiguous), d in {2, 4, 8}; n >= k, n < 2^32 - 1.
+ *   C          fp32 [k, d] current centroids, 0 < k <= 65536.
+ *   C_new      fp32 [k, d] out: RN32(mean of the cluster's points) (fp64 sum and division) for
+ *              non-empty clusters; the empty clusters, in increasing index, take the points of
+ *              largest best distance (ties: lowest point index).  May alias C.
+ *   assign     int32 [n] out: argmin_j of the pinned fp32 distance (the encoder's rule: e = x - c,
+ *              ((e_0^2 + e_1^2) + e_2^2) + ..., RN, no FMA), ties to the lowest index.
+ *   best       fp32 [n] out: the pinned distance to the assigned centroid.
+ *   objective  fp64 device scalar out: sum_i best_i (accumulated with atomics: order-dependent
+ *              in the last bits).
+ *   workspace  >= vecinfer_kmeans_workspace_bytes(k, d) bytes, 256-byte aligned, any contents.
+ * Deterministic except C_new, whose fp64 cluster sums are accumulated in atomic order (C_new is
+ * within one fp32 ulp of the exactly rounded mean).  Launches 3 kernels + 2 memsets on `stream`.
+ * Errors: INVALID_ARG (NULL / misaligned), UNSUPPORTED (d), SHAPE (k, n), EMPTY (n == 0),
+ * WORKSPACE, CUDA.
+ * ------------------------------------------------------------------------------------- */
+size_t vecinfer_kmeans_workspace_bytes(int32_t k, int32_t d);
+vecinfer_status_t vecinfer_kmeans_step(const float* X, int64_t n, int32_t d, const float* C,
+                                       int32_t k, float* C_new, int32_t* assign, float* best,
+                                       double* objective, void* workspace, size_t workspace_bytes,
+                                       vecinfer_stream_t stream);
+
 /* Diagnostics: how many thread-block clusters of `cluster_size` CTAs of the attention kernel can
  * be co-resident on the current device (0 = not schedulable); used by the split planner. */
 int32_t vecinfer_debug_attn_max_clusters(int32_t cluster_size);

@@ -439,3 +439,58 @@ def kmeans(X: np.ndarray, n_clusters: int, max_iters: int = 30, seed: int = 0):
             break
         C = newC
     return C, hist
+
+
+def pinned_sqdist(X: np.ndarray, C: np.ndarray) -> np.ndarray:
+    """Pinned fp32 squared distance of Eq. 2 under reading R9 for every (point, centroid) pair:
+    e_t = x_t - c_t, dist = ((e_0^2 + e_1^2) + e_2^2) + ..., every op an fp32 round-to-nearest op,
+    no fused multiply-add.  X: [n, d], C: [k, d] -> fp32 [n, k]."""
+    X = np.asarray(X, dtype=np.float32)
+    C = np.asarray(C, dtype=np.float32)
+    dist = None
+    for t in range(X.shape[1]):
+        e = X[:, None, t] - C[None, :, t]
+        e2 = e * e
+        dist = e2 if dist is None else dist + e2
+    return dist
+
+
+def kmeans_lloyd_step(X: np.ndarray, C: np.ndarray):
+    """One Lloyd iteration of the codebook k-means ("K-means ... maximum number of
+    iterations set to 30"), on fp32 points and fp32 centroids, in the order
+    the algorithm states:
+
+      1. assignment: a_i = argmin_j dist(x_i, C_j) with the pinned fp32 distance of Eq. 2 /
+         reading R9 (the encoder's rule, so a fitted codebook and its encoder agree), ties to the
+         lowest index; best_i = dist(x_i, C_{a_i});
+      2. update: for every cluster with n_j > 0 points, C'_j = RN32(sum_{a_i = j} x_i / n_j), the
+         sum and the division in fp64 (the exact mean up to one fp64 rounding each);
+      3. empty clusters (n_j = 0, in increasing j) are re-seeded at the points of largest best_i
+         (ties: lowest point index), one point per empty cluster.
+
+    Returns (C' fp32 [k, d], assign int64 [n], best fp32 [n], counts int64 [k], objective =
+    sum_i best_i in fp64).
+    """
+    X = np.asarray(X, dtype=np.float32)
+    C = np.asarray(C, dtype=np.float32)
+    n, k = X.shape[0], C.shape[0]
+    assign = np.empty(n, dtype=np.int64)
+    best = np.empty(n, dtype=np.float32)
+    step = max(1, (1 << 22) // max(k, 1))
+    for s0 in range(0, n, step):
+        dd = pinned_sqdist(X[s0:s0 + step], C)
+        a = np.argmin(dd, axis=1)                              # first minimum = lowest index
+        assign[s0:s0 + step] = a
+        best[s0:s0 + step] = dd[np.arange(dd.shape[0]), a]
+    counts = np.bincount(assign, minlength=k)
+    sums = np.zeros((k, X.shape[1]), dtype=np.float64)
+    np.add.at(sums, assign, X.astype(np.float64))
+    newC = C.copy()
+    nz = counts > 0
+    newC[nz] = (sums[nz] / counts[nz, None]).astype(np.float32)
+    empty = np.nonzero(~nz)[0]
+    if empty.size:
+        order = np.argsort(-best.astype(np.float64), kind="stable")   # largest best first, ties lowest index
+        for e_i, c in enumerate(empty):
+            newC[c] = X[order[e_i]]
+    return newC, assign, best, counts, float(best.astype(np.float64).sum())

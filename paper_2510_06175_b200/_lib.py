@@ -43,6 +43,9 @@ PROTOTYPES = {
     "vecinfer_last_error": (c_char_p, []),
     "vecinfer_status_string": (c_char_p, [c_i32]),
     "vecinfer_calibrate_workspace_bytes": (c_sz, [c_i32, c_i32]),
+    "vecinfer_kmeans_workspace_bytes": (c_sz, [c_i32, c_i32]),
+    "vecinfer_kmeans_step": (c_i32, [c_void_p, c_i64, c_i32, c_void_p, c_i32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_void_p, c_sz, c_void_p]),
     "vecinfer_calibrate_smooth": (c_i32, [c_void_p, c_i64, c_i32, c_i32, c_i64, c_i64, c_f32, c_void_p, c_void_p,
                                           c_void_p, c_sz, c_void_p]),
     "vecinfer_encode_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, VQ, VQ]),

@@ -1,0 +1,241 @@
+// Codebook k-means on the GPU (NEXT-3): one Lloyd iteration per call, the
+// codebook-construction step of the method ("C_k ... via K-means", "K-means ...
+// maximum number of iterations set to 30"; empty-cluster re-seeding SPEC S:184).  Offline, not on
+// the decode path; written so fitting a b4d4 codebook (65 536 centroids) is a GPU job.
+//
+//   1. assign (kmeans_assign_kernel): a_i = argmin_j dist(x_i, C_j) with the encoder's pinned fp32
+//      distance (Eq. 2 / reading R9: e_t = x_t - c_t, ((e_0^2 + e_1^2) + e_2^2) + ..., every op RN,
+//      no FMA), strict < scan in index order -> lowest index on ties.  Centroids are staged in
+//      shared memory in 32 KiB chunks and read as broadcasts; every thread keeps 8 points in
+//      registers.  The same thread then adds its points into the fp64 cluster sums and counts
+//      (global atomics) and its best distances into the objective.
+//   2. finalize (kmeans_finalize_kernel): C'_j = RN32(sum_j / n_j) (fp64 division) for n_j > 0.
+//   3. reseed (kmeans_reseed_kernel, one CTA): the empty clusters, in increasing j, take the points
+//      of largest best_i (ties: lowest i), one each -- E rounds of a block-wide max over the key
+//      (best_bits << 32 | ~i) restricted to keys below the previous pick.  No-op when E = 0.
+// Parity: oracle/vecinfer_oracle.py kmeans_lloyd_step (assignments and best bit-exact, counts
+// exact, C' within one fp32 ulp: the fp64 sums are accumulated in atomic order).
+#include "common.cuh"
+
+namespace vecinfer {
+namespace {
+
+constexpr int kKmThreads = 256;
+constexpr int kKmPts = 8;                 // points per thread
+constexpr int kKmChunkBytes = 32768;      // centroid chunk staged in shared memory
+
+template <int D>
+__device__ __forceinline__ float pinned_dist(const float (&x)[D], const float* c) {
+  float acc = 0.f;
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+    const float e = __fsub_rn(x[t], c[t]);
+    const float e2 = __fmul_rn(e, e);
+    acc = t == 0 ? e2 : __fadd_rn(acc, e2);
+  }
+  return acc;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kKmThreads) kmeans_assign_kernel(const float* __restrict__ X, int64_t n,
+                                                                    const float* __restrict__ C, int k,
+                                                                    int32_t* __restrict__ assign,
+                                                                    float* __restrict__ best,
+                                                                    double* __restrict__ sums,
+                                                                    int32_t* __restrict__ counts,
+                                                                    double* __restrict__ objective) {
+  constexpr int kChunk = kKmChunkBytes / (4 * D);
+  __shared__ __align__(16) float sc[kChunk * D];
+  __shared__ double sobj[kKmThreads / 32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kKmThreads * kKmPts;
+  float x[kKmPts][D];
+  float bd[kKmPts];
+  int bi[kKmPts];
+#pragma unroll
+  for (int p = 0; p < kKmPts; ++p) {
+    const int64_t i = base + p * kKmThreads + threadIdx.x;   // coalesced rows
+#pragma unroll
+    for (int t = 0; t < D; ++t) x[p][t] = i < n ? X[i * D + t] : 0.f;
+    bd[p] = __int_as_float(0x7f800000);
+    bi[p] = 0;
+  }
+  for (int c0 = 0; c0 < k; c0 += kChunk) {
+    const int nc = min(kChunk, k - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * D; e += kKmThreads) sc[e] = C[static_cast<int64_t>(c0) * D + e];
+    __syncthreads();
+    for (int j = 0; j < nc; ++j) {
+      float cj[D];
+#pragma unroll
+      for (int t = 0; t < D; ++t) cj[t] = sc[j * D + t];
+#pragma unroll
+      for (int p = 0; p < kKmPts; ++p) {
+        const float dd = pinned_dist<D>(x[p], cj);
+        if (dd < bd[p]) { bd[p] = dd; bi[p] = c0 + j; }
+      }
+    }
+  }
+  double obj = 0.0;
+#pragma unroll
+  for (int p = 0; p < kKmPts; ++p) {
+    const int64_t i = base + p * kKmThreads + threadIdx.x;
+    if (i >= n) continue;
+    assign[i] = bi[p];
+    best[i] = bd[p];
+    obj += static_cast<double>(bd[p]);
+    atomicAdd(&counts[bi[p]], 1);
+#pragma unroll
+    for (int t = 0; t < D; ++t) atomicAdd(&sums[static_cast<int64_t>(bi[p]) * D + t], static_cast<double>(x[p][t]));
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) obj += __shfl_xor_sync(0xffffffffu, obj, off);
+  if ((threadIdx.x & 31) == 0) sobj[threadIdx.x >> 5] = obj;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kKmThreads / 32; ++w) s += sobj[w];
+    atomicAdd(objective, s);
+  }
+}
+
+template <int D>
+__global__ void kmeans_finalize_kernel(const float* __restrict__ C, int k, const double* __restrict__ sums,
+                                       const int32_t* __restrict__ counts, float* __restrict__ Cn) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  const int cnt = counts[j];
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+    const int64_t e = static_cast<int64_t>(j) * D + t;
+    Cn[e] = cnt > 0 ? __double2float_rn(__ddiv_rn(sums[e], static_cast<double>(cnt))) : C[e];
+  }
+}
+
+// one CTA of 1024 threads
+template <int D>
+__global__ void __launch_bounds__(1024) kmeans_reseed_kernel(const float* __restrict__ X, int64_t n,
+                                                             const float* __restrict__ best, int k,
+                                                             const int32_t* __restrict__ counts,
+                                                             int32_t* __restrict__ empty_list,
+                                                             float* __restrict__ Cn) {
+  __shared__ int s_warp[32];
+  __shared__ int s_total;
+  __shared__ unsigned long long s_red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // 1. ordered list of the empty clusters (block-wide exclusive scan per 1024-cluster chunk)
+  int E = 0;
+  for (int c0 = 0; c0 < k; c0 += 1024) {
+    const int c = c0 + tid;
+    const bool emp = c < k && counts[c] == 0;
+    const unsigned m = __ballot_sync(0xffffffffu, emp);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int w = 0; w < 32; ++w) { const int v = s_warp[w]; s_warp[w] = run; run += v; }
+      s_total = run;
+    }
+    __syncthreads();
+    if (emp) empty_list[E + s_warp[warp] + __popc(m & ((1u << lane) - 1u))] = c;
+    E += s_total;
+    __syncthreads();
+  }
+  if (E == 0) return;
+  __threadfence_block();
+  __syncthreads();
+  // 2. E rounds: the point of largest key = (best bits << 32 | ~i) below the previous pick
+  unsigned long long prev = ~0ull;
+  for (int r = 0; r < E; ++r) {
+    unsigned long long mx = 0ull;
+    bool any = false;
+    for (int64_t i = tid; i < n; i += 1024) {
+      const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(best[i])) << 32) |
+                                     (0xFFFFFFFFull - static_cast<unsigned long long>(i));
+      if (key < prev && (!any || key > mx)) { mx = key; any = true; }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, off);
+      mx = o > mx ? o : mx;
+    }
+    if (lane == 0) s_red[warp] = mx;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long v = s_red[lane];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, off);
+        v = o > v ? o : v;
+      }
+      if (lane == 0) s_red[0] = v;
+    }
+    __syncthreads();
+    prev = s_red[0];
+    __syncthreads();
+    const int64_t pick = static_cast<int64_t>(0xFFFFFFFFull - (prev & 0xFFFFFFFFull));
+    if (tid < D) Cn[static_cast<int64_t>(empty_list[r]) * D + tid] = X[pick * D + tid];
+  }
+}
+
+struct KmWs {
+  size_t sums, counts, empty, total;
+};
+KmWs km_ws(int32_t k, int32_t d) {
+  KmWs w;
+  w.sums = 0;
+  w.counts = (static_cast<size_t>(k) * d * sizeof(double) + 255) & ~size_t(255);
+  w.empty = w.counts + ((static_cast<size_t>(k) * sizeof(int32_t) + 255) & ~size_t(255));
+  w.total = w.empty + static_cast<size_t>(k) * sizeof(int32_t);
+  return w;
+}
+
+template <int D>
+cudaError_t launch_kmeans(const float* X, int64_t n, const float* C, int k, float* Cn, int32_t* assign, float* best,
+                          double* obj, unsigned char* ws, cudaStream_t st) {
+  const KmWs w = km_ws(k, D);
+  double* sums = reinterpret_cast<double*>(ws + w.sums);
+  int32_t* counts = reinterpret_cast<int32_t*>(ws + w.counts);
+  int32_t* empty = reinterpret_cast<int32_t*>(ws + w.empty);
+  if (cudaMemsetAsync(ws, 0, w.empty, st) != cudaSuccess) return cudaGetLastError();
+  if (cudaMemsetAsync(obj, 0, sizeof(double), st) != cudaSuccess) return cudaGetLastError();
+  const int64_t per = static_cast<int64_t>(kKmThreads) * kKmPts;
+  const unsigned g = static_cast<unsigned>((n + per - 1) / per);
+  kmeans_assign_kernel<D><<<g, kKmThreads, 0, st>>>(X, n, C, k, assign, best, sums, counts, obj);
+  kmeans_finalize_kernel<D><<<(k + 255) / 256, 256, 0, st>>>(C, k, sums, counts, Cn);
+  kmeans_reseed_kernel<D><<<1, 1024, 0, st>>>(X, n, best, k, counts, empty, Cn);
+  return cudaPeekAtLastError();
+}
+
+}  // namespace
+}  // namespace vecinfer
+
+using namespace vecinfer;
+
+extern "C" size_t vecinfer_kmeans_workspace_bytes(int32_t k, int32_t d) {
+  if (k <= 0 || d <= 0) return 0;
+  return km_ws(k, d).total;
+}
+
+extern "C" vecinfer_status_t vecinfer_kmeans_step(const float* X, int64_t n, int32_t d, const float* C, int32_t k,
+                                                  float* C_new, int32_t* assign, float* best, double* objective,
+                                                  void* workspace, size_t workspace_bytes, vecinfer_stream_t stream) {
+  if (!X || !C || !C_new || !assign || !best || !objective)
+    return fail(VECINFER_ERR_INVALID_ARG, "kmeans_step: NULL pointer");
+  if (d != 2 && d != 4 && d != 8) return fail(VECINFER_ERR_UNSUPPORTED, "kmeans_step: sub-vector dim d must be 2, 4 or 8");
+  if (k <= 0 || k > 65536) return fail(VECINFER_ERR_SHAPE, "kmeans_step: need 0 < k <= 65536");
+  if (n <= 0) return fail(VECINFER_ERR_EMPTY, "kmeans_step: no points");
+  if (n < k) return fail(VECINFER_ERR_SHAPE, "kmeans_step: fewer points (%lld) than clusters (%d)", (long long)n, k);
+  if (n >= (int64_t(1) << 32) - 1) return fail(VECINFER_ERR_SHAPE, "kmeans_step: n must be < 2^32 - 1");
+  if (!aligned(X, 4) || !aligned(C, 4) || !aligned(C_new, 4) || !aligned(objective, 8))
+    return fail(VECINFER_ERR_INVALID_ARG, "kmeans_step: misaligned pointer");
+  const size_t need = vecinfer_kmeans_workspace_bytes(k, d);
+  if (!workspace || workspace_bytes < need)
+    return fail(VECINFER_ERR_WORKSPACE, "kmeans_step: workspace needs %zu bytes", need);
+  if (!aligned(workspace, 256)) return fail(VECINFER_ERR_INVALID_ARG, "kmeans_step: workspace must be 256-byte aligned");
+  cudaStream_t st = as_stream(stream);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  if (d == 2) launch_kmeans<2>(X, n, C, k, C_new, assign, best, objective, ws, st);
+  else if (d == 4) launch_kmeans<4>(X, n, C, k, C_new, assign, best, objective, ws, st);
+  else launch_kmeans<8>(X, n, C, k, C_new, assign, best, objective, ws, st);
+  return check_launch("kmeans_step");
+}

@@ -297,3 +297,44 @@ def merge_lse(o_parts: torch.Tensor, lse_parts: torch.Tensor, o_dtype: torch.dty
         _need(out, "out"), F32 if out.dtype == torch.float32 else BF16, _need(lse, "lse", torch.float32),
         _stream(o_parts.device)))
     return out, lse
+
+
+def kmeans_step(X: torch.Tensor, C: torch.Tensor, C_new: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+    """One Lloyd iteration of the codebook k-means on the GPU.
+
+    X fp32 [n, d], C fp32 [k, d] (d in {2, 4, 8}).  Returns (C_new fp32 [k, d], assign int32 [n],
+    best fp32 [n], objective fp64 [1]) -- all device tensors, nothing synchronised."""
+    n, d = X.shape
+    k = C.shape[0]
+    if C_new is None:
+        C_new = torch.empty_like(C)
+    assign = torch.empty(n, dtype=torch.int32, device=X.device)
+    best = torch.empty(n, dtype=torch.float32, device=X.device)
+    obj = torch.empty(1, dtype=torch.float64, device=X.device)
+    lib = _lib.load()
+    if workspace is None:
+        workspace = torch.empty(max(lib.vecinfer_kmeans_workspace_bytes(k, d), 256), dtype=torch.uint8, device=X.device)
+    check("vecinfer_kmeans_step", lib.vecinfer_kmeans_step(
+        _need(X, "X", torch.float32), n, d, _need(C, "C", torch.float32), k, _need(C_new, "C_new", torch.float32),
+        _need(assign, "assign", torch.int32), _need(best, "best", torch.float32), _need(obj, "objective", torch.float64),
+        ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream(X.device)))
+    return C_new, assign, best, obj
+
+
+def kmeans_fit(X: torch.Tensor, C0: torch.Tensor, max_iters: int = 30):
+    """Lloyd iterations from the initial centroids C0 (k-means, <= 30 iterations) until the
+    centroids stop changing.  Each iteration is one vecinfer_kmeans_step; the convergence test reads
+    one flag back to the host.  Returns (C fp32 [k, d], objective history)."""
+    C = C0.contiguous().clone()
+    lib = _lib.load()
+    ws = torch.empty(max(lib.vecinfer_kmeans_workspace_bytes(C.shape[0], C.shape[1]), 256), dtype=torch.uint8,
+                     device=X.device)
+    Cn = torch.empty_like(C)
+    hist = []
+    for _ in range(max_iters):
+        _, _, _, obj = kmeans_step(X, C, Cn, ws)
+        hist.append(obj)
+        if torch.equal(Cn, C):
+            break
+        C, Cn = Cn, C
+    return C, [float(h.item()) for h in hist]

@@ -72,6 +72,14 @@ def test_argument_validation_without_cuda(lib):
                                 None, None, 0, None)
     assert st == 3     # UNSUPPORTED (d = 16)
     assert lib.vecinfer_status_string(3) == b"VECINFER_ERR_UNSUPPORTED"
+    # k-means step (NEXT-3): d outside {2, 4, 8}, n < k, n == 0, short workspace
+    p = ctypes.c_void_p(256)
+    assert lib.vecinfer_kmeans_step(p, 100, 3, p, 16, p, p, p, p, p, 1 << 20, None) == 3
+    assert lib.vecinfer_kmeans_step(p, 8, 4, p, 16, p, p, p, p, p, 1 << 20, None) == 2
+    assert lib.vecinfer_kmeans_step(p, 0, 4, p, 16, p, p, p, p, p, 1 << 20, None) == 4
+    assert lib.vecinfer_kmeans_step(p, 100, 4, p, 16, p, p, p, p, p, 16, None) == 6
+    assert lib.vecinfer_kmeans_step(None, 100, 4, p, 16, p, p, p, p, p, 1 << 20, None) == 1
+    assert lib.vecinfer_kmeans_workspace_bytes(256, 4) >= 256 * 4 * 8 + 256 * 4
 
 
 def test_workspace_and_split_queries(lib):

@@ -496,6 +496,68 @@ def test_kmeans_examples(golden):
     assert len(ha) <= 30                                           # P:501 iteration cap
 
 
+def test_kmeans_lloyd_step_worked_example(golden):
+    """SPEC S:133 worked example through ONE pinned Lloyd step (P:501): from C0 = {(0,0), (10,10)}
+    the points {(0,0), (0,1), (10,10), (10,11)} split 2/2 and the means are the brute-force optimal
+    2-means {(0, 0.5), (10, 10.5)}; best distances 0, 1, 0, 1; objective 2."""
+    ex = golden["kmeans_example"]
+    X = np.array(ex["points"], dtype=np.float32)
+    C, a, best, cnt, obj = ref.kmeans_lloyd_step(X, np.array([[0, 0], [10, 10]], dtype=np.float32))
+    assert np.array_equal(C, np.array(ex["centroids"], dtype=np.float32))
+    assert a.tolist() == [0, 0, 1, 1] and cnt.tolist() == [2, 2]
+    assert best.tolist() == [0.0, 1.0, 0.0, 1.0] and obj == 2.0
+
+
+def test_kmeans_lloyd_step_reseeds_empty_clusters():
+    """an empty cluster is re-seeded at the point of largest distortion, ties to the
+    lowest point index; several empty clusters (increasing index) take successive worst points.
+    Hand-worked: best = [0, 1, 0, 1, 4] -> empty clusters 2, 3 take points 4 (best 4) and 1 (best 1,
+    lower index than point 3)."""
+    X = np.array([[0, 0], [0, 1], [10, 10], [10, 11], [0, -2]], dtype=np.float32)
+    C0 = np.array([[0, 0], [10, 10], [500, 500], [-500, 9]], dtype=np.float32)
+    C, a, best, cnt, _ = ref.kmeans_lloyd_step(X, C0)
+    assert best.tolist() == [0.0, 1.0, 0.0, 1.0, 4.0] and cnt.tolist() == [3, 2, 0, 0]
+    assert np.array_equal(C[0], np.array([0, -1 / 3], dtype=np.float32))   # RN32 of the exact mean
+    assert np.array_equal(C[2], X[4]) and np.array_equal(C[3], X[1])
+
+
+def test_kmeans_lloyd_step_exact_means_and_ties():
+    """Closed form: points c_j + delta with the deltas of each cluster summing to zero (dyadic, so
+    every op is exact) -> C' = the generating centres exactly; a point at the exact midpoint of two
+    centroids (a genuine tie of the pinned distance) goes to the lower index."""
+    rng = np.random.default_rng(5)
+    centres = (rng.integers(-40, 40, size=(16, 4)) * 8).astype(np.float32)
+    deltas = rng.integers(-3, 4, size=(16, 6, 4)).astype(np.float32) * 0.25
+    deltas -= deltas.mean(axis=1, keepdims=True)                             # zero-sum per cluster
+    X = (centres[:, None, :] + deltas).reshape(-1, 4).astype(np.float32)
+    assert np.all(np.abs(X - (centres[:, None, :] + deltas).reshape(-1, 4)) == 0)
+    C, a, _, cnt, _ = ref.kmeans_lloyd_step(X, centres)
+    assert np.array_equal(cnt, np.full(16, 6)) and np.array_equal(C, centres)
+    assert np.array_equal(a, np.repeat(np.arange(16), 6))
+    tie = np.array([[1.0, 0, 0, 0]], dtype=np.float32)
+    for C2 in (np.array([[0, 0, 0, 0], [2, 0, 0, 0]], np.float32), np.array([[2, 0, 0, 0], [0, 0, 0, 0]], np.float32)):
+        _, a2, b2, _, _ = ref.kmeans_lloyd_step(np.repeat(tie, 2, 0), C2)
+        assert a2.tolist() == [0, 0] and b2.tolist() == [1.0, 1.0]
+
+
+def test_kmeans_lloyd_step_fixed_point_and_descent():
+    """Invariants of Lloyd's algorithm: a codebook holding every distinct point is a fixed point
+    with objective 0; iterating from any start never increases the objective (up to fp32 rounding
+    of the pinned distances, 1e-6 relative)."""
+    rng = np.random.default_rng(9)
+    pts = rng.standard_normal((32, 4)).astype(np.float32)
+    X = np.repeat(pts, 3, axis=0)
+    C, _, _, _, obj = ref.kmeans_lloyd_step(X, pts)
+    assert np.array_equal(C, pts) and obj == 0.0
+    X = rng.standard_normal((3000, 4)).astype(np.float32)
+    C = X[rng.choice(3000, 64, replace=False)].copy()
+    objs = []
+    for _ in range(8):
+        C, _, _, _, obj = ref.kmeans_lloyd_step(X, C)
+        objs.append(obj)
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(objs, objs[1:]))
+
+
 # ------------------------------------------------------------ residual window (P:494, NEXT-1)
 def test_residual_window_special_cases():
     """Residual-window attention: empty residual == Eq. 10 VQ attention; empty VQ part == Eq. 1 on
