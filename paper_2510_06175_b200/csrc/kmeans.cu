@@ -6,8 +6,8 @@
 //   1. assign (kmeans_assign_kernel): a_i = argmin_j dist(x_i, C_j) with the encoder's pinned fp32
 //      distance (Eq. 2 / reading R9: e_t = x_t - c_t, ((e_0^2 + e_1^2) + e_2^2) + ..., every op RN,
 //      no FMA), strict < scan in index order -> lowest index on ties.  Centroids are staged in
-//      shared memory in 32 KiB chunks and read as broadcasts; every thread keeps 8 points in
-//      registers.  The same thread then adds its points into the fp64 cluster sums and counts
+//      shared memory in 32 KiB chunks and read as broadcasts; every thread keeps 8 points (2 for
+//      small n) in registers.  The same thread then adds its points into the fp64 cluster sums and counts
 //      (global atomics) and its best distances into the objective.
 //   2. finalize (kmeans_finalize_kernel): C'_j = RN32(sum_j / n_j) (fp64 division) for n_j > 0.
 //   3. reseed (kmeans_reseed_kernel, one CTA): the empty clusters, in increasing j, take the points
@@ -21,7 +21,6 @@ namespace vecinfer {
 namespace {
 
 constexpr int kKmThreads = 256;
-constexpr int kKmPts = 8;                 // points per thread
 constexpr int kKmChunkBytes = 32768;      // centroid chunk staged in shared memory
 
 template <int D>
@@ -36,7 +35,7 @@ __device__ __forceinline__ float pinned_dist(const float (&x)[D], const float* c
   return acc;
 }
 
-template <int D>
+template <int D, int kKmPts>   // kKmPts: points per thread (8, or 2 for small n: more CTAs)
 __global__ void __launch_bounds__(kKmThreads) kmeans_assign_kernel(const float* __restrict__ X, int64_t n,
                                                                     const float* __restrict__ C, int k,
                                                                     int32_t* __restrict__ assign,
@@ -198,9 +197,13 @@ cudaError_t launch_kmeans(const float* X, int64_t n, const float* C, int k, floa
   int32_t* empty = reinterpret_cast<int32_t*>(ws + w.empty);
   if (cudaMemsetAsync(ws, 0, w.empty, st) != cudaSuccess) return cudaGetLastError();
   if (cudaMemsetAsync(obj, 0, sizeof(double), st) != cudaSuccess) return cudaGetLastError();
-  const int64_t per = static_cast<int64_t>(kKmThreads) * kKmPts;
+  // 8 points per thread amortise the shared-memory centroid stream; below ~2 CTAs per SM at 8,
+  // 2 points per thread keep every SM busy
+  const bool big = n >= static_cast<int64_t>(device_sm_count()) * kKmThreads * 8 * 2;
+  const int64_t per = static_cast<int64_t>(kKmThreads) * (big ? 8 : 2);
   const unsigned g = static_cast<unsigned>((n + per - 1) / per);
-  kmeans_assign_kernel<D><<<g, kKmThreads, 0, st>>>(X, n, C, k, assign, best, sums, counts, obj);
+  if (big) kmeans_assign_kernel<D, 8><<<g, kKmThreads, 0, st>>>(X, n, C, k, assign, best, sums, counts, obj);
+  else kmeans_assign_kernel<D, 2><<<g, kKmThreads, 0, st>>>(X, n, C, k, assign, best, sums, counts, obj);
   kmeans_finalize_kernel<D><<<(k + 255) / 256, 256, 0, st>>>(C, k, sums, counts, Cn);
   kmeans_reseed_kernel<D><<<1, 1024, 0, st>>>(X, n, best, k, counts, empty, Cn);
   return cudaPeekAtLastError();
