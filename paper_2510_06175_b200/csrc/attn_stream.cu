@@ -668,22 +668,46 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       // units write o and L; pieces of split units publish (o_s, L_s) per element as one 64-bit
       // relaxed store of ~(L_s << 32 | o_s) to slot c + u (zero = empty: see the merge).
       const int nwA = rsh->nwA, b0 = rsh->b0, strad = rsh->strad;
+      // per (slot, head) weights f = 2^(m_slot - M_seg) and per (segment, head) maxima, computed once
+      // by 76 threads into the (idle) staging region, so the per-output combine below is a plain
+      // weighted sum: no exponentials, no max scans
+      float* sfw = reinterpret_cast<float*>(smem_raw + kMiscStage);   // [kSlots][4]
+      float* sMx = sfw + kSlots * 4;                                   // [2][4]
+      if (tid < kSlots * 4 + 8) {
+        const bool wslot = tid < kSlots * 4;
+        const int sl = wslot ? tid >> 2 : -1, g = tid & 3;
+        int sgi;
+        if (!wslot) sgi = (tid - kSlots * 4) >> 2;
+        else if (sl == kSlots - 1) sgi = strad >= 0 ? 0 : -1;
+        else if (sl == strad) sgi = 1;
+        else if (sl < nwA) sgi = 0;
+        else sgi = (nseg > 1 && sl >= b0) ? 1 : -1;
+        float M = -INFINITY, f = 0.f;
+        if (sgi >= 0 && sgi < nseg) {
+          const int w_lo = sgi == 0 ? 0 : b0, w_hi = sgi == 0 ? nwA : kNW;
+          const int xs = sgi == 0 ? strad : -1;   // the straddler's A piece lives in slot 16
+          for (int w = w_lo; w < w_hi; ++w) M = fmaxf(M, wm[(w == xs ? kSlots - 1 : w) * 4 + g]);
+          if (wslot) {
+            const float mv = wm[sl * 4 + g];
+            f = (M == -INFINITY || mv == -INFINITY) ? 0.f : ex2_approx(mv - M);   // empty piece: 0
+          }
+        }
+        if (wslot) sfw[tid] = f;
+        else sMx[tid - kSlots * 4] = M;
+      }
+      __syncthreads();
 #pragma unroll 1
       for (int idx = tid; idx < nseg * 512; idx += kThreads) {
         const int sgi = idx >> 9, g = (idx >> 7) & 3, dim = idx & 127;
         const int w_lo = sgi == 0 ? 0 : b0, w_hi = sgi == 0 ? nwA : kNW;
         const int xs = sgi == 0 ? strad : -1;   // the straddler's A piece lives in slot 16
-        float M = -INFINITY;
-#pragma unroll 4
-        for (int w = w_lo; w < w_hi; ++w) M = fmaxf(M, wm[(w == xs ? kSlots - 1 : w) * 4 + g]);
+        const float M = sMx[sgi * 4 + g];
         float ov = 0.f, lsum = 0.f;
         if (M != -INFINITY) {
 #pragma unroll 4
           for (int w = w_lo; w < w_hi; ++w) {
             const int sl = w == xs ? kSlots - 1 : w;
-            const float mv = wm[sl * 4 + g];
-            if (mv == -INFINITY) continue;   // an empty piece
-            const float f = ex2_approx(mv - M);
+            const float f = sfw[sl * 4 + g];
             lsum += f * wl[sl * 4 + g];
             ov += f * wacc[(sl * 4 + g) * kWRow + dim];
           }
