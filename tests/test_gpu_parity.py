@@ -354,6 +354,16 @@ def test_cfg4_full_size_sampled_units():
     _sampled_units_check(1, 196608, 2, seed=42)
 
 
+@pytest.mark.parametrize("B,N,kind", [(16, 32768, "stream"), (8, 32768, "stream"), (4, 32768, "split"),
+                                      (2, 32768, "split")])
+def test_mid_batch_auto_plan_sampled_units(B, N, kind):
+    """B*H_kv < #SMs: AUTO picks the stream partition when the cost model says the split plan's
+    waves waste more SMs (B = 8, 16 at 32k) and the split kernel otherwise; both checked on
+    sampled units at the full shape."""
+    assert vi.attn_kernel_kind(B, 8, N) == kind
+    _sampled_units_check(B, N, 3, seed=43 + B)
+
+
 # ------------------------------------------------- fused decode step (append + attention)
 @pytest.mark.parametrize("splits", [0, 1, 3, 8, 18])
 @pytest.mark.parametrize("lens", [[2048], [1500, 37], [33, 1]])
