@@ -181,7 +181,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     import synth
     from paper_2510_06175_b200 import vecinfer as vi
-    from paper_2510_06175_b200.sharding import batch_shard, gather_partials_packed, shard_range
+    from paper_2510_06175_b200.sharding import P2PExchange, batch_shard, gather_partials_packed, shard_range
 
     dev = torch.device("cuda", local_rank if args.backend == "nccl" else local_rank % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
@@ -276,17 +276,29 @@ def run_ours(args, rank, world, local_rank):
         if ev_pair is not None:
             ev_pair[1].record()
 
+    # sequence-sharded exchange: the fused peer-memory kernel (vecinfer_merge_lse_p2p: remote stores
+    # into every rank's IPC window + flags + rank-order merge, one launch) or NCCL all-gather +
+    # vecinfer_merge_lse (--exchange nccl)
+    p2p = P2PExchange(L * B * H_Q, D, dev) if (seq_sharded and args.exchange == "p2p") else None
+    lse_m = torch.empty(L * B, H_Q, dtype=torch.float32, device=dev) if seq_sharded else None
+
+    def exchange_and_merge():
+        if p2p is not None:
+            p2p.merge(o_part.view(L * B, H_Q, D), lse_all.view(L * B, H_Q), out=o_all.view(L * B, H_Q, D), lse=lse_m)
+            return
+        if args.backend == "gloo":
+            o_g, l_g = gather_partials_packed(o_part.cpu(), lse_all.cpu())
+            o_g, l_g = o_g.to(dev), l_g.to(dev)
+        else:
+            o_g, l_g = gather_partials_packed(o_part, lse_all)
+        vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
+                     o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D), lse=lse_m)
+
     def step_eager(evs=None):
         for l in range(L):
             layer(l, None if evs is None else evs[l])
-        if seq_sharded:   # one all-gather of the per-rank partials of all 32 layers, then LSE merge
-            if args.backend == "gloo":
-                o_g, l_g = gather_partials_packed(o_part.cpu(), lse_all.cpu())
-                o_g, l_g = o_g.to(dev), l_g.to(dev)
-            else:
-                o_g, l_g = gather_partials_packed(o_part, lse_all)
-            vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
-                         o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D))
+        if seq_sharded:   # exchange the per-rank partials of all 32 layers, then LSE merge
+            exchange_and_merge()
 
     append_kernels = 2 if max(kbits, vbits) == 16 else 1      # 16-bit: centroid-split search + finalize
     if fused:
@@ -389,13 +401,7 @@ def run_ours(args, rank, world, local_rank):
                 vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
                                lse=lse_all[l], workspace=ws[l])
         if seq_sharded:
-            if args.backend == "gloo":
-                o_g, l_g = gather_partials_packed(o_part.cpu(), lse_all.cpu())
-                o_g, l_g = o_g.to(dev), l_g.to(dev)
-            else:
-                o_g, l_g = gather_partials_packed(o_part, lse_all)
-            vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
-                         o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D))
+            exchange_and_merge()
 
     g_e2e = None
     if use_graph:   # the serving pattern: the 32 layer calls captured once, replayed per token
@@ -466,6 +472,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": args.workload, "desc": desc, "global_batch": B_glob, "seq_len": N,
                    "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": f"K-{CB_NAME[kbits]}/V-{CB_NAME[vbits]}",
                    "parallelism": ("seq-shard" if seq_sharded else "dp") + str(world),
+                   "exchange": (("p2p-fused-merge" if args.exchange == "p2p" else "nccl-allgather+merge_lse")
+                                if seq_sharded else None),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
                    "num_splits": S, "attn_kernel": kernel_kind, "cuda_graph": use_graph, "residual_window": R, "fused_append": fused_launch,
                    "dtype_detail": "u8 codes, bf16 q/k/v/o, fp16 hi/lo MMA operands, f32 accumulate"},
@@ -508,6 +516,8 @@ def main():
     ap.add_argument("--residual", type=int, default=0,
                     help="full-precision residual window of R tokens (P:494: 128); the step appends into it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="cfg4 at N>1: fused peer-memory exchange+merge kernel, or NCCL all-gather + merge_lse")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=2.0)
     args = ap.parse_args()

@@ -119,6 +119,7 @@ typedef struct {
 /* Device-side error bits written (atomicOr) into the optional err_flags word of encode_kv. */
 #define VECINFER_FLAG_RANGE 1u     /* |k * inv_lambda| >= 2^32: outside the pinned fixed point */
 #define VECINFER_FLAG_WRITE_POS 2u /* write_pos[b] + t outside [0, n_cap): row not written     */
+#define VECINFER_FLAG_P2P_TIMEOUT 4u /* vecinfer_merge_lse_p2p: a peer's partial did not arrive  */
 
 /* Programmatic dependent launch: every kernel is launched with PDL and reads only the static
  * weights (codebooks) before griddepcontrol.wait, so codebooks must not be produced by the
@@ -357,6 +358,42 @@ vecinfer_status_t vecinfer_kmeans_step(const float* X, int64_t n, int32_t d, con
                                        int32_t k, float* C_new, int32_t* assign, float* best,
                                        double* objective, void* workspace, size_t workspace_bytes,
                                        vecinfer_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Cross-GPU exchange fused with the LSE merge over peer memory (sequence-sharded
+ * 196k decoding, BASELINE configs[3]).  The all-gather + vecinfer_merge_lse pair becomes ONE
+ * kernel: every rank stores its partial rows straight into every peer's window (CUDA IPC mapping;
+ * NVLink / NVSwitch P2P between GPUs), raises a per-row flag, waits for the P flags of its own
+ * window and merges the P partials in rank order with vecinfer_merge_lse's arithmetic (bitwise the
+ * same result on every rank, and the same as all-gather + merge_lse).
+ *
+ * Setup (not on the hot path; these calls allocate / map and synchronise):
+ *   vecinfer_p2p_window_bytes(P, rows, D)      window size for P ranks, rows = B * H_q rows of D.
+ *   vecinfer_p2p_window_create(bytes, &w, h)   cudaMalloc + zero the own window, export its CUDA
+ *                                              IPC handle h (64 bytes) for the peers.
+ *   vecinfer_p2p_window_open(h, &w)            map a peer's window (cudaIpcOpenMemHandle).
+ *   vecinfer_p2p_window_close(w) / _destroy(w) unmap a peer's window / free the own window.
+ * vecinfer_merge_lse_p2p:
+ *   o_local, lse_local  this rank's normalised partial fp32 [B, H_q, D] / [B, H_q] (natural log).
+ *   windows             DEVICE array of P window pointers as mapped in this process, windows[rank]
+ *                       = the own window; every rank must pass the same P, B, H_q, D.
+ *   epoch               1, 2, 3, ... (0 reserved); the same sequence on every rank, one per call;
+ *                       slots are double-buffered by epoch parity.
+ *   o, o_dtype, lse     merged output [B, H_q, D] / [B, H_q].
+ *   err_flags           device uint32 (may be NULL): VECINFER_FLAG_P2P_TIMEOUT if a peer's rows
+ *                       did not arrive within 5 s (outputs are then zero / -inf, never a hang).
+ * Errors: INVALID_ARG, SHAPE (P, rank, D <= 1024), CUDA.
+ * ------------------------------------------------------------------------------------- */
+size_t vecinfer_p2p_window_bytes(int32_t P, int64_t rows, int32_t D);
+vecinfer_status_t vecinfer_p2p_window_create(size_t bytes, void** window, void* ipc_handle);
+vecinfer_status_t vecinfer_p2p_window_open(const void* ipc_handle, void** window);
+vecinfer_status_t vecinfer_p2p_window_close(void* window);
+vecinfer_status_t vecinfer_p2p_window_destroy(void* window);
+vecinfer_status_t vecinfer_merge_lse_p2p(const float* o_local, const float* lse_local,
+                                         void* const* windows, int32_t P, int32_t rank, int32_t B,
+                                         int32_t H_q, int32_t D, uint32_t epoch, void* o,
+                                         vecinfer_dtype_t o_dtype, float* lse, uint32_t* err_flags,
+                                         vecinfer_stream_t stream);
 
 /* Diagnostics: how many thread-block clusters of `cluster_size` CTAs of the attention kernel can
  * be co-resident on the current device (0 = not schedulable); used by the split planner. */

@@ -44,6 +44,13 @@ PROTOTYPES = {
     "vecinfer_status_string": (c_char_p, [c_i32]),
     "vecinfer_calibrate_workspace_bytes": (c_sz, [c_i32, c_i32]),
     "vecinfer_kmeans_workspace_bytes": (c_sz, [c_i32, c_i32]),
+    "vecinfer_p2p_window_bytes": (c_sz, [c_i32, c_i64, c_i32]),
+    "vecinfer_p2p_window_create": (c_i32, [c_sz, c_void_p, c_void_p]),
+    "vecinfer_p2p_window_open": (c_i32, [c_void_p, c_void_p]),
+    "vecinfer_p2p_window_close": (c_i32, [c_void_p]),
+    "vecinfer_p2p_window_destroy": (c_i32, [c_void_p]),
+    "vecinfer_merge_lse_p2p": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_i32, c_u32,
+                                       c_void_p, c_i32, c_void_p, c_void_p, c_void_p]),
     "vecinfer_kmeans_step": (c_i32, [c_void_p, c_i64, c_i32, c_void_p, c_i32, c_void_p, c_void_p, c_void_p, c_void_p,
                                      c_void_p, c_sz, c_void_p]),
     "vecinfer_calibrate_smooth": (c_i32, [c_void_p, c_i64, c_i32, c_i32, c_i64, c_i64, c_f32, c_void_p, c_void_p,

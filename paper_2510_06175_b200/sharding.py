@@ -64,3 +64,86 @@ def gather_partials_packed(o_local: torch.Tensor, lse_local: torch.Tensor, group
     no = o_local.numel()
     return (out[:, :no].reshape((world,) + tuple(o_local.shape)),
             out[:, no:].reshape((world,) + tuple(lse_local.shape)).contiguous())
+
+
+class P2PExchange:
+    """Fused cross-GPU exchange + LSE merge over peer memory (vecinfer_merge_lse_p2p): the
+    replacement for gather_partials_packed + vecinfer_merge_lse on the sequence-sharded path.
+
+    Setup (collective over `group`, any backend that can all_gather_object): every rank creates its
+    window (library cudaMalloc) and exports a CUDA IPC handle; the handles are all-gathered and the
+    peers' windows mapped.  merge() then runs ONE kernel per call: remote stores of this rank's
+    partial rows into every window, per-row release flags, acquire-polling of the own window, and
+    the rank-order merge.  Ranks must call merge() the same number of times with the same shapes.
+    """
+
+    def __init__(self, rows_max: int, D: int, device: torch.device, group=None):
+        import ctypes
+
+        from . import _lib
+        self._lib = _lib.load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.rows_max, self.D, self.device = rows_max, D, device
+        nbytes = self._lib.vecinfer_p2p_window_bytes(self.world, rows_max, D)
+        own = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        with torch.cuda.device(device):
+            _lib.check("vecinfer_p2p_window_create",
+                       self._lib.vecinfer_p2p_window_create(nbytes, ctypes.addressof(own), ctypes.addressof(handle)))
+        self._own = own.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        ptrs = []
+        self._opened = []
+        with torch.cuda.device(device):
+            for p, h in enumerate(handles):
+                if p == self.rank:
+                    ptrs.append(self._own)
+                    continue
+                w = ctypes.c_void_p()
+                hb = (ctypes.c_char * 64).from_buffer_copy(h)
+                _lib.check("vecinfer_p2p_window_open",
+                           self._lib.vecinfer_p2p_window_open(ctypes.addressof(hb), ctypes.addressof(w)))
+                ptrs.append(w.value)
+                self._opened.append(w.value)
+        self.windows = torch.tensor(ptrs, dtype=torch.int64, device=device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self.epoch = 0
+        self._group = group
+
+    def merge(self, o_local: torch.Tensor, lse_local: torch.Tensor, out: torch.Tensor | None = None,
+              lse: torch.Tensor | None = None, o_dtype: torch.dtype = torch.float32):
+        """o_local fp32 [B, H_q, D], lse_local fp32 [B, H_q] -> merged (o, lse) on every rank."""
+        import ctypes
+
+        from . import _lib
+        B, Hq, D = o_local.shape
+        if B * Hq > self.rows_max or D != self.D:
+            raise ValueError("partials larger than the window")
+        if not (o_local.is_contiguous() and lse_local.is_contiguous()):
+            raise ValueError("partials must be contiguous")
+        if out is None:
+            out = torch.empty(B, Hq, D, dtype=o_dtype, device=o_local.device)
+        if lse is None:
+            lse = torch.empty(B, Hq, dtype=torch.float32, device=o_local.device)
+        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 1
+        stream = ctypes.c_void_p(torch.cuda.current_stream(o_local.device).cuda_stream)
+        _lib.check("vecinfer_merge_lse_p2p", self._lib.vecinfer_merge_lse_p2p(
+            ctypes.c_void_p(o_local.data_ptr()), ctypes.c_void_p(lse_local.data_ptr()),
+            ctypes.c_void_p(self.windows.data_ptr()), self.world, self.rank, B, Hq, D, self.epoch,
+            ctypes.c_void_p(out.data_ptr()), 1 if out.dtype == torch.float32 else 0, ctypes.c_void_p(lse.data_ptr()),
+            ctypes.c_void_p(self.err.data_ptr()), stream))
+        return out, lse
+
+    def close(self):
+        """Unmap the peers' windows and free the own one (collective: call on every rank)."""
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self._group)
+        for w in self._opened:
+            self._lib.vecinfer_p2p_window_close(w)
+        self._opened = []
+        dist.barrier(group=self._group)
+        if self._own:
+            self._lib.vecinfer_p2p_window_destroy(self._own)
+            self._own = None

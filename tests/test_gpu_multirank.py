@@ -71,3 +71,82 @@ def test_sequence_sharded_two_ranks_one_gpu():
     assert np.array_equal(o0, o1) and np.array_equal(l0, l1)        # identical on every rank
     rel = np.abs(o0 - oref).max(-1) / np.abs(oref).max(-1)
     assert rel.max() <= 2e-3 and np.abs(l0 - lref).max() <= 2e-3
+
+
+# ------------------------------------------- fused peer-memory exchange + merge
+def _rank_p2p(rank, world, port, outq):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        from helpers import load_codebooks
+        from paper_2510_06175_b200 import vecinfer as vi
+        from paper_2510_06175_b200.sharding import P2PExchange, shard_range
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        B, HQ, D = 2, 32, 128
+        ex = P2PExchange(B * HQ, D, dev)
+        results = []
+        # 1. several exchanges through the same windows (both slot parities, changing data): the
+        #    fused kernel must equal vecinfer_merge_lse over all ranks' partials, bit for bit
+        for it in range(5):
+            parts = []
+            for r in range(world):   # every rank can regenerate every rank's partial (seeded)
+                g = torch.Generator().manual_seed(1000 * it + r)
+                o = torch.randn(B, HQ, D, generator=g)
+                L = torch.randn(B, HQ, generator=g) * 4
+                if it == 3 and r == 1:
+                    L[0, :5] = -float("inf")          # empty shards for some rows
+                    o[0, :5] = 0
+                parts.append((o, L))
+            o_p, l_p = parts[rank][0].to(dev), parts[rank][1].to(dev)
+            o_m, l_m = ex.merge(o_p.contiguous(), l_p.contiguous())
+            o_r, l_r = vi.merge_lse(torch.stack([p[0] for p in parts]).to(dev).contiguous(),
+                                    torch.stack([p[1] for p in parts]).to(dev).contiguous())
+            torch.cuda.synchronize()
+            results.append((o_m.cpu().numpy(), l_m.cpu().numpy(), o_r.cpu().numpy(), l_r.cpu().numpy()))
+        # 2. the sequence-sharded attention pattern (configs[3]): shard -> fused exchange -> o
+        cb = load_codebooks()
+        N = 4000
+        lam = torch.from_numpy(cb["lambda"]).to(dev)
+        ck = torch.from_numpy(cb["ck_b2d4"]).to(dev).to(torch.bfloat16)
+        cv = torch.from_numpy(cb["cv_b2d4"]).to(dev).to(torch.bfloat16)
+        kc = synth.gen_codes_torch((1, 8, N, 32), 8, seed=15, device=dev)
+        vc = synth.gen_codes_torch((1, 8, N, 32), 8, seed=16, device=dev)
+        q = torch.from_numpy(synth.gen_queries(1, 32, 8, 128, seed=17)).to(dev).to(torch.bfloat16)
+        seq = torch.tensor([N], dtype=torch.int32, device=dev)
+        b, e = shard_range(N, rank, world)
+        o_p, l_p = vi.attn_decode(q, lam, ck, cv, kc, vc, seq, tok_begin=b, tok_end=e)
+        o_s, l_s = ex.merge(o_p.contiguous(), l_p.contiguous())
+        o_full, l_full = vi.attn_decode(q, lam, ck, cv, kc, vc, seq)
+        torch.cuda.synchronize()
+        err = int(ex.err.item())
+        ex.close()
+        outq.put((rank, results, o_s.cpu().numpy(), l_s.cpu().numpy(), o_full.cpu().numpy(), l_full.cpu().numpy(), err))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_fused_exchange_two_ranks_one_gpu():
+    """vecinfer_merge_lse_p2p with two ranks sharing one B200 (CUDA IPC windows on the same device;
+    on an 8-GPU box the same stores go over NVLink): bitwise equal to all-gather + merge_lse on
+    every rank, across repeated exchanges (slot parity, empty rows), and the sharded attention it
+    assembles matches the unsharded kernel within 2e-3."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_p2p, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in ps), key=lambda x: x[0])
+    for p in ps:
+        p.join(timeout=60)
+    for rank, results, o_s, l_s, o_full, l_full, err in res:
+        assert err == 0, "peer partial timed out"
+        for o_m, l_m, o_r, l_r in results:
+            assert np.array_equal(o_m, o_r) and np.array_equal(l_m, l_r)
+        rel = np.abs(o_s - o_full).max(-1) / np.abs(o_full).max(-1)
+        assert rel.max() <= 2e-3 and np.abs(l_s - l_full).max() <= 2e-3
+    assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
