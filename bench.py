@@ -312,7 +312,8 @@ def run_ours(args, rank, world, local_rank):
             step_eager()
     torch.cuda.synchronize(dev)
 
-    use_graph = not args.no_graph and not seq_sharded   # NCCL all-gather kept eager
+    # NCCL all-gather kept eager; the fused P2P exchange keeps its epoch on the device: graph-safe
+    use_graph = not args.no_graph and (not seq_sharded or p2p is not None)
     K, W = args.steps, args.warmup
     if use_graph:
         g_step = torch.cuda.CUDAGraph()

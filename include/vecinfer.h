@@ -377,8 +377,10 @@ vecinfer_status_t vecinfer_kmeans_step(const float* X, int64_t n, int32_t d, con
  *   o_local, lse_local  this rank's normalised partial fp32 [B, H_q, D] / [B, H_q] (natural log).
  *   windows             DEVICE array of P window pointers as mapped in this process, windows[rank]
  *                       = the own window; every rank must pass the same P, B, H_q, D.
- *   epoch               1, 2, 3, ... (0 reserved); the same sequence on every rank, one per call;
- *                       slots are double-buffered by epoch parity.
+ *   epoch               0 = automatic (a counter in the own window's header, advanced by the
+ *                       kernel itself: graph-capturable); else explicit 1, 2, 3, ...  Either way
+ *                       every rank must make the same sequence of calls (slots are double-buffered
+ *                       by epoch parity; do not mix explicit and automatic on one window).
  *   o, o_dtype, lse     merged output [B, H_q, D] / [B, H_q].
  *   err_flags           device uint32 (may be NULL): VECINFER_FLAG_P2P_TIMEOUT if a peer's rows
  *                       did not arrive within 5 s (outputs are then zero / -inf, never a hang).

@@ -66,16 +66,18 @@ extern "C" vecinfer_status_t vecinfer_merge_lse(const float* o_parts, const floa
 namespace vecinfer {
 namespace {
 
+// window = [256-byte header: u32 epoch counter, u32 CTA-done counter][data][flags]
 struct P2PLayout {
   int64_t rows;
   int P, D;
+  static constexpr int64_t kHeader = 256;
   __host__ __device__ int64_t data_off(int par, int src, int64_t row) const {   // floats
-    return ((static_cast<int64_t>(par) * P + src) * rows + row) * (D + 1);
+    return kHeader / 4 + ((static_cast<int64_t>(par) * P + src) * rows + row) * (D + 1);
   }
   __host__ __device__ int64_t flag_off_bytes(int par, int src, int64_t row) const {
-    return 2ll * P * rows * (D + 1) * 4 + ((static_cast<int64_t>(par) * P + src) * rows + row) * 4;
+    return kHeader + 2ll * P * rows * (D + 1) * 4 + ((static_cast<int64_t>(par) * P + src) * rows + row) * 4;
   }
-  __host__ __device__ int64_t bytes() const { return 2ll * P * rows * ((D + 1) * 4 + 4); }
+  __host__ __device__ int64_t bytes() const { return kHeader + 2ll * P * rows * ((D + 1) * 4 + 4); }
 };
 
 __device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
@@ -96,8 +98,21 @@ __global__ void merge_lse_p2p_kernel(const float* __restrict__ o_local, const fl
                                      void* const* __restrict__ windows, P2PLayout lay, int rank, uint32_t epoch,
                                      void* o, int o_f32, float* lse, uint32_t* err, unsigned long long timeout_ns) {
   const int64_t row = blockIdx.x;
-  const int D = lay.D, P = lay.P, par = static_cast<int>(epoch & 1u);
+  const int D = lay.D, P = lay.P;
   __shared__ int s_ok;
+  __shared__ uint32_t s_epoch;
+  // epoch 0 = automatic: the own window's header counter + 1 (every CTA reads it before the last
+  // CTA of this launch advances it; the next launch on the stream starts after this one ends), so
+  // the exchange can be captured in a CUDA graph and replayed
+  uint32_t* hdr = static_cast<uint32_t*>(windows[rank]);
+  if (threadIdx.x == 0) {
+    uint32_t e = epoch;
+    if (e == 0) { e = *reinterpret_cast<volatile uint32_t*>(hdr) + 1u; if (e == 0) e = 1u; }
+    s_epoch = e;
+  }
+  __syncthreads();
+  epoch = s_epoch;
+  const int par = static_cast<int>(epoch & 1u);
   // 1. publish this rank's partial row into every window (own included)
   for (int p = 0; p < P; ++p) {
     float* dst = static_cast<float*>(windows[p]) + lay.data_off(par, rank, row);
@@ -143,6 +158,13 @@ __global__ void merge_lse_p2p_kernel(const float* __restrict__ o_local, const fl
     if (o_f32) static_cast<float*>(o)[row * D + d] = v;
     else static_cast<__nv_bfloat16*>(o)[row * D + d] = __float2bfloat16_rn(v);
     if (d == 0 && lse) lse[row] = empty ? -INFINITY : M + __logf(wsum);
+  }
+  if (threadIdx.x == 0) {   // the last CTA of the launch records the epoch it used (automatic mode)
+    __threadfence();
+    if (atomicAdd(hdr + 1, 1u) == gridDim.x - 1) {
+      hdr[1] = 0u;
+      hdr[0] = epoch;
+    }
   }
 }
 
@@ -204,7 +226,6 @@ extern "C" vecinfer_status_t vecinfer_merge_lse_p2p(const float* o_local, const 
   if (o_dtype != VECINFER_BF16 && o_dtype != VECINFER_F32) return fail(VECINFER_ERR_INVALID_ARG, "merge_lse_p2p: bad o_dtype");
   if (P <= 0 || B <= 0 || H_q <= 0 || D <= 0 || D > 1024) return fail(VECINFER_ERR_SHAPE, "merge_lse_p2p: bad size");
   if (rank < 0 || rank >= P) return fail(VECINFER_ERR_SHAPE, "merge_lse_p2p: rank %d outside [0, %d)", rank, P);
-  if (epoch == 0) return fail(VECINFER_ERR_INVALID_ARG, "merge_lse_p2p: epoch 0 is reserved (windows start zeroed)");
   const int64_t rows = static_cast<int64_t>(B) * H_q;
   if (rows > 2147483647) return fail(VECINFER_ERR_SHAPE, "merge_lse_p2p: too many rows");
   const P2PLayout lay{rows, P, D};

@@ -127,11 +127,11 @@ class P2PExchange:
             out = torch.empty(B, Hq, D, dtype=o_dtype, device=o_local.device)
         if lse is None:
             lse = torch.empty(B, Hq, dtype=torch.float32, device=o_local.device)
-        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 1
+        self.epoch += 1   # calls made (the kernel keeps the exchange epoch on the device: graph-safe)
         stream = ctypes.c_void_p(torch.cuda.current_stream(o_local.device).cuda_stream)
         _lib.check("vecinfer_merge_lse_p2p", self._lib.vecinfer_merge_lse_p2p(
             ctypes.c_void_p(o_local.data_ptr()), ctypes.c_void_p(lse_local.data_ptr()),
-            ctypes.c_void_p(self.windows.data_ptr()), self.world, self.rank, B, Hq, D, self.epoch,
+            ctypes.c_void_p(self.windows.data_ptr()), self.world, self.rank, B, Hq, D, 0,
             ctypes.c_void_p(out.data_ptr()), 1 if out.dtype == torch.float32 else 0, ctypes.c_void_p(lse.data_ptr()),
             ctypes.c_void_p(self.err.data_ptr()), stream))
         return out, lse

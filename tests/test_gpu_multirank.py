@@ -107,6 +107,31 @@ def _rank_p2p(rank, world, port, outq):
                                     torch.stack([p[1] for p in parts]).to(dev).contiguous())
             torch.cuda.synchronize()
             results.append((o_m.cpu().numpy(), l_m.cpu().numpy(), o_r.cpu().numpy(), l_r.cpu().numpy()))
+        # 1b. the exchange captured once in a CUDA graph and replayed (the epoch lives on the device)
+        o_in = torch.empty(B, HQ, D, device=dev)
+        l_in = torch.empty(B, HQ, device=dev)
+        o_out = torch.empty(B, HQ, D, device=dev)
+        l_out = torch.empty(B, HQ, device=dev)
+        o_in.zero_(); l_in.zero_()
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ex.merge(o_in, l_in, out=o_out, lse=l_out)
+        for it in range(5, 9):
+            parts = []
+            for r in range(world):
+                gen = torch.Generator().manual_seed(1000 * it + r)
+                parts.append((torch.randn(B, HQ, D, generator=gen), torch.randn(B, HQ, generator=gen) * 4))
+            o_in.copy_(parts[rank][0].to(dev))
+            l_in.copy_(parts[rank][1].to(dev))
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            o_r, l_r = vi.merge_lse(torch.stack([p[0] for p in parts]).to(dev).contiguous(),
+                                    torch.stack([p[1] for p in parts]).to(dev).contiguous())
+            torch.cuda.synchronize()
+            results.append((o_out.cpu().numpy(), l_out.cpu().numpy(), o_r.cpu().numpy(), l_r.cpu().numpy()))
         # 2. the sequence-sharded attention pattern (configs[3]): shard -> fused exchange -> o
         cb = load_codebooks()
         N = 4000
