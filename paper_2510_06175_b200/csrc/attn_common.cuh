@@ -184,8 +184,8 @@ template <int NTHREADS, int NWARPS, int WROW = 128, int DH = 128, bool PRESCALED
 __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s,
                                            const float* wm, const float* wl, const float* wacc,
                                            float* scratch) {
-  // PRESCALED: the warps already rescaled their partials to the CTA-wide running max of each head
-  // (wm[w][g] == that max for every w), so the combine is a plain sum over the warps.
+  // PRESCALED: the warps already rescaled their partials to the CTA-wide running max M of each head
+  // (M = max_w wm[w][g]), so the combine is a plain sum over the warps.
   const int tid = threadIdx.x;
   const int64_t unit = static_cast<int64_t>(b) * a.Hkv + h;
   const HeadMap hm = head_map(a, h);
@@ -196,9 +196,9 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     float M = -INFINITY;
     float osum = 0.f, lsum = 0.f;
     if constexpr (PRESCALED) {
-      M = wm[g];
 #pragma unroll
       for (int w = 0; w < NWARPS; ++w) {
+        M = fmaxf(M, wm[w * 4 + g]);
         lsum += wl[w * 4 + g];
         osum += wacc[(w * 4 + g) * WROW + dim];
       }

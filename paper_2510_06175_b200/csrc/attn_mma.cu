@@ -462,10 +462,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   }
 
   // ---- warp partials -> shared memory, rescaled to the CTA-wide running max of each head: every
-  // warp posts m_run, reads the 16 maxima back (a warp that overwrote its slot with the max already
-  // leaves the max unchanged) and stores f*acc, f*l with f = 2^(m_run - M); wm then holds M for
-  // every warp, so the combine (cta_finish<PRESCALED>, or the cluster path's generic one with
-  // f = 1) is a plain sum over the warps
+  // warp posts m_run, reads the 16 maxima back and stores f*acc, f*l with f = 2^(m_run - M), so the
+  // combine (cta_finish<PRESCALED>, or the cluster path with f = 1) is a max over wm plus a plain
+  // sum over the warps
   phase_mark(a.phase, cta_id, 2);
   griddep_launch_dependents();   // the next kernel may start its (static) prologue
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 4);
@@ -480,10 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 #pragma unroll
   for (int w = 0; w < kNW; ++w) Mh = fmaxf(Mh, wm[w * 4 + j]);
   const float fsc = m_run == -INFINITY ? 0.f : ex2_approx(m_run - Mh);
-  if (r == 0) {
-    wm[warp * 4 + j] = Mh;
-    wl[warp * 4 + j] = l_run * fsc;
-  }
+  if (r == 0) wl[warp * 4 + j] = l_run * fsc;   // (wm keeps the per-warp maxima: no write-after-read race)
   // thread (r, j): head j, dims (DH/8)r .. (DH/8)r + DH/8 - 1; MMA slots [t][0] + [t][1] hold dim
   // (DH/8)r + 2t, [t][2] + [t][3] dim (DH/8)r + 2t + 1 (hi + lo parts)
   float* dst = wacc + (warp * 4 + j) * kWRow + (DH / 8) * r;
@@ -511,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     if (M != -INFINITY) {
 #pragma unroll
       for (int w = 0; w < kNW; ++w) {
-        const float f = ex2_approx(wm[w * 4 + g] - M);
+        const float f = 1.f;   // partials are pre-scaled to the CTA max M
         lsum += f * wl[w * 4 + g];
         osum += f * wacc[(w * 4 + g) * kWRow + dim];
       }
