@@ -19,7 +19,7 @@
  *    non-OK status of the calling thread.
  *  - Thread-safe: no global mutable state except the thread-local error string and a
  *    per-device attribute cache.
- *  - Supported shapes (ABI v4): head_dim D in {128, 64}, sub_dim d = 4, code_bits in {4, 8, 16}
+ *  - Supported shapes (ABI v5): head_dim D in {128, 64}, sub_dim d = 4, code_bits in {4, 8, 16}
  *    (b1d4, b2d4, b4d4 in BASELINE.json notation = paper d4b4, d4b8, d4b16), K and V
  *    widths independent; GQA group G = H_q / H_kv in 1..8; contiguous or paged code caches.
  *    D = 64 runs the split attention kernel only (no residual window, no fused append).
@@ -29,6 +29,9 @@
  *    DEQUANT_MMA kernel (contiguous or paged, residual window allowed; no stream / LUT variant,
  *    decode_step appends with a separate encode launch).
  *    Anything else returns VECINFER_ERR_UNSUPPORTED.
+ *  - ABI v5 adds: n_tokens_max in vecinfer_attn_kernel_kind (the stream/split choice is a cost
+ *    model over it), vecinfer_kmeans_step (GPU codebook Lloyd iteration) and the fused
+ *    cross-GPU exchange + merge over peer memory (vecinfer_p2p_window_*, vecinfer_merge_lse_p2p).
  */
 #ifndef VECINFER_H_
 #define VECINFER_H_
