@@ -70,7 +70,10 @@ struct AttnArgs {
 
 // extra tokens' worth of work the split owning the appended row does (its encode), used to
 // shorten that split so it does not become the straggler
-constexpr int64_t kAppendTokenCost = 160;
+#ifndef VECINFER_APPEND_TOKEN_COST
+#define VECINFER_APPEND_TOKEN_COST 512   // measured: 0 / 160 / 320 / 512 -> 512 best (cfg3, cfg4 fused steps)
+#endif
+constexpr int64_t kAppendTokenCost = VECINFER_APPEND_TOKEN_COST;
 
 // GQA groups of up to 8 query heads run as hsplit = ceil(G/4) virtual KV heads of <= 4 query
 // heads each: virtual head h reads the codes, codebooks and lambda of KV head hc = h / hsplit and
