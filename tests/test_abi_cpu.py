@@ -80,6 +80,13 @@ def test_argument_validation_without_cuda(lib):
     assert lib.vecinfer_kmeans_step(p, 100, 4, p, 16, p, p, p, p, p, 16, None) == 6
     assert lib.vecinfer_kmeans_step(None, 100, 4, p, 16, p, p, p, p, p, 1 << 20, None) == 1
     assert lib.vecinfer_kmeans_workspace_bytes(256, 4) >= 256 * 4 * 8 + 256 * 4
+    # fused P2P exchange (§8(e)): window size = header + 2 parities x P x rows x ((D + 1) fp32 + flag)
+    assert lib.vecinfer_p2p_window_bytes(8, 1024, 128) == 256 + 2 * 8 * 1024 * (129 * 4 + 4)
+    assert lib.vecinfer_p2p_window_bytes(0, 1024, 128) == 0
+    assert lib.vecinfer_merge_lse_p2p(p, p, p, 2, 2, 1, 32, 128, 0, p, 1, p, None, None) == 2   # rank >= P
+    assert lib.vecinfer_merge_lse_p2p(p, p, p, 2, 0, 1, 32, 2048, 0, p, 1, p, None, None) == 2  # D > 1024
+    assert lib.vecinfer_merge_lse_p2p(None, p, p, 2, 0, 1, 32, 128, 0, p, 1, p, None, None) == 1
+    assert lib.vecinfer_p2p_window_create(0, p, p) == 1
 
 
 def test_workspace_and_split_queries(lib):
