@@ -392,6 +392,40 @@ def test_decode_step_fused_equals_encode_then_attend(splits, lens):
     _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))
 
 
+@pytest.mark.parametrize("B,N", [(1, 32768), (1, 196608), (64, 8192)])
+def test_decode_step_fused_full_size_bench_config(B, N):
+    """The bench's step at BASELINE configs[1] / [3] / [2] sizes: vecinfer_decode_step with the
+    fused append at row N-1 (AUTO plan: split S = 18 with the owner's 512-token budget, or the
+    stream partition at B = 64).  The appended codes equal the oracle's for every (b, h); the
+    output of sampled units equals the oracle over the updated cache."""
+    rng = np.random.default_rng(B + N)
+    q = synth.gen_queries(B, 32, 8, 128, seed=91)
+    kc = synth.gen_codes_torch((B, 8, N, 32), 8, seed=92, device=DEV)
+    vc = synth.gen_codes_torch((B, 8, N, 32), 8, seed=93, device=DEV)
+    kn = synth.gen_keys(1, 8, 128, seed=94, batch=B)[:, 0]
+    vn = synth.gen_values(1, 8, 128, seed=95, batch=B)[:, 0]
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    o, L = vi.decode_step(t_bf16(q), t_bf16(kn), t_bf16(vn), t_f32(CB["lambda"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(CB["ck_b2d4"]), t_bf16(CB["cv_b2d4"]), kc, vc, t_i32([N - 1] * B), t_i32([N] * B),
+                          err_flags=err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    o, L = o.cpu().numpy(), L.cpu().numpy()
+    new_k = kc[:, :, N - 1].cpu().numpy()
+    new_v = vc[:, :, N - 1].cpu().numpy()
+    for b in range(B):
+        for h in range(8):
+            kk, vv = ref.encode_kv(kn[b, h], vn[b, h], CB["inv_lambda"][h], CB["ck_b2d4"][h], CB["cv_b2d4"][h])
+            assert np.array_equal(new_k[b, h], kk.astype(np.uint8)) and np.array_equal(new_v[b, h], vv.astype(np.uint8))
+    for _ in range(3):
+        b, h = int(rng.integers(B)), int(rng.integers(8))
+        kk = kc[b, h].cpu().numpy().astype(np.int64)
+        vv = vc[b, h].cpu().numpy().astype(np.int64)
+        o_ref, L_ref = ref.attention_vq(q[b, 4 * h:4 * h + 4], CB["lambda"][h], CB["ck_b2d4"][h], CB["cv_b2d4"][h],
+                                        kk, vv)
+        _assert_close(o[b, 4 * h:4 * h + 4], L[b, 4 * h:4 * h + 4], o_ref, L_ref)
+
+
 def test_decode_step_append_outside_attended_range():
     """write_pos beyond seq_len: the row is written (by split 0) but not attended."""
     c = _attn_case(1, 8, 4, 600, [500], seed=80)
