@@ -18,9 +18,12 @@
 // Shared-memory codebook rows are 256 B: [C_k copies 0..15 | C_v copies 0..15] for centroid c,
 // in a 64 KiB-aligned region, so a gather address is ONE byte-permute: PRMT places code byte k
 // of a code word into address bits 8..15 next to the per-lane base (bits 0..7, 16..31).
-// Epilogue: warps combine through shared memory; splits merge by log-sum-exp in the last CTA
-// of each (b, h_kv), which stages all partials in shared memory first (fixed order s = 0..S-1
-// => deterministic).  See DESIGN.md "Kernel N4".
+// Epilogue: every warp rescales its partial to the CTA-wide running max (f = 2^(m_warp - M)) and
+// the CTA sums the 16 warp partials into the split's (o_s, L_s).  Single-wave grids merge the S
+// splits with the fence-free publish/consume protocol (attn_common.cuh cta_finish: each split
+// merges a 1/S slice of the outputs, one L-lane group per output, fixed butterfly order =>
+// deterministic); multi-wave grids merge in the last-arriving CTA; S <= 16 clusters can merge over
+// DSMEM.  See DESIGN.md "N4".
 #include "attn_tiles.cuh"
 
 namespace vecinfer {
