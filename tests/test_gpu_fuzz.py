@@ -5,6 +5,8 @@ GQA group (1..8), head dim (64/128), K/V code widths (every 4th case a NEXT-2 fo
 fixed or automatic splits, algorithm (auto / split / stream), paged or contiguous codes and a
 residual window, then checks the output against attention_decode_batch (same 2e-3 bars).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -41,9 +43,13 @@ def _paginate(codes, ps, rng):
     return pool, perm.astype(np.int32)
 
 
-@pytest.mark.parametrize("case", range(64))
+_FUZZ_BASE = int(os.environ.get("VECINFER_FUZZ_BASE", "700"))      # wider sweeps: set both variables
+_FUZZ_CASES = int(os.environ.get("VECINFER_FUZZ_CASES", "64"))
+
+
+@pytest.mark.parametrize("case", range(_FUZZ_CASES))
 def test_random_configuration(case):
-    rng = np.random.default_rng(700 + case)
+    rng = np.random.default_rng(_FUZZ_BASE + case)
     D = int(rng.choice([128, 128, 64]))
     B = int(rng.integers(1, 4))
     Hkv = int(rng.choice([1, 2, 8]))
