@@ -310,7 +310,8 @@ def run_ours(args, rank, world, local_rank):
         if seq_sharded:   # exchange the per-rank partials of all 32 layers, then LSE merge
             exchange_and_merge()
 
-    append_kernels = 2 if max(kbits, vbits) == 16 else 1      # 16-bit: centroid-split search + finalize
+    # 16-bit append: one centroid-split search launch (finalised in-kernel) up to 4096 token-heads
+    append_kernels = 2 if (max(kbits, vbits) == 16 and B * H_KV > 4096) else 1
     if fused:
         launches_per_step = L * vi.decode_step_launches(B, H_KV, n_local, kcfg, vcfg, residual_append=bool(R))
     else:

@@ -427,7 +427,10 @@ extern "C" int32_t vecinfer_decode_step_launches(int32_t B, int32_t H_kv, int64_
                                                  int32_t residual_append) {
   if (residual_append) return 1;
   if (decode_fuses(B, H_kv, n_cap, kcfg, vcfg, num_splits, algo)) return 1;
-  return 1 + ((kcfg.code_bits == 16 || vcfg.code_bits == 16) ? 2 : 1);   // 16-bit: split search + finalize
+  // 16-bit append (B*H_kv <= 4096 token-heads): one centroid-split search launch that also
+  // finalises (the last chunk CTA of each token-head); larger batches add a finalize launch
+  const bool big16 = (kcfg.code_bits == 16 || vcfg.code_bits == 16) && static_cast<int64_t>(B) * H_kv > 4096;
+  return 1 + (big16 ? 2 : 1);
 }
 
 extern "C" size_t vecinfer_decode_step_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int64_t n_cap,

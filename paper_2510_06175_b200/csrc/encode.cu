@@ -210,10 +210,15 @@ __global__ void __launch_bounds__(512) encode_append_kernel(EncArgs a) {
 // ------------------------------------------------------------------ 16-bit: centroid split
 // grid (ceil(B*T / kEncWarps), 65536 / kChunk16, H); stage one chunk of C_k and C_v.
 // kSplit (few token-heads, e.g. the decode append): one token-head per CTA and its 8 warps split
-// the chunk (128 centroids each); otherwise one token-head per warp scanning the whole chunk.
+// the chunk (128 centroids each); the K and V chunks are staged together (one barrier) and the
+// last of the 64 chunk CTAs of a token-head finalises its codes (no separate finalize launch).
+// Otherwise one token-head per warp scanning the whole chunk, finalised by encode_nn16_finalize.
+__device__ __forceinline__ void finalize_token_head(const EncArgs& a, int64_t bt, int b, int t, int h, int lane);
+
 template <bool kSplit>
 __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) {
-  __shared__ float4 sc[kChunk16];
+  __shared__ float4 sc[kSplit ? 2 * kChunk16 : kChunk16];
+  __shared__ bool s_last;
   griddep_wait();
   const int h = blockIdx.z;
   const int j0 = blockIdx.y * kChunk16;
@@ -224,19 +229,33 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) 
   const int jw = kSplit ? warp * kSpan : 0;
   const bool live = bt < static_cast<int64_t>(a.B) * a.T;
   const int b = live ? static_cast<int>(bt / a.T) : 0, t = live ? static_cast<int>(bt % a.T) : 0;
-  for (int which = 0; which < 2; ++which) {
-    const int bits = which ? a.vbits : a.kbits;
-    const int n_ent = 1 << bits;
-    __syncthreads();
+  auto stage = [&](int which, float4* dst) {
+    const int n_ent = 1 << (which ? a.vbits : a.kbits);
     if (j0 < n_ent) {
       const uint16_t* cb = which ? (a.cv + h * a.cv_hs) : (a.ck + h * a.ck_hs);
       for (int j = threadIdx.x; j < kChunk16; j += blockDim.x) {
         const uint2 w = *reinterpret_cast<const uint2*>(cb + 4 * (j0 + j));
-        sc[j] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
-                            __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+        dst[j] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                             __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
       }
     }
+  };
+  if constexpr (kSplit) {
+    stage(0, sc);
+    stage(1, sc + kChunk16);
     __syncthreads();
+  }
+  for (int which = 0; which < 2; ++which) {
+    const int bits = which ? a.vbits : a.kbits;
+    const int n_ent = 1 << bits;
+    const float4* tab = sc;
+    if constexpr (kSplit) {
+      tab = sc + which * kChunk16;
+    } else {
+      __syncthreads();
+      stage(which, sc);
+      __syncthreads();
+    }
     if (!live || j0 >= n_ent || bits != 16) continue;
     float x[4];
     if (which == 0) transform_key_lane(a, b, t, h, lane, x);
@@ -245,13 +264,28 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) 
     uint32_t bi = 0;
 #pragma unroll 4
     for (int j = jw; j < jw + kSpan; ++j) {
-      const float4 c = sc[j];
+      const float4 c = tab[j];
       const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
       if (dd < best) { best = dd; bi = j; }
     }
     const unsigned long long packed =
         (static_cast<unsigned long long>(__float_as_uint(best)) << 32) | static_cast<unsigned long long>(j0 + bi);
     atomicMin(a.ws + ((bt * a.H + h) * 2 + which) * 32 + lane, packed);
+  }
+  if constexpr (kSplit) {
+    // the last chunk CTA of this token-head finalises it: counters start at 0xFFFFFFFF (the
+    // per-call 0xFF fill), so arrival k sees k - 1 and the last one (k = gridDim.y - 1) sees
+    // gridDim.y - 2
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(a.ws + static_cast<int64_t>(a.B) * a.T * a.H * 64);
+    __syncthreads();   // every warp's atomicMin precedes thread 0's arrival
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = live && (atomicAdd(cnt + bt * a.H + h, 1u) + 2u == gridDim.y);
+    }
+    __syncthreads();
+    if (!s_last || warp != 0) return;
+    __threadfence();
+    finalize_token_head(a, bt, b, t, h, lane);
   }
 }
 
@@ -268,13 +302,7 @@ __device__ __forceinline__ void small_nn_global(const uint16_t* cb, const float 
   }
 }
 
-__global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_finalize(EncArgs a) {
-  griddep_wait();
-  const int h = blockIdx.y;
-  const int lane = threadIdx.x & 31;
-  const int64_t bt = static_cast<int64_t>(blockIdx.x) * kEncWarps + (threadIdx.x >> 5);
-  if (bt >= static_cast<int64_t>(a.B) * a.T) return;
-  const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
+__device__ __forceinline__ void finalize_token_head(const EncArgs& a, int64_t bt, int b, int t, int h, int lane) {
   int64_t row;
   if (!cache_row(a, b, t, h, lane, row)) return;
   for (int which = 0; which < 2; ++which) {
@@ -283,7 +311,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_finalize(EncArgs a
     uint32_t code;
     if (bits == 16) {
       unsigned long long* slot = a.ws + ((bt * a.H + h) * 2 + which) * 32 + lane;
-      code = static_cast<uint32_t>(*slot & 0xFFFFFFFFull);
+      code = static_cast<uint32_t>(__ldcg(slot) & 0xFFFFFFFFull);
       *slot = ~0ull;  // leave the workspace ready for the next call
     } else {
       float x[4];
@@ -295,6 +323,15 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_finalize(EncArgs a
     }
     store_code(codes, bits, row, lane, code, a.nsub);
   }
+}
+
+__global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_finalize(EncArgs a) {
+  griddep_wait();
+  const int h = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int64_t bt = static_cast<int64_t>(blockIdx.x) * kEncWarps + (threadIdx.x >> 5);
+  if (bt >= static_cast<int64_t>(a.B) * a.T) return;
+  finalize_token_head(a, bt, static_cast<int>(bt / a.T), static_cast<int>(bt % a.T), h, lane);
 }
 
 // ------------------------------------------------------------------ NEXT-2 formats
@@ -380,7 +417,8 @@ extern "C" size_t vecinfer_encode_workspace_bytes(int32_t B, int32_t T, int32_t 
                                                   vecinfer_vq_t vcfg) {
   if (B <= 0 || T <= 0 || H_kv <= 0) return 0;
   if (kcfg.code_bits != 16 && vcfg.code_bits != 16) return 0;
-  return static_cast<size_t>(B) * T * H_kv * 2 * 32 * sizeof(unsigned long long);
+  // packed minima [B*T*H][2][32] u64, then one arrival counter per token-head (decode append path)
+  return static_cast<size_t>(B) * T * H_kv * (2 * 32 * sizeof(unsigned long long) + sizeof(uint32_t));
 }
 
 static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int32_t B, int32_t T,
@@ -448,10 +486,11 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
     if (!workspace || workspace_bytes < need || !aligned(workspace, 8))
       return fail(VECINFER_ERR_WORKSPACE, "encode_kv: 16-bit codebooks need %zu bytes of workspace", need);
     if (cudaMemsetAsync(workspace, 0xFF, need, st) != cudaSuccess) return check_launch("encode_kv memset");
-    if (nbt * H_kv <= 4096)
+    if (nbt * H_kv <= 4096) {   // decode append: the last chunk CTA of each token-head finalises it
       encode_nn16_kernel<true><<<dim3(static_cast<unsigned>(nbt), 65536 / kChunk16, H_kv), kEncWarps * 32, 0, st>>>(a);
-    else
-      encode_nn16_kernel<false><<<dim3(static_cast<unsigned>(gx), 65536 / kChunk16, H_kv), kEncWarps * 32, 0, st>>>(a);
+      return check_launch("encode_nn16_kernel");
+    }
+    encode_nn16_kernel<false><<<dim3(static_cast<unsigned>(gx), 65536 / kChunk16, H_kv), kEncWarps * 32, 0, st>>>(a);
     vecinfer_status_t s = check_launch("encode_nn16_kernel");
     if (s != VECINFER_OK) return s;
     encode_nn16_finalize<<<dim3(static_cast<unsigned>(gx), H_kv), kEncWarps * 32, 0, st>>>(a);
