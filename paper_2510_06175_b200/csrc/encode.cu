@@ -96,25 +96,31 @@ __device__ __forceinline__ bool cache_row(const EncArgs& a, int b, int t, int h,
 }
 
 // ------------------------------------------------------------------ 4/8-bit: smem codebooks
+// centroids staged as pairs (32 B per 2 entries, pinned_dist4_x2 layout): one FADD2 / FMUL2 per
+// component for two centroids, same per-element rounding as the scalar pinned distance
+template <int N>
+__device__ __forceinline__ void scan_pairs(const uint4* sp, const float (&x)[4], uint32_t& bi) {
+  float best = __int_as_float(0x7f800000);
+  bi = 0;
+#pragma unroll 4
+  for (int p = 0; p < N / 2; ++p) {
+    const float2 d = pinned_dist4_x2(x[0], x[1], x[2], x[3], sp[2 * p], sp[2 * p + 1]);
+    if (d.x < best) { best = d.x; bi = 2 * p; }       // j = 2p first: lowest index on ties
+    if (d.y < best) { best = d.y; bi = 2 * p + 1; }
+  }
+}
+
 template <int KBITS, int VBITS>
 __global__ void __launch_bounds__(kEncWarps * 32) encode_small_kernel(EncArgs a) {
   constexpr int NK = 1 << KBITS, NV = 1 << VBITS;
-  __shared__ float4 sck[NK];
-  __shared__ float4 scv[NV];
+  __shared__ uint4 sck[NK];   // NK / 2 pairs x 32 B
+  __shared__ uint4 scv[NV];
   griddep_launch_dependents();
   const int h = blockIdx.y;
   const uint16_t* ck = a.ck + h * a.ck_hs;
   const uint16_t* cv = a.cv + h * a.cv_hs;
-  for (int j = threadIdx.x; j < NK; j += blockDim.x) {
-    const uint2 w = *reinterpret_cast<const uint2*>(ck + 4 * j);
-    sck[j] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
-                         __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
-  }
-  for (int j = threadIdx.x; j < NV; j += blockDim.x) {
-    const uint2 w = *reinterpret_cast<const uint2*>(cv + 4 * j);
-    scv[j] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
-                         __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
-  }
+  for (int p = threadIdx.x; p < NK / 2; p += blockDim.x) stage_centroid_pair(ck, 2 * p, sck + 2 * p);
+  for (int p = threadIdx.x; p < NV / 2; p += blockDim.x) stage_centroid_pair(cv, 2 * p, scv + 2 * p);
   __syncthreads();
   griddep_wait();
   const int lane = threadIdx.x & 31;
@@ -125,24 +131,11 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_small_kernel(EncArgs a)
   if (!cache_row(a, b, t, h, lane, row)) return;
   float x[4];
   transform_key_lane(a, b, t, h, lane, x);
-  float best = __int_as_float(0x7f800000);
-  uint32_t bi = 0;
-#pragma unroll 4
-  for (int j = 0; j < NK; ++j) {
-    const float4 c = sck[j];
-    const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
-    if (dd < best) { best = dd; bi = j; }
-  }
+  uint32_t bi;
+  scan_pairs<NK>(sck, x, bi);
   store_code(a.kcodes, KBITS, row, lane, bi, a.nsub);
   load_value_lane(a, b, t, h, lane, x);
-  best = __int_as_float(0x7f800000);
-  bi = 0;
-#pragma unroll 4
-  for (int j = 0; j < NV; ++j) {
-    const float4 c = scv[j];
-    const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
-    if (dd < best) { best = dd; bi = j; }
-  }
+  scan_pairs<NV>(scv, x, bi);
   store_code(a.vcodes, VBITS, row, lane, bi, a.nsub);
 }
 
@@ -217,7 +210,7 @@ __device__ __forceinline__ void finalize_token_head(const EncArgs& a, int64_t bt
 
 template <bool kSplit>
 __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) {
-  __shared__ float4 sc[kSplit ? 2 * kChunk16 : kChunk16];
+  __shared__ uint4 sc[kSplit ? 2 * kChunk16 : kChunk16];   // per stream: kChunk16 / 2 pairs x 32 B
   __shared__ bool s_last;
   griddep_wait();
   const int h = blockIdx.z;
@@ -229,15 +222,11 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) 
   const int jw = kSplit ? warp * kSpan : 0;
   const bool live = bt < static_cast<int64_t>(a.B) * a.T;
   const int b = live ? static_cast<int>(bt / a.T) : 0, t = live ? static_cast<int>(bt % a.T) : 0;
-  auto stage = [&](int which, float4* dst) {
+  auto stage = [&](int which, uint4* dst) {   // centroid pairs (pinned_dist4_x2 layout)
     const int n_ent = 1 << (which ? a.vbits : a.kbits);
     if (j0 < n_ent) {
       const uint16_t* cb = which ? (a.cv + h * a.cv_hs) : (a.ck + h * a.ck_hs);
-      for (int j = threadIdx.x; j < kChunk16; j += blockDim.x) {
-        const uint2 w = *reinterpret_cast<const uint2*>(cb + 4 * (j0 + j));
-        dst[j] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
-                             __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
-      }
+      for (int p = threadIdx.x; p < kChunk16 / 2; p += blockDim.x) stage_centroid_pair(cb, j0 + 2 * p, dst + 2 * p);
     }
   };
   if constexpr (kSplit) {
@@ -248,7 +237,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) 
   for (int which = 0; which < 2; ++which) {
     const int bits = which ? a.vbits : a.kbits;
     const int n_ent = 1 << bits;
-    const float4* tab = sc;
+    const uint4* tab = sc;
     if constexpr (kSplit) {
       tab = sc + which * kChunk16;
     } else {
@@ -260,13 +249,14 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) 
     float x[4];
     if (which == 0) transform_key_lane(a, b, t, h, lane, x);
     else load_value_lane(a, b, t, h, lane, x);
-    float best = __int_as_float(0x7f800000);
-    uint32_t bi = 0;
-#pragma unroll 4
-    for (int j = jw; j < jw + kSpan; ++j) {
-      const float4 c = tab[j];
-      const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
-      if (dd < best) { best = dd; bi = j; }
+    uint32_t bi;
+    scan_pairs<kSpan>(tab + jw, x, bi);   // pairs of the warp's span (jw even)
+    bi += jw;
+    float best;
+    {   // the pinned distance of the chosen centroid (exact: same per-element ops)
+      const int pp = static_cast<int>(bi) & ~1;
+      const float2 d = pinned_dist4_x2(x[0], x[1], x[2], x[3], tab[pp], tab[pp + 1]);
+      best = (bi & 1) ? d.y : d.x;
     }
     const unsigned long long packed =
         (static_cast<unsigned long long>(__float_as_uint(best)) << 32) | static_cast<unsigned long long>(j0 + bi);
