@@ -263,9 +263,10 @@ __device__ __forceinline__ float pinned_dist4(float x0, float x1, float x2, floa
   return __fadd_rn(s, __fmul_rn(e3, e3));
 }
 
-// The same pinned distance for two centroids j, j+1 at once with Blackwell's paired fp32 ops
-// (FADD2 / FMUL2: IEEE round-to-nearest per element, no contraction, subnormals kept -- the exact
-// per-element results of pinned_dist4, in 11 instructions for 2 pairs instead of 22).  Centroid
+// The same pinned distance for two centroids j, j+1 at once with Blackwell's paired fp32 ops for
+// the differences and squares (FADD2 / FMUL2: IEEE round-to-nearest per element, subnormals kept)
+// and scalar __fadd_rn for the ordered sums -- the exact per-element results of pinned_dist4 in 14
+// instructions for 2 pairs instead of 22.  Centroid
 // pair layout (32 B): p01 = {c_j.x, c_j+1.x, c_j.y, c_j+1.y}, p23 = {c_j.z, c_j+1.z, c_j.w, c_j+1.w};
 // returns {dist_j, dist_j+1}.
 __device__ __forceinline__ unsigned long long f32x2_pack(uint32_t lo, uint32_t hi) {
@@ -280,7 +281,7 @@ __device__ __forceinline__ unsigned long long f32x2_splat(float x) {
 }
 __device__ __forceinline__ float2 pinned_dist4_x2(float x0, float x1, float x2, float x3, const uint4& p01,
                                                   const uint4& p23) {
-  unsigned long long e0, e1, e2, e3, s;
+  unsigned long long e0, e1, e2, e3;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e0) : "l"(f32x2_splat(x0)), "l"(f32x2_pack(p01.x, p01.y)));
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e1) : "l"(f32x2_splat(x1)), "l"(f32x2_pack(p01.z, p01.w)));
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e2) : "l"(f32x2_splat(x2)), "l"(f32x2_pack(p23.x, p23.y)));
@@ -289,11 +290,15 @@ __device__ __forceinline__ float2 pinned_dist4_x2(float x0, float x1, float x2, 
   asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(e1) : "l"(e1));
   asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(e2) : "l"(e2));
   asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(e3) : "l"(e3));
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s) : "l"(e0), "l"(e1));
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s) : "l"(s), "l"(e2));
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s) : "l"(s), "l"(e3));
-  float d0, d1;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(s));
+  // the sums stay scalar __fadd_rn: ptxas contracts mul.rn.f32x2 followed by add.rn.f32x2 into
+  // FFMA2 (even with -fmad=false), which would round e_t^2 + s once instead of twice
+  float q0x, q0y, q1x, q1y, q2x, q2y, q3x, q3y;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(q0x), "=f"(q0y) : "l"(e0));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(q1x), "=f"(q1y) : "l"(e1));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(q2x), "=f"(q2y) : "l"(e2));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(q3x), "=f"(q3y) : "l"(e3));
+  const float d0 = __fadd_rn(__fadd_rn(__fadd_rn(q0x, q1x), q2x), q3x);
+  const float d1 = __fadd_rn(__fadd_rn(__fadd_rn(q0y, q1y), q2y), q3y);
   return make_float2(d0, d1);
 }
 // stage the bf16 centroid pair (j, j+1) of a [n][4] codebook into the 32-byte paired layout

@@ -61,16 +61,47 @@ __global__ void __launch_bounds__(kKmThreads) kmeans_assign_kernel(const float* 
   for (int c0 = 0; c0 < k; c0 += kChunk) {
     const int nc = min(kChunk, k - c0);
     __syncthreads();
-    for (int e = threadIdx.x; e < nc * D; e += kKmThreads) sc[e] = C[static_cast<int64_t>(c0) * D + e];
-    __syncthreads();
-    for (int j = 0; j < nc; ++j) {
-      float cj[D];
+    if constexpr (D == 4) {
+      // d = 4: centroid pairs in the FADD2 / FMUL2 layout (pinned_dist4_x2: the same per-element
+      // RN ops, two centroids per instruction); an odd last centroid is paired with itself
+      uint4* sp = reinterpret_cast<uint4*>(sc);
+      for (int q = threadIdx.x; q < (nc + 1) / 2; q += kKmThreads) {
+        const float* a = C + static_cast<int64_t>(c0 + 2 * q) * 4;
+        const float* b = (2 * q + 1 < nc) ? a + 4 : a;
+        sp[2 * q] = make_uint4(__float_as_uint(a[0]), __float_as_uint(b[0]), __float_as_uint(a[1]), __float_as_uint(b[1]));
+        sp[2 * q + 1] = make_uint4(__float_as_uint(a[2]), __float_as_uint(b[2]), __float_as_uint(a[3]), __float_as_uint(b[3]));
+      }
+      __syncthreads();
+      for (int q = 0; q < nc / 2; ++q) {
+        const uint4 p01 = sp[2 * q], p23 = sp[2 * q + 1];
 #pragma unroll
-      for (int t = 0; t < D; ++t) cj[t] = sc[j * D + t];
+        for (int p = 0; p < kKmPts; ++p) {
+          const float2 d = pinned_dist4_x2(x[p][0], x[p][1], x[p][2], x[p][3], p01, p23);
+          if (d.x < bd[p]) { bd[p] = d.x; bi[p] = c0 + 2 * q; }
+          if (d.y < bd[p]) { bd[p] = d.y; bi[p] = c0 + 2 * q + 1; }
+        }
+      }
+      if (nc & 1) {
+        const int q = nc / 2;
+        const uint4 p01 = sp[2 * q], p23 = sp[2 * q + 1];
 #pragma unroll
-      for (int p = 0; p < kKmPts; ++p) {
-        const float dd = pinned_dist<D>(x[p], cj);
-        if (dd < bd[p]) { bd[p] = dd; bi[p] = c0 + j; }
+        for (int p = 0; p < kKmPts; ++p) {
+          const float2 d = pinned_dist4_x2(x[p][0], x[p][1], x[p][2], x[p][3], p01, p23);
+          if (d.x < bd[p]) { bd[p] = d.x; bi[p] = c0 + 2 * q; }
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < nc * D; e += kKmThreads) sc[e] = C[static_cast<int64_t>(c0) * D + e];
+      __syncthreads();
+      for (int j = 0; j < nc; ++j) {
+        float cj[D];
+#pragma unroll
+        for (int t = 0; t < D; ++t) cj[t] = sc[j * D + t];
+#pragma unroll
+        for (int p = 0; p < kKmPts; ++p) {
+          const float dd = pinned_dist<D>(x[p], cj);
+          if (dd < bd[p]) { bd[p] = dd; bi[p] = c0 + j; }
+        }
       }
     }
   }
