@@ -29,7 +29,7 @@ int merge_mode_from_env() {
 }
 
 constexpr int kMaxSplits = 128;
-constexpr int64_t kMinTokensPerSplit = 512;
+constexpr int64_t kMinTokensPerSplit = 256;   // measured: N = 1024 runs S = 4 (5.4 us) instead of S = 2 (6.1 us)
 
 bool vq_d4(const vecinfer_vq_t& c) {
   return (c.head_dim == 128 || c.head_dim == 64) && c.sub_dim == 4 &&
