@@ -177,7 +177,9 @@ vecinfer_status_t vecinfer_calibrate_smooth(const void* k_cal_bf16, int64_t n_to
  *   workspace        >= vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg, vcfg) bytes (0 for
  *                    4/8-bit codebooks, which are searched from shared memory; 16-bit
  *                    codebooks are searched by centroid-split CTAs that combine partial
- *                    minima with 64-bit atomicMin on (dist_bits << 32 | index)).
+ *                    minima with 64-bit atomicMin on (dist_bits << 32 | index), plus one
+ *                    arrival counter per token-head for the in-kernel finalize of the decode
+ *                    append: B*T*H_kv*(2*32*8 + 4) bytes; any contents, the call fills it).
  * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, WORKSPACE, CUDA.
  * ------------------------------------------------------------------------------------- */
 size_t vecinfer_encode_workspace_bytes(int32_t B, int32_t T, int32_t H_kv, vecinfer_vq_t kcfg,

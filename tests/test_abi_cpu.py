@@ -96,7 +96,7 @@ def test_workspace_and_split_queries(lib):
     assert lib.vecinfer_calibrate_workspace_bytes(8, 128) >= 8 * 128 * 4
     from paper_2510_06175_b200._lib import VQ
     assert lib.vecinfer_encode_workspace_bytes(1, 1, 8, VQ(128, 4, 8), VQ(128, 4, 8)) == 0
-    assert lib.vecinfer_encode_workspace_bytes(1, 1, 8, VQ(128, 4, 16), VQ(128, 4, 8)) == 8 * 2 * 32 * 8
+    assert lib.vecinfer_encode_workspace_bytes(1, 1, 8, VQ(128, 4, 16), VQ(128, 4, 8)) == 8 * (2 * 32 * 8 + 4)
 
 
 def test_product_path_never_imports_the_oracle():
