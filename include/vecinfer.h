@@ -344,17 +344,19 @@ vecinfer_status_t vecinfer_merge_lse(const float* o_parts, const float* lse_part
  * P:501; empty-cluster re-seeding at the largest-distortion points).  NEXT-3.
  *   X          fp32 [n, d] points (row-major, contiguous), d in {2, 4, 8}; n >= k, n < 2^32 - 1.
  *   C          fp32 [k, d] current centroids, 0 < k <= 65536.
- *   C_new      fp32 [k, d] out: RN32(mean of the cluster's points) (fp64 sum and division) for
- *              non-empty clusters; the empty clusters, in increasing index, take the points of
- *              largest best distance (ties: lowest point index).  May alias C.
+ *   C_new      fp32 [k, d] out: RN32(mean of the cluster's points) for non-empty clusters, the sum
+ *              taken exactly in int64 fixed point (each x rounded to a 2^-e grid, e chosen from
+ *              max|x|, max|C| and n so that no sum overflows), then / 2^e / count in fp64; the
+ *              empty clusters, in increasing index, take the points of largest best distance
+ *              (ties: lowest point index).  May alias C.
  *   assign     int32 [n] out: argmin_j of the pinned fp32 distance (the encoder's rule: e = x - c,
  *              ((e_0^2 + e_1^2) + e_2^2) + ..., RN, no FMA), ties to the lowest index.
  *   best       fp32 [n] out: the pinned distance to the assigned centroid.
- *   objective  fp64 device scalar out: sum_i best_i (accumulated with atomics: order-dependent
- *              in the last bits).
+ *   objective  fp64 device scalar out: sum_i best_i (exact int64 fixed-point sum, as above).
  *   workspace  >= vecinfer_kmeans_workspace_bytes(k, d) bytes, 256-byte aligned, any contents.
- * Deterministic except C_new, whose fp64 cluster sums are accumulated in atomic order (C_new is
- * within one fp32 ulp of the exactly rounded mean).  Launches 3 kernels + 2 memsets on `stream`.
+ * Bitwise deterministic run to run (integer sums do not depend on the order the atomics land in;
+ * SPEC S:128, 187).  C_new is within one fp32 ulp of the exactly rounded mean (the fixed-point
+ * rounding of each point, <= 2^-(e+1)).  Launches 4 kernels + 1 memset on `stream`.
  * Errors: INVALID_ARG (NULL / misaligned), UNSUPPORTED (d), SHAPE (k, n), EMPTY (n == 0),
  * WORKSPACE, CUDA.
  * ------------------------------------------------------------------------------------- */

@@ -228,7 +228,10 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
         if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = L2 * kLn2;
       }
     } else if (a.merge_spin) {
-      // publish (o_s, L_s) as one 64-bit relaxed store of ~(L_s << 32 | o_s) (zero = empty)
+      // publish (o_s, L_s) as one 64-bit relaxed store of ~(L_s << 32 | o_s) (zero = empty); only
+      // for the real heads g < gp, the ones the consumers poll and zero (a padding element left
+      // non-zero would be taken as a fresh piece by a later launch reusing the workspace)
+      if (g >= hm.gp) continue;
       const int64_t pi = ((unit * a.S + s) * 4 + g) * 128 + dim;
       st_relaxed_gpu_u64(a.part_elem + pi, ~((static_cast<unsigned long long>(__float_as_uint(L2)) << 32) |
                                              __float_as_uint(ov)));

@@ -723,7 +723,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
             else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
             if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(sg.b) * a.Hq + sg.hq0 + g] = L2 * kLn2;
           }
-        } else {
+        } else if (g < sg.gp) {
+          // only the real heads are published: the consumers poll (and zero) g < gp only, so a
+          // padding slot written here would stay non-zero in the workspace for a later launch
           const int64_t pi = ((static_cast<int64_t>(vc) + sg.u) * 4 + g) * 128 + dim;
           st_relaxed_gpu_u64(part + pi, ~((static_cast<unsigned long long>(__float_as_uint(L2)) << 32) |
                                           __float_as_uint(ov)));

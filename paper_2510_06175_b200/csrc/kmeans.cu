@@ -7,14 +7,18 @@
 //      distance (Eq. 2 / reading R9: e_t = x_t - c_t, ((e_0^2 + e_1^2) + e_2^2) + ..., every op RN,
 //      no FMA), strict < scan in index order -> lowest index on ties.  Centroids are staged in
 //      shared memory in 32 KiB chunks and read as broadcasts; every thread keeps 8 points (2 for
-//      small n) in registers.  The same thread then adds its points into the fp64 cluster sums and counts
-//      (global atomics) and its best distances into the objective.
-//   2. finalize (kmeans_finalize_kernel): C'_j = RN32(sum_j / n_j) (fp64 division) for n_j > 0.
+//      small n) in registers.  The same thread then adds its points into the cluster sums and counts
+//      and its best distance into the objective (global atomics).  Sums and objective are exact
+//      int64 fixed-point sums (scale 2^e chosen from max|x|, max|C| and n by kmeans_bound_kernel so
+//      no sum can overflow): integer addition is associative, so the result does not depend on the
+//      order the atomics land in -- the step is bitwise reproducible run to run.
+//   2. finalize (kmeans_finalize_kernel): C'_j = RN32((sum_j / 2^e) / n_j) (fp64) for n_j > 0.
 //   3. reseed (kmeans_reseed_kernel, one CTA): the empty clusters, in increasing j, take the points
 //      of largest best_i (ties: lowest i), one each -- E rounds of a block-wide max over the key
 //      (best_bits << 32 | ~i) restricted to keys below the previous pick.  No-op when E = 0.
 // Parity: oracle/vecinfer_oracle.py kmeans_lloyd_step (assignments and best bit-exact, counts
-// exact, C' within one fp32 ulp: the fp64 sums are accumulated in atomic order).
+// exact, C' within one fp32 ulp: the per-point fixed-point rounding is <= 2^-(e+1), far below an
+// fp32 ulp of the mean at the data scales used, but not zero).
 #include "common.cuh"
 
 namespace vecinfer {
@@ -35,17 +39,61 @@ __device__ __forceinline__ float pinned_dist(const float (&x)[D], const float* c
   return acc;
 }
 
+// max |x| over the points and max |c| over the centroids as fp32 bits (|v| >= 0: unsigned order
+// of the bits is the float order), for the fixed-point scales of the sums and the objective
+__global__ void kmeans_bound_kernel(const float* __restrict__ X, int64_t nx, const float* __restrict__ C, int64_t nc,
+                                    uint32_t* __restrict__ bound) {
+  uint32_t mx = 0u, mc = 0u;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nx;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    mx = max(mx, __float_as_uint(fabsf(X[e])));
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nc;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    mc = max(mc, __float_as_uint(fabsf(C[e])));
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(bound, mx);
+    atomicMax(bound + 1, mc);
+  }
+}
+
+// Power-of-two scales 2^e_sum (cluster sums) and 2^e_obj (objective) such that n addends of
+// magnitude <= bound stay below 2^62 in int64: e = 61 - ceil(log2 n) - ceil(log2 bound), clamped.
+struct KmScale {
+  double s_sum, s_obj;
+};
+__device__ __forceinline__ int km_exp_for(double bound, int64_t n) {
+  int eb = 0, en = 0;
+  frexp(bound > 0.0 ? bound : 1.0, &eb);               // bound < 2^eb
+  frexp(static_cast<double>(n), &en);                  // n < 2^en
+  int e = 61 - en - eb;
+  return e > 200 ? 200 : (e < -200 ? -200 : e);
+}
+__device__ __forceinline__ KmScale km_scale(const uint32_t* bound, int64_t n, int D) {
+  const double xm = static_cast<double>(__uint_as_float(bound[0]));
+  const double cm = static_cast<double>(__uint_as_float(bound[1]));
+  KmScale sc;
+  sc.s_sum = ldexp(1.0, km_exp_for(xm, n));
+  sc.s_obj = ldexp(1.0, km_exp_for(static_cast<double>(D) * (xm + cm) * (xm + cm) * 1.0001, n));
+  return sc;
+}
+__device__ __forceinline__ long long to_fixed(double v, double scale) { return __double2ll_rn(v * scale); }
+
 template <int D, int kKmPts>   // kKmPts: points per thread (8, or 2 for small n: more CTAs)
 __global__ void __launch_bounds__(kKmThreads) kmeans_assign_kernel(const float* __restrict__ X, int64_t n,
                                                                     const float* __restrict__ C, int k,
                                                                     int32_t* __restrict__ assign,
                                                                     float* __restrict__ best,
-                                                                    double* __restrict__ sums,
+                                                                    unsigned long long* __restrict__ sums,
                                                                     int32_t* __restrict__ counts,
-                                                                    double* __restrict__ objective) {
+                                                                    unsigned long long* __restrict__ obj_fx,
+                                                                    const uint32_t* __restrict__ bound) {
   constexpr int kChunk = kKmChunkBytes / (4 * D);
   __shared__ __align__(16) float sc[kChunk * D];
-  __shared__ double sobj[kKmThreads / 32];
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kKmThreads * kKmPts;
   float x[kKmPts][D];
   float bd[kKmPts];
@@ -105,39 +153,42 @@ __global__ void __launch_bounds__(kKmThreads) kmeans_assign_kernel(const float* 
       }
     }
   }
-  double obj = 0.0;
+  const KmScale scl = km_scale(bound, n, D);
+  long long obj = 0;
 #pragma unroll
   for (int p = 0; p < kKmPts; ++p) {
     const int64_t i = base + p * kKmThreads + threadIdx.x;
     if (i >= n) continue;
     assign[i] = bi[p];
     best[i] = bd[p];
-    obj += static_cast<double>(bd[p]);
+    obj += to_fixed(static_cast<double>(bd[p]), scl.s_obj);
     atomicAdd(&counts[bi[p]], 1);
 #pragma unroll
-    for (int t = 0; t < D; ++t) atomicAdd(&sums[static_cast<int64_t>(bi[p]) * D + t], static_cast<double>(x[p][t]));
+    for (int t = 0; t < D; ++t)   // two's complement wrap-around add == exact signed int64 add
+      atomicAdd(&sums[static_cast<int64_t>(bi[p]) * D + t],
+                static_cast<unsigned long long>(to_fixed(static_cast<double>(x[p][t]), scl.s_sum)));
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) obj += __shfl_xor_sync(0xffffffffu, obj, off);
-  if ((threadIdx.x & 31) == 0) sobj[threadIdx.x >> 5] = obj;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < kKmThreads / 32; ++w) s += sobj[w];
-    atomicAdd(objective, s);
-  }
+  if ((threadIdx.x & 31) == 0) atomicAdd(obj_fx, static_cast<unsigned long long>(obj));
 }
 
 template <int D>
-__global__ void kmeans_finalize_kernel(const float* __restrict__ C, int k, const double* __restrict__ sums,
-                                       const int32_t* __restrict__ counts, float* __restrict__ Cn) {
+__global__ void kmeans_finalize_kernel(const float* __restrict__ C, int k, int64_t n,
+                                       const unsigned long long* __restrict__ sums,
+                                       const int32_t* __restrict__ counts, float* __restrict__ Cn,
+                                       const uint32_t* __restrict__ bound, const unsigned long long* __restrict__ obj_fx,
+                                       double* __restrict__ objective) {
+  const KmScale scl = km_scale(bound, n, D);
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j == 0) *objective = static_cast<double>(static_cast<long long>(*obj_fx)) / scl.s_obj;
   if (j >= k) return;
   const int cnt = counts[j];
 #pragma unroll
   for (int t = 0; t < D; ++t) {
     const int64_t e = static_cast<int64_t>(j) * D + t;
-    Cn[e] = cnt > 0 ? __double2float_rn(__ddiv_rn(sums[e], static_cast<double>(cnt))) : C[e];
+    const double sum = static_cast<double>(static_cast<long long>(sums[e])) / scl.s_sum;   // /2^e: exact
+    Cn[e] = cnt > 0 ? __double2float_rn(__ddiv_rn(sum, static_cast<double>(cnt))) : C[e];
   }
 }
 
@@ -208,13 +259,14 @@ __global__ void __launch_bounds__(1024) kmeans_reseed_kernel(const float* __rest
 }
 
 struct KmWs {
-  size_t sums, counts, empty, total;
+  size_t sums, counts, misc, empty, total;   // misc: u32 bound[2] (max|x|, max|c|) + u64 objective sum
 };
 KmWs km_ws(int32_t k, int32_t d) {
   KmWs w;
   w.sums = 0;
-  w.counts = (static_cast<size_t>(k) * d * sizeof(double) + 255) & ~size_t(255);
-  w.empty = w.counts + ((static_cast<size_t>(k) * sizeof(int32_t) + 255) & ~size_t(255));
+  w.counts = (static_cast<size_t>(k) * d * sizeof(unsigned long long) + 255) & ~size_t(255);
+  w.misc = w.counts + ((static_cast<size_t>(k) * sizeof(int32_t) + 255) & ~size_t(255));
+  w.empty = w.misc + 256;
   w.total = w.empty + static_cast<size_t>(k) * sizeof(int32_t);
   return w;
 }
@@ -223,19 +275,21 @@ template <int D>
 cudaError_t launch_kmeans(const float* X, int64_t n, const float* C, int k, float* Cn, int32_t* assign, float* best,
                           double* obj, unsigned char* ws, cudaStream_t st) {
   const KmWs w = km_ws(k, D);
-  double* sums = reinterpret_cast<double*>(ws + w.sums);
+  unsigned long long* sums = reinterpret_cast<unsigned long long*>(ws + w.sums);
   int32_t* counts = reinterpret_cast<int32_t*>(ws + w.counts);
+  uint32_t* bound = reinterpret_cast<uint32_t*>(ws + w.misc);
+  unsigned long long* obj_fx = reinterpret_cast<unsigned long long*>(ws + w.misc + 8);
   int32_t* empty = reinterpret_cast<int32_t*>(ws + w.empty);
   if (cudaMemsetAsync(ws, 0, w.empty, st) != cudaSuccess) return cudaGetLastError();
-  if (cudaMemsetAsync(obj, 0, sizeof(double), st) != cudaSuccess) return cudaGetLastError();
+  kmeans_bound_kernel<<<2 * device_sm_count(), 256, 0, st>>>(X, n * D, C, static_cast<int64_t>(k) * D, bound);
   // 8 points per thread amortise the shared-memory centroid stream; below ~2 CTAs per SM at 8,
   // 2 points per thread keep every SM busy
   const bool big = n >= static_cast<int64_t>(device_sm_count()) * kKmThreads * 8 * 2;
   const int64_t per = static_cast<int64_t>(kKmThreads) * (big ? 8 : 2);
   const unsigned g = static_cast<unsigned>((n + per - 1) / per);
-  if (big) kmeans_assign_kernel<D, 8><<<g, kKmThreads, 0, st>>>(X, n, C, k, assign, best, sums, counts, obj);
-  else kmeans_assign_kernel<D, 2><<<g, kKmThreads, 0, st>>>(X, n, C, k, assign, best, sums, counts, obj);
-  kmeans_finalize_kernel<D><<<(k + 255) / 256, 256, 0, st>>>(C, k, sums, counts, Cn);
+  if (big) kmeans_assign_kernel<D, 8><<<g, kKmThreads, 0, st>>>(X, n, C, k, assign, best, sums, counts, obj_fx, bound);
+  else kmeans_assign_kernel<D, 2><<<g, kKmThreads, 0, st>>>(X, n, C, k, assign, best, sums, counts, obj_fx, bound);
+  kmeans_finalize_kernel<D><<<(k + 255) / 256, 256, 0, st>>>(C, k, n, sums, counts, Cn, bound, obj_fx, obj);
   kmeans_reseed_kernel<D><<<1, 1024, 0, st>>>(X, n, best, k, counts, empty, Cn);
   return cudaPeekAtLastError();
 }

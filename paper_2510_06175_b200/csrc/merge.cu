@@ -97,8 +97,11 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 __global__ void merge_lse_p2p_kernel(const float* __restrict__ o_local, const float* __restrict__ lse_local,
                                      void* const* __restrict__ windows, P2PLayout lay, int rank, uint32_t epoch,
                                      void* o, int o_f32, float* lse, uint32_t* err, unsigned long long timeout_ns) {
-  const int64_t row = blockIdx.x;
+  // Persistent grid (at most the co-resident CTA count, see the launch): CTA c owns rows c, c+grid,
+  // ...; it publishes ALL of its rows before it waits for any, so progress never depends on the
+  // hardware dispatching CTAs in any particular order on any rank.
   const int D = lay.D, P = lay.P;
+  const int64_t rows = lay.rows;
   __shared__ int s_ok;
   __shared__ uint32_t s_epoch;
   // epoch 0 = automatic: the own window's header counter + 1 (every CTA reads it before the last
@@ -113,51 +116,59 @@ __global__ void merge_lse_p2p_kernel(const float* __restrict__ o_local, const fl
   __syncthreads();
   epoch = s_epoch;
   const int par = static_cast<int>(epoch & 1u);
-  // 1. publish this rank's partial row into every window (own included)
-  for (int p = 0; p < P; ++p) {
-    float* dst = static_cast<float*>(windows[p]) + lay.data_off(par, rank, row);
-    for (int d = threadIdx.x; d < D; d += blockDim.x) dst[d] = o_local[row * D + d];
-    if (threadIdx.x == 0) dst[D] = lse_local[row];
+  // 1. publish this rank's partial rows into every window (own included)
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    for (int p = 0; p < P; ++p) {
+      float* dst = static_cast<float*>(windows[p]) + lay.data_off(par, rank, row);
+      for (int d = threadIdx.x; d < D; d += blockDim.x) dst[d] = o_local[row * D + d];
+      if (threadIdx.x == 0) dst[D] = lse_local[row];
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();   // cumulative: the CTA's data stores (ordered by the barrier) first
-    for (int p = 0; p < P; ++p)
-      st_release_sys_u32(reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(windows[p]) +
-                                                     lay.flag_off_bytes(par, rank, row)), epoch);
-    // 2. wait for the P partials of this row in the own window
-    const unsigned char* mine = static_cast<const unsigned char*>(windows[rank]);
-    const unsigned long long t0 = globaltimer_ns();
-    int ok = 1;
-    for (int q = 0; q < P && ok; ++q) {
-      const uint32_t* f = reinterpret_cast<const uint32_t*>(mine + lay.flag_off_bytes(par, q, row));
-      while (ld_acquire_sys_u32(f) != epoch) {
-        if (globaltimer_ns() - t0 > timeout_ns) { ok = 0; break; }
-      }
-    }
-    if (!ok && err) atomicOr(err, VECINFER_FLAG_P2P_TIMEOUT);
-    s_ok = ok;
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x)
+      for (int p = 0; p < P; ++p)
+        st_release_sys_u32(reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(windows[p]) +
+                                                       lay.flag_off_bytes(par, rank, row)), epoch);
   }
-  __syncthreads();
-  // 3. merge in rank order (merge_lse_kernel's arithmetic), reading past L1 (peer-written data)
-  const float* win = static_cast<const float*>(windows[rank]);
-  float M = -INFINITY;
-  for (int s = 0; s < P; ++s) M = fmaxf(M, __ldcg(win + lay.data_off(par, s, row) + D));
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    float wsum = 0.f, osum = 0.f;
-    if (M != -INFINITY) {
-      for (int s = 0; s < P; ++s) {
-        const float* src = win + lay.data_off(par, s, row);
-        const float f = __expf(__ldcg(src + D) - M);
-        wsum += f;
-        osum += f * __ldcg(src + d);
+  const unsigned long long t0 = globaltimer_ns();
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    // 2. wait for the P partials of this row in the own window
+    if (threadIdx.x == 0) {
+      const unsigned char* mine = static_cast<const unsigned char*>(windows[rank]);
+      int ok = 1;
+      for (int q = 0; q < P && ok; ++q) {
+        const uint32_t* f = reinterpret_cast<const uint32_t*>(mine + lay.flag_off_bytes(par, q, row));
+        while (ld_acquire_sys_u32(f) != epoch) {
+          if (globaltimer_ns() - t0 > timeout_ns) { ok = 0; break; }
+        }
       }
+      if (!ok && err) atomicOr(err, VECINFER_FLAG_P2P_TIMEOUT);
+      s_ok = ok;
     }
-    const bool empty = !(wsum > 0.f) || !s_ok;
-    const float v = empty ? 0.f : osum / wsum;
-    if (o_f32) static_cast<float*>(o)[row * D + d] = v;
-    else static_cast<__nv_bfloat16*>(o)[row * D + d] = __float2bfloat16_rn(v);
-    if (d == 0 && lse) lse[row] = empty ? -INFINITY : M + __logf(wsum);
+    __syncthreads();
+    // 3. merge in rank order (merge_lse_kernel's arithmetic), reading past L1 (peer-written data)
+    const float* win = static_cast<const float*>(windows[rank]);
+    float M = -INFINITY;
+    for (int s = 0; s < P; ++s) M = fmaxf(M, __ldcg(win + lay.data_off(par, s, row) + D));
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+      float wsum = 0.f, osum = 0.f;
+      if (M != -INFINITY) {
+        for (int s = 0; s < P; ++s) {
+          const float* src = win + lay.data_off(par, s, row);
+          const float f = __expf(__ldcg(src + D) - M);
+          wsum += f;
+          osum += f * __ldcg(src + d);
+        }
+      }
+      const bool empty = !(wsum > 0.f) || !s_ok;
+      const float v = empty ? 0.f : osum / wsum;
+      if (o_f32) static_cast<float*>(o)[row * D + d] = v;
+      else static_cast<__nv_bfloat16*>(o)[row * D + d] = __float2bfloat16_rn(v);
+      if (d == 0 && lse) lse[row] = empty ? -INFINITY : M + __logf(wsum);
+    }
+    __syncthreads();   // s_ok is rewritten for the next row
   }
   if (threadIdx.x == 0) {   // the last CTA of the launch records the epoch it used (automatic mode)
     __threadfence();
@@ -231,7 +242,20 @@ extern "C" vecinfer_status_t vecinfer_merge_lse_p2p(const float* o_local, const 
   const P2PLayout lay{rows, P, D};
   const int threads = D >= 128 ? 128 : ((D + 31) / 32) * 32;
   const unsigned long long timeout_ns = 5000000000ull;   // 5 s: a missing peer flags instead of hanging
-  merge_lse_p2p_kernel<<<static_cast<unsigned>(rows), threads, 0, as_stream(stream)>>>(
+  // persistent grid capped at the co-resident CTA count (every CTA spin-waits on peer flags)
+  static int cached_threads = 0, resident = 0;   // benign race: idempotent
+  if (cached_threads != threads) {
+    cached_threads = threads;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_lse_p2p_kernel, threads, 0) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    resident = per_sm * device_sm_count();
+  }
+  const unsigned grid = static_cast<unsigned>(rows < resident ? rows : resident);
+  merge_lse_p2p_kernel<<<grid, threads, 0, as_stream(stream)>>>(
       o_local, lse_local, windows, lay, rank, epoch, o, o_dtype == VECINFER_F32, lse, err_flags, timeout_ns);
   return check_launch("merge_lse_p2p_kernel");
 }

@@ -147,3 +147,66 @@ class P2PExchange:
         if self._own:
             self._lib.vecinfer_p2p_window_destroy(self._own)
             self._own = None
+
+
+class SeqShardedStep:
+    """One decode step of an L-layer model whose single long sequence is sharded over the ranks
+    (BASELINE configs[3]): for every layer, this rank's attention over its token
+    shard [tok_begin, tok_end) writes a normalised partial (o_r, L_r), and that layer's partials are
+    exchanged and LSE-merged BEFORE the next layer runs -- the next layer's query depends on this
+    layer's output in a real model, so the exchange is paid once per layer, not once per step.
+
+    exchange="p2p": the fused peer-memory kernel (P2PExchange, one launch per layer; graph-safe).
+    exchange="allgather": one packed all-gather per layer + vecinfer_merge_lse (NCCL on device
+    tensors; gloo through host copies for the single-GPU functional tests).
+    Outputs: self.o [L, B, H_q, D] (o_dtype), self.lse [L, B, H_q], identical on every rank.
+    """
+
+    def __init__(self, layers: int, B: int, H_q: int, D: int, n_tokens: int, device: torch.device,
+                 H_kv: int = 8, exchange: str = "p2p", o_dtype: torch.dtype = torch.float32, group=None):
+        from . import vecinfer as vi
+        if exchange not in ("p2p", "allgather"):
+            raise ValueError("exchange must be 'p2p' or 'allgather'")
+        self.vi = vi
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.L, self.B, self.H_q, self.D = layers, B, H_q, D
+        self.tok_begin, self.tok_end = shard_range(n_tokens, self.rank, self.world)
+        n_local = self.tok_end - self.tok_begin
+        self.o_part = torch.empty(layers, B, H_q, D, dtype=torch.float32, device=device)
+        self.lse_part = torch.empty(layers, B, H_q, dtype=torch.float32, device=device)
+        self.o = torch.empty(layers, B, H_q, D, dtype=o_dtype, device=device)
+        self.lse = torch.empty(layers, B, H_q, dtype=torch.float32, device=device)
+        self.workspace = [vi.attn_workspace(B, H_q, H_kv, max(n_local, 1), device=device) for _ in range(layers)]
+        self.exchange = exchange
+        self.p2p = P2PExchange(B * H_q, D, device, group=group) if exchange == "p2p" else None
+        self.device = device
+
+    def exchange_layer(self, l: int):
+        """Exchange + merge layer l's partials (every rank ends with the same o[l], lse[l])."""
+        if self.p2p is not None:
+            self.p2p.merge(self.o_part[l], self.lse_part[l], out=self.o[l], lse=self.lse[l])
+            return
+        o_p, l_p = self.o_part[l], self.lse_part[l]
+        host = dist.get_backend(self.group) == "gloo"
+        o_g, l_g = gather_partials_packed(o_p.cpu() if host else o_p, l_p.cpu() if host else l_p, group=self.group)
+        if host:
+            o_g, l_g = o_g.to(self.device), l_g.to(self.device)
+        self.vi.merge_lse(o_g.contiguous(), l_g.contiguous(), o_dtype=self.o.dtype, out=self.o[l], lse=self.lse[l])
+
+    def run(self, attend):
+        """attend(l, o_part_l, lse_part_l) launches layer l's shard attention (e.g. vi.attn_decode with
+        tok_begin/tok_end and out=/lse=); the exchange of layer l follows it immediately."""
+        for l in range(self.L):
+            attend(l, self.o_part[l], self.lse_part[l])
+            self.exchange_layer(l)
+
+    def error(self) -> int:
+        """Non-zero if a peer partial timed out in the fused exchange (VECINFER_FLAG_P2P_TIMEOUT)."""
+        return int(self.p2p.err.item()) if self.p2p is not None else 0
+
+    def close(self):
+        if self.p2p is not None:
+            self.p2p.close()
+            self.p2p = None

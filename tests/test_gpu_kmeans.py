@@ -3,7 +3,8 @@
 One vecinfer_kmeans_step must reproduce oracle.kmeans_lloyd_step from the same fp32 centroids:
 assignments and best distances bit-exact (the encoder's pinned fp32 distance, lowest index on
 ties), counts exact, re-seeded empty clusters exact, and the updated centroids within one fp32 ulp
-of RN32(exact mean) (the GPU accumulates its fp64 cluster sums in atomic order).  Inputs follow the
+of RN32(exact mean) (the GPU sums each cluster exactly in int64 fixed point on a 2^-e grid, so
+the step is bitwise reproducible run to run; the grid rounding is the only difference).  Inputs follow the
 codebook-fitting recipe: pinned-transformed synthetic keys (C_k) and raw values (C_v) split into
 d-dim sub-vectors, plus dyadic tie cases and forced empty clusters.
 """
@@ -108,3 +109,16 @@ def test_kmeans_step_rejects_bad_arguments():
         vi.kmeans_step(X, torch.zeros(16, 4, device=DEV))        # n < k
     with pytest.raises(VecInferError):
         vi.kmeans_step(torch.zeros(40, 3, device=DEV), torch.zeros(4, 3, device=DEV))   # d = 3
+
+
+@pytest.mark.parametrize("d,k", [(4, 256), (2, 256), (8, 4096)])
+def test_kmeans_step_bitwise_reproducible(d, k):
+    """SPEC S:128 / S:187 determinism: the same step twice gives bitwise identical centroids and
+    objective (integer fixed-point sums; the atomics' landing order cannot change them)."""
+    X = _subvectors(8192 * 8 // d, d, "k", seed=901)
+    rng = np.random.default_rng(902)
+    C = X[rng.choice(X.shape[0], size=k, replace=False)].copy()
+    r1 = _gpu_step(X, C)
+    r2 = _gpu_step(X, C)
+    assert np.array_equal(r1[0].view(np.uint32), r2[0].view(np.uint32))
+    assert np.array_equal(r1[1], r2[1]) and r1[3] == r2[3]

@@ -324,8 +324,9 @@ def test_sharded_attention_plus_merge_equals_unsharded():
 
 
 # ------------------------------------------------------ BASELINE configs at full size
-def _sampled_units_check(B, N, n_units, seed, **kw):
-    """Full-size launch (auto splits, as bench.py) checked on sampled (b, h_kv) units."""
+def _sampled_units_check(B, N, n_units, seed, units=None, **kw):
+    """Full-size launch (auto splits, as bench.py) checked on sampled (b, h_kv) units, or on the
+    explicit list `units` (every unit, deterministically, where the oracle is fast enough)."""
     rng = np.random.default_rng(seed)
     q = synth.gen_queries(B, 32, 8, 128, seed=seed)
     kc = synth.gen_codes_torch((B, 8, N, 32), 8, seed=seed, device=DEV)
@@ -333,8 +334,9 @@ def _sampled_units_check(B, N, n_units, seed, **kw):
     o, L = vi.attn_decode(t_bf16(q), t_f32(CB["lambda"]), t_bf16(CB["ck_b2d4"]), t_bf16(CB["cv_b2d4"]), kc, vc,
                           t_i32([N] * B), **kw)
     o, L = o.cpu().numpy(), L.cpu().numpy()
-    for _ in range(n_units):
-        b, h = int(rng.integers(B)), int(rng.integers(8))
+    if units is None:
+        units = [(int(rng.integers(B)), int(rng.integers(8))) for _ in range(n_units)]
+    for b, h in units:
         kk = kc[b, h].cpu().numpy().astype(np.int64)   # synthetic inputs (synth/), not CUDA results
         vv = vc[b, h].cpu().numpy().astype(np.int64)
         o_ref, L_ref = ref.attention_vq(q[b, 4 * h:4 * h + 4], CB["lambda"][h], CB["ck_b2d4"][h], CB["cv_b2d4"][h],
@@ -343,7 +345,9 @@ def _sampled_units_check(B, N, n_units, seed, **kw):
 
 
 def test_cfg2_full_size_all_units():
-    _sampled_units_check(1, 32768, 8, seed=40)
+    """BASELINE configs[1] at full size (the bench's default launch): all 8 (b, h_kv) units, i.e.
+    all 32 query heads, each checked against the oracle."""
+    _sampled_units_check(1, 32768, 0, seed=40, units=[(0, h) for h in range(8)])
 
 
 def test_cfg3_full_size_sampled_units():
@@ -487,8 +491,11 @@ def test_attn_bitwidths(kb, vb, splits):
     _assert_close(o, L, *_run_ref(c))
 
 
-@pytest.mark.parametrize("kb,vb", [(4, 4), (8, 4), (4, 8)])
+@pytest.mark.parametrize("kb,vb", [(4, 4), (8, 4), (4, 8), (16, 16), (16, 8), (8, 16), (16, 4)])
 def test_decode_step_fused_bitwidths(kb, vb):
+    """vecinfer_decode_step at every code width pair: 4/8-bit fuse the append into the attention
+    launch, 16-bit (b4d4, 65 536-entry codebooks) run the centroid-split append launch first; the
+    appended codes are the oracle's bit for bit and the output matches the oracle."""
     B, lens = 1, [1000]
     c = _bits_case(B, kb, vb, 1003, lens, seed=120 + kb * vb)
     kn = synth.gen_keys(1, 8, 128, seed=121, batch=B)[:, 0]
@@ -498,12 +505,43 @@ def test_decode_step_fused_bitwidths(kb, vb):
     o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(CB["inv_lambda"]),
                           t_bf16(c["ck"]), t_bf16(c["cv"]), kcodes, vcodes, t_i32([999]), t_i32(lens),
                           kcfg=CFGS[kb], vcfg=CFGS[vb])
-    for h in range(8):
-        kk, vv = ref.encode_kv(kn[0, h], vn[0, h], CB["inv_lambda"][h], c["ck"][h], c["cv"][h])
+    for h in range(8):   # b4d4 books are shared by the heads ([65536, 4]), the others per head
+        ckh = c["ck"] if c["ck"].ndim == 2 else c["ck"][h]
+        cvh = c["cv"] if c["cv"].ndim == 2 else c["cv"][h]
+        kk, vv = ref.encode_kv(kn[0, h], vn[0, h], CB["inv_lambda"][h], ckh, cvh)
         c["kc"][0, h, 999], c["vc"][0, h, 999] = kk, vv
     assert np.array_equal(kcodes.cpu().numpy(), ref.pack_codes(c["kc"], kb))
     assert np.array_equal(vcodes.cpu().numpy(), ref.pack_codes(c["vc"], vb))
     _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))
+
+
+def test_decode_step_b4d4_full_size_bench_config():
+    """The bench's cfg5-b4d4 step at full size (B = 1, N = 65 536, 8 KV heads, shared 65 536-entry
+    codebooks): vecinfer_decode_step appends row N-1 (16-bit search launch) and attends; the
+    appended codes of all 8 heads are the oracle's bit for bit, and 3 heads' outputs match the oracle."""
+    N, bits = 65536, 16
+    kc = synth.gen_codes_torch((1, 8, N, 64), bits, seed=501, device=DEV)
+    vc = synth.gen_codes_torch((1, 8, N, 64), bits, seed=502, device=DEV)
+    q = synth.gen_queries(1, 32, 8, 128, seed=503)
+    kn = synth.gen_keys(1, 8, 128, seed=504)[:, 0]
+    vn = synth.gen_values(1, 8, 128, seed=505)[:, 0]
+    ck, cv = CB["ck_b4d4"], CB["cv_b4d4"]
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    o, L = vi.decode_step(t_bf16(q), t_bf16(kn), t_bf16(vn), t_f32(CB["lambda"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(ck), t_bf16(cv), kc, vc, t_i32([N - 1]), t_i32([N]), kcfg=vi.B4D4, vcfg=vi.B4D4,
+                          err_flags=err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    o, L = o.cpu().numpy(), L.cpu().numpy()
+    for h in range(8):
+        kk, vv = ref.encode_kv(kn[0, h], vn[0, h], CB["inv_lambda"][h], ck, cv)
+        assert np.array_equal(kc[0, h, N - 1].cpu().numpy(), ref.pack_codes(kk[None], bits)[0])
+        assert np.array_equal(vc[0, h, N - 1].cpu().numpy(), ref.pack_codes(vv[None], bits)[0])
+    for h in (0, 3, 7):
+        kk = ref.unpack_codes(kc[0, h].cpu().numpy(), bits)
+        vv = ref.unpack_codes(vc[0, h].cpu().numpy(), bits)
+        o_ref, L_ref = ref.attention_vq(q[0, 4 * h:4 * h + 4], CB["lambda"][h], ck, cv, kk, vv)
+        _assert_close(o[0, 4 * h:4 * h + 4], L[0, 4 * h:4 * h + 4], o_ref, L_ref)
 
 
 @pytest.mark.parametrize("bits", [4, 16])
@@ -570,8 +608,9 @@ def test_decode_step_appends_to_residual():
 
 
 def test_vqkv_cache_protocol_replay():
-    """Cache manager (residual R = 8, flush of the oldest 8 rows when 16 are held) over 40 decode
-    steps vs the oracle replay: flushed tokens are the ORACLE's codes, the window is raw."""
+    """Cache manager (residual R = 8; when an append brings the window to 16 rows,
+    the oldest 8 are flushed before attending) over 40 decode steps vs the oracle replay: flushed
+    tokens are the ORACLE's codes, the window is raw and never attended with more than 15 rows."""
     from paper_2510_06175_b200.cache import VQKVCache
     B, R, steps = 2, 8, 40
     cache = VQKVCache(B, 8, 256, t_f32(CB["lambda"]), t_f32(CB["inv_lambda"]), t_bf16(CB["ck_b2d4"]),
@@ -583,7 +622,7 @@ def test_vqkv_cache_protocol_replay():
     for i in range(steps):
         o, L = cache.step(t_bf16(qs[i]), t_bf16(ks[:, i]), t_bf16(vs[:, i]))
         n_tot = i + 1
-        if n_tot - n_q > 2 * R:     # the cache flushed before this step's append
+        if n_tot - n_q == 2 * R:    # this append filled the window: the oldest R rows were flushed
             n_q += R
         kc = np.zeros((B, 8, max(n_q, 1), 32), np.int64)
         vc = np.zeros_like(kc)
@@ -598,5 +637,5 @@ def test_vqkv_cache_protocol_replay():
             K_res=ks[:, n_q:n_tot].transpose(0, 2, 1, 3), V_res=vs[:, n_q:n_tot].transpose(0, 2, 1, 3),
             res_lens=[n_tot - n_q] * B)
         _assert_close(o.cpu().numpy(), L.cpu().numpy(), o_ref, L_ref)
-    assert cache.n_q == n_q == 24 and cache.n_r == 16
+    assert cache.n_q == n_q == 32 and cache.n_r == 8
     assert np.array_equal(cache.kc[:, :, :n_q].cpu().numpy(), kc.astype(np.uint8))

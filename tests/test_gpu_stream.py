@@ -53,6 +53,27 @@ def test_stream_repeated_calls_reuse_workspace():
         _assert_close(o, L, *_run_ref(c))
 
 
+def test_workspace_reuse_across_groups_batches_and_splits():
+    """One serving-sized workspace reused by calls that change G (2, 5: groups with padding head
+    slots), B and the split plan, through both kernels with the publish/consume merges.  Only the
+    real heads are published, so no padding element is left behind for a later call to take as a
+    fresh piece.  Every call matches the oracle, and every call repeated at the end of
+    the sequence on the same (now well-used) workspace is bitwise identical to its first run."""
+    ws = vi.attn_workspace(6, 64, 8, 3000, 40)
+    cases = [(5, 1, 12, "mma"), (2, 3, 5, "mma"), (5, 3, 0, "stream"), (2, 1, 7, "stream"), (5, 2, 3, "stream"),
+             (2, 6, 0, "mma"), (5, 6, 12, "mma"), (2, 2, 0, "stream"), (5, 4, 18, "mma"), (5, 1, 0, "mma"), (2, 1, 20, "mma")]
+    first = []
+    for i, (G, B, splits, algo) in enumerate(cases):
+        lens = [2900 - 411 * b for b in range(B)]
+        c = _attn_case(B, 8, G, 3000, lens, seed=360 + i)
+        o, L = _run_gpu(c, algo=algo, num_splits=splits, workspace=ws)
+        _assert_close(o, L, *_run_ref(c))
+        first.append((c, o, L))
+    for (G, B, splits, algo), (c, o1, L1) in zip(cases, first):
+        o2, L2 = _run_gpu(c, algo=algo, num_splits=splits, workspace=ws)
+        assert np.array_equal(o1, o2) and np.array_equal(L1, L2), (G, B, splits, algo)
+
+
 def test_stream_auto_many_units():
     """B*H_kv = 160 >= #SMs: AUTO picks the stream kernel (one unit per CTA plus a few split)."""
     lens = [300 + 37 * b for b in range(20)]
