@@ -179,7 +179,7 @@ vecinfer_status_t vecinfer_calibrate_smooth(const void* k_cal_bf16, int64_t n_to
  *                    codebooks are searched by centroid-split CTAs that combine partial
  *                    minima with 64-bit atomicMin on (dist_bits << 32 | index), plus one
  *                    arrival counter per token-head for the in-kernel finalize of the decode
- *                    append: B*T*H_kv*(2*32*8 + 4) bytes; any contents, the call fills it).
+ *                    append: B*T*H_kv*(2*32*8 + 4) bytes; any contents, the call fills it and leaves it zero).
  * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, WORKSPACE, CUDA.
  * ------------------------------------------------------------------------------------- */
 size_t vecinfer_encode_workspace_bytes(int32_t B, int32_t T, int32_t H_kv, vecinfer_vq_t kcfg,
@@ -228,7 +228,8 @@ vecinfer_status_t vecinfer_encode_kv_paged(const void* k_bf16, const void* v_bf1
  *               LUT variant: not supported (VECINFER_ERR_UNSUPPORTED).
  *   workspace   >= vecinfer_attn_workspace_bytes(B, H_q, H_kv, D, n_tokens_max, num_splits)
  *               bytes, where n_tokens_max bounds the attended range; MUST be zero-filled once
- *               when first allocated (the kernel leaves its counters at zero on exit).
+ *               when first allocated.  Every launch leaves the whole workspace zero on exit, so
+ *               one workspace may serve calls of any shape that it is large enough for.
  * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, WORKSPACE, CUDA.
  * ------------------------------------------------------------------------------------- */
 /* pieces per unit (num_splits if > 0, else the heuristic's upper bound), and the number of

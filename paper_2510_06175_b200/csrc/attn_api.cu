@@ -50,8 +50,10 @@ struct WsLayout {
 
 // counters: one 64-bit word per unit; split partials (split/LUT kernels): U*S x (L [4], o [4][128])
 // fp32; stream elements (stream kernel, auto mode only): (U + #SMs) x [4][128] 64-bit words.  The
-// two partial regions are disjoint, so a workspace shared by both kernels keeps the stream region
-// zero (its "empty" value) whatever the split kernel wrote.
+// layout depends on the call's (B, H_kv, S), so one workspace reused by calls of different shapes
+// sees every word in several roles: every kernel therefore leaves EVERY word it wrote at zero on
+// exit (counters return to zero, published elements and fp32 partials are zeroed by their
+// consumer), and zero is the "empty" value of every region.
 WsLayout ws_layout(int32_t B, int32_t H_kv, int32_t S, bool stream_region) {
   WsLayout w;
   const size_t units = static_cast<size_t>(B) * H_kv;

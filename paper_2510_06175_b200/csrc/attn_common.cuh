@@ -42,7 +42,7 @@ struct AttnArgs {
   float* lse;
   float* part_o;     // [B*Hkv*S][4][128]
   float* part_l;     // [B*Hkv*S][4]   (log2 domain)
-  uint32_t* counter; // [B*Hkv] 64-bit words: low half = last-CTA count, high half = spin epoch
+  uint32_t* counter; // [B*Hkv] 64-bit words: last-arriver counts (low half), zero on exit
   unsigned long long* phase;  // profiling builds: per-CTA phase stamps (else null)
   // fused decode append (vecinfer_decode_step): encode the new token's k, v of each (b, h_kv)
   // into cache row write_pos[b] inside the attention launch (append == 0: plain attention)
@@ -158,6 +158,9 @@ __device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
         lv[k] = ok ? __ldcg(pl + 4 * (s0 + k)) : -INFINITY;
         xv[k] = ok ? __ldcg(po + static_cast<int64_t>(s0 + k) * 512) : 0.f;
       }
+#pragma unroll
+      for (int k = 0; k < 32; ++k)   // consumed: each o element is read by this thread only
+        if (s0 + k < a.S) __stcg(const_cast<float*>(po) + static_cast<int64_t>(s0 + k) * 512, 0.f);
       float mc = -INFINITY;
 #pragma unroll
       for (int k = 0; k < 32; ++k) mc = fmaxf(mc, lv[k]);
@@ -181,6 +184,11 @@ __device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
     else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
     if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
   }
+  // the L partials are read by every dim thread of their head: zero them once all reads are done,
+  // so the whole workspace is zero on exit (a later call with another layout may reuse any word)
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.S * 4; i += NTHREADS)
+    if ((i & 3) < hm.gp) __stcg(a.part_l + unit * a.S * 4 + i, 0.f);
 }
 
 template <int NTHREADS, int NWARPS, int WROW = 128, int DH = 128, bool PRESCALED = false>
@@ -235,7 +243,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
       const int64_t pi = ((unit * a.S + s) * 4 + g) * 128 + dim;
       st_relaxed_gpu_u64(a.part_elem + pi, ~((static_cast<unsigned long long>(__float_as_uint(L2)) << 32) |
                                              __float_as_uint(ov)));
-    } else {
+    } else if (g < hm.gp) {   // real heads only: merge_splits consumes (zeroes) exactly these
       const int64_t pi = (unit * a.S + s) * 4 + g;
       a.part_o[pi * 128 + dim] = ov;
       if (dim == 0) a.part_l[pi] = L2;
@@ -323,7 +331,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
   phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 6);
   __syncthreads();
   phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 7);
-  // low 32-bit half of the unit's 64-bit barrier word (the high half holds the spin-merge epoch)
+  // low 32-bit half of the unit's 64-bit barrier word (reset to zero by the merging CTA)
   if (tid == 0) s_last = (atom_add_acq_rel_gpu(&a.counter[2 * unit], 1u) == static_cast<uint32_t>(a.S - 1));
   __syncthreads();
   phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);

@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
             unsigned long long* bar = reinterpret_cast<unsigned long long*>(a.counter) + sg.u;
             const unsigned long long old = atom_add_acq_rel_gpu_u64(bar, 1ull);
             lastp = (old & 0xFFFFFFFFull) == static_cast<unsigned long long>(sg.P - 1);
-            if (lastp) red_add_release_gpu_u64(bar, (1ull << 32) - static_cast<unsigned long long>(sg.P));
+            if (lastp) red_add_release_gpu_u64(bar, 0ull - static_cast<unsigned long long>(sg.P));   // back to zero
           }
           sflag[tid] = lastp;
         }

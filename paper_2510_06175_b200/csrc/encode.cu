@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_kernel(EncArgs a) 
     __syncthreads();
     if (!s_last || warp != 0) return;
     __threadfence();
+    if (lane == 0) cnt[bt * a.H + h] = 0u;   // every arrival is in: the word is left zero on exit
     finalize_token_head(a, bt, b, t, h, lane);
   }
 }
@@ -293,6 +294,16 @@ __device__ __forceinline__ void small_nn_global(const uint16_t* cb, const float 
 }
 
 __device__ __forceinline__ void finalize_token_head(const EncArgs& a, int64_t bt, int b, int t, int h, int lane) {
+  // consume the 16-bit minima first (zeroed even when the write row is invalid: the workspace is
+  // left zero on exit; it may be part of a vecinfer_decode_step workspace that other calls lay out
+  // differently)
+  uint32_t code16[2] = {0u, 0u};
+  for (int which = 0; which < 2; ++which) {
+    if ((which ? a.vbits : a.kbits) != 16) continue;
+    unsigned long long* slot = a.ws + ((bt * a.H + h) * 2 + which) * 32 + lane;
+    code16[which] = static_cast<uint32_t>(__ldcg(slot) & 0xFFFFFFFFull);
+    *slot = 0ull;
+  }
   int64_t row;
   if (!cache_row(a, b, t, h, lane, row)) return;
   for (int which = 0; which < 2; ++which) {
@@ -300,9 +311,7 @@ __device__ __forceinline__ void finalize_token_head(const EncArgs& a, int64_t bt
     uint8_t* codes = which ? a.vcodes : a.kcodes;
     uint32_t code;
     if (bits == 16) {
-      unsigned long long* slot = a.ws + ((bt * a.H + h) * 2 + which) * 32 + lane;
-      code = static_cast<uint32_t>(__ldcg(slot) & 0xFFFFFFFFull);
-      *slot = ~0ull;  // leave the workspace ready for the next call
+      code = code16[which];
     } else {
       float x[4];
       if (which == 0) transform_key_lane(a, b, t, h, lane, x);
@@ -475,7 +484,11 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
     const size_t need = vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg, vcfg);
     if (!workspace || workspace_bytes < need || !aligned(workspace, 8))
       return fail(VECINFER_ERR_WORKSPACE, "encode_kv: 16-bit codebooks need %zu bytes of workspace", need);
-    if (cudaMemsetAsync(workspace, 0xFF, need, st) != cudaSuccess) return check_launch("encode_kv memset");
+    // minima start at ~0 and the arrival counters at 0xFFFFFFFF; the kernels zero every word they
+    // consume, and the finalize-kernel path (no counters) fills only the minima
+    const size_t minima = static_cast<size_t>(B) * T * H_kv * 2 * 32 * sizeof(unsigned long long);
+    if (cudaMemsetAsync(workspace, 0xFF, nbt * H_kv <= 4096 ? need : minima, st) != cudaSuccess)
+      return check_launch("encode_kv memset");
     if (nbt * H_kv <= 4096) {   // decode append: the last chunk CTA of each token-head finalises it
       encode_nn16_kernel<true><<<dim3(static_cast<unsigned>(nbt), 65536 / kChunk16, H_kv), kEncWarps * 32, 0, st>>>(a);
       return check_launch("encode_nn16_kernel");

@@ -74,6 +74,43 @@ def test_workspace_reuse_across_groups_batches_and_splits():
         assert np.array_equal(o1, o2) and np.array_equal(L1, L2), (G, B, splits, algo)
 
 
+def test_workspace_left_zero_by_every_merge_path():
+    """The workspace layout depends on each call's (B, H_kv, S), so one buffer reused by calls of
+    different shapes sees every word in several roles; the contract (vecinfer.h) is that every
+    launch leaves the WHOLE workspace zero.  Checked after each call for every merge path: split
+    kernel spin merge, multi-wave last-CTA merge (fp32 partials), stream kernel spin and
+    last-arriver merges, and the 16-bit decode-step append (its centroid-split minima and arrival
+    counters live in the same buffer), with G = 5 padding slots."""
+    ws = vi.decode_step_workspace(6, 40, 8, 3000, kcfg=vi.B4D4, vcfg=vi.B4D4, num_splits=40)
+    cases = [(5, 1, 12, "mma"), (5, 4, 18, "mma"), (2, 3, 0, "stream"), (5, 3, 40, "stream"), (4, 6, 40, "mma"),
+             (4, 2, 7, "stream")]
+    for i, (G, B, splits, algo) in enumerate(cases):
+        lens = [2900 - 411 * b for b in range(B)]
+        c = _attn_case(B, 8, G, 3000, lens, seed=380 + i)
+        o, L = _run_gpu(c, algo=algo, num_splits=splits, workspace=ws)
+        torch.cuda.synchronize()
+        assert int(ws.count_nonzero()) == 0, (G, B, splits, algo)
+        _assert_close(o, L, *_run_ref(c))
+    # 16-bit decode step (separate centroid-split append launch + attention) on the same buffer
+    B, N = 2, 1003
+    c = _bits_case(B, 16, 16, N, [1000, 700], seed=390)
+    kn = synth.gen_keys(1, 8, 128, seed=391, batch=B)[:, 0]
+    vn = synth.gen_values(1, 8, 128, seed=392, batch=B)[:, 0]
+    kcodes = t_u8(ref.pack_codes(c["kc"], 16))
+    vcodes = t_u8(ref.pack_codes(c["vc"], 16))
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(c["ck"]), t_bf16(c["cv"]), kcodes, vcodes, t_i32([999, 699]), t_i32([1000, 700]),
+                          kcfg=vi.B4D4, vcfg=vi.B4D4, workspace=ws)
+    torch.cuda.synchronize()
+    assert int(ws.count_nonzero()) == 0, "16-bit decode step"
+    for b, p in ((0, 999), (1, 699)):
+        for h in range(8):
+            kk, vv = ref.encode_kv(kn[b, h], vn[b, h], CB["inv_lambda"][h], c["ck"], c["cv"])
+            c["kc"][b, h, p], c["vc"][b, h, p] = kk, vv
+    c["seq_lens"] = np.array([1000, 700], dtype=np.int32)
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))
+
+
 def test_stream_auto_many_units():
     """B*H_kv = 160 >= #SMs: AUTO picks the stream kernel (one unit per CTA plus a few split)."""
     lens = [300 + 37 * b for b in range(20)]
