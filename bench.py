@@ -197,7 +197,8 @@ def run_reference(args, rank, world):
               f"over {args.steps} steps of ~{args.ref_step_seconds}s, {threads} single-threaded oracle processes "
               f"(one per host core, NumPy fp64)")
     line = {"impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong" if (args.workload == "cfg4" and world > 1) else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "desc": desc, "global_batch": B, "seq_len": N},
             "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": sample},
@@ -315,37 +316,39 @@ def run_ours(args, rank, world, local_rank):
                            lse=lse_all[l], workspace=ws[l])
         if ev_pair is not None:
             ev_pair[1].record()
+        if seq_sharded:   # layer l's output feeds layer l+1: its partials are exchanged right away
+            exchange_layer(l)
 
-    # sequence-sharded exchange: the fused peer-memory kernel (vecinfer_merge_lse_p2p: remote stores
-    # into every rank's IPC window + flags + rank-order merge, one launch) or NCCL all-gather +
-    # vecinfer_merge_lse (--exchange nccl)
-    p2p = P2PExchange(L * B * H_Q, D, dev) if (seq_sharded and args.exchange == "p2p") else None
-    lse_m = torch.empty(L * B, H_Q, dtype=torch.float32, device=dev) if seq_sharded else None
+    # sequence-sharded exchange, once PER LAYER (16.1 KiB of partials per rank and layer at B = 1):
+    # the fused peer-memory kernel (vecinfer_merge_lse_p2p: remote stores into every rank's IPC
+    # window + flags + rank-order merge, one launch, graph-safe) or NCCL all-gather of the packed
+    # partials + vecinfer_merge_lse (--exchange nccl; gloo through host copies for 1-GPU checks)
+    p2p = P2PExchange(B * H_Q, D, dev) if (seq_sharded and args.exchange == "p2p") else None
+    lse_m = torch.empty(L, B, H_Q, dtype=torch.float32, device=dev) if seq_sharded else None
 
-    def exchange_and_merge():
+    def exchange_layer(l):
         if p2p is not None:
-            p2p.merge(o_part.view(L * B, H_Q, D), lse_all.view(L * B, H_Q), out=o_all.view(L * B, H_Q, D), lse=lse_m)
+            p2p.merge(o_part[l], lse_all[l], out=o_all[l], lse=lse_m[l])
             return
         if args.backend == "gloo":
-            o_g, l_g = gather_partials_packed(o_part.cpu(), lse_all.cpu())
+            o_g, l_g = gather_partials_packed(o_part[l].cpu(), lse_all[l].cpu())
             o_g, l_g = o_g.to(dev), l_g.to(dev)
         else:
-            o_g, l_g = gather_partials_packed(o_part, lse_all)
-        vi.merge_lse(o_g.reshape(world, L * B, H_Q, D).contiguous(), l_g.reshape(world, L * B, H_Q).contiguous(),
-                     o_dtype=torch.bfloat16, out=o_all.view(L * B, H_Q, D), lse=lse_m)
+            o_g, l_g = gather_partials_packed(o_part[l], lse_all[l])
+        vi.merge_lse(o_g.contiguous(), l_g.contiguous(), o_dtype=torch.bfloat16, out=o_all[l], lse=lse_m[l])
 
     def step_eager(evs=None):
         for l in range(L):
             layer(l, None if evs is None else evs[l])
-        if seq_sharded:   # exchange the per-rank partials of all 32 layers, then LSE merge
-            exchange_and_merge()
 
     # 16-bit append: one centroid-split search launch (finalised in-kernel) up to 4096 token-heads
     append_kernels = 2 if (max(kbits, vbits) == 16 and B * H_KV > 4096) else 1
     if fused:
         launches_per_step = L * vi.decode_step_launches(B, H_KV, n_local, kcfg, vcfg, residual_append=bool(R))
     else:
-        launches_per_step = L * ((append_kernels if owns_tail else 0) + 1) + (1 if seq_sharded else 0)
+        # + one exchange per layer when sequence-sharded (the P2P kernel; NCCL's own kernels and
+        # merge_lse with --exchange nccl: 1 of ours)
+        launches_per_step = L * ((append_kernels if owns_tail else 0) + 1 + (1 if seq_sharded else 0))
 
     # ---- warm-up (eager) so lazy init/attributes happen outside capture
     with torch.cuda.stream(stream):
@@ -400,6 +403,7 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    elapsed_ms_local = elapsed_ms
     elapsed_ms = max_over_ranks(elapsed_ms)
 
     # ---- dominant kernel (vecinfer_attn_decode) timed alone: K replays of the 32-layer attention
@@ -438,6 +442,7 @@ def run_ours(args, rank, world, local_rank):
         if seq_sharded:
             vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_part[l],
                            lse=lse_all[l], workspace=ws[l])
+            exchange_layer(l)
         else:
             vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
                            lse=lse_all[l], workspace=ws[l])
@@ -445,8 +450,6 @@ def run_ours(args, rank, world, local_rank):
     def layers_e2e():
         for l in range(L):
             layer_e2e(l)
-        if seq_sharded:
-            exchange_and_merge()
 
     # Pipelined end-to-end step (graph path): the H2D copies of q / k_new / v_new are issued in
     # chunks of 8 layers on a copy stream, a chunk's launches wait only for its own inputs, and the
@@ -519,6 +522,15 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         e2e_ms = t0e.elapsed_time(t1e)
     e2e_ms = max_over_ranks(e2e_ms)
+    # per-rank evidence (every rank's own device time, device identity and process group backend)
+    rank_info = {"rank": rank, "step_ms": elapsed_ms_local / K, "device": torch.cuda.get_device_name(dev),
+                 "pci_bus_id": torch.cuda.get_device_properties(dev).pci_bus_id if hasattr(
+                     torch.cuda.get_device_properties(dev), "pci_bus_id") else None, "cuda_device": dev.index}
+    ranks = [rank_info]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, rank_info)
+    p2p_err = int(p2p.err.item()) if p2p is not None else 0
     h2d = q_h.numel() * 2 + kn_h.numel() * 2 + vn_h.numel() * 2 if owns_tail else q_h.numel() * 2
     d2h = o_h.numel() * 2
 
@@ -558,7 +570,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": args.workload, "desc": desc, "global_batch": B_glob, "seq_len": N,
                    "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": f"K-{CB_NAME[kbits]}/V-{CB_NAME[vbits]}",
                    "parallelism": ("seq-shard" if seq_sharded else "dp") + str(world),
-                   "exchange": (("p2p-fused-merge" if args.exchange == "p2p" else "nccl-allgather+merge_lse")
+                   "exchange": (("p2p-fused-merge" if args.exchange == "p2p" else
+                                 f"{args.backend}-allgather+merge_lse") + ", per layer (32 exchanges per step)"
                                 if seq_sharded else None),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
                    "num_splits": S, "attn_kernel": kernel_kind, "cuda_graph": use_graph, "residual_window": R, "fused_append": fused_launch,
@@ -580,6 +593,12 @@ def run_ours(args, rank, world, local_rank):
                 "ms_per_step": e2e_ms / K, "api": ("32 x vecinfer.decode_step + pinned H2D / D2H copies in 4 layer chunks pipelined on two copy streams, one CUDA graph per step, host sync on the result; " if g_e2e is not None else "32 eager vecinfer calls, ")
                        + "pinned H2D of q/k/v and D2H of o every step"},
         "gpu_launches": launches_per_step * K,
+        "ranks": ranks if world > 1 else None,
+        "dist": ({"backend": args.backend, "world": world, "p2p_timeout_flag": p2p_err,
+                  "nccl_version": (".".join(map(str, torch.cuda.nccl.version())) if args.backend == "nccl" else None),
+                  "shard": f"rank r attends tokens [r*N/{world}, (r+1)*N/{world}) (32-aligned)" if seq_sharded else
+                  (f"batch slice {B} of {B_glob} sequences per rank" if args.workload == "cfg3" else "replica")}
+                 if world > 1 else None),
         "clocks": clk.summary(),
         "prefill_encode": {"tokens_per_s": prefill_tok_s, "alu_frac": prefill_alu_frac,
                            "note": "bulk vecinfer_encode_kv, all 8 KV heads, K+V, 4096-token chunks back to back after a warm-up"},
@@ -594,7 +613,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: cfg2 (configs[1]) at N=1; cfg4 (configs[3], 196k tokens sequence-sharded with a "
+                         "per-layer exchange, strong scaling) at N>1; cfg3 = batch x head sharding (weak)")
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -611,6 +632,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload is None:
+        args.workload = "cfg4" if world > 1 else "cfg2"
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
