@@ -78,12 +78,20 @@ typedef struct {
  *  DEQUANT_MMA_STREAM: DEQUANT_MMA with the stream partition (units cut into pieces so every
  *    CTA gets the same number of tokens; pieces merged in fixed order).  AUTO selects it for
  *    B*H_kv >= #SMs (batch decode); forcing it here with num_splits = S > 0 gives exactly S
- *    pieces per unit (grid min(B*H_kv*S, #SMs) persistent CTAs). */
+ *    pieces per unit (grid min(B*H_kv*S, #SMs) persistent CTAs).
+ *  DEQUANT_TC: the split DEQUANT_MMA kernel with the score contraction (Alg. 1 l.11 as q~ K^T)
+ *    on the 5th-generation tensor cores: each 4-warp group stages its 128 gathered K^ rows in
+ *    tensor memory (tcgen05.st), one thread issues tcgen05.mma (A = K^ in TMEM, B = q~ hi/lo in
+ *    shared memory, fp32 scores in TMEM), the scores return with tcgen05.ld; P.V stays on
+ *    mma.sync.  Contiguous caches, D = 128, K codebooks b1d4 / b2d4 (V: b1d4 / b2d4 / b4d4);
+ *    anything else is VECINFER_ERR_UNSUPPORTED.  AUTO never selects it: measured slower than
+ *    DEQUANT_MMA on B200. */
 typedef enum {
   VECINFER_ATTN_AUTO = 0,
   VECINFER_ATTN_DEQUANT_MMA = 1,
   VECINFER_ATTN_LUT = 2,
-  VECINFER_ATTN_DEQUANT_MMA_STREAM = 3
+  VECINFER_ATTN_DEQUANT_MMA_STREAM = 3,
+  VECINFER_ATTN_DEQUANT_TC = 4
 } vecinfer_attn_algo_t;
 
 /* Paged code cache (serving integration): k_codes / v_codes are a pool of

@@ -217,8 +217,13 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: NULL pointer");
   if (o_dtype != VECINFER_BF16 && o_dtype != VECINFER_F32) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad o_dtype");
   if (algo != VECINFER_ATTN_AUTO && algo != VECINFER_ATTN_DEQUANT_MMA && algo != VECINFER_ATTN_LUT &&
-      algo != VECINFER_ATTN_DEQUANT_MMA_STREAM)
+      algo != VECINFER_ATTN_DEQUANT_MMA_STREAM && algo != VECINFER_ATTN_DEQUANT_TC)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad algo");
+  const bool tc = algo == VECINFER_ATTN_DEQUANT_TC;
+  if (tc && (pg || kcfg.head_dim != 128 || vcfg.head_dim != 128 || kcfg.sub_dim != 4 || vcfg.sub_dim != 4 ||
+             (kcfg.code_bits != 4 && kcfg.code_bits != 8) || (vcfg.code_bits != 4 && vcfg.code_bits != 8 && vcfg.code_bits != 16)))
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: DEQUANT_TC needs a contiguous cache, D = 128, d = 4 and K codes "
+                "of 4 or 8 bits");
   if (B <= 0 || H_q <= 0 || H_kv <= 0 || n_cap <= 0) return fail(VECINFER_ERR_SHAPE, "attn_decode: non-positive size");
   if (H_q % H_kv != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode: H_q %% H_kv != 0");
   const int Gfull = H_q / H_kv;
@@ -262,7 +267,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
       return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_paged: paged caches run the split DEQUANT_MMA kernel only");
     if (tok_begin % 32 != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode_paged: tok_begin must be a multiple of 32");
   }
-  const bool use_sk = !pg && !next2 && D == 128 && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
+  const bool use_sk = !tc && !pg && !next2 && D == 128 && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
   SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
   if (D == 64) plan.cluster = 0;   // the DSMEM cluster merge is written for 128-dim rows
   const int32_t S = plan.S;
@@ -311,6 +316,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.rcpV = 1.0 / static_cast<double>(V);
   a.merge = !stream_split ? kMergeNone : (V <= sms ? kMergeSpin : kMergeLast);
   a.cluster = plan.cluster;
+  a.tc = tc ? 1 : 0;
   a.merge_kernel = (S > 1 && !plan.cluster && algo != VECINFER_ATTN_LUT && D == 128) ? merge_mode_from_env() : 0;
   // every CTA co-resident (one CTA per SM, grid <= SMs): spin-barrier + sliced merge
   a.merge_spin = (S > 1 && !plan.cluster && !a.merge_kernel && algo != VECINFER_ATTN_LUT &&
@@ -408,7 +414,7 @@ static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t k
   const int64_t units = static_cast<int64_t>(B) * H_kv;
   if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
     return num_splits == 0 || units * num_splits <= device_sm_count();   // persistent grids: separate append
-  if (!paged && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
+  if (!paged && algo != VECINFER_ATTN_DEQUANT_TC && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
   const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
   const int mac = plan.cluster ? attn_mma_max_active_clusters(plan.S) : 0;
   const int64_t waves = plan.cluster ? (units + (mac > 0 ? mac : 1) - 1) / (mac > 0 ? mac : 1)
@@ -420,6 +426,7 @@ static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t k
 extern "C" int32_t vecinfer_attn_kernel_kind(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits,
                                              vecinfer_attn_algo_t algo) {
   if (algo == VECINFER_ATTN_LUT) return 2;
+  if (algo == VECINFER_ATTN_DEQUANT_TC) return 0;
   return use_stream(B, H_kv, n_tokens_max, num_splits, false, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM) ? 1 : 0;
 }
 

@@ -29,6 +29,7 @@ struct AttnArgs {
   int S;                       // splits per (b, h_kv)
   int n_items;                 // B * H_kv * S work items
   int cluster;                 // 1: the S splits of a (b, h_kv) form one cluster, merged over DSMEM
+  int tc;                      // 1: split kernel with the tcgen05 score contraction (VECINFER_ATTN_DEQUANT_TC)
   int merge_kernel;            // 1: split partials are merged by a separate PDL-launched kernel
   int merge_spin;              // 1: single-wave grid, every CTA merges a slice after an arrival barrier
   // stream kernel (attn_stream.cu): U = B*H_kv units and V virtual CTAs tile one line of U*V ticks

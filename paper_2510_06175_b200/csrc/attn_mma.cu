@@ -25,6 +25,11 @@
 // deterministic); multi-wave grids merge in the last-arriving CTA; S <= 16 clusters can merge over
 // DSMEM.  See DESIGN.md "N4".
 #include "attn_tiles.cuh"
+#include "tc.cuh"
+
+#ifndef VECINFER_TC_EXP
+#define VECINFER_TC_EXP 0   // != 0 only in timing-experiment builds (results not valid)
+#endif
 
 namespace vecinfer {
 namespace {
@@ -34,8 +39,18 @@ constexpr int kMiscQ = 0;
 constexpr int kMiscNew = 2688;                       // 128 B: codes of the appended token (K at +0, V at +64)
 constexpr int kMiscW = 2816;                         // wm[16][4], wl[16][4], wacc[16][4][kWRow]
 constexpr int kWRow = 132;   // warp-partial row stride: the 16-byte stores of a warp spread over all banks
-constexpr int kMiscBytes = kMiscW + (kNW * 8 + kNW * 4 * kWRow) * 4;   // 37120
+constexpr int kMiscWEnd = kMiscW + (kNW * 8 + kNW * 4 * kWRow) * 4;   // 37120
+// tcgen05 score path (TC): B operand = q~ hi/lo [16 rows x 128] fp16 in the K-major no-swizzle
+// canonical layout (element (n, k) at ((k/8)*2 + n/8)*128 + (n%8)*16 + (k%8)*2; rows 8..15 zero),
+// then the TMEM base address and one mbarrier per 4-warp group
+constexpr int kMiscTCB = 37888;
+constexpr int kMiscTCM = kMiscTCB + 4096;            // [0]: TMEM base, [8 + 8g]: mbarrier of group g
+constexpr int kMiscBytes = kMiscTCM + 64;            // 42048
+static_assert(kMiscWEnd <= kMiscTCB, "misc layout");
 static_assert(4 * kQRow * 4 <= kMiscNew, "q~ rows");
+// TMEM columns: group g (warps 4g..4g+3, one per 32-lane quarter) stages its 128-token K^ tile in
+// columns [64g, 64g + 64) (128 fp16 dims per lane = token) and gets its scores in [256 + 16g, +16)
+constexpr uint32_t kTmemCols = 512;
 constexpr int kClusterMax = 16;                      // DSMEM merge buffer: [16][4][128] + m, l
 constexpr int kCbufBytes = kClusterMax * 4 * 130 * 4;
 constexpr int kSmemBytes = 65536 + kTab + kCbufBytes + 1024;  // pad + table + cluster buffer + slack
@@ -46,10 +61,31 @@ template <int KB, int VB>
 constexpr int smem_bytes() { return (!Fmt<KB>::kSmem && !Fmt<VB>::kSmem) ? kSmemBytesNoTab : kSmemBytes; }   // (== smem_for)
 
 
-template <int KB, int VB, int DH>
+// K code row of one token for the tcgen05 score path (lane = token): 32 sub-vector codes
+template <int KB> struct KRowT { uint4 w[Fmt<KB>::kRow / 16]; };
+// shared address of the centroid of sub-vector m of a K row (code byte / nibble -> address bits 8..)
+template <int KB, int M>
+__device__ __forceinline__ uint32_t krow_addr(const KRowT<KB>& kr, uint32_t base) {
+  if constexpr (KB == 8) {
+    const uint4& q = kr.w[M / 16];
+    constexpr int wi = (M / 4) % 4;
+    const uint32_t w = wi == 0 ? q.x : wi == 1 ? q.y : wi == 2 ? q.z : q.w;
+    return prmt(w, base, 0x7604u | ((M & 3) << 4));
+  } else {
+    const uint4& q = kr.w[0];
+    constexpr int wi = M / 8;
+    const uint32_t w = wi == 0 ? q.x : wi == 1 ? q.y : wi == 2 ? q.z : q.w;
+    return Fmt<4>::nib8<M % 8>(w) | base;
+  }
+}
+
+template <int KB, int VB, int DH, bool TC>
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
   // DH = head dim (128, or 64: NEXT-4).  KS score k-steps (4 sub-vectors each) per 16 tokens,
   // VS V sub-vectors per lane r (2 P.V m-tiles each), NL lanes holding a q~ row.
+  // TC: the score contraction runs on tcgen05 (K^ tile in TMEM, q~ in shared memory, fp32 scores
+  // in TMEM) instead of mma.sync; contiguous caches, D = 128, 4/8-bit K codebooks only.
+  static_assert(!TC || ((KB == 4 || KB == 8) && DH == 128), "TC path: d = 4 K codebooks in the shared table, D = 128");
   using FK = FmtD<KB, DH>;
   using FV = FmtD<VB, DH>;
   constexpr int KR = FK::kRow, VR = FV::kRow;
@@ -77,6 +113,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   // to each CTA; larger problems run persistent CTAs (one per SM) over items, so the per-CTA
   // prologue/epilogue and the wave ramp are paid once per item instead of once per wave.
   const int nblk = gridDim.x * gridDim.y * gridDim.z;
+  // tcgen05 state: TMEM columns (allocated once per CTA), one mbarrier per 4-warp group whose phase
+  // advances once per issued score MMA batch, the q~ B tile (rows 8..15 stay zero)
+  unsigned char* tcb = smem_raw + kMiscTCB;
+  uint32_t* tc_misc = reinterpret_cast<uint32_t*>(smem_raw + kMiscTCM);
+  uint32_t tc_phase = 0;
+  if constexpr (TC) {
+    if (warp == 0) tc::alloc(smem_u32(tc_misc), kTmemCols);
+    if (tid < 4) tc::mbar_init(smem_u32(tc_misc + 2 + 2 * tid), 1);
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tid < 128) *reinterpret_cast<uint4*>(tcb + ((tid >> 3) * 2 + 1) * 128 + (tid & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+  }
   bool first = true;
   for (int item = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); item < a.n_items; item += nblk) {
   const int s = item % a.S, h = (item / a.S) % a.Hkv, b = item / (a.S * a.Hkv);
@@ -143,7 +190,33 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   // first tile's loads go out before the query transform so HBM latency overlaps it
   TileCodes<KB, VB> nxt;
-  if (warp < ntile) {
+  // TC path (contiguous): K rows by token (lane = row of the warp's tile), V codes as in TileCodes
+  const int64_t row0 = unit * a.n_cap + r0;   // cache row of the split's first token
+  const uint8_t* const kq = a.kcodes + (row0 + lane) * KR;   // this lane's row of the split's first tile
+  const uint8_t* const vq = vcb + row0 * VR;
+  auto load_krow = [&](KRowT<KB>& kr, int it) {
+    const int rem = ntok - 32 * it;
+    const uint8_t* p = kq + static_cast<int64_t>(it) * (32 * KR);
+#pragma unroll
+    for (int i = 0; i < KR / 16; ++i) kr.w[i] = lane < rem ? ldg_nc_u128(p + 16 * i) : make_uint4(0u, 0u, 0u, 0u);
+  };
+  auto load_vtile = [&](TileCodes<KB, VB>& tcv, int it) {   // the V half of a TileCodes
+    const int rem = ntok - 32 * it;
+    const uint8_t* p = vq + static_cast<int64_t>(it) * (32 * VR);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int t0 = 16 * q + 2 * j;
+      tcv.v[q][0] = (rem >= 32 || t0 < rem) ? FV::ldv(p + (16 * q) * VR) : VCode<VB>{};
+      tcv.v[q][1] = (rem >= 32 || t0 + 1 < rem) ? FV::ldv(p + (16 * q + 1) * VR) : VCode<VB>{};
+      tcv.v[q][2] = (rem >= 32 || t0 + 8 < rem) ? FV::ldv(p + (16 * q + 8) * VR) : VCode<VB>{};
+      tcv.v[q][3] = (rem >= 32 || t0 + 9 < rem) ? FV::ldv(p + (16 * q + 9) * VR) : VCode<VB>{};
+    }
+  };
+  KRowT<KB> kfirst0, kfirst1;
+  if constexpr (TC) {
+    if (warp < ntile) { load_krow(kfirst0, warp); load_vtile(nxt, warp); }
+    if (warp + kNW < ntile) load_krow(kfirst1, warp + kNW);
+  } else if (warp < ntile) {
     const int rem = ntok - 32 * warp;
     if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
     else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
@@ -207,8 +280,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     float* dq = sq + kQRow * warp + qoff(lane);
     if (warp < hm.gp) qtransform_lane(qw, lam4, a.qscale, lane, dq, NL);
     else if (lane < NL) *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (TC) {
+      // B operand of the tcgen05 score MMA: row 2g = RN16(q~_g), row 2g+1 = RN16(q~_g - hi), dims in
+      // natural order (this lane's sub-vector = K elements 4 lane .. 4 lane + 3)
+      const float4 v = *reinterpret_cast<const float4*>(dq);
+      const float in[4] = {v.x, v.y, v.z, v.w};
+      float hi[4], lo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        hi[i] = __half2float(__float2half_rn(in[i]));
+        lo[i] = in[i] - hi[i];
+      }
+      unsigned char* cm = tcb + (lane >> 1) * 2 * 128 + (lane & 1) * 8;
+      *reinterpret_cast<uint2*>(cm + (2 * warp) * 16) = make_uint2(pack_half2(hi[0], hi[1]), pack_half2(hi[2], hi[3]));
+      *reinterpret_cast<uint2*>(cm + (2 * warp + 1) * 16) = make_uint2(pack_half2(lo[0], lo[1]), pack_half2(lo[2], lo[3]));
+      tc::fence_proxy_async_smem();   // generic-proxy stores -> the tensor core reads them
+    }
   }
+  if constexpr (TC) tc::fence_before();
   __syncthreads();
+  if constexpr (TC) tc::fence_after();
   if (kCanAppend && owner) {
     if (warp == 0 || warp == 8) {
       const float* sbest = reinterpret_cast<const float*>(smem_raw + kMiscW + 8192);
@@ -238,8 +329,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   // B fragments of the score MMA: column n = lane/4 <-> (head n/2, part n%2); rows k
   // <-> sub-vector 8j+t, components {0,1} (b0) and {2,3} (b1)
-  uint32_t bq0[KS], bq1[KS];
-  {
+  uint32_t bq0[TC ? 1 : KS], bq1[TC ? 1 : KS];
+  if constexpr (!TC) {
     const int gq = r >> 1, part = r & 1;
 #pragma unroll
     for (int t = 0; t < KS; ++t) {
@@ -322,77 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
   }
 
-  for (int it = warp; it < ntile; it += kNW) {
-    TileCodes<KB, VB> cur = nxt;
-    if constexpr (kCanAppend) {
-    if (it == patch_tile) {   // the appended row: codes just encoded, not the stale load
-      KCode<KB> nk;
-      VCode<VB> nv;
-      if constexpr (KB == 8) nk = *reinterpret_cast<const uint2*>(newcodes + 8 * j);
-      else nk = *reinterpret_cast<const uint32_t*>(newcodes + Fmt<(KB <= 8 ? KB : 8)>::kOffK * j);
-      if constexpr (VB == 8) nv = *reinterpret_cast<const uint32_t*>(newcodes + 64 + 4 * r);
-      else nv = *reinterpret_cast<const uint16_t*>(newcodes + 64 + Fmt<(VB <= 8 ? VB : 8)>::kOffV * r);
-      const int qp = patch_row >> 4, rr = patch_row & 15;
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (q != qp) continue;
-        if (r == rr) cur.k[q][0] = nk;
-        if (r + 8 == rr) cur.k[q][1] = nk;
-        if (2 * j == rr) cur.v[q][0] = nv;
-        if (2 * j + 1 == rr) cur.v[q][1] = nv;
-        if (2 * j + 8 == rr) cur.v[q][2] = nv;
-        if (2 * j + 9 == rr) cur.v[q][3] = nv;
-      }
-    }
-    }
-    const int rem_cur = ntok - 32 * it;
-    if (it + kNW < ntile) {
-      if (paged) {
-        const int64_t tok = r0 + 32 * static_cast<int64_t>(it + kNW);
-        const int64_t rw = row_in(pg_ahead, tok);
-        kp = kcb + rw * KR;
-        vp = vcb + rw * VR;
-        if (it + 2 * kNW < ntile) pg_ahead = page_of(tok + 32 * kNW);
-      } else {
-        kp += kStepK;
-        vp += kStepV;
-      }
-      const int rem = rem_cur - 32 * kNW;
-      if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
-      else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
-    }
-
-    // ---- scores (log2 units) for tile tokens 16q + {r, r+8}, head j; two independent MMA
-    // accumulator chains per sub-tile (k-steps 0-3 and 4-7) halve the dependent HMMA latency
-    float sc[2][2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-      if constexpr (Fmt<KB>::kWide) {   // d8b8: one 16-byte gather = virtual sub-vectors 2i, 2i+1
-        static_for<0, KS / 2>([&](auto I) {
-          constexpr int i = decltype(I)::value, t = 2 * i;
-          const uint4 wa = lds_u128(Fmt<KB>::template kaddr<i>(cur.k[q][0], kbase));
-          const uint4 wb = lds_u128(Fmt<KB>::template kaddr<i>(cur.k[q][1], kbase));
-          if (t < KS / 2) {
-            mma_16816(d0, wa.x, wb.x, wa.y, wb.y, bq0[t], bq1[t]);
-            mma_16816(d0, wa.z, wb.z, wa.w, wb.w, bq0[t + 1], bq1[t + 1]);
-          } else {
-            mma_16816(d1, wa.x, wb.x, wa.y, wb.y, bq0[t], bq1[t]);
-            mma_16816(d1, wa.z, wb.z, wa.w, wb.w, bq0[t + 1], bq1[t + 1]);
-          }
-        });
-      } else {
-        static_for<0, KS>([&](auto T) {
-          constexpr int t = decltype(T)::value;
-          const uint2 ea = gather_k<KB, t>(cur.k[q][0], kbase, cbk);
-          const uint2 eb = gather_k<KB, t>(cur.k[q][1], kbase, cbk);
-          if (t < KS / 2) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
-          else mma_16816(d1, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
-        });
-      }
-      sc[q][0] = (d0[0] + d1[0]) + (d0[1] + d1[1]);
-      sc[q][1] = (d0[2] + d1[2]) + (d0[3] + d1[3]);
-    }
+  // mask of a ragged tile, online softmax (Alg. 1 l.12-13, 18) and P.V (l.16) of one 32-token tile
+  // given its scores sc[q][0/1] (tokens 16q + r / 16q + r + 8, head j; mma accumulator layout)
+  auto softmax_pv = [&](float (&sc)[2][2], const TileCodes<KB, VB>& cur, int rem_cur) {
     if (rem_cur < 32) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -462,8 +485,213 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         });
       }
     }
-  }
+  };
 
+  if constexpr (!TC) {
+    for (int it = warp; it < ntile; it += kNW) {
+      TileCodes<KB, VB> cur = nxt;
+      if constexpr (kCanAppend) {
+      if (it == patch_tile) {   // the appended row: codes just encoded, not the stale load
+        KCode<KB> nk;
+        VCode<VB> nv;
+        if constexpr (KB == 8) nk = *reinterpret_cast<const uint2*>(newcodes + 8 * j);
+        else nk = *reinterpret_cast<const uint32_t*>(newcodes + Fmt<(KB <= 8 ? KB : 8)>::kOffK * j);
+        if constexpr (VB == 8) nv = *reinterpret_cast<const uint32_t*>(newcodes + 64 + 4 * r);
+        else nv = *reinterpret_cast<const uint16_t*>(newcodes + 64 + Fmt<(VB <= 8 ? VB : 8)>::kOffV * r);
+        const int qp = patch_row >> 4, rr = patch_row & 15;
+  #pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q != qp) continue;
+          if (r == rr) cur.k[q][0] = nk;
+          if (r + 8 == rr) cur.k[q][1] = nk;
+          if (2 * j == rr) cur.v[q][0] = nv;
+          if (2 * j + 1 == rr) cur.v[q][1] = nv;
+          if (2 * j + 8 == rr) cur.v[q][2] = nv;
+          if (2 * j + 9 == rr) cur.v[q][3] = nv;
+        }
+      }
+      }
+      const int rem_cur = ntok - 32 * it;
+      if (it + kNW < ntile) {
+        if (paged) {
+          const int64_t tok = r0 + 32 * static_cast<int64_t>(it + kNW);
+          const int64_t rw = row_in(pg_ahead, tok);
+          kp = kcb + rw * KR;
+          vp = vcb + rw * VR;
+          if (it + 2 * kNW < ntile) pg_ahead = page_of(tok + 32 * kNW);
+        } else {
+          kp += kStepK;
+          vp += kStepV;
+        }
+        const int rem = rem_cur - 32 * kNW;
+        if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
+        else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
+      }
+  
+      // ---- scores (log2 units) for tile tokens 16q + {r, r+8}, head j; two independent MMA
+      // accumulator chains per sub-tile (k-steps 0-3 and 4-7) halve the dependent HMMA latency
+      float sc[2][2];
+  #pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+        if constexpr (Fmt<KB>::kWide) {   // d8b8: one 16-byte gather = virtual sub-vectors 2i, 2i+1
+          static_for<0, KS / 2>([&](auto I) {
+            constexpr int i = decltype(I)::value, t = 2 * i;
+            const uint4 wa = lds_u128(Fmt<KB>::template kaddr<i>(cur.k[q][0], kbase));
+            const uint4 wb = lds_u128(Fmt<KB>::template kaddr<i>(cur.k[q][1], kbase));
+            if (t < KS / 2) {
+              mma_16816(d0, wa.x, wb.x, wa.y, wb.y, bq0[t], bq1[t]);
+              mma_16816(d0, wa.z, wb.z, wa.w, wb.w, bq0[t + 1], bq1[t + 1]);
+            } else {
+              mma_16816(d1, wa.x, wb.x, wa.y, wb.y, bq0[t], bq1[t]);
+              mma_16816(d1, wa.z, wb.z, wa.w, wb.w, bq0[t + 1], bq1[t + 1]);
+            }
+          });
+        } else {
+          static_for<0, KS>([&](auto T) {
+            constexpr int t = decltype(T)::value;
+            const uint2 ea = gather_k<KB, t>(cur.k[q][0], kbase, cbk);
+            const uint2 eb = gather_k<KB, t>(cur.k[q][1], kbase, cbk);
+            if (t < KS / 2) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
+            else mma_16816(d1, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
+          });
+        }
+        sc[q][0] = (d0[0] + d1[0]) + (d0[1] + d1[1]);
+        sc[q][1] = (d0[2] + d1[2]) + (d0[3] + d1[3]);
+      }
+      softmax_pv(sc, cur, rem_cur);
+    }
+  }
+  if constexpr (TC) {
+    // tcgen05 score path.  Group g = warps 4g..4g+3 (TMEM lane quarters 0..3) processes 128-token
+    // chunks; warp 4g+k owns tile it = 4g + k + 16n of iteration n (the same tiles as the mma.sync
+    // path).  Per tile: every lane gathers the 32 centroids of ITS token (row = lane) into TMEM
+    // columns [64g, 64g + 64) (tcgen05.st, no LSU traffic), the group meets at a named barrier and
+    // one thread issues 8 MMAs (M = 128 tokens, N = 16 = 4 heads x {hi, lo} + 8 zero rows, K = 16
+    // dims each) committed to the group's mbarrier; the scores come back with tcgen05.ld.16x256b in
+    // the mma.sync accumulator layout, so the softmax and the P.V are the same code as above.
+    // Software pipeline: MMA(n + 1) is issued before the softmax / P.V of tile n (one A buffer:
+    // tile n + 1 is staged only after MMA(n) completed; one D buffer: read before the barrier).
+    // warp-uniform by construction (shuffle from lane 0): lets the compiler keep the TMEM addresses
+    // and the barrier ids in uniform registers
+    const int wu = __shfl_sync(0xffffffffu, warp, 0);
+    const int grp = wu >> 2, quarter = wu & 3;
+    const int n_g = ntile > 4 * grp ? (ntile - 4 * grp + kNW - 1) / kNW : 0;
+    const uint32_t tmem = tc_misc[0];
+    const uint32_t lane_sh = static_cast<uint32_t>(32 * quarter) << 16;
+    const uint32_t t_a = tmem + 64 * grp, t_d = tmem + 256 + 16 * grp;
+    const uint32_t mbar = smem_u32(tc_misc + 2 + 2 * grp);
+    const uint32_t b_s = smem_u32(tcb);
+    constexpr uint32_t kIdesc = tc::idesc_f16_f32<128, 16>();
+    auto issue_scores = [&](const KRowT<KB>& kr, int it) {
+      if (it < ntile) {
+        KRowT<KB> k = kr;
+        if constexpr (kCanAppend) {
+          if (it == patch_tile && lane == patch_row) {   // the appended row: codes just encoded
+#pragma unroll
+            for (int i = 0; i < KR / 16; ++i) k.w[i] = *reinterpret_cast<const uint4*>(newcodes + 16 * i);
+          }
+        }
+        // 4 chunks of 8 sub-vectors (16 TMEM columns); the gathers of chunk c + 1 are in flight
+        // while chunk c is stored
+        auto gather = [&](auto C, uint32_t (&v)[16]) {
+          constexpr int c = decltype(C)::value;
+          static_for<0, 8>([&](auto MM) {
+            constexpr int mm = decltype(MM)::value;
+            const uint2 e = lds_u64(krow_addr<KB, 8 * c + mm>(k, kbase));
+            v[2 * mm] = e.x;
+            v[2 * mm + 1] = e.y;
+          });
+        };
+        uint32_t va[16], vb[16];
+#if VECINFER_TC_EXP == 2   // timing experiment: gathers kept, no TMEM stores
+        uint32_t x = 0;
+        gather(std::integral_constant<int, 0>{}, va); gather(std::integral_constant<int, 1>{}, vb);
+        for (int i = 0; i < 16; ++i) x ^= va[i] ^ vb[i];
+        gather(std::integral_constant<int, 2>{}, va); gather(std::integral_constant<int, 3>{}, vb);
+        for (int i = 0; i < 16; ++i) x ^= va[i] ^ vb[i];
+        if (x == 0x12345678u) tc::st_32x32b_x16(t_a + lane_sh, va);
+#else
+        gather(std::integral_constant<int, 0>{}, va);
+        gather(std::integral_constant<int, 1>{}, vb);
+        tc::st_32x32b_x16(t_a + lane_sh, va);
+        gather(std::integral_constant<int, 2>{}, va);
+        tc::st_32x32b_x16(t_a + lane_sh + 16, vb);
+        gather(std::integral_constant<int, 3>{}, vb);
+        tc::st_32x32b_x16(t_a + lane_sh + 32, va);
+        tc::st_32x32b_x16(t_a + lane_sh + 48, vb);
+#endif
+#if VECINFER_TC_EXP != 1   // (1: timing experiment without the store wait)
+        tc::wait_st();
+#endif
+      }
+      tc::fence_before();
+      // the group's quarter-0 warp waits for the other three and issues; they only arrive (their
+      // next TMEM write follows the wait for this MMA, so the barrier phases cannot overlap)
+      if (quarter == 0) {
+#if VECINFER_TC_EXP != 3   // (3: timing experiment without the group barrier)
+        tc::bar_sync(1 + grp, 128);
+#endif
+        tc::fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int s8 = 0; s8 < (VECINFER_TC_EXP == 4 ? 0 : 8); ++s8)   // (4: timing experiment, no MMA)
+            tc::mma_f16_ts(t_d, t_a + 8 * s8, tc::smem_desc_kmajor(b_s + 512 * s8, 256, 128), kIdesc, s8 > 0 ? 1u : 0u);
+          tc::commit(mbar);
+        }
+      } else {
+#if VECINFER_TC_EXP != 3
+        tc::bar_arrive(1 + grp, 128);
+#endif
+      }
+    };
+    KRowT<KB> kn1 = kfirst1;   // K row of the warp's next tile
+    TileCodes<KB, VB> cur = nxt;   // V codes of the current tile
+    if (n_g > 0) issue_scores(kfirst0, warp);
+    for (int n = 0; n < n_g; ++n) {
+      const int it = warp + kNW * n;
+      const int rem_cur = ntok - 32 * it;
+      KRowT<KB> kn2;
+      if (it + 2 * kNW < ntile) load_krow(kn2, it + 2 * kNW);   // K row of tile n + 2 (MMA(n + 2))
+      tc::mbar_wait(mbar, tc_phase & 1u);
+      ++tc_phase;
+      tc::fence_after();
+      float sc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+      if (it < ntile && VECINFER_TC_EXP != 5) {   // (5: timing experiment, no TMEM load)
+        float d0[4], d1[4];
+        tc::ld_16x256b(t_d + lane_sh, d0);                // tokens r, r + 8 (cols 2j, 2j+1 = head j hi, lo)
+        tc::ld_16x256b(t_d + lane_sh + (16u << 16), d1);  // tokens 16 + r, 16 + r + 8
+        tc::wait_ld();
+        sc[0][0] = d0[0] + d0[1];
+        sc[0][1] = d0[2] + d0[3];
+        sc[1][0] = d1[0] + d1[1];
+        sc[1][1] = d1[2] + d1[3];
+      }
+      if (n + 1 < n_g) issue_scores(kn1, it + kNW);
+      if (it + kNW < ntile) load_vtile(nxt, it + kNW);   // V codes of tile n + 1
+      if (it < ntile) {
+        if constexpr (kCanAppend) {
+          if (it == patch_tile) {   // the appended row's V codes
+            VCode<VB> nv;
+            if constexpr (VB == 8) nv = *reinterpret_cast<const uint32_t*>(newcodes + 64 + 4 * r);
+            else nv = *reinterpret_cast<const uint16_t*>(newcodes + 64 + Fmt<(VB <= 8 ? VB : 8)>::kOffV * r);
+            const int qp = patch_row >> 4, rr = patch_row & 15;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              if (q != qp) continue;
+              if (2 * j == rr) cur.v[q][0] = nv;
+              if (2 * j + 1 == rr) cur.v[q][1] = nv;
+              if (2 * j + 8 == rr) cur.v[q][2] = nv;
+              if (2 * j + 9 == rr) cur.v[q][3] = nv;
+            }
+          }
+        }
+        softmax_pv(sc, cur, rem_cur);
+      }
+      kn1 = kn2;
+      cur = nxt;
+    }
+  }
   // ---- warp partials -> shared memory, rescaled to the CTA-wide running max of each head: every
   // warp posts m_run, reads the 16 maxima back and stores f*acc, f*l with f = 2^(m_run - M), so the
   // combine (cta_finish<PRESCALED>, or the cluster path with f = 1) is a max over wm plus a plain
@@ -549,6 +777,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   }
   phase_mark(a.phase, cta_id, 4);
   }  // item loop
+  if constexpr (TC) {   // every issued MMA was waited for; all TMEM reads are done after this barrier
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::dealloc(tc_misc[0], kTmemCols);
+  }
 }
 
 }  // namespace
@@ -564,20 +797,29 @@ static int smem_for(int kf, int vf) { return (!has_table(kf) && !has_table(vf)) 
   X(kFmtD8B8, kFmtD8B8) X(kFmtD8B12, kFmtD8B12) X(kFmtD4B10, kFmtD4B10)           \
   X(kFmtD2B8, kFmtD2B8) X(kFmtD4B10, kFmtD8B12) X(kFmtD8B12, kFmtD8B8)
 
+// tcgen05 score path (VECINFER_ATTN_DEQUANT_TC; the host validated the formats: d = 4 shared-table K
+// codebooks, D = 128, contiguous caches)
+static AttnKernel kernel_tc(int kf, int vf) {
+  static const AttnKernel table[2][3] = {
+      {attn_mma_kernel<4, 4, 128, true>, attn_mma_kernel<4, 8, 128, true>, attn_mma_kernel<4, 16, 128, true>},
+      {attn_mma_kernel<8, 4, 128, true>, attn_mma_kernel<8, 8, 128, true>, attn_mma_kernel<8, 16, 128, true>}};
+  return table[kf == 8 ? 1 : 0][vf == 4 ? 0 : vf == 8 ? 1 : 2];
+}
+
 static AttnKernel kernel_for(int kf, int vf, int dh = 128) {
 #define VECINFER_PAIR(K, V) \
-  if (kf == K && vf == V) return dh == 128 ? attn_mma_kernel<K, V, 128> : nullptr;
+  if (kf == K && vf == V) return dh == 128 ? attn_mma_kernel<K, V, 128, false> : nullptr;
   VECINFER_NEXT2_PAIRS(VECINFER_PAIR)
 #undef VECINFER_PAIR
   const int ki = kf == 4 ? 0 : kf == 8 ? 1 : kf == 16 ? 2 : -1, vi = vf == 4 ? 0 : vf == 8 ? 1 : vf == 16 ? 2 : -1;
   if (ki < 0 || vi < 0) return nullptr;
   static const AttnKernel table[2][3][3] = {
-      {{attn_mma_kernel<4, 4, 128>, attn_mma_kernel<4, 8, 128>, attn_mma_kernel<4, 16, 128>},
-       {attn_mma_kernel<8, 4, 128>, attn_mma_kernel<8, 8, 128>, attn_mma_kernel<8, 16, 128>},
-       {attn_mma_kernel<16, 4, 128>, attn_mma_kernel<16, 8, 128>, attn_mma_kernel<16, 16, 128>}},
-      {{attn_mma_kernel<4, 4, 64>, attn_mma_kernel<4, 8, 64>, attn_mma_kernel<4, 16, 64>},
-       {attn_mma_kernel<8, 4, 64>, attn_mma_kernel<8, 8, 64>, attn_mma_kernel<8, 16, 64>},
-       {attn_mma_kernel<16, 4, 64>, attn_mma_kernel<16, 8, 64>, attn_mma_kernel<16, 16, 64>}}};
+      {{attn_mma_kernel<4, 4, 128, false>, attn_mma_kernel<4, 8, 128, false>, attn_mma_kernel<4, 16, 128, false>},
+       {attn_mma_kernel<8, 4, 128, false>, attn_mma_kernel<8, 8, 128, false>, attn_mma_kernel<8, 16, 128, false>},
+       {attn_mma_kernel<16, 4, 128, false>, attn_mma_kernel<16, 8, 128, false>, attn_mma_kernel<16, 16, 128, false>}},
+      {{attn_mma_kernel<4, 4, 64, false>, attn_mma_kernel<4, 8, 64, false>, attn_mma_kernel<4, 16, 64, false>},
+       {attn_mma_kernel<8, 4, 64, false>, attn_mma_kernel<8, 8, 64, false>, attn_mma_kernel<8, 16, 64, false>},
+       {attn_mma_kernel<16, 4, 64, false>, attn_mma_kernel<16, 8, 64, false>, attn_mma_kernel<16, 16, 64, false>}}};
   return table[dh == 64 ? 1 : 0][ki][vi];
 }
 
@@ -592,6 +834,8 @@ static void set_attrs_once() {
     for (int dh : {128, 64})
       for (int kb : {4, 8, 16})
         for (int vb : {4, 8, 16}) set_attr(kernel_for(kb, vb, dh), smem_for(kb, vb));
+    for (int kb : {4, 8})
+      for (int vb : {4, 8, 16}) set_attr(kernel_tc(kb, vb), smem_for(kb, vb));
 #define VECINFER_PAIR(K, V) set_attr(kernel_for(K, V), smem_for(K, V));
     VECINFER_NEXT2_PAIRS(VECINFER_PAIR)
 #undef VECINFER_PAIR
@@ -654,7 +898,8 @@ cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_
   }
   cfg.attrs = at;
   cfg.numAttrs = n;
-  return cudaLaunchKernelEx(&cfg, kernel_for(kbits, vbits, a.D), a);
+  const AttnKernel k = a.tc ? kernel_tc(kbits, vbits) : kernel_for(kbits, vbits, a.D);
+  return cudaLaunchKernelEx(&cfg, k, a);
 }
 
 }  // namespace vecinfer

@@ -19,7 +19,7 @@ from ._lib import VQ, I64x2, I64x3, Paged, Residual, check
 _lib.load()   # fail loudly at import if the native library is missing
 
 BF16, F32 = 0, 1
-ALGOS = {"auto": 0, "mma": 1, "dequant_mma": 1, "lut": 2, "stream": 3, "dequant_mma_stream": 3}
+ALGOS = {"auto": 0, "mma": 1, "dequant_mma": 1, "lut": 2, "stream": 3, "dequant_mma_stream": 3, "tc": 4, "dequant_tc": 4}
 
 
 @dataclass(frozen=True)
