@@ -24,8 +24,9 @@
  *    widths independent; GQA group G = H_q / H_kv in 1..8; contiguous or paged code caches.
  *    D = 64 runs the split attention kernel only (no residual window, no fused append).
  *    The paper's other configurations, D = 128 only:
- *    d8b8 {128, 8, 8}, d8b12 {128, 8, 12}, d4b10 {128, 4, 10}, d2b8 {128, 2, 8}; attention pairs
- *    (f, f) and the mixed K-d4b10 / V-d8b12 and K-d8b12 / V-d8b8 of Table 3, on the split
+ *    d8b8 {128, 8, 8}, d8b12 {128, 8, 12}, d4b10 {128, 4, 10}, d2b8 {128, 2, 8}, d8b16
+ *    {128, 8, 16} (Table 5's 2-bit row: 65 536 eight-dim centroids, 1 MiB bf16 per book);
+ *    attention pairs (f, f) and the mixed K-d4b10 / V-d8b12 and K-d8b12 / V-d8b8 of Table 3, on the split
  *    DEQUANT_MMA kernel (contiguous or paged, residual window allowed; no stream / LUT variant,
  *    decode_step appends with a separate encode launch).
  *    Anything else returns VECINFER_ERR_UNSUPPORTED.

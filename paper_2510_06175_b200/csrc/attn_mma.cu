@@ -57,8 +57,19 @@ constexpr int kSmemBytes = 65536 + kTab + kCbufBytes + 1024;  // pad + table + c
 // 16-bit K and V: no shared table -> only misc + cluster buffer, leaving the L1 to the global
 // codebook gathers
 constexpr int kSmemBytesNoTab = kMiscBytes + 1024 + kCbufBytes + 1024;
-template <int KB, int VB>
-constexpr int smem_bytes() { return (!Fmt<KB>::kSmem && !Fmt<VB>::kSmem) ? kSmemBytesNoTab : kSmemBytes; }   // (== smem_for)
+constexpr int kSepTab = 65536;   // one separate (NEXT-2) table per stream that needs it
+// shared-memory layout of a format pair: misc at 0; the classic [K | V] 256-row table (4/8-bit
+// d = 4, d8b8, d2b8) at the next 64 KiB boundary; separate d8b12 / d4b10 tables (K, then V) after
+// it (or after misc when there is no classic table); the cluster-merge buffer last
+constexpr bool classic_tab(int f) { return f == 4 || f == 8 || f == kFmtD8B8 || f == kFmtD2B8; }
+constexpr bool sep_tab(int f) { return f == kFmtD8B12 || f == kFmtD4B10; }
+constexpr int smem_layout_bytes(int kf, int vf) {
+  const int nsep = (sep_tab(kf) ? 1 : 0) + (sep_tab(vf) ? 1 : 0);
+  if (classic_tab(kf) || classic_tab(vf)) return kSmemBytes + nsep * kSepTab;
+  if (nsep) return ((kMiscBytes + 1023) & ~1023) + nsep * kSepTab + kCbufBytes + 1024;
+  return kSmemBytesNoTab;
+}
+static_assert(smem_layout_bytes(kFmtD8B12, kFmtD8B8) <= 232448, "largest layout exceeds 227 KiB");
 
 
 // K code row of one token for the tcgen05 score path (lane = token): 32 sub-vector codes
@@ -98,9 +109,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   // shared layout: misc at the bottom, the codebook table at the next 64 KiB boundary
   const uint32_t raw_s = smem_u32(smem_raw);
+  constexpr bool kClassic = classic_tab(KB) || classic_tab(VB);
+  constexpr bool kSepK = Fmt<KB>::kSep, kSepV = Fmt<VB>::kSep;
   uint32_t tab_off;
-  if constexpr (!Fmt<KB>::kSmem && !Fmt<VB>::kSmem) {
-    tab_off = (kMiscBytes + 1023) & ~1023;   // no table: the "table" base only anchors the cluster buffer
+  if constexpr (!kClassic) {
+    tab_off = (kMiscBytes + 1023) & ~1023;   // no classic table: separate tables / cluster buffer start here
   } else {
     tab_off = ((raw_s + 65535u) & ~65535u) - raw_s;
     if (tab_off < static_cast<uint32_t>(kMiscBytes)) tab_off += 65536u;
@@ -108,6 +121,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   unsigned char* tab = smem_raw + tab_off;
   float* sq = reinterpret_cast<float*>(smem_raw + kMiscQ);
   const uint32_t tab_s = raw_s + tab_off;
+  constexpr uint32_t kSepOff = kClassic ? kTab : 0;               // relative to tab
+  constexpr uint32_t kSepVOff = kSepOff + (kSepK ? kSepTab : 0);
+  constexpr uint32_t kCbufOff = kSepVOff + (kSepV ? kSepTab : 0);
 
   // Work items = (split s, KV head h, batch b), s fastest.  Grids of up to one wave map one item
   // to each CTA; larger problems run persistent CTAs (one per SM) over items, so the per-CTA
@@ -222,6 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
   }
   table_store<KB, VB>(tab, tabv, tid);
+  sep_fill<KB>(tab + kSepOff, cbk, tid, kThreads);     // NEXT-2 d8b12 / d4b10 books (no-ops otherwise)
+  sep_fill<VB>(tab + kSepVOff, cbv, tid, kThreads);
   unsigned char* newcodes = smem_raw + kMiscNew;   // [0,64): K code row, [64,128): V code row
   if (kCanAppend && owner) {
     // Eq. 9: encode the new token (S then H on the key, VQ on both), 8 warps per stream, each
@@ -347,8 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
   }
 
-  const uint32_t kbase = tab_s + table_lane_off<KB>(lane);
-  const uint32_t vbase = tab_s + 128 + table_lane_off<VB>(lane);
+  const uint32_t kbase = (kSepK ? tab_s + kSepOff : tab_s) + table_lane_off<KB>(lane);
+  const uint32_t vbase = (kSepV ? tab_s + kSepVOff : tab_s + 128) + table_lane_off<VB>(lane);
 
   float acc[2 * VS][4];
 #pragma unroll
@@ -745,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
     cluster_wait();   // every CTA of the cluster has started: DSMEM of the leader is valid
     const uint32_t rank = cluster_ctarank();
-    float* cbuf = reinterpret_cast<float*>(tab + ((!Fmt<KB>::kSmem && !Fmt<VB>::kSmem) ? 0 : kTab));   // [16][4][128] acc, [16][4] M, l
+    float* cbuf = reinterpret_cast<float*>(tab + kCbufOff);   // [16][4][128] acc, [16][4] M, l
     float* cM = cbuf + kClusterMax * 4 * 128;
     float* cL = cM + kClusterMax * 4;
     const uint32_t cb_s = smem_u32(cbuf);
@@ -788,14 +806,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
 using AttnKernel = void (*)(const AttnArgs);
 
-static bool has_table(int f) { return f == 4 || f == 8 || f == kFmtD8B8 || f == kFmtD2B8; }
-static int smem_for(int kf, int vf) { return (!has_table(kf) && !has_table(vf)) ? kSmemBytesNoTab : kSmemBytes; }
+static int smem_for(int kf, int vf) { return smem_layout_bytes(kf, vf); }
 
 // the NEXT-2 (K, V) format pairs with a kernel: each format with itself and the paper's mixed
 // configurations K-d4b10 / V-d8b12 (2-bit) and K-d8b12 / V-d8b8 (1.25-bit), Table 3 / P:993-999
 #define VECINFER_NEXT2_PAIRS(X)                                                   \
   X(kFmtD8B8, kFmtD8B8) X(kFmtD8B12, kFmtD8B12) X(kFmtD4B10, kFmtD4B10)           \
-  X(kFmtD2B8, kFmtD2B8) X(kFmtD4B10, kFmtD8B12) X(kFmtD8B12, kFmtD8B8)
+  X(kFmtD2B8, kFmtD2B8) X(kFmtD4B10, kFmtD8B12) X(kFmtD8B12, kFmtD8B8) X(kFmtD8B16, kFmtD8B16)
 
 // tcgen05 score path (VECINFER_ATTN_DEQUANT_TC; the host validated the formats: d = 4 shared-table K
 // codebooks, D = 128, contiguous caches)

@@ -24,9 +24,11 @@ __device__ __forceinline__ uint2 bf16x4_to_f16x4(uint2 w) {
 // shared table (rows of 256 B: [16 K replicas | 16 V replicas]); 16-bit codebooks (65536 x 4 bf16 =
 // 512 KiB) do not fit shared memory and are gathered from global memory (L2/L1 resident).
 template <int BITS> struct Fmt;
+// kSep: the format has its own shared table (1024 / 4096-entry NEXT-2 books) instead of a half
+// of the classic 256-row [K | V] table
 template <> struct Fmt<8> {
   static constexpr int kRow = 32, kOffK = 8, kOffV = 4;
-  static constexpr bool kSmem = true, kGeneric = false, kWide = false;
+  static constexpr bool kSmem = true, kGeneric = false, kWide = false, kSep = false;
   static __device__ __forceinline__ uint32_t lane_off(int lane) { return (lane & 15) * 8; }   // copy lane % 16
   using K = uint2;
   using V = uint32_t;
@@ -43,7 +45,7 @@ template <> struct Fmt<8> {
 };
 template <> struct Fmt<4> {
   static constexpr int kRow = 16, kOffK = 4, kOffV = 2;
-  static constexpr bool kSmem = true, kGeneric = false, kWide = false;
+  static constexpr bool kSmem = true, kGeneric = false, kWide = false, kSep = false;
   static __device__ __forceinline__ uint32_t lane_off(int lane) { return (lane & 15) * 8; }
   using K = uint32_t;
   using V = uint32_t;   // low 16 bits
@@ -58,7 +60,7 @@ template <> struct Fmt<4> {
 };
 template <> struct Fmt<16> {
   static constexpr int kRow = 64, kOffK = 16, kOffV = 8;
-  static constexpr bool kSmem = false, kGeneric = false, kWide = false;
+  static constexpr bool kSmem = false, kGeneric = false, kWide = false, kSep = false;
   using K = uint4;
   using V = uint2;
   static __device__ __forceinline__ K ldk(const uint8_t* p) { return ldg_nc_u128(p); }
@@ -111,7 +113,7 @@ struct FmtG {
   static constexpr int kRow = 128 / SUB * BITS / 8;        // bytes per cached row
   static constexpr int kOffK = 32 / SUB * BITS / 8;        // K chunk bytes (= lane stride)
   static constexpr int kOffV = 16 / SUB * BITS / 8;        // V chunk bytes
-  static constexpr bool kSmem = false, kGeneric = true, kWide = false;
+  static constexpr bool kSmem = false, kGeneric = true, kWide = false, kSep = false;
   static_assert(kOffV * 8 == 16 / SUB * BITS, "V chunk must be whole bytes");
   static constexpr int kRowAl = (kRow % 16 == 0) ? 16 : (kRow % 8 == 0) ? 8 : 4;
   static constexpr int gcd(int x, int y) { return y == 0 ? x : gcd(y, x % y); }
@@ -145,9 +147,36 @@ struct FmtG {
     }
   }
 };
-constexpr int kFmtD8B8 = 808, kFmtD8B12 = 812, kFmtD4B10 = 410, kFmtD2B8 = 208;
-template <> struct Fmt<kFmtD8B12> : FmtG<8, 12> {};
-template <> struct Fmt<kFmtD4B10> : FmtG<4, 10> {};
+constexpr int kFmtD8B8 = 808, kFmtD8B12 = 812, kFmtD4B10 = 410, kFmtD2B8 = 208, kFmtD8B16 = 816;
+// d8b12 and d4b10 read their books from their own shared tables (one per stream, 64 KiB each), not
+// through L1: d8b12 = 4096 x 16-byte fp16 centroids, unreplicated, one LDS.128 per code = two
+// virtual sub-vectors ("wide", as d8b8); d4b10 = 1024 x 8-byte centroids in 8 replicas (rows of
+// 64 B, lane l reads replica l % 8).  kSepShift = log2 row pitch, kSepReps = replicas.
+template <> struct Fmt<kFmtD8B12> : FmtG<8, 12> {
+  static constexpr bool kSmem = true, kGeneric = false, kWide = true, kSep = true;
+  static constexpr int kSepShift = 4, kSepReps = 1, kSepEnt = 4096, kSepCent = 16;
+  static __device__ __forceinline__ uint32_t sep_lane_off(int) { return 0u; }
+  template <int I> static __device__ __forceinline__ uint32_t kaddr(const K& c, uint32_t base) {
+    return base + (code<I>(c.w) << 4);
+  }
+  template <int I> static __device__ __forceinline__ uint32_t vaddr(const V& c, uint32_t base) {
+    return base + (code<I>(c.w) << 4);
+  }
+};
+template <> struct Fmt<kFmtD4B10> : FmtG<4, 10> {
+  static constexpr bool kSmem = true, kGeneric = false, kWide = false, kSep = true;
+  static constexpr int kSepShift = 6, kSepReps = 8, kSepEnt = 1024, kSepCent = 8;
+  static __device__ __forceinline__ uint32_t sep_lane_off(int lane) { return (lane & 7) * 8; }
+  template <int T> static __device__ __forceinline__ uint32_t kaddr(const K& c, uint32_t base) {
+    return base + (code<T>(c.w) << 6);
+  }
+  template <int U> static __device__ __forceinline__ uint32_t vaddr(const V& c, uint32_t base) {
+    return base + (code<U>(c.w) << 6);
+  }
+};
+// d8b16 (Table 5's 2-bit row): 65 536 eight-dim centroids = 1 MiB bf16 per book, far
+// beyond shared memory, gathered through L1/L2 like b4d4 (larger books cost efficiency)
+template <> struct Fmt<kFmtD8B16> : FmtG<8, 16> {};
 // 256-entry books live in the shared table like b2d4 (code byte -> address bits 8..15, rows of
 // 256 B = [K half | V half]).  d8b8: the 16-byte centroid in 8 copies per half (lane l reads copy
 // l % 8: one LDS.128 per quarter-warp phase hits 8 distinct 16-byte bank groups) and one 16-byte
@@ -155,7 +184,7 @@ template <> struct Fmt<kFmtD4B10> : FmtG<4, 10> {};
 // (one LDS.32 per lane, all 32 banks); a virtual sub-vector is two gathers.
 template <> struct Fmt<kFmtD8B8> {
   static constexpr int kRow = 16, kOffK = 4, kOffV = 2;   // K chunk: codes 4j..4j+3, V: 2r, 2r+1
-  static constexpr bool kSmem = true, kGeneric = false, kWide = true;
+  static constexpr bool kSmem = true, kGeneric = false, kWide = true, kSep = false;
   static __device__ __forceinline__ uint32_t lane_off(int lane) { return (lane & 7) * 16; }
   using K = uint32_t;
   using V = uint32_t;   // low 16 bits
@@ -171,7 +200,7 @@ template <> struct Fmt<kFmtD8B8> {
 };
 template <> struct Fmt<kFmtD2B8> {
   static constexpr int kRow = 64, kOffK = 16, kOffV = 8;  // K chunk: codes 16j..16j+15, V: 8r..8r+7
-  static constexpr bool kSmem = true, kGeneric = false, kWide = false;
+  static constexpr bool kSmem = true, kGeneric = false, kWide = false, kSep = false;
   static __device__ __forceinline__ uint32_t lane_off(int lane) { return lane * 4; }
   using K = uint4;
   using V = uint2;
@@ -257,8 +286,31 @@ __device__ __forceinline__ uint4 table_pattern(const uint16_t* cb, int j) {
 
 template <int F>
 __device__ __forceinline__ uint32_t table_lane_off(int lane) {
-  if constexpr (Fmt<F>::kSmem) return Fmt<F>::lane_off(lane);
+  if constexpr (Fmt<F>::kSep) return Fmt<F>::sep_lane_off(lane);
+  else if constexpr (Fmt<F>::kSmem) return Fmt<F>::lane_off(lane);
   else return 0u;
+}
+
+// fill of a separate (NEXT-2) table: centroid j (bf16, kSepCent / 2 dims) -> fp16 at row j, in
+// kSepReps replicas; 16-byte stores, all threads of the CTA
+template <int F>
+__device__ __forceinline__ void sep_fill(unsigned char* tab, const uint16_t* cb, int tid, int nthreads) {
+  if constexpr (Fmt<F>::kSep) {
+    constexpr int kEnt = Fmt<F>::kSepEnt, kReps = Fmt<F>::kSepReps, kPitch = 1 << Fmt<F>::kSepShift;
+    if constexpr (Fmt<F>::kSepCent == 16) {
+      for (int j = tid; j < kEnt; j += nthreads) {
+        const uint2 lo = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(cb + 8 * j));
+        const uint2 hi = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(cb + 8 * j + 4));
+        *reinterpret_cast<uint4*>(tab + j * kPitch) = make_uint4(lo.x, lo.y, hi.x, hi.y);
+      }
+    } else {   // 8-byte centroids, kReps replicas = kReps / 2 stores of the centroid pair
+      for (int i = tid; i < kEnt * (kReps / 2); i += nthreads) {
+        const int j = i / (kReps / 2), u = i % (kReps / 2);
+        const uint2 e = bf16x4_to_f16x4(*reinterpret_cast<const uint2*>(cb + 4 * j));
+        *reinterpret_cast<uint4*>(tab + j * kPitch + 16 * u) = make_uint4(e.x, e.y, e.x, e.y);
+      }
+    }
+  }
 }
 
 // codebook table fill in two halves, so the codebook loads can be issued first and the shared

@@ -402,7 +402,7 @@ bool vq_d4(const vecinfer_vq_t& c) {
          (c.code_bits == 4 || c.code_bits == 8 || c.code_bits == 16);
 }
 bool vq_next2(const vecinfer_vq_t& c) {
-  return c.head_dim == 128 && ((c.sub_dim == 8 && (c.code_bits == 8 || c.code_bits == 12)) ||
+  return c.head_dim == 128 && ((c.sub_dim == 8 && (c.code_bits == 8 || c.code_bits == 12 || c.code_bits == 16)) ||
                                (c.sub_dim == 4 && c.code_bits == 10) || (c.sub_dim == 2 && c.code_bits == 8));
 }
 bool vq_supported(const vecinfer_vq_t& c) { return vq_d4(c) || vq_next2(c); }

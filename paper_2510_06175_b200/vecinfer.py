@@ -49,6 +49,7 @@ B1D4, B2D4, B4D4 = VQConfig(128, 4, 4), VQConfig(128, 4, 8), VQConfig(128, 4, 16
 # the paper's other configurations, D = 128,
 # split kernel: each with itself, plus K-d4b10 / V-d8b12 (2-bit) and K-d8b12 / V-d8b8 (1.25-bit)
 D8B8, D8B12, D4B10, D2B8 = VQConfig(128, 8, 8), VQConfig(128, 8, 12), VQConfig(128, 4, 10), VQConfig(128, 2, 8)
+D8B16 = VQConfig(128, 8, 16)   # Table 5's 2-bit row: 65 536 eight-dim centroids
 
 
 def _stream(dev: torch.device):

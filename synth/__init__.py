@@ -137,6 +137,19 @@ def product_grid_codebook(n_levels: int, sub_dim: int = 4, step: float = 0.5) ->
     return cb
 
 
+def product_codebook(levels: np.ndarray) -> np.ndarray:
+    """Product codebook from per-dimension levels [d, n]: entry j has coordinate t = levels[t][digit_t(j)],
+    digit_t(j) = (j // n**t) % n (dimension 0 is the least significant digit).  Index expansion only
+    (used to build the frozen 65 536-entry d8b16 books from their 8 x 4 stored levels)."""
+    levels = np.asarray(levels, dtype=np.float32)
+    d, n = levels.shape
+    idx = np.arange(n ** d)
+    cb = np.empty((n ** d, d), dtype=np.float32)
+    for t in range(d):
+        cb[:, t] = levels[t][(idx // n ** t) % n]
+    return cb
+
+
 def dyadic_points(n: int, sub_dim: int, n_levels: int, step: float, seed: int, denom: int = 8) -> np.ndarray:
     """Random dyadic points covering the grid range, including exact level midpoints (genuine ties)."""
     rng = np.random.default_rng(seed)

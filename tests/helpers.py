@@ -8,6 +8,7 @@ import synth
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CODEBOOKS = os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz")
 CODEBOOKS_NEXT2 = os.path.join(ROOT, "data", "next2_codebooks.npz")   # d8b8, d8b12, d4b10, d2b8
+LEVELS_D8B16 = os.path.join(ROOT, "data", "d8b16_levels.npz")          # 8 x 4 levels -> 65 536 x 8 book
 
 # north_star: outputs within 2e-3 max-abs relative error (bf16 I/O, fp32 accumulation);
 # measured per (b, h_q) row on the fp32 output (reading R13)
@@ -27,6 +28,10 @@ def load_codebooks():
         for k in z.files:
             if k.startswith("ck_") or k.startswith("cv_"):
                 out[k] = synth.bf16_from_bits(z[k])
+    if os.path.exists(LEVELS_D8B16):   # d8b16: shared product books from their stored levels
+        z = np.load(LEVELS_D8B16)
+        out["ck_d8b16"] = synth.product_codebook(synth.bf16_from_bits(z["lv_d8b16_k"]))
+        out["cv_d8b16"] = synth.product_codebook(synth.bf16_from_bits(z["lv_d8b16_v"]))
     return out
 
 

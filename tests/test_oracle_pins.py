@@ -433,7 +433,7 @@ def test_pack_byte_widths_are_the_bitstream(bits):
     assert np.array_equal(ref.unpack_bitstream(ref.pack_codes(codes, bits), bits), codes)
 
 
-@pytest.mark.parametrize("sub_dim,bits", [(4, 10), (8, 12), (8, 8), (2, 8)])
+@pytest.mark.parametrize("sub_dim,bits", [(4, 10), (8, 12), (8, 8), (2, 8), (8, 16)])
 def test_pack_roundtrip_next2_formats(sub_dim, bits):
     """d4b10 / d8b12 / d8b8 / d2b8 rows: M = 128/d codes, M*b/8 bytes
     (P:143), lossless."""
@@ -446,10 +446,11 @@ def test_pack_roundtrip_next2_formats(sub_dim, bits):
     assert np.all(ref.pack_codes(extremes, bits) == 0xFF) and np.all(ref.pack_codes(0 * extremes, bits) == 0)
 
 
-@pytest.mark.parametrize("sub_dim,n_levels", [(8, 2), (2, 16), (8, 3)])
+@pytest.mark.parametrize("sub_dim,n_levels", [(8, 2), (2, 16), (8, 3), (8, 4)])
 def test_encode_product_grid_other_sub_dims(sub_dim, n_levels):
-    """Eq. 2 with d = 8 (2^8 and 3^8 = 6561 entries) and d = 2 (16^2): the separable closed form
-    of test_encode_product_grid_closed_form at the other sub-vector sizes."""
+    """Eq. 2 with d = 8 (2^8, 3^8 = 6561 and 4^8 = 65 536 entries: the d8b16 size) and
+    d = 2 (16^2): the separable closed form of test_encode_product_grid_closed_form at the other
+    sub-vector sizes."""
     cb = synth.product_grid_codebook(n_levels, sub_dim, step=0.5)
     n = 400
     X = synth.dyadic_points(n, sub_dim, n_levels, 0.5, seed=sub_dim * 7 + n_levels)
@@ -461,7 +462,7 @@ def test_encode_product_grid_other_sub_dims(sub_dim, n_levels):
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("dk,nk,dv,nv", [(8, 4096, 8, 256), (4, 1024, 2, 256)])
+@pytest.mark.parametrize("dk,nk,dv,nv", [(8, 4096, 8, 256), (4, 1024, 2, 256), (8, 65536, 8, 65536)])
 def test_vq_attention_identity_other_formats(dk, nk, dv, nv):
     """The exhaustive-codebook identity pin at K-d8b12 / V-d8b8 and K-d4b10 / V-d2b8 (Table 3
     mixed configurations): Eq. 10 over codes = Eq. 1 over the reconstructed keys."""
