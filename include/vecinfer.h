@@ -101,7 +101,8 @@ typedef enum {
  * two >= 32; n_cap (the per-sequence capacity) must not exceed bt_stride * page_size.  Entries
  * outside [0, n_pages) are flagged as VECINFER_FLAG_WRITE_POS by the encoders and must not be
  * reached by attended tokens.  Token ranges must start at a multiple of 32.  The *_paged entry
- * points run the split attention kernel (the stream kernel and the LUT variant are contiguous-only).
+ * points run the split or the stream attention kernel (the LUT and DEQUANT_TC variants are
+ * contiguous-only).
  *   block_table  device int32 [B, bt_stride] (caller owned).                                   */
 typedef struct {
   const int32_t* block_table;
@@ -271,7 +272,9 @@ vecinfer_status_t vecinfer_attn_decode(const void* q_bf16, int32_t B, int32_t H_
                                        vecinfer_dtype_t o_dtype, float* lse, void* workspace,
                                        size_t workspace_bytes, vecinfer_stream_t stream,
                                        const vecinfer_residual_t* residual);
-/* vecinfer_attn_decode over a paged code cache (split kernel; tok_begin % 32 == 0). */
+/* vecinfer_attn_decode over a paged code cache (tok_begin % 32 == 0).  The split kernel and, for
+ * batch decode (AUTO's choice or DEQUANT_MMA_STREAM), the stream kernel: every 16-token sub-tile
+ * is translated through the block table; results equal the contiguous cache bit for bit. */
 vecinfer_status_t vecinfer_attn_decode_paged(const void* q_bf16, int32_t B, int32_t H_q,
                                              int32_t H_kv, int64_t q_stride_b, int64_t q_stride_h,
                                              const float* lambda, const void* ck_bf16,

@@ -260,14 +260,13 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: misaligned lambda/codebooks/codes");
   const int64_t range = tok_end >= 0 ? (tok_end - tok_begin < n_cap ? tok_end - tok_begin : n_cap) : n_cap;
   const bool lut = algo == VECINFER_ATTN_LUT;
-  if (pg) {   // paged code cache: split kernel only, 32-aligned token ranges
+  if (pg) {   // paged code cache: split or stream kernel, 32-aligned token ranges
     const vecinfer_status_t v = check_paged(pg, n_cap, "attn_decode_paged");
     if (v != VECINFER_OK) return v;
-    if (lut || algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
-      return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_paged: paged caches run the split DEQUANT_MMA kernel only");
+    if (lut) return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_paged: paged caches run the DEQUANT_MMA kernels only");
     if (tok_begin % 32 != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode_paged: tok_begin must be a multiple of 32");
   }
-  const bool use_sk = !tc && !pg && !next2 && D == 128 && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
+  const bool use_sk = !tc && !next2 && D == 128 && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
   SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
   if (D == 64) plan.cluster = 0;   // the DSMEM cluster merge is written for 128-dim rows
   const int32_t S = plan.S;
@@ -414,7 +413,7 @@ static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t k
   const int64_t units = static_cast<int64_t>(B) * H_kv;
   if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
     return num_splits == 0 || units * num_splits <= device_sm_count();   // persistent grids: separate append
-  if (!paged && algo != VECINFER_ATTN_DEQUANT_TC && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
+  if (algo != VECINFER_ATTN_DEQUANT_TC && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
   const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
   const int mac = plan.cluster ? attn_mma_max_active_clusters(plan.S) : 0;
   const int64_t waves = plan.cluster ? (units + (mac > 0 ? mac : 1) - 1) / (mac > 0 ? mac : 1)

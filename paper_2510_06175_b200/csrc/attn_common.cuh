@@ -207,7 +207,20 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     const int g = idx / DH, dim = idx % DH;
     float M = -INFINITY;
     float osum = 0.f, lsum = 0.f;
-    if constexpr (PRESCALED) {
+    if constexpr (PRESCALED && NWARPS == 16) {
+      // head g is warp-uniform (DH is a multiple of 32): lanes l and l + 16 read warp l % 16's
+      // (max, l) once, a 16-lane butterfly gives the CTA max and the l sum to every lane
+      const int lane = tid & 31;
+      M = wm[(lane & 15) * 4 + g];
+      lsum = wl[(lane & 15) * 4 + g];
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) {
+        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+      }
+#pragma unroll
+      for (int w = 0; w < NWARPS; ++w) osum += wacc[(w * 4 + g) * WROW + dim];
+    } else if constexpr (PRESCALED) {
 #pragma unroll
       for (int w = 0; w < NWARPS; ++w) {
         M = fmaxf(M, wm[w * 4 + g]);

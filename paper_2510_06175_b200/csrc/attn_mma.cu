@@ -724,9 +724,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   float* wacc = wl + kNW * 4;
   if (r == 0) wm[warp * 4 + j] = m_run;
   __syncthreads();
-  float Mh = -INFINITY;
-#pragma unroll
-  for (int w = 0; w < kNW; ++w) Mh = fmaxf(Mh, wm[w * 4 + j]);
+  // CTA max of head j: lanes (r, j) read warps r and r + 8, then a max over the 8 lanes of head j
+  float Mh = fmaxf(wm[r * 4 + j], wm[(r + 8) * 4 + j]);
+  Mh = fmaxf(Mh, __shfl_xor_sync(0xffffffffu, Mh, 4));
+  Mh = fmaxf(Mh, __shfl_xor_sync(0xffffffffu, Mh, 8));
+  Mh = fmaxf(Mh, __shfl_xor_sync(0xffffffffu, Mh, 16));
   const float fsc = m_run == -INFINITY ? 0.f : ex2_approx(m_run - Mh);
   if (r == 0) wl[warp * 4 + j] = l_run * fsc;   // (wm keeps the per-warp maxima: no write-after-read race)
   // thread (r, j): head j, dims (DH/8)r .. (DH/8)r + DH/8 - 1; MMA slots [t][0] + [t][1] hold dim

@@ -192,7 +192,8 @@ __device__ __noinline__ void merge_consume(const AttnArgs& a, unsigned long long
   if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
 }
 
-template <int KB, int VB>
+// PG: paged code caches (a separate instantiation: the translation must not cost the contiguous path)
+template <int KB, int VB, bool PG>
 __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_constant__ AttnArgs a) {
   constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
   constexpr bool kCanAppend = KB <= 8 && VB <= 8;
@@ -306,6 +307,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       const uint8_t* kp = nullptr;
       const uint8_t* vp = nullptr;
       TileCodes<KB, VB> nxt;
+      // paged code caches (NEXT-4): pieces start at 16-token multiples (tok_begin % 32 == 0) and
+      // pages hold >= 32 tokens, so every 16-token sub-tile lies in one page; each sub-tile is
+      // translated through the block table, whose entries are read one tile ahead
+      constexpr bool paged = PG;
+      int pgn0 = 0, pgn1 = 0;   // pages of the two sub-tiles of the next tile to load
+      auto page_of = [&](int bb, int64_t tok) -> int { return a.bt[bb * a.bt_stride + (tok >> a.page_shift)]; };
+      auto load_paged = [&](const SegSh& sg, int64_t tstart, int p0, int p1, int rem) {
+        const int64_t pmask = (int64_t(1) << a.page_shift) - 1;
+        const int64_t row0 = ((static_cast<int64_t>(p0) * a.Hc + sg.hc) << a.page_shift) + (tstart & pmask);
+        const int64_t row1 = ((static_cast<int64_t>(p1) * a.Hc + sg.hc) << a.page_shift) + ((tstart + 16) & pmask);
+        load_subtile<KB, VB, 0>(nxt, a.kcodes + (row0 + r) * KR + Fmt<KB>::kOffK * j,
+                                a.vcodes + (row0 + 2 * j) * VR + Fmt<VB>::kOffV * r, rem, r, j);
+        load_subtile<KB, VB, 1>(nxt, a.kcodes + (row1 + r) * KR + Fmt<KB>::kOffK * j,
+                                a.vcodes + (row1 + 2 * j) * VR + Fmt<VB>::kOffV * r, rem - 16, r, j);
+      };
       // sets up piece `seg` of this warp and issues its first tile loads
       auto setup_piece = [&]() {
         const SegSh& sg = segs[seg];
@@ -329,7 +345,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
             patch_row = static_cast<int>(rel & 31);
           }
         }
-        if (ntile > 0) load_tile_tail(nxt, kp, vp, ntok, r, j);   // (predicated: one code path)
+        if constexpr (paged) {
+          const int p0 = ntok > 0 ? page_of(sg.b, tok0) : 0;
+          const int p1 = ntok > 16 ? page_of(sg.b, tok0 + 16) : 0;
+          if (ntile > 0) load_paged(sg, tok0, p0, p1, ntok);
+          pgn0 = ntok > 32 ? page_of(sg.b, tok0 + 32) : 0;
+          pgn1 = ntok > 48 ? page_of(sg.b, tok0 + 48) : 0;
+        } else if (ntile > 0) {
+          load_tile_tail(nxt, kp, vp, ntok, r, j);   // (predicated: one code path)
+        }
         // residual rows of the unit: row t belongs to piece t % P, and within the piece's warps
         // (rank rho of nw) to rows t = k + P * (rho + nw * i)
         rlen = sg.rlen;
@@ -404,8 +428,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
               if (warp == 0) put_code<KB>(nc, lane, ii);
               else put_code<VB>(nc + 64, lane, ii);
               const int64_t p = sg.p_row;
-              if (p >= 0 && p < a.n_cap) {
-                const int64_t row = static_cast<int64_t>(sg.cu) * a.n_cap + p;
+              int pgw = 0;
+              if (p >= 0 && p < a.n_cap && (!paged || ((pgw = page_of(sg.b, p)) >= 0 && pgw < a.n_pages))) {
+                const int64_t row = paged ? ((static_cast<int64_t>(pgw) * a.Hc + sg.hc) << a.page_shift) +
+                                                (p & ((int64_t(1) << a.page_shift) - 1))
+                                          : static_cast<int64_t>(sg.cu) * a.n_cap + p;
                 if (warp == 0) put_code<KB>(a.kcodes_w + row * KR, lane, ii);
                 else put_code<VB>(a.vcodes_w + row * VR, lane, ii);
               } else if (lane == 0 && a.err) {
@@ -551,11 +578,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           }
           const int rem_cur = ntok - 32 * it;
           if (it + 1 < ntile) {
-            kp += 32 * KR;
-            vp += 32 * VR;
             const int rem = rem_cur - 32;
-            if (rem >= 32) load_tile_full(nxt, kp, vp);
-            else load_tile_tail(nxt, kp, vp, rem, r, j);
+            if constexpr (paged) {
+              const SegSh& sgp = segs[seg];
+              const int64_t tn = tok0 + 32 * static_cast<int64_t>(it + 1);
+              load_paged(sgp, tn, pgn0, pgn1, rem);
+              pgn0 = rem > 32 ? page_of(sgp.b, tn + 32) : 0;
+              pgn1 = rem > 48 ? page_of(sgp.b, tn + 48) : 0;
+            } else {
+              kp += 32 * KR;
+              vp += 32 * VR;
+              if (rem >= 32) load_tile_full(nxt, kp, vp);
+              else load_tile_tail(nxt, kp, vp, rem, r, j);
+            }
           }
           // tile body, specialised on whether sub-tile 1 holds tokens (a trailing half tile skips it);
           // the common full-tile instance is straight-line code the scheduler can interleave
@@ -839,21 +874,25 @@ using AttnKernel = void (*)(const AttnArgs);
 
 static int smem_for(int kb, int vb) { return (kb > 8 && vb > 8) ? kSmemBytesNoTab : kSmemBytes; }
 
-static AttnKernel kernel_for(int kb, int vb) {
+static AttnKernel kernel_for(int kb, int vb, bool paged = false) {
   const int ki = kb == 4 ? 0 : kb == 8 ? 1 : 2, vi = vb == 4 ? 0 : vb == 8 ? 1 : 2;
-  static const AttnKernel table[3][3] = {
-      {attn_stream_kernel<4, 4>, attn_stream_kernel<4, 8>, attn_stream_kernel<4, 16>},
-      {attn_stream_kernel<8, 4>, attn_stream_kernel<8, 8>, attn_stream_kernel<8, 16>},
-      {attn_stream_kernel<16, 4>, attn_stream_kernel<16, 8>, attn_stream_kernel<16, 16>}};
-  return table[ki][vi];
+  static const AttnKernel table[2][3][3] = {
+      {{attn_stream_kernel<4, 4, false>, attn_stream_kernel<4, 8, false>, attn_stream_kernel<4, 16, false>},
+       {attn_stream_kernel<8, 4, false>, attn_stream_kernel<8, 8, false>, attn_stream_kernel<8, 16, false>},
+       {attn_stream_kernel<16, 4, false>, attn_stream_kernel<16, 8, false>, attn_stream_kernel<16, 16, false>}},
+      {{attn_stream_kernel<4, 4, true>, attn_stream_kernel<4, 8, true>, attn_stream_kernel<4, 16, true>},
+       {attn_stream_kernel<8, 4, true>, attn_stream_kernel<8, 8, true>, attn_stream_kernel<8, 16, true>},
+       {attn_stream_kernel<16, 4, true>, attn_stream_kernel<16, 8, true>, attn_stream_kernel<16, 16, true>}}};
+  return table[paged ? 1 : 0][ki][vi];
 }
 
 static void set_attrs_once() {
   static bool done = false;  // benign race: idempotent attributes
   if (!done) {
-    for (int kb : {4, 8, 16})
-      for (int vb : {4, 8, 16})
-        cudaFuncSetAttribute(kernel_for(kb, vb), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(kb, vb));
+    for (int pg : {0, 1})
+      for (int kb : {4, 8, 16})
+        for (int vb : {4, 8, 16})
+          cudaFuncSetAttribute(kernel_for(kb, vb, pg), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(kb, vb));
     done = true;
   }
 }
@@ -881,7 +920,7 @@ cudaError_t launch_attn_stream(const AttnArgs& a, int kbits, int vbits, cudaStre
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel_for(kbits, vbits), a);
+  return cudaLaunchKernelEx(&cfg, kernel_for(kbits, vbits, a.bt != nullptr), a);
 }
 
 }  // namespace vecinfer

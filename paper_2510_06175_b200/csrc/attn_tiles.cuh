@@ -384,6 +384,30 @@ __device__ __forceinline__ void load_tile_tail(TileCodes<KB, VB>& tc, const uint
   }
 }
 
+// one 16-token sub-tile Q of a tile from its own row base (paged caches: the two sub-tiles of a
+// tile may lie in different pages).  kq points at this lane's K bytes of the sub-tile's row r, vq at
+// its V bytes of row 2j; rem = tokens left from the sub-tile start (rows beyond read as code 0)
+template <int KB, int VB, int Q>
+__device__ __forceinline__ void load_subtile(TileCodes<KB, VB>& tc, const uint8_t* kq, const uint8_t* vq, int rem,
+                                             int r, int j) {
+  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
+  if (rem >= 16) {   // full sub-tile: unpredicated loads
+    tc.k[Q][0] = Fmt<KB>::ldk(kq);
+    tc.k[Q][1] = Fmt<KB>::ldk(kq + 8 * KR);
+    tc.v[Q][0] = Fmt<VB>::ldv(vq);
+    tc.v[Q][1] = Fmt<VB>::ldv(vq + VR);
+    tc.v[Q][2] = Fmt<VB>::ldv(vq + 8 * VR);
+    tc.v[Q][3] = Fmt<VB>::ldv(vq + 9 * VR);
+    return;
+  }
+  tc.k[Q][0] = r < rem ? Fmt<KB>::ldk(kq) : Fmt<KB>::zk();
+  tc.k[Q][1] = r + 8 < rem ? Fmt<KB>::ldk(kq + 8 * KR) : Fmt<KB>::zk();
+  tc.v[Q][0] = 2 * j < rem ? Fmt<VB>::ldv(vq) : VCode<VB>{};
+  tc.v[Q][1] = 2 * j + 1 < rem ? Fmt<VB>::ldv(vq + VR) : VCode<VB>{};
+  tc.v[Q][2] = 2 * j + 8 < rem ? Fmt<VB>::ldv(vq + 8 * VR) : VCode<VB>{};
+  tc.v[Q][3] = 2 * j + 9 < rem ? Fmt<VB>::ldv(vq + 9 * VR) : VCode<VB>{};
+}
+
 // store the packed code of sub-vector `lane` (4/8-bit) for the fused append
 template <int BITS>
 __device__ __forceinline__ void put_code(unsigned char* row, int lane, uint32_t code) {

@@ -144,7 +144,59 @@ def test_paged_rejects_bad_descriptors():
     with pytest.raises(VecInferError):
         vi.attn_decode(*args, block_table=t_i32(bt), tok_begin=16)          # range start not 32-aligned
     with pytest.raises(VecInferError):
-        vi.attn_decode(*args, block_table=t_i32(bt), algo="stream")         # contiguous-only kernel
+        vi.attn_decode(*args, block_table=t_i32(bt), algo="lut")            # contiguous-only variant
     kbad = torch.zeros(kpool.shape[0], 8, 48, 32, dtype=torch.uint8, device="cuda")   # page_size 48
     with pytest.raises(VecInferError):
         vi.attn_decode(args[0], args[1], args[2], args[3], kbad, kbad, args[6], block_table=t_i32(bt))
+
+
+# ---------------------------------------------------------------- stream kernel over paged pools
+@pytest.mark.parametrize("page_size", [32, 64])
+@pytest.mark.parametrize("splits", [0, 3, 40])   # 0: one piece per CTA; 40 x 24 units > #SMs: persistent
+def test_paged_stream_equals_contiguous(page_size, splits):
+    """The stream partition cuts units at 16-token boundaries, so a 32-token tile's two sub-tiles
+    can lie in different pages: each is translated separately.  Bit-equal to the contiguous stream
+    kernel, and vs the oracle."""
+    n_cap = 2048
+    lens = [2048, 1000, 37]
+    c = _attn_case(len(lens), 8, 4, n_cap, lens, seed=550 + page_size + splits)
+    kpool, bt = _paginate(c["kc"].astype(np.uint8), page_size, seed=551)
+    vpool, _ = _paginate(c["vc"].astype(np.uint8), page_size, seed=551)
+    o_c, L_c = _run_gpu(c, algo="stream", num_splits=splits)
+    o_p, L_p = vi.attn_decode(t_bf16(c["q"]), t_f32(c["lam"]), t_bf16(c["ck"]), t_bf16(c["cv"]), t_u8(kpool),
+                              t_u8(vpool), t_i32(c["seq_lens"]), block_table=t_i32(bt), algo="stream",
+                              num_splits=splits)
+    o_p, L_p = o_p.cpu().numpy(), L_p.cpu().numpy()
+    assert np.array_equal(o_p, o_c) and np.array_equal(L_p, L_c)
+    _assert_close(o_p, L_p, *_run_ref(c))
+
+
+def test_paged_stream_auto_batch_decode_and_fused_append():
+    """B*H_kv >= #SMs: AUTO runs the stream kernel on the paged pool, and decode_step fuses the append
+    (owner pieces write the new codes at the translated rows)."""
+    B, n_cap, ps = 20, 512, 64
+    lens = [n_cap - 3 - (7 * b) % 40 for b in range(B)]
+    c = _attn_case(B, 8, 4, n_cap, lens, seed=560)
+    kpool, bt = _paginate(c["kc"].astype(np.uint8), ps, seed=561)
+    vpool, _ = _paginate(c["vc"].astype(np.uint8), ps, seed=561)
+    assert vi.attn_kernel_kind(B, 8, n_cap) == "stream"
+    o_p, L_p = vi.attn_decode(t_bf16(c["q"]), t_f32(c["lam"]), t_bf16(c["ck"]), t_bf16(c["cv"]), t_u8(kpool),
+                              t_u8(vpool), t_i32(c["seq_lens"]), block_table=t_i32(bt))
+    _assert_close(o_p.cpu().numpy(), L_p.cpu().numpy(), *_run_ref(c))
+    kn = synth.gen_keys(1, 8, 128, seed=562, batch=B)[:, 0]
+    vn = synth.gen_values(1, 8, 128, seed=563, batch=B)[:, 0]
+    wp = [n - 1 for n in lens]
+    kp, vp = t_u8(kpool), t_u8(vpool)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    assert vi.decode_step_launches(B, 8, n_cap) == 1
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(CB["inv_lambda"]),
+                          t_bf16(c["ck"]), t_bf16(c["cv"]), kp, vp, t_i32(wp), t_i32(lens), err_flags=err,
+                          block_table=t_i32(bt))
+    assert int(err.item()) == 0
+    for b in range(B):
+        for h in range(8):
+            kk, vv = ref.encode_kv(kn[b, h], vn[b, h], CB["inv_lambda"][h], c["ck"][h], c["cv"][h])
+            c["kc"][b, h, wp[b]], c["vc"][b, h, wp[b]] = kk, vv
+    assert np.array_equal(_unpaginate(kp.cpu().numpy(), bt, ps), c["kc"].astype(np.uint8))
+    assert np.array_equal(_unpaginate(vp.cpu().numpy(), bt, ps), c["vc"].astype(np.uint8))
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_run_ref(c))
