@@ -245,8 +245,8 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
                 "the pairs (f, f), (d4b10, d8b12), (d8b12, d8b8)");
   if (kcfg.head_dim != vcfg.head_dim) return fail(VECINFER_ERR_SHAPE, "attn_decode: K and V head_dim differ");
   const int D = kcfg.head_dim;
-  if (D == 64 && (algo == VECINFER_ATTN_LUT || algo == VECINFER_ATTN_DEQUANT_MMA_STREAM || res))
-    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: head_dim 64 runs the split DEQUANT_MMA kernel without a residual window");
+  if (D == 64 && (algo == VECINFER_ATTN_LUT || algo == VECINFER_ATTN_DEQUANT_MMA_STREAM))
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: head_dim 64 runs the split DEQUANT_MMA kernel");
   if (algo == VECINFER_ATTN_LUT && (kcfg.code_bits != 8 || vcfg.code_bits != 8))
     return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: the LUT variant is implemented for b2d4 only");
   if (tok_begin < 0 || (tok_end >= 0 && tok_end < tok_begin))
@@ -409,11 +409,11 @@ static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t k
                          int32_t num_splits, vecinfer_attn_algo_t algo, bool paged = false) {
   if (algo == VECINFER_ATTN_LUT || kcfg.code_bits > 8 || vcfg.code_bits > 8 || B <= 0 || H_kv <= 0) return false;
   if (vq_next2(kcfg) || vq_next2(vcfg)) return false;   // NEXT-2 formats: separate encode launch
-  if (kcfg.head_dim != 128) return false;   // the fused encode is written for 128-dim keys
+  if (kcfg.head_dim != 128 && kcfg.head_dim != 64) return false;
   const int64_t units = static_cast<int64_t>(B) * H_kv;
   if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
     return num_splits == 0 || units * num_splits <= device_sm_count();   // persistent grids: separate append
-  if (algo != VECINFER_ATTN_DEQUANT_TC && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
+  if (algo != VECINFER_ATTN_DEQUANT_TC && kcfg.head_dim == 128 && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
   const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
   const int mac = plan.cluster ? attn_mma_max_active_clusters(plan.S) : 0;
   const int64_t waves = plan.cluster ? (units + (mac > 0 ? mac : 1) - 1) / (mac > 0 ? mac : 1)

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   using FV = FmtD<VB, DH>;
   constexpr int KR = FK::kRow, VR = FV::kRow;
   constexpr int KS = DH / 16, VS = DH / 32, NL = DH / 4;
-  constexpr bool kCanAppend = KB <= 8 && VB <= 8 && DH == 128;   // d = 4, 4/8-bit codebooks
+  constexpr bool kCanAppend = KB <= 8 && VB <= 8;   // d = 4, 4/8-bit codebooks (D = 128 or 64)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
@@ -253,12 +253,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     const uint16_t* cb = isv ? cbv : cbk;
     if (lane < P) stage[warp * 32 + lane] = bf16x4_to_float4(*reinterpret_cast<const uint2*>(cb + 4 * (P * w8 + lane)));
     float x[4];
+    const int le = lane & (NL - 1);   // D = 64: the upper half-warp duplicates the lower one
     if (!isv) {
-      const bool bad = key_transform_lane(a.knew + b * a.kn_sb + hc * a.kn_sh + 4 * lane,
-                                          a.inv_lambda + hc * 128 + 4 * lane, a.inv_sqrt_d, lane, x);
+      const bool bad = key_transform_lane(a.knew + b * a.kn_sb + hc * a.kn_sh + 4 * le,
+                                          a.inv_lambda + hc * DH + 4 * le, a.inv_sqrt_d, lane, x, NL);
       if (bad && warp == 0 && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
     } else {
-      const float4 v = bf16x4_to_float4(*reinterpret_cast<const uint2*>(a.vnew + b * a.vn_sb + hc * a.vn_sh + 4 * lane));
+      const float4 v = bf16x4_to_float4(*reinterpret_cast<const uint2*>(a.vnew + b * a.vn_sb + hc * a.vn_sh + 4 * le));
       x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
     }
     __syncwarp();
@@ -279,21 +280,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   const int rlen = a.res ? min(a.res_lens[b], static_cast<int32_t>(a.r_cap)) : 0;
   const int t_res0 = s + a.S * warp;
   const int64_t res_off = a.res ? b * a.res_sb + hc * a.res_sh : 0;
+  // rows of DH bf16: lane l < NL holds key elements 4l..4l+3, thread (r, j) the DH/8 value
+  // elements (DH/8) r .. of its accumulator slots (two uint4 at D = 128, one at D = 64)
   uint2 rk = make_uint2(0u, 0u);
   uint4 rv0 = make_uint4(0u, 0u, 0u, 0u), rv1 = rv0;
-  if (t_res0 < rlen) {
-    const bool is_new = a.res_append && t_res0 == rlen - 1;
-    const uint16_t* krow = is_new ? a.knew + b * a.kn_sb + hc * a.kn_sh : a.kres + res_off + t_res0 * 128;
-    const uint16_t* vrow = is_new ? a.vnew + b * a.vn_sb + hc * a.vn_sh : a.vres + res_off + t_res0 * 128;
-    rk = *reinterpret_cast<const uint2*>(krow + 4 * lane);
-    rv0 = *reinterpret_cast<const uint4*>(vrow + 16 * r);
-    rv1 = *reinterpret_cast<const uint4*>(vrow + 16 * r + 8);
-    if (is_new) {   // write the new token's raw rows into the window (this warp is the only writer)
-      reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.kres) + res_off + t_res0 * 128)[lane] = rk;
-      reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.vres) + res_off + t_res0 * 128)[lane] =
+  auto res_row = [&](int t) {
+    const bool is_new = a.res_append && t == rlen - 1;
+    const uint16_t* krow = is_new ? a.knew + b * a.kn_sb + hc * a.kn_sh : a.kres + res_off + static_cast<int64_t>(t) * DH;
+    const uint16_t* vrow = is_new ? a.vnew + b * a.vn_sb + hc * a.vn_sh : a.vres + res_off + static_cast<int64_t>(t) * DH;
+    rk = lane < NL ? *reinterpret_cast<const uint2*>(krow + 4 * lane) : make_uint2(0u, 0u);
+    rv0 = *reinterpret_cast<const uint4*>(vrow + (DH / 8) * r);
+    if constexpr (DH == 128) rv1 = *reinterpret_cast<const uint4*>(vrow + 16 * r + 8);
+    if (is_new && lane < NL) {   // write the new token's raw rows into the window (this warp is the only writer)
+      reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.kres) + res_off + static_cast<int64_t>(t) * DH)[lane] = rk;
+      reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.vres) + res_off + static_cast<int64_t>(t) * DH)[lane] =
           *reinterpret_cast<const uint2*>(vrow + 4 * lane);
     }
-  }
+  };
+  if (t_res0 < rlen) res_row(t_res0);
   if (warp < 4) {   // Eq. 7 query transform (heads g >= G are zero padding)
     float* dq = sq + kQRow * warp + qoff(lane);
     if (warp < hm.gp) qtransform_lane(qw, lam4, a.qscale, lane, dq, NL);
@@ -329,14 +333,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         const float c = sbest[(warp + w) * 32 + lane];
         if (c < bb) { bb = c; ii = sidx[(warp + w) * 32 + lane]; }
       }
-      if (warp == 0) put_code<(KB <= 8 ? KB : 8)>(newcodes, lane, ii);
-      else put_code<(VB <= 8 ? VB : 8)>(newcodes + 64, lane, ii);
+      if (warp == 0) put_code<(KB <= 8 ? KB : 8)>(newcodes, lane, ii, NL);
+      else put_code<(VB <= 8 ? VB : 8)>(newcodes + 64, lane, ii, NL);
       int pgw = 0;
       const bool pok = p_row >= 0 && p_row < a.n_cap && (!paged || ((pgw = page_of(p_row)) >= 0 && pgw < a.n_pages));
       if (pok) {
         const int64_t rw = row_in(pgw, p_row);
-        if (warp == 0) put_code<(KB <= 8 ? KB : 8)>(a.kcodes_w + rw * KR, lane, ii);
-        else put_code<(VB <= 8 ? VB : 8)>(a.vcodes_w + rw * VR, lane, ii);
+        if (warp == 0) put_code<(KB <= 8 ? KB : 8)>(a.kcodes_w + rw * KR, lane, ii, NL);
+        else put_code<(VB <= 8 ? VB : 8)>(a.vcodes_w + rw * VR, lane, ii, NL);
       } else if (lane == 0 && a.err) {
         atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
       }
@@ -376,31 +380,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   // ---- residual window (NEXT-1): raw bf16 rows scored with the raw q (q k^T = q~ k~^T, Eq. 7),
   // folded into this warp's online-softmax state before the code tiles; the P.V goes into the hi
   // slots of the MMA accumulator layout (thread (r, j) owns head j, dims 16r + 2t + {0, 1})
-  if constexpr (DH == 128) if (t_res0 < rlen) {
+  if (t_res0 < rlen) {
     float qr[4][4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-      const float4 v = g < hm.gp ? bf16x4_to_float4(*reinterpret_cast<const uint2*>(
-                                       a.q + b * a.q_sb + (hm.hq0 + g) * a.q_sh + 4 * lane))
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v = (g < hm.gp && lane < NL) ? bf16x4_to_float4(*reinterpret_cast<const uint2*>(
+                                                      a.q + b * a.q_sb + (hm.hq0 + g) * a.q_sh + 4 * lane))
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
       qr[g][0] = v.x * a.qscale_raw; qr[g][1] = v.y * a.qscale_raw;
       qr[g][2] = v.z * a.qscale_raw; qr[g][3] = v.w * a.qscale_raw;
     }
     for (int t = t_res0; t < rlen; t += a.S * kNW) {
-      if (t != t_res0) {   // rows beyond the first (long windows, few splits)
-        const uint16_t* krow = a.kres + res_off + t * 128;
-        const uint16_t* vrow = a.vres + res_off + t * 128;
-        const bool is_new = a.res_append && t == rlen - 1;
-        rk = *reinterpret_cast<const uint2*>((is_new ? a.knew + b * a.kn_sb + hc * a.kn_sh : krow) + 4 * lane);
-        const uint16_t* vsrc = is_new ? a.vnew + b * a.vn_sb + hc * a.vn_sh : vrow;
-        rv0 = *reinterpret_cast<const uint4*>(vsrc + 16 * r);
-        rv1 = *reinterpret_cast<const uint4*>(vsrc + 16 * r + 8);
-        if (is_new) {
-          reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.kres) + res_off + t * 128)[lane] = rk;
-          reinterpret_cast<uint2*>(const_cast<uint16_t*>(a.vres) + res_off + t * 128)[lane] =
-              *reinterpret_cast<const uint2*>(vsrc + 4 * lane);
-        }
-      }
+      if (t != t_res0) res_row(t);   // rows beyond the first (long windows, few splits)
       const float4 kv = bf16x4_to_float4(rk);
       float sg[4];
 #pragma unroll
@@ -414,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       if (sj > m_run + kTau) {   // per-lane: all 8 lanes of head j agree
         const float alpha = ex2_approx(m_run - sj);
 #pragma unroll
-        for (int tt = 0; tt < 8; ++tt) {
+        for (int tt = 0; tt < 2 * VS; ++tt) {
           acc[tt][0] *= alpha; acc[tt][1] *= alpha; acc[tt][2] *= alpha; acc[tt][3] *= alpha;
         }
         l_run *= alpha;
@@ -424,9 +415,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       if (r == 0) l_run += p;                         // once per head (lanes r = 0 of each j)
       const uint32_t vw[8] = {rv0.x, rv0.y, rv0.z, rv0.w, rv1.x, rv1.y, rv1.z, rv1.w};
 #pragma unroll
-      for (int tt = 0; tt < 8; ++tt) {
-        acc[tt][0] += p * __uint_as_float(vw[tt] << 16);             // dim 16r + 2tt
-        acc[tt][2] += p * __uint_as_float(vw[tt] & 0xFFFF0000u);     // dim 16r + 2tt + 1
+      for (int tt = 0; tt < 2 * VS; ++tt) {
+        acc[tt][0] += p * __uint_as_float(vw[tt] << 16);             // dim (DH/8) r + 2tt
+        acc[tt][2] += p * __uint_as_float(vw[tt] & 0xFFFF0000u);     // dim (DH/8) r + 2tt + 1
       }
     }
   }
@@ -510,12 +501,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       TileCodes<KB, VB> cur = nxt;
       if constexpr (kCanAppend) {
       if (it == patch_tile) {   // the appended row: codes just encoded, not the stale load
-        KCode<KB> nk;
-        VCode<VB> nv;
-        if constexpr (KB == 8) nk = *reinterpret_cast<const uint2*>(newcodes + 8 * j);
-        else nk = *reinterpret_cast<const uint32_t*>(newcodes + Fmt<(KB <= 8 ? KB : 8)>::kOffK * j);
-        if constexpr (VB == 8) nv = *reinterpret_cast<const uint32_t*>(newcodes + 64 + 4 * r);
-        else nv = *reinterpret_cast<const uint16_t*>(newcodes + 64 + Fmt<(VB <= 8 ? VB : 8)>::kOffV * r);
+        const KCode<KB> nk = new_kchunk<KB, DH>(newcodes, j);
+        const VCode<VB> nv = new_vchunk<VB, DH>(newcodes + 64, r);
         const int qp = patch_row >> 4, rr = patch_row & 15;
   #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -690,9 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       if (it < ntile) {
         if constexpr (kCanAppend) {
           if (it == patch_tile) {   // the appended row's V codes
-            VCode<VB> nv;
-            if constexpr (VB == 8) nv = *reinterpret_cast<const uint32_t*>(newcodes + 64 + 4 * r);
-            else nv = *reinterpret_cast<const uint16_t*>(newcodes + 64 + Fmt<(VB <= 8 ? VB : 8)>::kOffV * r);
+            const VCode<VB> nv = new_vchunk<VB, DH>(newcodes + 64, r);
             const int qp = patch_row >> 4, rr = patch_row & 15;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {

@@ -409,14 +409,32 @@ __device__ __forceinline__ void load_subtile(TileCodes<KB, VB>& tc, const uint8_
 }
 
 // store the packed code of sub-vector `lane` (4/8-bit) for the fused append
+// (all 32 lanes call it; lanes >= nsub -- D = 64: 16 sub-vectors -- hold duplicates and do not store)
 template <int BITS>
-__device__ __forceinline__ void put_code(unsigned char* row, int lane, uint32_t code) {
+__device__ __forceinline__ void put_code(unsigned char* row, int lane, uint32_t code, int nsub = 32) {
   if constexpr (BITS == 8) {
-    row[lane] = static_cast<uint8_t>(code);
+    if (lane < nsub) row[lane] = static_cast<uint8_t>(code);
   } else {
     const uint32_t hi = __shfl_xor_sync(0xffffffffu, code, 1);
-    if ((lane & 1) == 0) row[lane >> 1] = static_cast<uint8_t>(code | (hi << 4));
+    if ((lane & 1) == 0 && lane < nsub) row[lane >> 1] = static_cast<uint8_t>(code | (hi << 4));
   }
+}
+
+// the appended row's code chunks (just encoded into shared memory) in the per-lane register layout
+// of FmtD<BITS, DH>: K chunk of lane j, V chunk of lane r
+template <int BITS, int DH>
+__device__ __forceinline__ KCode<BITS> new_kchunk(const unsigned char* nc, int j) {
+  if constexpr (BITS == 8 && DH == 128) return *reinterpret_cast<const uint2*>(nc + 8 * j);
+  else if constexpr (BITS == 8) return make_uint2(*reinterpret_cast<const uint32_t*>(nc + 4 * j), 0u);
+  else if constexpr (DH == 128) return *reinterpret_cast<const uint32_t*>(nc + 4 * j);
+  else return *reinterpret_cast<const uint16_t*>(nc + 2 * j);
+}
+template <int BITS, int DH>
+__device__ __forceinline__ VCode<BITS> new_vchunk(const unsigned char* nc, int r) {
+  if constexpr (BITS == 8 && DH == 128) return *reinterpret_cast<const uint32_t*>(nc + 4 * r);
+  else if constexpr (BITS == 8) return *reinterpret_cast<const uint16_t*>(nc + 2 * r);
+  else if constexpr (DH == 128) return *reinterpret_cast<const uint16_t*>(nc + 2 * r);
+  else return nc[r];
 }
 
 // Query transform of Eq. 7 for one head (one warp): ((q * lambda) H_pm) * qscale, fp32 FWHT

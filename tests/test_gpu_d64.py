@@ -1,7 +1,8 @@
 """head_dim 64 (the paper's Fig. 10 variant): 16 sub-vectors of 4 dims per
 head.  Encode must match the oracle bit for bit (its pinned transform is written for any D: 64-point
 integer Hadamard, 1/sqrt(64) = 0.125), attention must match the oracle within the usual 2e-3.
-D = 64 runs the split kernel (no residual window, no fused append, no stream/LUT variant).
+D = 64 runs the split kernel, with the residual window and the fused decode append (no stream /
+LUT variant).
 """
 import numpy as np
 import pytest
@@ -96,25 +97,65 @@ def test_d64_token_range_and_bf16():
     assert np.array_equal(synth.round_to_bf16(of.astype(np.float32)), ob.astype(np.float32))
 
 
-def test_d64_decode_step():
-    """D = 64 decode step: separate append launch + attention; appended codes are the oracle's."""
-    lens = [700, 64]
+@pytest.mark.parametrize("bits,lens", [(8, [700, 64]), (4, [3000, 901]), (8, [40000])])
+def test_d64_decode_step(bits, lens):
+    """D = 64 decode step with the append fused into the attention launch (the owner split encodes
+    the new token on 16 lanes: 64-point integer FWHT, 16 sub-vectors); appended codes are the
+    oracle's bit for bit, the output matches the oracle."""
     B = len(lens)
-    c = _case(B, 4, 710, lens, seed=640)
+    c = _case(B, 4, max(lens) + 10, lens, seed=640 + bits, bits=bits)
     kn = synth.gen_keys(1, 8, D, seed=641, batch=B)[:, 0]
     vn = synth.gen_values(1, 8, D, seed=642, batch=B)[:, 0]
     wp = [n - 1 for n in lens]
-    kcodes, vcodes = t_u8(ref.pack_codes(c["kc"], 8)), t_u8(ref.pack_codes(c["vc"], 8))
+    kcodes, vcodes = t_u8(ref.pack_codes(c["kc"], bits)), t_u8(ref.pack_codes(c["vc"], bits))
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
     o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(INV), t_bf16(c["ck"]),
-                          t_bf16(c["cv"]), kcodes, vcodes, t_i32(wp), t_i32(lens), kcfg=CFG64[8], vcfg=CFG64[8])
-    assert vi.decode_step_launches(B, 8, 710, CFG64[8], CFG64[8]) == 2
+                          t_bf16(c["cv"]), kcodes, vcodes, t_i32(wp), t_i32(lens), kcfg=CFG64[bits], vcfg=CFG64[bits],
+                          err_flags=err)
+    assert int(err.item()) == 0
+    assert vi.decode_step_launches(B, 8, max(lens) + 10, CFG64[bits], CFG64[bits]) == 1
     for b in range(B):
         for h in range(8):
             kk, vv = ref.encode_kv(kn[b, h], vn[b, h], INV[h], c["ck"][h], c["cv"][h])
             c["kc"][b, h, wp[b]], c["vc"][b, h, wp[b]] = kk, vv
-    assert np.array_equal(kcodes.cpu().numpy(), ref.pack_codes(c["kc"], 8))
-    assert np.array_equal(vcodes.cpu().numpy(), ref.pack_codes(c["vc"], 8))
+    assert np.array_equal(kcodes.cpu().numpy(), ref.pack_codes(c["kc"], bits))
+    assert np.array_equal(vcodes.cpu().numpy(), ref.pack_codes(c["vc"], bits))
     _assert_close(o.cpu().numpy(), L.cpu().numpy(), *_ref(c))
+
+
+@pytest.mark.parametrize("splits", [0, 1, 3, 18])
+@pytest.mark.parametrize("n_q,r_lens", [([3000, 700], [128, 5]), ([0, 1000], [17, 0])])
+def test_d64_residual_window(splits, n_q, r_lens):
+    """Full-precision residual window at D = 64 (raw bf16 rows of 64 elements)."""
+    B = len(n_q)
+    c = _case(B, 4, max(n_q) + 4, n_q, seed=660 + splits)
+    K_res = synth.gen_keys(256, 8, D, seed=661, batch=B).transpose(0, 2, 1, 3).copy()
+    V_res = synth.gen_values(256, 8, D, seed=662, batch=B).transpose(0, 2, 1, 3).copy()
+    rl = np.asarray(r_lens)
+    o, L = _run(c, num_splits=splits, k_res=t_bf16(K_res), v_res=t_bf16(V_res), res_lens=t_i32(rl))
+    _assert_close(o, L, *ref.attention_decode_batch(c["q"], c["lam"], c["ck"], c["cv"], c["kc"], c["vc"],
+                                                    c["seq_lens"], K_res=K_res, V_res=V_res, res_lens=rl))
+
+
+def test_d64_decode_step_appends_to_residual():
+    c = _case(2, 4, 2004, [2000, 300], seed=670)
+    K_res = synth.gen_keys(128, 8, D, seed=671, batch=2).transpose(0, 2, 1, 3).copy()
+    V_res = synth.gen_values(128, 8, D, seed=672, batch=2).transpose(0, 2, 1, 3).copy()
+    kn = synth.gen_keys(1, 8, D, seed=673, batch=2)[:, 0]
+    vn = synth.gen_values(1, 8, D, seed=674, batch=2)[:, 0]
+    kr, vr = t_bf16(K_res), t_bf16(V_res)
+    lens = np.array([41, 2])                       # the new token becomes row lens-1
+    o, L = vi.decode_step(t_bf16(c["q"]), t_bf16(kn), t_bf16(vn), t_f32(c["lam"]), t_f32(INV), t_bf16(c["ck"]),
+                          t_bf16(c["cv"]), t_u8(ref.pack_codes(c["kc"], 8)), t_u8(ref.pack_codes(c["vc"], 8)),
+                          t_i32([0, 0]), t_i32(c["seq_lens"]), kcfg=CFG64[8], vcfg=CFG64[8], k_res=kr, v_res=vr,
+                          res_lens=t_i32(lens), append_to_residual=True)
+    for b in range(2):
+        K_res[b, :, lens[b] - 1] = kn[b]
+        V_res[b, :, lens[b] - 1] = vn[b]
+    assert np.array_equal(kr.float().cpu().numpy(), K_res) and np.array_equal(vr.float().cpu().numpy(), V_res)
+    _assert_close(o.cpu().numpy(), L.cpu().numpy(), *ref.attention_decode_batch(
+        c["q"], c["lam"], c["ck"], c["cv"], c["kc"], c["vc"], c["seq_lens"], K_res=K_res, V_res=V_res,
+        res_lens=lens))
 
 
 def test_d64_unsupported_paths_fail_loudly():
@@ -123,9 +164,6 @@ def test_d64_unsupported_paths_fail_loudly():
         _run(c, algo="stream")
     with pytest.raises(VecInferError):
         _run(c, algo="lut")
-    kr = torch.zeros(1, 8, 16, D, dtype=torch.bfloat16, device="cuda")
-    with pytest.raises(VecInferError):
-        _run(c, k_res=kr, v_res=kr, res_lens=t_i32([4]))
     with pytest.raises(VecInferError):   # K and V head dims must agree
         vi.attn_decode(t_bf16(c["q"]), t_f32(c["lam"]), t_bf16(c["ck"]), t_bf16(c["cv"]),
                        t_u8(ref.pack_codes(c["kc"], 8)), t_u8(ref.pack_codes(c["vc"], 8)), t_i32(c["seq_lens"]),
