@@ -407,13 +407,21 @@ extern "C" vecinfer_status_t vecinfer_attn_decode_paged(const void* q_bf16, int3
 // 16-bit codebooks or the LUT variant.
 static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
                          int32_t num_splits, vecinfer_attn_algo_t algo, bool paged = false) {
-  if (algo == VECINFER_ATTN_LUT || kcfg.code_bits > 8 || vcfg.code_bits > 8 || B <= 0 || H_kv <= 0) return false;
-  if (vq_next2(kcfg) || vq_next2(vcfg)) return false;   // NEXT-2 formats: separate encode launch
+  if (algo == VECINFER_ATTN_LUT || B <= 0 || H_kv <= 0) return false;
+  // NEXT-2 formats: the split kernel fuses the append for books of <= 1024 entries (d8b8, d2b8,
+  // d4b10); d8b12 / d8b16 keep the separate encode launch
+  auto small_next2 = [](const vecinfer_vq_t& c) {
+    return vq_next2(c) && ((c.sub_dim == 8 && c.code_bits == 8) || (c.sub_dim == 2 && c.code_bits == 8) ||
+                           (c.sub_dim == 4 && c.code_bits == 10));
+  };
+  const bool n2 = vq_next2(kcfg) || vq_next2(vcfg);
+  if (n2 && !(small_next2(kcfg) && small_next2(vcfg))) return false;
+  if (!n2 && (kcfg.code_bits > 8 || vcfg.code_bits > 8)) return false;
   if (kcfg.head_dim != 128 && kcfg.head_dim != 64) return false;
   const int64_t units = static_cast<int64_t>(B) * H_kv;
   if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
     return num_splits == 0 || units * num_splits <= device_sm_count();   // persistent grids: separate append
-  if (algo != VECINFER_ATTN_DEQUANT_TC && kcfg.head_dim == 128 && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
+  if (!n2 && algo != VECINFER_ATTN_DEQUANT_TC && kcfg.head_dim == 128 && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
   const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
   const int mac = plan.cluster ? attn_mma_max_active_clusters(plan.S) : 0;
   const int64_t waves = plan.cluster ? (units + (mac > 0 ? mac : 1) - 1) / (mac > 0 ? mac : 1)

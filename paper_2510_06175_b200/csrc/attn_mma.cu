@@ -102,6 +102,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   constexpr int KR = FK::kRow, VR = FV::kRow;
   constexpr int KS = DH / 16, VS = DH / 32, NL = DH / 4;
   constexpr bool kCanAppend = KB <= 8 && VB <= 8;   // d = 4, 4/8-bit codebooks (D = 128 or 64)
+  // fused append of the NEXT-2 formats with books of <= 1024 entries (d8b8, d2b8, d4b10): a generic
+  // all-thread centroid scan in the owner split (d8b12 / d8b16 books are too large to scan inside
+  // the attention launch: vecinfer_decode_step appends them with a separate encode launch)
+  constexpr auto gen_ok = [](int f) { return f == kFmtD8B8 || f == kFmtD2B8 || f == kFmtD4B10; };
+  constexpr bool kGenAppend = gen_ok(KB) && gen_ok(VB) && DH == 128;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   bool owner = false;
   int patch_tile = -1, patch_row = 0;
   int64_t p_row = 0;
-  if (kCanAppend && a.append) {
+  if ((kCanAppend || kGenAppend) && a.append) {
     p_row = a.write_pos[b];
     const bool in_range = p_row >= beg && p_row < e;
     owner = in_range ? (p_row >= r0 && p_row < r1) : (s == 0);
@@ -273,6 +278,97 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
     sbest[warp * 32 + lane] = best;
     sidx[warp * 32 + lane] = bi;
+  }
+  if constexpr (kGenAppend) if (owner) {
+    // Eq. 9 for the d8b8 / d2b8 / d4b10 formats: warp 0 writes the pinned key transform, warp 8 the
+    // raw value to shared memory; then for every sub-vector m all 256 threads of a stream scan
+    // centroids j = t, t + 256, ... with the pinned distance (fp32 RN, no FMA, left to right over
+    // the d dims: reading R9), the minima reduce as (dist_bits << 32 | j) -- lowest index on ties --
+    // and the codes are packed into the row's little-endian bit string (R11)
+    float* xs = reinterpret_cast<float*>(smem_raw + kMiscW);                              // [2][128]
+    unsigned long long* gbest = reinterpret_cast<unsigned long long*>(smem_raw + kMiscW + 1024);   // [2][64]
+    if (warp == 0) {
+      float x[4];
+      const bool bad = key_transform_lane(a.knew + b * a.kn_sb + hc * a.kn_sh + 4 * lane,
+                                          a.inv_lambda + hc * 128 + 4 * lane, a.inv_sqrt_d, lane, x);
+      if (bad && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
+      *reinterpret_cast<float4*>(xs + 4 * lane) = make_float4(x[0], x[1], x[2], x[3]);
+    } else if (warp == 8) {
+      *reinterpret_cast<float4*>(xs + 128 + 4 * lane) =
+          bf16x4_to_float4(*reinterpret_cast<const uint2*>(a.vnew + b * a.vn_sb + hc * a.vn_sh + 4 * lane));
+    }
+    if (tid < 128) gbest[tid] = ~0ull;
+    __syncthreads();
+    const int which = warp >> 3, t = tid & 255;
+    const int sub = which ? fmt_sub(VB) : fmt_sub(KB), bits = which ? fmt_bits(VB) : fmt_bits(KB);
+    const int M = 128 / sub;
+    const float* xw = xs + 128 * which;
+    // centroids come from the stream's shared table (filled above, exact fp16 copies of the bf16
+    // book): d4b10 = separate table (64-B rows of 8 replicas), d8b8 / d2b8 = the stream's half of
+    // the classic 256-B rows (8 x 16 B / 32 x 4 B replicas); thread t reads replica t % reps
+    auto scan = [&](auto FF, uint32_t base) {
+      constexpr int F = decltype(FF)::value;
+      constexpr int kSub = fmt_sub(F), kEnt = 1 << fmt_bits(F);
+      for (int m = 0; m < M; ++m) {
+        float xm[kSub];
+#pragma unroll
+        for (int u = 0; u < kSub; ++u) xm[u] = xw[m * kSub + u];
+        unsigned long long key = ~0ull;
+        for (int jj = t; jj < kEnt; jj += 256) {
+          float c[kSub];
+          if constexpr (F == kFmtD4B10) {
+            const uint2 w = lds_u64(base + jj * 64 + (t & 7) * 8);
+            const float2 c01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+            const float2 c23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+            c[0] = c01.x; c[1] = c01.y; c[2] = c23.x; c[3] = c23.y;
+          } else if constexpr (F == kFmtD8B8) {
+            const uint4 w = lds_u128(base + jj * 256 + (t & 7) * 16);
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float2 cc = __half22float2(*reinterpret_cast<const __half2*>(&ww[u]));
+              c[2 * u] = cc.x; c[2 * u + 1] = cc.y;
+            }
+          } else {   // d2b8
+            const uint32_t w = lds_u32(base + jj * 256 + (t & 31) * 4);
+            const float2 cc = __half22float2(*reinterpret_cast<const __half2*>(&w));
+            c[0] = cc.x; c[1] = cc.y;
+          }
+          float ee = __fsub_rn(xm[0], c[0]);
+          float dsum = __fmul_rn(ee, ee);
+#pragma unroll
+          for (int u = 1; u < kSub; ++u) {
+            ee = __fsub_rn(xm[u], c[u]);
+            dsum = __fadd_rn(dsum, __fmul_rn(ee, ee));
+          }
+          const unsigned long long k2 = (static_cast<unsigned long long>(__float_as_uint(dsum)) << 32) | static_cast<uint32_t>(jj);
+          key = k2 < key ? k2 : key;
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+          const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, key, off);
+          key = o2 < key ? o2 : key;
+        }
+        if (lane == 0) atomicMin(&gbest[64 * which + m], key);
+      }
+    };
+    if (which == 0) scan(std::integral_constant<int, KB>{}, Fmt<KB>::kSep ? tab_s + kSepOff : tab_s);
+    else scan(std::integral_constant<int, VB>{}, Fmt<VB>::kSep ? tab_s + kSepVOff : tab_s + 128);
+    __syncthreads();
+    // pack: byte i of the row = bits [8i, 8i + 8) of the bit string (b >= 8: <= 2 codes per byte)
+    const int rb = M * bits / 8;
+    int pgw = 0;
+    const bool pok = p_row >= 0 && p_row < a.n_cap && (!paged || ((pgw = page_of(p_row)) >= 0 && pgw < a.n_pages));
+    uint8_t* dst = pok ? (which ? a.vcodes_w + row_in(pgw, p_row) * VR : a.kcodes_w + row_in(pgw, p_row) * KR) : nullptr;
+    for (int i = t; i < rb; i += 256) {
+      const int p = 8 * i, c0 = p / bits, off = p - c0 * bits;
+      uint32_t w = static_cast<uint32_t>(gbest[64 * which + c0] & 0xFFFFFFFFull);
+      if (c0 + 1 < M) w |= static_cast<uint32_t>(gbest[64 * which + c0 + 1] & 0xFFFFFFFFull) << bits;
+      const uint8_t byte = static_cast<uint8_t>(w >> off);
+      newcodes[64 * which + i] = byte;
+      if (dst) dst[i] = byte;
+    }
+    if (!pok && t == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
   }
   // residual window rows handled by this warp: t = s + S * (warp + kNW * k), first one preloaded
   // here so its latency hides behind the prologue; the appended row (decode step into the
@@ -499,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   if constexpr (!TC) {
     for (int it = warp; it < ntile; it += kNW) {
       TileCodes<KB, VB> cur = nxt;
-      if constexpr (kCanAppend) {
+      if constexpr (kCanAppend || kGenAppend) {
       if (it == patch_tile) {   // the appended row: codes just encoded, not the stale load
         const KCode<KB> nk = new_kchunk<KB, DH>(newcodes, j);
         const VCode<VB> nv = new_vchunk<VB, DH>(newcodes + 64, r);

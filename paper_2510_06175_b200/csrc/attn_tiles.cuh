@@ -422,20 +422,46 @@ __device__ __forceinline__ void put_code(unsigned char* row, int lane, uint32_t 
 
 // the appended row's code chunks (just encoded into shared memory) in the per-lane register layout
 // of FmtD<BITS, DH>: K chunk of lane j, V chunk of lane r
+// NEXT-2 formats: d8b8 / d2b8 chunks are aligned words; the bit-string formats (d4b10, ...) are
+// assembled byte by byte (little-endian, reading R11)
+template <int NB, int NW>
+__device__ __forceinline__ void bytes_to_words(const unsigned char* p, uint32_t (&w)[NW]) {
+#pragma unroll
+  for (int i = 0; i < NW; ++i) w[i] = 0u;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) w[i >> 2] |= static_cast<uint32_t>(p[i]) << (8 * (i & 3));
+}
 template <int BITS, int DH>
 __device__ __forceinline__ KCode<BITS> new_kchunk(const unsigned char* nc, int j) {
   if constexpr (BITS == 8 && DH == 128) return *reinterpret_cast<const uint2*>(nc + 8 * j);
   else if constexpr (BITS == 8) return make_uint2(*reinterpret_cast<const uint32_t*>(nc + 4 * j), 0u);
-  else if constexpr (DH == 128) return *reinterpret_cast<const uint32_t*>(nc + 4 * j);
-  else return *reinterpret_cast<const uint16_t*>(nc + 2 * j);
+  else if constexpr (BITS == 4 && DH == 128) return *reinterpret_cast<const uint32_t*>(nc + 4 * j);
+  else if constexpr (BITS == 4) return *reinterpret_cast<const uint16_t*>(nc + 2 * j);
+  else if constexpr (BITS == kFmtD8B8) return *reinterpret_cast<const uint32_t*>(nc + 4 * j);
+  else if constexpr (BITS == kFmtD2B8) return *reinterpret_cast<const uint4*>(nc + 16 * j);
+  else {
+    KCode<BITS> c;
+    bytes_to_words<Fmt<BITS>::kOffK>(nc + Fmt<BITS>::kOffK * j, c.w);
+    return c;
+  }
 }
 template <int BITS, int DH>
 __device__ __forceinline__ VCode<BITS> new_vchunk(const unsigned char* nc, int r) {
   if constexpr (BITS == 8 && DH == 128) return *reinterpret_cast<const uint32_t*>(nc + 4 * r);
   else if constexpr (BITS == 8) return *reinterpret_cast<const uint16_t*>(nc + 2 * r);
-  else if constexpr (DH == 128) return *reinterpret_cast<const uint16_t*>(nc + 2 * r);
-  else return nc[r];
+  else if constexpr (BITS == 4 && DH == 128) return *reinterpret_cast<const uint16_t*>(nc + 2 * r);
+  else if constexpr (BITS == 4) return nc[r];
+  else if constexpr (BITS == kFmtD8B8) return *reinterpret_cast<const uint16_t*>(nc + 2 * r);
+  else if constexpr (BITS == kFmtD2B8) return *reinterpret_cast<const uint2*>(nc + 8 * r);
+  else {
+    VCode<BITS> c;
+    bytes_to_words<Fmt<BITS>::kOffV>(nc + Fmt<BITS>::kOffV * r, c.w);
+    return c;
+  }
 }
+// sub-vector size and code width of a format id (b for d = 4, else 100 d + b)
+constexpr int fmt_sub(int f) { return f < 100 ? 4 : f / 100; }
+constexpr int fmt_bits(int f) { return f < 100 ? f : f % 100; }
 
 // Query transform of Eq. 7 for one head (one warp): ((q * lambda) H_pm) * qscale, fp32 FWHT
 // (2 register + 5 shuffle stages); q (4 bf16) and lambda (float4) are this lane's 4 channels;

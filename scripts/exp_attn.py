@@ -28,7 +28,7 @@ def _paginate(kc, ps, seed):
     return pool, perm.view(B, npb).to(torch.int32)
 
 
-FMTS = {"b2d4": (4, 8), "b1d4": (4, 4), "d8b8": (8, 8), "d8b12": (8, 12), "d4b10": (4, 10), "d2b8": (2, 8),
+FMTS = {"b2d4": (4, 8), "b1d4": (4, 4), "b4d4": (4, 16), "d8b8": (8, 8), "d8b12": (8, 12), "d4b10": (4, 10), "d2b8": (2, 8),
         "d8b16": (8, 16)}
 
 
@@ -37,7 +37,7 @@ def _book(name, side, dev):
         z = np.load(os.path.join(ROOT, "data", "d8b16_levels.npz"))
         cb = synth.product_codebook(synth.bf16_from_bits(z[f"lv_d8b16_{side}"]))
         return torch.from_numpy(cb).to(dev).to(torch.bfloat16)
-    z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz" if name in ("b2d4", "b1d4") else
+    z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz" if name in ("b2d4", "b1d4", "b4d4") else
                              "next2_codebooks.npz"))
     return torch.from_numpy(synth.bf16_from_bits(z[f"c{side}_{name}"])).to(dev).to(torch.bfloat16)
 

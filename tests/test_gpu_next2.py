@@ -139,16 +139,20 @@ def test_next2_residual_window():
     _assert_close(o, L, *_ref(c, K_res=K_res, V_res=V_res, res_lens=r_lens))
 
 
-@pytest.mark.parametrize("kn,vn", [("d4b10", "d8b12"), ("d2b8", "d2b8"), ("d8b16", "d8b16")])
-def test_next2_decode_step(kn, vn):
-    """Separate generic append launch + split attention; the appended rows are the oracle's."""
+@pytest.mark.parametrize("kn,vn,wp_off", [("d4b10", "d8b12", 1), ("d2b8", "d2b8", 1), ("d8b16", "d8b16", 1),
+                                           ("d8b8", "d8b8", 1), ("d4b10", "d4b10", 1), ("d8b8", "d8b8", 40),
+                                           ("d2b8", "d2b8", 33)])
+def test_next2_decode_step(kn, vn, wp_off):
+    """decode_step: books of <= 1024 entries (d8b8, d2b8, d4b10) append inside the attention launch
+    (the owner split's all-thread scan), d8b12 / d8b16 with a separate generic encode launch; the
+    appended rows are the oracle's bit for bit, in the first or a middle tile of the owner split."""
     B, H = 2, 8
     lens = [600, 77]
     c = _case(kn, vn, B, H, 4, 610, lens, seed=850)
     kcfg, vcfg = c["kcfg"], c["vcfg"]
     kn_ = synth.gen_keys(1, H, 128, seed=851, batch=B)[:, 0]
     vn_ = synth.gen_values(1, H, 128, seed=852, batch=B)[:, 0]
-    wp = [n - 1 for n in lens]
+    wp = [max(n - wp_off, 0) for n in lens]
     kcodes = t_u8(ref.pack_codes(c["kc"], kcfg.code_bits))
     vcodes = t_u8(ref.pack_codes(c["vc"], vcfg.code_bits))
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -156,7 +160,8 @@ def test_next2_decode_step(kn, vn):
                           t_bf16(c["ck"]), t_bf16(c["cv"]), kcodes, vcodes, t_i32(wp), t_i32(lens), kcfg=kcfg,
                           vcfg=vcfg, err_flags=err)
     assert int(err.item()) == 0
-    assert vi.decode_step_launches(B, H, 610, kcfg, vcfg) == 2   # (the separate generic append)
+    fused = kn in ("d8b8", "d2b8", "d4b10") and vn in ("d8b8", "d2b8", "d4b10")
+    assert vi.decode_step_launches(B, H, 610, kcfg, vcfg) == (1 if fused else 2)
     for b in range(B):
         for h in range(H):
             ckh = c["ck"] if c["ck"].ndim == 2 else c["ck"][h]
