@@ -546,12 +546,37 @@ def run_ours(args, rank, world, local_rank):
     e2e_value = total_bytes / (e2e_ms / 1e3) / 1e9
     peak, peak_src = load_peaks()
     attn_avg_ms = float(np.mean(attn_ms))
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01", f"attn_{args.workload}_traffic.json")
-    if os.path.exists(tp):   # dram__bytes_read.sum + dram__bytes_write.sum per launch, committed ncu capture
-        with open(tp) as f:
-            traffic = json.load(f)["traffic_per_launch"]
+    traffic, ncu = None, None
+    for tp in (os.path.join(ROOT, "profiles", "r02", f"attn_{args.workload}_ncu.json"),
+               os.path.join(ROOT, "profiles", "r01", f"attn_{args.workload}_traffic.json")):
+        if os.path.exists(tp):   # committed ncu --set full capture of this launch (scripts/ncu_summary.py)
+            with open(tp) as f:
+                ncu = json.load(f)
+            traffic = ncu["traffic_per_launch"]   # dram__bytes_read.sum + dram__bytes_write.sum per launch
+            ncu["file"] = os.path.relpath(tp, ROOT)
+            break
     achieved = code_bytes_rank / (attn_avg_ms / 1e3) / 1e9
+    # the binding on-chip resource: the L1/shared LSU data pipe, one wavefront
+    # per clock per SM; wavefronts per unit (shared gathers + global code loads) from the ncu capture
+    lsu = None
+    if ncu is not None and "lsu_wavefronts_per_unit" in ncu:
+        sm_hz = (clk.summary()["sm_mhz"] or 1965.0) * 1e6
+        n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        w = ncu["lsu_wavefronts_per_unit"]
+        bound = n_sms * sm_hz / w * unit_bytes / 1e9
+        lsu = {"wavefronts_per_unit": w, "shared_per_unit": ncu["lsu_shared_wavefronts_per_unit"],
+               "global_per_unit": ncu["lsu_global_wavefronts_per_unit"], "bound_gbs": bound,
+               "frac": achieved / bound, "capture": ncu["file"],
+               "note": "LSU-bound ceiling = #SMs x SM clock x 1 wavefront/clk / wavefronts per unit x bytes per unit"}
+    gather = None
+    if kbits == 16 and vbits == 16:   # b4d4: the codebook gathers run through L1/L2 (scripts/ubench_gather16.cu)
+        clk_per_unit = 59.0           # measured gather bound, profiles/r02/ubench_gather16_b4d4.txt
+        sm_hz = (clk.summary()["sm_mhz"] or 1965.0) * 1e6
+        n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        gbound = n_sms * sm_hz / clk_per_unit * unit_bytes / 1e9
+        gather = {"bound_gbs": gbound, "frac": achieved / gbound, "clk_per_unit": clk_per_unit,
+                  "source": "profiles/r02/ubench_gather16_b4d4.txt (random 8-B gathers from two 512 KiB books, "
+                            "attention launch shape, codes streamed from HBM)"}
     step_ms = elapsed_ms / K
     cpu = None
     if not args.no_cpu_baseline:
@@ -587,7 +612,8 @@ def run_ours(args, rank, world, local_rank):
                      "attn_us_p90": float(np.percentile(attn_ms, 90)) * 1e3,
                      "timing": "CUDA events around K replays of a graph of the 32 layers' vecinfer_attn_decode launches "
                                "(launching stream), per-launch = total/(K*32), inter-kernel gaps included",
-                     "algorithmic_bytes_per_launch": code_bytes_rank, "peak_source": peak_src},
+                     "algorithmic_bytes_per_launch": code_bytes_rank, "peak_source": peak_src,
+                     "lsu_bound": lsu, "gather_bound": gather},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_ms / K, "api": ("32 x vecinfer.decode_step + pinned H2D / D2H copies in 4 layer chunks pipelined on two copy streams, one CUDA graph per step, host sync on the result; " if g_e2e is not None else "32 eager vecinfer calls, ")
