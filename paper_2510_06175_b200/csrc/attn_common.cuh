@@ -303,6 +303,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
           st_relaxed_gpu_u64(pp + static_cast<int64_t>(p) * 512, 0ull);
         }
       }
+      phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 10);
       // ~w = (L_s << 32 | o_s); the neutral element ~0 decodes to (o, L) = (0, bits 0) -> mark it
       float lv[kMaxPer], xv[kMaxPer];
       float m = -INFINITY;

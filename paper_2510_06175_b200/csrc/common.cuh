@@ -361,9 +361,11 @@ unsigned long long* phase_buffer();  // host: set by vecinfer_debug_set_phase_bu
 #ifdef VECINFER_PHASE_TIMING
 __device__ __forceinline__ void phase_mark(unsigned long long* buf, int cta, int slot) {
   if (threadIdx.x == 0 && buf) {
-    unsigned long long t;
+    unsigned long long t, c;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    buf[cta * 16 + slot] = t;   // 16 slots per CTA
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    buf[cta * 32 + slot] = t;        // 16 slots per CTA: globaltimer (ns, coarse, comparable across SMs)
+    buf[cta * 32 + 16 + slot] = c;   // and the SM cycle counter (fine, within the CTA)
   }
 }
 #else

@@ -22,6 +22,7 @@ from paper_2510_06175_b200 import _lib, vecinfer as vi  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", action="append", required=True)
+    ap.add_argument("--sm-mhz", type=float, default=1965.0, help="SM clock converting the cycle stamps")
     args = ap.parse_args()
     lib = _lib.load()
     dev = torch.device("cuda", 0)
@@ -33,7 +34,7 @@ def main():
         B, N, splits = map(int, c.split(",")[:3])
         S = vi.attn_num_splits(B, 8, N, splits)
         nct = vi.attn_num_ctas(B, 8, N, splits)
-        buf = torch.zeros(nct * 16, dtype=torch.int64, device=dev)
+        buf = torch.zeros(nct * 32, dtype=torch.int64, device=dev)
         lib.vecinfer_debug_set_phase_buffer.argtypes = [ctypes.c_void_p]
         lib.vecinfer_debug_set_phase_buffer(ctypes.c_void_p(buf.data_ptr()))
         kc = synth.gen_codes_torch((B, 8, N, 32), 8, seed=1, device=dev)
@@ -45,9 +46,12 @@ def main():
             buf.zero_()
             vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, workspace=ws)
             torch.cuda.synchronize()
-        t = buf.view(nct, 16).cpu().numpy().astype(np.float64)
+        both = buf.view(nct, 32).cpu().numpy().astype(np.float64)
+        t, cyc = both[:, :16], both[:, 16:]
         t0 = t[:, 0].min()
-        rel = (t - t0) / 1e3
+        # within a CTA: SM cycles at the sampled clock (fine); the CTA's start: globaltimer (coarse)
+        mhz = args.sm_mhz
+        rel = np.where(t == 0, 0.0, (t[:, :1] - t0) / 1e3 + (cyc - cyc[:, :1]) / mhz)
         span = (t[:, 4].max() - t0) / 1e3
         print(f"B={B} N={N} S={S} CTAs={nct}: span {span:.2f} us")
 
@@ -75,7 +79,9 @@ def main():
             st(rel[:, 2] - rel[:, 1], "main loop warp 0 (incl. bq)")
             st(rel[:, 3] - rel[:, 2], "warp partials -> smem + sync")
             st(rel[:, 8] - rel[:, 3], "combine + publish")
-            st(rel[:, 5] - rel[:, 8], "poll + stage (wait for splits)")
+            st(rel[:, 10] - rel[:, 8], "merge loads + poll (all seen)")
+            st(rel[:, 5] - rel[:, 10], "fold + output store")
+            st(rel[:, 8], "publish done (rel)")
             st(rel[:, 4] - rel[:, 5], "slice merge")
         st(rel[:, 4], "CTA end (rel)")
 
