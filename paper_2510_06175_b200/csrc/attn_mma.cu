@@ -67,7 +67,9 @@ constexpr int smem_layout_bytes(int kf, int vf) {
   const int nsep = (sep_tab(kf) ? 1 : 0) + (sep_tab(vf) ? 1 : 0);
   if (classic_tab(kf) || classic_tab(vf)) return kSmemBytes + nsep * kSepTab;
   if (nsep) return ((kMiscBytes + 1023) & ~1023) + nsep * kSepTab + kCbufBytes + 1024;
-  return kSmemBytesNoTab;
+  // no shared table (16-bit K and V: the books are gathered through L1/L2): no cluster buffer either
+  // (the planner never clusters these), so the smallest carveout leaves the L1 the most capacity
+  return kMiscBytes + 1024;
 }
 static_assert(smem_layout_bytes(kFmtD8B12, kFmtD8B8) <= 232448, "largest layout exceeds 227 KiB");
 
@@ -925,6 +927,8 @@ static AttnKernel kernel_for(int kf, int vf, int dh = 128) {
 
 static void set_attr(AttnKernel k, int smem) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // carveout = the smallest that fits: the rest of the 256 KiB stays L1 (16-bit books live there)
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxL1);
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
