@@ -558,16 +558,25 @@ def run_ours(args, rank, world, local_rank):
     achieved = code_bytes_rank / (attn_avg_ms / 1e3) / 1e9
     # the binding on-chip resource: the L1/shared LSU data pipe, one wavefront
     # per clock per SM; wavefronts per unit (shared gathers + global code loads) from the ncu capture
+    # per-unit cost of the main loop from the steady-state capture (18 x 8 units of 65536 tokens, one
+    # split: fixed per-launch work amortised away); the launch's own capture adds its fixed costs
+    # (table fill, combine, merge polls) and is reported beside it
     lsu = None
-    if ncu is not None and "lsu_wavefronts_per_unit" in ncu:
+    sp = os.path.join(ROOT, "profiles", "r02", "attn_steady_ncu.json")
+    if kbits == 8 and vbits == 8 and os.path.exists(sp):
+        with open(sp) as f:
+            steady = json.load(f)
         sm_hz = (clk.summary()["sm_mhz"] or 1965.0) * 1e6
         n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        w = ncu["lsu_wavefronts_per_unit"]
+        w = steady["lsu_wavefronts_per_unit"]
         bound = n_sms * sm_hz / w * unit_bytes / 1e9
-        lsu = {"wavefronts_per_unit": w, "shared_per_unit": ncu["lsu_shared_wavefronts_per_unit"],
-               "global_per_unit": ncu["lsu_global_wavefronts_per_unit"], "bound_gbs": bound,
-               "frac": achieved / bound, "capture": ncu["file"],
-               "note": "LSU-bound ceiling = #SMs x SM clock x 1 wavefront/clk / wavefronts per unit x bytes per unit"}
+        lsu = {"wavefronts_per_unit": w, "shared_per_unit": steady["lsu_shared_wavefronts_per_unit"],
+               "global_per_unit": steady["lsu_global_wavefronts_per_unit"], "bound_gbs": bound,
+               "frac": achieved / bound, "steady_capture": os.path.relpath(sp, ROOT),
+               "launch_wavefronts_per_unit": ncu.get("lsu_wavefronts_per_unit") if ncu else None,
+               "launch_lsu_pipe_pct": ncu.get("lsu_pipe_pct") if ncu else None,
+               "note": "LSU data-pipe ceiling = #SMs x SM clock x 1 wavefront/clk / main-loop wavefronts per unit "
+                       "x bytes per unit (DESIGN.md section 5)"}
     gather = None
     if kbits == 16 and vbits == 16:   # b4d4: the codebook gathers run through L1/L2 (scripts/ubench_gather16.cu)
         clk_per_unit = 59.0           # measured gather bound, profiles/r02/ubench_gather16_b4d4.txt
