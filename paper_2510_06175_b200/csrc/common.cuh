@@ -366,6 +366,11 @@ __device__ __forceinline__ void phase_mark(unsigned long long* buf, int cta, int
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
     buf[cta * 32 + slot] = t;        // 16 slots per CTA: globaltimer (ns, coarse, comparable across SMs)
     buf[cta * 32 + 16 + slot] = c;   // and the SM cycle counter (fine, within the CTA)
+    if (slot == 0) {                 // slot 15: the SM the CTA runs on
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      buf[cta * 32 + 15] = sm;
+    }
   }
 }
 #else

@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", action="append", required=True)
     ap.add_argument("--sm-mhz", type=float, default=1965.0, help="SM clock converting the cycle stamps")
+    ap.add_argument("--per-cta", action="store_true")
     args = ap.parse_args()
     lib = _lib.load()
     dev = torch.device("cuda", 0)
@@ -84,6 +85,17 @@ def main():
             st(rel[:, 8], "publish done (rel)")
             st(rel[:, 4] - rel[:, 5], "slice merge")
         st(rel[:, 4], "CTA end (rel)")
+        if args.per_cta:   # per-CTA main loop vs SM id (is the spread systematic?)
+            sm = both[:, 15].astype(int)
+            ml = rel[:, 2] - rel[:, 1]
+            order = np.argsort(ml)
+            print("   slowest CTAs (cta, sm, main loop us):", [(int(i), int(sm[i]), round(float(ml[i]), 2)) for i in order[-8:]])
+            print("   fastest CTAs (cta, sm, main loop us):", [(int(i), int(sm[i]), round(float(ml[i]), 2)) for i in order[:8]])
+            # per GPC-ish groups: SM id // 18
+            for g in range(0, 148, 37):
+                sel = (sm >= g) & (sm < g + 37)
+                if sel.any():
+                    print(f"   SMs {g:3d}-{g + 36:3d}: main loop mean {ml[sel].mean():.2f} us over {sel.sum()} CTAs")
 
 if __name__ == "__main__":
     main()
