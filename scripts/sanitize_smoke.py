@@ -36,9 +36,58 @@ for name, cfg in (("b1d4", vi.B1D4), ("b2d4", vi.B2D4), ("b4d4", vi.B4D4)):
                    seq + 1, kcfg=cfg, vcfg=cfg)
     vi.decode_step(q, kn, vn, lam, inv, ck, cv, kc, vc, torch.tensor([N, N // 3], dtype=torch.int32, device=dev),
                    seq + 1, kcfg=cfg, vcfg=cfg, algo="stream")
+# ---- round-2 paths
 ck = T(synth.bf16_from_bits(z["ck_b2d4"])).to(torch.bfloat16)
-vi.attn_decode(q, lam, ck, ck, kc[..., :32].contiguous() if kc.shape[-1] >= 32 else kc, vc[..., :32].contiguous(),
-               seq, algo="lut") if False else None
+cv = T(synth.bf16_from_bits(z["cv_b2d4"])).to(torch.bfloat16)
+B, N = 3, 700
+kc = synth.gen_codes_torch((B, 8, N + 40, 32), 8, seed=11, device=dev)
+vc = synth.gen_codes_torch((B, 8, N + 40, 32), 8, seed=12, device=dev)
+q = T(synth.gen_queries(B, 32, 8, 128, seed=13)).to(torch.bfloat16)
+seq = torch.tensor([N, 333, 31], dtype=torch.int32, device=dev)
+kn = T(synth.gen_keys(1, 8, 128, seed=14, batch=B)[:, 0]).to(torch.bfloat16)
+vn = T(synth.gen_values(1, 8, 128, seed=15, batch=B)[:, 0]).to(torch.bfloat16)
+wp = seq - 1
+# tcgen05 score path (split / multi-wave persistent / fused append)
+for splits in (0, 3, 60):
+    vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, algo="tc")
+vi.decode_step(q, kn, vn, lam, inv, ck, cv, kc, vc, wp, seq, algo="tc")
+# paged stream kernel (16-token sub-tiles across pages) + paged fused append
+ps = 32
+npb = (N + 40 + ps - 1) // ps
+pool_k = synth.gen_codes_torch((B * npb + 2, 8, ps, 32), 8, seed=16, device=dev)
+pool_v = synth.gen_codes_torch((B * npb + 2, 8, ps, 32), 8, seed=17, device=dev)
+bt = torch.randperm(B * npb + 2, device=dev)[:B * npb].view(B, npb).to(torch.int32)
+for splits in (0, 3, 60):
+    vi.attn_decode(q, lam, ck, cv, pool_k, pool_v, seq, num_splits=splits, algo="stream", block_table=bt)
+vi.decode_step(q, kn, vn, lam, inv, ck, cv, pool_k, pool_v, wp, seq, algo="stream", block_table=bt)
+# head_dim 64: residual window + fused append
+c64 = vi.VQConfig(64, 4, 8)
+kc64 = synth.gen_codes_torch((B, 8, N + 40, 16), 8, seed=18, device=dev)
+vc64 = synth.gen_codes_torch((B, 8, N + 40, 16), 8, seed=19, device=dev)
+q64 = T(synth.gen_queries(B, 32, 8, 64, seed=20)).to(torch.bfloat16)
+kr = T(synth.gen_keys(64, 8, 64, seed=21, batch=B).transpose(0, 2, 1, 3)).to(torch.bfloat16)
+vr = T(synth.gen_values(64, 8, 64, seed=22, batch=B).transpose(0, 2, 1, 3)).to(torch.bfloat16)
+rl = torch.tensor([64, 9, 1], dtype=torch.int32, device=dev)
+lam64, inv64 = lam[:, :64].contiguous(), inv[:, :64].contiguous()
+vi.attn_decode(q64, lam64, ck, cv, kc64, vc64, seq, kcfg=c64, vcfg=c64, k_res=kr, v_res=vr, res_lens=rl)
+kn64, vn64 = kn[..., :64].contiguous(), vn[..., :64].contiguous()
+vi.decode_step(q64, kn64, vn64, lam64, inv64, ck, cv, kc64, vc64, wp, seq, kcfg=c64, vcfg=c64)
+# NEXT-2: separate shared tables (d8b12, d4b10), fused generic append (d4b10, d2b8), d8b16
+z2 = np.load(os.path.join(ROOT, "data", "next2_codebooks.npz"))
+for name, cfg in (("d8b12", vi.D8B12), ("d4b10", vi.D4B10), ("d2b8", vi.D2B8)):
+    ckn = T(synth.bf16_from_bits(z2[f"ck_{name}"])).to(torch.bfloat16)
+    cvn = T(synth.bf16_from_bits(z2[f"cv_{name}"])).to(torch.bfloat16)
+    kcn = synth.gen_codes_torch((B, 8, N + 40, cfg.row_bytes), 8, seed=23, device=dev)
+    vcn = synth.gen_codes_torch((B, 8, N + 40, cfg.row_bytes), 8, seed=24, device=dev)
+    vi.attn_decode(q, lam, ckn, cvn, kcn, vcn, seq, kcfg=cfg, vcfg=cfg, num_splits=3)
+    vi.decode_step(q, kn, vn, lam, inv, ckn, cvn, kcn, vcn, wp, seq, kcfg=cfg, vcfg=cfg)
+zl = np.load(os.path.join(ROOT, "data", "d8b16_levels.npz"))
+ck16 = T(synth.product_codebook(synth.bf16_from_bits(zl["lv_d8b16_k"]))).to(torch.bfloat16)
+cv16 = T(synth.product_codebook(synth.bf16_from_bits(zl["lv_d8b16_v"]))).to(torch.bfloat16)
+kc16 = synth.gen_codes_torch((1, 8, 200, 32), 8, seed=25, device=dev)
+vc16 = synth.gen_codes_torch((1, 8, 200, 32), 8, seed=26, device=dev)
+vi.decode_step(q[:1], kn[:1], vn[:1], lam, inv, ck16, cv16, kc16, vc16, torch.tensor([150], dtype=torch.int32, device=dev),
+               torch.tensor([151], dtype=torch.int32, device=dev), kcfg=vi.D8B16, vcfg=vi.D8B16)
 vi.calibrate_smooth(T(synth.gen_calibration_keys(8, 128, n_samples=1, sample_len=64)).to(torch.bfloat16))
 vi.merge_lse(torch.randn(3, 2, 32, 128, device=dev), torch.randn(3, 2, 32, device=dev))
 # codebook k-means (assign / finalize / re-seed: four far centroids get no points)
