@@ -313,14 +313,30 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       constexpr bool paged = PG;
       int pgn0 = 0, pgn1 = 0;   // pages of the two sub-tiles of the next tile to load
       auto page_of = [&](int bb, int64_t tok) -> int { return a.bt[bb * a.bt_stride + (tok >> a.page_shift)]; };
-      auto load_paged = [&](const SegSh& sg, int64_t tstart, int p0, int p1, int rem) {
+      // this lane's K / V bytes of row 0 of page 0 of the piece's KV head (set by setup_piece):
+      // row (pg, t) of the head = pkb + (pg * Hc * page_size + t % page_size) * KR
+      const uint8_t* pkb = nullptr;
+      const uint8_t* pvb = nullptr;
+      auto load_paged = [&](int64_t tstart, int p0, int p1, int rem) {
         const int64_t pmask = (int64_t(1) << a.page_shift) - 1;
-        const int64_t row0 = ((static_cast<int64_t>(p0) * a.Hc + sg.hc) << a.page_shift) + (tstart & pmask);
-        const int64_t row1 = ((static_cast<int64_t>(p1) * a.Hc + sg.hc) << a.page_shift) + ((tstart + 16) & pmask);
-        load_subtile<KB, VB, 0>(nxt, a.kcodes + (row0 + r) * KR + Fmt<KB>::kOffK * j,
-                                a.vcodes + (row0 + 2 * j) * VR + Fmt<VB>::kOffV * r, rem, r, j);
-        load_subtile<KB, VB, 1>(nxt, a.kcodes + (row1 + r) * KR + Fmt<KB>::kOffK * j,
-                                a.vcodes + (row1 + 2 * j) * VR + Fmt<VB>::kOffV * r, rem - 16, r, j);
+        const int64_t sk = static_cast<int64_t>(a.Hc) << a.page_shift;   // rows between page indices
+        const int64_t o0 = p0 * sk + (tstart & pmask);
+        if ((tstart & pmask) + 16 <= pmask) {   // both sub-tiles in page p0: one contiguous tile
+          if (rem >= 32) load_tile_full<KB, VB>(nxt, pkb + o0 * KR, pvb + o0 * VR);
+          else load_tile_tail<KB, VB>(nxt, pkb + o0 * KR, pvb + o0 * VR, rem, r, j);
+          return;
+        }
+        const int64_t o1 = p1 * sk + ((tstart + 16) & pmask);   // sub-tile 1 starts page p1
+        load_subtile<KB, VB, 0>(nxt, pkb + o0 * KR, pvb + o0 * VR, rem, r, j);
+        load_subtile<KB, VB, 1>(nxt, pkb + o1 * KR, pvb + o1 * VR, rem - 16, r, j);
+      };
+      // block-table entries of a tile starting at token t: its page, and the next page if its second
+      // sub-tile starts one (rem = tokens from t).  (Reusing the previous tile's entries and reading
+      // the table only at page starts was measured slower: the reads become conditional and chained.)
+      auto tile_pages = [&](int bb, int64_t t, int rem, int& p0, int& p1) {
+        const int64_t pmask = (int64_t(1) << a.page_shift) - 1;
+        p0 = rem > 0 ? page_of(bb, t) : 0;
+        p1 = (rem > 16 && (t & pmask) + 16 > pmask) ? page_of(bb, t + 16) : p0;
       };
       // sets up piece `seg` of this warp and issues its first tile loads
       auto setup_piece = [&]() {
@@ -346,11 +362,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           }
         }
         if constexpr (paged) {
-          const int p0 = ntok > 0 ? page_of(sg.b, tok0) : 0;
-          const int p1 = ntok > 16 ? page_of(sg.b, tok0 + 16) : 0;
-          if (ntile > 0) load_paged(sg, tok0, p0, p1, ntok);
-          pgn0 = ntok > 32 ? page_of(sg.b, tok0 + 32) : 0;
-          pgn1 = ntok > 48 ? page_of(sg.b, tok0 + 48) : 0;
+          pkb = a.kcodes + ((static_cast<int64_t>(sg.hc) << a.page_shift) + r) * KR + Fmt<KB>::kOffK * j;
+          pvb = a.vcodes + ((static_cast<int64_t>(sg.hc) << a.page_shift) + 2 * j) * VR + Fmt<VB>::kOffV * r;
+          int p0, p1;
+          tile_pages(sg.b, tok0, ntok, p0, p1);
+          if (ntile > 0) load_paged(tok0, p0, p1, ntok);
+          tile_pages(sg.b, tok0 + 32, ntok - 32, pgn0, pgn1);
         } else if (ntile > 0) {
           load_tile_tail(nxt, kp, vp, ntok, r, j);   // (predicated: one code path)
         }
@@ -580,11 +597,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           if (it + 1 < ntile) {
             const int rem = rem_cur - 32;
             if constexpr (paged) {
-              const SegSh& sgp = segs[seg];
               const int64_t tn = tok0 + 32 * static_cast<int64_t>(it + 1);
-              load_paged(sgp, tn, pgn0, pgn1, rem);
-              pgn0 = rem > 32 ? page_of(sgp.b, tn + 32) : 0;
-              pgn1 = rem > 48 ? page_of(sgp.b, tn + 48) : 0;
+              load_paged(tn, pgn0, pgn1, rem);
+              tile_pages(segs[seg].b, tn + 32, rem - 32, pgn0, pgn1);
             } else {
               kp += 32 * KR;
               vp += 32 * VR;
