@@ -22,7 +22,8 @@
  *  - Supported shapes (ABI v5): head_dim D in {128, 64}, sub_dim d = 4, code_bits in {4, 8, 16}
  *    (b1d4, b2d4, b4d4 in BASELINE.json notation = paper d4b4, d4b8, d4b16), K and V
  *    widths independent; GQA group G = H_q / H_kv in 1..8; contiguous or paged code caches.
- *    D = 64 runs the split attention kernel only (no residual window, no fused append).
+ *    D = 64: split kernel (residual window, fused append) and, for batch decode without those,
+ *    the stream kernel.
  *    The paper's other configurations, D = 128 only:
  *    d8b8 {128, 8, 8}, d8b12 {128, 8, 12}, d4b10 {128, 4, 10}, d2b8 {128, 2, 8}, d8b16
  *    {128, 8, 16} (Table 5's 2-bit row: 65 536 eight-dim centroids, 1 MiB bf16 per book);

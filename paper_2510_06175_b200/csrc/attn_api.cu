@@ -245,8 +245,10 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
                 "the pairs (f, f), (d4b10, d8b12), (d8b12, d8b8)");
   if (kcfg.head_dim != vcfg.head_dim) return fail(VECINFER_ERR_SHAPE, "attn_decode: K and V head_dim differ");
   const int D = kcfg.head_dim;
-  if (D == 64 && (algo == VECINFER_ATTN_LUT || algo == VECINFER_ATTN_DEQUANT_MMA_STREAM))
-    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: head_dim 64 runs the split DEQUANT_MMA kernel");
+  if (D == 64 && (algo == VECINFER_ATTN_LUT ||
+                  (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM && (res || app || pg))))
+    return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: head_dim 64 runs the stream kernel only without a residual "
+                "window, fused append or paging");
   if (algo == VECINFER_ATTN_LUT && (kcfg.code_bits != 8 || vcfg.code_bits != 8))
     return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode: the LUT variant is implemented for b2d4 only");
   if (tok_begin < 0 || (tok_end >= 0 && tok_end < tok_begin))
@@ -266,7 +268,9 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
     if (lut) return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_paged: paged caches run the DEQUANT_MMA kernels only");
     if (tok_begin % 32 != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode_paged: tok_begin must be a multiple of 32");
   }
-  const bool use_sk = !tc && !next2 && D == 128 && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
+  // stream partition: D = 128, or D = 64 without a residual window, fused append or paging (those
+  // run the split kernel's persistent grid)
+  const bool use_sk = !tc && !next2 && (D == 128 || (!res && !app && !pg)) && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
   SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
   if (D == 64) plan.cluster = 0;   // the DSMEM cluster merge is written for 128-dim rows
   if (kcfg.code_bits == 16 && vcfg.code_bits == 16 && !next2) plan.cluster = 0;   // (no cluster buffer: L1 capacity)
@@ -420,8 +424,8 @@ static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t k
   if (!n2 && (kcfg.code_bits > 8 || vcfg.code_bits > 8)) return false;
   if (kcfg.head_dim != 128 && kcfg.head_dim != 64) return false;
   const int64_t units = static_cast<int64_t>(B) * H_kv;
-  if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)
-    return num_splits == 0 || units * num_splits <= device_sm_count();   // persistent grids: separate append
+  if (algo == VECINFER_ATTN_DEQUANT_MMA_STREAM)   // (D = 64: the stream kernel has no fused append)
+    return kcfg.head_dim == 128 && (num_splits == 0 || units * num_splits <= device_sm_count());
   if (!n2 && algo != VECINFER_ATTN_DEQUANT_TC && kcfg.head_dim == 128 && use_stream(B, H_kv, n_cap, num_splits, false)) return true;
   const SplitPlan plan = plan_splits(B, H_kv, n_cap, num_splits);
   const int mac = plan.cluster ? attn_mma_max_active_clusters(plan.S) : 0;

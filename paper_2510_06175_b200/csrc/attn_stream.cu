@@ -138,12 +138,13 @@ __device__ __forceinline__ void compute_seg(const AttnArgs& a, int vc, int u, Se
 // thread (r, j) owns head j, dims 16r..16r+15 (float4 k = dims 16r+4k..16r+4k+3; the MMA slots
 // [t][0] + [t][1] hold dim 16r+2t, [t][2] + [t][3] dim 16r+2t+1).  Row stride 132 spreads the
 // 16-byte stores of the 32 lanes over all banks (4 wavefronts per store).
+template <int DH>
 __device__ __forceinline__ void store_state(float* dacc, float* dm, float* dl, int r, int j, float m, float l,
-                                            const float (&acc)[8][4]) {
+                                            const float (&acc)[DH / 16][4]) {
   if (r == 0) { dm[j] = m; dl[j] = l; }
-  float* d = dacc + j * kWRow + 16 * r;
+  float* d = dacc + j * kWRow + (DH / 8) * r;
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < DH / 32; ++k)
     *reinterpret_cast<float4*>(d + 4 * k) =
         make_float4(acc[2 * k][0] + acc[2 * k][1], acc[2 * k][2] + acc[2 * k][3],
                     acc[2 * k + 1][0] + acc[2 * k + 1][1], acc[2 * k + 1][2] + acc[2 * k + 1][3]);
@@ -153,7 +154,7 @@ __device__ __forceinline__ void store_state(float* dacc, float* dm, float* dl, i
 // element (b, h, g, dim), combined in slot order by log-sum-exp (Alg. 1 l.729-730) and consumed
 // (zeroed) for the next launch.  Chunks of 8 loads in flight.
 __device__ __noinline__ void merge_consume(const AttnArgs& a, unsigned long long* part, int b, int hq0, int g, int dim,
-                                           int64_t slot0, int P) {
+                                           int64_t slot0, int P, int dh) {
   unsigned long long* pp = part + (slot0 * 4 + g) * 128 + dim;
   float m = -INFINITY, wsum = 0.f, osum = 0.f;
   for (int s0 = 0; s0 < P; s0 += 8) {
@@ -186,17 +187,23 @@ __device__ __noinline__ void merge_consume(const AttnArgs& a, unsigned long long
   }
   const bool empty = !(wsum > 0.f);
   const float ov = empty ? 0.f : osum / wsum;
-  const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hq0 + g) * 128 + dim;
+  const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hq0 + g) * dh + dim;
   if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
   else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
   if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(b) * a.Hq + hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
 }
 
-// PG: paged code caches (a separate instantiation: the translation must not cost the contiguous path)
-template <int KB, int VB, bool PG>
+// PG: paged code caches (a separate instantiation: the translation must not cost the contiguous path).
+// DH: head dim 128, or 64 (NEXT-4; contiguous, no residual window, no fused append: the host routes
+// those to the split kernel).  Published partials keep 128-float rows per head either way.
+template <int KB, int VB, bool PG, int DH>
 __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_constant__ AttnArgs a) {
-  constexpr int KR = Fmt<KB>::kRow, VR = Fmt<VB>::kRow;
-  constexpr bool kCanAppend = KB <= 8 && VB <= 8;
+  static_assert(DH == 128 || (DH == 64 && !PG), "D = 64: contiguous caches");
+  using FK = FmtD<KB, DH>;
+  using FV = FmtD<VB, DH>;
+  constexpr int KR = FK::kRow, VR = FV::kRow;
+  constexpr int KS = DH / 16, VS = DH / 32, NL = DH / 4, NO = 4 * DH;   // k-steps, V m-tile pairs, q lanes, outputs
+  constexpr bool kCanAppend = KB <= 8 && VB <= 8 && DH == 128;
   constexpr bool kTable = Fmt<KB>::kSmem || Fmt<VB>::kSmem;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -253,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       const int qseg = (warp - 8) >> 2, qg = warp & 3;   // warps 8..11: heads of segment A, 12..15: of B
       const bool qwarp = warp >= 8 && warp < 8 + 4 * nseg;
       float4 lam4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (qwarp) lam4 = *reinterpret_cast<const float4*>(a.lambda + (qseg ? hmB.hc : hmA.hc) * 128 + 4 * lane);
+      if (qwarp) lam4 = *reinterpret_cast<const float4*>(a.lambda + (qseg ? hmB.hc : hmA.hc) * DH + 4 * (lane & (NL - 1)));
       const int q_gp = qseg ? hmB.gp : hmA.gp;
       if (first) griddep_wait();
       first = false;
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       uint2 qw = make_uint2(0u, 0u);
       if (qwarp && qg < q_gp) {
         const int bq = qseg && hB == 0 ? bA + 1 : bA, hq0 = qseg ? hmB.hq0 : hmA.hq0;
-        qw = *reinterpret_cast<const uint2*>(a.q + bq * a.q_sb + (hq0 + qg) * a.q_sh + 4 * lane);
+        qw = *reinterpret_cast<const uint2*>(a.q + bq * a.q_sb + (hq0 + qg) * a.q_sh + 4 * (lane & (NL - 1)));
       }
       // ---- segments and warp assignment: the round's 16-token sub-tiles (A's, then B's) go to
       // the warps in contiguous balanced ranges [w*ns/16, (w+1)*ns/16); segment A = warps
@@ -351,8 +358,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         ntok = static_cast<int>(max(int64_t(0), min(tend, static_cast<int64_t>(sg.t1)) - tok0));
         ntile = (ntok + 31) >> 5;
         const int64_t unit = sg.cu;   // cache unit of the codes
-        kp = a.kcodes + (unit * a.n_cap + tok0 + r) * KR + Fmt<KB>::kOffK * j;
-        vp = a.vcodes + (unit * a.n_cap + tok0 + 2 * j) * VR + Fmt<VB>::kOffV * r;
+        kp = a.kcodes + (unit * a.n_cap + tok0 + r) * KR + FK::kOffK * j;
+        vp = a.vcodes + (unit * a.n_cap + tok0 + 2 * j) * VR + FV::kOffV * r;
         patch_tile = -1;
         if (kCanAppend && sg.patch) {
           const int64_t rel = sg.p_row - tok0;
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           if (ntile > 0) load_paged(tok0, p0, p1, ntok);
           tile_pages(sg.b, tok0 + 32, ntok - 32, pgn0, pgn1);
         } else if (ntile > 0) {
-          load_tile_tail(nxt, kp, vp, ntok, r, j);   // (predicated: one code path)
+          load_tile_tail<KB, VB, DH>(nxt, kp, vp, ntok, r, j);   // (predicated: one code path)
         }
         // residual rows of the unit: row t belongs to piece t % P, and within the piece's warps
         // (rank rho of nw) to rows t = k + P * (rho + nw * i)
@@ -386,8 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       // ---- query transform (Eq. 7): sq[seg][g] = ((q_g * lambda) H) * qscale
       if (qwarp) {
         float* dq = sq + kQSeg * qseg + kQRow * qg + qoff(lane);
-        if (qg < q_gp) qtransform_lane(qw, lam4, a.qscale, lane, dq);
-        else *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (qg < q_gp) qtransform_lane(qw, lam4, a.qscale, lane, dq, NL);
+        else if (lane < NL) *reinterpret_cast<float4*>(dq) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
 
       if (ua == u_first) phase_mark(a.phase, vc, 11);
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       if (ua == u_first) phase_mark(a.phase, vc, 1);
 
       // ---- main loop over this warp's pieces (<= 2)
-      float acc[8][4];
+      float acc[2 * VS][4];
       float m_run = -INFINITY, l_run = 0.f;
 #pragma unroll 1
       for (int wp = 0; wp < np; ++wp) {
@@ -471,14 +478,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           l_run += __shfl_xor_sync(0xffffffffu, l_run, 4);
           l_run += __shfl_xor_sync(0xffffffffu, l_run, 8);
           l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);
-          store_state(wacc + (kSlots - 1) * 4 * kWRow, wm + (kSlots - 1) * 4, wl + (kSlots - 1) * 4, r, j, m_run, l_run, acc);
+          store_state<DH>(wacc + (kSlots - 1) * 4 * kWRow, wm + (kSlots - 1) * 4, wl + (kSlots - 1) * 4, r, j, m_run, l_run, acc);
           seg = 1;
           setup_piece();
         }
         m_run = -INFINITY;
         l_run = 0.f;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+        for (int t = 0; t < 2 * VS; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
         const uint16_t* cbk = seg ? cbkB : cbkA;
         const uint16_t* cbv = seg ? cbvB : cbvA;
         const uint32_t kbase = tab_s + ((seg && !rsh->sameB) ? kTab : 0) + (lane & 15) * 8;
@@ -486,13 +493,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
 
         // B fragments of the score MMA: column n = lane/4 <-> (head n/2, part n%2); rows k
         // <-> sub-vector 8j+t, components {0,1} (b0) and {2,3} (b1)
-        uint32_t bq0[8], bq1[8];
+        uint32_t bq0[KS], bq1[KS];
         {
           const int gq = r >> 1, part = r & 1;
           const float* sqs = sq + kQSeg * seg + kQRow * gq;
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const float4 v = *reinterpret_cast<const float4*>(sqs + qoff(8 * j + t));
+          for (int t = 0; t < KS; ++t) {
+            const float4 v = *reinterpret_cast<const float4*>(sqs + qoff(KS * j + t));
             const float in[4] = {v.x, v.y, v.z, v.w};
             float o[4];
 #pragma unroll
@@ -509,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         // Eq. 7), folded into this warp's online-softmax state before the code tiles; the P.V
         // goes into the hi slots of the MMA accumulator layout (thread (r, j) owns head j, dims
         // 16r + 2t + {0, 1})
-        if (t_res < rlen) {
+        if constexpr (DH == 128) if (t_res < rlen) {
           const SegSh& sgr = segs[seg];
           const int bb = sgr.b, hh = sgr.hc;
           float qr[4][4];
@@ -603,8 +610,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
             } else {
               kp += 32 * KR;
               vp += 32 * VR;
-              if (rem >= 32) load_tile_full(nxt, kp, vp);
-              else load_tile_tail(nxt, kp, vp, rem, r, j);
+              if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
+              else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
             }
           }
           // tile body, specialised on whether sub-tile 1 holds tokens (a trailing half tile skips it);
@@ -623,11 +630,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
                 }
               }
               float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-              static_for<0, 8>([&](auto T) {
+              static_for<0, KS>([&](auto T) {
                 constexpr int t = decltype(T)::value;
                 const uint2 ea = gather_k<KB, t>(cur.k[q][0], kbase, cbk);
                 const uint2 eb = gather_k<KB, t>(cur.k[q][1], kbase, cbk);
-                if (t < 4) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
+                if (t < KS / 2) mma_16816(d0, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
                 else mma_16816(d1, ea.x, eb.x, ea.y, eb.y, bq0[t], bq1[t]);
               });
               sc[q][0] = (d0[0] + d1[0]) + (d0[1] + d1[1]);
@@ -653,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
               const float m_new = need ? mx : m_run;
               const float alpha = need ? ex2_approx(m_run - m_new) : 1.f;  // 0 when m_run was -inf
 #pragma unroll
-              for (int t = 0; t < 8; ++t) {
+              for (int t = 0; t < 2 * VS; ++t) {
                 acc[t][0] *= alpha; acc[t][1] *= alpha; acc[t][2] *= alpha; acc[t][3] *= alpha;
               }
               l_run *= alpha;
@@ -679,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
               const uint32_t bp1 = movmatrix_trans(prmt(hb, lb, 0x7632));  // (hi, lo) of token r + 8
 
               // ---- P.V (Alg. 1 l.16): m-tile t <-> sub-vector 4r + t/2, components 2(t%2) + {0,1}
-              static_for<0, 4>([&](auto Uc) {
+              static_for<0, VS>([&](auto Uc) {
                 constexpr int u = decltype(Uc)::value;
                 const uint2 g0 = gather_v<VB, u>(cur.v[q][0], vbase, cbv);
                 const uint2 g1 = gather_v<VB, u>(cur.v[q][1], vbase, cbv);
@@ -705,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       l_run += __shfl_xor_sync(0xffffffffu, l_run, 4);
       l_run += __shfl_xor_sync(0xffffffffu, l_run, 8);
       l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);
-      if (np > 0) store_state(wacc + warp * 4 * kWRow, wm + warp * 4, wl + warp * 4, r, j, m_run, l_run, acc);
+      if (np > 0) store_state<DH>(wacc + warp * 4 * kWRow, wm + warp * 4, wl + warp * 4, r, j, m_run, l_run, acc);
       const bool last_round = ua + 2 > u_last && vc + static_cast<int>(gridDim.x) >= a.V;
       if (ua + 2 > u_last) phase_mark(a.phase, vc, 2);
       if (last_round) griddep_launch_dependents();   // the next kernel may start its static prologue
@@ -747,8 +754,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       }
       __syncthreads();
 #pragma unroll 1
-      for (int idx = tid; idx < nseg * 512; idx += kThreads) {
-        const int sgi = idx >> 9, g = (idx >> 7) & 3, dim = idx & 127;
+      for (int idx = tid; idx < nseg * NO; idx += kThreads) {
+        const int sgi = idx / NO, g = (idx / DH) & 3, dim = idx % DH;
         const int w_lo = sgi == 0 ? 0 : b0, w_hi = sgi == 0 ? nwA : kNW;
         const int xs = sgi == 0 ? strad : -1;   // the straddler's A piece lives in slot 16
         const float M = sMx[sgi * 4 + g];
@@ -768,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         const SegSh& sg = segs[sgi];
         if (sg.P == 1) {
           if (g < sg.gp) {
-            const int64_t oi = (static_cast<int64_t>(sg.b) * a.Hq + sg.hq0 + g) * 128 + dim;
+            const int64_t oi = (static_cast<int64_t>(sg.b) * a.Hq + sg.hq0 + g) * DH + dim;
             if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
             else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
             if (dim == 0 && a.lse) a.lse[static_cast<int64_t>(sg.b) * a.Hq + sg.hq0 + g] = L2 * kLn2;
@@ -803,8 +810,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           if (!sflag[sgi]) continue;
           const SegSh& sg = segs[sgi];
           const int64_t c1 = div_fix(static_cast<int64_t>(sg.u) * a.V, a.U, a.rcpU);
-          const int g = tid >> 7, dim = tid & 127;
-          if (g < sg.gp) merge_consume(a, part, sg.b, sg.hq0, g, dim, c1 + sg.u, sg.P);
+          const int g = tid / DH, dim = tid % DH;
+          if (tid < NO && g < sg.gp) merge_consume(a, part, sg.b, sg.hq0, g, dim, c1 + sg.u, sg.P, DH);
         }
       }
       if (ua + 2 > u_last) phase_mark(a.phase, vc, 3);
@@ -824,8 +831,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       int E[2] = {0, 0}, nout[2] = {0, 0}, per[2] = {0, 0};
       for (int i = 0; i < nrec; ++i) {
         const int* rec = sflag + 4 + 4 * i;
-        per[i] = (512 + rec[2] - 1) / rec[2];
-        nout[i] = max(0, min(512, (rec[1] + 1) * per[i]) - rec[1] * per[i]);
+        per[i] = (NO + rec[2] - 1) / rec[2];
+        nout[i] = max(0, min(NO, (rec[1] + 1) * per[i]) - rec[1] * per[i]);
         E[i] = nout[i] * rec[2];
       }
 #pragma unroll 1
@@ -834,12 +841,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         const int* rec = sflag + 4 + 4 * i;
         const int u = rec[0], k = rec[1], P = rec[2];
         const int oo = ee / P, p = ee - oo * P;
-        const int o = k * per[i] + oo;   // g * 128 + dim
+        const int o = k * per[i] + oo;   // g * DH + dim
         float2 v = make_float2(0.f, -INFINITY);
         const int bu = div_small(u, a.Hkv);
-        if ((o >> 7) < head_map(a, u - bu * a.Hkv).gp) {
+        if (o / DH < head_map(a, u - bu * a.Hkv).gp) {
           const int64_t c1 = div_fix(static_cast<int64_t>(u) * a.V, a.U, a.rcpU);
-          unsigned long long* pp = part + (c1 + u + p) * 512 + o;
+          unsigned long long* pp = part + (c1 + u + p) * 512 + (o / DH) * 128 + o % DH;
           unsigned long long w;
           while ((w = ld_relaxed_gpu_u64(pp)) == 0ull) if (VECINFER_SPIN_NS > 0) __nanosleep(VECINFER_SPIN_NS);
           st_relaxed_gpu_u64(pp, 0ull);
@@ -855,7 +862,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         const int i = t < nout[0] ? 0 : 1, tt = t - (i ? nout[0] : 0);
         const int* rec = sflag + 4 + 4 * i;
         const int u = rec[0], k = rec[1], P = rec[2];
-        const int o = k * per[i] + tt, g = o >> 7, dim = o & 127;
+        const int o = k * per[i] + tt, g = o / DH, dim = o % DH;
         const int b = div_small(u, a.Hkv);
         const HeadMap hmu = head_map(a, u - b * a.Hkv);
         if (g >= hmu.gp) continue;
@@ -871,7 +878,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           }
         }
         const bool empty = !(wsum > 0.f);
-        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hmu.hq0 + g) * 128 + dim;
+        const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hmu.hq0 + g) * DH + dim;
         const float ov = empty ? 0.f : osum * __frcp_rn(wsum);
         if (a.o_f32) static_cast<float*>(a.o)[oi] = ov;
         else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
@@ -889,25 +896,29 @@ using AttnKernel = void (*)(const AttnArgs);
 
 static int smem_for(int kb, int vb) { return (kb > 8 && vb > 8) ? kSmemBytesNoTab : kSmemBytes; }
 
-static AttnKernel kernel_for(int kb, int vb, bool paged = false) {
+static AttnKernel kernel_for(int kb, int vb, bool paged = false, int dh = 128) {
   const int ki = kb == 4 ? 0 : kb == 8 ? 1 : 2, vi = vb == 4 ? 0 : vb == 8 ? 1 : 2;
-  static const AttnKernel table[2][3][3] = {
-      {{attn_stream_kernel<4, 4, false>, attn_stream_kernel<4, 8, false>, attn_stream_kernel<4, 16, false>},
-       {attn_stream_kernel<8, 4, false>, attn_stream_kernel<8, 8, false>, attn_stream_kernel<8, 16, false>},
-       {attn_stream_kernel<16, 4, false>, attn_stream_kernel<16, 8, false>, attn_stream_kernel<16, 16, false>}},
-      {{attn_stream_kernel<4, 4, true>, attn_stream_kernel<4, 8, true>, attn_stream_kernel<4, 16, true>},
-       {attn_stream_kernel<8, 4, true>, attn_stream_kernel<8, 8, true>, attn_stream_kernel<8, 16, true>},
-       {attn_stream_kernel<16, 4, true>, attn_stream_kernel<16, 8, true>, attn_stream_kernel<16, 16, true>}}};
-  return table[paged ? 1 : 0][ki][vi];
+  static const AttnKernel table[3][3][3] = {
+      {{attn_stream_kernel<4, 4, false, 128>, attn_stream_kernel<4, 8, false, 128>, attn_stream_kernel<4, 16, false, 128>},
+       {attn_stream_kernel<8, 4, false, 128>, attn_stream_kernel<8, 8, false, 128>, attn_stream_kernel<8, 16, false, 128>},
+       {attn_stream_kernel<16, 4, false, 128>, attn_stream_kernel<16, 8, false, 128>, attn_stream_kernel<16, 16, false, 128>}},
+      {{attn_stream_kernel<4, 4, true, 128>, attn_stream_kernel<4, 8, true, 128>, attn_stream_kernel<4, 16, true, 128>},
+       {attn_stream_kernel<8, 4, true, 128>, attn_stream_kernel<8, 8, true, 128>, attn_stream_kernel<8, 16, true, 128>},
+       {attn_stream_kernel<16, 4, true, 128>, attn_stream_kernel<16, 8, true, 128>, attn_stream_kernel<16, 16, true, 128>}},
+      {{attn_stream_kernel<4, 4, false, 64>, attn_stream_kernel<4, 8, false, 64>, attn_stream_kernel<4, 16, false, 64>},
+       {attn_stream_kernel<8, 4, false, 64>, attn_stream_kernel<8, 8, false, 64>, attn_stream_kernel<8, 16, false, 64>},
+       {attn_stream_kernel<16, 4, false, 64>, attn_stream_kernel<16, 8, false, 64>, attn_stream_kernel<16, 16, false, 64>}}};
+  return table[dh == 64 ? 2 : paged ? 1 : 0][ki][vi];
 }
 
 static void set_attrs_once() {
   static bool done = false;  // benign race: idempotent attributes
   if (!done) {
-    for (int pg : {0, 1})
+    for (int var : {0, 1, 2})
       for (int kb : {4, 8, 16})
         for (int vb : {4, 8, 16})
-          cudaFuncSetAttribute(kernel_for(kb, vb, pg), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(kb, vb));
+          cudaFuncSetAttribute(kernel_for(kb, vb, var == 1, var == 2 ? 64 : 128),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(kb, vb));
     done = true;
   }
 }
@@ -935,7 +946,7 @@ cudaError_t launch_attn_stream(const AttnArgs& a, int kbits, int vbits, cudaStre
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel_for(kbits, vbits, a.bt != nullptr), a);
+  return cudaLaunchKernelEx(&cfg, kernel_for(kbits, vbits, a.bt != nullptr, a.D), a);
 }
 
 }  // namespace vecinfer

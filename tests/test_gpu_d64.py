@@ -158,10 +158,34 @@ def test_d64_decode_step_appends_to_residual():
         res_lens=lens))
 
 
+@pytest.mark.parametrize("lens,splits", [([1, 17, 513], 0), ([4097, 0, 33], 0), ([2500, 2400, 2300], 3),
+                                         ([3000, 1000, 7], 40)])   # 40 x 24 units > #SMs: persistent
+def test_d64_stream_kernel(lens, splits):
+    """D = 64 through the stream partition (pieces cut at 16-token boundaries, straddling warps,
+    spin and last-arriver merges), bitwise reproducible, vs the oracle."""
+    c = _case(len(lens), 4, max(lens) + 3, lens, seed=690 + splits + len(lens))
+    o1, L1 = _run(c, algo="stream", num_splits=splits)
+    o2, L2 = _run(c, algo="stream", num_splits=splits)
+    assert np.array_equal(o1, o2) and np.array_equal(L1, L2)
+    _assert_close(o1, L1, *_ref(c))
+
+
+@pytest.mark.parametrize("G,bits", [(4, 8), (5, 8), (8, 4), (4, 16)])
+def test_d64_stream_auto_batch_decode(G, bits):
+    """B*H_kv >= #SMs: AUTO picks the stream kernel at D = 64 too (GQA 5 / 8: two virtual heads)."""
+    B = 20
+    lens = [300 + 37 * b for b in range(B)]
+    c = _case(B, G, max(lens) + 1, lens, seed=700 + G + bits, bits=bits)
+    assert vi.attn_kernel_kind(B, 8 * (2 if G > 4 else 1), max(lens) + 1) == "stream"
+    o, L = _run(c)
+    _assert_close(o, L, *_ref(c))
+
+
 def test_d64_unsupported_paths_fail_loudly():
     c = _case(1, 4, 256, [256], seed=650)
-    with pytest.raises(VecInferError):
-        _run(c, algo="stream")
+    kr = torch.zeros(1, 8, 16, D, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(VecInferError):   # the D = 64 stream kernel has no residual window
+        _run(c, algo="stream", k_res=kr, v_res=kr, res_lens=t_i32([4]))
     with pytest.raises(VecInferError):
         _run(c, algo="lut")
     with pytest.raises(VecInferError):   # K and V head dims must agree
