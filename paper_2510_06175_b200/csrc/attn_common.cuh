@@ -112,10 +112,9 @@ __device__ __forceinline__ int64_t div_fix(int64_t x, int64_t d, double rcp) {
   return q;
 }
 
-// Token range [r0, r1) of split s for (b, h) within the attended range [beg, e).
-__device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int64_t& r0, int64_t& r1,
-                                            int64_t* pbeg = nullptr, int64_t* pend = nullptr) {
-  int64_t len = a.seq_lens[b];
+// Token range [r0, r1) of split s within the attended range [beg, e) of a sequence of len tokens.
+__device__ __forceinline__ void split_range_len(const AttnArgs& a, int64_t len, int s, int64_t& r0, int64_t& r1,
+                                                int64_t* pbeg = nullptr, int64_t* pend = nullptr) {
   if (len > a.n_cap) len = a.n_cap;
   if (len < 0) len = 0;
   int64_t e = a.tok_end < 0 ? len : (a.tok_end < len ? a.tok_end : len);
@@ -131,6 +130,10 @@ __device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int
   if (r0 > e) r0 = e;
   r1 = r0 + chunk;
   if (r1 > e) r1 = e;
+}
+__device__ __forceinline__ void split_range(const AttnArgs& a, int b, int s, int64_t& r0, int64_t& r1,
+                                            int64_t* pbeg = nullptr, int64_t* pend = nullptr) {
+  split_range_len(a, a.seq_lens[b], s, r0, r1, pbeg, pend);
 }
 
 // CTA epilogue shared by all kernels: combine per-warp (m, l, acc) partials held in shared
@@ -280,7 +283,7 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     const int o0 = s * per, nout = max(0, min(4 * DH, o0 + per) - o0);
     const int L = S >= 32 ? 32 : (1 << (31 - __clz(S)));
     const int groups = NTHREADS / L, lg = tid / L, ll = tid % L;
-    constexpr int kMaxPer = 8;   // splits per lane: S <= 256
+    constexpr int kMaxPer = 4;   // splits per lane: S <= 128 (kMaxSplits)
     for (int t0 = 0; t0 < nout; t0 += groups) {   // one pass unless S is tiny and DH... (uniform)
       const int t = t0 + lg;
       const int o = o0 + t, g = o / DH, dim = o % DH;
@@ -316,7 +319,11 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
         lv[k] = has ? __uint_as_float(static_cast<uint32_t>(v >> 32)) : -INFINITY;
         m = fmaxf(m, lv[k]);
       }
-      for (int off = 1; off < L; off <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {   // butterflies inside the L-lane group (L uniform)
+        const float o2 = __shfl_xor_sync(0xffffffffu, m, off);
+        if (off < L) m = fmaxf(m, o2);
+      }
       float wsum = 0.f, osum = 0.f;
       if (m != -INFINITY) {
 #pragma unroll
@@ -326,9 +333,14 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
           osum += f * xv[k];
         }
       }
-      for (int off = 1; off < L; off <<= 1) {
-        wsum += __shfl_xor_sync(0xffffffffu, wsum, off);
-        osum += __shfl_xor_sync(0xffffffffu, osum, off);
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const float a2 = __shfl_xor_sync(0xffffffffu, wsum, off);
+        const float b2 = __shfl_xor_sync(0xffffffffu, osum, off);
+        if (off < L) {
+          wsum += a2;
+          osum += b2;
+        }
       }
       if (act && ll == 0) {
         const bool empty = !(wsum > 0.f);

@@ -160,18 +160,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   const int hc = hm.hc;
   const uint16_t* cbk = a.ck + hc * a.ck_hs;
   const uint16_t* cbv = a.cv + hc * a.cv_hs;
-  const uint4 tabv = table_load<KB, VB>(cbk, cbv, tid);   // stored after the first tile's loads
+  const uint4 tabv = table_load<KB, VB>(cbk, cbv, tid);   // stored while seq_lens is in flight
   float4 lam4 = make_float4(0.f, 0.f, 0.f, 0.f);   // warps 0..3: lambda of head h (static)
   if (warp < 4) lam4 = *reinterpret_cast<const float4*>(a.lambda + hc * DH + 4 * (lane & (NL - 1)));
   if (first) griddep_wait();
+  phase_mark(a.phase, cta_id, 9);
   first = false;
   // q of the warp's query head goes out right after the wait, next to the seq_lens read below
   uint2 qw = make_uint2(0u, 0u);
   if (warp < hm.gp)
     qw = *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (hm.hq0 + warp) * a.q_sh + 4 * (lane & (NL - 1)));
 
+  // seq_lens goes out next; the codebook table (its loads were issued before the wait) is stored
+  // while it is in flight, then the split range and the first tile's loads follow
+  const int64_t len_b = a.seq_lens[b];
+  table_store<KB, VB>(tab, tabv, tid);
+  sep_fill<KB>(tab + kSepOff, cbk, tid, kThreads);     // NEXT-2 d8b12 / d4b10 books (no-ops otherwise)
+  sep_fill<VB>(tab + kSepVOff, cbv, tid, kThreads);
   int64_t r0, r1, beg, e;
-  split_range(a, b, s, r0, r1, &beg, &e);
+  split_range_len(a, len_b, s, r0, r1, &beg, &e);
   const int ntok = static_cast<int>(r1 - r0);
   const int ntile = (ntok + 31) >> 5;
   const int64_t unit = static_cast<int64_t>(b) * a.Hc + hc;   // cache unit of the codes
@@ -244,9 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
     else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
   }
-  table_store<KB, VB>(tab, tabv, tid);
-  sep_fill<KB>(tab + kSepOff, cbk, tid, kThreads);     // NEXT-2 d8b12 / d4b10 books (no-ops otherwise)
-  sep_fill<VB>(tab + kSepVOff, cbv, tid, kThreads);
+  phase_mark(a.phase, cta_id, 13);   // first tile issued (after seq_lens)
   unsigned char* newcodes = smem_raw + kMiscNew;   // [0,64): K code row, [64,128): V code row
   if (kCanAppend && owner) {
     // Eq. 9: encode the new token (S then H on the key, VQ on both), 8 warps per stream, each
@@ -417,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       tc::fence_proxy_async_smem();   // generic-proxy stores -> the tensor core reads them
     }
   }
+  phase_mark(a.phase, cta_id, 14);   // thread 0: table stored, q~ written (warp 0)
   if constexpr (TC) tc::fence_before();
   __syncthreads();
   if constexpr (TC) tc::fence_after();

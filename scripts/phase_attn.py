@@ -77,6 +77,10 @@ def main():
             st(rel[:, 4] - rel[:, 5], "slice merge")
         else:                                # split kernel (attn_mma.cu) stamps
             st(rel[:, 1] - rel[:, 0], "prologue (fill+q~+sync)")
+            st(rel[:, 9] - rel[:, 0], "  start -> after griddep wait")
+            st(rel[:, 13] - rel[:, 9], "  wait -> seq_lens, 1st tile issued")
+            st(rel[:, 14] - rel[:, 13], "  table store + q~ (warp 0)")
+            st(rel[:, 1] - rel[:, 14], "  barrier (slowest warp)")
             st(rel[:, 2] - rel[:, 1], "main loop warp 0 (incl. bq)")
             st(rel[:, 3] - rel[:, 2], "warp partials -> smem + sync")
             st(rel[:, 8] - rel[:, 3], "combine + publish")
