@@ -313,23 +313,51 @@ __device__ __forceinline__ void sep_fill(unsigned char* tab, const uint16_t* cb,
   }
 }
 
-// codebook table fill in two halves, so the codebook loads can be issued first and the shared
-// stores placed after the (dependent) first code-tile loads: thread t owns centroid j = t/2 of
-// C_k (t even) or C_v (t odd)
+// codebook table fill in two halves, so the codebook loads can be issued first (raw bf16 words,
+// before the grid-dependency wait) and converted + stored to shared memory later: thread t owns
+// centroid j = t/2 of C_k (t even) or C_v (t odd)
+template <int F>
+__device__ __forceinline__ uint4 table_raw(const uint16_t* cb, int j) {
+  if constexpr (F == kFmtD8B8) {
+    const uint2 lo = *reinterpret_cast<const uint2*>(cb + 8 * j), hi = *reinterpret_cast<const uint2*>(cb + 8 * j + 4);
+    return make_uint4(lo.x, lo.y, hi.x, hi.y);
+  } else if constexpr (F == kFmtD2B8) {
+    return make_uint4(*reinterpret_cast<const uint32_t*>(cb + 2 * j), 0u, 0u, 0u);
+  } else {
+    const uint2 w = *reinterpret_cast<const uint2*>(cb + 4 * j);
+    return make_uint4(w.x, w.y, 0u, 0u);
+  }
+}
+template <int F>
+__device__ __forceinline__ uint4 table_cvt(const uint4 raw) {   // raw bf16 words -> the store pattern
+  if constexpr (F == kFmtD8B8) {
+    const uint2 lo = bf16x4_to_f16x4(make_uint2(raw.x, raw.y)), hi = bf16x4_to_f16x4(make_uint2(raw.z, raw.w));
+    return make_uint4(lo.x, lo.y, hi.x, hi.y);
+  } else if constexpr (F == kFmtD2B8) {
+    const uint32_t h = pack_half2(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u));
+    return make_uint4(h, h, h, h);
+  } else {
+    const uint2 e = bf16x4_to_f16x4(make_uint2(raw.x, raw.y));
+    return make_uint4(e.x, e.y, e.x, e.y);
+  }
+}
 template <int KB, int VB>
 __device__ __forceinline__ uint4 table_load(const uint16_t* ck, const uint16_t* cv, int tid) {
   const int j = tid >> 1, which = tid & 1;
   const int n = which ? smem_entries<VB>() : smem_entries<KB>();
   if (j >= n) return make_uint4(0u, 0u, 0u, 0u);
-  return which ? table_pattern<VB>(cv, j) : table_pattern<KB>(ck, j);
+  return which ? table_raw<VB>(cv, j) : table_raw<KB>(ck, j);
 }
 template <int KB, int VB>
-__device__ __forceinline__ void table_store(unsigned char* tab, const uint4 v, int tid) {
+__device__ __forceinline__ void table_store(unsigned char* tab, uint4 raw, int tid) {
   // 8 x 16-byte stores per half-row, rotated so that the 8 threads of a quarter-warp hit 8
-  // different bank groups
+  // different bank groups.  The empty asm pins the conversion after this point (the compiler would
+  // otherwise hoist it -- and the wait for the codebook loads -- above the grid-dependency wait).
+  asm volatile("" : "+r"(raw.x), "+r"(raw.y), "+r"(raw.z), "+r"(raw.w));
   const int j = tid >> 1, which = tid & 1;
   const int n = which ? smem_entries<VB>() : smem_entries<KB>();
   if (j >= n) return;
+  const uint4 v = which ? table_cvt<VB>(raw) : table_cvt<KB>(raw);
   unsigned char* row = tab + j * 256 + which * 128;
 #pragma unroll
   for (int u0 = 0; u0 < 8; ++u0) {
