@@ -609,7 +609,13 @@ def run_ours(args, rank, world, local_rank):
                                 if seq_sharded else None),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
                    "num_splits": S, "attn_kernel": kernel_kind, "cuda_graph": use_graph, "residual_window": R, "fused_append": fused_launch,
-                   "dtype_detail": "u8 codes, bf16 q/k/v/o, fp16 hi/lo MMA operands, f32 accumulate"},
+                   "dtype_detail": "u8 codes, bf16 q/k/v/o, fp16 hi/lo MMA operands, f32 accumulate",
+                   "step": "DESIGN.md R16: one decoded token through the attention of all 32 layers (per layer: "
+                           "append-encode of the new token + attention, one fused vecinfer_decode_step launch "
+                           "when possible); SURVEY c.2's single attention-layer call = roofline.attn_us_avg",
+                   "attn_timing_pattern": "back-to-back layer launches in one CUDA graph with programmatic "
+                                          "dependent launch (the next layer's static prologue may overlap this "
+                                          "layer's tail; its dynamic reads wait for completion)"},
         "us_per_layer_call": step_ms * 1e3 / L,
         "tokens_per_s": B_glob * 1e3 / step_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
