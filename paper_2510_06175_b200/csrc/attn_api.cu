@@ -273,7 +273,9 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   const bool use_sk = !tc && !next2 && (D == 128 || (!res && !app && !pg)) && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
   SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
   if (D == 64) plan.cluster = 0;   // the DSMEM cluster merge is written for 128-dim rows
-  if (kcfg.code_bits == 16 && vcfg.code_bits == 16 && !next2) plan.cluster = 0;   // (no cluster buffer: L1 capacity)
+  // formats without any shared table (b4d4 d = 4 and d8b16 books through L1/L2) get the smallest
+  // shared allocation -- no cluster buffer, so never the DSMEM cluster merge
+  if ((kf == 16 || kf == 816) && (vf == 16 || vf == 816)) plan.cluster = 0;
   const int32_t S = plan.S;
   const WsLayout wl = ws_layout(B, H_kv, plan_splits(B, H_kv, range, num_splits).S, true);
   const int64_t U = static_cast<int64_t>(B) * H_kv;
