@@ -77,6 +77,21 @@ static int hsplit_of(int32_t H_q, int32_t H_kv) {
 // Stream kernel (attn_stream.cu) for batch decode: B*H_kv >= #SMs units over V = #SMs CTAs (a
 // unit crossing a CTA boundary is split in two and merged).  VECINFER_STREAM=0 disables it,
 // =1 forces it for any auto-split call (experiments).
+// stream partition: virtual tokens charged for each split-unit start (a CTA's extra segment costs
+// its table fill, first-tile latency and combine; measured at cfg3: CTAs with 5 segments ran their
+// rounds 6 us longer than those with 4).  Sweep 0 / 512 / 1024 / 2048 / 3072 over five batch shapes
+// (profiles/r02/exp_stream_seg_cost.txt): 1024 is best overall (cfg3 105.8 -> 103.9 us).
+// VECINFER_SEG_COST overrides (experiments).
+static int seg_cost_tokens() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VECINFER_SEG_COST");
+    v = e ? atoi(e) : 1024;
+    if (v < 0) v = 0;
+  }
+  return v;
+}
+
 static int stream_mode_from_env() {
   static int mode = -2;
   if (mode == -2) {
@@ -317,6 +332,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.S = S;
   a.n_items = B * H_kv * S;
   a.U = static_cast<int>(U);
+  a.seg_cost = seg_cost_tokens();
   a.V = static_cast<int>(V);
   a.rcpU = 1.0 / static_cast<double>(U);
   a.rcpV = 1.0 / static_cast<double>(V);

@@ -36,6 +36,7 @@ struct AttnArgs {
   // (unit u = [u*V, (u+1)*V), CTA c = [c*U, (c+1)*U))
   int U, V;
   double rcpU, rcpV;           // 1/U, 1/V (host, double): division-free tick arithmetic
+  int seg_cost;                // stream partition: virtual tokens per split-unit start (segment setup cost)
   int merge;                   // kMergeNone / kMergeSpin / kMergeLast
   unsigned long long* part_elem;   // [U + V][4][128] published (o, L) elements (zero = empty)
   void* o;

@@ -85,9 +85,14 @@ static_assert(2 * kQSeg * 4 <= kMiscNew, "q~ rows");
 // token offset (within the unit's attended range of n tokens) of local tick tau in [0, V]:
 // proportional, rounded down to 16 tokens; X = extra virtual tokens at the end of the range that
 // account for the encode of the appended row so its piece is not the straggler
-__device__ __forceinline__ int64_t piece_tok(int64_t tau, int64_t V, double rcpV, int64_t n, int64_t X) {
+// Xs = virtual tokens at the START of a split unit that stand for the fixed cost of a segment
+// (table fill, first-tile latency, combine): a CTA gets one more segment per unit start inside its
+// tick range, and these virtual tokens shorten its real share accordingly
+__device__ __forceinline__ int64_t piece_tok(int64_t tau, int64_t V, double rcpV, int64_t n, int64_t X,
+                                             int64_t Xs = 0) {
   if (tau >= V) return n;
-  const int64_t t = div_fix(tau * (n + X), V, rcpV) & ~int64_t(15);
+  int64_t t = div_fix(tau * (n + X + Xs), V, rcpV) - Xs;
+  t = t < 0 ? 0 : (t & ~int64_t(15));
   return t < n ? t : n;
 }
 
@@ -107,8 +112,9 @@ __device__ __forceinline__ void compute_seg(const AttnArgs& a, int vc, int u, Se
   if (beg < 0) beg = 0;
   const int P = static_cast<int>(c2 - c1 + 1);
   const int64_t X = (a.append && P > 1) ? kAppendTokenCost : 0;
-  o.t0 = beg + piece_tok(tau0, V, a.rcpV, e - beg, X);
-  o.t1 = beg + piece_tok(tau1, V, a.rcpV, e - beg, X);
+  const int64_t Xs = P > 1 ? a.seg_cost : 0;
+  o.t0 = beg + piece_tok(tau0, V, a.rcpV, e - beg, X, Xs);
+  o.t1 = beg + piece_tok(tau1, V, a.rcpV, e - beg, X, Xs);
   o.u = u; o.b = b; o.h = h;
   const HeadMap hm = head_map(a, h);
   o.hc = hm.hc; o.hq0 = hm.hq0; o.gp = hm.gp;

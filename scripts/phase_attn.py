@@ -89,7 +89,16 @@ def main():
             st(rel[:, 8], "publish done (rel)")
             st(rel[:, 4] - rel[:, 5], "slice merge")
         st(rel[:, 4], "CTA end (rel)")
-        if args.per_cta:   # per-CTA main loop vs SM id (is the spread systematic?)
+        if args.per_cta and np.isfinite(rel[:, 12]).any():   # stream kernel: main loop vs segments per CTA
+            U, V = B * 8, nct
+            segs_per = np.array([((c * U + U - 1) // V) - ((c * U) // V) + 1 for c in range(nct)])
+            ml = rel[:, 2] - rel[:, 1]
+            end = rel[:, 4]
+            for ns in sorted(set(segs_per.tolist())):
+                sel = segs_per == ns
+                print(f"   CTAs with {ns} segments ({(ns + 1) // 2} rounds): n={sel.sum()}, main loop mean {ml[sel].mean():.2f} "
+                      f"max {ml[sel].max():.2f} us, end mean {end[sel].mean():.2f} max {end[sel].max():.2f} us")
+        if args.per_cta and not np.isfinite(rel[:, 12]).any():   # per-CTA main loop vs SM id (is the spread systematic?)
             sm = both[:, 15].astype(int)
             ml = rel[:, 2] - rel[:, 1]
             order = np.argsort(ml)
