@@ -323,7 +323,23 @@ def run_ours(args, rank, world, local_rank):
     # the fused peer-memory kernel (vecinfer_merge_lse_p2p: remote stores into every rank's IPC
     # window + flags + rank-order merge, one launch, graph-safe) or NCCL all-gather of the packed
     # partials + vecinfer_merge_lse (--exchange nccl; gloo through host copies for 1-GPU checks)
-    p2p = P2PExchange(B * H_Q, D, dev) if (seq_sharded and args.exchange == "p2p") else None
+    p2p, p2p_fallback = None, None
+    if seq_sharded and args.exchange == "p2p":
+        # the peer windows need CUDA IPC + peer access between the ranks' GPUs; if the platform
+        # refuses (on every rank alike: the outcome is all-reduced), run the all-gather exchange
+        ok, why = 1, None
+        try:
+            p2p = P2PExchange(B * H_Q, D, dev)
+        except Exception as ex:   # noqa: BLE001 -- reported in the line
+            ok, why = 0, f"{type(ex).__name__}: {ex}"
+        t_ok = torch.tensor([ok], dtype=torch.int32, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+        if int(t_ok.item()) == 0:
+            if p2p is not None:
+                p2p.close()
+                p2p = None
+            args.exchange = "nccl"
+            p2p_fallback = why or "a peer rank could not map the P2P windows"
     lse_m = torch.empty(L, B, H_Q, dtype=torch.float32, device=dev) if seq_sharded else None
 
     def exchange_layer(l):
@@ -635,7 +651,7 @@ def run_ours(args, rank, world, local_rank):
                        + "pinned H2D of q/k/v and D2H of o every step"},
         "gpu_launches": launches_per_step * K,
         "ranks": ranks if world > 1 else None,
-        "dist": ({"backend": args.backend, "world": world, "p2p_timeout_flag": p2p_err,
+        "dist": ({"backend": args.backend, "world": world, "p2p_timeout_flag": p2p_err, "p2p_fallback": p2p_fallback,
                   "nccl_version": (".".join(map(str, torch.cuda.nccl.version())) if args.backend == "nccl" else None),
                   "shard": f"rank r attends tokens [r*N/{world}, (r+1)*N/{world}) (32-aligned)" if seq_sharded else
                   (f"batch slice {B} of {B_glob} sequences per rank" if args.workload == "cfg3" else "replica")}
