@@ -43,11 +43,15 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, phase_timing: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, phase_timing: bool = False, defines=(), out=None) -> str:
     global BUILD, LIB
     if phase_timing:
         BUILD, LIB = BUILD + "_phase", LIB_PHASE
         FLAGS.append("-DVECINFER_PHASE_TIMING")
+    if out:   # experiment variant (-D macros) into its own object dir and library; VECINFER_LIB loads it
+        LIB = os.path.abspath(out)
+        BUILD = os.path.join(ROOT, "build", os.path.splitext(os.path.basename(out))[0])
+    FLAGS.extend("-D" + d for d in defines)
     os.makedirs(BUILD, exist_ok=True)
     srcs = _sources()
     headers = [d for d in _deps() if not d.endswith(".cu")]
@@ -88,5 +92,8 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
     ap.add_argument("--phase-timing", action="store_true")
+    ap.add_argument("-D", "--define", action="append", default=[], help="experiment macro NAME=VALUE")
+    ap.add_argument("--out", help="experiment library path (with --define)")
     args = ap.parse_args()
-    print(build(force=args.force, verbose=args.verbose, phase_timing=args.phase_timing))
+    print(build(force=args.force, verbose=args.verbose, phase_timing=args.phase_timing, defines=args.define,
+                out=args.out))

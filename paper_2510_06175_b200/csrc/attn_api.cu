@@ -291,6 +291,10 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   // formats without any shared table (b4d4 d = 4 and d8b16 books through L1/L2) get the smallest
   // shared allocation -- no cluster buffer, so never the DSMEM cluster merge
   if ((kf == 16 || kf == 816) && (vf == 16 || vf == 816)) plan.cluster = 0;
+#ifndef VECINFER_CODE_TMA
+#define VECINFER_CODE_TMA 0
+#endif
+  if (VECINFER_CODE_TMA > 0 && kf == 8 && vf == 8) plan.cluster = 0;   // TMA stages replace the cluster buffer
   const int32_t S = plan.S;
   const WsLayout wl = ws_layout(B, H_kv, plan_splits(B, H_kv, range, num_splits).S, true);
   const int64_t U = static_cast<int64_t>(B) * H_kv;

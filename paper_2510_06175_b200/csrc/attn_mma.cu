@@ -30,6 +30,12 @@
 #ifndef VECINFER_TC_EXP
 #define VECINFER_TC_EXP 0   // != 0 only in timing-experiment builds (results not valid)
 #endif
+// Code tiles staged by the TMA engine (cp.async.bulk into per-warp shared stages, mbarrier
+// completion) instead of LDG into registers: VECINFER_CODE_TMA = stages per warp (0 = LDG path).
+// b2d4 / D = 128 / contiguous caches, mma.sync score path.
+#ifndef VECINFER_CODE_TMA
+#define VECINFER_CODE_TMA 0
+#endif
 
 namespace vecinfer {
 namespace {
@@ -53,7 +59,14 @@ static_assert(4 * kQRow * 4 <= kMiscNew, "q~ rows");
 constexpr uint32_t kTmemCols = 512;
 constexpr int kClusterMax = 16;                      // DSMEM merge buffer: [16][4][128] + m, l
 constexpr int kCbufBytes = kClusterMax * 4 * 130 * 4;
+constexpr int kTmaSt = VECINFER_CODE_TMA;
+constexpr int kTmaStage = 2048;                      // one 32-token tile: K rows (1 KiB) | V rows (1 KiB)
 constexpr int kSmemBytes = 65536 + kTab + kCbufBytes + 1024;  // pad + table + cluster buffer + slack
+// b2d4 with TMA-staged code tiles: the per-warp stages take the cluster buffer's place (the planner
+// never clusters it then)
+constexpr bool tma_fmt(int kf, int vf) { return kTmaSt > 0 && kf == 8 && vf == 8; }
+constexpr int kSmemBytesTma = 65536 + kTab + kNW * kTmaSt * kTmaStage + 1024;
+static_assert(kSmemBytesTma <= 232448 - 1024, "TMA stages exceed 227 KiB");
 // 16-bit K and V: no shared table -> only misc + cluster buffer, leaving the L1 to the global
 // codebook gathers
 constexpr int kSmemBytesNoTab = kMiscBytes + 1024 + kCbufBytes + 1024;
@@ -65,6 +78,7 @@ constexpr bool classic_tab(int f) { return f == 4 || f == 8 || f == kFmtD8B8 || 
 constexpr bool sep_tab(int f) { return f == kFmtD8B12 || f == kFmtD4B10; }
 constexpr int smem_layout_bytes(int kf, int vf) {
   const int nsep = (sep_tab(kf) ? 1 : 0) + (sep_tab(vf) ? 1 : 0);
+  if (tma_fmt(kf, vf)) return kSmemBytesTma > kSmemBytes ? kSmemBytesTma : kSmemBytes;
   if (classic_tab(kf) || classic_tab(vf)) return kSmemBytes + nsep * kSepTab;
   if (nsep) return ((kMiscBytes + 1023) & ~1023) + nsep * kSepTab + kCbufBytes + 1024;
   // no shared table (16-bit K and V: the books are gathered through L1/L2): no cluster buffer either
@@ -109,6 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   // the attention launch: vecinfer_decode_step appends them with a separate encode launch)
   constexpr auto gen_ok = [](int f) { return f == kFmtD8B8 || f == kFmtD2B8 || f == kFmtD4B10; };
   constexpr bool kGenAppend = gen_ok(KB) && gen_ok(VB) && DH == 128;
+  constexpr bool kTma = tma_fmt(KB, VB) && DH == 128 && !TC;   // contiguous caches only (runtime)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
@@ -146,6 +161,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     if (tid < 4) tc::mbar_init(smem_u32(tc_misc + 2 + 2 * tid), 1);
     if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (tid < 128) *reinterpret_cast<uint4*>(tcb + ((tid >> 3) * 2 + 1) * 128 + (tid & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  // TMA-staged code tiles: warp w owns kTmaSt stages of kTmaStage bytes above the table and one
+  // mbarrier per stage (misc TCB region, unused without TC); n_iss / n_con count the warp's issued /
+  // consumed tiles across work items (stage = n % kTmaSt, phase parity = (n / kTmaSt) & 1)
+  const uint32_t tma_stg = tab_s + kTab + static_cast<uint32_t>(warp * kTmaSt * kTmaStage);
+  const uint32_t tma_bar = raw_s + kMiscTCB + static_cast<uint32_t>(warp * kTmaSt * 8);
+  uint32_t n_iss = 0, n_con = 0;
+  if constexpr (kTma) {
+    if (lane < kTmaSt) tc::mbar_init(tma_bar + 8 * lane, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
   }
   bool first = true;
   for (int item = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); item < a.n_items; item += nblk) {
@@ -242,11 +268,33 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       tcv.v[q][3] = (rem >= 32 || t0 + 9 < rem) ? FV::ldv(p + (16 * q + 9) * VR) : VCode<VB>{};
     }
   };
+  // TMA: lane 0 issues the bulk copies of tile `it` (K rows, then V rows; a ragged tile copies its
+  // valid rows only -- the rest of the stage is stale and masked at the shared loads)
+  auto tma_issue = [&](int it) {
+    const uint32_t st = n_iss % kTmaSt;
+    ++n_iss;
+    if (lane == 0) {
+      const int rows = ntok - 32 * it < 32 ? ntok - 32 * it : 32;
+      const uint32_t bar = tma_bar + 8 * st, dst = tma_stg + st * kTmaStage;
+      const int64_t row = row0 + 32 * static_cast<int64_t>(it);
+      mbar_expect_tx(bar, static_cast<uint32_t>(rows * (KR + VR)));
+      bulk_g2s(dst, a.kcodes + row * KR, static_cast<uint32_t>(rows * KR), bar);
+      bulk_g2s(dst + kTmaStage / 2, a.vcodes + row * VR, static_cast<uint32_t>(rows * VR), bar);
+    }
+  };
+  const bool tma_on = kTma && !paged;
   KRowT<KB> kfirst0, kfirst1;
+  if constexpr (kTma) {
+    if (tma_on) {
+#pragma unroll
+      for (int k = 0; k < kTmaSt; ++k)
+        if (warp + kNW * k < ntile) tma_issue(warp + kNW * k);
+    }
+  }
   if constexpr (TC) {
     if (warp < ntile) { load_krow(kfirst0, warp); load_vtile(nxt, warp); }
     if (warp + kNW < ntile) load_krow(kfirst1, warp + kNW);
-  } else if (warp < ntile) {
+  } else if (warp < ntile && !tma_on) {
     const int rem = ntok - 32 * warp;
     if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
     else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
@@ -602,7 +650,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   if constexpr (!TC) {
     for (int it = warp; it < ntile; it += kNW) {
-      TileCodes<KB, VB> cur = nxt;
+      TileCodes<KB, VB> cur;
+      if constexpr (!kTma) {
+        cur = nxt;
+      } else if (tma_on) {   // wait for the stage, read the tile's fragments, refill the stage
+        const uint32_t st = n_con % kTmaSt, par = (n_con / kTmaSt) & 1u;
+        ++n_con;
+        tc::mbar_wait(tma_bar + 8 * st, par);
+        const int rem = ntok - 32 * it;
+        const uint32_t kb = tma_stg + st * kTmaStage + r * KR + FK::kOffK * j;
+        const uint32_t vb = tma_stg + st * kTmaStage + kTmaStage / 2 + 2 * j * VR + FV::kOffV * r;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const bool full = rem >= 32;
+          cur.k[q][0] = (full || 16 * q + r < rem) ? lds_u64(kb + (16 * q) * KR) : Fmt<KB>::zk();
+          cur.k[q][1] = (full || 16 * q + r + 8 < rem) ? lds_u64(kb + (16 * q + 8) * KR) : Fmt<KB>::zk();
+          const int t0 = 16 * q + 2 * j;
+          cur.v[q][0] = (full || t0 < rem) ? lds_u32(vb + (16 * q) * VR) : VCode<VB>{};
+          cur.v[q][1] = (full || t0 + 1 < rem) ? lds_u32(vb + (16 * q + 1) * VR) : VCode<VB>{};
+          cur.v[q][2] = (full || t0 + 8 < rem) ? lds_u32(vb + (16 * q + 8) * VR) : VCode<VB>{};
+          cur.v[q][3] = (full || t0 + 9 < rem) ? lds_u32(vb + (16 * q + 9) * VR) : VCode<VB>{};
+        }
+        __syncwarp();   // every lane has read the stage before the async proxy overwrites it
+        if (it + kNW * kTmaSt < ntile) {
+          if (lane == 0) tc::fence_proxy_async_smem();
+          tma_issue(it + kNW * kTmaSt);
+        }
+      } else {
+        cur = nxt;
+      }
       if constexpr (kCanAppend || kGenAppend) {
       if (it == patch_tile) {   // the appended row: codes just encoded, not the stale load
         const KCode<KB> nk = new_kchunk<KB, DH>(newcodes, j);
@@ -621,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       }
       }
       const int rem_cur = ntok - 32 * it;
-      if (it + kNW < ntile) {
+      if (!tma_on && it + kNW < ntile) {
         if (paged) {
           const int64_t tok = r0 + 32 * static_cast<int64_t>(it + kNW);
           const int64_t rw = row_in(pg_ahead, tok);
