@@ -19,7 +19,7 @@
  *    non-OK status of the calling thread.
  *  - Thread-safe: no global mutable state except the thread-local error string and a
  *    per-device attribute cache.
- *  - Supported shapes (ABI v5): head_dim D in {128, 64}, sub_dim d = 4, code_bits in {4, 8, 16}
+ *  - Supported shapes (ABI v6): head_dim D in {128, 64}, sub_dim d = 4, code_bits in {4, 8, 16}
  *    (b1d4, b2d4, b4d4 in BASELINE.json notation = paper d4b4, d4b8, d4b16), K and V
  *    widths independent; GQA group G = H_q / H_kv in 1..8; contiguous or paged code caches.
  *    D = 64: split kernel (residual window, fused append) and, for batch decode without those,
@@ -34,6 +34,9 @@
  *  - ABI v5 adds: n_tokens_max in vecinfer_attn_kernel_kind (the stream/split choice is a cost
  *    model over it), vecinfer_kmeans_step (GPU codebook Lloyd iteration) and the fused
  *    cross-GPU exchange + merge over peer memory (vecinfer_p2p_window_*, vecinfer_merge_lse_p2p).
+ *  - ABI v6 adds: the tcgen05 score variant (VECINFER_ATTN_DEQUANT_TC), d8b16, and the
+ *    cross-GPU merge fused into the attention launch itself (vecinfer_attn_decode_xr,
+ *    vecinfer_decode_step_xr, vecinfer_xr_window_bytes).
  */
 #ifndef VECINFER_H_
 #define VECINFER_H_
@@ -45,7 +48,7 @@
 extern "C" {
 #endif
 
-#define VECINFER_ABI_VERSION 5
+#define VECINFER_ABI_VERSION 6
 
 typedef struct CUstream_st* vecinfer_stream_t; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -417,6 +420,61 @@ vecinfer_status_t vecinfer_merge_lse_p2p(const float* o_local, const float* lse_
                                          int32_t H_q, int32_t D, uint32_t epoch, void* o,
                                          vecinfer_dtype_t o_dtype, float* lse, uint32_t* err_flags,
                                          vecinfer_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Sequence-sharded attention with the cross-GPU merge fused into the attention launch (SURVEY
+ * §8(e): "N4's epilogue stores partials straight into peers' symmetric windows ... then local N5").
+ * Each rank attends its own token shard (its own cache, as vecinfer_attn_decode /
+ * vecinfer_decode_step); inside the same launch every CTA merges its slice of outputs over the
+ * rank's S splits (the single-wave spin merge), stores the slice's rank partial (o_r, L_r) as
+ * self-validating 64-bit words straight into every rank's window, waits for the P partials of its
+ * slice in its own window, and merges them (log-sum-exp, Alg. 1 l.729-730 / S:314-322) into the
+ * FINAL o and lse.  No separate exchange kernel, no host round trip, graph-capturable.
+ *   xr.world, xr.rank  P ranks, this rank (0 <= rank < P <= 16); every rank calls with the same
+ *                      B, H_q, D and the same sequence of calls (slots alternate by a launch
+ *                      counter in the own window's header: a rank may run at most one call ahead).
+ *   xr.windows         DEVICE array [P] of window pointers as mapped in this process (windows from
+ *                      vecinfer_p2p_window_create / _open, sized by vecinfer_xr_window_bytes;
+ *                      windows[rank] = the own window).  Zero-initialised by create; left
+ *                      consistent by every call.
+ *   xr.rows_max        rows (B * H_q) the windows were sized for.
+ *   xr.err_flags       device uint32 (may be NULL): VECINFER_FLAG_P2P_TIMEOUT if a peer's partial
+ *                      did not arrive within 5 s (that rank's share then counts as empty).
+ * The launch must be a single wave of the split kernel: B * H_kv * S <= #SMs with S >= 2 splits
+ * (the planner's S, raised to 2 if it chose 1).  Contiguous caches, DEQUANT_MMA / AUTO (not the
+ * stream partition, the LUT or the tcgen05 variant).  Otherwise UNSUPPORTED: use
+ * vecinfer_attn_decode + vecinfer_merge_lse_p2p.  o / lse receive the merged result on every rank.
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t world;
+  int32_t rank;
+  void* const* windows;
+  int64_t rows_max;
+  uint32_t* err_flags;
+} vecinfer_xrank_t;
+size_t vecinfer_xr_window_bytes(int32_t P, int64_t rows, int32_t D);
+vecinfer_status_t vecinfer_attn_decode_xr(const void* q_bf16, int32_t B, int32_t H_q, int32_t H_kv,
+                                          int64_t q_stride_b, int64_t q_stride_h, const float* lambda,
+                                          const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride,
+                                          int64_t cv_head_stride, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
+                                          const uint8_t* k_codes, const uint8_t* v_codes, int64_t n_cap,
+                                          const int32_t* seq_lens, int64_t tok_begin, int64_t tok_end,
+                                          float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
+                                          void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
+                                          size_t workspace_bytes, vecinfer_stream_t stream,
+                                          const vecinfer_residual_t* residual, const vecinfer_xrank_t* xr);
+vecinfer_status_t vecinfer_decode_step_xr(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,
+                                          int32_t B, int32_t H_q, int32_t H_kv, const int64_t q_strides[2],
+                                          const int64_t k_new_strides[2], const int64_t v_new_strides[2],
+                                          const float* lambda, const float* inv_lambda, const void* ck_bf16,
+                                          const void* cv_bf16, int64_t ck_head_stride, int64_t cv_head_stride,
+                                          vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes,
+                                          uint8_t* v_codes, int64_t n_cap, const int32_t* write_pos,
+                                          const int32_t* seq_lens, float softmax_scale, int32_t num_splits,
+                                          vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype,
+                                          float* lse, uint32_t* err_flags, void* workspace,
+                                          size_t workspace_bytes, vecinfer_stream_t stream,
+                                          const vecinfer_residual_t* residual, const vecinfer_xrank_t* xr);
 
 /* Diagnostics: how many thread-block clusters of `cluster_size` CTAs of the attention kernel can
  * be co-resident on the current device (0 = not schedulable); used by the split planner. */

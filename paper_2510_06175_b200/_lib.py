@@ -29,6 +29,12 @@ class Paged(ctypes.Structure):
                 ("n_pages", ctypes.c_int32)]
 
 
+class XRank(ctypes.Structure):
+    """vecinfer_xrank_t: cross-GPU merge fused into the attention launch."""
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("windows", ctypes.c_void_p),
+                ("rows_max", ctypes.c_int64), ("err_flags", ctypes.c_void_p)]
+
+
 class VQ(ctypes.Structure):
     """vecinfer_vq_t {head_dim, sub_dim, code_bits}."""
     _fields_ = [("head_dim", c_i32), ("sub_dim", c_i32), ("code_bits", c_i32)]
@@ -84,6 +90,16 @@ PROTOTYPES = {
                                            c_void_p, c_i64, c_void_p, c_void_p, c_f32, c_i32, c_i32, c_void_p,
                                            c_i32, c_void_p, c_void_p, c_void_p, c_sz, c_void_p,
                                            ctypes.POINTER(Residual), ctypes.POINTER(Paged)]),
+    "vecinfer_xr_window_bytes": (c_sz, [c_i32, c_i64, c_i32]),
+    "vecinfer_attn_decode_xr": (c_i32, [c_void_p, c_i32, c_i32, c_i32, c_i64, c_i64, c_void_p, c_void_p, c_void_p,
+                                        c_i64, c_i64, VQ, VQ, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_i64, c_f32,
+                                        c_i32, c_i32, c_void_p, c_i32, c_void_p, c_void_p, c_sz, c_void_p,
+                                        ctypes.POINTER(Residual), ctypes.POINTER(XRank)]),
+    "vecinfer_decode_step_xr": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, I64x2, I64x2, I64x2,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, VQ, VQ, c_void_p,
+                                        c_void_p, c_i64, c_void_p, c_void_p, c_f32, c_i32, c_i32, c_void_p, c_i32,
+                                        c_void_p, c_void_p, c_void_p, c_sz, c_void_p, ctypes.POINTER(Residual),
+                                        ctypes.POINTER(XRank)]),
     "vecinfer_debug_attn_max_clusters": (c_i32, [c_i32]),
     "vecinfer_decode_step_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i64, VQ, VQ, c_i32]),
     "vecinfer_merge_lse": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_void_p, c_i32, c_void_p,

@@ -227,7 +227,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
                                    void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
                                    size_t workspace_bytes, vecinfer_stream_t stream, const AppendArgs* app,
                                    const vecinfer_residual_t* res, bool res_append,
-                                   const vecinfer_paged_t* pg = nullptr) {
+                                   const vecinfer_paged_t* pg = nullptr, const vecinfer_xrank_t* xr = nullptr) {
   if (!q_bf16 || !lambda || !ck_bf16 || !cv_bf16 || !k_codes || !v_codes || !seq_lens || !o)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: NULL pointer");
   if (o_dtype != VECINFER_BF16 && o_dtype != VECINFER_F32) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad o_dtype");
@@ -283,10 +283,30 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
     if (lut) return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_paged: paged caches run the DEQUANT_MMA kernels only");
     if (tok_begin % 32 != 0) return fail(VECINFER_ERR_SHAPE, "attn_decode_paged: tok_begin must be a multiple of 32");
   }
+  const int64_t n_sms = device_sm_count();
+  if (xr) {   // fused cross-rank merge: the single-wave spin merge of the split kernel
+    if (xr->world < 1 || xr->world > 16 || xr->rank < 0 || xr->rank >= xr->world)
+      return fail(VECINFER_ERR_SHAPE, "attn_decode_xr: rank %d / world %d outside [0, world), world in 1..16",
+                  xr->rank, xr->world);
+    if (!xr->windows) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode_xr: NULL windows");
+    if (xr->rows_max < static_cast<int64_t>(B) * H_q)
+      return fail(VECINFER_ERR_SHAPE, "attn_decode_xr: windows sized for %lld rows < B*H_q", (long long)xr->rows_max);
+    if (pg || lut || tc || next2 || D != 128 || algo == VECINFER_ATTN_DEQUANT_MMA_STREAM ||
+        static_cast<int64_t>(B) * H_kv * 2 > n_sms)
+      return fail(VECINFER_ERR_UNSUPPORTED, "attn_decode_xr: needs the single-wave split kernel (contiguous cache, "
+                  "D = 128 with d = 4 books, B*H_kv*2 <= %lld SMs, DEQUANT_MMA / AUTO); use attn_decode + "
+                  "merge_lse_p2p", (long long)n_sms);
+  }
   // stream partition: D = 128, or D = 64 without a residual window, fused append or paging (those
   // run the split kernel's persistent grid)
-  const bool use_sk = !tc && !next2 && (D == 128 || (!res && !app && !pg)) && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
+  const bool use_sk = !xr && !tc && !next2 && (D == 128 || (!res && !app && !pg)) && use_stream(B, H_kv, range, num_splits, lut, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM);
   SplitPlan plan = use_sk ? SplitPlan{1, 0} : plan_splits(B, H_kv, range, num_splits);
+  if (xr) {   // 2 <= S <= #SMs / (B*H_kv), no cluster: every CTA co-resident for the spin merge
+    const int64_t smax = n_sms / (static_cast<int64_t>(B) * H_kv);
+    if (plan.S < 2) plan.S = 2;
+    if (plan.S > smax) plan.S = static_cast<int>(smax);
+    plan.cluster = 0;
+  }
   if (D == 64) plan.cluster = 0;   // the DSMEM cluster merge is written for 128-dim rows
   // formats without any shared table (b4d4 d = 4 and d8b16 books through L1/L2) get the smallest
   // shared allocation -- no cluster buffer, so never the DSMEM cluster merge
@@ -296,6 +316,8 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
 #endif
   if (VECINFER_CODE_TMA > 0 && kf == 8 && vf == 8) plan.cluster = 0;   // TMA stages replace the cluster buffer
   const int32_t S = plan.S;
+  // (the offsets follow the planner's S, as vecinfer_attn_workspace_bytes sized it; the xr path's
+  // S <= max(2, that S) fits the element region, which holds max(#SMs, units * S) + units rows)
   const WsLayout wl = ws_layout(B, H_kv, plan_splits(B, H_kv, range, num_splits).S, true);
   const int64_t U = static_cast<int64_t>(B) * H_kv;
   const int64_t sms = device_sm_count();
@@ -343,10 +365,15 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   a.merge = !stream_split ? kMergeNone : (V <= sms ? kMergeSpin : kMergeLast);
   a.cluster = plan.cluster;
   a.tc = tc ? 1 : 0;
-  a.merge_kernel = (S > 1 && !plan.cluster && algo != VECINFER_ATTN_LUT && D == 128) ? merge_mode_from_env() : 0;
+  a.merge_kernel = (!xr && S > 1 && !plan.cluster && algo != VECINFER_ATTN_LUT && D == 128) ? merge_mode_from_env() : 0;
   // every CTA co-resident (one CTA per SM, grid <= SMs): spin-barrier + sliced merge
   a.merge_spin = (S > 1 && !plan.cluster && !a.merge_kernel && algo != VECINFER_ATTN_LUT &&
-                  static_cast<int64_t>(B) * H_kv * S <= device_sm_count() && !getenv("VECINFER_NO_SPIN")) ? 1 : 0;
+                  static_cast<int64_t>(B) * H_kv * S <= n_sms && (xr || !getenv("VECINFER_NO_SPIN"))) ? 1 : 0;
+  a.xr_P = xr ? xr->world : 0;
+  a.xr_rank = xr ? xr->rank : 0;
+  a.xr_win = xr ? xr->windows : nullptr;
+  a.xr_rows = xr ? xr->rows_max : 0;
+  a.xr_err = xr ? xr->err_flags : nullptr;
   a.o = o; a.o_f32 = (o_dtype == VECINFER_F32); a.lse = lse;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   a.counter = S > 1 ? reinterpret_cast<uint32_t*>(ws + wl.counter) : nullptr;
@@ -493,7 +520,8 @@ static vecinfer_status_t decode_step_impl(const void* q_bf16, const void* k_new_
                                                   vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype,
                                                   float* lse, uint32_t* err_flags, void* workspace,
                                                   size_t workspace_bytes, vecinfer_stream_t stream,
-                                                  const vecinfer_residual_t* residual, const vecinfer_paged_t* pg) {
+                                                  const vecinfer_residual_t* residual, const vecinfer_paged_t* pg,
+                                                  const vecinfer_xrank_t* xr = nullptr) {
   if (!k_new_bf16 || !v_new_bf16 || !inv_lambda || !write_pos || !q_strides || !k_new_strides || !v_new_strides)
     return fail(VECINFER_ERR_INVALID_ARG, "decode_step: NULL pointer");
   for (int i = 0; i < 2; ++i)
@@ -507,7 +535,7 @@ static vecinfer_status_t decode_step_impl(const void* q_bf16, const void* k_new_
                    inv_lambda, write_pos, err_flags};
     return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
-                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, true, pg);
+                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, true, pg, xr);
   }
   const bool fuse = decode_fuses(B, H_kv * hsplit_of(H_q, H_kv), n_cap, kcfg, vcfg, num_splits, algo, pg != nullptr);
   if (!fuse) {   // separate append + attention launches (always for the paper-faithful LUT variant)
@@ -529,13 +557,13 @@ static vecinfer_status_t decode_step_impl(const void* q_bf16, const void* k_new_
     if (st != VECINFER_OK) return st;
     return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
-                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false, pg);
+                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false, pg, xr);
   }
   AppendArgs app{k_new_bf16, v_new_bf16, k_new_strides[0], k_new_strides[1], v_new_strides[0], v_new_strides[1],
                  inv_lambda, write_pos, err_flags};
   return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                    cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
-                   algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, false, pg);
+                   algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, false, pg, xr);
 }
 
 extern "C" vecinfer_status_t vecinfer_decode_step(const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16,
@@ -570,4 +598,42 @@ extern "C" vecinfer_status_t vecinfer_decode_step_paged(
                           lambda, inv_lambda, ck_bf16, cv_bf16, ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes,
                           v_codes, n_cap, write_pos, seq_lens, softmax_scale, num_splits, algo, o, o_dtype, lse,
                           err_flags, workspace, workspace_bytes, stream, residual, paged);
+}
+
+extern "C" size_t vecinfer_xr_window_bytes(int32_t P, int64_t rows, int32_t D) {
+  if (P <= 0 || rows <= 0 || D <= 0) return 0;
+  return static_cast<size_t>(kXrHeaderWords) * 8 + static_cast<size_t>(2) * P * rows * D * 8;
+}
+
+extern "C" vecinfer_status_t vecinfer_attn_decode_xr(const void* q_bf16, int32_t B, int32_t H_q, int32_t H_kv,
+                                                     int64_t q_stride_b, int64_t q_stride_h, const float* lambda,
+                                                     const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride,
+                                                     int64_t cv_head_stride, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
+                                                     const uint8_t* k_codes, const uint8_t* v_codes, int64_t n_cap,
+                                                     const int32_t* seq_lens, int64_t tok_begin, int64_t tok_end,
+                                                     float softmax_scale, int32_t num_splits, vecinfer_attn_algo_t algo,
+                                                     void* o, vecinfer_dtype_t o_dtype, float* lse, void* workspace,
+                                                     size_t workspace_bytes, vecinfer_stream_t stream,
+                                                     const vecinfer_residual_t* residual, const vecinfer_xrank_t* xr) {
+  if (!xr) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode_xr: NULL xr descriptor");
+  return attn_impl(q_bf16, B, H_q, H_kv, q_stride_b, q_stride_h, lambda, ck_bf16, cv_bf16, ck_head_stride,
+                   cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, tok_begin, tok_end, softmax_scale,
+                   num_splits, algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false,
+                   nullptr, xr);
+}
+
+extern "C" vecinfer_status_t vecinfer_decode_step_xr(
+    const void* q_bf16, const void* k_new_bf16, const void* v_new_bf16, int32_t B, int32_t H_q, int32_t H_kv,
+    const int64_t q_strides[2], const int64_t k_new_strides[2], const int64_t v_new_strides[2], const float* lambda,
+    const float* inv_lambda, const void* ck_bf16, const void* cv_bf16, int64_t ck_head_stride, int64_t cv_head_stride,
+    vecinfer_vq_t kcfg, vecinfer_vq_t vcfg, uint8_t* k_codes, uint8_t* v_codes, int64_t n_cap,
+    const int32_t* write_pos, const int32_t* seq_lens, float softmax_scale, int32_t num_splits,
+    vecinfer_attn_algo_t algo, void* o, vecinfer_dtype_t o_dtype, float* lse, uint32_t* err_flags, void* workspace,
+    size_t workspace_bytes, vecinfer_stream_t stream, const vecinfer_residual_t* residual,
+    const vecinfer_xrank_t* xr) {
+  if (!xr) return fail(VECINFER_ERR_INVALID_ARG, "decode_step_xr: NULL xr descriptor");
+  return decode_step_impl(q_bf16, k_new_bf16, v_new_bf16, B, H_q, H_kv, q_strides, k_new_strides, v_new_strides,
+                          lambda, inv_lambda, ck_bf16, cv_bf16, ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes,
+                          v_codes, n_cap, write_pos, seq_lens, softmax_scale, num_splits, algo, o, o_dtype, lse,
+                          err_flags, workspace, workspace_bytes, stream, residual, nullptr, xr);
 }

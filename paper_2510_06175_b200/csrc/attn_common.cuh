@@ -67,7 +67,121 @@ struct AttnArgs {
   const int32_t* res_lens;
   int res_append;
   float qscale_raw;      // softmax_scale * log2(e): raw-query scale for the residual scores
+  // cross-GPU merge fused into the launch (vecinfer_attn_decode_xr): xr_P ranks, 0 = off; windows
+  // [xr_P] of 64-bit words: a 256-byte header (epoch, arrival counter), then [2][xr_P][xr_rows][D]
+  int xr_P, xr_rank;
+  void* const* xr_win;
+  int64_t xr_rows;
+  uint32_t* xr_err;
 };
+
+constexpr unsigned long long kXrTimeoutNs = 5000000000ull;   // a missing peer flags instead of hanging
+constexpr int kXrHeaderWords = 32;                          // 256-byte window header
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long xr_clock_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Fused cross-rank step of one output element (o row `row`, dimension `dim`), called by every lane
+// of an L-lane merge group after the rank-local merge (m, wsum, osum; log2 domain, identical in
+// all L lanes).  The rank partial (o_r, L_r) is published as ~(L_r << 32 | o_r) (zero = not yet
+// written) into slot [par][rank][row][dim] of every rank's window (lane ll stores to ranks ll,
+// ll + L, ...); then the lanes poll the P slots [par][p][row][dim] of the own window, consume them
+// (store zero back: slots of a parity are reused two calls later, after every rank has passed this
+// call), and merge the P partials with a fixed butterfly -- the same arithmetic and order on every
+// rank, so all ranks hold bitwise the same o.  Alg. 1 l.729-730 / S:314-322 over ranks.
+template <int DH>
+__device__ __forceinline__ void xr_merge(const AttnArgs& a, int64_t row, int dim, bool act, int ll, int L,
+                                         float m, float wsum, float osum, uint32_t par, int64_t row_lse) {
+  const int P = a.xr_P;
+  const bool empty = !(wsum > 0.f);
+  const float ov = empty ? 0.f : osum * __frcp_rn(wsum);
+  const float lr = empty ? -INFINITY : m + __log2f(wsum);
+  const unsigned long long word =
+      ~((static_cast<unsigned long long>(__float_as_uint(lr)) << 32) | __float_as_uint(ov));
+  const int64_t blk = a.xr_rows * DH;                  // one rank's slot block
+  const int64_t slot = row * DH + dim;
+  if (act) {
+    for (int p = ll; p < P; p += L) {
+      unsigned long long* w = static_cast<unsigned long long*>(a.xr_win[p]) + kXrHeaderWords +
+                              (static_cast<int64_t>(par) * P + a.xr_rank) * blk + slot;
+      st_relaxed_sys_u64(w, word);
+    }
+  }
+  unsigned long long* own = static_cast<unsigned long long*>(a.xr_win[a.xr_rank]) + kXrHeaderWords +
+                            static_cast<int64_t>(par) * P * blk + slot;
+  constexpr int kPer = 8;                              // ranks per lane: P <= 16, L >= 2
+  unsigned long long w[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int p = ll + k * L;
+    w[k] = (act && p < P) ? ld_relaxed_sys_u64(own + p * blk) : ~0ull;
+  }
+  bool late = false;
+  const unsigned long long t0 = xr_clock_ns();
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int p = ll + k * L;
+    if (act && p < P) {
+      while (w[k] == 0ull) {
+        if (xr_clock_ns() - t0 > kXrTimeoutNs) { late = true; break; }
+        w[k] = ld_relaxed_sys_u64(own + p * blk);
+      }
+      st_relaxed_gpu_u64(own + p * blk, 0ull);
+    }
+  }
+  if (late && a.xr_err) atomicOr(a.xr_err, VECINFER_FLAG_P2P_TIMEOUT);
+  float lv[kPer], xv[kPer];
+  float M = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int p = ll + k * L;
+    const unsigned long long v = ~w[k];
+    const bool has = act && p < P && w[k] != 0ull;     // a timed-out rank counts as empty
+    xv[k] = has ? __uint_as_float(static_cast<uint32_t>(v)) : 0.f;
+    lv[k] = has ? __uint_as_float(static_cast<uint32_t>(v >> 32)) : -INFINITY;
+    M = fmaxf(M, lv[k]);
+  }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float o2 = __shfl_xor_sync(0xffffffffu, M, off);
+    if (off < L) M = fmaxf(M, o2);
+  }
+  float ws = 0.f, os = 0.f;
+  if (M != -INFINITY) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const float f = lv[k] == -INFINITY ? 0.f : ex2_approx(lv[k] - M);
+      ws += f;
+      os += f * xv[k];
+    }
+  }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float a2 = __shfl_xor_sync(0xffffffffu, ws, off);
+    const float b2 = __shfl_xor_sync(0xffffffffu, os, off);
+    if (off < L) {
+      ws += a2;
+      os += b2;
+    }
+  }
+  if (act && ll == 0) {
+    const bool emp = !(ws > 0.f);
+    const float o_fin = emp ? 0.f : os * __frcp_rn(ws);
+    if (a.o_f32) static_cast<float*>(a.o)[slot] = o_fin;
+    else static_cast<__nv_bfloat16*>(a.o)[slot] = __float2bfloat16_rn(o_fin);
+    if (dim == 0 && a.lse) a.lse[row_lse] = emp ? -INFINITY : (M + __log2f(ws)) * kLn2;
+  }
+}
 
 
 // extra tokens' worth of work the split owning the appended row does (its encode), used to
@@ -196,7 +310,7 @@ __device__ __forceinline__ void merge_splits(const AttnArgs& a, int b, int h) {
     if ((i & 3) < hm.gp) __stcg(a.part_l + unit * a.S * 4 + i, 0.f);
 }
 
-template <int NTHREADS, int NWARPS, int WROW = 128, int DH = 128, bool PRESCALED = false>
+template <int NTHREADS, int NWARPS, int WROW = 128, int DH = 128, bool PRESCALED = false, bool XR = false>
 __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int s,
                                            const float* wm, const float* wl, const float* wacc,
                                            float* scratch) {
@@ -285,6 +399,13 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
     const int L = S >= 32 ? 32 : (1 << (31 - __clz(S)));
     const int groups = NTHREADS / L, lg = tid / L, ll = tid % L;
     constexpr int kMaxPer = 4;   // splits per lane: S <= 128 (kMaxSplits)
+    // fused cross-rank merge: this launch's slot parity from the own window's epoch counter (read
+    // by every CTA before it arrives below; the last arrival advances it)
+    uint32_t xr_epoch = 0;
+    if constexpr (XR) {
+      xr_epoch = ld_acquire_gpu(static_cast<const uint32_t*>(a.xr_win[a.xr_rank])) + 1u;
+      if (xr_epoch == 0) xr_epoch = 1u;
+    }
     for (int t0 = 0; t0 < nout; t0 += groups) {   // one pass unless S is tiny and DH... (uniform)
       const int t = t0 + lg;
       const int o = o0 + t, g = o / DH, dim = o % DH;
@@ -343,6 +464,11 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
           osum += b2;
         }
       }
+      if constexpr (XR) {   // the rank partial goes to every rank; o, lse are the final merge
+        const int64_t row = static_cast<int64_t>(b) * a.Hq + hm.hq0 + g;
+        xr_merge<DH>(a, row, dim, act, ll, L, m, wsum, osum, xr_epoch & 1u, row);
+        continue;
+      }
       if (act && ll == 0) {
         const bool empty = !(wsum > 0.f);
         const int64_t oi = (static_cast<int64_t>(b) * a.Hq + hm.hq0 + g) * DH + dim;
@@ -351,6 +477,16 @@ __device__ __forceinline__ void cta_finish(const AttnArgs& a, int b, int h, int 
         else static_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(ov);
         if (dim == 0 && a.lse)
           a.lse[static_cast<int64_t>(b) * a.Hq + hm.hq0 + g] = empty ? -INFINITY : (m + __log2f(wsum)) * kLn2;
+      }
+    }
+    if constexpr (XR) {   // arrival; the last CTA of the launch records the epoch it used
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t* hdr = static_cast<uint32_t*>(a.xr_win[a.xr_rank]);
+        if (atom_add_acq_rel_gpu(hdr + 1, 1u) == static_cast<uint32_t>(a.n_items - 1)) {
+          st_relaxed_gpu(hdr + 1, 0u);
+          st_relaxed_gpu(hdr, xr_epoch);
+        }
       }
     }
     phase_mark(a.phase, (b * a.Hkv + h) * a.S + s, 5);

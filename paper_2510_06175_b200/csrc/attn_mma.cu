@@ -106,7 +106,8 @@ __device__ __forceinline__ uint32_t krow_addr(const KRowT<KB>& kr, uint32_t base
   }
 }
 
-template <int KB, int VB, int DH, bool TC>
+// XR: the fused cross-rank merge variant (vecinfer_attn_decode_xr; single-wave spin merge only)
+template <int KB, int VB, int DH, bool TC, bool XR = false>
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
   // DH = head dim (128, or 64: NEXT-4).  KS score k-steps (4 sub-vectors each) per 16 tokens,
   // VS V sub-vectors per lane r (2 P.V m-tiles each), NL lanes holding a q~ row.
@@ -907,7 +908,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   __syncthreads();
   phase_mark(a.phase, cta_id, 3);
   if (!a.cluster) {
-    cta_finish<kThreads, kNW, kWRow, DH, true>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
+    cta_finish<kThreads, kNW, kWRow, DH, true, XR>(a, b, h, s, wm, wl, wacc, reinterpret_cast<float*>(tab));
     phase_mark(a.phase, cta_id, 4);
     continue;
   }
@@ -1007,6 +1008,20 @@ static AttnKernel kernel_for(int kf, int vf, int dh = 128) {
   return table[dh == 64 ? 1 : 0][ki][vi];
 }
 
+// fused cross-rank merge variants: d = 4 K / V books, D = 128
+static AttnKernel kernel_xr(int kf, int vf) {
+  const int ki = kf == 4 ? 0 : kf == 8 ? 1 : kf == 16 ? 2 : -1, vi = vf == 4 ? 0 : vf == 8 ? 1 : vf == 16 ? 2 : -1;
+  if (ki < 0 || vi < 0) return nullptr;
+  static const AttnKernel table[3][3] = {
+      {attn_mma_kernel<4, 4, 128, false, true>, attn_mma_kernel<4, 8, 128, false, true>,
+       attn_mma_kernel<4, 16, 128, false, true>},
+      {attn_mma_kernel<8, 4, 128, false, true>, attn_mma_kernel<8, 8, 128, false, true>,
+       attn_mma_kernel<8, 16, 128, false, true>},
+      {attn_mma_kernel<16, 4, 128, false, true>, attn_mma_kernel<16, 8, 128, false, true>,
+       attn_mma_kernel<16, 16, 128, false, true>}};
+  return table[ki][vi];
+}
+
 static void set_attr(AttnKernel k, int smem) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   // carveout = the smallest that fits: the rest of the 256 KiB stays L1 (16-bit books live there)
@@ -1022,6 +1037,8 @@ static void set_attrs_once() {
         for (int vb : {4, 8, 16}) set_attr(kernel_for(kb, vb, dh), smem_for(kb, vb));
     for (int kb : {4, 8})
       for (int vb : {4, 8, 16}) set_attr(kernel_tc(kb, vb), smem_for(kb, vb));
+    for (int kb : {4, 8, 16})
+      for (int vb : {4, 8, 16}) set_attr(kernel_xr(kb, vb), smem_for(kb, vb));
 #define VECINFER_PAIR(K, V) set_attr(kernel_for(K, V), smem_for(K, V));
     VECINFER_NEXT2_PAIRS(VECINFER_PAIR)
 #undef VECINFER_PAIR
@@ -1084,7 +1101,8 @@ cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_
   }
   cfg.attrs = at;
   cfg.numAttrs = n;
-  const AttnKernel k = a.tc ? kernel_tc(kbits, vbits) : kernel_for(kbits, vbits, a.D);
+  const AttnKernel k = a.xr_P > 0 ? kernel_xr(kbits, vbits) : a.tc ? kernel_tc(kbits, vbits) : kernel_for(kbits, vbits, a.D);
+  if (!k) return cudaErrorInvalidDeviceFunction;
   return cudaLaunchKernelEx(&cfg, k, a);
 }
 

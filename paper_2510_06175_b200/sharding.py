@@ -149,6 +149,79 @@ class P2PExchange:
             self._own = None
 
 
+class XRankWindows:
+    """Peer-memory windows of the cross-GPU merge fused INTO the attention launch
+    (vecinfer_attn_decode_xr / vecinfer_decode_step_xr; "N4's epilogue stores partials
+    straight into peers' symmetric windows").  Pass as `xr=` to vecinfer.attn_decode / decode_step:
+    each rank attends its own sequence shard and the launch returns the merged o, lse on every rank.
+
+    Setup is collective over `group` (CUDA IPC handles all-gathered, peers mapped), as P2PExchange.
+    XRankWindows.local(P, ...) builds P descriptors over P windows of ONE process (ranks run as
+    concurrent launches on P streams of one GPU: the single-GPU functional tests)."""
+
+    def __init__(self, rows_max: int, D: int, device: torch.device, group=None, _local=None):
+        import ctypes
+
+        from . import _lib
+        self._lib = _lib.load()
+        self.rows_max, self.D, self.device = rows_max, D, device
+        self._opened, self._own, self._group = [], None, group
+        if _local is not None:   # (world, rank, windows tensor, err tensor, keep-alive buffers)
+            self.world, self.rank, self.windows, self.err, self._bufs = _local
+        else:
+            self.world = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+            nbytes = self._lib.vecinfer_xr_window_bytes(self.world, rows_max, D)
+            own = ctypes.c_void_p()
+            handle = (ctypes.c_char * 64)()
+            with torch.cuda.device(device):
+                _lib.check("vecinfer_p2p_window_create",
+                           self._lib.vecinfer_p2p_window_create(nbytes, ctypes.addressof(own), ctypes.addressof(handle)))
+            self._own = own.value
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(handle), group=group)
+            ptrs = []
+            with torch.cuda.device(device):
+                for p, h in enumerate(handles):
+                    if p == self.rank:
+                        ptrs.append(self._own)
+                        continue
+                    w = ctypes.c_void_p()
+                    hb = (ctypes.c_char * 64).from_buffer_copy(h)
+                    _lib.check("vecinfer_p2p_window_open",
+                               self._lib.vecinfer_p2p_window_open(ctypes.addressof(hb), ctypes.addressof(w)))
+                    ptrs.append(w.value)
+                    self._opened.append(w.value)
+            self.windows = torch.tensor(ptrs, dtype=torch.int64, device=device)
+            self.err = torch.zeros(1, dtype=torch.int32, device=device)
+            self._bufs = []
+        self._struct = _lib.XRank(self.world, self.rank, self.windows.data_ptr(), rows_max, self.err.data_ptr())
+        self.desc = ctypes.pointer(self._struct)
+
+    @classmethod
+    def local(cls, P: int, rows_max: int, D: int, device: torch.device):
+        """P single-process ranks over P in-process windows (one per rank, zero-filled)."""
+        from . import _lib
+        nbytes = _lib.load().vecinfer_xr_window_bytes(P, rows_max, D)
+        bufs = [torch.zeros(nbytes, dtype=torch.uint8, device=device) for _ in range(P)]
+        windows = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=device)
+        err = torch.zeros(1, dtype=torch.int32, device=device)
+        return [cls(rows_max, D, device, _local=(P, r, windows, err, bufs)) for r in range(P)]
+
+    def close(self):
+        """Unmap the peers' windows and free the own one (collective unless built by local())."""
+        if self._own is None:
+            return
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self._group)
+        for w in self._opened:
+            self._lib.vecinfer_p2p_window_close(w)
+        self._opened = []
+        dist.barrier(group=self._group)
+        self._lib.vecinfer_p2p_window_destroy(self._own)
+        self._own = None
+
+
 class SeqShardedStep:
     """One decode step of an L-layer model whose single long sequence is sharded over the ranks
     (BASELINE configs[3]): for every layer, this rank's attention over its token

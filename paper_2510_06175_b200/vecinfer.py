@@ -191,10 +191,12 @@ def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.
                 out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
                 workspace: torch.Tensor | None = None, k_res: torch.Tensor | None = None,
                 v_res: torch.Tensor | None = None, res_lens: torch.Tensor | None = None,
-                block_table: torch.Tensor | None = None):
+                block_table: torch.Tensor | None = None, xr=None):
     """Decode attention of q [B, H_q, D] (bf16) over the VQ cache (Eq. 10 / Alg. 1), plus an optional
     full-precision residual window k_res/v_res [B, H_kv, r_cap, D] with res_lens [B].
     With block_table [B, pages_per_seq] the code caches are page pools [n_pages, H_kv, page_size, row].
+    xr (sharding.XRankWindows): this rank's cache is one sequence shard; the launch merges the
+    ranks' partials over peer memory itself (vecinfer_attn_decode_xr) and returns the final o, lse.
     Returns (o [B, H_q, D] o_dtype, lse [B, H_q] fp32, natural log)."""
     B, Hq, D = q.shape
     Hkv, n_cap = k_codes.shape[1], k_codes.shape[2]
@@ -221,7 +223,11 @@ def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.
             _need(seq_lens, "seq_lens", torch.int32), tok_begin, tok_end, softmax_scale, num_splits, ALGOS[algo],
             _need(out, "out"), odt, _need(lse, "lse", torch.float32), ctypes.c_void_p(workspace.data_ptr()),
             workspace.numel(), _stream(q.device), _residual(k_res, v_res, res_lens))
-    if pg is not None:
+    if xr is not None:
+        if pg is not None:
+            raise ValueError("the fused cross-rank merge runs on contiguous caches")
+        check("vecinfer_attn_decode_xr", lib.vecinfer_attn_decode_xr(*args, xr.desc))
+    elif pg is not None:
         check("vecinfer_attn_decode_paged", lib.vecinfer_attn_decode_paged(*args, pg))
     else:
         check("vecinfer_attn_decode", lib.vecinfer_attn_decode(*args))
@@ -237,7 +243,7 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
                 err_flags: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
                 k_res: torch.Tensor | None = None, v_res: torch.Tensor | None = None,
                 res_lens: torch.Tensor | None = None, append_to_residual: bool = False,
-                block_table: torch.Tensor | None = None):
+                block_table: torch.Tensor | None = None, xr=None):
     """Fused layer decode step = encode_kv(T=1) of k_new/v_new [B, H_kv, D] at row write_pos[b]
     followed by attn_decode over [0, seq_lens[b]) -- one launch (vecinfer_decode_step).  With a
     residual window and append_to_residual, the new token is copied to residual row res_lens[b]-1
@@ -261,6 +267,10 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
         workspace = torch.zeros(max(need, 256), dtype=torch.uint8, device=q.device)
     fn = lib.vecinfer_decode_step_paged if pg is not None else lib.vecinfer_decode_step
     extra = (pg,) if pg is not None else ()
+    if xr is not None:   # sequence shard + fused cross-rank merge (vecinfer_decode_step_xr)
+        if pg is not None:
+            raise ValueError("the fused cross-rank merge runs on contiguous caches")
+        fn, extra = lib.vecinfer_decode_step_xr, (xr.desc,)
     check("vecinfer_decode_step", fn(
         _need(q, "q", torch.bfloat16), _need(k_new, "k_new", torch.bfloat16), _need(v_new, "v_new", torch.bfloat16),
         B, Hq, Hkv, I64x2(q.stride(0), q.stride(1)), I64x2(k_new.stride(0), k_new.stride(1)),
