@@ -294,26 +294,33 @@ def run_ours(args, rank, world, local_rank):
     fused_launch = fused and vi.decode_step_launches(B, H_KV, n_local, kcfg, vcfg, residual_append=bool(R)) == 1
     kernel_kind = vi.attn_kernel_kind(B, H_KV, n_local)
 
+    # VECINFER_ATTN_FLAG_EARLY_CACHE: seq_lens / write_pos and layer l's cache are never written by
+    # the kernel right before layer l's launch (that is layer l-1's, or an H2D copy), so the split
+    # kernel may read them and issue its first code tile before the PDL wait
+    EC = not args.no_early_cache
+
     def layer(l, ev_pair=None):
         if fused and R:   # one launch: the new token goes to residual row R-1, attention over codes + window
             vi.decode_step(q_all[l], kn_all[l][:, 0], vn_all[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
                            seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l],
-                           k_res=kres[l], v_res=vres[l], res_lens=res_lens, append_to_residual=True)
+                           k_res=kres[l], v_res=vres[l], res_lens=res_lens, append_to_residual=True, early_cache=EC)
             return
         if fused:   # one launch: append-encode of the new token + attention (vecinfer_decode_step)
             vi.decode_step(q_all[l], kn_all[l][:, 0], vn_all[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
-                           seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l])
+                           seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l],
+                           early_cache=EC)
             return
         if owns_tail:
             vi.encode_kv(kn_all[l], vn_all[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg, workspace=enc_ws)
         if ev_pair is not None:
             ev_pair[0].record()
+        ec = EC and not owns_tail   # an encode_kv launched right before writes this layer's cache
         if seq_sharded:
             vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_part[l],
-                           lse=lse_all[l], workspace=ws[l])
+                           lse=lse_all[l], workspace=ws[l], early_cache=ec)
         else:
             vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
-                           lse=lse_all[l], workspace=ws[l])
+                           lse=lse_all[l], workspace=ws[l], early_cache=ec)
         if ev_pair is not None:
             ev_pair[1].record()
         if seq_sharded:   # layer l's output feeds layer l+1: its partials are exchanged right away
@@ -384,7 +391,7 @@ def run_ours(args, rank, world, local_rank):
         with torch.cuda.graph(g_attn, stream=stream):
             for l in range(L):
                 vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
-                               lse=lse_all[l], workspace=ws[l])
+                               lse=lse_all[l], workspace=ws[l], early_cache=EC)
     torch.cuda.synchronize(dev)
 
     def barrier():
@@ -450,18 +457,19 @@ def run_ours(args, rank, world, local_rank):
         if fused:
             vi.decode_step(q_d[l], kn_d[l][:, 0], vn_d[l][:, 0], lam, inv, ck, cv, kcs[l], vcs[l], write_pos,
                            seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l], lse=lse_all[l], workspace=ws[l],
-                           **({"k_res": kres[l], "v_res": vres[l], "res_lens": res_lens,
-                               "append_to_residual": True} if R else {}))
+                           early_cache=EC, **({"k_res": kres[l], "v_res": vres[l], "res_lens": res_lens,
+                                               "append_to_residual": True} if R else {}))
             return
         if owns_tail:
             vi.encode_kv(kn_d[l], vn_d[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg, workspace=enc_ws)
+        ec = EC and not owns_tail
         if seq_sharded:
             vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_part[l],
-                           lse=lse_all[l], workspace=ws[l])
+                           lse=lse_all[l], workspace=ws[l], early_cache=ec)
             exchange_layer(l)
         else:
             vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
-                           lse=lse_all[l], workspace=ws[l])
+                           lse=lse_all[l], workspace=ws[l], early_cache=ec)
 
     def layers_e2e():
         for l in range(L):
@@ -624,7 +632,7 @@ def run_ours(args, rank, world, local_rank):
                                  f"{args.backend}-allgather+merge_lse") + ", per layer (32 exchanges per step)"
                                 if seq_sharded else None),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
-                   "num_splits": S, "attn_kernel": kernel_kind, "cuda_graph": use_graph, "residual_window": R, "fused_append": fused_launch,
+                   "num_splits": S, "attn_kernel": kernel_kind, "cuda_graph": use_graph, "residual_window": R, "fused_append": fused_launch, "early_cache": EC,
                    "dtype_detail": "u8 codes, bf16 q/k/v/o, fp16 hi/lo MMA operands, f32 accumulate",
                    "step": "DESIGN.md R16: one decoded token through the attention of all 32 layers (per layer: "
                            "append-encode of the new token + attention, one fused vecinfer_decode_step launch "
@@ -675,6 +683,8 @@ def main():
                          "per-layer exchange, strong scaling) at N>1; cfg3 = batch x head sharding (weak)")
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-early-cache", action="store_true",
+                    help="launch without VECINFER_ATTN_FLAG_EARLY_CACHE (all cache reads after the PDL wait)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N>1 (gloo: ranks may share one GPU; functional check)")
     ap.add_argument("--unfused", action="store_true", help="separate encode_kv + attn_decode launches per layer")

@@ -37,6 +37,7 @@
  *  - ABI v6 adds: the tcgen05 score variant (VECINFER_ATTN_DEQUANT_TC), d8b16, and the
  *    cross-GPU merge fused into the attention launch itself (vecinfer_attn_decode_xr,
  *    vecinfer_decode_step_xr, vecinfer_xr_window_bytes).
+ *  - ABI v7 adds: VECINFER_ATTN_FLAG_EARLY_CACHE, OR'ed into the algo argument.
  */
 #ifndef VECINFER_H_
 #define VECINFER_H_
@@ -48,7 +49,7 @@
 extern "C" {
 #endif
 
-#define VECINFER_ABI_VERSION 6
+#define VECINFER_ABI_VERSION 7
 
 typedef struct CUstream_st* vecinfer_stream_t; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -98,6 +99,18 @@ typedef enum {
   VECINFER_ATTN_DEQUANT_MMA_STREAM = 3,
   VECINFER_ATTN_DEQUANT_TC = 4
 } vecinfer_attn_algo_t;
+
+/* Launch-ordering hint OR'ed into the algo argument of the attention / decode-step calls (ABI v7):
+ * the caller promises that seq_lens, write_pos, the block table and the code caches were NOT
+ * written by the kernel immediately preceding this call on the stream (e.g. the preceding kernel
+ * is the previous layer's attention or the QKV projection; the step's seq_lens update and the
+ * cache writes of earlier launches are at least two kernels back).  The split kernel then reads
+ * them, derives its token range and issues its first code tile BEFORE the programmatic-dependent-
+ * launch wait, so under PDL these loads overlap the previous kernel's tail; q, k_new / v_new and
+ * the residual window are still read after the wait.  Results are identical with and without the
+ * flag.  Ignored by the stream and LUT kernels and by a decode step that appends with a separate
+ * encode launch (that launch writes the cache right before the attention). */
+#define VECINFER_ATTN_FLAG_EARLY_CACHE 0x100
 
 /* Paged code cache (serving integration): k_codes / v_codes are a pool of
  * n_pages pages laid out [n_pages, H_kv, page_size, row_bytes]; token t of batch row b lives in

@@ -102,6 +102,14 @@ static int stream_mode_from_env() {
 }
 }  // namespace
 
+// the algo argument without / with the VECINFER_ATTN_FLAG_EARLY_CACHE launch-ordering bit
+static vecinfer_attn_algo_t algo_base(vecinfer_attn_algo_t a) {
+  return static_cast<vecinfer_attn_algo_t>(static_cast<uint32_t>(a) & ~static_cast<uint32_t>(VECINFER_ATTN_FLAG_EARLY_CACHE));
+}
+static bool algo_early(vecinfer_attn_algo_t a) {
+  return (static_cast<uint32_t>(a) & static_cast<uint32_t>(VECINFER_ATTN_FLAG_EARLY_CACHE)) != 0;
+}
+
 struct SplitPlan;
 static SplitPlan plan_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits);
 
@@ -228,6 +236,8 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
                                    size_t workspace_bytes, vecinfer_stream_t stream, const AppendArgs* app,
                                    const vecinfer_residual_t* res, bool res_append,
                                    const vecinfer_paged_t* pg = nullptr, const vecinfer_xrank_t* xr = nullptr) {
+  const bool early = algo_early(algo);
+  algo = algo_base(algo);
   if (!q_bf16 || !lambda || !ck_bf16 || !cv_bf16 || !k_codes || !v_codes || !seq_lens || !o)
     return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: NULL pointer");
   if (o_dtype != VECINFER_BF16 && o_dtype != VECINFER_F32) return fail(VECINFER_ERR_INVALID_ARG, "attn_decode: bad o_dtype");
@@ -369,6 +379,7 @@ static vecinfer_status_t attn_impl(const void* q_bf16, int32_t B, int32_t H_q, i
   // every CTA co-resident (one CTA per SM, grid <= SMs): spin-barrier + sliced merge
   a.merge_spin = (S > 1 && !plan.cluster && !a.merge_kernel && algo != VECINFER_ATTN_LUT &&
                   static_cast<int64_t>(B) * H_kv * S <= n_sms && (xr || !getenv("VECINFER_NO_SPIN"))) ? 1 : 0;
+  a.early = early ? 1 : 0;
   a.xr_P = xr ? xr->world : 0;
   a.xr_rank = xr ? xr->rank : 0;
   a.xr_win = xr ? xr->windows : nullptr;
@@ -486,6 +497,7 @@ static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t k
 // which attention kernel a call runs: 0 split (attn_mma.cu), 1 stream (attn_stream.cu), 2 LUT
 extern "C" int32_t vecinfer_attn_kernel_kind(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits,
                                              vecinfer_attn_algo_t algo) {
+  algo = algo_base(algo);
   if (algo == VECINFER_ATTN_LUT) return 2;
   if (algo == VECINFER_ATTN_DEQUANT_TC) return 0;
   return use_stream(B, H_kv, n_tokens_max, num_splits, false, algo == VECINFER_ATTN_DEQUANT_MMA_STREAM) ? 1 : 0;
@@ -496,6 +508,7 @@ extern "C" int32_t vecinfer_decode_step_launches(int32_t B, int32_t H_kv, int64_
                                                  vecinfer_vq_t vcfg, int32_t num_splits, vecinfer_attn_algo_t algo,
                                                  int32_t residual_append) {
   if (residual_append) return 1;
+  algo = algo_base(algo);
   if (decode_fuses(B, H_kv, n_cap, kcfg, vcfg, num_splits, algo)) return 1;
   // 16-bit append (B*H_kv <= 4096 token-heads): one centroid-split search launch that also
   // finalises (the last chunk CTA of each token-head); larger batches add a finalize launch
@@ -529,15 +542,16 @@ static vecinfer_status_t decode_step_impl(const void* q_bf16, const void* k_new_
       return fail(VECINFER_ERR_INVALID_ARG, "decode_step: k_new/v_new strides must be non-negative multiples of 4");
   if (!aligned(k_new_bf16, 8) || !aligned(v_new_bf16, 8) || !aligned(inv_lambda, 16))
     return fail(VECINFER_ERR_INVALID_ARG, "decode_step: misaligned k_new/v_new/inv_lambda");
+  const vecinfer_attn_algo_t algo_b = algo_base(algo);   // (the early-cache bit stays on `algo`)
   if (residual && residual->append_new) {   // the new token goes to the residual window (raw copy)
-    if (algo == VECINFER_ATTN_LUT) return fail(VECINFER_ERR_UNSUPPORTED, "decode_step: residual needs the MMA kernel");
+    if (algo_b == VECINFER_ATTN_LUT) return fail(VECINFER_ERR_UNSUPPORTED, "decode_step: residual needs the MMA kernel");
     AppendArgs app{k_new_bf16, v_new_bf16, k_new_strides[0], k_new_strides[1], v_new_strides[0], v_new_strides[1],
                    inv_lambda, write_pos, err_flags};
     return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
                      algo, o, o_dtype, lse, workspace, workspace_bytes, stream, &app, residual, true, pg, xr);
   }
-  const bool fuse = decode_fuses(B, H_kv * hsplit_of(H_q, H_kv), n_cap, kcfg, vcfg, num_splits, algo, pg != nullptr);
+  const bool fuse = decode_fuses(B, H_kv * hsplit_of(H_q, H_kv), n_cap, kcfg, vcfg, num_splits, algo_b, pg != nullptr);
   if (!fuse) {   // separate append + attention launches (always for the paper-faithful LUT variant)
     const int64_t ks[3] = {k_new_strides[0], 0, k_new_strides[1]};
     const int64_t vs[3] = {v_new_strides[0], 0, v_new_strides[1]};
@@ -555,9 +569,10 @@ static vecinfer_status_t decode_step_impl(const void* q_bf16, const void* k_new_
                                 ck_head_stride, cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, write_pos,
                                 err_flags, ews, ew, stream);
     if (st != VECINFER_OK) return st;
+    // the encode launch just wrote the cache: the attention must not read it before its wait
     return attn_impl(q_bf16, B, H_q, H_kv, q_strides[0], q_strides[1], lambda, ck_bf16, cv_bf16, ck_head_stride,
                      cv_head_stride, kcfg, vcfg, k_codes, v_codes, n_cap, seq_lens, 0, -1, softmax_scale, num_splits,
-                     algo, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false, pg, xr);
+                     algo_b, o, o_dtype, lse, workspace, workspace_bytes, stream, nullptr, residual, false, pg, xr);
   }
   AppendArgs app{k_new_bf16, v_new_bf16, k_new_strides[0], k_new_strides[1], v_new_strides[0], v_new_strides[1],
                  inv_lambda, write_pos, err_flags};

@@ -32,6 +32,7 @@ struct AttnArgs {
   int tc;                      // 1: split kernel with the tcgen05 score contraction (VECINFER_ATTN_DEQUANT_TC)
   int merge_kernel;            // 1: split partials are merged by a separate PDL-launched kernel
   int merge_spin;              // 1: single-wave grid, every CTA merges a slice after an arrival barrier
+  int early;                   // 1: seq_lens / write_pos / codes read before the grid-dependency wait
   // stream kernel (attn_stream.cu): U = B*H_kv units and V virtual CTAs tile one line of U*V ticks
   // (unit u = [u*V, (u+1)*V), CTA c = [c*U, (c+1)*U))
   int U, V;

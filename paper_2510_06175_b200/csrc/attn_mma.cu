@@ -190,13 +190,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   const uint4 tabv = table_load<KB, VB>(cbk, cbv, tid);   // stored while seq_lens is in flight
   float4 lam4 = make_float4(0.f, 0.f, 0.f, 0.f);   // warps 0..3: lambda of head h (static)
   if (warp < 4) lam4 = *reinterpret_cast<const float4*>(a.lambda + hc * DH + 4 * (lane & (NL - 1)));
-  if (first) griddep_wait();
+  // early (VECINFER_ATTN_FLAG_EARLY_CACHE): seq_lens, write_pos and the cached codes were not
+  // written by the kernel just before on the stream, so the split range and the first tile's code
+  // loads go out before the grid-dependency wait too (under programmatic dependent launch they
+  // overlap the previous kernel's tail); only q, k_new / v_new and the residual window wait
+  const bool wait_late = first && a.early;
+  if (first && !a.early) griddep_wait();
   phase_mark(a.phase, cta_id, 9);
   first = false;
   // q of the warp's query head goes out right after the wait, next to the seq_lens read below
   uint2 qw = make_uint2(0u, 0u);
-  if (warp < hm.gp)
-    qw = *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (hm.hq0 + warp) * a.q_sh + 4 * (lane & (NL - 1)));
+  auto load_q = [&]() {
+    if (warp < hm.gp)
+      qw = *reinterpret_cast<const uint2*>(a.q + b * a.q_sb + (hm.hq0 + warp) * a.q_sh + 4 * (lane & (NL - 1)));
+  };
+  if (!wait_late) load_q();
 
   // seq_lens goes out next; the codebook table (its loads were issued before the wait) is stored
   // while it is in flight, then the split range and the first tile's loads follow
@@ -299,6 +307,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     const int rem = ntok - 32 * warp;
     if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
     else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
+  }
+  if (wait_late) {
+    griddep_wait();
+    load_q();
   }
   phase_mark(a.phase, cta_id, 13);   // first tile issued (after seq_lens)
   unsigned char* newcodes = smem_raw + kMiscNew;   // [0,64): K code row, [64,128): V code row

@@ -20,6 +20,7 @@ _lib.load()   # fail loudly at import if the native library is missing
 
 BF16, F32 = 0, 1
 ALGOS = {"auto": 0, "mma": 1, "dequant_mma": 1, "lut": 2, "stream": 3, "dequant_mma_stream": 3, "tc": 4, "dequant_tc": 4}
+EARLY_CACHE = 0x100   # VECINFER_ATTN_FLAG_EARLY_CACHE (ABI v7), OR-ed into the algo argument
 
 
 @dataclass(frozen=True)
@@ -191,12 +192,14 @@ def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.
                 out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
                 workspace: torch.Tensor | None = None, k_res: torch.Tensor | None = None,
                 v_res: torch.Tensor | None = None, res_lens: torch.Tensor | None = None,
-                block_table: torch.Tensor | None = None, xr=None):
+                block_table: torch.Tensor | None = None, xr=None, early_cache: bool = False):
     """Decode attention of q [B, H_q, D] (bf16) over the VQ cache (Eq. 10 / Alg. 1), plus an optional
     full-precision residual window k_res/v_res [B, H_kv, r_cap, D] with res_lens [B].
     With block_table [B, pages_per_seq] the code caches are page pools [n_pages, H_kv, page_size, row].
     xr (sharding.XRankWindows): this rank's cache is one sequence shard; the launch merges the
     ranks' partials over peer memory itself (vecinfer_attn_decode_xr) and returns the final o, lse.
+    early_cache: VECINFER_ATTN_FLAG_EARLY_CACHE (seq_lens and the codes were not written by the kernel
+    just before this launch on the stream: the first code tile is read before the PDL wait).
     Returns (o [B, H_q, D] o_dtype, lse [B, H_q] fp32, natural log)."""
     B, Hq, D = q.shape
     Hkv, n_cap = k_codes.shape[1], k_codes.shape[2]
@@ -220,7 +223,8 @@ def attn_decode(q: torch.Tensor, lam: torch.Tensor, ck: torch.Tensor, cv: torch.
     args = (_need(q, "q", torch.bfloat16), B, Hq, Hkv, q.stride(0), q.stride(1), _need(lam, "lambda", torch.float32),
             _need(ck, "ck", torch.bfloat16), _need(cv, "cv", torch.bfloat16), _cb_stride(ck), _cb_stride(cv),
             kcfg.c(), vcfg.c(), _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
-            _need(seq_lens, "seq_lens", torch.int32), tok_begin, tok_end, softmax_scale, num_splits, ALGOS[algo],
+            _need(seq_lens, "seq_lens", torch.int32), tok_begin, tok_end, softmax_scale, num_splits,
+            ALGOS[algo] | (EARLY_CACHE if early_cache else 0),
             _need(out, "out"), odt, _need(lse, "lse", torch.float32), ctypes.c_void_p(workspace.data_ptr()),
             workspace.numel(), _stream(q.device), _residual(k_res, v_res, res_lens))
     if xr is not None:
@@ -243,11 +247,11 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
                 err_flags: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
                 k_res: torch.Tensor | None = None, v_res: torch.Tensor | None = None,
                 res_lens: torch.Tensor | None = None, append_to_residual: bool = False,
-                block_table: torch.Tensor | None = None, xr=None):
+                block_table: torch.Tensor | None = None, xr=None, early_cache: bool = False):
     """Fused layer decode step = encode_kv(T=1) of k_new/v_new [B, H_kv, D] at row write_pos[b]
     followed by attn_decode over [0, seq_lens[b]) -- one launch (vecinfer_decode_step).  With a
     residual window and append_to_residual, the new token is copied to residual row res_lens[b]-1
-    instead (no encode) and attended from there."""
+    instead (no encode) and attended from there.  early_cache: as in attn_decode (write_pos too)."""
     B, Hq, D = q.shape
     Hkv, n_cap = k_codes.shape[1], k_codes.shape[2]
     pg = None
@@ -279,8 +283,8 @@ def decode_step(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, lam: 
         _need(cv, "cv", torch.bfloat16), _cb_stride(ck), _cb_stride(cv), kcfg.c(), vcfg.c(),
         _need(k_codes, "k_codes", torch.uint8), _need(v_codes, "v_codes", torch.uint8), n_cap,
         _need(write_pos, "write_pos", torch.int32), _need(seq_lens, "seq_lens", torch.int32), softmax_scale,
-        num_splits, ALGOS[algo], _need(out, "out"), F32 if out.dtype == torch.float32 else BF16,
-        _need(lse, "lse", torch.float32),
+        num_splits, ALGOS[algo] | (EARLY_CACHE if early_cache else 0), _need(out, "out"),
+        F32 if out.dtype == torch.float32 else BF16, _need(lse, "lse", torch.float32),
         ctypes.c_void_p(err_flags.data_ptr()) if err_flags is not None else ctypes.c_void_p(0),
         ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream(q.device),
         _residual(k_res, v_res, res_lens, append_to_residual), *extra))

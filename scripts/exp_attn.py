@@ -42,7 +42,7 @@ def _book(name, side, dev):
     return torch.from_numpy(synth.bf16_from_bits(z[f"c{side}_{name}"])).to(dev).to(torch.bfloat16)
 
 
-def run(B, N, splits, algo, reps=20, with_encode=False, paged=0, dh=128, fmt=("b2d4", "b2d4")):
+def run(B, N, splits, algo, reps=20, with_encode=False, paged=0, dh=128, fmt=("b2d4", "b2d4"), early=False):
     dev = torch.device("cuda", 0)
     z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz"))
     lam = torch.from_numpy(z["lambda"]).to(dev)
@@ -85,14 +85,16 @@ def run(B, N, splits, algo, reps=20, with_encode=False, paged=0, dh=128, fmt=("b
         for i in range(n_l):
             if with_encode == "fused":
                 vi.decode_step(q, kn[:, 0], vn[:, 0], lam, inv, ck, cv, kcs[i % copies], vcs[i % copies], wp, seq,
-                               num_splits=splits, out=o, lse=lse, workspace=ws[i % copies], kcfg=kcfg, vcfg=vcfg)
+                               num_splits=splits, out=o, lse=lse, workspace=ws[i % copies], kcfg=kcfg, vcfg=vcfg,
+                               early_cache=early)
                 continue
             if with_encode:
                 vi.encode_kv(kn, vn, inv, ck, cv, kcs[i % copies], vcs[i % copies], wp, kcfg, vcfg, block_table=bt)
             if algo == "none":
                 continue
             vi.attn_decode(q, lam, ck, cv, kcs[i % copies], vcs[i % copies], seq, num_splits=splits, algo=algo,
-                           out=o, lse=lse, workspace=ws[i % copies], block_table=bt, kcfg=kcfg, vcfg=vcfg)
+                           out=o, lse=lse, workspace=ws[i % copies], block_table=bt, kcfg=kcfg, vcfg=vcfg,
+                           early_cache=early and not with_encode)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(s):      # CUDAGraph.replay() launches on the CURRENT stream
         g.replay()
@@ -108,7 +110,7 @@ def run(B, N, splits, algo, reps=20, with_encode=False, paged=0, dh=128, fmt=("b
         V = vi.attn_num_ctas(B, 8, N, splits)
     except Exception:
         V = -1
-    print(f"{fmt[0]}/{fmt[1]} B={B:3d} N={N:7d} S={S:3d} V={V:4d} algo={algo:4s} enc={with_encode}: {us:8.2f} us/launch  {nbytes / us / 1e3:7.0f} GB/s  "
+    print(f"{'early ' if early else ''}{fmt[0]}/{fmt[1]} B={B:3d} N={N:7d} S={S:3d} V={V:4d} algo={algo:4s} enc={with_encode}: {us:8.2f} us/launch  {nbytes / us / 1e3:7.0f} GB/s  "
           f"({100 * nbytes / us / 1e3 / 6553.6:.1f}% of 6553.6)  cyc/token-head@1.9GHz/SM={us * 1.9e3 * 148 / (B * 8 * N):.2f}",
           flush=True)
 
@@ -118,13 +120,15 @@ if __name__ == "__main__":
     ap.add_argument("--case", action="append", required=True)
     ap.add_argument("--paged", type=int, default=0, help="page size of a random-permuted paged cache (0: contiguous)")
     ap.add_argument("--dh", type=int, default=128, help="head dim (128 or 64)")
+    ap.add_argument("--early", action="store_true", help="VECINFER_ATTN_FLAG_EARLY_CACHE launches")
     ap.add_argument("--fmt", action="append", default=None, help="K,V formats, e.g. d8b12,d8b8 (default b2d4,b2d4)")
     args = ap.parse_args()
     for f in args.fmt or ["b2d4,b2d4"]:
         for c in args.case:
             p = c.split(",")
             run(int(p[0]), int(p[1]), int(p[2]), p[3] if len(p) > 3 else "mma", paged=args.paged, dh=args.dh,
-                with_encode=(p[4] if p[4] == "fused" else True) if len(p) > 4 else False, fmt=tuple(f.split(",")))
+                with_encode=(p[4] if p[4] == "fused" else True) if len(p) > 4 else False, fmt=tuple(f.split(",")),
+                early=args.early)
     from paper_2510_06175_b200 import _lib
     lib = _lib.load()
     print("max active clusters (size: n):", {c: lib.vecinfer_debug_attn_max_clusters(c) for c in (2, 4, 8, 12, 16)})

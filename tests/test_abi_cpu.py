@@ -38,7 +38,7 @@ def test_every_declared_symbol_is_exported(lib):
     for name in declared_functions():
         assert hasattr(lib, name), f"{name} not exported"
         assert name in _lib.PROTOTYPES, f"{name} missing from the Python prototypes"
-    assert lib.vecinfer_abi_version() == 6
+    assert lib.vecinfer_abi_version() == 7
 
 
 def test_library_contains_sm100a_code(lib):
