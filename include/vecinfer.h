@@ -107,9 +107,10 @@ typedef enum {
  * cache writes of earlier launches are at least two kernels back).  The split kernel then reads
  * them, derives its token range and issues its first code tile BEFORE the programmatic-dependent-
  * launch wait, so under PDL these loads overlap the previous kernel's tail; q, k_new / v_new and
- * the residual window are still read after the wait.  Results are identical with and without the
- * flag.  Ignored by the stream and LUT kernels and by a decode step that appends with a separate
- * encode launch (that launch writes the cache right before the attention). */
+ * the residual window are still read after the wait.  The stream kernel does the same for its
+ * first round (its segments and first tiles) when no residual window is given.  Results are
+ * identical with and without the flag.  Ignored by the LUT kernel and by a decode step that appends
+ * with a separate encode launch (that launch writes the cache right before the attention). */
 #define VECINFER_ATTN_FLAG_EARLY_CACHE 0x100
 
 /* Paged code cache (serving integration): k_codes / v_codes are a pool of

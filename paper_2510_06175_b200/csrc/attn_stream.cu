@@ -268,15 +268,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       float4 lam4 = make_float4(0.f, 0.f, 0.f, 0.f);
       if (qwarp) lam4 = *reinterpret_cast<const float4*>(a.lambda + (qseg ? hmB.hc : hmA.hc) * DH + 4 * (lane & (NL - 1)));
       const int q_gp = qseg ? hmB.gp : hmA.gp;
-      if (first) griddep_wait();
+      // VECINFER_ATTN_FLAG_EARLY_CACHE (no residual window): the segments (seq_lens, write_pos) and
+      // the first tiles' code loads go out before the grid-dependency wait; q after it
+      const bool wait_late = first && a.early && !a.res;
+      if (first && !wait_late) griddep_wait();
       first = false;
 
       // ---- dynamic inputs
       uint2 qw = make_uint2(0u, 0u);
-      if (qwarp && qg < q_gp) {
-        const int bq = qseg && hB == 0 ? bA + 1 : bA, hq0 = qseg ? hmB.hq0 : hmA.hq0;
-        qw = *reinterpret_cast<const uint2*>(a.q + bq * a.q_sb + (hq0 + qg) * a.q_sh + 4 * (lane & (NL - 1)));
-      }
+      auto load_q = [&]() {
+        if (qwarp && qg < q_gp) {
+          const int bq = qseg && hB == 0 ? bA + 1 : bA, hq0 = qseg ? hmB.hq0 : hmA.hq0;
+          qw = *reinterpret_cast<const uint2*>(a.q + bq * a.q_sb + (hq0 + qg) * a.q_sh + 4 * (lane & (NL - 1)));
+        }
+      };
+      if (!wait_late) load_q();
       // ---- segments and warp assignment: the round's 16-token sub-tiles (A's, then B's) go to
       // the warps in contiguous balanced ranges [w*ns/16, (w+1)*ns/16); segment A = warps
       // [0, nwA), segment B = warps [b0, 16) (at most one warp in both: it straddles).  Warp 0
@@ -394,6 +400,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         t_step = sg.P * nw;
       };
       if (np > 0) setup_piece();
+      if (wait_late) {
+        griddep_wait();
+        load_q();
+      }
       if (ua == u_first) phase_mark(a.phase, vc, 12);
 
       // ---- query transform (Eq. 7): sq[seg][g] = ((q_g * lambda) H) * qscale

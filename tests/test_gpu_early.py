@@ -66,10 +66,22 @@ def test_early_attention_paged():
     _assert_close(*outs[1], *_run_ref(c))
 
 
-@pytest.mark.parametrize("splits", [0, 3])
-def test_early_decode_step_fused_append(splits):
+@pytest.mark.parametrize("lens", [[2048] * 20, [3000, 17, 0, 1500, 999]])
+def test_early_stream_kernel(lens):
+    """The stream partition (forced, and AUTO at B * H_kv >= #SMs) with the flag: bit-identical."""
+    c = _attn_case(len(lens), 8, 4, max(lens) + 16, lens, seed=960 + len(lens))
+    algo = "auto" if len(lens) >= 19 else "stream"
+    if algo == "auto":
+        assert vi.attn_kernel_kind(len(lens), 8, max(lens) + 16) == "stream"
+    o0, L0 = _attn(c, False, algo=algo)
+    o1, L1 = _attn(c, True, algo=algo)
+    assert np.array_equal(o0, o1) and np.array_equal(L0, L1)
+    _assert_close(o1, L1, *_run_ref(c))
+
+
+@pytest.mark.parametrize("splits,lens", [(0, [1500, 37]), (3, [1500, 37]), (0, [600] * 20)])   # B = 20: stream
+def test_early_decode_step_fused_append(splits, lens):
     """decode_step with the flag: the appended codes are the oracle's; output == flagless launch."""
-    lens = [1500, 37]
     B = len(lens)
     res = []
     for early in (False, True):
