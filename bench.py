@@ -262,8 +262,16 @@ def run_ours(args, rank, world, local_rank):
     prefill_tok_s = B * n_local / (prefill_ms / 1e3)
     # ALU roofline of the encode: the pinned distance costs 4 sub + 4 mul + 3 add per (sub-vector,
     # centroid) pair at 128 fp32 lanes/clk/SM (N2)
-    prefill_alu_frac = (prefill_tok_s * H_KV * (D // 4) * ((1 << kbits) + (1 << vbits)) * 11 /
-                        (128 * torch.cuda.get_device_properties(dev).multi_processor_count * 1.965e9))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    # 4/8-bit books: the full pinned scan on the fp32 ALU; 16-bit books (65 536 entries): the
+    # tensor-core filter bounds the encode -- one mma.sync m16n8k16 per 128 (sub-vector, centroid)
+    # pairs at the measured 0.465 HMMA/clk/SM (profiles/r01_ubench_hmma_lds_hbm.txt); the exact
+    # rescans of the selected chunks are counted as overhead
+    pairs16 = sum(1 << b for b in (kbits, vbits) if b == 16)
+    pairs_alu = sum(1 << b for b in (kbits, vbits) if b != 16)
+    tok_t = H_KV * (D // 4) * (pairs_alu * 11 / (128 * n_sm * 1.965e9) + pairs16 / (128 * 0.465 * n_sm * 1.965e9))
+    prefill_bound = "mma.sync filter (HMMA rate)" if pairs16 else "fp32 ALU (pinned distance)"
+    prefill_alu_frac = prefill_tok_s * tok_t
     kcs = [kc0] + [kc0.clone() for _ in range(L - 1)]
     vcs = [vc0] + [vc0.clone() for _ in range(L - 1)]
     # cache layout seen by the kernels: rows [0, n_local) of this rank's shard
@@ -665,7 +673,7 @@ def run_ours(args, rank, world, local_rank):
                   (f"batch slice {B} of {B_glob} sequences per rank" if args.workload == "cfg3" else "replica")}
                  if world > 1 else None),
         "clocks": clk.summary(),
-        "prefill_encode": {"tokens_per_s": prefill_tok_s, "alu_frac": prefill_alu_frac,
+        "prefill_encode": {"tokens_per_s": prefill_tok_s, "alu_frac": prefill_alu_frac, "bound": prefill_bound,
                            "note": "bulk vecinfer_encode_kv, all 8 KV heads, K+V, 4096-token chunks back to back after a warm-up"},
         "setup_s": gen_s,
     }

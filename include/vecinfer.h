@@ -203,11 +203,15 @@ vecinfer_status_t vecinfer_calibrate_smooth(const void* k_cal_bf16, int64_t n_to
  *   write_pos        device int32 [B]: cache row of token t = 0 of batch b (e.g. seq_len).
  *   err_flags        device uint32 (may be NULL): VECINFER_FLAG_* bits are OR-ed in.
  *   workspace        >= vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg, vcfg) bytes (0 for
- *                    4/8-bit codebooks, which are searched from shared memory; 16-bit
- *                    codebooks are searched by centroid-split CTAs that combine partial
- *                    minima with 64-bit atomicMin on (dist_bits << 32 | index), plus one
- *                    arrival counter per token-head for the in-kernel finalize of the decode
- *                    append: B*T*H_kv*(2*32*8 + 4) bytes; any contents, the call fills it and leaves it zero).
+ *                    4/8-bit codebooks, which are searched from shared memory).  16-bit codebooks
+ *                    (65 536 entries) are searched in passes of <= 512 token-heads by a tensor-core
+ *                    filter (mma bf16 over a_j = ||c_j||^2 - 2 x.c_j with a rigorous error bound)
+ *                    that keeps, per sub-vector and 512-centroid chunk, bounds on the chunk's best
+ *                    approximate distance, and an exact selection that rescans only the chunks
+ *                    that can hold the pinned-distance argmin (codes identical to the full scan):
+ *                    min(B*T, max(1, 512/H_kv)) * H_kv * 64 KiB.  Contents on entry are never read
+ *                    before written; every word the call writes is zero again on exit (a
+ *                    zero-filled workspace stays zero).  ABI v7: was B*T*H_kv*516 bytes.
  * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, WORKSPACE, CUDA.
  * ------------------------------------------------------------------------------------- */
 size_t vecinfer_encode_workspace_bytes(int32_t B, int32_t T, int32_t H_kv, vecinfer_vq_t kcfg,

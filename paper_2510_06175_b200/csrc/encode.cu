@@ -333,6 +333,300 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_nn16_finalize(EncArgs a
   finalize_token_head(a, bt, static_cast<int>(bt / a.T), static_cast<int>(bt % a.T), h, lane);
 }
 
+
+// ------------------------------------------------------------------ 16-bit: tensor-core filter
+// Exact nearest-centroid search over a 65 536-entry book in two launches (decode append and bulk).
+//
+// Filter (nn16_filter_kernel, mma.sync bf16 -> fp32): with D_j = ||x - c_j||^2 = ||x||^2 + a_j,
+// a_j = ||c_j||^2 - 2 x.c_j is a dense contraction over K = 16: A row (sub-vector x) =
+// [-2x split into three bf16 parts (hi, mid, lo: exact, 24 bits) | 1, 1, 1 | 0], B column
+// (centroid c, bf16-exact) = [c | c | c | ||c||^2 as three bf16 parts | 0].  Every product is
+// exact; only the tensor core's fp32 accumulation rounds, by at most 17 * 2^-23 * S with
+// S = sum |terms| <= 2.1 ||x||_1 max|c_i| + 1.01 max ||c||^2 (bounds per 512-centroid chunk).  For
+// each (sub-vector, chunk) the filter stores lo = min_j~ a~_j - E and hi = min_j~ a~_j + E with
+// E = 2^-17 S (4x the accumulation bound), so lo <= a_j for every j of the chunk and hi >= a_j of
+// the chunk's approximate argmin.
+//
+// Selection (nn16_select_kernel): the pinned distance (fp32 RN, no FMA, reading R9) of any
+// centroid is D_j (1 + delta), |delta| <= 7 * 2^-24.  U = min_k (||x||^2 + hi_k) (1 + 2^-19) + slack
+// bounds the minimum pinned distance from above; a chunk can hold the pinned argmin only if
+// (||x||^2 + lo_k) (1 - 2^-19) - slack <= U.  Every such chunk (usually one) is scanned with the
+// exact pinned distance and the (dist_bits << 32 | index) minimum -- lowest index on ties -- is
+// the code: bit-identical to the full scan, at ~1/100 of its ALU work.  The workspace entries are
+// written by the filter and zeroed by the selection that consumes them.
+constexpr int kNC16 = 128;          // chunks of the 65 536-entry book
+constexpr int kCS16 = 512;          // centroids per chunk (64 n-tiles of 8)
+constexpr int kFW16 = 8;            // warps per filter CTA: two m16 tiles (32 rows) each
+constexpr int kRows16 = 32 * kFW16; // book rows per filter CTA
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%10,%10,%10};\n"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(0.f));
+}
+
+__device__ __forceinline__ uint32_t bf16_bits_rn(float v) {
+  return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
+}
+// v = p0 + p1 + p2 exactly (three bf16 parts of an fp32 value)
+__device__ __forceinline__ void split3_bf16(float v, uint32_t& p0, uint32_t& p1, uint32_t& p2) {
+  p0 = bf16_bits_rn(v);
+  const float r1 = v - __uint_as_float(p0 << 16);
+  p1 = bf16_bits_rn(r1);
+  const float r2 = r1 - __uint_as_float(p1 << 16);
+  p2 = bf16_bits_rn(r2);
+}
+
+// book z of the launch -> stream s (0 = K, 1 = V) and head hb (per-head books) / shared flag
+__device__ __forceinline__ void nn16_book(const EncArgs& a, int z, int& s, int& hb, bool& shared) {
+  const bool k16 = a.kbits == 16, v16 = a.vbits == 16;
+  const int nk = k16 ? (a.ck_hs ? a.H : 1) : 0;
+  s = z < nk ? 0 : 1;
+  hb = s == 0 ? z : z - nk;
+  shared = (s == 0 ? a.ck_hs : a.cv_hs) == 0;
+  (void)v16;
+}
+
+// workspace (float2 lo/hi) of sub-vector m, stream s, token-head (btl, h) of the pass
+__device__ __forceinline__ int64_t nn16_ws_row(const EncArgs& a, int64_t btl, int h, int s, int m) {
+  return (((btl * a.H + h) * 2 + s) * 32 + m) * kNC16;
+}
+
+// grid (kNC16 / ncpb, row blocks, books); rows of book (s, hb): (token, [head,] sub-vector) of the
+// pass.  A CTA filters its 256 rows against ncpb consecutive chunks: the rows' x and A fragments are
+// built once, the chunks go through two shared fragment buffers (chunk c + 1 is staged -- its
+// centroids prefetched into registers a chunk earlier -- while c is multiplied).
+__global__ void __launch_bounds__(kFW16 * 32) nn16_filter_kernel(EncArgs a, int64_t bt0, int nbt_p, int ncpb) {
+  __shared__ uint2 sfrag[2][(kCS16 / 8) * 32];   // B fragments of a chunk's 64 n-tiles (2 x 16 KiB)
+  __shared__ float sx[kFW16][32][4];
+  __shared__ float sbnd[2][kFW16][2];            // per-warp (max |c_i|, max ||c||^2) of the staged chunk
+  int s, hb;
+  bool shared;
+  nn16_book(a, blockIdx.z, s, hb, shared);
+  const int nsub = a.nsub;
+  const int64_t rows = static_cast<int64_t>(nbt_p) * (shared ? a.H : 1) * nsub;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kRows16;
+  if (row0 >= rows) return;   // (per-head books have H x fewer rows than the grid is sized for)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int chunk0 = blockIdx.x * ncpb;
+  // centroids (static codebook) are loaded before the grid-dependency wait; column j of n-tile nt =
+  // centroid chunk * 512 + 8 nt + j; lane (j, t) of the fragment holds k = 2t, 2t+1 | 2t+8, 2t+9
+  const uint16_t* cbook = s == 0 ? a.ck + hb * a.ck_hs : a.cv + hb * a.cv_hs;
+  constexpr int kPer = kCS16 / (kFW16 * 32);
+  uint2 cw[kPer];
+  auto prefetch = [&](int chunk) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q)
+      cw[q] = *reinterpret_cast<const uint2*>(cbook + (static_cast<int64_t>(chunk) * kCS16 + tid + kFW16 * 32 * q) * 4);
+  };
+  auto stage = [&](int buf) {
+    float cmax = 0.f, nmax = 0.f;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int i = tid + kFW16 * 32 * q;
+      const uint2 w = cw[q];
+      const float c0 = __uint_as_float(w.x << 16), c1 = __uint_as_float(w.x & 0xFFFF0000u);
+      const float c2 = __uint_as_float(w.y << 16), c3 = __uint_as_float(w.y & 0xFFFF0000u);
+      const float n = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(c0, c0), __fmul_rn(c1, c1)), __fmul_rn(c2, c2)), __fmul_rn(c3, c3));
+      uint32_t n0, n1, n2;
+      split3_bf16(n, n0, n1, n2);
+      cmax = fmaxf(cmax, fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))));
+      nmax = fmaxf(nmax, n);
+      uint2* f = sfrag[buf] + (i >> 3) * 32 + (i & 7) * 4;
+      f[0] = make_uint2(w.x, w.x);                 // k 0,1 | 8,9   = c0 c1 | c0 c1
+      f[1] = make_uint2(w.y, w.y);                 // k 2,3 | 10,11 = c2 c3 | c2 c3
+      f[2] = make_uint2(w.x, n0 | (n1 << 16));     // k 4,5 | 12,13 = c0 c1 | n0 n1
+      f[3] = make_uint2(w.y, n2);                  // k 6,7 | 14,15 = c2 c3 | n2 0
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, off));
+      nmax = fmaxf(nmax, __shfl_xor_sync(0xffffffffu, nmax, off));
+    }
+    if (lane == 0) { sbnd[buf][warp][0] = cmax; sbnd[buf][warp][1] = nmax; }
+  };
+  prefetch(chunk0);
+  griddep_wait();   // k / v may come from the previous kernel; the workspace is reused across passes
+  // x of the warp's 32 rows (lane l <-> row 32 warp + l): nsub = 32: one token-head; 16: two
+  const int64_t wr0 = row0 + 32 * warp;
+  float xr[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int part = 0; part < 32 / nsub; ++part) {
+    const int64_t th = (wr0 + part * nsub) / nsub;
+    if (wr0 + part * nsub >= rows) break;
+    const int64_t btl = shared ? th / a.H : th;
+    const int h = shared ? static_cast<int>(th % a.H) : hb;
+    const int64_t bt = bt0 + btl;
+    const int b = static_cast<int>(bt / a.T), tt = static_cast<int>(bt % a.T);
+    float x[4];
+    if (s == 0) transform_key_lane(a, b, tt, h, lane, x);
+    else load_value_lane(a, b, tt, h, lane, x);
+    if ((lane >= part * nsub && lane < (part + 1) * nsub) || nsub == 32) {
+      xr[0] = x[0]; xr[1] = x[1]; xr[2] = x[2]; xr[3] = x[3];
+    }
+  }
+  stage(0);
+  if (ncpb > 1) prefetch(chunk0 + 1);
+  *reinterpret_cast<float4*>(sx[warp][lane]) = make_float4(xr[0], xr[1], xr[2], xr[3]);
+  __syncthreads();
+  // A fragments of the two m16 tiles: row r0 = 16 mt + g, r1 = r0 + 8
+  uint32_t af[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const float* x0 = sx[warp][16 * mt + g];
+    const float* x1 = sx[warp][16 * mt + g + 8];
+    const int c = (t & 1) * 2;   // components c, c + 1
+    uint32_t h0[2], m0[2], l0[2], h1[2], m1[2], l1[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      split3_bf16(-2.f * x0[c + u], h0[u], m0[u], l0[u]);
+      split3_bf16(-2.f * x1[c + u], h1[u], m1[u], l1[u]);
+    }
+    const uint32_t one = 0x3F80u;
+    if (t < 2) {   // k 2t, 2t+1 = hi parts; k 2t+8, 2t+9 = lo parts
+      af[mt][0] = h0[0] | (h0[1] << 16); af[mt][1] = h1[0] | (h1[1] << 16);
+      af[mt][2] = l0[0] | (l0[1] << 16); af[mt][3] = l1[0] | (l1[1] << 16);
+    } else {       // k 2t = 4 + c: mid parts; k 12..15 = 1, 1, 1, 0
+      af[mt][0] = m0[0] | (m0[1] << 16); af[mt][1] = m1[0] | (m1[1] << 16);
+      af[mt][2] = t == 2 ? (one | (one << 16)) : one;
+      af[mt][3] = af[mt][2];
+    }
+  }
+  // per-row constants of the epilogue: the row's ||x||_1 and its workspace row
+  for (int ci = 0; ci < ncpb; ++ci) {
+    const int buf = ci & 1;
+    float mn[2][2] = {{INFINITY, INFINITY}, {INFINITY, INFINITY}};
+#pragma unroll 4
+    for (int nt = 0; nt < kCS16 / 8; ++nt) {
+      const uint2 bf = sfrag[buf][nt * 32 + lane];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        float d[4];
+        mma_bf16_16816(d, af[mt][0], af[mt][1], af[mt][2], af[mt][3], bf.x, bf.y);
+        mn[mt][0] = fminf(mn[mt][0], fminf(d[0], d[1]));
+        mn[mt][1] = fminf(mn[mt][1], fminf(d[2], d[3]));
+      }
+    }
+    float cm = 0.f, nm = 0.f;
+#pragma unroll
+    for (int w = 0; w < kFW16; ++w) { cm = fmaxf(cm, sbnd[buf][w][0]); nm = fmaxf(nm, sbnd[buf][w][1]); }
+    const int chunk = chunk0 + ci;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float v = mn[mt][hf];
+        v = fminf(v, __shfl_xor_sync(0xffffffffu, v, 1));
+        v = fminf(v, __shfl_xor_sync(0xffffffffu, v, 2));
+        const int rl = 16 * mt + g + 8 * hf;   // row of the warp
+        const int64_t r = wr0 + rl;
+        if (t != 0 || r >= rows) continue;
+        const float* xx = sx[warp][rl];
+        const float x1n = fabsf(xx[0]) + fabsf(xx[1]) + fabsf(xx[2]) + fabsf(xx[3]);
+        const float E = 0x1p-17f * (2.1f * x1n * cm + 1.01f * nm);
+        const int m = static_cast<int>(r % nsub);
+        const int64_t th = r / nsub;
+        const int64_t btl = shared ? th / a.H : th;
+        const int h = shared ? static_cast<int>(th % a.H) : hb;
+        reinterpret_cast<float2*>(a.ws)[nn16_ws_row(a, btl, h, s, m) + chunk] = make_float2(v - E, v + E);
+      }
+    if (ci + 1 < ncpb) {   // stage chunk ci + 1 into the other buffer (last read in iteration ci - 1)
+      stage(buf ^ 1);
+      if (ci + 2 < ncpb) prefetch(chunk0 + ci + 2);
+      __syncthreads();
+    }
+  }
+}
+
+// grid (pass token rows, H, 2 streams x 4 row groups), 8 warps: warp w of row group z selects and
+// stores the 16-bit code of sub-vector m = 8 z + w (one memory round trip for the chunk bounds,
+// one per scanned chunk: the chunk is copied into the warp's shared buffer with every cp.async of a
+// lane in flight).  A 4/8-bit stream is encoded by warp 0 of its row group 0.
+constexpr int kSelWarps = 8;
+constexpr int kSelSmem = kSelWarps * kCS16 * 8;   // one 4 KiB chunk buffer per warp
+__global__ void __launch_bounds__(kSelWarps * 32) nn16_select_kernel(EncArgs a, int64_t bt0) {
+  __shared__ __align__(16) unsigned char sel_smem[kSelSmem];
+  griddep_wait();
+  const int64_t btl = blockIdx.x, bt = bt0 + btl;
+  const int h = blockIdx.y, s = blockIdx.z >> 2, grp = blockIdx.z & 3;
+  const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nsub = a.nsub;
+  const int bits = s ? a.vbits : a.kbits;
+  const uint16_t* cb = s ? a.cv + h * a.cv_hs : a.ck + h * a.ck_hs;
+  const int m = kSelWarps * grp + warp;
+  if (bits == 16 ? m >= nsub : (grp != 0 || warp != 0)) return;
+  float x[4];
+  if (s == 0) transform_key_lane(a, b, t, h, lane, x);
+  else load_value_lane(a, b, t, h, lane, x);
+  if (bits != 16) {   // 4/8-bit stream next to a 16-bit one: the shared-nothing small scan
+    int64_t row;
+    if (!cache_row(a, b, t, h, lane, row)) return;
+    uint32_t code;
+    if (bits == 8) small_nn_global<8>(cb, x, code);
+    else small_nn_global<4>(cb, x, code);
+    store_code(s ? a.vcodes : a.kcodes, bits, row, lane, code, nsub);
+    return;
+  }
+  const uint32_t sbuf = smem_u32(sel_smem) + static_cast<uint32_t>(warp * kCS16 * 8);
+  float xm[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) xm[i] = __shfl_sync(0xffffffffu, x[i], m);
+  const float X2 = xm[0] * xm[0] + xm[1] * xm[1] + xm[2] * xm[2] + xm[3] * xm[3];
+  const float slack = 0x1p-20f * X2;
+  float2* pm = reinterpret_cast<float2*>(a.ws) + nn16_ws_row(a, btl, h, s, m);
+  float2 lh[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) lh[i] = __ldcg(pm + lane + 32 * i);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) __stcg(pm + lane + 32 * i, make_float2(0.f, 0.f));   // consumed
+  float U = INFINITY;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) U = fminf(U, (X2 + lh[i].y + slack) * (1.f + 0x1p-19f));
+#pragma unroll
+  for (int off = 16; off; off >>= 1) U = fminf(U, __shfl_xor_sync(0xffffffffu, U, off));
+  unsigned selm[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) selm[i] = __ballot_sync(0xffffffffu, (X2 + lh[i].x - slack) * (1.f - 0x1p-19f) <= U);
+  unsigned long long best = ~0ull;
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    unsigned sel = i == 0 ? selm[0] : i == 1 ? selm[1] : i == 2 ? selm[2] : selm[3];
+    while (sel) {
+      const int k = __ffs(sel) - 1 + 32 * i;
+      sel &= sel - 1;
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(cb + static_cast<int64_t>(k) * kCS16 * 4);
+#pragma unroll
+      for (int q = 0; q < kCS16 * 8 / 16 / 32; ++q)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbuf + 16 * (lane + 32 * q)),
+                     "l"(src + 16 * (lane + 32 * q)) : "memory");
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+#pragma unroll 4
+      for (int q = 0; q < kCS16 / 32; ++q) {
+        const float4 c = bf16x4_to_float4(lds_u64(sbuf + 8 * (32 * q + lane)));
+        const float dd = pinned_dist4(xm[0], xm[1], xm[2], xm[3], c.x, c.y, c.z, c.w);
+        const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(dd)) << 32) |
+                                       static_cast<uint32_t>(k * kCS16 + 32 * q + lane);
+        best = key < best ? key : best;
+      }
+      __syncwarp();   // the buffer is read before the next chunk's copies overwrite it
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, off);
+    best = o < best ? o : best;
+  }
+  int64_t row;
+  if (!cache_row(a, b, t, h, lane, row)) return;
+  if (lane == 0)   // 16-bit codes: sub-vector m is the little-endian u16 at byte 2m of the row
+    reinterpret_cast<uint16_t*>((s ? a.vcodes : a.kcodes) + row * (nsub * 2))[m] = static_cast<uint16_t>(best & 0xFFFFull);
+}
+
 // ------------------------------------------------------------------ NEXT-2 formats
 // d8b8 / d8b12 / d4b10 / d2b8, D = 128.  One CTA of 256 threads
 // per (token-head, K or V): warp 0 produces the row (key: the pinned smooth + integer FWHT above;
@@ -412,12 +706,33 @@ bool vq_supported(const vecinfer_vq_t& c) { return vq_d4(c) || vq_next2(c); }
 
 using namespace vecinfer;
 
+// token rows (b, t) per filter + selection pass: about 512 token-heads (32 MiB of workspace)
+static int64_t nn16_pass_rows(int64_t nbt, int H) {
+  int64_t p = 512 / (H > 0 ? H : 1);
+  if (p < 1) p = 1;
+  return nbt < p ? nbt : p;
+}
+
 extern "C" size_t vecinfer_encode_workspace_bytes(int32_t B, int32_t T, int32_t H_kv, vecinfer_vq_t kcfg,
                                                   vecinfer_vq_t vcfg) {
   if (B <= 0 || T <= 0 || H_kv <= 0) return 0;
   if (kcfg.code_bits != 16 && vcfg.code_bits != 16) return 0;
-  // packed minima [B*T*H][2][32] u64, then one arrival counter per token-head (decode append path)
-  return static_cast<size_t>(B) * T * H_kv * (2 * 32 * sizeof(unsigned long long) + sizeof(uint32_t));
+  // tensor-core filter: (lo, hi) per (token-head, stream, sub-vector, 512-centroid chunk) of one
+  // pass of nn16_pass_rows(...) token rows (fp32 pairs: 64 KiB per token-head)
+  // (the full-scan experiment behind VECINFER_NN16_SCAN=1 needs B*T*H_kv*516 bytes: packed minima +
+  // one arrival counter per token-head; it fails with VECINFER_ERR_WORKSPACE if this is smaller)
+  return static_cast<size_t>(nn16_pass_rows(static_cast<int64_t>(B) * T, H_kv)) * H_kv * 2 * 32 * kNC16 * 2 * sizeof(float);
+}
+
+// VECINFER_NN16_SCAN=1: 16-bit codes by the full pinned scan (centroid-split CTAs) instead of the
+// tensor-core filter (A/B experiments; same codes)
+static bool nn16_scan_from_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VECINFER_NN16_SCAN");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int32_t B, int32_t T,
@@ -480,8 +795,33 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
     if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_generic_kernel: %s", cudaGetErrorString(e)); }
     return check_launch("encode_generic_kernel");
   }
-  if (kcfg.code_bits == 16 || vcfg.code_bits == 16) {
+  if ((kcfg.code_bits == 16 || vcfg.code_bits == 16) && !nn16_scan_from_env()) {
+    // tensor-core filter + exact selection (two PDL launches per pass of ~512 token-heads)
     const size_t need = vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg, vcfg);
+    if (!workspace || workspace_bytes < need || !aligned(workspace, 16))
+      return fail(VECINFER_ERR_WORKSPACE, "encode_kv: 16-bit codebooks need %zu bytes of workspace", need);
+    if (kcfg.head_dim != 128 && kcfg.head_dim != 64) return fail(VECINFER_ERR_UNSUPPORTED, "encode_kv: 16-bit head_dim");
+    const int64_t np = nn16_pass_rows(nbt, H_kv);
+    const int nbk = (kcfg.code_bits == 16 ? (ck_head_stride ? H_kv : 1) : 0) +
+                    (vcfg.code_bits == 16 ? (cv_head_stride ? H_kv : 1) : 0);
+    for (int64_t b0 = 0; b0 < nbt; b0 += np) {
+      const int nb = static_cast<int>(nbt - b0 < np ? nbt - b0 : np);
+      // rows of the largest book (shared books hold every head's rows)
+      const int64_t rows = static_cast<int64_t>(nb) * H_kv * a.nsub;
+      const int64_t rblk = (rows + kRows16 - 1) / kRows16;
+      // chunks per CTA: amortise the rows' transform over up to 8 chunks while keeping >= ~4 CTAs per SM
+      int ncpb = 8;
+      while (ncpb > 1 && (kNC16 / ncpb) * rblk * nbk < 4 * device_sm_count()) ncpb >>= 1;
+      const dim3 g1(kNC16 / ncpb, static_cast<unsigned>(rblk), static_cast<unsigned>(nbk));
+      cudaError_t e = launch_pdl(nn16_filter_kernel, g1, dim3(kFW16 * 32), 0, st, a, b0, nb, ncpb);
+      if (e == cudaSuccess)
+        e = launch_pdl(nn16_select_kernel, dim3(static_cast<unsigned>(nb), H_kv, 8), dim3(kSelWarps * 32), 0, st, a, b0);
+      if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_kv (16-bit): %s", cudaGetErrorString(e)); }
+    }
+    return check_launch("encode_kv (16-bit)");
+  }
+  if (kcfg.code_bits == 16 || vcfg.code_bits == 16) {   // VECINFER_NN16_SCAN=1: the full pinned scan
+    const size_t need = static_cast<size_t>(B) * T * H_kv * (2 * 32 * sizeof(unsigned long long) + sizeof(uint32_t));
     if (!workspace || workspace_bytes < need || !aligned(workspace, 8))
       return fail(VECINFER_ERR_WORKSPACE, "encode_kv: 16-bit codebooks need %zu bytes of workspace", need);
     // minima start at ~0 and the arrival counters at 0xFFFFFFFF; the kernels zero every word they

@@ -96,7 +96,10 @@ def test_workspace_and_split_queries(lib):
     assert lib.vecinfer_calibrate_workspace_bytes(8, 128) >= 8 * 128 * 4
     from paper_2510_06175_b200._lib import VQ
     assert lib.vecinfer_encode_workspace_bytes(1, 1, 8, VQ(128, 4, 8), VQ(128, 4, 8)) == 0
-    assert lib.vecinfer_encode_workspace_bytes(1, 1, 8, VQ(128, 4, 16), VQ(128, 4, 8)) == 8 * (2 * 32 * 8 + 4)
+    # 16-bit books: (lo, hi) fp32 pairs per (token-head, stream, sub-vector, 512-centroid chunk) of one
+    # pass of <= 512 token-heads
+    assert lib.vecinfer_encode_workspace_bytes(1, 1, 8, VQ(128, 4, 16), VQ(128, 4, 8)) == 8 * 2 * 32 * 128 * 8
+    assert lib.vecinfer_encode_workspace_bytes(4, 4096, 8, VQ(128, 4, 16), VQ(128, 4, 16)) == 512 * 2 * 32 * 128 * 8
 
 
 def test_product_path_never_imports_the_oracle():

@@ -1,0 +1,143 @@
+"""16-bit codebooks (65 536 entries): the tensor-core filter + exact selection of encode_kv.
+
+The filter (mma.sync bf16 over a_j = ||c_j||^2 - 2 x.c_j) only decides WHICH 512-centroid chunks
+are scanned with the pinned distance (R9); codes must stay bit-identical to the oracle's
+full scan, lowest index on ties.  The cases target the filter's weak spots: near-ties (points a
+hair from a centroid, so D_min << ||x||^2 and the ranking hangs on cancellation), exact
+real-arithmetic ties between two centroids, inputs far outside the book's range, per-head books,
+several passes of the workspace, head_dim 64, and the full-scan path kept behind
+VECINFER_NN16_SCAN=1 as the A/B reference.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import ref
+from helpers import load_codebooks
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2510_06175_b200 import vecinfer as vi  # noqa: E402
+from test_gpu_parity import _encode_gpu, _encode_ref, t_bf16  # noqa: E402
+
+CB = load_codebooks()
+B4D4_64 = vi.VQConfig(64, 4, 16)
+
+
+def _random_book(seed, n=65536, scale=1.0, heads=None):
+    shape = (n, 4) if heads is None else (heads, n, 4)
+    return synth.round_to_bf16(np.random.default_rng(seed).normal(0, scale, shape).astype(np.float32))
+
+
+def test_nn16_per_head_books_several_passes():
+    """Per-head K books (8 x 65 536 random bf16 centroids) and one shared V book; B*T*H = 520
+    token-heads = two workspace passes (~512 token-heads each)."""
+    H, T = 8, 65
+    k = synth.gen_keys(T, H, 128, seed=1600)
+    v = synth.gen_values(T, H, 128, seed=1601)
+    ck = _random_book(1602, heads=H)
+    cv = CB["cv_b4d4"]
+    got = _encode_gpu(k, v, CB["inv_lambda"], ck, cv, T + 3, [3], vi.B4D4, vi.B4D4)
+    want = _encode_ref(k, v, CB["inv_lambda"], ck, cv, T + 3, [3], vi.B4D4, vi.B4D4)
+    assert np.array_equal(got[0], want[0]), "key codes differ"
+    assert np.array_equal(got[1], want[1]), "value codes differ"
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-7, 1e-5, 1e-3])
+def test_nn16_points_next_to_centroids(eps):
+    """Values = a centroid + eps noise (untransformed V path): D_min is ~eps^2 while ||x||^2 is
+    O(1), the cancellation regime of a_j = ||c||^2 - 2 x.c.  eps = 0 gives exact hits (and the
+    lowest index among duplicate centroids)."""
+    cv = _random_book(1610)
+    cv[7] = cv[40000]                                    # a duplicate centroid: lowest index wins
+    rng = np.random.default_rng(1611)
+    T = 6
+    idx = rng.integers(0, 65536, size=(T, 32))
+    idx[0, :4] = 40000
+    pts = cv[idx].reshape(1, T, 1, 128) + eps * rng.standard_normal((1, T, 1, 128)).astype(np.float32)
+    pts = synth.round_to_bf16(pts.astype(np.float32))
+    k = np.zeros_like(pts)
+    got = _encode_gpu(k, pts, np.ones((1, 128), np.float32), CB["ck_b4d4"], cv, T, [0], vi.B4D4, vi.B4D4)
+    want = _encode_ref(k, pts, np.ones((1, 128), np.float32), CB["ck_b4d4"], cv, T, [0], vi.B4D4, vi.B4D4)
+    assert np.array_equal(got[1], want[1])
+    if eps == 0.0:
+        codes = ref.unpack_codes(got[1][0, 0, 0], 16)
+        assert codes[0] == 7                             # cv[7] == cv[40000]: the lower index
+
+
+def test_nn16_midpoint_ties():
+    """Points exactly halfway between two centroids that differ in one coordinate by a power of
+    two: equal distances in real arithmetic; the pinned fp32 distance (or the index) decides."""
+    cv = _random_book(1620)
+    rng = np.random.default_rng(1621)
+    T = 4
+    pts = np.zeros((T * 32, 4), np.float32)
+    for i in range(T * 32):
+        j1 = int(rng.integers(0, 65536))
+        j2 = int(rng.integers(0, 65536))
+        c = cv[j1].copy()
+        dim = int(rng.integers(0, 4))
+        c[dim] = cv[j1, dim] + np.float32(0.25)       # a second centroid 0.25 away in one dimension
+        cv[j2] = synth.round_to_bf16(c)
+        pts[i] = (cv[j1].astype(np.float64) + cv[j2].astype(np.float64)) / 2
+    pts = synth.round_to_bf16(pts.reshape(1, T, 1, 128))   # (the kernel reads bf16 inputs)
+    k = np.zeros_like(pts)
+    got = _encode_gpu(k, pts, np.ones((1, 128), np.float32), CB["ck_b4d4"], cv, T, [0], vi.B4D4, vi.B4D4)
+    want = _encode_ref(k, pts, np.ones((1, 128), np.float32), CB["ck_b4d4"], cv, T, [0], vi.B4D4, vi.B4D4)
+    assert np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("scale", [1e-3, 40.0])
+def test_nn16_inputs_outside_the_book_range(scale):
+    """Keys far larger / smaller than the centroids (the error bounds scale with ||x||_1 max|c|)."""
+    T = 5
+    k = synth.round_to_bf16((synth.gen_keys(T, 2, 128, seed=1630) * scale).astype(np.float32))
+    v = synth.round_to_bf16((synth.gen_values(T, 2, 128, seed=1631) * scale).astype(np.float32))
+    got = _encode_gpu(k, v, CB["inv_lambda"][:2], CB["ck_b4d4"], CB["cv_b4d4"], T, [0], vi.B4D4, vi.B4D4)
+    want = _encode_ref(k, v, CB["inv_lambda"][:2], CB["ck_b4d4"], CB["cv_b4d4"], T, [0], vi.B4D4, vi.B4D4)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("kcfg,vcfg", [(vi.B4D4, vi.B2D4), (vi.B1D4, vi.B4D4)])
+def test_nn16_mixed_with_small_books(kcfg, vcfg):
+    T = 9
+    k = synth.gen_keys(T, 3, 128, seed=1640, batch=2)
+    v = synth.gen_values(T, 3, 128, seed=1641, batch=2)
+    name = {4: "b1d4", 8: "b2d4", 16: "b4d4"}
+    ck = CB[f"ck_{name[kcfg.code_bits]}"]
+    cv = CB[f"cv_{name[vcfg.code_bits]}"]
+    ck = ck if ck.ndim == 2 else ck[:3]
+    cv = cv if cv.ndim == 2 else cv[:3]
+    got = _encode_gpu(k, v, CB["inv_lambda"][:3], ck, cv, T + 2, [2, 0], kcfg, vcfg)
+    want = _encode_ref(k, v, CB["inv_lambda"][:3], ck, cv, T + 2, [2, 0], kcfg, vcfg)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_nn16_head_dim_64():
+    T = 7
+    k = synth.gen_keys(T, 4, 64, seed=1650)
+    v = synth.gen_values(T, 4, 64, seed=1651)
+    inv = CB["inv_lambda"][:4, :64].copy()
+    got = _encode_gpu(k, v, inv, CB["ck_b4d4"], CB["cv_b4d4"], T, [0], B4D4_64, B4D4_64)
+    want = _encode_ref(k, v, inv, CB["ck_b4d4"], CB["cv_b4d4"], T, [0], B4D4_64, B4D4_64)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_nn16_workspace_left_zero():
+    """The selection zeroes every (lo, hi) pair the filter wrote: a zero-filled workspace stays
+    zero (decode_step places it next to the attention workspace, which must stay zero)."""
+    T, H = 3, 8
+    k = synth.gen_keys(T, H, 128, seed=1660)
+    v = synth.gen_values(T, H, 128, seed=1661)
+    ws = vi.encode_workspace(1, T, H, vi.B4D4, vi.B4D4, device="cuda").zero_()
+    kc = torch.zeros(1, H, T, 64, dtype=torch.uint8, device="cuda")
+    vc = torch.zeros_like(kc)
+    vi.encode_kv(t_bf16(k), t_bf16(v), torch.from_numpy(CB["inv_lambda"]).cuda(), t_bf16(CB["ck_b4d4"]),
+                 t_bf16(CB["cv_b4d4"]), kc, vc, torch.zeros(1, dtype=torch.int32, device="cuda"), vi.B4D4, vi.B4D4,
+                 workspace=ws)
+    torch.cuda.synchronize()
+    assert int(ws.count_nonzero().item()) == 0
