@@ -13,6 +13,7 @@
 // with 64-bit atomicMin on (dist_bits << 32 | j) -- exact argmin with lowest-index ties,
 // since dist >= 0 makes the fp32 bit pattern order-preserving.
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace vecinfer {
 namespace {
@@ -541,6 +542,231 @@ __global__ void __launch_bounds__(kFW16 * 32) nn16_filter_kernel(EncArgs a, int6
   }
 }
 
+// tcgen05 variant of the filter (opt-in VECINFER_NN16_TC=1: measured 1.2-1.6x slower than the
+// mma.sync filter, see below; same arithmetic and error bound, same workspace contract): one CTA of 4 warps holds 128 book rows as the M = 128 A tile in shared memory (K-major,
+// no swizzle, K = 16: [-2x hi | mid | lo parts | 1 1 1 0]); the chunk's centroids stream through
+// two 4 KiB B tiles of N = 128 centroids ([c | c | c | ||c||^2 parts | 0]); one thread issues
+// tcgen05.mma kind::f16 (bf16 in, fp32 out) into one of two 128-column TMEM accumulators (unit u+1's
+// MMA runs while the warps read unit u), and thread r reads TMEM lane r = its own row with
+// tcgen05.ld.32x32b.x64 and folds the values with 3-input FMNMX.  The MMA leaves the SM's issue slots
+// to the min reduction, but at K = 16 each unit's MMA is tiny (136 clk at peak) and the per-unit
+// hand-off (mbarrier wait, TMEM load, restage, CTA barrier) with only 8 warps per SM costs more than
+// the mma.sync filter's barrier-free loop over 32 warps (ncu: barrier + wait stalls dominate).
+constexpr int kTcRows = 128;                      // M
+constexpr int kTcN = 128;                         // centroids per MMA (unit): 128 or 256
+constexpr int kTcTile = kTcRows * 32;             // A tile bytes (128 x 16 bf16)
+// N = 128: two CTAs per SM (2 x 256 TMEM columns, > 76 KiB of shared memory each); N = 256 (measured
+// slower): one CTA per SM with all 512 columns
+constexpr int kTcSmem = kTcN == 128 ? 80 * 1024 : 120 * 1024;
+__device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+               :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(0u) : "memory");   // D = A.B^T (no accumulate)
+}
+__device__ __forceinline__ void sts_u128(uint32_t saddr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" :: "r"(saddr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void tc_ld_32x32b_x64(uint32_t taddr, uint32_t (&r)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,"
+      "%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr) : "memory");
+}
+// byte offset of (row r, 16-byte K group kg) in a K-major no-swizzle 128 x 16 tile: core matrices of
+// 8 rows x 16 B, next 8 rows at +128 B (SBO), next K group at +2048 B (LBO)
+__device__ __forceinline__ uint32_t tc_tile_off(int r, int kg) { return kg * 2048 + (r >> 3) * 128 + (r & 7) * 16; }
+// the same for the N = kTcN-row B tile (next K group at + kTcN * 16 B)
+__device__ __forceinline__ uint32_t tc_btile_off(int r, int kg) { return kg * (kTcN * 16) + (r >> 3) * 128 + (r & 7) * 16; }
+
+// grid (kNC16 / ncpb, row blocks of 128, books), 256 threads: warps w and w + 4 read TMEM lane
+// quadrant w (rows 32w..32w+31), columns [0, 64) / [64, 128) of each unit; warps 0-3 build the A tile,
+// warps 4-7 stage the B tiles one unit ahead (centroids prefetched into registers two units ahead)
+__global__ void __launch_bounds__(256) nn16_filter_tc_kernel(EncArgs a, int64_t bt0, int nbt_p, int ncpb) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  // [0, 4K) A tile | [4K, 12K) B ring (2 units) | mbarriers, TMEM address, bounds, half-row minima
+  constexpr int kBT = kTcN * 32;   // B tile bytes
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tsm + kTcTile + 2 * kBT);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tsm + kTcTile + 2 * kBT + 16);
+  float* sbnd = reinterpret_cast<float*>(tsm + kTcTile + 2 * kBT + 32);    // [2 chunk slots][4 warps][2]
+  float* smin = reinterpret_cast<float*>(tsm + kTcTile + 2 * kBT + 128);   // [128 rows]
+  int s, hb;
+  bool shared;
+  nn16_book(a, blockIdx.z, s, hb, shared);
+  const int nsub = a.nsub;
+  const int64_t rows = static_cast<int64_t>(nbt_p) * (shared ? a.H : 1) * nsub;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kTcRows;
+  if (row0 >= rows) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool stager = warp >= 4;
+  const int rt = tid & 127;   // row (warps 0-3) / staged centroid of the unit (warps 4-7)
+  constexpr int kUpc = kCS16 / kTcN;   // units per chunk
+  const int chunk0 = blockIdx.x * ncpb, nunits = ncpb * kUpc;
+  const uint32_t sA = smem_u32(tsm), sB = sA + kTcTile;
+  if (warp == 0) tc::alloc(smem_u32(tmem_slot), 2 * kTcN);
+  if (tid == 0) {
+    tc::mbar_init(smem_u32(mbar), 1);
+    tc::mbar_init(smem_u32(mbar + 1), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint16_t* cbook = s == 0 ? a.ck + hb * a.ck_hs : a.cv + hb * a.cv_hs;
+  // a stager handles centroids rt (and rt + 128 when N = 256) of each unit
+  auto fetch = [&](int u) -> uint4 {
+    if (u >= nunits) return make_uint4(0u, 0u, 0u, 0u);
+    const uint16_t* p = cbook + (static_cast<int64_t>(chunk0) * kCS16 + kTcN * u + rt) * 4;
+    const uint2 w0 = *reinterpret_cast<const uint2*>(p);
+    const uint2 w1 = kTcN == 256 ? *reinterpret_cast<const uint2*>(p + 128 * 4) : make_uint2(0u, 0u);
+    return make_uint4(w0.x, w0.y, w1.x, w1.y);
+  };
+  float cm_acc = 0.f, nm_acc = 0.f;   // stagers: bounds of the chunk being staged
+  auto stage = [&](int u, uint4 w4) {   // B row = centroid: K 0..7 = c c, K 8..15 = c n0 n1 n2 0
+#pragma unroll
+    for (int e = 0; e < kTcN / 128; ++e) {
+      const uint2 w = e ? make_uint2(w4.z, w4.w) : make_uint2(w4.x, w4.y);
+      const float c0 = __uint_as_float(w.x << 16), c1 = __uint_as_float(w.x & 0xFFFF0000u);
+      const float c2 = __uint_as_float(w.y << 16), c3 = __uint_as_float(w.y & 0xFFFF0000u);
+      const float n = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(c0, c0), __fmul_rn(c1, c1)), __fmul_rn(c2, c2)), __fmul_rn(c3, c3));
+      uint32_t n0, n1, n2;
+      split3_bf16(n, n0, n1, n2);
+      const uint32_t b = sB + (u & 1) * kBT;
+      const int col = rt + 128 * e;
+      sts_u128(b + tc_btile_off(col, 0), make_uint4(w.x, w.y, w.x, w.y));
+      sts_u128(b + tc_btile_off(col, 1), make_uint4(w.x, w.y, n0 | (n1 << 16), n2));
+      cm_acc = fmaxf(cm_acc, fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))));
+      nm_acc = fmaxf(nm_acc, n);
+    }
+    if (u % kUpc == kUpc - 1) {   // the chunk's last unit: its bounds go to the chunk's slot
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        cm_acc = fmaxf(cm_acc, __shfl_xor_sync(0xffffffffu, cm_acc, off));
+        nm_acc = fmaxf(nm_acc, __shfl_xor_sync(0xffffffffu, nm_acc, off));
+      }
+      if (lane == 0) {
+        float* bd = sbnd + (((u / kUpc) & 1) * 4 + (warp - 4)) * 2;
+        bd[0] = cm_acc;
+        bd[1] = nm_acc;
+      }
+      cm_acc = 0.f;
+      nm_acc = 0.f;
+    }
+  };
+  uint4 wa = make_uint4(0u, 0u, 0u, 0u), wb = wa;
+  if (stager) { wa = fetch(0); wb = fetch(1); }
+  griddep_wait();
+  float x1n = 0.f;
+  if (!stager) {   // the row's x (nsub = 16: two token-heads per warp) -> A row
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
+    const int64_t wr0 = row0 + 32 * warp;
+    for (int part = 0; part < 32 / nsub; ++part) {
+      if (wr0 + part * nsub >= rows) break;
+      const int64_t th = (wr0 + part * nsub) / nsub;
+      const int64_t btl = shared ? th / a.H : th;
+      const int h = shared ? static_cast<int>(th % a.H) : hb;
+      const int64_t bt = bt0 + btl;
+      const int b = static_cast<int>(bt / a.T), tt = static_cast<int>(bt % a.T);
+      float xx[4];
+      if (s == 0) transform_key_lane(a, b, tt, h, lane, xx);
+      else load_value_lane(a, b, tt, h, lane, xx);
+      if ((lane >= part * nsub && lane < (part + 1) * nsub) || nsub == 32) {
+        x[0] = xx[0]; x[1] = xx[1]; x[2] = xx[2]; x[3] = xx[3];
+      }
+    }
+    uint32_t hi[4], mi[4], lo[4];   // K 0..3 hi, 4..7 mid, 8..11 lo parts of -2x, 12..14 = 1, 15 = 0
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split3_bf16(-2.f * x[i], hi[i], mi[i], lo[i]);
+    sts_u128(sA + tc_tile_off(rt, 0), make_uint4(hi[0] | (hi[1] << 16), hi[2] | (hi[3] << 16),
+                                                mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16)));
+    sts_u128(sA + tc_tile_off(rt, 1), make_uint4(lo[0] | (lo[1] << 16), lo[2] | (lo[3] << 16), 0x3F803F80u, 0x00003F80u));
+    x1n = fabsf(x[0]) + fabsf(x[1]) + fabsf(x[2]) + fabsf(x[3]);
+  } else {
+    stage(0, wa);
+    if (nunits > 1) stage(1, wb);
+    wa = fetch(2);
+    wb = fetch(3);
+  }
+  tc::fence_proxy_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = *tmem_slot;
+  constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kTcN >> 3) << 17) |
+                              (static_cast<uint32_t>(kTcRows >> 4) << 24);   // f32 D, bf16 A / B, K-major
+  const uint64_t adesc = tc::smem_desc_kmajor(sA, 2048, 128);
+  if (tid == 0) {
+    for (int u = 0; u < 2 && u < nunits; ++u) {
+      tc_mma_ss(tbase + u * kTcN, adesc, tc::smem_desc_kmajor(sB + u * kBT, kBT / 2, 128), kIdesc);
+      tc::commit(smem_u32(mbar + u));
+    }
+  }
+  const uint32_t tcol = (static_cast<uint32_t>(32 * (warp & 3)) << 16) + (kTcN / 2) * (warp >> 2);
+  float mn = INFINITY;
+  for (int u = 0; u < nunits; ++u) {
+    const int buf = u & 1;
+    tc::mbar_wait(smem_u32(mbar + buf), (u >> 1) & 1);
+    tc::fence_after();
+#pragma unroll
+    for (int hq = 0; hq < kTcN / 128; ++hq) {   // this warp's half of the unit's columns, 64 at a time
+      uint32_t v[64];
+      tc_ld_32x32b_x64(tbase + tcol + buf * kTcN + 64 * hq, v);
+      tc::wait_ld();
+      float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+#pragma unroll
+      for (int i = 0; i < 64; i += 8) {
+        m4[0] = fminf(m4[0], fminf(__uint_as_float(v[i]), __uint_as_float(v[i + 1])));
+        m4[1] = fminf(m4[1], fminf(__uint_as_float(v[i + 2]), __uint_as_float(v[i + 3])));
+        m4[2] = fminf(m4[2], fminf(__uint_as_float(v[i + 4]), __uint_as_float(v[i + 5])));
+        m4[3] = fminf(m4[3], fminf(__uint_as_float(v[i + 6]), __uint_as_float(v[i + 7])));
+      }
+      mn = fminf(mn, fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3])));
+    }
+    const bool chunk_end = u % kUpc == kUpc - 1;
+    if (stager) {
+      if (chunk_end) { smin[rt] = mn; mn = INFINITY; }
+      if (u + 2 < nunits) {   // unit u + 2 into the buffers unit u used (its MMA is complete)
+        stage(u + 2, wa);
+        wa = wb;
+        wb = fetch(u + 4);
+      }
+      tc::fence_proxy_async_smem();
+    }
+    tc::fence_before();
+    __syncthreads();   // D[buf] read by every warp, B[buf] restaged, half-row minima posted
+    tc::fence_after();
+    if (tid == 0 && u + 2 < nunits) {
+      tc_mma_ss(tbase + buf * kTcN, adesc, tc::smem_desc_kmajor(sB + buf * kBT, kBT / 2, 128), kIdesc);
+      tc::commit(smem_u32(mbar + buf));
+    }
+    if (!stager && chunk_end) {   // chunk done: (lo, hi) of this row
+      const int ci = u / kUpc;
+      const float* bd = sbnd + (ci & 1) * 8;
+      const float cm = fmaxf(fmaxf(bd[0], bd[2]), fmaxf(bd[4], bd[6]));
+      const float nm = fmaxf(fmaxf(bd[1], bd[3]), fmaxf(bd[5], bd[7]));
+      const float v = fminf(mn, smin[rt]);
+      mn = INFINITY;
+      const int64_t r = row0 + rt;
+      if (r < rows) {
+        const float E = 0x1p-17f * (2.1f * x1n * cm + 1.01f * nm);
+        const int m = static_cast<int>(r % nsub);
+        const int64_t th = r / nsub;
+        const int64_t btl = shared ? th / a.H : th;
+        const int h = shared ? static_cast<int>(th % a.H) : hb;
+        reinterpret_cast<float2*>(a.ws)[nn16_ws_row(a, btl, h, s, m) + chunk0 + ci] = make_float2(v - E, v + E);
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::dealloc(tbase, 2 * kTcN);
+}
+
 // grid (pass token rows, H, 2 streams x 4 row groups), 8 warps: warp w of row group z selects and
 // stores the 16-bit code of sub-vector m = 8 z + w (one memory round trip for the chunk bounds,
 // one per scanned chunk: the chunk is copied into the warp's shared buffer with every cp.async of a
@@ -735,6 +961,17 @@ static bool nn16_scan_from_env() {
   return v == 1;
 }
 
+// VECINFER_NN16_TC=1: the tcgen05 filter instead of the mma.sync one (A/B; same codes).  Measured
+// slower (N2): mma.sync stays the default.
+static bool nn16_hmma_from_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VECINFER_NN16_TC");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int32_t B, int32_t T,
                                      int32_t H_kv, const int64_t k_strides[3], const int64_t v_strides[3],
                                      const float* inv_lambda, const void* ck_bf16, const void* cv_bf16,
@@ -801,6 +1038,12 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
     if (!workspace || workspace_bytes < need || !aligned(workspace, 16))
       return fail(VECINFER_ERR_WORKSPACE, "encode_kv: 16-bit codebooks need %zu bytes of workspace", need);
     if (kcfg.head_dim != 128 && kcfg.head_dim != 64) return fail(VECINFER_ERR_UNSUPPORTED, "encode_kv: 16-bit head_dim");
+    static bool attr_done = false;   // benign race: idempotent attribute
+    if (!attr_done) {
+      cudaFuncSetAttribute(nn16_filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+      attr_done = true;
+    }
+    const bool hmma = nn16_hmma_from_env();
     const int64_t np = nn16_pass_rows(nbt, H_kv);
     const int nbk = (kcfg.code_bits == 16 ? (ck_head_stride ? H_kv : 1) : 0) +
                     (vcfg.code_bits == 16 ? (cv_head_stride ? H_kv : 1) : 0);
@@ -808,12 +1051,21 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
       const int nb = static_cast<int>(nbt - b0 < np ? nbt - b0 : np);
       // rows of the largest book (shared books hold every head's rows)
       const int64_t rows = static_cast<int64_t>(nb) * H_kv * a.nsub;
-      const int64_t rblk = (rows + kRows16 - 1) / kRows16;
-      // chunks per CTA: amortise the rows' transform over up to 8 chunks while keeping >= ~4 CTAs per SM
-      int ncpb = 8;
-      while (ncpb > 1 && (kNC16 / ncpb) * rblk * nbk < 4 * device_sm_count()) ncpb >>= 1;
-      const dim3 g1(kNC16 / ncpb, static_cast<unsigned>(rblk), static_cast<unsigned>(nbk));
-      cudaError_t e = launch_pdl(nn16_filter_kernel, g1, dim3(kFW16 * 32), 0, st, a, b0, nb, ncpb);
+      cudaError_t e;
+      if (!hmma) {   // tcgen05 filter (VECINFER_NN16_TC=1): 128-row CTAs, <= 2 per SM (256 TMEM columns each)
+        const int64_t rblk = (rows + kTcRows - 1) / kTcRows;
+        int ncpb = 8;
+        while (ncpb > 1 && (kNC16 / ncpb) * rblk * nbk < (kTcN == 128 ? 2 : 1) * device_sm_count()) ncpb >>= 1;
+        const dim3 g1(kNC16 / ncpb, static_cast<unsigned>(rblk), static_cast<unsigned>(nbk));
+        e = launch_pdl(nn16_filter_tc_kernel, g1, dim3(2 * kTcRows), kTcSmem, st, a, b0, nb, ncpb);
+      } else {       // mma.sync filter (default)
+        const int64_t rblk = (rows + kRows16 - 1) / kRows16;
+        // chunks per CTA: amortise the rows' transform over up to 8 chunks while keeping >= ~4 CTAs per SM
+        int ncpb = 8;
+        while (ncpb > 1 && (kNC16 / ncpb) * rblk * nbk < 4 * device_sm_count()) ncpb >>= 1;
+        const dim3 g1(kNC16 / ncpb, static_cast<unsigned>(rblk), static_cast<unsigned>(nbk));
+        e = launch_pdl(nn16_filter_kernel, g1, dim3(kFW16 * 32), 0, st, a, b0, nb, ncpb);
+      }
       if (e == cudaSuccess)
         e = launch_pdl(nn16_select_kernel, dim3(static_cast<unsigned>(nb), H_kv, 8), dim3(kSelWarps * 32), 0, st, a, b0);
       if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_kv (16-bit): %s", cudaGetErrorString(e)); }

@@ -141,3 +141,17 @@ def test_nn16_workspace_left_zero():
                  workspace=ws)
     torch.cuda.synchronize()
     assert int(ws.count_nonzero().item()) == 0
+
+
+def test_nn16_tcgen05_filter_variant():
+    """The opt-in tcgen05 filter (VECINFER_NN16_TC=1: A tile in shared memory, two TMEM accumulators,
+    tcgen05.mma kind::f16 bf16 -> fp32) runs every case of this file to the same oracle codes.  The
+    switch is read once per process, hence the subprocess."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, VECINFER_NN16_TC="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_nn16.py"),
+                        "-k", "not tcgen05"], env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
