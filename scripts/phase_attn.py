@@ -33,8 +33,9 @@ def main():
     cv = torch.from_numpy(synth.bf16_from_bits(z["cv_b2d4"])).to(dev).to(torch.bfloat16)
     for c in args.case:
         B, N, splits = map(int, c.split(",")[:3])
+        algo = c.split(",")[3] if len(c.split(",")) > 3 else "auto"
         S = vi.attn_num_splits(B, 8, N, splits)
-        nct = vi.attn_num_ctas(B, 8, N, splits)
+        nct = vi.attn_num_ctas(B, 8, N, splits) if algo != "stream" else 148
         buf = torch.zeros(nct * 32, dtype=torch.int64, device=dev)
         lib.vecinfer_debug_set_phase_buffer.argtypes = [ctypes.c_void_p]
         lib.vecinfer_debug_set_phase_buffer(ctypes.c_void_p(buf.data_ptr()))
@@ -45,7 +46,7 @@ def main():
         ws = vi.attn_workspace(B, 32, 8, N, splits, device=dev)
         for _ in range(5):
             buf.zero_()
-            vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, workspace=ws)
+            vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, workspace=ws, algo=algo)
             torch.cuda.synchronize()
         both = buf.view(nct, 32).cpu().numpy().astype(np.float64)
         t, cyc = both[:, :16], both[:, 16:]

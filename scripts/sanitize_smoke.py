@@ -11,10 +11,27 @@ import synth  # noqa: E402
 from paper_2510_06175_b200 import vecinfer as vi  # noqa: E402
 
 dev = torch.device("cuda", 0)
+NN16_ONLY = "--nn16-only" in sys.argv   # (run under VECINFER_NN16_TC=1 for the tcgen05 filter)
 z = np.load(os.path.join(ROOT, "data", "llama8b_synth_codebooks.npz"))
 lam = torch.from_numpy(z["lambda"]).to(dev)
 inv = torch.from_numpy(z["inv_lambda"]).to(dev)
 T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+# 16-bit books (tensor-core filter + exact selection): per-head books over two passes, D = 64
+ck16h = T(synth.round_to_bf16(np.random.default_rng(5).normal(0, 1, (8, 65536, 4)).astype(np.float32))).to(torch.bfloat16)
+cv16s = T(synth.bf16_from_bits(z["cv_b4d4"])).to(torch.bfloat16)
+k65 = T(synth.gen_keys(65, 8, 128, seed=6)).to(torch.bfloat16)
+v65 = T(synth.gen_values(65, 8, 128, seed=7)).to(torch.bfloat16)
+kc65 = torch.zeros(1, 8, 70, 64, dtype=torch.uint8, device=dev)
+vc65 = torch.zeros_like(kc65)
+vi.encode_kv(k65, v65, inv, ck16h, cv16s, kc65, vc65, torch.zeros(1, dtype=torch.int32, device=dev), vi.B4D4, vi.B4D4)
+c16_64 = vi.VQConfig(64, 4, 16)
+kc6 = torch.zeros(1, 4, 8, 32, dtype=torch.uint8, device=dev)
+vi.encode_kv(k65[:, :7, :4, :64].contiguous(), v65[:, :7, :4, :64].contiguous(), inv[:4, :64].contiguous(), cv16s, cv16s,
+             kc6, kc6.clone(), torch.zeros(1, dtype=torch.int32, device=dev), c16_64, c16_64)
+if NN16_ONLY:
+    torch.cuda.synchronize()
+    print("sanitize smoke (16-bit encode only) done")
+    sys.exit(0)
 for name, cfg in (("b1d4", vi.B1D4), ("b2d4", vi.B2D4), ("b4d4", vi.B4D4)):
     ck = T(synth.bf16_from_bits(z[f"ck_{name}"])).to(torch.bfloat16)
     cv = T(synth.bf16_from_bits(z[f"cv_{name}"])).to(torch.bfloat16)
@@ -47,6 +64,11 @@ seq = torch.tensor([N, 333, 31], dtype=torch.int32, device=dev)
 kn = T(synth.gen_keys(1, 8, 128, seed=14, batch=B)[:, 0]).to(torch.bfloat16)
 vn = T(synth.gen_values(1, 8, 128, seed=15, batch=B)[:, 0]).to(torch.bfloat16)
 wp = seq - 1
+# VECINFER_ATTN_FLAG_EARLY_CACHE: split, stream and fused decode step with the pre-wait cache reads
+for splits in (0, 3):
+    vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, early_cache=True)
+vi.attn_decode(q, lam, ck, cv, kc, vc, seq, algo="stream", early_cache=True)
+vi.decode_step(q, kn, vn, lam, inv, ck, cv, kc, vc, wp, seq, early_cache=True)
 # tcgen05 score path (split / multi-wave persistent / fused append)
 for splits in (0, 3, 60):
     vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, algo="tc")
