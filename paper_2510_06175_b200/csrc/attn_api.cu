@@ -110,6 +110,10 @@ static bool algo_early(vecinfer_attn_algo_t a) {
   return (static_cast<uint32_t>(a) & static_cast<uint32_t>(VECINFER_ATTN_FLAG_EARLY_CACHE)) != 0;
 }
 
+namespace vecinfer {
+int encode_launch_count(int64_t nbt, int H, const vecinfer_vq_t& k, const vecinfer_vq_t& v);   // encode.cu
+}
+
 struct SplitPlan;
 static SplitPlan plan_splits(int32_t B, int32_t H_kv, int64_t n_tokens_max, int32_t num_splits);
 
@@ -510,10 +514,9 @@ extern "C" int32_t vecinfer_decode_step_launches(int32_t B, int32_t H_kv, int64_
   if (residual_append) return 1;
   algo = algo_base(algo);
   if (decode_fuses(B, H_kv, n_cap, kcfg, vcfg, num_splits, algo)) return 1;
-  // 16-bit append (B*H_kv <= 4096 token-heads): one centroid-split search launch that also
-  // finalises (the last chunk CTA of each token-head); larger batches add a finalize launch
-  const bool big16 = (kcfg.code_bits == 16 || vcfg.code_bits == 16) && static_cast<int64_t>(B) * H_kv > 4096;
-  return 1 + (big16 ? 2 : 1);
+  // separate append: 16-bit d = 4 and d8b12 / d8b16 books take a filter + selection launch pair
+  // (plus a generic launch for the other stream of a mixed NEXT-2 pair); others one encode launch
+  return 1 + encode_launch_count(B, H_kv, kcfg, vcfg);
 }
 
 extern "C" size_t vecinfer_decode_step_workspace_bytes(int32_t B, int32_t H_q, int32_t H_kv, int64_t n_cap,

@@ -12,6 +12,8 @@
 // centroid-split CTAs (1024 centroids staged per CTA) whose per-lane minima are combined
 // with 64-bit atomicMin on (dist_bits << 32 | j) -- exact argmin with lowest-index ties,
 // since dist >= 0 makes the fp32 bit pattern order-preserving.
+#include <type_traits>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -43,6 +45,7 @@ struct EncArgs {
   float inv_sqrt_d;
   int D, nsub;             // head dim (64 or 128) and sub-vectors (lanes holding the key) = D / 4
   unsigned long long* ws;  // 16-bit path: [B*T*H][2][32] packed minima
+  int gen_mask;            // encode_generic_kernel: bit z = encode stream z (the filter does the others)
 };
 
 // Smoothing + exact integer FWHT + fixed-point -> fp32 (key_transform_lane), flags range errors.
@@ -369,6 +372,15 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(0.f));
 }
 
+__device__ __forceinline__ void mma_bf16_16816_acc(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                                   uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 __device__ __forceinline__ uint32_t bf16_bits_rn(float v) {
   return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
 }
@@ -381,14 +393,17 @@ __device__ __forceinline__ void split3_bf16(float v, uint32_t& p0, uint32_t& p1,
   p2 = bf16_bits_rn(r2);
 }
 
+// streams searched by the tensor-core filter: 65 536-entry d = 4 books and the d = 8 books of 4096 /
+// 65 536 entries (NEXT-2 d8b12, d8b16)
+__host__ __device__ __forceinline__ bool nn_filtered(int sub, int bits) {
+  return (sub == 4 && bits == 16) || (sub == 8 && (bits == 12 || bits == 16));
+}
 // book z of the launch -> stream s (0 = K, 1 = V) and head hb (per-head books) / shared flag
 __device__ __forceinline__ void nn16_book(const EncArgs& a, int z, int& s, int& hb, bool& shared) {
-  const bool k16 = a.kbits == 16, v16 = a.vbits == 16;
-  const int nk = k16 ? (a.ck_hs ? a.H : 1) : 0;
+  const int nk = nn_filtered(a.ksub, a.kbits) ? (a.ck_hs ? a.H : 1) : 0;
   s = z < nk ? 0 : 1;
   hb = s == 0 ? z : z - nk;
   shared = (s == 0 ? a.ck_hs : a.cv_hs) == 0;
-  (void)v16;
 }
 
 // workspace (float2 lo/hi) of sub-vector m, stream s, token-head (btl, h) of the pass
@@ -396,124 +411,158 @@ __device__ __forceinline__ int64_t nn16_ws_row(const EncArgs& a, int64_t btl, in
   return (((btl * a.H + h) * 2 + s) * 32 + m) * kNC16;
 }
 
-// grid (kNC16 / ncpb, row blocks, books); rows of book (s, hb): (token, [head,] sub-vector) of the
-// pass.  A CTA filters its 256 rows against ncpb consecutive chunks: the rows' x and A fragments are
-// built once, the chunks go through two shared fragment buffers (chunk c + 1 is staged -- its
+// grid (max chunks / ncpb, row blocks, books); rows of book (s, hb): (token, [head,] sub-vector) of
+// the pass.  A CTA filters its 256 rows against ncpb consecutive chunks: the rows' x and A fragments
+// are built once, the chunks go through two shared fragment buffers (chunk c + 1 is staged -- its
 // centroids prefetched into registers a chunk earlier -- while c is multiplied).
+// DS = sub-vector dims: 4 (K = 16, one MMA per n-tile) or 8 (K = 32, two chained MMAs:
+// [hi | mid] . [c | c] then [lo | 1 1 1 0 0 0 0 0] . [c | n0 n1 n2 0 0 0 0 0]).
+template <int DS>
 __global__ void __launch_bounds__(kFW16 * 32) nn16_filter_kernel(EncArgs a, int64_t bt0, int nbt_p, int ncpb) {
-  __shared__ uint2 sfrag[2][(kCS16 / 8) * 32];   // B fragments of a chunk's 64 n-tiles (2 x 16 KiB)
-  __shared__ float sx[kFW16][32][4];
-  __shared__ float sbnd[2][kFW16][2];            // per-warp (max |c_i|, max ||c||^2) of the staged chunk
+  extern __shared__ __align__(16) unsigned char fsm[];
+  using Frag = typename std::conditional<DS == 4, uint2, uint4>::type;   // B fragment words of a lane
+  Frag* sfrag = reinterpret_cast<Frag*>(fsm);                             // [2][64 n-tiles][32 lanes]
+  float* sx = reinterpret_cast<float*>(fsm + 2 * (kCS16 / 8) * 32 * sizeof(Frag));   // [warps][32 rows][DS]
+  float* sbnd = sx + kFW16 * 32 * DS;                                     // [2][warps][2]
   int s, hb;
   bool shared;
   nn16_book(a, blockIdx.z, s, hb, shared);
-  const int nsub = a.nsub;
+  const int nsub = a.D / DS;
+  const int nch = (1 << (s ? a.vbits : a.kbits)) / kCS16;
   const int64_t rows = static_cast<int64_t>(nbt_p) * (shared ? a.H : 1) * nsub;
   const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kRows16;
-  if (row0 >= rows) return;   // (per-head books have H x fewer rows than the grid is sized for)
+  const int chunk0 = blockIdx.x * ncpb;
+  if (row0 >= rows || chunk0 >= nch) return;   // (per-head books: fewer rows; 4096-entry books: 8 chunks)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int chunk0 = blockIdx.x * ncpb;
   // centroids (static codebook) are loaded before the grid-dependency wait; column j of n-tile nt =
   // centroid chunk * 512 + 8 nt + j; lane (j, t) of the fragment holds k = 2t, 2t+1 | 2t+8, 2t+9
   const uint16_t* cbook = s == 0 ? a.ck + hb * a.ck_hs : a.cv + hb * a.cv_hs;
   constexpr int kPer = kCS16 / (kFW16 * 32);
-  uint2 cw[kPer];
+  Frag cw[kPer];
   auto prefetch = [&](int chunk) {
 #pragma unroll
     for (int q = 0; q < kPer; ++q)
-      cw[q] = *reinterpret_cast<const uint2*>(cbook + (static_cast<int64_t>(chunk) * kCS16 + tid + kFW16 * 32 * q) * 4);
+      cw[q] = *reinterpret_cast<const Frag*>(cbook + (static_cast<int64_t>(chunk) * kCS16 + tid + kFW16 * 32 * q) * DS);
   };
   auto stage = [&](int buf) {
     float cmax = 0.f, nmax = 0.f;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const int i = tid + kFW16 * 32 * q;
-      const uint2 w = cw[q];
-      const float c0 = __uint_as_float(w.x << 16), c1 = __uint_as_float(w.x & 0xFFFF0000u);
-      const float c2 = __uint_as_float(w.y << 16), c3 = __uint_as_float(w.y & 0xFFFF0000u);
-      const float n = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(c0, c0), __fmul_rn(c1, c1)), __fmul_rn(c2, c2)), __fmul_rn(c3, c3));
+      uint32_t w[DS / 2];
+      if constexpr (DS == 4) { w[0] = cw[q].x; w[1] = cw[q].y; }
+      else { w[0] = cw[q].x; w[1] = cw[q].y; w[2] = cw[q].z; w[3] = cw[q].w; }
+      float n = 0.f;
+#pragma unroll
+      for (int u = 0; u < DS / 2; ++u) {
+        const float c0 = __uint_as_float(w[u] << 16), c1 = __uint_as_float(w[u] & 0xFFFF0000u);
+        n = __fadd_rn(__fadd_rn(n, __fmul_rn(c0, c0)), __fmul_rn(c1, c1));
+        cmax = fmaxf(cmax, fmaxf(fabsf(c0), fabsf(c1)));
+      }
       uint32_t n0, n1, n2;
       split3_bf16(n, n0, n1, n2);
-      cmax = fmaxf(cmax, fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))));
       nmax = fmaxf(nmax, n);
-      uint2* f = sfrag[buf] + (i >> 3) * 32 + (i & 7) * 4;
-      f[0] = make_uint2(w.x, w.x);                 // k 0,1 | 8,9   = c0 c1 | c0 c1
-      f[1] = make_uint2(w.y, w.y);                 // k 2,3 | 10,11 = c2 c3 | c2 c3
-      f[2] = make_uint2(w.x, n0 | (n1 << 16));     // k 4,5 | 12,13 = c0 c1 | n0 n1
-      f[3] = make_uint2(w.y, n2);                  // k 6,7 | 14,15 = c2 c3 | n2 0
+      Frag* f = sfrag + (buf * (kCS16 / 8) + (i >> 3)) * 32 + (i & 7) * 4;
+      if constexpr (DS == 4) {
+        f[0] = make_uint2(w[0], w[0]);                 // k 0,1 | 8,9   = c0 c1 | c0 c1
+        f[1] = make_uint2(w[1], w[1]);                 // k 2,3 | 10,11 = c2 c3 | c2 c3
+        f[2] = make_uint2(w[0], n0 | (n1 << 16));     // k 4,5 | 12,13 = c0 c1 | n0 n1
+        f[3] = make_uint2(w[1], n2);                   // k 6,7 | 14,15 = c2 c3 | n2 0
+      } else {   // lane t: first MMA (c pair t | c pair t), second MMA (c pair t | n parts)
+        f[0] = make_uint4(w[0], w[0], w[0], n0 | (n1 << 16));
+        f[1] = make_uint4(w[1], w[1], w[1], n2);
+        f[2] = make_uint4(w[2], w[2], w[2], 0u);
+        f[3] = make_uint4(w[3], w[3], w[3], 0u);
+      }
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
       cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, off));
       nmax = fmaxf(nmax, __shfl_xor_sync(0xffffffffu, nmax, off));
     }
-    if (lane == 0) { sbnd[buf][warp][0] = cmax; sbnd[buf][warp][1] = nmax; }
+    if (lane == 0) { sbnd[(buf * kFW16 + warp) * 2] = cmax; sbnd[(buf * kFW16 + warp) * 2 + 1] = nmax; }
   };
   prefetch(chunk0);
   griddep_wait();   // k / v may come from the previous kernel; the workspace is reused across passes
-  // x of the warp's 32 rows (lane l <-> row 32 warp + l): nsub = 32: one token-head; 16: two
+  // x of the warp's 32 rows: the token-heads' transforms (lane l holds dims 4l..4l+3) -> sx rows
   const int64_t wr0 = row0 + 32 * warp;
-  float xr[4] = {0.f, 0.f, 0.f, 0.f};
+  float* sxw = sx + warp * 32 * DS;
   for (int part = 0; part < 32 / nsub; ++part) {
-    const int64_t th = (wr0 + part * nsub) / nsub;
-    if (wr0 + part * nsub >= rows) break;
-    const int64_t btl = shared ? th / a.H : th;
-    const int h = shared ? static_cast<int>(th % a.H) : hb;
-    const int64_t bt = bt0 + btl;
-    const int b = static_cast<int>(bt / a.T), tt = static_cast<int>(bt % a.T);
-    float x[4];
-    if (s == 0) transform_key_lane(a, b, tt, h, lane, x);
-    else load_value_lane(a, b, tt, h, lane, x);
-    if ((lane >= part * nsub && lane < (part + 1) * nsub) || nsub == 32) {
-      xr[0] = x[0]; xr[1] = x[1]; xr[2] = x[2]; xr[3] = x[3];
+    const int64_t rp = wr0 + part * nsub;
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
+    if (rp < rows) {
+      const int64_t th = rp / nsub;
+      const int64_t btl = shared ? th / a.H : th;
+      const int h = shared ? static_cast<int>(th % a.H) : hb;
+      const int64_t bt = bt0 + btl;
+      const int b = static_cast<int>(bt / a.T), tt = static_cast<int>(bt % a.T);
+      if (s == 0) transform_key_lane(a, b, tt, h, lane, x);
+      else load_value_lane(a, b, tt, h, lane, x);
+    }
+    if (lane < a.D / 4) {   // dims 4l.. of the token-head = row (4l) / DS, components (4l) % DS ..
+      float* d = sxw + (part * nsub + (4 * lane) / DS) * DS + (4 * lane) % DS;
+      d[0] = x[0]; d[1] = x[1]; d[2] = x[2]; d[3] = x[3];
     }
   }
   stage(0);
-  if (ncpb > 1) prefetch(chunk0 + 1);
-  *reinterpret_cast<float4*>(sx[warp][lane]) = make_float4(xr[0], xr[1], xr[2], xr[3]);
+  if (ncpb > 1 && chunk0 + 1 < nch) prefetch(chunk0 + 1);
   __syncthreads();
-  // A fragments of the two m16 tiles: row r0 = 16 mt + g, r1 = r0 + 8
-  uint32_t af[2][4];
+  // A fragments of the two m16 tiles: row r0 = 16 mt + g, r1 = r0 + 8 (DS = 8: [mma][mt][4])
+  constexpr int NM = DS == 4 ? 1 : 2;
+  uint32_t af[NM][2][4];
+  const uint32_t one = 0x3F80u;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
-    const float* x0 = sx[warp][16 * mt + g];
-    const float* x1 = sx[warp][16 * mt + g + 8];
-    const int c = (t & 1) * 2;   // components c, c + 1
+    const float* x0 = sxw + (16 * mt + g) * DS;
+    const float* x1 = sxw + (16 * mt + g + 8) * DS;
+    const int c = DS == 4 ? (t & 1) * 2 : 2 * t;   // components c, c + 1
     uint32_t h0[2], m0[2], l0[2], h1[2], m1[2], l1[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       split3_bf16(-2.f * x0[c + u], h0[u], m0[u], l0[u]);
       split3_bf16(-2.f * x1[c + u], h1[u], m1[u], l1[u]);
     }
-    const uint32_t one = 0x3F80u;
-    if (t < 2) {   // k 2t, 2t+1 = hi parts; k 2t+8, 2t+9 = lo parts
-      af[mt][0] = h0[0] | (h0[1] << 16); af[mt][1] = h1[0] | (h1[1] << 16);
-      af[mt][2] = l0[0] | (l0[1] << 16); af[mt][3] = l1[0] | (l1[1] << 16);
-    } else {       // k 2t = 4 + c: mid parts; k 12..15 = 1, 1, 1, 0
-      af[mt][0] = m0[0] | (m0[1] << 16); af[mt][1] = m1[0] | (m1[1] << 16);
-      af[mt][2] = t == 2 ? (one | (one << 16)) : one;
-      af[mt][3] = af[mt][2];
+    if constexpr (DS == 4) {
+      if (t < 2) {   // k 2t, 2t+1 = hi parts; k 2t+8, 2t+9 = lo parts
+        af[0][mt][0] = h0[0] | (h0[1] << 16); af[0][mt][1] = h1[0] | (h1[1] << 16);
+        af[0][mt][2] = l0[0] | (l0[1] << 16); af[0][mt][3] = l1[0] | (l1[1] << 16);
+      } else {       // k 2t = 4 + c: mid parts; k 12..15 = 1, 1, 1, 0
+        af[0][mt][0] = m0[0] | (m0[1] << 16); af[0][mt][1] = m1[0] | (m1[1] << 16);
+        af[0][mt][2] = t == 2 ? (one | (one << 16)) : one;
+        af[0][mt][3] = af[0][mt][2];
+      }
+    } else {         // first MMA: k 2t.. = hi, k 2t+8.. = mid; second: k 2t.. = lo, k 8..15 = 1 1 1 0 ..
+      af[0][mt][0] = h0[0] | (h0[1] << 16); af[0][mt][1] = h1[0] | (h1[1] << 16);
+      af[0][mt][2] = m0[0] | (m0[1] << 16); af[0][mt][3] = m1[0] | (m1[1] << 16);
+      af[NM - 1][mt][0] = l0[0] | (l0[1] << 16); af[NM - 1][mt][1] = l1[0] | (l1[1] << 16);
+      af[NM - 1][mt][2] = t == 0 ? (one | (one << 16)) : t == 1 ? one : 0u;
+      af[NM - 1][mt][3] = af[NM - 1][mt][2];
     }
   }
-  // per-row constants of the epilogue: the row's ||x||_1 and its workspace row
-  for (int ci = 0; ci < ncpb; ++ci) {
+  const int nci = min(ncpb, nch - chunk0);
+  for (int ci = 0; ci < nci; ++ci) {
     const int buf = ci & 1;
     float mn[2][2] = {{INFINITY, INFINITY}, {INFINITY, INFINITY}};
 #pragma unroll 4
     for (int nt = 0; nt < kCS16 / 8; ++nt) {
-      const uint2 bf = sfrag[buf][nt * 32 + lane];
+      const Frag bf = sfrag[(buf * (kCS16 / 8) + nt) * 32 + lane];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         float d[4];
-        mma_bf16_16816(d, af[mt][0], af[mt][1], af[mt][2], af[mt][3], bf.x, bf.y);
+        if constexpr (DS == 4) {
+          mma_bf16_16816(d, af[0][mt][0], af[0][mt][1], af[0][mt][2], af[0][mt][3], bf.x, bf.y);
+        } else {
+          mma_bf16_16816(d, af[0][mt][0], af[0][mt][1], af[0][mt][2], af[0][mt][3], bf.x, bf.y);
+          mma_bf16_16816_acc(d, af[NM - 1][mt][0], af[NM - 1][mt][1], af[NM - 1][mt][2], af[NM - 1][mt][3], bf.z, bf.w);
+        }
         mn[mt][0] = fminf(mn[mt][0], fminf(d[0], d[1]));
         mn[mt][1] = fminf(mn[mt][1], fminf(d[2], d[3]));
       }
     }
     float cm = 0.f, nm = 0.f;
 #pragma unroll
-    for (int w = 0; w < kFW16; ++w) { cm = fmaxf(cm, sbnd[buf][w][0]); nm = fmaxf(nm, sbnd[buf][w][1]); }
+    for (int w = 0; w < kFW16; ++w) { cm = fmaxf(cm, sbnd[(buf * kFW16 + w) * 2]); nm = fmaxf(nm, sbnd[(buf * kFW16 + w) * 2 + 1]); }
     const int chunk = chunk0 + ci;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
@@ -525,21 +574,28 @@ __global__ void __launch_bounds__(kFW16 * 32) nn16_filter_kernel(EncArgs a, int6
         const int rl = 16 * mt + g + 8 * hf;   // row of the warp
         const int64_t r = wr0 + rl;
         if (t != 0 || r >= rows) continue;
-        const float* xx = sx[warp][rl];
-        const float x1n = fabsf(xx[0]) + fabsf(xx[1]) + fabsf(xx[2]) + fabsf(xx[3]);
-        const float E = 0x1p-17f * (2.1f * x1n * cm + 1.01f * nm);
+        const float* xx = sxw + rl * DS;
+        float x1n = 0.f;
+#pragma unroll
+        for (int u = 0; u < DS; ++u) x1n += fabsf(xx[u]);
+        // accumulation bound: DS = 4: 16 products, E = 4x; DS = 8: 32 chained, E = 4x (2^-16)
+        const float E = (DS == 4 ? 0x1p-17f : 0x1p-16f) * (2.1f * x1n * cm + 1.01f * nm);
         const int m = static_cast<int>(r % nsub);
         const int64_t th = r / nsub;
         const int64_t btl = shared ? th / a.H : th;
         const int h = shared ? static_cast<int>(th % a.H) : hb;
         reinterpret_cast<float2*>(a.ws)[nn16_ws_row(a, btl, h, s, m) + chunk] = make_float2(v - E, v + E);
       }
-    if (ci + 1 < ncpb) {   // stage chunk ci + 1 into the other buffer (last read in iteration ci - 1)
+    if (ci + 1 < nci) {   // stage chunk ci + 1 into the other buffer (last read in iteration ci - 1)
       stage(buf ^ 1);
-      if (ci + 2 < ncpb) prefetch(chunk0 + ci + 2);
+      if (ci + 2 < nci) prefetch(chunk0 + ci + 2);
       __syncthreads();
     }
   }
+}
+template <int DS>
+constexpr int nn_filter_smem() {
+  return 2 * (kCS16 / 8) * 32 * (DS == 4 ? 8 : 16) + kFW16 * 32 * DS * 4 + 2 * kFW16 * 2 * 4;
 }
 
 // tcgen05 variant of the filter (opt-in VECINFER_NN16_TC=1: measured 1.2-1.6x slower than the
@@ -853,6 +909,107 @@ __global__ void __launch_bounds__(kSelWarps * 32) nn16_select_kernel(EncArgs a, 
     reinterpret_cast<uint16_t*>((s ? a.vcodes : a.kcodes) + row * (nsub * 2))[m] = static_cast<uint16_t>(best & 0xFFFFull);
 }
 
+// d = 8 books (NEXT-2 d8b12 / d8b16): grid (pass token rows, H, 2 streams), 8 warps; warp w selects
+// sub-vectors w and w + 8 (chunks of 512 x 16 B copied to the warp's 8 KiB buffer with cp.async),
+// then the row's 16 codes are packed into its little-endian bit string (reading R11) and stored.
+constexpr int kSel8Smem = 8 * kCS16 * 16;
+__global__ void __launch_bounds__(256) nn_select8_kernel(EncArgs a, int64_t bt0) {
+  extern __shared__ __align__(16) unsigned char s8m[];
+  __shared__ uint32_t scode[16];
+  griddep_wait();
+  const int64_t btl = blockIdx.x, bt = bt0 + btl;
+  const int h = blockIdx.y, s = blockIdx.z;
+  const int sub = s ? a.vsub : a.ksub, bits = s ? a.vbits : a.kbits;
+  if (!nn_filtered(sub, bits)) return;
+  const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint16_t* cb = s ? a.cv + h * a.cv_hs : a.ck + h * a.ck_hs;
+  float x[4];
+  if (s == 0) transform_key_lane(a, b, t, h, lane, x);
+  else load_value_lane(a, b, t, h, lane, x);
+  const uint32_t sbuf = smem_u32(s8m) + static_cast<uint32_t>(warp * kCS16 * 16);
+  for (int m = warp; m < 16; m += 8) {
+    float xm[8];   // dims 8m .. 8m + 7 = lanes 2m, 2m + 1
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      xm[i] = __shfl_sync(0xffffffffu, x[i], 2 * m);
+      xm[4 + i] = __shfl_sync(0xffffffffu, x[i], 2 * m + 1);
+    }
+    float X2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) X2 += xm[i] * xm[i];
+    const float slack = 0x1p-20f * X2;
+    float2* pm = reinterpret_cast<float2*>(a.ws) + nn16_ws_row(a, btl, h, s, m);
+    const int nch = (1 << bits) / kCS16;
+    float2 lh[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lh[i] = lane + 32 * i < nch ? __ldcg(pm + lane + 32 * i) : make_float2(INFINITY, INFINITY);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < nch) __stcg(pm + lane + 32 * i, make_float2(0.f, 0.f));   // consumed
+    // pinned distance of d = 8: relative error <= 10 * 2^-24 -> (1 +- 2^-18) factors
+    float U = INFINITY;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) U = fminf(U, (X2 + lh[i].y + slack) * (1.f + 0x1p-18f));
+#pragma unroll
+    for (int off = 16; off; off >>= 1) U = fminf(U, __shfl_xor_sync(0xffffffffu, U, off));
+    unsigned selm[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) selm[i] = __ballot_sync(0xffffffffu, (X2 + lh[i].x - slack) * (1.f - 0x1p-18f) <= U);
+    unsigned long long best = ~0ull;
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i) {
+      unsigned sel = i == 0 ? selm[0] : i == 1 ? selm[1] : i == 2 ? selm[2] : selm[3];
+      while (sel) {
+        const int k = __ffs(sel) - 1 + 32 * i;
+        sel &= sel - 1;
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(cb + static_cast<int64_t>(k) * kCS16 * 8);
+#pragma unroll
+        for (int q = 0; q < kCS16 * 16 / 16 / 32; ++q)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbuf + 16 * (lane + 32 * q)),
+                       "l"(src + 16 * (lane + 32 * q)) : "memory");
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+#pragma unroll 2
+        for (int q = 0; q < kCS16 / 32; ++q) {
+          const uint4 w = lds_u128(sbuf + 16 * (32 * q + lane));
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+          float dsum = 0.f;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {   // left to right over the 8 dims, fp32 RN, no FMA (R9)
+            const float e0 = __fsub_rn(xm[2 * u], __uint_as_float(ww[u] << 16));
+            const float e1 = __fsub_rn(xm[2 * u + 1], __uint_as_float(ww[u] & 0xFFFF0000u));
+            dsum = u == 0 ? __fmul_rn(e0, e0) : __fadd_rn(dsum, __fmul_rn(e0, e0));
+            dsum = __fadd_rn(dsum, __fmul_rn(e1, e1));
+          }
+          const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(dsum)) << 32) |
+                                         static_cast<uint32_t>(k * kCS16 + 32 * q + lane);
+          best = key < best ? key : best;
+        }
+        __syncwarp();
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, off);
+      best = o < best ? o : best;
+    }
+    if (lane == 0) scode[m] = static_cast<uint32_t>(best & 0xFFFFFFFFull);
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  int64_t row;
+  if (!cache_row(a, b, t, h, lane, row)) return;
+  const int rb = 16 * bits / 8;
+  uint8_t* dst = (s ? a.vcodes : a.kcodes) + row * rb;
+  for (int i = lane; i < rb; i += 32) {   // byte i = row bits [8i, 8i + 8): <= 2 codes (b >= 8)
+    const int p = 8 * i, c0 = p / bits, off = p - c0 * bits;
+    uint32_t w = scode[c0];
+    if (c0 + 1 < 16) w |= scode[c0 + 1] << bits;
+    dst[i] = static_cast<uint8_t>(w >> off);
+  }
+}
+
 // ------------------------------------------------------------------ NEXT-2 formats
 // d8b8 / d8b12 / d4b10 / d2b8, D = 128.  One CTA of 256 threads
 // per (token-head, K or V): warp 0 produces the row (key: the pinned smooth + integer FWHT above;
@@ -866,8 +1023,10 @@ constexpr int kGenThreads = 256;
 __global__ void __launch_bounds__(kGenThreads) encode_generic_kernel(EncArgs a) {
   __shared__ __align__(16) float xs[128];
   __shared__ unsigned long long best[64];
+  __shared__ uint4 sbook[512];
   griddep_launch_dependents();
   const int which = blockIdx.z, h = blockIdx.y;
+  if (!((a.gen_mask >> which) & 1)) return;   // this stream goes through the tensor-core filter
   const int64_t bt = blockIdx.x;
   const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -884,12 +1043,19 @@ __global__ void __launch_bounds__(kGenThreads) encode_generic_kernel(EncArgs a) 
     else load_value_lane(a, b, t, h, lane, x);
     *reinterpret_cast<float4*>(xs + 4 * lane) = make_float4(x[0], x[1], x[2], x[3]);
   }
+  // books of <= 8 KiB (d8b8, d4b10, d2b8: the formats this kernel serves) are staged in shared memory
+  const bool staged = n_ent * sub * 2 <= static_cast<int>(sizeof(sbook));
+  if (staged)
+    for (int i = tid; i < n_ent * sub / 8; i += kGenThreads) sbook[i] = reinterpret_cast<const uint4*>(cb)[i];
   __syncthreads();
-  for (int m = 0; m < M; ++m) {
+  const uint16_t* book = staged ? reinterpret_cast<const uint16_t*>(sbook) : cb;
+  // warp w owns sub-vectors m = w, w + 8, ...: its lanes scan centroids j = lane, lane + 32, ... and a
+  // shuffle tree keeps the (dist_bits << 32 | j) minimum -- no cross-warp reduction per sub-vector
+  for (int m = warp; m < M; m += kGenThreads / 32) {
     const float* xm = xs + m * sub;
     unsigned long long key = ~0ull;
-    for (int j = tid; j < n_ent; j += kGenThreads) {
-      const uint16_t* c = cb + static_cast<int64_t>(j) * sub;
+    for (int j = lane; j < n_ent; j += 32) {
+      const uint16_t* c = book + static_cast<int64_t>(j) * sub;
       float e = __fsub_rn(xm[0], __uint_as_float(static_cast<uint32_t>(c[0]) << 16));
       float dsum = __fmul_rn(e, e);
       for (int u = 1; u < sub; ++u) {
@@ -904,7 +1070,7 @@ __global__ void __launch_bounds__(kGenThreads) encode_generic_kernel(EncArgs a) 
       const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, off);
       key = o < key ? o : key;
     }
-    if (lane == 0) atomicMin(&best[m], key);
+    if (lane == 0) best[m] = key;
   }
   __syncthreads();
   const int rb = M * bits / 8;
@@ -939,10 +1105,26 @@ static int64_t nn16_pass_rows(int64_t nbt, int H) {
   return nbt < p ? nbt : p;
 }
 
+static bool nn16_scan_from_env();
+namespace vecinfer {
+// kernel launches of one vecinfer_encode_kv call of B*T token rows (vecinfer_decode_step_launches)
+int encode_launch_count(int64_t nbt, int H, const vecinfer_vq_t& k, const vecinfer_vq_t& v) {
+  if (nbt <= 0) return 0;
+  const bool kf = nn_filtered(k.sub_dim, k.code_bits), vf = nn_filtered(v.sub_dim, v.code_bits);
+  const bool next2 = vq_next2(k) || vq_next2(v);
+  if ((kf || vf) && !(!next2 && nn16_scan_from_env())) {
+    const int64_t np = nn16_pass_rows(nbt, H);
+    return static_cast<int>(2 * ((nbt + np - 1) / np)) + (next2 && !(kf && vf) ? 1 : 0);
+  }
+  if (k.code_bits == 16 || v.code_bits == 16) return nbt * H <= 4096 ? 1 : 2;   // (full-scan experiment)
+  return 1;
+}
+}  // namespace vecinfer
+
 extern "C" size_t vecinfer_encode_workspace_bytes(int32_t B, int32_t T, int32_t H_kv, vecinfer_vq_t kcfg,
                                                   vecinfer_vq_t vcfg) {
   if (B <= 0 || T <= 0 || H_kv <= 0) return 0;
-  if (kcfg.code_bits != 16 && vcfg.code_bits != 16) return 0;
+  if (!nn_filtered(kcfg.sub_dim, kcfg.code_bits) && !nn_filtered(vcfg.sub_dim, vcfg.code_bits)) return 0;
   // tensor-core filter: (lo, hi) per (token-head, stream, sub-vector, 512-centroid chunk) of one
   // pass of nn16_pass_rows(...) token rows (fp32 pairs: 64 KiB per token-head)
   // (the full-scan experiment behind VECINFER_NN16_SCAN=1 needs B*T*H_kv*516 bytes: packed minima +
@@ -1025,32 +1207,42 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
   const int64_t gx = (nbt + kEncWarps - 1) / kEncWarps;
   if (gx > 2147483647) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many tokens");
   if (H_kv > 65535) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many heads");
-  if (vq_next2(kcfg) || vq_next2(vcfg)) {   // one generic launch encodes both streams
-    if (nbt > 2147483647) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many tokens");
-    const cudaError_t e = launch_pdl(encode_generic_kernel, dim3(static_cast<unsigned>(nbt), H_kv, 2),
-                                     dim3(kGenThreads), 0, st, a);
-    if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_generic_kernel: %s", cudaGetErrorString(e)); }
-    return check_launch("encode_generic_kernel");
-  }
-  if ((kcfg.code_bits == 16 || vcfg.code_bits == 16) && !nn16_scan_from_env()) {
-    // tensor-core filter + exact selection (two PDL launches per pass of ~512 token-heads)
+  a.gen_mask = 3;
+  const bool kfilt = nn_filtered(kcfg.sub_dim, kcfg.code_bits), vfilt = nn_filtered(vcfg.sub_dim, vcfg.code_bits);
+  const bool next2 = vq_next2(kcfg) || vq_next2(vcfg);
+  // 65 536-entry d = 4 books and the 4096 / 65 536-entry d = 8 books: tensor-core filter + exact
+  // selection (two PDL launches per pass of ~512 token-heads); a NEXT-2 stream outside that set is
+  // encoded by the generic scan (gen_mask), in its own launch
+  const bool use_filter = (kfilt || vfilt) && !(!next2 && nn16_scan_from_env());
+  if (use_filter) {
     const size_t need = vecinfer_encode_workspace_bytes(B, T, H_kv, kcfg, vcfg);
     if (!workspace || workspace_bytes < need || !aligned(workspace, 16))
-      return fail(VECINFER_ERR_WORKSPACE, "encode_kv: 16-bit codebooks need %zu bytes of workspace", need);
+      return fail(VECINFER_ERR_WORKSPACE, "encode_kv: 16-bit / d8 codebooks need %zu bytes of workspace", need);
     if (kcfg.head_dim != 128 && kcfg.head_dim != 64) return fail(VECINFER_ERR_UNSUPPORTED, "encode_kv: 16-bit head_dim");
-    static bool attr_done = false;   // benign race: idempotent attribute
+    const int ds = kfilt ? kcfg.sub_dim : vcfg.sub_dim;   // (the filtered streams of a pair share d)
+    static bool attr_done = false;   // benign race: idempotent attributes
     if (!attr_done) {
       cudaFuncSetAttribute(nn16_filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+      cudaFuncSetAttribute(nn16_filter_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, nn_filter_smem<4>());
+      cudaFuncSetAttribute(nn16_filter_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, nn_filter_smem<8>());
+      cudaFuncSetAttribute(nn_select8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSel8Smem);
       attr_done = true;
     }
-    const bool hmma = nn16_hmma_from_env();
+    if (next2 && !(kfilt && vfilt)) {   // the other stream: the generic scan, one CTA per (token-head)
+      a.gen_mask = kfilt ? 2 : 1;
+      if (nbt > 2147483647) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many tokens");
+      const cudaError_t e = launch_pdl(encode_generic_kernel, dim3(static_cast<unsigned>(nbt), H_kv, 2),
+                                       dim3(kGenThreads), 0, st, a);
+      if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_generic_kernel: %s", cudaGetErrorString(e)); }
+    }
+    const bool hmma = nn16_hmma_from_env() || ds == 8;   // (the tcgen05 variant covers d = 4)
     const int64_t np = nn16_pass_rows(nbt, H_kv);
-    const int nbk = (kcfg.code_bits == 16 ? (ck_head_stride ? H_kv : 1) : 0) +
-                    (vcfg.code_bits == 16 ? (cv_head_stride ? H_kv : 1) : 0);
+    const int nbk = (kfilt ? (ck_head_stride ? H_kv : 1) : 0) + (vfilt ? (cv_head_stride ? H_kv : 1) : 0);
+    const int maxch = (1 << ((kfilt ? kcfg.code_bits : 0) > (vfilt ? vcfg.code_bits : 0) ? kcfg.code_bits : vcfg.code_bits)) / kCS16;
     for (int64_t b0 = 0; b0 < nbt; b0 += np) {
       const int nb = static_cast<int>(nbt - b0 < np ? nbt - b0 : np);
       // rows of the largest book (shared books hold every head's rows)
-      const int64_t rows = static_cast<int64_t>(nb) * H_kv * a.nsub;
+      const int64_t rows = static_cast<int64_t>(nb) * H_kv * (kcfg.head_dim / ds);
       cudaError_t e;
       if (!hmma) {   // tcgen05 filter (VECINFER_NN16_TC=1): 128-row CTAs, <= 2 per SM (256 TMEM columns each)
         const int64_t rblk = (rows + kTcRows - 1) / kTcRows;
@@ -1062,15 +1254,24 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
         const int64_t rblk = (rows + kRows16 - 1) / kRows16;
         // chunks per CTA: amortise the rows' transform over up to 8 chunks while keeping >= ~4 CTAs per SM
         int ncpb = 8;
-        while (ncpb > 1 && (kNC16 / ncpb) * rblk * nbk < 4 * device_sm_count()) ncpb >>= 1;
-        const dim3 g1(kNC16 / ncpb, static_cast<unsigned>(rblk), static_cast<unsigned>(nbk));
-        e = launch_pdl(nn16_filter_kernel, g1, dim3(kFW16 * 32), 0, st, a, b0, nb, ncpb);
+        while (ncpb > 1 && ((maxch + ncpb - 1) / ncpb) * rblk * nbk < 4 * device_sm_count()) ncpb >>= 1;
+        const dim3 g1((maxch + ncpb - 1) / ncpb, static_cast<unsigned>(rblk), static_cast<unsigned>(nbk));
+        e = ds == 4 ? launch_pdl(nn16_filter_kernel<4>, g1, dim3(kFW16 * 32), nn_filter_smem<4>(), st, a, b0, nb, ncpb)
+                    : launch_pdl(nn16_filter_kernel<8>, g1, dim3(kFW16 * 32), nn_filter_smem<8>(), st, a, b0, nb, ncpb);
       }
       if (e == cudaSuccess)
-        e = launch_pdl(nn16_select_kernel, dim3(static_cast<unsigned>(nb), H_kv, 8), dim3(kSelWarps * 32), 0, st, a, b0);
-      if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_kv (16-bit): %s", cudaGetErrorString(e)); }
+        e = ds == 4 ? launch_pdl(nn16_select_kernel, dim3(static_cast<unsigned>(nb), H_kv, 8), dim3(kSelWarps * 32), 0, st, a, b0)
+                    : launch_pdl(nn_select8_kernel, dim3(static_cast<unsigned>(nb), H_kv, 2), dim3(256), kSel8Smem, st, a, b0);
+      if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_kv (filter): %s", cudaGetErrorString(e)); }
     }
-    return check_launch("encode_kv (16-bit)");
+    return check_launch("encode_kv (filter)");
+  }
+  if (next2) {   // one generic launch encodes both streams
+    if (nbt > 2147483647) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many tokens");
+    const cudaError_t e = launch_pdl(encode_generic_kernel, dim3(static_cast<unsigned>(nbt), H_kv, 2),
+                                     dim3(kGenThreads), 0, st, a);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_generic_kernel: %s", cudaGetErrorString(e)); }
+    return check_launch("encode_generic_kernel");
   }
   if (kcfg.code_bits == 16 || vcfg.code_bits == 16) {   // VECINFER_NN16_SCAN=1: the full pinned scan
     const size_t need = static_cast<size_t>(B) * T * H_kv * (2 * 32 * sizeof(unsigned long long) + sizeof(uint32_t));

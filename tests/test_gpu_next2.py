@@ -161,7 +161,10 @@ def test_next2_decode_step(kn, vn, wp_off):
                           vcfg=vcfg, err_flags=err)
     assert int(err.item()) == 0
     fused = kn in ("d8b8", "d2b8", "d4b10") and vn in ("d8b8", "d2b8", "d4b10")
-    assert vi.decode_step_launches(B, H, 610, kcfg, vcfg) == (1 if fused else 2)
+    # separate append of d8b12 / d8b16 streams: tensor-core filter + exact selection (2 launches), plus
+    # one generic launch for the other stream of a mixed pair, then the attention launch
+    filt = [n in ("d8b12", "d8b16") for n in (kn, vn)]
+    assert vi.decode_step_launches(B, H, 610, kcfg, vcfg) == (1 if fused else 3 + (1 if any(filt) and not all(filt) else 0))
     for b in range(B):
         for h in range(H):
             ckh = c["ck"] if c["ck"].ndim == 2 else c["ck"][h]

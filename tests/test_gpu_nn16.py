@@ -155,3 +155,56 @@ def test_nn16_tcgen05_filter_variant():
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_nn16.py"),
                         "-k", "not tcgen05"], env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+# ---- d = 8 books (NEXT-2 d8b12: 4096 entries, d8b16: 65 536 entries): K = 32 filter, two chained MMAs
+def _random_book8(seed, n, heads=None, scale=1.0):
+    shape = (n, 8) if heads is None else (heads, n, 8)
+    return synth.round_to_bf16(np.random.default_rng(seed).normal(0, scale, shape).astype(np.float32))
+
+
+def test_nn_d8b12_per_head_books_several_passes():
+    """Per-head 4096 x 8 K books and a shared V book, 65 tokens x 8 heads = two passes."""
+    H, T = 8, 65
+    k = synth.gen_keys(T, H, 128, seed=1700)
+    v = synth.gen_values(T, H, 128, seed=1701)
+    ck = _random_book8(1702, 4096, heads=H)
+    cv = _random_book8(1703, 4096)
+    got = _encode_gpu(k, v, CB["inv_lambda"], ck, cv, T + 2, [2], vi.D8B12, vi.D8B12)
+    want = _encode_ref(k, v, CB["inv_lambda"], ck, cv, T + 2, [2], vi.D8B12, vi.D8B12)
+    assert np.array_equal(got[0], want[0]), "key codes differ"
+    assert np.array_equal(got[1], want[1]), "value codes differ"
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-6, 1e-3])
+def test_nn_d8b16_points_next_to_centroids(eps):
+    cv = _random_book8(1710, 65536)
+    cv[9] = cv[50000]                                     # duplicate: the lower index wins
+    rng = np.random.default_rng(1711)
+    T = 4
+    idx = rng.integers(0, 65536, size=(T, 16))
+    idx[0, :2] = 50000
+    pts = cv[idx].reshape(1, T, 1, 128) + eps * rng.standard_normal((1, T, 1, 128)).astype(np.float32)
+    pts = synth.round_to_bf16(pts.astype(np.float32))
+    k = np.zeros_like(pts)
+    got = _encode_gpu(k, pts, np.ones((1, 128), np.float32), cv, cv, T, [0], vi.D8B16, vi.D8B16)
+    want = _encode_ref(k, pts, np.ones((1, 128), np.float32), cv, cv, T, [0], vi.D8B16, vi.D8B16)
+    assert np.array_equal(got[1], want[1])
+    if eps == 0.0:
+        assert ref.unpack_codes(got[1][0, 0, 0], 16)[0] == 9
+
+
+@pytest.mark.parametrize("kn,vn", [("d8b12", "d8b8"), ("d4b10", "d8b12"), ("d8b16", "d8b16")])
+def test_nn_d8_mixed_pairs(kn, vn):
+    """The paper's mixed pairs: the d8b12 / d8b16 stream through the filter, the other (d8b8 / d4b10)
+    through the generic scan in its own launch."""
+    cfg = {"d8b8": vi.D8B8, "d8b12": vi.D8B12, "d4b10": vi.D4B10, "d8b16": vi.D8B16}
+    T = 6
+    k = synth.gen_keys(T, 3, 128, seed=1720, batch=2)
+    v = synth.gen_values(T, 3, 128, seed=1721, batch=2)
+    ck, cv = CB[f"ck_{kn}"], CB[f"cv_{vn}"]
+    ck = ck if ck.ndim == 2 else ck[:3]
+    cv = cv if cv.ndim == 2 else cv[:3]
+    got = _encode_gpu(k, v, CB["inv_lambda"][:3], ck, cv, T + 1, [1, 0], cfg[kn], cfg[vn])
+    want = _encode_ref(k, v, CB["inv_lambda"][:3], ck, cv, T + 1, [1, 0], cfg[kn], cfg[vn])
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
