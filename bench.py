@@ -455,11 +455,15 @@ def run_ours(args, rank, world, local_rank):
         attn_ms = [elapsed_ms / (K * L)]
 
     # ---- end to end through the public API: pinned host inputs -> device, eager calls, D2H read
-    q_h = q_all.cpu().pin_memory()
-    kn_h = kn_all.cpu().pin_memory()
-    vn_h = vn_all.cpu().pin_memory()
+    # a layer's inputs (q | k_new | v_new, bf16) are one slot of a packed pinned host buffer and of
+    # its device twin, so a chunk of layers is ONE host-to-device copy
+    nq, nk, nv = q_all[0].numel(), kn_all[0].numel(), vn_all[0].numel()
+    h_in = torch.cat([q_all.reshape(L, nq), kn_all.reshape(L, nk), vn_all.reshape(L, nv)], dim=1).cpu().pin_memory()
+    d_in = torch.empty_like(h_in, device=dev)
+    q_d = [d_in[l, :nq].view(q_all.shape[1:]) for l in range(L)]
+    kn_d = [d_in[l, nq:nq + nk].view(kn_all.shape[1:]) for l in range(L)]
+    vn_d = [d_in[l, nq + nk:].view(vn_all.shape[1:]) for l in range(L)]
     o_h = torch.empty(o_all.shape, dtype=o_all.dtype).pin_memory()
-    q_d, kn_d, vn_d = torch.empty_like(q_all), torch.empty_like(kn_all), torch.empty_like(vn_all)
 
     def layer_e2e(l):
         if fused:
@@ -492,31 +496,31 @@ def run_ours(args, rank, world, local_rank):
     cs_in = torch.cuda.Stream(device=dev) if pipelined else None
     cs_out = torch.cuda.Stream(device=dev) if pipelined else None
 
-    n_chunks = 4 if L % 4 == 0 else 1   # layer chunks: few, large copies (a copy node costs ~2 us)
+    # 4 layer chunks, one packed copy each per direction (a copy node costs ~2 us: 6 uneven chunks
+    # with small first / last ones measured slower at cfg2, 1172 vs 1186 GB/s e2e)
+    # large batches (>= 256 KiB of inputs per layer, e.g. cfg3) use 8 chunks: the first chunk's copy is
+    # not overlapped, so its size matters more than the extra copy nodes
+    n_chunks = (8 if h_in[0].numel() * h_in.element_size() >= 256 * 1024 else 4) if L % 8 == 0 else 1
+    chunks = [(c * L // n_chunks, (c + 1) * L // n_chunks) for c in range(n_chunks)]
 
     def step_e2e_pipelined_body():
-        per = L // n_chunks
-        ev_in = [torch.cuda.Event() for _ in range(n_chunks)]
-        ev_out = [torch.cuda.Event() for _ in range(n_chunks)]
+        ev_in = [torch.cuda.Event() for _ in chunks]
+        ev_out = [torch.cuda.Event() for _ in chunks]
         cur = torch.cuda.current_stream(dev)
         cs_in.wait_stream(cur)
         cs_out.wait_stream(cur)
         with torch.cuda.stream(cs_in):
-            for c in range(n_chunks):
-                sl = slice(c * per, (c + 1) * per)
-                q_d[sl].copy_(q_h[sl], non_blocking=True)
-                kn_d[sl].copy_(kn_h[sl], non_blocking=True)
-                vn_d[sl].copy_(vn_h[sl], non_blocking=True)
+            for c, (a, b) in enumerate(chunks):
+                d_in[a:b].copy_(h_in[a:b], non_blocking=True)
                 ev_in[c].record(cs_in)
-        for c in range(n_chunks):
-            sl = slice(c * per, (c + 1) * per)
+        for c, (a, b) in enumerate(chunks):
             cur.wait_event(ev_in[c])
-            for l in range(c * per, (c + 1) * per):
+            for l in range(a, b):
                 layer_e2e(l)
             ev_out[c].record(cur)
             with torch.cuda.stream(cs_out):
                 cs_out.wait_event(ev_out[c])
-                o_h[sl].copy_(o_all[sl], non_blocking=True)
+                o_h[a:b].copy_(o_all[a:b], non_blocking=True)
         cur.wait_stream(cs_in)
         cur.wait_stream(cs_out)
 
@@ -529,16 +533,20 @@ def run_ours(args, rank, world, local_rank):
         with torch.cuda.graph(g_e2e, stream=stream):
             step_e2e_pipelined_body()
 
+    done_ev = torch.cuda.Event()
+
     def step_e2e():
         if g_e2e is not None:
             g_e2e.replay()
         else:
-            q_d.copy_(q_h, non_blocking=True)
-            kn_d.copy_(kn_h, non_blocking=True)
-            vn_d.copy_(vn_h, non_blocking=True)
+            d_in.copy_(h_in, non_blocking=True)
             layers_e2e()
             o_h.copy_(o_all, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
+        # the host waits for the step's result (o in pinned host memory) by polling an event: a
+        # serving loop spins here rather than sleeping in cudaStreamSynchronize
+        done_ev.record(torch.cuda.current_stream(dev))
+        while not done_ev.query():
+            pass
 
 
     with torch.cuda.stream(stream):
@@ -563,7 +571,7 @@ def run_ours(args, rank, world, local_rank):
         ranks = [None] * world
         dist.all_gather_object(ranks, rank_info)
     p2p_err = int(p2p.err.item()) if p2p is not None else 0
-    h2d = q_h.numel() * 2 + kn_h.numel() * 2 + vn_h.numel() * 2 if owns_tail else q_h.numel() * 2
+    h2d = h_in.numel() * h_in.element_size()   # q, k_new, v_new of every layer (packed slots)
     d2h = o_h.numel() * 2
 
     if rank != 0:
@@ -663,7 +671,7 @@ def run_ours(args, rank, world, local_rank):
                      "lsu_bound": lsu, "gather_bound": gather},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_ms / K, "api": ("32 x vecinfer.decode_step + pinned H2D / D2H copies in 4 layer chunks pipelined on two copy streams, one CUDA graph per step, host sync on the result; " if g_e2e is not None else "32 eager vecinfer calls, ")
+                "ms_per_step": e2e_ms / K, "api": ("32 x vecinfer.decode_step + pinned H2D / D2H copies in 4 layer chunks (8 at >= 256 KiB of inputs per layer; one packed copy per chunk and direction) pipelined on two copy streams, one CUDA graph per step, host waits on the result (event poll); " if g_e2e is not None else "32 eager vecinfer calls, ")
                        + "pinned H2D of q/k/v and D2H of o every step"},
         "gpu_launches": launches_per_step * K,
         "ranks": ranks if world > 1 else None,
