@@ -208,3 +208,37 @@ def test_nn_d8_mixed_pairs(kn, vn):
     got = _encode_gpu(k, v, CB["inv_lambda"][:3], ck, cv, T + 1, [1, 0], cfg[kn], cfg[vn])
     want = _encode_ref(k, v, CB["inv_lambda"][:3], ck, cv, T + 1, [1, 0], cfg[kn], cfg[vn])
     assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("fmt", ["b4d4", "d8b16"])
+def test_nn_filter_paged_pool(fmt):
+    """The filter path writes through the block table: paged prefill + 1-token append land at the
+    translated rows with the oracle's codes; spare pages stay untouched."""
+    from test_gpu_paged import _unpaginate
+    cfg = {"b4d4": vi.B4D4, "d8b16": vi.D8B16}[fmt]
+    B, H, ps, npb = 2, 4, 32, 3
+    n_cap = ps * npb
+    rng = np.random.default_rng(1730)
+    n_pages = B * npb + 2
+    bt = rng.permutation(n_pages)[:B * npb].reshape(B, npb).astype(np.int32)
+    kpool = torch.zeros(n_pages, H, ps, cfg.row_bytes, dtype=torch.uint8, device="cuda")
+    vpool = torch.zeros_like(kpool)
+    T = 7
+    k = synth.gen_keys(T, H, 128, seed=1731, batch=B)
+    v = synth.gen_values(T, H, 128, seed=1732, batch=B)
+    inv, ck, cv = CB["inv_lambda"][:H], CB[f"ck_{fmt}"], CB[f"cv_{fmt}"]
+    wp = np.array([0, 40], np.int32)
+    vi.encode_kv(t_bf16(k), t_bf16(v), torch.from_numpy(inv).cuda(), t_bf16(ck), t_bf16(cv), kpool, vpool,
+                 torch.from_numpy(wp).cuda(), cfg, cfg, block_table=torch.from_numpy(bt).cuda())
+    kc = _unpaginate(kpool.cpu().numpy(), bt, ps)
+    vc = _unpaginate(vpool.cpu().numpy(), bt, ps)
+    exp_k = np.zeros((B, H, n_cap, cfg.row_bytes), np.uint8)
+    exp_v = np.zeros_like(exp_k)
+    for b in range(B):
+        for h in range(H):
+            kk, vv = ref.encode_kv(k[b, :, h], v[b, :, h], inv[h], ck, cv)
+            exp_k[b, h, wp[b]:wp[b] + T] = ref.pack_codes(kk, cfg.code_bits)
+            exp_v[b, h, wp[b]:wp[b] + T] = ref.pack_codes(vv, cfg.code_bits)
+    assert np.array_equal(kc, exp_k) and np.array_equal(vc, exp_v)
+    spare = np.setdiff1d(np.arange(n_pages), bt.ravel())
+    assert not kpool[torch.from_numpy(spare).cuda().long()].any()
