@@ -212,7 +212,8 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     import synth
     from paper_2510_06175_b200 import vecinfer as vi
-    from paper_2510_06175_b200.sharding import P2PExchange, batch_shard, gather_partials_packed, shard_range
+    from paper_2510_06175_b200.sharding import (P2PExchange, XRankWindows, batch_shard, gather_partials_packed,
+                                                shard_range)
 
     dev = torch.device("cuda", local_rank if args.backend == "nccl" else local_rank % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
@@ -323,7 +324,10 @@ def run_ours(args, rank, world, local_rank):
         if ev_pair is not None:
             ev_pair[0].record()
         ec = EC and not owns_tail   # an encode_kv launched right before writes this layer's cache
-        if seq_sharded:
+        if seq_sharded and xrw is not None:   # attention + cross-rank merge in one launch
+            vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
+                           lse=lse_m[l], workspace=ws[l], early_cache=ec, xr=xrw)
+        elif seq_sharded:
             vi.attn_decode(q_all[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_part[l],
                            lse=lse_all[l], workspace=ws[l], early_cache=ec)
         else:
@@ -331,14 +335,31 @@ def run_ours(args, rank, world, local_rank):
                            lse=lse_all[l], workspace=ws[l], early_cache=ec)
         if ev_pair is not None:
             ev_pair[1].record()
-        if seq_sharded:   # layer l's output feeds layer l+1: its partials are exchanged right away
+        if seq_sharded and xrw is None:   # layer l's output feeds layer l+1: its partials are exchanged right away
             exchange_layer(l)
 
     # sequence-sharded exchange, once PER LAYER (16.1 KiB of partials per rank and layer at B = 1):
     # the fused peer-memory kernel (vecinfer_merge_lse_p2p: remote stores into every rank's IPC
     # window + flags + rank-order merge, one launch, graph-safe) or NCCL all-gather of the packed
     # partials + vecinfer_merge_lse (--exchange nccl; gloo through host copies for 1-GPU checks)
-    p2p, p2p_fallback = None, None
+    p2p, p2p_fallback, xrw = None, None, None
+    if seq_sharded and args.exchange == "xr":
+        # the cross-rank merge fused INTO the attention launch (vecinfer_attn_decode_xr): each CTA
+        # stores its rank-merged slice into every rank's window and merges the P partials itself; no
+        # exchange launch at all.  Same IPC windows as P2PExchange; falls back to it if mapping fails.
+        ok, why = 1, None
+        try:
+            xrw = XRankWindows(B * H_Q, D, dev)
+        except Exception as ex:   # noqa: BLE001 -- reported in the line
+            ok, why = 0, f"{type(ex).__name__}: {ex}"
+        t_ok = torch.tensor([ok], dtype=torch.int32, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+        if int(t_ok.item()) == 0:
+            if xrw is not None:
+                xrw.close()
+                xrw = None
+            args.exchange = "p2p"
+            p2p_fallback = why or "a peer rank could not map the fused-merge windows"
     if seq_sharded and args.exchange == "p2p":
         # the peer windows need CUDA IPC + peer access between the ranks' GPUs; if the platform
         # refuses (on every rank alike: the outcome is all-reduced), run the all-gather exchange
@@ -354,7 +375,7 @@ def run_ours(args, rank, world, local_rank):
                 p2p.close()
                 p2p = None
             args.exchange = "nccl"
-            p2p_fallback = why or "a peer rank could not map the P2P windows"
+            p2p_fallback = (p2p_fallback + "; " if p2p_fallback else "") + (why or "a peer rank could not map the P2P windows")
     lse_m = torch.empty(L, B, H_Q, dtype=torch.float32, device=dev) if seq_sharded else None
 
     def exchange_layer(l):
@@ -379,7 +400,7 @@ def run_ours(args, rank, world, local_rank):
     else:
         # + one exchange per layer when sequence-sharded (the P2P kernel; NCCL's own kernels and
         # merge_lse with --exchange nccl: 1 of ours)
-        launches_per_step = L * ((append_kernels if owns_tail else 0) + 1 + (1 if seq_sharded else 0))
+        launches_per_step = L * ((append_kernels if owns_tail else 0) + 1 + (1 if seq_sharded and xrw is None else 0))
 
     # ---- warm-up (eager) so lazy init/attributes happen outside capture
     with torch.cuda.stream(stream):
@@ -388,7 +409,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize(dev)
 
     # NCCL all-gather kept eager; the fused P2P exchange keeps its epoch on the device: graph-safe
-    use_graph = not args.no_graph and (not seq_sharded or p2p is not None)
+    use_graph = not args.no_graph and (not seq_sharded or p2p is not None or xrw is not None)
     K, W = args.steps, args.warmup
     if use_graph:
         g_step = torch.cuda.CUDAGraph()
@@ -475,7 +496,10 @@ def run_ours(args, rank, world, local_rank):
         if owns_tail:
             vi.encode_kv(kn_d[l], vn_d[l], inv, ck, cv, kcs[l], vcs[l], write_pos, kcfg, vcfg, workspace=enc_ws)
         ec = EC and not owns_tail
-        if seq_sharded:
+        if seq_sharded and xrw is not None:
+            vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_all[l],
+                           lse=lse_m[l], workspace=ws[l], early_cache=ec, xr=xrw)
+        elif seq_sharded:
             vi.attn_decode(q_d[l], lam, ck, cv, kcs[l], vcs[l], seq_lens, kcfg=kcfg, vcfg=vcfg, out=o_part[l],
                            lse=lse_all[l], workspace=ws[l], early_cache=ec)
             exchange_layer(l)
@@ -570,7 +594,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         ranks = [None] * world
         dist.all_gather_object(ranks, rank_info)
-    p2p_err = int(p2p.err.item()) if p2p is not None else 0
+    p2p_err = int(p2p.err.item()) if p2p is not None else (int(xrw.err.item()) if xrw is not None else 0)
     h2d = h_in.numel() * h_in.element_size()   # q, k_new, v_new of every layer (packed slots)
     d2h = o_h.numel() * 2
 
@@ -644,8 +668,9 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": args.workload, "desc": desc, "global_batch": B_glob, "seq_len": N,
                    "layers_per_step": L, "q_heads": H_Q, "kv_heads": H_KV, "head_dim": D, "codebook": f"K-{CB_NAME[kbits]}/V-{CB_NAME[vbits]}",
                    "parallelism": ("seq-shard" if seq_sharded else "dp") + str(world),
-                   "exchange": (("p2p-fused-merge" if args.exchange == "p2p" else
-                                 f"{args.backend}-allgather+merge_lse") + ", per layer (32 exchanges per step)"
+                   "exchange": ((("xr: cross-rank merge fused into the attention launch (vecinfer_attn_decode_xr)"
+                                  if args.exchange == "xr" else "p2p-fused-merge" if args.exchange == "p2p" else
+                                  f"{args.backend}-allgather+merge_lse") + ", per layer (32 exchanges per step)")
                                 if seq_sharded else None),
                    "l2": f"inputs larger than L2: {L} distinct layer caches = {code_bytes_rank * L / 2**20:.0f} MiB/rank per step",
                    "num_splits": S, "attn_kernel": kernel_kind, "cuda_graph": use_graph, "residual_window": R, "fused_append": fused_launch, "early_cache": EC,
@@ -707,8 +732,9 @@ def main():
     ap.add_argument("--residual", type=int, default=0,
                     help="full-precision residual window of R tokens (P:494: 128); the step appends into it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
-                    help="cfg4 at N>1: fused peer-memory exchange+merge kernel, or NCCL all-gather + merge_lse")
+    ap.add_argument("--exchange", default="xr", choices=["xr", "p2p", "nccl"],
+                    help="cfg4 at N>1: merge fused into the attention launch (xr), a separate fused peer-memory "
+                         "exchange+merge kernel (p2p), or NCCL all-gather + merge_lse")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=2.0)
     args = ap.parse_args()
