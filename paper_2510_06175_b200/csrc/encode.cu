@@ -598,22 +598,9 @@ constexpr int nn_filter_smem() {
   return 2 * (kCS16 / 8) * 32 * (DS == 4 ? 8 : 16) + kFW16 * 32 * DS * 4 + 2 * kFW16 * 2 * 4;
 }
 
-// tcgen05 variant of the filter (opt-in VECINFER_NN16_TC=1: measured 1.2-1.6x slower than the
-// mma.sync filter, see below; same arithmetic and error bound, same workspace contract): one CTA of 4 warps holds 128 book rows as the M = 128 A tile in shared memory (K-major,
-// no swizzle, K = 16: [-2x hi | mid | lo parts | 1 1 1 0]); the chunk's centroids stream through
-// two 4 KiB B tiles of N = 128 centroids ([c | c | c | ||c||^2 parts | 0]); one thread issues
-// tcgen05.mma kind::f16 (bf16 in, fp32 out) into one of two 128-column TMEM accumulators (unit u+1's
-// MMA runs while the warps read unit u), and thread r reads TMEM lane r = its own row with
-// tcgen05.ld.32x32b.x64 and folds the values with 3-input FMNMX.  The MMA leaves the SM's issue slots
-// to the min reduction, but at K = 16 each unit's MMA is tiny (136 clk at peak) and the per-unit
-// hand-off (mbarrier wait, TMEM load, restage, CTA barrier) with only 8 warps per SM costs more than
-// the mma.sync filter's barrier-free loop over 32 warps (ncu: barrier + wait stalls dominate).
+// tcgen05 helpers of the warp-specialised filter variant below (M = 128 rows, K = 16, bf16 in, fp32 out)
 constexpr int kTcRows = 128;                      // M
-constexpr int kTcN = 128;                         // centroids per MMA (unit): 128 or 256
 constexpr int kTcTile = kTcRows * 32;             // A tile bytes (128 x 16 bf16)
-// N = 128: two CTAs per SM (2 x 256 TMEM columns, > 76 KiB of shared memory each); N = 256 (measured
-// slower): one CTA per SM with all 512 columns
-constexpr int kTcSmem = kTcN == 128 ? 80 * 1024 : 120 * 1024;
 __device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
@@ -640,20 +627,39 @@ __device__ __forceinline__ void tc_ld_32x32b_x64(uint32_t taddr, uint32_t (&r)[6
 // byte offset of (row r, 16-byte K group kg) in a K-major no-swizzle 128 x 16 tile: core matrices of
 // 8 rows x 16 B, next 8 rows at +128 B (SBO), next K group at +2048 B (LBO)
 __device__ __forceinline__ uint32_t tc_tile_off(int r, int kg) { return kg * 2048 + (r >> 3) * 128 + (r & 7) * 16; }
-// the same for the N = kTcN-row B tile (next K group at + kTcN * 16 B)
-__device__ __forceinline__ uint32_t tc_btile_off(int r, int kg) { return kg * (kTcN * 16) + (r >> 3) * 128 + (r & 7) * 16; }
 
-// grid (kNC16 / ncpb, row blocks of 128, books), 256 threads: warps w and w + 4 read TMEM lane
-// quadrant w (rows 32w..32w+31), columns [0, 64) / [64, 128) of each unit; warps 0-3 build the A tile,
-// warps 4-7 stage the B tiles one unit ahead (centroids prefetched into registers two units ahead)
-__global__ void __launch_bounds__(256) nn16_filter_tc_kernel(EncArgs a, int64_t bt0, int nbt_p, int ncpb) {
-  extern __shared__ __align__(1024) unsigned char tsm[];
-  // [0, 4K) A tile | [4K, 12K) B ring (2 units) | mbarriers, TMEM address, bounds, half-row minima
-  constexpr int kBT = kTcN * 32;   // B tile bytes
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(tsm + kTcTile + 2 * kBT);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tsm + kTcTile + 2 * kBT + 16);
-  float* sbnd = reinterpret_cast<float*>(tsm + kTcTile + 2 * kBT + 32);    // [2 chunk slots][4 warps][2]
-  float* smin = reinterpret_cast<float*>(tsm + kTcTile + 2 * kBT + 128);   // [128 rows]
+// Warp-specialised tcgen05 filter (opt-in VECINFER_NN16_TC=1; same arithmetic, error bound and
+// workspace contract as nn16_filter_kernel): one CTA per SM (all 512 TMEM columns), 128 book rows as
+// the A tile in shared memory (K-major, no swizzle, K = 16: [-2x hi | mid | lo | 1 1 1 0]); warp 0
+// issues tcgen05.mma kind::f16 (bf16 in, fp32 out, N = 256 centroids [c | c | c | ||c||^2 parts | 0]
+// per unit) into one of two 256-column TMEM accumulators, warps 1-3 stage B tiles into a 4-deep
+// ring, warps 4-11 read D (TMEM lane quadrant w % 4 = their 32 rows, one half of the columns each,
+// tcgen05.ld.32x32b.x64) and fold the minima with 3-input FMNMX.  Hand-offs are mbarriers only:
+// bfull / bempty per B stage, dfull / dempty per accumulator.  Measured ~1.15x SLOWER than the
+// mma.sync filter: reading the fp32 accumulator back out of TMEM (128 x 256 x 4 B per unit) caps the
+// min-reduction near the mma.sync pipe's own rate (0.465 HMMA x 128 results per clk and SM), so the
+// tensor-core speed-up has nothing to feed (profiles/r02/exp_nn16_filter.txt).
+constexpr int kWsN = 256, kWsStages = 4;
+constexpr int kWsBT = kWsN * 32;                           // B tile bytes (256 x 16 bf16)
+constexpr int kWsSmem = 120 * 1024;                        // > 114 KiB: one CTA per SM
+__device__ __forceinline__ uint32_t ws_btile_off(int r, int kg) { return kg * (kWsN * 16) + (r >> 3) * 128 + (r & 7) * 16; }
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mbar) : "memory");
+}
+
+constexpr int kWsThreads = 384;   // warp 0 MMA, 1-3 stagers, 4-11 reducers (two per TMEM lane quadrant)
+__global__ void __launch_bounds__(kWsThreads, 1) nn16_filter_ws_kernel(EncArgs a, int64_t bt0, int nbt_p, int ncpb) {
+  extern __shared__ __align__(1024) unsigned char wsm[];
+  // [0, 4K) A | [4K, 4K + 4 x 8K) B ring | barriers | TMEM slot | chunk bounds [ncpb][2]
+  const uint32_t sA = smem_u32(wsm), sB = sA + kTcTile;
+  unsigned char* misc = wsm + kTcTile + kWsStages * kWsBT;
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(misc);
+  uint64_t* bempty = bfull + kWsStages;
+  uint64_t* dfull = bempty + kWsStages;
+  uint64_t* dempty = dfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
+  float* cbnd = reinterpret_cast<float*>(misc + 256);   // [ncpb][2]: max |c_i|, max ||c||^2 per chunk
+  float* smin = cbnd + 64;                              // [128 rows]: column-half minima of a chunk
   int s, hb;
   bool shared;
   nn16_book(a, blockIdx.z, s, hb, shared);
@@ -662,65 +668,38 @@ __global__ void __launch_bounds__(256) nn16_filter_tc_kernel(EncArgs a, int64_t 
   const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kTcRows;
   if (row0 >= rows) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool stager = warp >= 4;
-  const int rt = tid & 127;   // row (warps 0-3) / staged centroid of the unit (warps 4-7)
-  constexpr int kUpc = kCS16 / kTcN;   // units per chunk
-  const int chunk0 = blockIdx.x * ncpb, nunits = ncpb * kUpc;
-  const uint32_t sA = smem_u32(tsm), sB = sA + kTcTile;
-  if (warp == 0) tc::alloc(smem_u32(tmem_slot), 2 * kTcN);
+  const int chunk0 = blockIdx.x * ncpb, nunits = ncpb * (kCS16 / kWsN);
+  const uint16_t* cbook = s == 0 ? a.ck + hb * a.ck_hs : a.cv + hb * a.cv_hs;
+  const uint16_t* crange = cbook + static_cast<int64_t>(chunk0) * kCS16 * 4;
+  if (warp == 0) tc::alloc(smem_u32(tmem_slot), 512);
   if (tid == 0) {
-    tc::mbar_init(smem_u32(mbar), 1);
-    tc::mbar_init(smem_u32(mbar + 1), 1);
+    for (int i = 0; i < kWsStages; ++i) { tc::mbar_init(smem_u32(bfull + i), 96); tc::mbar_init(smem_u32(bempty + i), 1); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(smem_u32(dfull + i), 1); tc::mbar_init(smem_u32(dempty + i), 8); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint16_t* cbook = s == 0 ? a.ck + hb * a.ck_hs : a.cv + hb * a.cv_hs;
-  // a stager handles centroids rt (and rt + 128 when N = 256) of each unit
-  auto fetch = [&](int u) -> uint4 {
-    if (u >= nunits) return make_uint4(0u, 0u, 0u, 0u);
-    const uint16_t* p = cbook + (static_cast<int64_t>(chunk0) * kCS16 + kTcN * u + rt) * 4;
-    const uint2 w0 = *reinterpret_cast<const uint2*>(p);
-    const uint2 w1 = kTcN == 256 ? *reinterpret_cast<const uint2*>(p + 128 * 4) : make_uint2(0u, 0u);
-    return make_uint4(w0.x, w0.y, w1.x, w1.y);
-  };
-  float cm_acc = 0.f, nm_acc = 0.f;   // stagers: bounds of the chunk being staged
-  auto stage = [&](int u, uint4 w4) {   // B row = centroid: K 0..7 = c c, K 8..15 = c n0 n1 n2 0
-#pragma unroll
-    for (int e = 0; e < kTcN / 128; ++e) {
-      const uint2 w = e ? make_uint2(w4.z, w4.w) : make_uint2(w4.x, w4.y);
+  // chunk bounds (static codebook), all threads, before the grid-dependency wait
+  for (int ci = warp; ci < ncpb; ci += kWsThreads / 32) {
+    float cm = 0.f, nm = 0.f;
+    for (int j = lane; j < kCS16; j += 32) {
+      const uint2 w = *reinterpret_cast<const uint2*>(crange + (static_cast<int64_t>(ci) * kCS16 + j) * 4);
       const float c0 = __uint_as_float(w.x << 16), c1 = __uint_as_float(w.x & 0xFFFF0000u);
       const float c2 = __uint_as_float(w.y << 16), c3 = __uint_as_float(w.y & 0xFFFF0000u);
-      const float n = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(c0, c0), __fmul_rn(c1, c1)), __fmul_rn(c2, c2)), __fmul_rn(c3, c3));
-      uint32_t n0, n1, n2;
-      split3_bf16(n, n0, n1, n2);
-      const uint32_t b = sB + (u & 1) * kBT;
-      const int col = rt + 128 * e;
-      sts_u128(b + tc_btile_off(col, 0), make_uint4(w.x, w.y, w.x, w.y));
-      sts_u128(b + tc_btile_off(col, 1), make_uint4(w.x, w.y, n0 | (n1 << 16), n2));
-      cm_acc = fmaxf(cm_acc, fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))));
-      nm_acc = fmaxf(nm_acc, n);
+      cm = fmaxf(cm, fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))));
+      nm = fmaxf(nm, __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(c0, c0), __fmul_rn(c1, c1)), __fmul_rn(c2, c2)), __fmul_rn(c3, c3)));
     }
-    if (u % kUpc == kUpc - 1) {   // the chunk's last unit: its bounds go to the chunk's slot
 #pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        cm_acc = fmaxf(cm_acc, __shfl_xor_sync(0xffffffffu, cm_acc, off));
-        nm_acc = fmaxf(nm_acc, __shfl_xor_sync(0xffffffffu, nm_acc, off));
-      }
-      if (lane == 0) {
-        float* bd = sbnd + (((u / kUpc) & 1) * 4 + (warp - 4)) * 2;
-        bd[0] = cm_acc;
-        bd[1] = nm_acc;
-      }
-      cm_acc = 0.f;
-      nm_acc = 0.f;
+    for (int off = 16; off; off >>= 1) {
+      cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, off));
+      nm = fmaxf(nm, __shfl_xor_sync(0xffffffffu, nm, off));
     }
-  };
-  uint4 wa = make_uint4(0u, 0u, 0u, 0u), wb = wa;
-  if (stager) { wa = fetch(0); wb = fetch(1); }
+    if (lane == 0) { cbnd[2 * ci] = cm; cbnd[2 * ci + 1] = nm; }
+  }
   griddep_wait();
   float x1n = 0.f;
-  if (!stager) {   // the row's x (nsub = 16: two token-heads per warp) -> A row
+  if (warp >= 4 && warp < 8) {   // first-half reducers: the row's x -> A row (row rt = 32 (warp - 4) + lane = TMEM lane)
+    const int rw = warp - 4;
     float x[4] = {0.f, 0.f, 0.f, 0.f};
-    const int64_t wr0 = row0 + 32 * warp;
+    const int64_t wr0 = row0 + 32 * rw;
     for (int part = 0; part < 32 / nsub; ++part) {
       if (wr0 + part * nsub >= rows) break;
       const int64_t th = (wr0 + part * nsub) / nsub;
@@ -735,92 +714,121 @@ __global__ void __launch_bounds__(256) nn16_filter_tc_kernel(EncArgs a, int64_t 
         x[0] = xx[0]; x[1] = xx[1]; x[2] = xx[2]; x[3] = xx[3];
       }
     }
-    uint32_t hi[4], mi[4], lo[4];   // K 0..3 hi, 4..7 mid, 8..11 lo parts of -2x, 12..14 = 1, 15 = 0
+    uint32_t hi[4], mi[4], lo[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) split3_bf16(-2.f * x[i], hi[i], mi[i], lo[i]);
+    const int rt = 32 * rw + lane;
     sts_u128(sA + tc_tile_off(rt, 0), make_uint4(hi[0] | (hi[1] << 16), hi[2] | (hi[3] << 16),
                                                 mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16)));
     sts_u128(sA + tc_tile_off(rt, 1), make_uint4(lo[0] | (lo[1] << 16), lo[2] | (lo[3] << 16), 0x3F803F80u, 0x00003F80u));
     x1n = fabsf(x[0]) + fabsf(x[1]) + fabsf(x[2]) + fabsf(x[3]);
-  } else {
-    stage(0, wa);
-    if (nunits > 1) stage(1, wb);
-    wa = fetch(2);
-    wb = fetch(3);
+    tc::fence_proxy_async_smem();
   }
-  tc::fence_proxy_async_smem();
   tc::fence_before();
-  __syncthreads();
+  __syncthreads();   // A tile, chunk bounds, barriers and the TMEM address are ready
   tc::fence_after();
   const uint32_t tbase = *tmem_slot;
-  constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kTcN >> 3) << 17) |
-                              (static_cast<uint32_t>(kTcRows >> 4) << 24);   // f32 D, bf16 A / B, K-major
-  const uint64_t adesc = tc::smem_desc_kmajor(sA, 2048, 128);
-  if (tid == 0) {
-    for (int u = 0; u < 2 && u < nunits; ++u) {
-      tc_mma_ss(tbase + u * kTcN, adesc, tc::smem_desc_kmajor(sB + u * kBT, kBT / 2, 128), kIdesc);
-      tc::commit(smem_u32(mbar + u));
+  if (warp == 0) {   // MMA issuer: the whole warp waits, lane 0 issues
+    constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kWsN >> 3) << 17) |
+                                (static_cast<uint32_t>(kTcRows >> 4) << 24);
+    const uint64_t adesc = tc::smem_desc_kmajor(sA, 2048, 128);
+    for (int u = 0; u < nunits; ++u) {
+      const int st = u % kWsStages, d = u & 1;
+      tc::mbar_wait(smem_u32(bfull + st), (u / kWsStages) & 1);
+      tc::mbar_wait(smem_u32(dempty + d), ((u >> 1) & 1) ^ 1);
+      tc::fence_after();
+      if (lane == 0) {
+        tc_mma_ss(tbase + d * kWsN, adesc, tc::smem_desc_kmajor(sB + st * kWsBT, kWsBT / 2, 128), kIdesc);
+        tc::commit(smem_u32(bempty + st));
+        tc::commit(smem_u32(dfull + d));
+      }
+      __syncwarp();
     }
-  }
-  const uint32_t tcol = (static_cast<uint32_t>(32 * (warp & 3)) << 16) + (kTcN / 2) * (warp >> 2);
-  float mn = INFINITY;
-  for (int u = 0; u < nunits; ++u) {
-    const int buf = u & 1;
-    tc::mbar_wait(smem_u32(mbar + buf), (u >> 1) & 1);
-    tc::fence_after();
+  } else if (warp < 4) {   // stagers: centroid i = t, t + 96, t + 192 of each unit
+    const int t = tid - 32;
+    constexpr int kPer = (kWsN + 95) / 96;
+    uint2 cw[kPer];
+    auto fetch = [&](int u) {
 #pragma unroll
-    for (int hq = 0; hq < kTcN / 128; ++hq) {   // this warp's half of the unit's columns, 64 at a time
-      uint32_t v[64];
-      tc_ld_32x32b_x64(tbase + tcol + buf * kTcN + 64 * hq, v);
-      tc::wait_ld();
+      for (int q = 0; q < kPer; ++q) {
+        const int i = t + 96 * q;
+        cw[q] = (i < kWsN && u < nunits) ? *reinterpret_cast<const uint2*>(crange + (static_cast<int64_t>(u) * kWsN + i) * 4)
+                                         : make_uint2(0u, 0u);
+      }
+    };
+    fetch(0);
+    for (int u = 0; u < nunits; ++u) {
+      const int st = u % kWsStages;
+      tc::mbar_wait(smem_u32(bempty + st), ((u / kWsStages) & 1) ^ 1);
+      const uint32_t b = sB + st * kWsBT;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int i = t + 96 * q;
+        if (i >= kWsN) continue;
+        const uint2 w = cw[q];
+        const float c0 = __uint_as_float(w.x << 16), c1 = __uint_as_float(w.x & 0xFFFF0000u);
+        const float c2 = __uint_as_float(w.y << 16), c3 = __uint_as_float(w.y & 0xFFFF0000u);
+        const float n = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(c0, c0), __fmul_rn(c1, c1)), __fmul_rn(c2, c2)), __fmul_rn(c3, c3));
+        uint32_t n0, n1, n2;
+        split3_bf16(n, n0, n1, n2);
+        sts_u128(b + ws_btile_off(i, 0), make_uint4(w.x, w.y, w.x, w.y));
+        sts_u128(b + ws_btile_off(i, 1), make_uint4(w.x, w.y, n0 | (n1 << 16), n2));
+      }
+      fetch(u + 1);
+      tc::fence_proxy_async_smem();
+      mbar_arrive(smem_u32(bfull + st));
+    }
+  } else {   // reducers: warp w reads rows 32 ((w - 4) % 4) + lane (its TMEM lane quadrant), columns half (w - 4) / 4
+    const int rw = (warp - 4) & 3, half = (warp - 4) >> 2, rt = 32 * rw + lane;
+    const uint32_t tl = (static_cast<uint32_t>(32 * rw) << 16) + half * (kWsN / 2);
+    // the first-half warp holds the row's ||x||_1 (x1n); the pair meets on named barrier 1 + rw
+    float mn = INFINITY;
+    for (int u = 0; u < nunits; ++u) {
+      const int d = u & 1;
+      tc::mbar_wait(smem_u32(dfull + d), (u >> 1) & 1);
+      tc::fence_after();
       float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
 #pragma unroll
-      for (int i = 0; i < 64; i += 8) {
-        m4[0] = fminf(m4[0], fminf(__uint_as_float(v[i]), __uint_as_float(v[i + 1])));
-        m4[1] = fminf(m4[1], fminf(__uint_as_float(v[i + 2]), __uint_as_float(v[i + 3])));
-        m4[2] = fminf(m4[2], fminf(__uint_as_float(v[i + 4]), __uint_as_float(v[i + 5])));
-        m4[3] = fminf(m4[3], fminf(__uint_as_float(v[i + 6]), __uint_as_float(v[i + 7])));
+      for (int hq = 0; hq < kWsN / 128; ++hq) {
+        uint32_t v[64];
+        tc_ld_32x32b_x64(tbase + tl + d * kWsN + 64 * hq, v);
+        tc::wait_ld();
+#pragma unroll
+        for (int i = 0; i < 64; i += 8) {
+          m4[0] = fminf(m4[0], fminf(__uint_as_float(v[i]), __uint_as_float(v[i + 1])));
+          m4[1] = fminf(m4[1], fminf(__uint_as_float(v[i + 2]), __uint_as_float(v[i + 3])));
+          m4[2] = fminf(m4[2], fminf(__uint_as_float(v[i + 4]), __uint_as_float(v[i + 5])));
+          m4[3] = fminf(m4[3], fminf(__uint_as_float(v[i + 6]), __uint_as_float(v[i + 7])));
+        }
       }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(dempty + d));   // D[d] free for unit u + 2
       mn = fminf(mn, fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3])));
-    }
-    const bool chunk_end = u % kUpc == kUpc - 1;
-    if (stager) {
-      if (chunk_end) { smin[rt] = mn; mn = INFINITY; }
-      if (u + 2 < nunits) {   // unit u + 2 into the buffers unit u used (its MMA is complete)
-        stage(u + 2, wa);
-        wa = wb;
-        wb = fetch(u + 4);
-      }
-      tc::fence_proxy_async_smem();
-    }
-    tc::fence_before();
-    __syncthreads();   // D[buf] read by every warp, B[buf] restaged, half-row minima posted
-    tc::fence_after();
-    if (tid == 0 && u + 2 < nunits) {
-      tc_mma_ss(tbase + buf * kTcN, adesc, tc::smem_desc_kmajor(sB + buf * kBT, kBT / 2, 128), kIdesc);
-      tc::commit(smem_u32(mbar + buf));
-    }
-    if (!stager && chunk_end) {   // chunk done: (lo, hi) of this row
-      const int ci = u / kUpc;
-      const float* bd = sbnd + (ci & 1) * 8;
-      const float cm = fmaxf(fmaxf(bd[0], bd[2]), fmaxf(bd[4], bd[6]));
-      const float nm = fmaxf(fmaxf(bd[1], bd[3]), fmaxf(bd[5], bd[7]));
-      const float v = fminf(mn, smin[rt]);
-      mn = INFINITY;
-      const int64_t r = row0 + rt;
-      if (r < rows) {
-        const float E = 0x1p-17f * (2.1f * x1n * cm + 1.01f * nm);
-        const int m = static_cast<int>(r % nsub);
-        const int64_t th = r / nsub;
-        const int64_t btl = shared ? th / a.H : th;
-        const int h = shared ? static_cast<int>(th % a.H) : hb;
-        reinterpret_cast<float2*>(a.ws)[nn16_ws_row(a, btl, h, s, m) + chunk0 + ci] = make_float2(v - E, v + E);
+      if ((u & 1) == 1) {   // chunk u / 2 done: the second-half warp hands its minima to the first
+        const int ci = u >> 1;
+        if (half) smin[rt] = mn;
+        tc::bar_sync(1 + rw, 64);
+        if (!half) {
+          const float v = fminf(mn, smin[rt]);
+          const int64_t r = row0 + rt;
+          if (r < rows) {
+            const float E = 0x1p-17f * (2.1f * x1n * cbnd[2 * ci] + 1.01f * cbnd[2 * ci + 1]);
+            const int m = static_cast<int>(r % nsub);
+            const int64_t th = r / nsub;
+            const int64_t btl = shared ? th / a.H : th;
+            const int h = shared ? static_cast<int>(th % a.H) : hb;
+            reinterpret_cast<float2*>(a.ws)[nn16_ws_row(a, btl, h, s, m) + chunk0 + ci] = make_float2(v - E, v + E);
+          }
+        }
+        tc::bar_sync(1 + rw, 64);   // smin[rt] is read before the next chunk overwrites it
+        mn = INFINITY;
       }
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::dealloc(tbase, 2 * kTcN);
+  if (warp == 0) tc::dealloc(tbase, 512);
 }
 
 // grid (pass token rows, H, 2 streams x 4 row groups), 8 warps: warp w of row group z selects and
@@ -1154,6 +1162,7 @@ static bool nn16_hmma_from_env() {
   return v == 1;
 }
 
+
 static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int32_t B, int32_t T,
                                      int32_t H_kv, const int64_t k_strides[3], const int64_t v_strides[3],
                                      const float* inv_lambda, const void* ck_bf16, const void* cv_bf16,
@@ -1222,7 +1231,7 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
     const int ds = kfilt ? kcfg.sub_dim : vcfg.sub_dim;   // (the filtered streams of a pair share d)
     static bool attr_done = false;   // benign race: idempotent attributes
     if (!attr_done) {
-      cudaFuncSetAttribute(nn16_filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+      cudaFuncSetAttribute(nn16_filter_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmem);
       cudaFuncSetAttribute(nn16_filter_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, nn_filter_smem<4>());
       cudaFuncSetAttribute(nn16_filter_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, nn_filter_smem<8>());
       cudaFuncSetAttribute(nn_select8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSel8Smem);
@@ -1244,12 +1253,12 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
       // rows of the largest book (shared books hold every head's rows)
       const int64_t rows = static_cast<int64_t>(nb) * H_kv * (kcfg.head_dim / ds);
       cudaError_t e;
-      if (!hmma) {   // tcgen05 filter (VECINFER_NN16_TC=1): 128-row CTAs, <= 2 per SM (256 TMEM columns each)
+      if (!hmma) {   // warp-specialised tcgen05 filter (VECINFER_NN16_TC=1): one CTA per SM
         const int64_t rblk = (rows + kTcRows - 1) / kTcRows;
-        int ncpb = 8;
-        while (ncpb > 1 && (kNC16 / ncpb) * rblk * nbk < (kTcN == 128 ? 2 : 1) * device_sm_count()) ncpb >>= 1;
+        int ncpb = 16;
+        while (ncpb > 1 && (kNC16 / ncpb) * rblk * nbk < device_sm_count()) ncpb >>= 1;
         const dim3 g1(kNC16 / ncpb, static_cast<unsigned>(rblk), static_cast<unsigned>(nbk));
-        e = launch_pdl(nn16_filter_tc_kernel, g1, dim3(2 * kTcRows), kTcSmem, st, a, b0, nb, ncpb);
+        e = launch_pdl(nn16_filter_ws_kernel, g1, dim3(kWsThreads), kWsSmem, st, a, b0, nb, ncpb);
       } else {       // mma.sync filter (default)
         const int64_t rblk = (rows + kRows16 - 1) / kRows16;
         // chunks per CTA: amortise the rows' transform over up to 8 chunks while keeping >= ~4 CTAs per SM
