@@ -1027,13 +1027,16 @@ __global__ void __launch_bounds__(256) nn_select8_kernel(EncArgs a, int64_t bt0)
 // nearest centroid with the lowest index on ties.  The codes are then packed into the row's
 // little-endian bit string (code m in bits [m b, m b + b), reading R11).
 constexpr int kGenThreads = 256;
+constexpr int kGenGroups = 4;   // sub-vector groups per (token-head, stream): 16 / 32 / 64 sub-vectors -> 4 / 8 / 16 per CTA
 
 __global__ void __launch_bounds__(kGenThreads) encode_generic_kernel(EncArgs a) {
   __shared__ __align__(16) float xs[128];
   __shared__ unsigned long long best[64];
   __shared__ uint4 sbook[512];
   griddep_launch_dependents();
-  const int which = blockIdx.z, h = blockIdx.y;
+  // grid z = stream x kGenGroups row groups: group g encodes sub-vectors [g M / G, (g + 1) M / G), a
+  // whole number of bytes of the row's bit string for every format served here (8 x 10 bits = 10 B)
+  const int which = blockIdx.z / kGenGroups, grp = blockIdx.z % kGenGroups, h = blockIdx.y;
   if (!((a.gen_mask >> which) & 1)) return;   // this stream goes through the tensor-core filter
   const int64_t bt = blockIdx.x;
   const int b = static_cast<int>(bt / a.T), t = static_cast<int>(bt % a.T);
@@ -1059,7 +1062,8 @@ __global__ void __launch_bounds__(kGenThreads) encode_generic_kernel(EncArgs a) 
   const uint16_t* book = staged ? reinterpret_cast<const uint16_t*>(sbook) : cb;
   // warp w owns sub-vectors m = w, w + 8, ...: its lanes scan centroids j = lane, lane + 32, ... and a
   // shuffle tree keeps the (dist_bits << 32 | j) minimum -- no cross-warp reduction per sub-vector
-  for (int m = warp; m < M; m += kGenThreads / 32) {
+  const int mg0 = grp * M / kGenGroups, mg1 = (grp + 1) * M / kGenGroups;
+  for (int m = mg0 + warp; m < mg1; m += kGenThreads / 32) {
     const float* xm = xs + m * sub;
     unsigned long long key = ~0ull;
     for (int j = lane; j < n_ent; j += 32) {
@@ -1083,7 +1087,7 @@ __global__ void __launch_bounds__(kGenThreads) encode_generic_kernel(EncArgs a) 
   __syncthreads();
   const int rb = M * bits / 8;
   uint8_t* dst = (which ? a.vcodes : a.kcodes) + row * rb;
-  for (int i = tid; i < rb; i += kGenThreads) {   // byte i = row bits [8i, 8i + 8): <= 2 codes (b >= 8)
+  for (int i = mg0 * bits / 8 + tid; i < mg1 * bits / 8; i += kGenThreads) {   // byte i = row bits [8i, 8i + 8): <= 2 codes (b >= 8)
     const int p = 8 * i, c0 = p / bits, off = p - c0 * bits;
     uint32_t w = static_cast<uint32_t>(best[c0] & 0xFFFFFFFFull);
     if (c0 + 1 < M) w |= static_cast<uint32_t>(best[c0 + 1] & 0xFFFFFFFFull) << bits;
@@ -1240,7 +1244,7 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
     if (next2 && !(kfilt && vfilt)) {   // the other stream: the generic scan, one CTA per (token-head)
       a.gen_mask = kfilt ? 2 : 1;
       if (nbt > 2147483647) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many tokens");
-      const cudaError_t e = launch_pdl(encode_generic_kernel, dim3(static_cast<unsigned>(nbt), H_kv, 2),
+      const cudaError_t e = launch_pdl(encode_generic_kernel, dim3(static_cast<unsigned>(nbt), H_kv, 2 * kGenGroups),
                                        dim3(kGenThreads), 0, st, a);
       if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_generic_kernel: %s", cudaGetErrorString(e)); }
     }
@@ -1277,7 +1281,7 @@ static vecinfer_status_t encode_impl(const void* k_bf16, const void* v_bf16, int
   }
   if (next2) {   // one generic launch encodes both streams
     if (nbt > 2147483647) return fail(VECINFER_ERR_SHAPE, "encode_kv: too many tokens");
-    const cudaError_t e = launch_pdl(encode_generic_kernel, dim3(static_cast<unsigned>(nbt), H_kv, 2),
+    const cudaError_t e = launch_pdl(encode_generic_kernel, dim3(static_cast<unsigned>(nbt), H_kv, 2 * kGenGroups),
                                      dim3(kGenThreads), 0, st, a);
     if (e != cudaSuccess) { cudaGetLastError(); return fail(VECINFER_ERR_CUDA, "encode_generic_kernel: %s", cudaGetErrorString(e)); }
     return check_launch("encode_generic_kernel");
