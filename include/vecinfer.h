@@ -323,9 +323,13 @@ vecinfer_status_t vecinfer_attn_decode_paged(const void* q_bf16, int32_t B, int3
  *   k_codes, v_codes  the code caches (written at row write_pos[b], read over [0, seq_lens[b])).
  *   Other arguments as in vecinfer_attn_decode (token range = whole sequence) and
  *   vecinfer_encode_kv (err_flags); workspace >= vecinfer_decode_step_workspace_bytes(...), zero-
- *   filled once.  Grids of more than one wave, 16-bit codebooks and the LUT variant run the
- *   append as its own launch first (same results).  The codebooks must be b2d4 for the fused launch; with
- *   algo = VECINFER_ATTN_LUT the call is executed as the two separate launches.
+ *   filled once.  The append runs inside the attention launch for the d = 4 books of 16 / 256
+ *   entries (b1d4, b2d4, any K/V mix of them) and for d8b8 / d4b10 when the grid is one wave (the
+ *   stream partition always budgets it).  Otherwise it runs first as its own encode (same codes):
+ *   grids of several waves, the LUT variant, d2b8 (measured faster separate), and the large books
+ *   -- 65 536-entry d = 4 and 4096 / 65 536-entry d = 8 -- through the tensor-core filter + exact
+ *   selection of vecinfer_encode_kv (two launches).  vecinfer_decode_step_launches reports the
+ *   count.
  * Errors: as vecinfer_encode_kv and vecinfer_attn_decode.
  * ------------------------------------------------------------------------------------- */
 /* kernel launches one vecinfer_decode_step call makes (1: the append is fused into attention) */
