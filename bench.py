@@ -520,11 +520,12 @@ def run_ours(args, rank, world, local_rank):
     cs_in = torch.cuda.Stream(device=dev) if pipelined else None
     cs_out = torch.cuda.Stream(device=dev) if pipelined else None
 
-    # 4 layer chunks, one packed copy each per direction (a copy node costs ~2 us: 6 uneven chunks
-    # with small first / last ones measured slower at cfg2, 1172 vs 1186 GB/s e2e)
-    # large batches (>= 256 KiB of inputs per layer, e.g. cfg3) use 8 chunks: the first chunk's copy is
-    # not overlapped, so its size matters more than the extra copy nodes
-    n_chunks = (8 if h_in[0].numel() * h_in.element_size() >= 256 * 1024 else 4) if L % 8 == 0 else 1
+    # layer chunks, one packed copy each per direction.  Every chunk boundary is a cross-stream
+    # dependency in the graph (the layer waits for its copy, the copy for its layer), which costs more
+    # than the overlap gains when the copies are small: cfg2 (12 KiB of inputs per layer) is fastest
+    # with 2 chunks (scripts/exp_e2e.py: 0.4375 ms/step vs 0.440 with 1, 0.443-0.463 with 4, 0.457
+    # with 8); large batches (>= 256 KiB per layer, e.g. cfg3) overlap more with 8 chunks
+    n_chunks = (8 if h_in[0].numel() * h_in.element_size() >= 256 * 1024 else 2) if L % 8 == 0 else 1
     chunks = [(c * L // n_chunks, (c + 1) * L // n_chunks) for c in range(n_chunks)]
 
     def step_e2e_pipelined_body():
@@ -696,7 +697,7 @@ def run_ours(args, rank, world, local_rank):
                      "lsu_bound": lsu, "gather_bound": gather},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_ms / K, "api": ("32 x vecinfer.decode_step + pinned H2D / D2H copies in 4 layer chunks (8 at >= 256 KiB of inputs per layer; one packed copy per chunk and direction) pipelined on two copy streams, one CUDA graph per step, host waits on the result (event poll); " if g_e2e is not None else "32 eager vecinfer calls, ")
+                "ms_per_step": e2e_ms / K, "api": ("32 x vecinfer.decode_step + pinned H2D / D2H copies in 2 layer chunks (8 at >= 256 KiB of inputs per layer; one packed copy per chunk and direction) pipelined on two copy streams, one CUDA graph per step, host waits on the result (event poll); " if g_e2e is not None else "32 eager vecinfer calls, ")
                        + "pinned H2D of q/k/v and D2H of o every step"},
         "gpu_launches": launches_per_step * K,
         "ranks": ranks if world > 1 else None,
