@@ -522,30 +522,40 @@ def run_ours(args, rank, world, local_rank):
 
     # layer chunks, one packed copy each per direction.  Every chunk boundary is a cross-stream
     # dependency in the graph (the layer waits for its copy, the copy for its layer), which costs more
-    # than the overlap gains when the copies are small: cfg2 (12 KiB of inputs per layer) is fastest
-    # with 2 chunks (scripts/exp_e2e.py: 0.4375 ms/step vs 0.440 with 1, 0.443-0.463 with 4, 0.457
-    # with 8); large batches (>= 256 KiB per layer, e.g. cfg3) overlap more with 8 chunks
-    n_chunks = (8 if h_in[0].numel() * h_in.element_size() >= 256 * 1024 else 2) if L % 8 == 0 else 1
-    chunks = [(c * L // n_chunks, (c + 1) * L // n_chunks) for c in range(n_chunks)]
+    # than the overlap gains when the copies are small: at cfg2 (12 KiB of inputs per layer) two
+    # copies per direction, split so that only layer 0's inputs and layer 31's output are exposed, are
+    # fastest (scripts/exp_e2e.py: 0.4353 ms/step vs 0.4375 for two halves, 0.440 with 1 chunk,
+    # 0.443-0.463 with 4); large batches (>= 256 KiB per layer, e.g. cfg3) overlap more with 8 chunks
+    if h_in[0].numel() * h_in.element_size() >= 256 * 1024 and L % 8 == 0:
+        chunks_in = [(c * L // 8, (c + 1) * L // 8) for c in range(8)]
+        chunks_out = chunks_in
+    elif L > 1:   # small inputs: layer 0's own copy, then the rest; the last layer's output on its own
+        chunks_in, chunks_out = [(0, 1), (1, L)], [(0, L - 1), (L - 1, L)]
+    else:
+        chunks_in = chunks_out = [(0, L)]
 
     def step_e2e_pipelined_body():
-        ev_in = [torch.cuda.Event() for _ in chunks]
-        ev_out = [torch.cuda.Event() for _ in chunks]
+        ev_in = [torch.cuda.Event() for _ in chunks_in]
         cur = torch.cuda.current_stream(dev)
         cs_in.wait_stream(cur)
         cs_out.wait_stream(cur)
         with torch.cuda.stream(cs_in):
-            for c, (a, b) in enumerate(chunks):
+            for c, (a, b) in enumerate(chunks_in):
                 d_in[a:b].copy_(h_in[a:b], non_blocking=True)
                 ev_in[c].record(cs_in)
-        for c, (a, b) in enumerate(chunks):
-            cur.wait_event(ev_in[c])
-            for l in range(a, b):
-                layer_e2e(l)
-            ev_out[c].record(cur)
-            with torch.cuda.stream(cs_out):
-                cs_out.wait_event(ev_out[c])
-                o_h[a:b].copy_(o_all[a:b], non_blocking=True)
+        first_of = {a: c for c, (a, b) in enumerate(chunks_in)}
+        last_of = {b - 1: (a, b) for (a, b) in chunks_out}
+        for l in range(L):
+            if l in first_of:
+                cur.wait_event(ev_in[first_of[l]])
+            layer_e2e(l)
+            if l in last_of:
+                a, b = last_of[l]
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                with torch.cuda.stream(cs_out):
+                    cs_out.wait_event(ev)
+                    o_h[a:b].copy_(o_all[a:b], non_blocking=True)
         cur.wait_stream(cs_in)
         cur.wait_stream(cs_out)
 
@@ -697,7 +707,7 @@ def run_ours(args, rank, world, local_rank):
                      "lsu_bound": lsu, "gather_bound": gather},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_ms / K, "api": ("32 x vecinfer.decode_step + pinned H2D / D2H copies in 2 layer chunks (8 at >= 256 KiB of inputs per layer; one packed copy per chunk and direction) pipelined on two copy streams, one CUDA graph per step, host waits on the result (event poll); " if g_e2e is not None else "32 eager vecinfer calls, ")
+                "ms_per_step": e2e_ms / K, "api": ("32 x vecinfer.decode_step + pinned H2D / D2H copies in 2 chunks per direction (layer 0 | layers 1-31 in, layers 0-30 | layer 31 out; 8 chunks at >= 256 KiB of inputs per layer; packed copies) pipelined on two copy streams, one CUDA graph per step, host waits on the result (event poll); " if g_e2e is not None else "32 eager vecinfer calls, ")
                        + "pinned H2D of q/k/v and D2H of o every step"},
         "gpu_launches": launches_per_step * K,
         "ranks": ranks if world > 1 else None,

@@ -57,24 +57,32 @@ def main():
             for l in range(L):
                 layer(l)
             return
-        C = args.chunks
-        ch = [(c * L // C, (c + 1) * L // C) for c in range(C)]
-        ev_in = [torch.cuda.Event() for _ in ch]
-        ev_out = [torch.cuda.Event() for _ in ch]
+        if args.chunks > 0:
+            C = args.chunks
+            hin = [(c * L // C, (c + 1) * L // C) for c in range(C)]
+            hout = hin
+        else:   # -1: inputs [0,1) + [1,L), outputs [0,L-1) + [L-1,L)
+            hin, hout = [(0, 1), (1, L)], [(0, L - 1), (L - 1, L)]
+        ev_in = [torch.cuda.Event() for _ in hin]
         cs_in.wait_stream(cur)
         cs_out.wait_stream(cur)
         with torch.cuda.stream(cs_in):
-            for c, (a, b) in enumerate(ch):
+            for c, (a, b) in enumerate(hin):
                 d_in[a:b].copy_(h_in[a:b], non_blocking=True)
                 ev_in[c].record(cs_in)
-        for c, (a, b) in enumerate(ch):
-            cur.wait_event(ev_in[c])
-            for l in range(a, b):
-                layer(l)
-            ev_out[c].record(cur)
-            with torch.cuda.stream(cs_out):
-                cs_out.wait_event(ev_out[c])
-                o_h[a:b].copy_(o[a:b], non_blocking=True)
+        start_of = {a: c for c, (a, b) in enumerate(hin)}
+        end_of = {b - 1: (a, b) for (a, b) in hout}
+        for l in range(L):
+            if l in start_of:
+                cur.wait_event(ev_in[start_of[l]])
+            layer(l)
+            if l in end_of:
+                a, b = end_of[l]
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                with torch.cuda.stream(cs_out):
+                    cs_out.wait_event(ev)
+                    o_h[a:b].copy_(o[a:b], non_blocking=True)
         cur.wait_stream(cs_in)
         cur.wait_stream(cs_out)
 
