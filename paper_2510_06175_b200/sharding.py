@@ -229,6 +229,7 @@ class SeqShardedStep:
     exchanged and LSE-merged BEFORE the next layer runs -- the next layer's query depends on this
     layer's output in a real model, so the exchange is paid once per layer, not once per step.
 
+    exchange="xr": the merge fused INTO the attention launch (XRankWindows; graph-safe, no exchange launch).
     exchange="p2p": the fused peer-memory kernel (P2PExchange, one launch per layer; graph-safe).
     exchange="allgather": one packed all-gather per layer + vecinfer_merge_lse (NCCL on device
     tensors; gloo through host copies for the single-GPU functional tests).
@@ -238,8 +239,8 @@ class SeqShardedStep:
     def __init__(self, layers: int, B: int, H_q: int, D: int, n_tokens: int, device: torch.device,
                  H_kv: int = 8, exchange: str = "p2p", o_dtype: torch.dtype = torch.float32, group=None):
         from . import vecinfer as vi
-        if exchange not in ("p2p", "allgather"):
-            raise ValueError("exchange must be 'p2p' or 'allgather'")
+        if exchange not in ("xr", "p2p", "allgather"):
+            raise ValueError("exchange must be 'xr', 'p2p' or 'allgather'")
         self.vi = vi
         self.group = group
         self.world = dist.get_world_size(group)
@@ -254,6 +255,7 @@ class SeqShardedStep:
         self.workspace = [vi.attn_workspace(B, H_q, H_kv, max(n_local, 1), device=device) for _ in range(layers)]
         self.exchange = exchange
         self.p2p = P2PExchange(B * H_q, D, device, group=group) if exchange == "p2p" else None
+        self.xr = XRankWindows(B * H_q, D, device, group=group) if exchange == "xr" else None
         self.device = device
 
     def exchange_layer(self, l: int):
@@ -270,16 +272,26 @@ class SeqShardedStep:
 
     def run(self, attend):
         """attend(l, o_part_l, lse_part_l) launches layer l's shard attention (e.g. vi.attn_decode with
-        tok_begin/tok_end and out=/lse=); the exchange of layer l follows it immediately."""
+        tok_begin/tok_end and out=/lse=); the exchange of layer l follows it immediately.
+        exchange="xr": attend(l, o_l, lse_l, xr=windows) must pass xr= to vi.attn_decode / decode_step,
+        which then writes the MERGED layer output itself (one launch per layer, no exchange)."""
         for l in range(self.L):
+            if self.xr is not None:
+                attend(l, self.o[l], self.lse[l], xr=self.xr)
+                continue
             attend(l, self.o_part[l], self.lse_part[l])
             self.exchange_layer(l)
 
     def error(self) -> int:
         """Non-zero if a peer partial timed out in the fused exchange (VECINFER_FLAG_P2P_TIMEOUT)."""
+        if self.xr is not None:
+            return int(self.xr.err.item())
         return int(self.p2p.err.item()) if self.p2p is not None else 0
 
     def close(self):
         if self.p2p is not None:
             self.p2p.close()
             self.p2p = None
+        if self.xr is not None:
+            self.xr.close()
+            self.xr = None

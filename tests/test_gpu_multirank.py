@@ -217,11 +217,11 @@ def _rank_layers(rank, world, port, outq, exchange):
         step = SeqShardedStep(L, 1, 32, 128, N, dev, exchange=exchange)
         b, e = step.tok_begin, step.tok_end
 
-        def attend(l, o_part, lse_part):
+        def attend(l, o_part, lse_part, xr=None):
             vi.attn_decode(qs[l], lam, ck, cv, kcs[l], vcs[l], seq, tok_begin=b, tok_end=e, out=o_part, lse=lse_part,
-                           workspace=step.workspace[l])
+                           workspace=step.workspace[l], xr=xr)
         outs = []
-        if exchange == "p2p":   # the layers and their exchanges captured in ONE graph, replayed twice
+        if exchange in ("p2p", "xr"):   # the layers and their exchanges captured in ONE graph, replayed twice
             s = torch.cuda.Stream(device=dev)
             s.wait_stream(torch.cuda.current_stream(dev))
             with torch.cuda.stream(s):
@@ -231,7 +231,7 @@ def _rank_layers(rank, world, port, outq, exchange):
             with torch.cuda.graph(g, stream=s):
                 step.run(attend)
         for _ in range(2):
-            if exchange == "p2p":
+            if exchange in ("p2p", "xr"):
                 g.replay()
             else:
                 step.run(attend)
@@ -246,7 +246,7 @@ def _rank_layers(rank, world, port, outq, exchange):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange,world", [("p2p", 2), ("p2p", 3), ("allgather", 2)])
+@pytest.mark.parametrize("exchange,world", [("xr", 2), ("p2p", 2), ("p2p", 3), ("allgather", 2)])
 def test_per_layer_sharded_exchange_vs_oracle(exchange, world):
     """The sharded step as bench.py runs it at N > 1 (configs[3] pattern): every layer attends its
     token shard and exchanges + merges its partial BEFORE the next layer starts (fused P2P kernel
