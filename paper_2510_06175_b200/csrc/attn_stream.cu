@@ -415,57 +415,66 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
 
       if (ua == u_first) phase_mark(a.phase, vc, 11);
       // ---- fused decode append: the owner piece of a unit encodes its new token (Eq. 9: S then H
-      // on the key, VQ on both), 8 warps per stream, each scanning 1/8 of the centroids (bf16
-      // codebook -> fp32, pinned distance, lowest index on ties)
-      bool synced = false;
+      // on the key, VQ on both; bf16 codebook -> fp32, pinned distance, lowest index on ties).  The
+      // round's owner segments (G = 1 or 2) are encoded in ONE phase: the 16 warps form 2G groups
+      // (segment, K or V) of 8 / G warps, each warp scanning n_ent * G / 8 centroids in batches of 32
+      // staged by itself, then one barrier and a per-group reduction in warp order.
       if constexpr (kCanAppend) {
         if (a.append) {
-#pragma unroll 1
-          for (int sgi = 0; sgi < nseg; ++sgi) {
-            if (!segs[sgi].owner) continue;
-            if (synced) __syncthreads();   // the previous encode's staging is consumed
+          int own0 = -1, own1 = -1;
+          for (int sgi = 0; sgi < nseg; ++sgi)
+            if (segs[sgi].owner) { if (own0 < 0) own0 = sgi; else own1 = sgi; }
+          const int G = own0 < 0 ? 0 : (own1 < 0 ? 1 : 2);
+          if (G > 0) {
+            const int wps = 8 / G;                      // warps per (segment, stream)
+            const int grp = warp / wps, wi = warp - grp * wps;
+            const int sgi = (grp >> 1) ? own1 : own0;
+            const bool isv = grp & 1;
             const SegSh& sg = segs[sgi];
             const int bb = sg.b, hh = sg.hc;
-            const bool isv = warp >= 8;
-            const int w8 = warp & 7;
-            const int P8 = (isv ? (1 << VB) : (1 << KB)) / 8;   // centroids per warp
+            const int n_ent = isv ? (1 << VB) : (1 << KB);
+            const int P = n_ent / wps;                  // centroids of this warp
             float4* stage = reinterpret_cast<float4*>(smem_raw + kMiscStage);
             float* sbest = reinterpret_cast<float*>(smem_raw + kMiscBest);
             uint32_t* sidx = reinterpret_cast<uint32_t*>(smem_raw + kMiscIdx);
             const uint16_t* cb = isv ? (sgi ? cbvB : cbvA) : (sgi ? cbkB : cbkA);
-            if (lane < P8) stage[warp * 32 + lane] = bf16x4_to_float4(*reinterpret_cast<const uint2*>(cb + 4 * (P8 * w8 + lane)));
             float x[4];
             if (!isv) {
               const bool bad = key_transform_lane(a.knew + bb * a.kn_sb + hh * a.kn_sh + 4 * lane,
                                                   a.inv_lambda + hh * 128 + 4 * lane, a.inv_sqrt_d, lane, x);
-              if (bad && warp == 0 && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
+              if (bad && wi == 0 && lane == 0 && a.err) atomicOr(a.err, VECINFER_FLAG_RANGE);
             } else {
               const float4 v = bf16x4_to_float4(*reinterpret_cast<const uint2*>(a.vnew + bb * a.vn_sb + hh * a.vn_sh + 4 * lane));
               x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
             }
-            __syncwarp();
             float best = __int_as_float(0x7f800000);
             uint32_t bi = 0;
+#pragma unroll 1
+            for (int c0 = 0; c0 < P; c0 += 32) {        // batches of 32 centroids staged by this warp
+              const int nb = P - c0 < 32 ? P - c0 : 32;
+              const int j0 = P * wi + c0;
+              if (lane < nb) stage[warp * 32 + lane] = bf16x4_to_float4(*reinterpret_cast<const uint2*>(cb + 4 * (j0 + lane)));
+              __syncwarp();
 #pragma unroll 8
-            for (int i = 0; i < P8; ++i) {
-              const float4 c = stage[warp * 32 + i];
-              const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
-              if (dd < best) { best = dd; bi = P8 * w8 + i; }
+              for (int i = 0; i < nb; ++i) {
+                const float4 c = stage[warp * 32 + i];
+                const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
+                if (dd < best) { best = dd; bi = j0 + i; }
+              }
+              __syncwarp();   // the batch is read before the next one overwrites it
             }
             sbest[warp * 32 + lane] = best;
             sidx[warp * 32 + lane] = bi;
             __syncthreads();
-            synced = true;
-            if (warp == 0 || warp == 8) {
+            if (wi == 0) {   // reduce the group's warps in warp (= centroid index) order
               float bbst = sbest[warp * 32 + lane];
               uint32_t ii = sidx[warp * 32 + lane];
-#pragma unroll
-              for (int w = 1; w < 8; ++w) {
+              for (int w = 1; w < wps; ++w) {
                 const float c = sbest[(warp + w) * 32 + lane];
                 if (c < bbst) { bbst = c; ii = sidx[(warp + w) * 32 + lane]; }
               }
               unsigned char* nc = newcodes + 128 * sgi;
-              if (warp == 0) put_code<KB>(nc, lane, ii);
+              if (!isv) put_code<KB>(nc, lane, ii);
               else put_code<VB>(nc + 64, lane, ii);
               const int64_t p = sg.p_row;
               int pgw = 0;
@@ -473,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
                 const int64_t row = paged ? ((static_cast<int64_t>(pgw) * a.Hc + sg.hc) << a.page_shift) +
                                                 (p & ((int64_t(1) << a.page_shift) - 1))
                                           : static_cast<int64_t>(sg.cu) * a.n_cap + p;
-                if (warp == 0) put_code<KB>(a.kcodes_w + row * KR, lane, ii);
+                if (!isv) put_code<KB>(a.kcodes_w + row * KR, lane, ii);
                 else put_code<VB>(a.vcodes_w + row * VR, lane, ii);
               } else if (lane == 0 && a.err) {
                 atomicOr(a.err, VECINFER_FLAG_WRITE_POS);
