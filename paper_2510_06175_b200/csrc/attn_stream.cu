@@ -438,6 +438,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
             float* sbest = reinterpret_cast<float*>(smem_raw + kMiscBest);
             uint32_t* sidx = reinterpret_cast<uint32_t*>(smem_raw + kMiscIdx);
             const uint16_t* cb = isv ? (sgi ? cbvB : cbvA) : (sgi ? cbkB : cbkA);
+            // the first batch's centroids go out before the key transform (its loads + shuffles hide
+            // the L2 round trip)
+            uint2 cw = lane < (P < 32 ? P : 32) ? *reinterpret_cast<const uint2*>(cb + 4 * (P * wi + lane)) : make_uint2(0u, 0u);
             float x[4];
             if (!isv) {
               const bool bad = key_transform_lane(a.knew + bb * a.kn_sb + hh * a.kn_sh + 4 * lane,
@@ -453,7 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
             for (int c0 = 0; c0 < P; c0 += 32) {        // batches of 32 centroids staged by this warp
               const int nb = P - c0 < 32 ? P - c0 : 32;
               const int j0 = P * wi + c0;
-              if (lane < nb) stage[warp * 32 + lane] = bf16x4_to_float4(*reinterpret_cast<const uint2*>(cb + 4 * (j0 + lane)));
+              if (c0 > 0 && lane < nb) cw = *reinterpret_cast<const uint2*>(cb + 4 * (j0 + lane));
+              if (lane < nb) stage[warp * 32 + lane] = bf16x4_to_float4(cw);
               __syncwarp();
 #pragma unroll 8
               for (int i = 0; i < nb; ++i) {
