@@ -439,8 +439,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
             uint32_t* sidx = reinterpret_cast<uint32_t*>(smem_raw + kMiscIdx);
             const uint16_t* cb = isv ? (sgi ? cbvB : cbvA) : (sgi ? cbkB : cbkA);
             // the first batch's centroids go out before the key transform (its loads + shuffles hide
-            // the L2 round trip)
-            uint2 cw = lane < (P < 32 ? P : 32) ? *reinterpret_cast<const uint2*>(cb + 4 * (P * wi + lane)) : make_uint2(0u, 0u);
+            // the L2 round trip).  Batches of 32 centroids are staged as 16 pairs in the
+            // pinned_dist4_x2 layout (two centroids per paired FADD2 / FMUL2, per-element RN)
+            // (P <= 64: at most two batches, both loaded here)
+            uint2 cwa[2], cwb[2];
+#pragma unroll
+            for (int bt = 0; bt < 2; ++bt) {
+              const int nbb = P - 32 * bt < 32 ? P - 32 * bt : 32;
+              cwa[bt] = cwb[bt] = make_uint2(0u, 0u);
+              if (lane < nbb / 2) {
+                cwa[bt] = *reinterpret_cast<const uint2*>(cb + 4 * (P * wi + 32 * bt + 2 * lane));
+                cwb[bt] = *reinterpret_cast<const uint2*>(cb + 4 * (P * wi + 32 * bt + 2 * lane + 1));
+              }
+            }
             float x[4];
             if (!isv) {
               const bool bad = key_transform_lane(a.knew + bb * a.kn_sb + hh * a.kn_sh + 4 * lane,
@@ -450,26 +461,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
               const float4 v = bf16x4_to_float4(*reinterpret_cast<const uint2*>(a.vnew + bb * a.vn_sb + hh * a.vn_sh + 4 * lane));
               x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
             }
+            if (ua == u_first) phase_mark(a.phase, vc, 13);   // (thread 0: its K transform done)
             float best = __int_as_float(0x7f800000);
             uint32_t bi = 0;
-#pragma unroll 1
-            for (int c0 = 0; c0 < P; c0 += 32) {        // batches of 32 centroids staged by this warp
-              const int nb = P - c0 < 32 ? P - c0 : 32;
+            uint4* sp = reinterpret_cast<uint4*>(stage) + warp * 32;   // 16 pairs x 32 B
+#pragma unroll
+            for (int bt = 0; bt < 2; ++bt) {             // batches of 32 centroids staged by this warp
+              const int c0 = 32 * bt;
+              if (c0 >= P) break;
+              const int nb = P - c0 < 32 ? P - c0 : 32;  // (even: books of 16 / 256 entries)
               const int j0 = P * wi + c0;
-              if (c0 > 0 && lane < nb) cw = *reinterpret_cast<const uint2*>(cb + 4 * (j0 + lane));
-              if (lane < nb) stage[warp * 32 + lane] = bf16x4_to_float4(cw);
+              if (lane < nb / 2) {   // the pair layout of stage_centroid_pair
+                const uint2 ca = cwa[bt], cbb = cwb[bt];
+                sp[2 * lane] = make_uint4(ca.x << 16, cbb.x << 16, ca.x & 0xFFFF0000u, cbb.x & 0xFFFF0000u);
+                sp[2 * lane + 1] = make_uint4(ca.y << 16, cbb.y << 16, ca.y & 0xFFFF0000u, cbb.y & 0xFFFF0000u);
+              }
               __syncwarp();
-#pragma unroll 8
-              for (int i = 0; i < nb; ++i) {
-                const float4 c = stage[warp * 32 + i];
-                const float dd = pinned_dist4(x[0], x[1], x[2], x[3], c.x, c.y, c.z, c.w);
-                if (dd < best) { best = dd; bi = j0 + i; }
+#pragma unroll 4
+              for (int pi = 0; pi < nb / 2; ++pi) {
+                const float2 d = pinned_dist4_x2(x[0], x[1], x[2], x[3], sp[2 * pi], sp[2 * pi + 1]);
+                if (d.x < best) { best = d.x; bi = j0 + 2 * pi; }       // lower index first: ties keep it
+                if (d.y < best) { best = d.y; bi = j0 + 2 * pi + 1; }
               }
               __syncwarp();   // the batch is read before the next one overwrites it
             }
             sbest[warp * 32 + lane] = best;
             sidx[warp * 32 + lane] = bi;
+            if (ua == u_first) phase_mark(a.phase, vc, 14);   // (thread 0: its scan done)
             __syncthreads();
+            if (ua == u_first) phase_mark(a.phase, vc, 10);   // (every warp's scan done)
             if (wi == 0) {   // reduce the group's warps in warp (= centroid index) order
               float bbst = sbest[warp * 32 + lane];
               uint32_t ii = sidx[warp * 32 + lane];

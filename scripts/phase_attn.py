@@ -34,6 +34,7 @@ def main():
     for c in args.case:
         B, N, splits = map(int, c.split(",")[:3])
         algo = c.split(",")[3] if len(c.split(",")) > 3 else "auto"
+        fused = len(c.split(",")) > 4 and c.split(",")[4] == "fused"   # decode_step with the fused append
         S = vi.attn_num_splits(B, 8, N, splits)
         nct = vi.attn_num_ctas(B, 8, N, splits) if algo != "stream" else 148
         buf = torch.zeros(nct * 32, dtype=torch.int64, device=dev)
@@ -46,7 +47,14 @@ def main():
         ws = vi.attn_workspace(B, 32, 8, N, splits, device=dev)
         for _ in range(5):
             buf.zero_()
-            vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, workspace=ws, algo=algo)
+            if fused:
+                inv = torch.from_numpy(z["inv_lambda"]).to(dev)
+                kn = torch.from_numpy(synth.gen_keys(1, 8, 128, seed=4, batch=B)[:, 0]).to(dev).to(torch.bfloat16)
+                vn = torch.from_numpy(synth.gen_values(1, 8, 128, seed=5, batch=B)[:, 0]).to(dev).to(torch.bfloat16)
+                vi.decode_step(q, kn, vn, lam, inv, ck, cv, kc, vc, seq - 1, seq, num_splits=splits,
+                               workspace=vi.decode_step_workspace(B, 32, 8, N, device=dev), algo=algo)
+            else:
+                vi.attn_decode(q, lam, ck, cv, kc, vc, seq, num_splits=splits, workspace=ws, algo=algo)
             torch.cuda.synchronize()
         both = buf.view(nct, 32).cpu().numpy().astype(np.float64)
         t, cyc = both[:, :16], both[:, 16:]
@@ -71,6 +79,10 @@ def main():
             st(rel[:, 12] - rel[:, 6], "prologue: piece setup (loads)")
             st(rel[:, 11] - rel[:, 12], "prologue: q~ transform")
             st(rel[:, 1] - rel[:, 11], "prologue: encode + sync")
+            st(rel[:, 13] - rel[:, 11], "  encode: transform (thread 0)")
+            st(rel[:, 14] - rel[:, 13], "  encode: scan (thread 0)")
+            st(rel[:, 10] - rel[:, 14], "  encode: barrier (slowest warp)")
+            st(rel[:, 1] - rel[:, 10], "  encode: reduce + store + sync")
             st(rel[:, 2] - rel[:, 1], "main loop warp 0 (last round)")
             st(rel[:, 7] - rel[:, 2], "wait for slowest warp")
             st(rel[:, 9] - rel[:, 7], "combine + store")
