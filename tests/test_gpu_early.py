@@ -168,3 +168,41 @@ def test_early_layer_chain_in_graph(N):
         o_ref, L_ref = ref.attention_vq(q_last[0, 4 * h:4 * h + 4], CB["lambda"][h], CB["ck_b2d4"][h],
                                         CB["cv_b2d4"][h], kk, vv)
         _assert_close(o[L - 1][0, 4 * h:4 * h + 4], lse[L - 1][0, 4 * h:4 * h + 4], o_ref, L_ref)
+
+
+def test_early_persistent_grid_residual_and_d64():
+    """Pre-wait reads on the paths with extra state: a persistent multi-item split grid (forced 40
+    splits x 16 units > #SMs: only the first item reads before the wait), a residual window (read
+    after the wait), and head_dim 64."""
+    lens = [3000, 2500]
+    c = _attn_case(2, 8, 4, 3000, lens, seed=970)
+    o0, L0 = _attn(c, False, num_splits=40)
+    o1, L1 = _attn(c, True, num_splits=40)
+    assert np.array_equal(o0, o1) and np.array_equal(L0, L1)
+    _assert_close(o1, L1, *_run_ref(c))
+    # residual window rows next to the codes
+    B, R = 2, 24
+    kr = t_bf16(synth.gen_keys(R, 8, 128, seed=971, batch=B).transpose(0, 2, 1, 3))
+    vr = t_bf16(synth.gen_values(R, 8, 128, seed=972, batch=B).transpose(0, 2, 1, 3))
+    rl = t_i32([R, 5])
+    outs = []
+    for early in (False, True):
+        o, L = vi.attn_decode(t_bf16(c["q"]), t_f32(c["lam"]), t_bf16(c["ck"]), t_bf16(c["cv"]), t_u8(c["kc"]),
+                              t_u8(c["vc"]), t_i32(c["seq_lens"]), k_res=kr, v_res=vr, res_lens=rl, num_splits=3,
+                              early_cache=early)
+        outs.append((o.cpu().numpy(), L.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    # head_dim 64 (split kernel and the D = 64 stream partition)
+    c64 = vi.VQConfig(64, 4, 8)
+    kc64 = synth.gen_codes_torch((20, 8, 1500, 16), 8, seed=973, device="cuda")
+    vc64 = synth.gen_codes_torch((20, 8, 1500, 16), 8, seed=974, device="cuda")
+    q64 = t_bf16(synth.gen_queries(20, 32, 8, 64, seed=975))
+    lam64 = t_f32(CB["lambda"][:, :64])
+    seq = t_i32([1500 - 7 * i for i in range(20)])
+    for algo in ("mma", "stream"):
+        res = []
+        for early in (False, True):
+            o, L = vi.attn_decode(q64, lam64, t_bf16(c["ck"]), t_bf16(c["cv"]), kc64, vc64, seq, kcfg=c64, vcfg=c64,
+                                  algo=algo, early_cache=early)
+            res.append((o.cpu().numpy(), L.cpu().numpy()))
+        assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1]), algo
