@@ -242,3 +242,45 @@ def test_nn_filter_paged_pool(fmt):
     assert np.array_equal(kc, exp_k) and np.array_equal(vc, exp_v)
     spare = np.setdiff1d(np.arange(n_pages), bt.ravel())
     assert not kpool[torch.from_numpy(spare).cuda().long()].any()
+
+
+def test_nn16_filter_matches_the_full_scan_at_scale():
+    """Cross-check at a size the oracle cannot brute-force in seconds (4096 token-heads x 2 streams x
+    32 sub-vectors against 65 536 centroids, keys with outlier channels, values next to centroids):
+    the tensor-core filter path and the full pinned scan (VECINFER_NN16_SCAN=1, the round-1 kernel)
+    give identical codes.  (Parity against the oracle itself is pinned by the cases above.)"""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    script = f"""
+import sys
+sys.path.insert(0, {here!r})
+import numpy as np, torch, synth
+from helpers import load_codebooks
+from paper_2510_06175_b200 import vecinfer as vi
+CB = load_codebooks()
+T, H = 512, 8
+k = synth.gen_keys(T, H, 128, seed=1800)
+cv = CB['cv_b4d4']
+rng = np.random.default_rng(1801)
+v = cv[rng.integers(0, 65536, size=(T * H * 32,))].reshape(1, T, H, 128)
+v = synth.round_to_bf16((v + 1e-3 * rng.standard_normal(v.shape)).astype(np.float32))
+t = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda().to(torch.bfloat16)
+kc = torch.zeros(1, H, T, 64, dtype=torch.uint8, device='cuda')
+vc = torch.zeros_like(kc)
+vi.encode_kv(t(k), t(v), torch.from_numpy(CB['inv_lambda']).cuda(), t(CB['ck_b4d4']), t(cv), kc, vc,
+             torch.zeros(1, dtype=torch.int32, device='cuda'), vi.B4D4, vi.B4D4)
+torch.cuda.synchronize()
+np.save(sys.argv[1], np.concatenate([kc.cpu().numpy().ravel(), vc.cpu().numpy().ravel()]))
+"""
+    outs = []
+    for scan in ("0", "1"):
+        path = os.path.join("/tmp", f"nn16_xcheck_{scan}_{os.getpid()}.npy")
+        env = dict(os.environ, VECINFER_NN16_SCAN=scan)
+        r = subprocess.run([sys.executable, "-c", script, path], env=env, cwd=os.path.dirname(here),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs.append(np.load(path))
+        os.remove(path)
+    assert np.array_equal(outs[0], outs[1])
