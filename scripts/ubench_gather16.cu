@@ -21,6 +21,15 @@ __device__ __forceinline__ uint2 ld_nc_na(const void* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
   return v;
 }
+// centroid ci of a book whose entries [0, kSlice) also sit in shared memory (slice, 8 B each):
+// a predicated LDS for those, a predicated LDG for the rest (no branch)
+__device__ __forceinline__ uint2 ld_split(const void* g, uint32_t s, uint32_t ci, uint32_t n_slice) {
+  uint2 v;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %2, %3;\n\t@p ld.shared.v2.u32 {%0,%1}, [%4];\n\t"
+               "@!p ld.global.nc.v2.u32 {%0,%1}, [%5];\n\t}"
+               : "=r"(v.x), "=r"(v.y) : "r"(ci), "r"(n_slice), "r"(s), "l"(g));
+  return v;
+}
 __device__ __forceinline__ uint4 ld_codes(const void* p) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
@@ -29,13 +38,24 @@ __device__ __forceinline__ uint4 ld_codes(const void* p) {
 
 // one warp-step = 32 token-heads x (K or V) half-rows: lane l reads 16 B of codes (8 codes) and
 // gathers 8 centroids; two steps (K, V) per 32 token-half-rows.  Per token-head: 32 K + 32 V codes.
-template <bool kHbmCodes, bool kNoAlloc, bool kTwoTables>
+// kSlice > 0: entries [0, kSlice) of each book are staged in shared memory first (K slice, then V)
+template <bool kHbmCodes, bool kNoAlloc, bool kTwoTables, int kSlice = 0>
 __global__ void __launch_bounds__(512, 1) gather_kernel(const uint8_t* kcodes, const uint8_t* vcodes,
                                                         const uint16_t* ck, const uint16_t* cv,
                                                         long long rows_per_cta, unsigned* sink) {
+  extern __shared__ __align__(16) uint8_t slice_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint16_t* cvv = kTwoTables ? cv : ck;
   uint32_t acc = 0;
+  const uint32_t sk = static_cast<uint32_t>(__cvta_generic_to_shared(slice_smem));
+  const uint32_t sv = sk + kSlice * 8;
+  if (kSlice > 0) {
+    for (int i = threadIdx.x; i < kSlice / 2; i += 512) {
+      reinterpret_cast<uint4*>(slice_smem)[i] = reinterpret_cast<const uint4*>(ck)[i];
+      reinterpret_cast<uint4*>(slice_smem + kSlice * 8)[i] = reinterpret_cast<const uint4*>(cvv)[i];
+    }
+    __syncthreads();
+  }
   // each CTA streams its own contiguous code rows (64 B per row = one token-head's K or V codes)
   const long long row0 = blockIdx.x * rows_per_cta;
   uint32_t h = blockIdx.x * 7919u + threadIdx.x * 104729u;
@@ -56,24 +76,33 @@ __global__ void __launch_bounds__(512, 1) gather_kernel(const uint8_t* kcodes, c
     for (int i = 0; i < 8; ++i) {
       const uint32_t ci = (kw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
       const uint32_t di = (vw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-      const uint2 a = kNoAlloc ? ld_nc_na(ck + 4 * ci) : ld_nc(ck + 4 * ci);
-      const uint2 b = kNoAlloc ? ld_nc_na(cvv + 4 * di) : ld_nc(cvv + 4 * di);
+      uint2 a, b;
+      if (kSlice > 0) {
+        a = ld_split(ck + 4 * ci, sk + 8 * ci, ci, kSlice);
+        b = ld_split(cvv + 4 * di, sv + 8 * di, di, kSlice);
+      } else {
+        a = kNoAlloc ? ld_nc_na(ck + 4 * ci) : ld_nc(ck + 4 * ci);
+        b = kNoAlloc ? ld_nc_na(cvv + 4 * di) : ld_nc(cvv + 4 * di);
+      }
       acc += a.x ^ a.y ^ b.x ^ b.y;
     }
   }
   if (acc == 0x9e3779b9u) atomicAdd(sink, acc);
 }
 
-template <bool H, bool N, bool T>
+template <bool H, bool N, bool T, int SL = 0>
 void run(const char* name, const uint8_t* kc, const uint8_t* vc, const uint16_t* ck, const uint16_t* cv,
          long long rows_per_cta, int sms, unsigned* sink, int clk_mhz) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  gather_kernel<H, N, T><<<sms, 512>>>(kc, vc, ck, cv, rows_per_cta, sink);
+  const int smem = SL * 16;
+  cudaFuncSetAttribute(gather_kernel<H, N, T, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gather_kernel<H, N, T, SL>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxL1);
+  gather_kernel<H, N, T, SL><<<sms, 512, smem>>>(kc, vc, ck, cv, rows_per_cta, sink);
   cudaEventRecord(e0);
   const int reps = 5;
-  for (int i = 0; i < reps; ++i) gather_kernel<H, N, T><<<sms, 512>>>(kc, vc, ck, cv, rows_per_cta, sink);
+  for (int i = 0; i < reps; ++i) gather_kernel<H, N, T, SL><<<sms, 512, smem>>>(kc, vc, ck, cv, rows_per_cta, sink);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -115,6 +144,10 @@ int main() {
   run<true, true, true>("HBM codes, L1::no_allocate, K+V books", kc, vc, ck, cv, rows_per_cta, sms, sink, clk_mhz);
   run<false, false, true>("hashed codes, L1-allocating, K+V books", kc, vc, ck, cv, rows_per_cta, sms, sink, clk_mhz);
   run<true, false, false>("HBM codes, L1-allocating, one book (K=V)", kc, vc, ck, cv, rows_per_cta, sms, sink, clk_mhz);
+  run<true, false, true, 4096>("HBM codes, K+V books, 2x 32 KiB in smem", kc, vc, ck, cv, rows_per_cta, sms, sink, clk_mhz);
+  run<true, false, true, 8192>("HBM codes, K+V books, 2x 64 KiB in smem", kc, vc, ck, cv, rows_per_cta, sms, sink, clk_mhz);
+  run<true, false, true, 11776>("HBM codes, K+V books, 2x 92 KiB in smem", kc, vc, ck, cv, rows_per_cta, sms, sink, clk_mhz);
+  run<true, false, true, 14336>("HBM codes, K+V books, 2x 112 KiB in smem", kc, vc, ck, cv, rows_per_cta, sms, sink, clk_mhz);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
   return 0;
