@@ -333,29 +333,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
       int pgn0 = 0, pgn1 = 0;   // pages of the two sub-tiles of the next tile to load
       auto page_of = [&](int bb, int64_t tok) -> int { return a.bt[bb * a.bt_stride + (tok >> a.page_shift)]; };
       // this lane's K / V bytes of row 0 of page 0 of the piece's KV head (set by setup_piece):
-      // row (pg, t) of the head = pkb + (pg * Hc * page_size + t % page_size) * KR
+      // row (pg, t) of the head = pkb + pg * (Hc * page_size * KR) + (t % page_size) * KR
       const uint8_t* pkb = nullptr;
       const uint8_t* pvb = nullptr;
-      auto load_paged = [&](int64_t tstart, int p0, int p1, int rem) {
-        const int64_t pmask = (int64_t(1) << a.page_shift) - 1;
-        const int64_t sk = static_cast<int64_t>(a.Hc) << a.page_shift;   // rows between page indices
-        const int64_t o0 = p0 * sk + (tstart & pmask);
-        if ((tstart & pmask) + 16 <= pmask) {   // both sub-tiles in page p0: one contiguous tile
-          if (rem >= 32) load_tile_full<KB, VB>(nxt, pkb + o0 * KR, pvb + o0 * VR);
-          else load_tile_tail<KB, VB>(nxt, pkb + o0 * KR, pvb + o0 * VR, rem, r, j);
-          return;
+      // both sub-tiles translated unconditionally (sub-tile 1 of a tile inside one page has p1 = p0):
+      // per sub-tile one 32 x 32 -> 64-bit multiply-add for the page plus the in-page row, no branch
+      // (tokens, page ids and the bytes between pages of one head fit 32 bits)
+      auto load_paged = [&](int tstart, int p0, int p1, int rem) {
+        const uint32_t pmask = (1u << a.page_shift) - 1u;
+        const uint32_t rows_pg = static_cast<uint32_t>(a.Hc) << a.page_shift;   // rows between page indices
+        const uint32_t i0 = static_cast<uint32_t>(tstart) & pmask, i1 = static_cast<uint32_t>(tstart + 16) & pmask;
+        const uint8_t* k0 = pkb + static_cast<uint64_t>(static_cast<uint32_t>(p0)) * (rows_pg * KR) + i0 * KR;
+        const uint8_t* v0 = pvb + static_cast<uint64_t>(static_cast<uint32_t>(p0)) * (rows_pg * VR) + i0 * VR;
+        const uint8_t* k1 = pkb + static_cast<uint64_t>(static_cast<uint32_t>(p1)) * (rows_pg * KR) + i1 * KR;
+        const uint8_t* v1 = pvb + static_cast<uint64_t>(static_cast<uint32_t>(p1)) * (rows_pg * VR) + i1 * VR;
+        if (rem >= 32) {   // one (warp-uniform) branch per tile: full tiles load unpredicated
+          load_subtile<KB, VB, 0>(nxt, k0, v0, 16, r, j);
+          load_subtile<KB, VB, 1>(nxt, k1, v1, 16, r, j);
+        } else {
+          load_subtile<KB, VB, 0>(nxt, k0, v0, rem, r, j);
+          load_subtile<KB, VB, 1>(nxt, k1, v1, rem - 16, r, j);
         }
-        const int64_t o1 = p1 * sk + ((tstart + 16) & pmask);   // sub-tile 1 starts page p1
-        load_subtile<KB, VB, 0>(nxt, pkb + o0 * KR, pvb + o0 * VR, rem, r, j);
-        load_subtile<KB, VB, 1>(nxt, pkb + o1 * KR, pvb + o1 * VR, rem - 16, r, j);
       };
-      // block-table entries of a tile starting at token t: its page, and the next page if its second
-      // sub-tile starts one (rem = tokens from t).  (Reusing the previous tile's entries and reading
+      // block-table entries of a tile starting at token t (rem = tokens from t): the pages of its two
+      // sub-tiles, both read (predicated, no branch).  (Reusing the previous tile's entries and reading
       // the table only at page starts was measured slower: the reads become conditional and chained.)
-      auto tile_pages = [&](int bb, int64_t t, int rem, int& p0, int& p1) {
-        const int64_t pmask = (int64_t(1) << a.page_shift) - 1;
-        p0 = rem > 0 ? page_of(bb, t) : 0;
-        p1 = (rem > 16 && (t & pmask) + 16 > pmask) ? page_of(bb, t + 16) : p0;
+      const int32_t* btp = nullptr;   // block-table row of the piece's sequence (setup_piece)
+      auto tile_pages = [&](int t, int rem, int& p0, int& p1) {
+        p0 = rem > 0 ? __ldg(btp + (t >> a.page_shift)) : 0;
+        p1 = rem > 16 ? __ldg(btp + ((t + 16) >> a.page_shift)) : p0;
       };
       // sets up piece `seg` of this warp and issues its first tile loads
       auto setup_piece = [&]() {
@@ -383,10 +389,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
         if constexpr (paged) {
           pkb = a.kcodes + ((static_cast<int64_t>(sg.hc) << a.page_shift) + r) * KR + Fmt<KB>::kOffK * j;
           pvb = a.vcodes + ((static_cast<int64_t>(sg.hc) << a.page_shift) + 2 * j) * VR + Fmt<VB>::kOffV * r;
+          btp = a.bt + sg.b * a.bt_stride;
+          const int t0 = static_cast<int>(tok0);
           int p0, p1;
-          tile_pages(sg.b, tok0, ntok, p0, p1);
-          if (ntile > 0) load_paged(tok0, p0, p1, ntok);
-          tile_pages(sg.b, tok0 + 32, ntok - 32, pgn0, pgn1);
+          tile_pages(t0, ntok, p0, p1);
+          if (ntile > 0) load_paged(t0, p0, p1, ntok);
+          tile_pages(t0 + 32, ntok - 32, pgn0, pgn1);
         } else if (ntile > 0) {
           load_tile_tail<KB, VB, DH>(nxt, kp, vp, ntok, r, j);   // (predicated: one code path)
         }
@@ -653,9 +661,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           if (it + 1 < ntile) {
             const int rem = rem_cur - 32;
             if constexpr (paged) {
-              const int64_t tn = tok0 + 32 * static_cast<int64_t>(it + 1);
+              const int tn = static_cast<int>(tok0) + 32 * (it + 1);
               load_paged(tn, pgn0, pgn1, rem);
-              tile_pages(segs[seg].b, tn + 32, rem - 32, pgn0, pgn1);
+              tile_pages(tn + 32, rem - 32, pgn0, pgn1);
             } else {
               kp += 32 * KR;
               vp += 32 * VR;
