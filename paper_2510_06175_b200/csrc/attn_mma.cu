@@ -711,12 +711,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       }
       const int rem_cur = ntok - 32 * it;
       if (!tma_on && it + kNW < ntile) {
-        if (paged) {
-          const int64_t tok = r0 + 32 * static_cast<int64_t>(it + kNW);
-          const int64_t rw = row_in(pg_ahead, tok);
-          kp = kcb + rw * KR;
-          vp = vcb + rw * VR;
-          if (it + 2 * kNW < ntile) pg_ahead = page_of(tok + 32 * kNW);
+        if (paged) {   // row (pg * Hc + hc) * page_size + tok % page_size: 32 x 32 -> 64-bit multiply-adds
+          const int tok = static_cast<int>(r0) + 32 * (it + kNW);
+          const uint32_t prow = static_cast<uint32_t>(pg_ahead) * static_cast<uint32_t>(a.Hc) + static_cast<uint32_t>(hc);
+          const uint32_t tin = static_cast<uint32_t>(tok) & ((1u << a.page_shift) - 1u);
+          kp = kcb + static_cast<uint64_t>(prow) * (static_cast<uint32_t>(KR) << a.page_shift) + tin * KR;
+          vp = vcb + static_cast<uint64_t>(prow) * (static_cast<uint32_t>(VR) << a.page_shift) + tin * VR;
+          if (it + 2 * kNW < ntile) pg_ahead = __ldg(a.bt + b * a.bt_stride + ((tok + 32 * kNW) >> a.page_shift));
         } else {
           kp += kStepK;
           vp += kStepV;
