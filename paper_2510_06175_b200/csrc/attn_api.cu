@@ -3,6 +3,7 @@
 
 #include "attn_common.cuh"
 
+
 using namespace vecinfer;
 
 namespace vecinfer {
@@ -479,10 +480,9 @@ static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t k
   if (algo == VECINFER_ATTN_LUT || B <= 0 || H_kv <= 0) return false;
   // NEXT-2 formats: the split kernel fuses the append for books of <= 1024 entries (d8b8, d2b8,
   // d4b10); d8b12 / d8b16 keep the separate encode launch
-  // (d2b8 is excluded since the late round-2 generic encode: its separate append launch + attention
-  // measured faster than the owner split's 64-sub-vector scan, e.g. 28.0 vs 32.8 us at N = 32k)
   auto small_next2 = [](const vecinfer_vq_t& c) {
-    return vq_next2(c) && ((c.sub_dim == 8 && c.code_bits == 8) || (c.sub_dim == 4 && c.code_bits == 10));
+    return vq_next2(c) && ((c.sub_dim == 8 && c.code_bits == 8) || (c.sub_dim == 4 && c.code_bits == 10) ||
+                           (c.sub_dim == 2 && c.code_bits == 8));
   };
   const bool n2 = vq_next2(kcfg) || vq_next2(vcfg);
   if (n2 && !(small_next2(kcfg) && small_next2(vcfg))) return false;

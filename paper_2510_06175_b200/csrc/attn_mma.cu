@@ -349,10 +349,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   }
   if constexpr (kGenAppend) if (owner) {
     // Eq. 9 for the d8b8 / d2b8 / d4b10 formats: warp 0 writes the pinned key transform, warp 8 the
-    // raw value to shared memory; then for every sub-vector m all 256 threads of a stream scan
-    // centroids j = t, t + 256, ... with the pinned distance (fp32 RN, no FMA, left to right over
-    // the d dims: reading R9), the minima reduce as (dist_bits << 32 | j) -- lowest index on ties --
-    // and the codes are packed into the row's little-endian bit string (R11)
+    // raw value to shared memory; then the 8 warps of a stream scan its sub-vectors against every
+    // centroid with the pinned distance (fp32 RN, no FMA, left to right over the d dims: reading
+    // R9), the minima reduce as (dist_bits << 32 | j) -- lowest index on ties -- and the codes are
+    // packed into the row's little-endian bit string (R11)
     float* xs = reinterpret_cast<float*>(smem_raw + kMiscW);                              // [2][128]
     unsigned long long* gbest = reinterpret_cast<unsigned long long*>(smem_raw + kMiscW + 1024);   // [2][64]
     if (warp == 0) {
@@ -365,7 +365,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       *reinterpret_cast<float4*>(xs + 128 + 4 * lane) =
           bf16x4_to_float4(*reinterpret_cast<const uint2*>(a.vnew + b * a.vn_sb + hc * a.vn_sh + 4 * lane));
     }
-    if (tid < 128) gbest[tid] = ~0ull;
     __syncthreads();
     const int which = warp >> 3, t = tid & 255;
     const int sub = which ? fmt_sub(VB) : fmt_sub(KB), bits = which ? fmt_bits(VB) : fmt_bits(KB);
@@ -373,51 +372,65 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     const float* xw = xs + 128 * which;
     // centroids come from the stream's shared table (filled above, exact fp16 copies of the bf16
     // book): d4b10 = separate table (64-B rows of 8 replicas), d8b8 / d2b8 = the stream's half of
-    // the classic 256-B rows (8 x 16 B / 32 x 4 B replicas); thread t reads replica t % reps
+    // the classic 256-B rows (8 x 16 B / 32 x 4 B replicas).  Warp w (of the stream's 8) scans
+    // sub-vectors m = w, w + 8, ... (M / 8 of them) against entries jj = lane, lane + 32, ...: each
+    // centroid load serves all of the warp's sub-vectors, the running minima stay in registers
+    // (independent chains), and one cross-lane reduction per sub-vector ends the scan.  Replica
+    // choice: the 32 lanes' loads of one step hit distinct banks.
     auto scan = [&](auto FF, uint32_t base) {
       constexpr int F = decltype(FF)::value;
-      constexpr int kSub = fmt_sub(F), kEnt = 1 << fmt_bits(F);
-      for (int m = 0; m < M; ++m) {
-        float xm[kSub];
+      constexpr int kSub = fmt_sub(F), kEnt = 1 << fmt_bits(F), kMW = 128 / kSub / 8;
+      const int w8 = warp & 7;
+      float xm[kMW][kSub];
 #pragma unroll
-        for (int u = 0; u < kSub; ++u) xm[u] = xw[m * kSub + u];
-        unsigned long long key = ~0ull;
-        for (int jj = t; jj < kEnt; jj += 256) {
-          float c[kSub];
-          if constexpr (F == kFmtD4B10) {
-            const uint2 w = lds_u64(base + jj * 64 + (t & 7) * 8);
-            const float2 c01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
-            const float2 c23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
-            c[0] = c01.x; c[1] = c01.y; c[2] = c23.x; c[3] = c23.y;
-          } else if constexpr (F == kFmtD8B8) {
-            const uint4 w = lds_u128(base + jj * 256 + (t & 7) * 16);
-            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+      for (int mi = 0; mi < kMW; ++mi)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float2 cc = __half22float2(*reinterpret_cast<const __half2*>(&ww[u]));
-              c[2 * u] = cc.x; c[2 * u + 1] = cc.y;
-            }
-          } else {   // d2b8
-            const uint32_t w = lds_u32(base + jj * 256 + (t & 31) * 4);
-            const float2 cc = __half22float2(*reinterpret_cast<const __half2*>(&w));
-            c[0] = cc.x; c[1] = cc.y;
+        for (int u = 0; u < kSub; ++u) xm[mi][u] = xw[(w8 + 8 * mi) * kSub + u];
+      unsigned long long key[kMW];
+#pragma unroll
+      for (int mi = 0; mi < kMW; ++mi) key[mi] = ~0ull;
+#pragma unroll 4
+      for (int jj = lane; jj < kEnt; jj += 32) {
+        float c[kSub];
+        if constexpr (F == kFmtD4B10) {
+          const uint2 w = lds_u64(base + jj * 64 + ((lane >> 1) & 7) * 8);
+          const float2 c01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+          const float2 c23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+          c[0] = c01.x; c[1] = c01.y; c[2] = c23.x; c[3] = c23.y;
+        } else if constexpr (F == kFmtD8B8) {
+          const uint4 w = lds_u128(base + jj * 256 + (lane & 7) * 16);
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float2 cc = __half22float2(*reinterpret_cast<const __half2*>(&ww[u]));
+            c[2 * u] = cc.x; c[2 * u + 1] = cc.y;
           }
-          float ee = __fsub_rn(xm[0], c[0]);
+        } else {   // d2b8
+          const uint32_t w = lds_u32(base + jj * 256 + lane * 4);
+          const float2 cc = __half22float2(*reinterpret_cast<const __half2*>(&w));
+          c[0] = cc.x; c[1] = cc.y;
+        }
+#pragma unroll
+        for (int mi = 0; mi < kMW; ++mi) {
+          float ee = __fsub_rn(xm[mi][0], c[0]);
           float dsum = __fmul_rn(ee, ee);
 #pragma unroll
           for (int u = 1; u < kSub; ++u) {
-            ee = __fsub_rn(xm[u], c[u]);
+            ee = __fsub_rn(xm[mi][u], c[u]);
             dsum = __fadd_rn(dsum, __fmul_rn(ee, ee));
           }
           const unsigned long long k2 = (static_cast<unsigned long long>(__float_as_uint(dsum)) << 32) | static_cast<uint32_t>(jj);
-          key = k2 < key ? k2 : key;
+          key[mi] = k2 < key[mi] ? k2 : key[mi];
         }
+      }
+#pragma unroll
+      for (int mi = 0; mi < kMW; ++mi) {
 #pragma unroll
         for (int off = 16; off; off >>= 1) {
-          const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, key, off);
-          key = o2 < key ? o2 : key;
+          const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, key[mi], off);
+          key[mi] = o2 < key[mi] ? o2 : key[mi];
         }
-        if (lane == 0) atomicMin(&gbest[64 * which + m], key);
+        if (lane == 0) gbest[64 * which + w8 + 8 * mi] = key[mi];
       }
     };
     if (which == 0) scan(std::integral_constant<int, KB>{}, Fmt<KB>::kSep ? tab_s + kSepOff : tab_s);
@@ -711,13 +724,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       }
       const int rem_cur = ntok - 32 * it;
       if (!tma_on && it + kNW < ntile) {
-        if (paged) {   // row (pg * Hc + hc) * page_size + tok % page_size: 32 x 32 -> 64-bit multiply-adds
-          const int tok = static_cast<int>(r0) + 32 * (it + kNW);
-          const uint32_t prow = static_cast<uint32_t>(pg_ahead) * static_cast<uint32_t>(a.Hc) + static_cast<uint32_t>(hc);
-          const uint32_t tin = static_cast<uint32_t>(tok) & ((1u << a.page_shift) - 1u);
-          kp = kcb + static_cast<uint64_t>(prow) * (static_cast<uint32_t>(KR) << a.page_shift) + tin * KR;
-          vp = vcb + static_cast<uint64_t>(prow) * (static_cast<uint32_t>(VR) << a.page_shift) + tin * VR;
-          if (it + 2 * kNW < ntile) pg_ahead = __ldg(a.bt + b * a.bt_stride + ((tok + 32 * kNW) >> a.page_shift));
+        if (paged) {
+          const int64_t tok = r0 + 32 * static_cast<int64_t>(it + kNW);
+          const int64_t rw = row_in(pg_ahead, tok);
+          kp = kcb + rw * KR;
+          vp = vcb + rw * VR;
+          if (it + 2 * kNW < ntile) pg_ahead = page_of(tok + 32 * kNW);
         } else {
           kp += kStepK;
           vp += kStepV;
