@@ -478,11 +478,13 @@ extern "C" vecinfer_status_t vecinfer_attn_decode_paged(const void* q_bf16, int3
 static bool decode_fuses(int32_t B, int32_t H_kv, int64_t n_cap, vecinfer_vq_t kcfg, vecinfer_vq_t vcfg,
                          int32_t num_splits, vecinfer_attn_algo_t algo, bool paged = false) {
   if (algo == VECINFER_ATTN_LUT || B <= 0 || H_kv <= 0) return false;
-  // NEXT-2 formats: the split kernel fuses the append for books of <= 1024 entries (d8b8, d2b8,
-  // d4b10); d8b12 / d8b16 keep the separate encode launch
+  // NEXT-2 formats: the split kernel fuses the append for the books in its shared tables (d8b8,
+  // d2b8, d4b10, d8b12 -- VECINFER_NO_FUSE_D8B12 keeps d8b12 on the separate launches, experiments);
+  // d8b16 keeps the separate encode launch
   auto small_next2 = [](const vecinfer_vq_t& c) {
     return vq_next2(c) && ((c.sub_dim == 8 && c.code_bits == 8) || (c.sub_dim == 4 && c.code_bits == 10) ||
-                           (c.sub_dim == 2 && c.code_bits == 8));
+                           (c.sub_dim == 2 && c.code_bits == 8) ||
+                           (c.sub_dim == 8 && c.code_bits == 12 && !getenv("VECINFER_NO_FUSE_D8B12")));
   };
   const bool n2 = vq_next2(kcfg) || vq_next2(vcfg);
   if (n2 && !(small_next2(kcfg) && small_next2(vcfg))) return false;

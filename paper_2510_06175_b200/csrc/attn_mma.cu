@@ -119,10 +119,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   constexpr int KR = FK::kRow, VR = FV::kRow;
   constexpr int KS = DH / 16, VS = DH / 32, NL = DH / 4;
   constexpr bool kCanAppend = KB <= 8 && VB <= 8;   // d = 4, 4/8-bit codebooks (D = 128 or 64)
-  // fused append of the NEXT-2 formats with books of <= 1024 entries (d8b8, d2b8, d4b10): a generic
-  // all-thread centroid scan in the owner split (d8b12 / d8b16 books are too large to scan inside
-  // the attention launch: vecinfer_decode_step appends them with a separate encode launch)
-  constexpr auto gen_ok = [](int f) { return f == kFmtD8B8 || f == kFmtD2B8 || f == kFmtD4B10; };
+  // fused append of the NEXT-2 formats whose books live in shared memory (d8b8, d2b8, d4b10,
+  // d8b12): a 16-warp centroid scan in the owner split (the 1 MiB d8b16 books are not resident:
+  // vecinfer_decode_step appends them with the separate filter encode)
+  constexpr auto gen_ok = [](int f) { return f == kFmtD8B8 || f == kFmtD2B8 || f == kFmtD4B10 || f == kFmtD8B12; };
   constexpr bool kGenAppend = gen_ok(KB) && gen_ok(VB) && DH == 128;
   constexpr bool kTma = tma_fmt(KB, VB) && DH == 128 && !TC;   // contiguous caches only (runtime)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -369,7 +369,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     const int which = warp >> 3, t = tid & 255;
     const int sub = which ? fmt_sub(VB) : fmt_sub(KB), bits = which ? fmt_bits(VB) : fmt_bits(KB);
     const int M = 128 / sub;
-    const float* xw = xs + 128 * which;
     // centroids come from the stream's shared table (filled above, exact fp16 copies of the bf16
     // book): d4b10 = separate table (64-B rows of 8 replicas), d8b8 / d2b8 = the stream's half of
     // the classic 256-B rows (8 x 16 B / 32 x 4 B replicas).  Warp w (of the stream's 8) scans
@@ -377,10 +376,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     // centroid load serves all of the warp's sub-vectors, the running minima stay in registers
     // (independent chains), and one cross-lane reduction per sub-vector ends the scan.  Replica
     // choice: the 32 lanes' loads of one step hit distinct banks.
-    auto scan = [&](auto FF, uint32_t base) {
+    auto scan = [&](auto FF, uint32_t base, int st) {
       constexpr int F = decltype(FF)::value;
       constexpr int kSub = fmt_sub(F), kEnt = 1 << fmt_bits(F), kMW = 128 / kSub / 8;
       const int w8 = warp & 7;
+      const float* xw = xs + 128 * st;
       float xm[kMW][kSub];
 #pragma unroll
       for (int mi = 0; mi < kMW; ++mi)
@@ -397,8 +397,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           const float2 c01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
           const float2 c23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
           c[0] = c01.x; c[1] = c01.y; c[2] = c23.x; c[3] = c23.y;
-        } else if constexpr (F == kFmtD8B8) {
-          const uint4 w = lds_u128(base + jj * 256 + (lane & 7) * 16);
+        } else if constexpr (F == kFmtD8B8 || F == kFmtD8B12) {
+          // d8b8: 8 replicas in the stream's 128-byte half-row; d8b12: unreplicated 16-byte rows
+          // (32 consecutive rows per step: conflict-free)
+          const uint4 w = F == kFmtD8B8 ? lds_u128(base + jj * 256 + (lane & 7) * 16) : lds_u128(base + jj * 16);
           const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -430,11 +432,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, key[mi], off);
           key[mi] = o2 < key[mi] ? o2 : key[mi];
         }
-        if (lane == 0) gbest[64 * which + w8 + 8 * mi] = key[mi];
+        if (lane == 0) gbest[64 * st + w8 + 8 * mi] = key[mi];
       }
     };
-    if (which == 0) scan(std::integral_constant<int, KB>{}, Fmt<KB>::kSep ? tab_s + kSepOff : tab_s);
-    else scan(std::integral_constant<int, VB>{}, Fmt<VB>::kSep ? tab_s + kSepVOff : tab_s + 128);
+    // (a mixed pair's lighter stream finishing early does not matter: the scan is issue-bound, so
+    // the heavier stream's warps get the freed issue slots -- handing them part of its entry range
+    // was measured neutral)
+    if (which == 0) scan(std::integral_constant<int, KB>{}, Fmt<KB>::kSep ? tab_s + kSepOff : tab_s, 0);
+    else scan(std::integral_constant<int, VB>{}, Fmt<VB>::kSep ? tab_s + kSepVOff : tab_s + 128, 1);
     __syncthreads();
     // pack: byte i of the row = bits [8i, 8i + 8) of the bit string (b >= 8: <= 2 codes per byte)
     const int rb = M * bits / 8;
