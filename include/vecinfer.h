@@ -28,8 +28,12 @@
  *    d8b8 {128, 8, 8}, d8b12 {128, 8, 12}, d4b10 {128, 4, 10}, d2b8 {128, 2, 8}, d8b16
  *    {128, 8, 16} (Table 5's 2-bit row: 65 536 eight-dim centroids, 1 MiB bf16 per book);
  *    attention pairs (f, f) and the mixed K-d4b10 / V-d8b12 and K-d8b12 / V-d8b8 of Table 3, on the split
- *    DEQUANT_MMA kernel (contiguous or paged, residual window allowed; no stream / LUT variant,
- *    decode_step appends with a separate encode launch).
+ *    DEQUANT_MMA kernel (contiguous or paged, residual window allowed; no stream / LUT variant;
+ *    decode_step fuses the append for the books held in the kernel's shared tables -- d8b8,
+ *    d8b12, d4b10, d2b8 -- and appends d8b16 with a separate encode launch).  The kernel keeps
+ *    these books (like the d = 4 ones) as fp16 copies: every centroid value must be exactly
+ *    representable in fp16 (0 or 2^-14 <= |c| <= 65504 with <= 11 significant bits; bf16 values
+ *    in the fp16 normal range are), else attention and the fused append's codes are not exact.
  *    Anything else returns VECINFER_ERR_UNSUPPORTED.
  *  - ABI v5 adds: n_tokens_max in vecinfer_attn_kernel_kind (the stream/split choice is a cost
  *    model over it), vecinfer_kmeans_step (GPU codebook Lloyd iteration) and the fused
@@ -324,12 +328,11 @@ vecinfer_status_t vecinfer_attn_decode_paged(const void* q_bf16, int32_t B, int3
  *   Other arguments as in vecinfer_attn_decode (token range = whole sequence) and
  *   vecinfer_encode_kv (err_flags); workspace >= vecinfer_decode_step_workspace_bytes(...), zero-
  *   filled once.  The append runs inside the attention launch for the d = 4 books of 16 / 256
- *   entries (b1d4, b2d4, any K/V mix of them) and for d8b8 / d4b10 when the grid is one wave (the
- *   stream partition always budgets it).  Otherwise it runs first as its own encode (same codes):
- *   grids of several waves, the LUT variant, d2b8 (measured faster separate), and the large books
- *   -- 65 536-entry d = 4 and 4096 / 65 536-entry d = 8 -- through the tensor-core filter + exact
- *   selection of vecinfer_encode_kv (two launches).  vecinfer_decode_step_launches reports the
- *   count.
+ *   entries (b1d4, b2d4, any K/V mix of them) and for d8b8 / d8b12 / d4b10 / d2b8 and their mixed
+ *   pairs when the grid is one wave (the stream partition always budgets it).  Otherwise it runs
+ *   first as its own encode (same codes): grids of several waves, the LUT variant, and the
+ *   65 536-entry books (b4d4, d8b16) through the tensor-core filter + exact selection of
+ *   vecinfer_encode_kv (two launches).  vecinfer_decode_step_launches reports the count.
  * Errors: as vecinfer_encode_kv and vecinfer_attn_decode.
  * ------------------------------------------------------------------------------------- */
 /* kernel launches one vecinfer_decode_step call makes (1: the append is fused into attention) */
