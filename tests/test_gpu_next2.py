@@ -186,3 +186,40 @@ def test_next2_unsupported_fail_loudly():
     c2 = _case("d8b8", "d8b12", 1, 8, 4, 256, [256], seed=861)   # no kernel for this pair
     with pytest.raises(VecInferError):
         _run(c2)
+
+
+@pytest.mark.parametrize("kn,vn", [("d8b8", "d8b8"), ("d8b12", "d8b12"), ("d4b10", "d4b10"), ("d2b8", "d2b8"),
+                                   ("d4b10", "d8b12"), ("d8b12", "d8b8")])
+def test_next2_fused_append_many_steps(kn, vn):
+    """48 consecutive fused decode steps (one launch each: the owner split's shared-table scan)
+    append 48 x 8 token-heads; the cache afterwards equals vecinfer_encode_kv of the same tokens
+    (the separate encoders) and the oracle's packed rows, byte for byte."""
+    B, H, n_cap, T = 1, 8, 4096, 48
+    kcfg, vcfg = FMT[kn], FMT[vn]
+    assert vi.decode_step_launches(B, H, n_cap, kcfg, vcfg) == 1
+    c = _case(kn, vn, B, H, 4, n_cap, [n_cap], seed=870)
+    K = synth.gen_keys(T, H, 128, seed=871, batch=B)     # [B, T, H, D]
+    V = synth.gen_values(T, H, 128, seed=872, batch=B)
+    kcodes = t_u8(ref.pack_codes(c["kc"], kcfg.code_bits))
+    vcodes = t_u8(ref.pack_codes(c["vc"], vcfg.code_bits))
+    kref, vref = kcodes.clone(), vcodes.clone()
+    q, lam, inv = t_bf16(c["q"]), t_f32(c["lam"]), t_f32(CB["inv_lambda"])
+    ck, cv = t_bf16(c["ck"]), t_bf16(c["cv"])
+    ws = vi.decode_step_workspace(B, 4 * H, H, n_cap, kcfg, vcfg)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    p0 = n_cap - T
+    for t in range(T):
+        vi.decode_step(q, t_bf16(K[:, t]), t_bf16(V[:, t]), lam, inv, ck, cv, kcodes, vcodes, t_i32([p0 + t]),
+                       t_i32([p0 + t + 1]), kcfg=kcfg, vcfg=vcfg, workspace=ws, err_flags=err)
+    vi.encode_kv(t_bf16(K), t_bf16(V), inv, ck, cv, kref, vref, t_i32([p0]), kcfg, vcfg)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    assert torch.equal(kcodes, kref) and torch.equal(vcodes, vref)
+    for t in range(T):
+        for h in range(H):
+            ckh = c["ck"] if c["ck"].ndim == 2 else c["ck"][h]
+            cvh = c["cv"] if c["cv"].ndim == 2 else c["cv"][h]
+            c["kc"][0, h, p0 + t], c["vc"][0, h, p0 + t] = ref.encode_kv(K[0, t, h], V[0, t, h],
+                                                                         CB["inv_lambda"][h], ckh, cvh)
+    assert np.array_equal(kcodes.cpu().numpy(), ref.pack_codes(c["kc"], kcfg.code_bits))
+    assert np.array_equal(vcodes.cpu().numpy(), ref.pack_codes(c["vc"], vcfg.code_bits))
