@@ -107,7 +107,9 @@ __device__ __forceinline__ uint32_t krow_addr(const KRowT<KB>& kr, uint32_t base
 }
 
 // XR: the fused cross-rank merge variant (vecinfer_attn_decode_xr; single-wave spin merge only)
-template <int KB, int VB, int DH, bool TC, bool XR = false>
+// PG: paged code caches (a separate instantiation, so the contiguous kernels carry no translation
+// code: the small cfg2 launch is sensitive to any change of its code)
+template <int KB, int VB, int DH, bool TC, bool XR = false, bool PG = false>
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
   // DH = head dim (128, or 64: NEXT-4).  KS score k-steps (4 sub-vectors each) per 16 tokens,
   // VS V sub-vectors per lane r (2 P.V m-tiles each), NL lanes holding a q~ row.
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   // lane-resolved code pointers of this warp's first tile.  Paged caches: tiles are 32-aligned
   // (tok_begin % 32 == 0, chunks of 32) so a tile never crosses a page; the page of the tile after
   // next is read one tile ahead so its latency hides behind the current tile.
-  const bool paged = a.bt != nullptr;
+  constexpr bool paged = PG;
   const uint8_t* kcb = a.kcodes + static_cast<int64_t>(r) * KR + FK::kOffK * j;
   const uint8_t* vcb = a.vcodes + static_cast<int64_t>(2 * j) * VR + FV::kOffV * r;
   const int64_t pmask = (int64_t(1) << a.page_shift) - 1;
@@ -729,12 +731,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       }
       const int rem_cur = ntok - 32 * it;
       if (!tma_on && it + kNW < ntile) {
-        if (paged) {
-          const int64_t tok = r0 + 32 * static_cast<int64_t>(it + kNW);
-          const int64_t rw = row_in(pg_ahead, tok);
-          kp = kcb + rw * KR;
-          vp = vcb + rw * VR;
-          if (it + 2 * kNW < ntile) pg_ahead = page_of(tok + 32 * kNW);
+        if constexpr (paged) {   // row (pg * Hc + hc) * page_size + tok % page_size: 32 x 32 -> 64-bit multiply-adds
+          const int tok = static_cast<int>(r0) + 32 * (it + kNW);
+          const uint32_t prow = static_cast<uint32_t>(pg_ahead) * static_cast<uint32_t>(a.Hc) + static_cast<uint32_t>(hc);
+          const uint32_t tin = static_cast<uint32_t>(tok) & ((1u << a.page_shift) - 1u);
+          kp = kcb + static_cast<uint64_t>(prow) * (static_cast<uint32_t>(KR) << a.page_shift) + tin * KR;
+          vp = vcb + static_cast<uint64_t>(prow) * (static_cast<uint32_t>(VR) << a.page_shift) + tin * VR;
+          if (it + 2 * kNW < ntile) pg_ahead = __ldg(a.bt + b * a.bt_stride + ((tok + 32 * kNW) >> a.page_shift));
         } else {
           kp += kStepK;
           vp += kStepV;
@@ -1021,21 +1024,31 @@ static AttnKernel kernel_tc(int kf, int vf) {
   return table[kf == 8 ? 1 : 0][vf == 4 ? 0 : vf == 8 ? 1 : 2];
 }
 
-static AttnKernel kernel_for(int kf, int vf, int dh = 128) {
+template <bool PG>
+static AttnKernel kernel_for_t(int kf, int vf, int dh) {
 #define VECINFER_PAIR(K, V) \
-  if (kf == K && vf == V) return dh == 128 ? attn_mma_kernel<K, V, 128, false> : nullptr;
+  if (kf == K && vf == V) return dh == 128 ? attn_mma_kernel<K, V, 128, false, false, PG> : nullptr;
   VECINFER_NEXT2_PAIRS(VECINFER_PAIR)
 #undef VECINFER_PAIR
   const int ki = kf == 4 ? 0 : kf == 8 ? 1 : kf == 16 ? 2 : -1, vi = vf == 4 ? 0 : vf == 8 ? 1 : vf == 16 ? 2 : -1;
   if (ki < 0 || vi < 0) return nullptr;
   static const AttnKernel table[2][3][3] = {
-      {{attn_mma_kernel<4, 4, 128, false>, attn_mma_kernel<4, 8, 128, false>, attn_mma_kernel<4, 16, 128, false>},
-       {attn_mma_kernel<8, 4, 128, false>, attn_mma_kernel<8, 8, 128, false>, attn_mma_kernel<8, 16, 128, false>},
-       {attn_mma_kernel<16, 4, 128, false>, attn_mma_kernel<16, 8, 128, false>, attn_mma_kernel<16, 16, 128, false>}},
-      {{attn_mma_kernel<4, 4, 64, false>, attn_mma_kernel<4, 8, 64, false>, attn_mma_kernel<4, 16, 64, false>},
-       {attn_mma_kernel<8, 4, 64, false>, attn_mma_kernel<8, 8, 64, false>, attn_mma_kernel<8, 16, 64, false>},
-       {attn_mma_kernel<16, 4, 64, false>, attn_mma_kernel<16, 8, 64, false>, attn_mma_kernel<16, 16, 64, false>}}};
+      {{attn_mma_kernel<4, 4, 128, false, false, PG>, attn_mma_kernel<4, 8, 128, false, false, PG>,
+        attn_mma_kernel<4, 16, 128, false, false, PG>},
+       {attn_mma_kernel<8, 4, 128, false, false, PG>, attn_mma_kernel<8, 8, 128, false, false, PG>,
+        attn_mma_kernel<8, 16, 128, false, false, PG>},
+       {attn_mma_kernel<16, 4, 128, false, false, PG>, attn_mma_kernel<16, 8, 128, false, false, PG>,
+        attn_mma_kernel<16, 16, 128, false, false, PG>}},
+      {{attn_mma_kernel<4, 4, 64, false, false, PG>, attn_mma_kernel<4, 8, 64, false, false, PG>,
+        attn_mma_kernel<4, 16, 64, false, false, PG>},
+       {attn_mma_kernel<8, 4, 64, false, false, PG>, attn_mma_kernel<8, 8, 64, false, false, PG>,
+        attn_mma_kernel<8, 16, 64, false, false, PG>},
+       {attn_mma_kernel<16, 4, 64, false, false, PG>, attn_mma_kernel<16, 8, 64, false, false, PG>,
+        attn_mma_kernel<16, 16, 64, false, false, PG>}}};
   return table[dh == 64 ? 1 : 0][ki][vi];
+}
+static AttnKernel kernel_for(int kf, int vf, int dh = 128, bool pg = false) {
+  return pg ? kernel_for_t<true>(kf, vf, dh) : kernel_for_t<false>(kf, vf, dh);
 }
 
 // fused cross-rank merge variants: d = 4 K / V books, D = 128
@@ -1064,12 +1077,13 @@ static void set_attrs_once() {
   if (!done) {
     for (int dh : {128, 64})
       for (int kb : {4, 8, 16})
-        for (int vb : {4, 8, 16}) set_attr(kernel_for(kb, vb, dh), smem_for(kb, vb));
+        for (int vb : {4, 8, 16})
+          for (bool pg : {false, true}) set_attr(kernel_for(kb, vb, dh, pg), smem_for(kb, vb));
     for (int kb : {4, 8})
       for (int vb : {4, 8, 16}) set_attr(kernel_tc(kb, vb), smem_for(kb, vb));
     for (int kb : {4, 8, 16})
       for (int vb : {4, 8, 16}) set_attr(kernel_xr(kb, vb), smem_for(kb, vb));
-#define VECINFER_PAIR(K, V) set_attr(kernel_for(K, V), smem_for(K, V));
+#define VECINFER_PAIR(K, V) set_attr(kernel_for(K, V), smem_for(K, V)); set_attr(kernel_for(K, V, 128, true), smem_for(K, V));
     VECINFER_NEXT2_PAIRS(VECINFER_PAIR)
 #undef VECINFER_PAIR
     done = true;
@@ -1131,7 +1145,7 @@ cudaError_t launch_attn_mma(const AttnArgs& a, int kbits, int vbits, cudaStream_
   }
   cfg.attrs = at;
   cfg.numAttrs = n;
-  const AttnKernel k = a.xr_P > 0 ? kernel_xr(kbits, vbits) : a.tc ? kernel_tc(kbits, vbits) : kernel_for(kbits, vbits, a.D);
+  const AttnKernel k = a.xr_P > 0 ? kernel_xr(kbits, vbits) : a.tc ? kernel_tc(kbits, vbits) : kernel_for(kbits, vbits, a.D, a.bt != nullptr);
   if (!k) return cudaErrorInvalidDeviceFunction;
   return cudaLaunchKernelEx(&cfg, k, a);
 }
