@@ -127,6 +127,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   constexpr auto gen_ok = [](int f) { return f == kFmtD8B8 || f == kFmtD2B8 || f == kFmtD4B10 || f == kFmtD8B12; };
   constexpr bool kGenAppend = gen_ok(KB) && gen_ok(VB) && DH == 128;
   constexpr bool kTma = tma_fmt(KB, VB) && DH == 128 && !TC;   // contiguous caches only (runtime)
+  // 65 536-entry d = 4 books (gathered through L1/L2): a warp's tile takes ~20 us, so the next
+  // tile's code loads go out after the current tile instead of before it -- their HBM latency hides
+  // behind the other warps' gathers, and the two tiles' codes are never live together (b4d4 stack
+  // 128 -> 56 B, cfg5 b4d4 137.4 -> 127.2 us; d8b16 measured 1.4 % slower this way: kept early)
+  constexpr bool kLateNext = (KB == 16 || VB == 16) && DH == 128 && !TC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, j = lane & 3;
@@ -730,6 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       }
       }
       const int rem_cur = ntok - 32 * it;
+      auto issue_next = [&]() {
       if (!tma_on && it + kNW < ntile) {
         if constexpr (paged) {   // row (pg * Hc + hc) * page_size + tok % page_size: 32 x 32 -> 64-bit multiply-adds
           const int tok = static_cast<int>(r0) + 32 * (it + kNW);
@@ -746,6 +752,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         if (rem >= 32) load_tile_full<KB, VB, DH>(nxt, kp, vp);
         else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
       }
+      };
+      if constexpr (!kLateNext) issue_next();
   
       // ---- scores (log2 units) for tile tokens 16q + {r, r+8}, head j; two independent MMA
       // accumulator chains per sub-tile (k-steps 0-3 and 4-7) halve the dependent HMMA latency
@@ -779,6 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         sc[q][1] = (d0[2] + d1[2]) + (d0[3] + d1[3]);
       }
       softmax_pv(sc, cur, rem_cur);
+      if constexpr (kLateNext) issue_next();
     }
   }
   if constexpr (TC) {
