@@ -658,6 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
             }
           }
           const int rem_cur = ntok - 32 * it;
+          auto issue_next = [&]() {
           if (it + 1 < ntile) {
             const int rem = rem_cur - 32;
             if constexpr (paged) {
@@ -671,6 +672,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
               else load_tile_tail<KB, VB, DH>(nxt, kp, vp, rem, r, j);
             }
           }
+          };
+          // 65 536-entry books: the next tile's codes are loaded after this tile (as in the split
+          // kernel: tiles are long, the HBM latency hides behind the other warps' gathers, and the
+          // two tiles' codes are never live together)
+          constexpr bool kLateNext = (KB == 16 || VB == 16) && DH == 128;
+          if constexpr (!kLateNext) issue_next();
           // tile body, specialised on whether sub-tile 1 holds tokens (a trailing half tile skips it);
           // the common full-tile instance is straight-line code the scheduler can interleave
           auto tile_body = [&](auto TWO) {
@@ -762,6 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_stream_kernel(const __grid_c
           if (rem_cur > 16) tile_body(std::true_type{});
           else tile_body(std::false_type{});
 #endif
+          if constexpr (kLateNext) issue_next();
         }
       }
 
